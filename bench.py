@@ -1,0 +1,331 @@
+#!/usr/bin/env python3
+"""Benchmark of the hot path (BASELINE.json metric: source x point pair
+evaluations per second, with the roofline fraction).
+
+Workload (BASELINE.json configs[1], the metric's own configuration): the
+point-source superposition microbenchmark — 2^20 seeded evaluation points in a
+4x4x1 mm box, 2^16 history sources on a bidirectional raster, T~ and grad T~
+evaluated at t_end in fp64. One "step" = one full superpose
+over all 2^20 points (6.87e10 pairs).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+
+  * value    — pairs/s over all ranks, inputs resident in HBM, device-timed with
+               CUDA events per step (L2 flushed between steps by a 256 MiB write,
+               outside the step's events), max over ranks.
+  * e2e      — the same metric through the C ABI with host buffers
+               (tg_superpose_batch: pinned host points -> device -> host value
+               and gradient), wall-clock per synchronous call.
+  * roofline — K1 main kernel (k1_partial): 49 algorithmic FP64 flops per pair
+                x pairs per launch / mean launch time (CUDA events
+               on its stream), against the FP64 DFMA peak measured live on this
+               GPU (tg_fp64_peak; MEASURED_PEAKS.json has no fp64 figure).
+  * cpu_baseline — the unmodified reference's superpose (oracle/_ref, threaded
+               with its own parallel_for over all host cores) on a bounded
+               sample of the same workload; the C oracle port if _ref is absent.
+  * --impl reference — that CPU path alone, as the reference arm.
+Multi-GPU (torchrun): every rank evaluates its own 2^20-point slab against the
+replicated sources (weak scaling; no data-path collective — the path shards by
+points with no exchange).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_2511_20432_b200 import workloads as W  # noqa: E402
+
+FLOPS_PER_PAIR = 49.0  # value + gradient, exp counted at libdevice cost
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--points", type=int, default=W.CONFIG1_POINTS)
+    ap.add_argument("--sources", type=int, default=W.CONFIG1_SOURCES)
+    ap.add_argument("--cpu-seconds", type=float, default=10.0,
+                    help="target CPU work for the bounded cpu_baseline sample")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ncu", action="store_true", help="profiling run: no clocks/cpu legs")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def workload(n_src):
+    mat = dict(W.MATERIAL)
+    path = dict(waypoints=W.config1_waypoints(), start_time=0.0, plane_z=1e-3)
+    return mat, path, n_src
+
+
+def make_sources(tg, n_src):
+    src = tg.discretize_scan(tg.ScanPath(W.config1_waypoints(), 0.0, 1e-3),
+                             tg.LaserSpec(**W.LASER), tg.Material(**W.MATERIAL))[:n_src]
+    return src, float(src[-1, 4])
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            self.proc.wait(timeout=5)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 3 + i and r[3 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def cpu_baseline(src, t, budget_s, threads=None):
+    """Reference superpose on a bounded sample (rank 0, N=1 only)."""
+    from oracle import pyoracle
+    kw = dict(**W.MATERIAL, **W.LASER)
+    threads = threads or os.cpu_count() or 1
+    if pyoracle.ref_available():
+        impl, kind = pyoracle.RefLib(), "reference"
+        call = lambda pts: impl.superpose(src, pts, t, threads=threads, **kw)  # noqa: E731
+        cores = threads
+    else:
+        impl, kind = pyoracle.COracle(), "port"
+        call = lambda pts: impl.superpose(src, pts, t, **kw)  # noqa: E731
+        cores = 1
+    all_pts = W.config1_points()
+    # calibrate on a small slice, then size the sample for ~budget_s
+    n0 = max(64, min(4096, 8 * cores))
+    t0 = time.perf_counter()
+    call(all_pts[:n0])
+    dt0 = time.perf_counter() - t0
+    n = int(min(len(all_pts), max(n0, n0 * budget_s / max(dt0, 1e-6))))
+    stride = max(1, len(all_pts) // n)
+    pts = np.ascontiguousarray(all_pts[::stride][:n])
+    t0 = time.perf_counter()
+    call(pts)
+    secs = time.perf_counter() - t0
+    pairs = float(len(pts)) * len(src)
+    return {"value": pairs / secs, "unit": "pairs/s", "cores": cores, "kind": kind,
+            "sample": f"{len(pts)} of the 2^20 config-1 points (every {stride}th) x {len(src)} "
+                      f"sources, value+grad at t_end, {secs:.2f} s"}
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    import paper_2511_20432_b200 as tg  # host-only use: discretize_scan for the inputs
+    src, t = make_sources(tg, args.sources)
+    per_step = max(1.0, min(30.0, 120.0 / max(1, args.steps + args.warmup)))
+    for _ in range(args.warmup):
+        cpu_baseline(src, t, per_step / 4)
+    vals = [cpu_baseline(src, t, per_step) for _ in range(args.steps)]
+    v = float(np.mean([x["value"] for x in vals]))
+    cb = dict(vals[-1])
+    cb["value"] = v
+    line = {
+        "impl": "reference", "metric": "source x point pair evals/s (superpose, value+grad)",
+        "value": v, "unit": "pairs/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": float(W.CONFIG1_POINTS) * len(src) / v * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded, SURVEY.md §8d)",
+        "config": {"workload": "config1: 2^20 points x 2^16 raster sources, superpose at t_end",
+                   "points": W.CONFIG1_POINTS, "sources": len(src), "cull_exponent": 60.0},
+        "cpu_baseline": cb,
+        "e2e": {"value": v, "unit": "pairs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_ours(args):
+    import torch
+    import paper_2511_20432_b200 as tg
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl")
+    dev = torch.device("cuda", local)
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    ctx = tg.Context(local)
+    src, t = make_sources(tg, args.sources)
+    ctx.set_sources(src, tg.Material(**W.MATERIAL))
+    n = args.points
+    # weak scaling: each rank owns its own seeded slab of 2^20 points
+    pts_np = W.config1_points(n, seed=W.CONFIG1_SEED + rank)
+    pts = torch.from_numpy(pts_np).to(dev)
+    val = torch.empty(n, dtype=torch.float64, device=dev)
+    grad = torch.empty((n, 3), dtype=torch.float64, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    sp = stream.cuda_stream
+    pairs_per_step = float(n) * len(src)
+
+    def step():
+        ctx.superpose(pts, t, out=(val, grad), stream=sp)
+
+    fp64_peak = ctx.fp64_peak_tflops() if not args.ncu else None
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+
+    ctx.set_profiling(True)
+    ctx.profile(reset=True)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    sampler = ClockSampler(local)
+    barrier()
+    with sampler:
+        for i in range(args.steps):
+            flush.zero_()
+            evs[i][0].record(stream)
+            step()
+            evs[i][1].record(stream)
+        barrier()
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+    prof = ctx.profile()
+    ctx.set_profiling(False)
+    total_ms = float(sum(step_ms))
+    if world > 1:
+        import torch.distributed as dist
+        tt = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        total_ms = float(tt.item())
+    value = world * pairs_per_step * args.steps / (total_ms * 1e-3)
+
+    # e2e through the C ABI with host buffers (pinned), H2D + compute + D2H per step
+    pin_pts = torch.from_numpy(pts_np).pin_memory()
+    pin_val = torch.empty(n, dtype=torch.float64).pin_memory()
+    pin_grad = torch.empty((n, 3), dtype=torch.float64).pin_memory()
+    pv, pg = pin_val.numpy(), pin_grad.numpy()
+    pp = pin_pts.numpy()
+    for _ in range(max(1, args.warmup // 2)):
+        ctx.superpose(pp, t, out=(pv, pg))
+    barrier()
+    e2e_s = 0.0
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        ctx.superpose(pp, t, out=(pv, pg))
+        e2e_s += time.perf_counter() - t0
+    if world > 1:
+        import torch.distributed as dist
+        tt = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_s = float(tt.item())
+    e2e = world * pairs_per_step * args.steps / e2e_s
+
+    if rank != 0:
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+            dist.destroy_process_group()
+        return 0
+
+    k1_mean_ms = prof["k1_ms"] / max(1, prof["k1_launches"])
+    pairs_per_launch = prof["k1_pairs"] / max(1, prof["k1_launches"])
+    achieved = FLOPS_PER_PAIR * pairs_per_launch / (k1_mean_ms * 1e-3) / 1e12 if k1_mean_ms else None
+    roof = {"kernel": "k1_partial<2,true>", "bound": "fp64", "achieved": achieved,
+            "peak": fp64_peak, "unit": "TFLOP/s",
+            "frac": (achieved / fp64_peak) if (achieved and fp64_peak) else None,
+            "traffic": None,
+            "peak_source": "measured live: tg_fp64_peak DFMA-chain microbenchmark on this GPU",
+            "flops_per_pair": FLOPS_PER_PAIR, "pairs_per_launch": pairs_per_launch,
+            "mean_launch_ms": k1_mean_ms,
+            "k1_share_of_step": prof["k1_ms"] / max(1e-9, float(sum(step_ms)))}
+    line = {
+        "metric": "source x point pair evals/s (superpose, value+grad)",
+        "value": value, "unit": "pairs/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded, SURVEY.md §8d)",
+        "config": {"workload": "config1: 2^20 points x 2^16 raster sources, superpose at t_end",
+                   "points_per_gpu": n, "sources": len(src), "cull_exponent": 60.0,
+                   "parallelism": f"point slabs x{world}, sources replicated",
+                   "l2": "flushed between steps (256 MiB write outside the step events)"},
+        "e2e": {"value": e2e, "unit": "pairs/s", "h2d_bytes_per_step": int(pp.nbytes),
+                "d2h_bytes_per_step": int(pv.nbytes + pg.nbytes)},
+        "gpu_launches": prof["launches"],
+        "roofline": roof,
+        "clocks": sampler.summary(),
+    }
+    if world == 1 and not args.no_cpu_baseline and not args.ncu:
+        try:
+            line["cpu_baseline"] = cpu_baseline(src, t, args.cpu_seconds)
+        except Exception as e:  # reported, not fatal
+            line["cpu_baseline"] = {"value": None, "error": str(e)}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

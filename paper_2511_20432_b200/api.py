@@ -1,0 +1,265 @@
+"""Python mirror of the reference's hot-path interface over the C ABI.
+
+Names, argument meaning and error behaviour follow proj/include/thermiga/*.hpp:
+``discretize_scan`` (analytic.hpp:45-48), ``superpose`` (analytic.hpp:73-75),
+``Simulation`` / ``run_time_loop`` (driver.hpp:20-47), ``assemble_flux_load``
+(assembly.hpp:37-40), ``dirichlet_values`` (mesh.hpp:121-125), ``theta_step``
+(timestep.hpp:26-29).  Every compute call goes through
+``_lib/libthermiga_b200.so`` (sm_100a kernels); there is no CPU fallback —
+without the library or a B200 the calls raise.
+
+Arrays: numpy arrays are host memory (the C ABI stages them through the
+device); torch CUDA tensors are passed as device pointers (no copies).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import _build
+
+_dp = C.POINTER(C.c_double)
+_ip = C.POINTER(C.c_int)
+
+
+class ThermigaError(RuntimeError):
+    """Base class; ``code`` is the TG_* status (= reference CLI exit code)."""
+    code = 1
+
+
+class ConfigError(ThermigaError):
+    code = 2
+
+
+class NumericError(ThermigaError):
+    code = 3
+
+
+class IOError_(ThermigaError):
+    code = 4
+
+
+class CudaError(ThermigaError):
+    code = 5
+
+
+_ERRORS = {1: ThermigaError, 2: ConfigError, 3: NumericError, 4: IOError_, 5: CudaError}
+
+TG_OK = 0
+
+
+class _Material(C.Structure):
+    _fields_ = [("conductivity", C.c_double), ("density", C.c_double),
+                ("heat_capacity", C.c_double), ("platform_temperature", C.c_double)]
+
+
+class _Laser(C.Structure):
+    _fields_ = [("power", C.c_double), ("speed", C.c_double), ("spot_radius", C.c_double),
+                ("absorptivity", C.c_double), ("dt", C.c_double)]
+
+
+@dataclass
+class Material:
+    """thermiga::Material (analytic.hpp:10-20)."""
+    conductivity: float
+    density: float
+    heat_capacity: float
+    platform_temperature: float = 0.0
+
+    def diffusivity(self) -> float:
+        return self.conductivity / (self.density * self.heat_capacity)
+
+    def volumetric_capacity(self) -> float:
+        return self.density * self.heat_capacity
+
+    def _c(self):
+        return _Material(self.conductivity, self.density, self.heat_capacity,
+                         self.platform_temperature)
+
+
+@dataclass
+class LaserSpec:
+    """thermiga::LaserSpec (analytic.hpp:22-31)."""
+    power: float
+    speed: float
+    spot_radius: float
+    absorptivity: float
+    dt: float
+
+    def _c(self):
+        return _Laser(self.power, self.speed, self.spot_radius, self.absorptivity, self.dt)
+
+
+@dataclass
+class ScanPath:
+    """thermiga::ScanPath (analytic.hpp:42-47)."""
+    waypoints: Sequence[Sequence[float]] = field(default_factory=list)
+    start_time: float = 0.0
+    plane_z: float = 0.0
+
+
+@dataclass
+class SuperposeOptions:
+    """thermiga::SuperposeOptions (analytic.hpp:60-66)."""
+    cull_exponent: float = 60.0
+
+
+_LIB = None
+
+
+def lib(auto_build: bool = True):
+    """Load libthermiga_b200.so (building it in-tree with nvcc when missing)."""
+    global _LIB
+    if _LIB is not None:
+        return _LIB
+    if auto_build and (not os.path.exists(_build.LIB) or os.environ.get("TG_REBUILD")):
+        _build.build()
+    if not os.path.exists(_build.LIB):
+        raise CudaError(f"native library missing: {_build.LIB}")
+    L = C.CDLL(_build.LIB)
+    L.tg_abi_version.restype = C.c_int
+    L.tg_ctx_create.argtypes = [C.c_int, C.POINTER(C.c_void_p)]
+    L.tg_ctx_destroy.argtypes = [C.c_void_p]
+    L.tg_last_error.restype = C.c_char_p
+    L.tg_last_error.argtypes = [C.c_void_p]
+    L.tg_set_profiling.argtypes = [C.c_void_p, C.c_int]
+    L.tg_profile_read.argtypes = [C.c_void_p, _dp, C.c_int]
+    L.tg_fp64_peak.argtypes = [C.c_void_p, _dp]
+    L.tg_discretize_scan.argtypes = [_dp, C.c_int, C.c_double, C.c_double,
+                                     C.POINTER(_Laser), C.POINTER(_Material), _dp, C.c_int]
+    L.tg_set_sources.argtypes = [C.c_void_p, _dp, C.c_int, C.POINTER(_Material)]
+    L.tg_superpose_batch.argtypes = [C.c_void_p, _dp, C.c_long, C.c_double, C.c_double, _dp, _dp]
+    L.tg_superpose_batch_device.argtypes = [C.c_void_p, C.c_void_p, C.c_long, C.c_double,
+                                            C.c_double, C.c_void_p, C.c_void_p, C.c_void_p]
+    _LIB = L
+    return L
+
+
+def _f64(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def _p(a):
+    return None if a is None else a.ctypes.data_as(_dp)
+
+
+def discretize_scan(path: ScanPath, laser: LaserSpec, mat: Material) -> np.ndarray:
+    """Point sources {x, y, z, E, t_activate, tau} (n, 6); analytic.cpp:22-71."""
+    L = lib()
+    wp = _f64(np.asarray(path.waypoints, dtype=np.float64).reshape(-1, 2))
+    las, m = laser._c(), mat._c()
+    n = L.tg_discretize_scan(_p(wp), len(wp), path.start_time, path.plane_z, C.byref(las),
+                             C.byref(m), None, 0)
+    if n < 0:
+        raise ThermigaError("discretize_scan: invalid laser, material or empty path")
+    out = np.zeros((n, 6))
+    L.tg_discretize_scan(_p(wp), len(wp), path.start_time, path.plane_z, C.byref(las),
+                         C.byref(m), _p(out), n)
+    return out
+
+
+class Context:
+    """A device context (one CUDA stream, resident buffers) on one GPU."""
+
+    def __init__(self, device: int = 0):
+        L = self._L = lib()
+        h = C.c_void_p()
+        rc = L.tg_ctx_create(device, C.byref(h))
+        self._h = h
+        if rc != TG_OK:
+            msg = L.tg_last_error(h).decode() if h else "context creation failed"
+            if h:
+                L.tg_ctx_destroy(h)
+            self._h = None
+            raise _ERRORS.get(rc, ThermigaError)(msg)
+        self.n_sources = 0
+        self.material: Optional[Material] = None
+
+    def _check(self, rc):
+        if rc != TG_OK:
+            raise _ERRORS.get(rc, ThermigaError)(self._L.tg_last_error(self._h).decode())
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._L.tg_ctx_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- profiling ----------------------------------------------------------
+    def set_profiling(self, on: bool = True):
+        self._check(self._L.tg_set_profiling(self._h, int(on)))
+
+    def profile(self, reset: bool = False) -> dict:
+        out = np.zeros(8)
+        self._check(self._L.tg_profile_read(self._h, _p(out), int(reset)))
+        return dict(k1_ms=out[0], k1_launches=int(out[1]), k1_pairs=out[2], k2_ms=out[3],
+                    k2_launches=int(out[4]), k2_bytes=out[5], launches=int(out[6]))
+
+    def fp64_peak_tflops(self) -> float:
+        out = C.c_double(0.0)
+        self._check(self._L.tg_fp64_peak(self._h, C.byref(out)))
+        return out.value
+
+    # -- K1 -------------------------------------------------------------------
+    def set_sources(self, sources, mat: Material):
+        s = _f64(np.asarray(sources).reshape(-1, 6))
+        m = mat._c()
+        self._check(self._L.tg_set_sources(self._h, _p(s), len(s), C.byref(m)))
+        self.n_sources = len(s)
+        self.material = mat
+
+    def superpose(self, points, t: float, opts: SuperposeOptions = SuperposeOptions(),
+                  grad: bool = True, out=None, stream=None):
+        """T~ and grad T~ at every point (superpose, analytic.cpp:92-109).
+
+        numpy input -> numpy (value (n,), grad (n,3)); torch CUDA input -> device
+        tensors written in place of ``out`` (or newly allocated)."""
+        if hasattr(points, "is_cuda") and points.is_cuda:
+            import torch
+            n = points.shape[0]
+            if out is None:
+                val = torch.empty(n, dtype=torch.float64, device=points.device)
+                g = torch.empty((n, 3), dtype=torch.float64, device=points.device) if grad else None
+            else:
+                val, g = out
+            st = stream if stream is not None else torch.cuda.current_stream(points.device).cuda_stream
+            self._check(self._L.tg_superpose_batch_device(
+                self._h, C.c_void_p(points.data_ptr()), n, float(t), float(opts.cull_exponent),
+                C.c_void_p(val.data_ptr()), C.c_void_p(g.data_ptr()) if g is not None else None,
+                C.c_void_p(st)))
+            return val, g
+        p = _f64(np.asarray(points).reshape(-1, 3))
+        n = len(p)
+        if out is None:
+            val = np.zeros(n)
+            g = np.zeros((n, 3)) if grad else None
+        else:
+            val, g = out
+        self._check(self._L.tg_superpose_batch(self._h, _p(p), n, float(t),
+                                               float(opts.cull_exponent), _p(val), _p(g)))
+        return val, g
+
+
+def superpose(sources, mat: Material, x, t: float, opts: SuperposeOptions = SuperposeOptions(),
+              ctx: Optional[Context] = None):
+    """Reference-shaped convenience: one or many points -> (value, grad)."""
+    own = ctx is None
+    ctx = ctx or Context()
+    try:
+        ctx.set_sources(sources, mat)
+        pts = np.asarray(x, dtype=np.float64)
+        single = pts.ndim == 1
+        v, g = ctx.superpose(pts.reshape(-1, 3), t, opts)
+        return (v[0], g[0]) if single else (v, g)
+    finally:
+        if own:
+            ctx.close()

@@ -1,0 +1,155 @@
+// Device context behind the C ABI: one CUDA stream, grow-only device buffers,
+// the uploaded scan history and the profiling counters.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "../../include/thermiga_b200.h"
+#include "host/analytic.hpp"
+#include "k1_superpose.cuh"
+
+namespace tgb {
+
+struct cuda_error : std::runtime_error {
+  explicit cuda_error(const std::string& m) : std::runtime_error(m) {}
+};
+
+inline void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess)
+    throw cuda_error(std::string("cuda: ") + what + ": " + cudaGetErrorString(e));
+}
+#define TG_CUDA(call) ::tgb::cuda_check((call), #call)
+
+// Grow-only device allocation.
+template <typename T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t cap = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+  T* ensure(size_t n) {
+    if (n > cap) {
+      if (p) TG_CUDA(cudaFree(p));
+      p = nullptr;
+      cap = 0;
+      TG_CUDA(cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(T)));
+      cap = n;
+    }
+    return p;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+};
+
+// Per-kernel event timing for the roofline (CUDA events on the launch stream).
+struct KernelTimer {
+  bool on = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> live;  // pending pairs
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pool;
+  double k1_ms = 0.0, k2_ms = 0.0;
+  std::vector<int> kinds;
+  double k1_pairs = 0.0, k2_bytes = 0.0;
+  long launches = 0, k1_launches = 0, k2_launches = 0;
+
+  std::pair<cudaEvent_t, cudaEvent_t> get() {
+    if (!pool.empty()) {
+      auto e = pool.back();
+      pool.pop_back();
+      return e;
+    }
+    std::pair<cudaEvent_t, cudaEvent_t> e;
+    TG_CUDA(cudaEventCreate(&e.first));
+    TG_CUDA(cudaEventCreate(&e.second));
+    return e;
+  }
+  // Bracket one launch of kernel class `kind` (1 = K1 main, 2 = K2 main).
+  template <typename F>
+  void timed(int kind, cudaStream_t s, F&& launch) {
+    if (!on) {
+      launch();
+      return;
+    }
+    auto e = get();
+    TG_CUDA(cudaEventRecord(e.first, s));
+    launch();
+    TG_CUDA(cudaEventRecord(e.second, s));
+    live.push_back(e);
+    kinds.push_back(kind);
+  }
+  void collect() {
+    for (size_t i = 0; i < live.size(); ++i) {
+      TG_CUDA(cudaEventSynchronize(live[i].second));
+      float ms = 0.f;
+      TG_CUDA(cudaEventElapsedTime(&ms, live[i].first, live[i].second));
+      (kinds[i] == 1 ? k1_ms : k2_ms) += ms;
+      pool.push_back(live[i]);
+    }
+    live.clear();
+    kinds.clear();
+  }
+  void reset() {
+    collect();
+    k1_ms = k2_ms = 0.0;
+    k1_pairs = k2_bytes = 0.0;
+    launches = k1_launches = k2_launches = 0;
+  }
+  ~KernelTimer() {
+    for (auto& e : live) pool.push_back(e);
+    for (auto& e : pool) {
+      cudaEventDestroy(e.first);
+      cudaEventDestroy(e.second);
+    }
+  }
+};
+
+}  // namespace tgb
+
+struct tg_ctx {
+  int device = 0;
+  int sm_count = 148;
+  cudaStream_t stream = nullptr;
+  std::string err;
+  tgb::KernelTimer timer;
+
+  // K1 state
+  tgb::Material mat;
+  int n_src = 0;
+  tgb::DevBuf<double> src6;
+  tgb::DevBuf<tgb::SrcRec> rec;
+  tgb::DevBuf<double> part;
+  tgb::DevBuf<double> pts, val, grad;
+  int k1_points_per_thread = 2;
+
+  cudaStream_t pick(void* s) const { return s ? static_cast<cudaStream_t>(s) : stream; }
+};
+
+namespace tgb {
+
+// K1 on device arrays: prepare the per-time source records, run the partial
+// kernel over S source splits, then the epilogue selected by `mode`.
+enum class K1Mode { field, dirichlet, flux };
+
+struct K1Flux {
+  const int* index = nullptr;      // qp ids of the points (nullable = identity)
+  const double* normals = nullptr; // per qp
+  const double* weights = nullptr; // per qp
+  double k = 0.0;
+};
+
+void k1_run(tg_ctx* ctx, const double* d_src6, int n_src, const double* d_pts,
+            const int* d_index, long n_pts, double t, double cull, K1Mode mode, double* d_out_a,
+            double* d_out_b, const K1Flux& flux, cudaStream_t stream);
+
+}  // namespace tgb

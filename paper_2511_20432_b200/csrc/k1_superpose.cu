@@ -1,0 +1,302 @@
+// K1 — batched point-source superposition of the analytic field T~ and its
+// gradient (reference: superpose, proj/src/analytic.cpp:92-109).
+//
+// Layout and schedule (sm_100a):
+//   * per call, k1_prepare_sources turns the history {x, y, z, E, t_act, tau}
+//     into 64-byte SrcRec records holding every per-source, per-time constant
+//     (the reference recomputes pow(pi*spread, 1.5) per pair, analytic.cpp:104);
+//   * k1_partial: one thread owns P points (registers), a CTA owns 256*P points
+//     and one contiguous source range; source records stream through a 3-stage
+//     shared-memory ring filled by TMA bulk copies (cp.async.bulk + mbarrier)
+//     and are read as warp-wide broadcasts;
+//   * the source dimension is split into S ranges (grid.y) so that the grid
+//     holds >= ~16 waves of CTAs on 148 SMs; k1_combine_* sums the S partials in
+//     a fixed order (deterministic reruns) and applies the caller's epilogue
+//     (plain field, -k dT/dn * w flux integrand, or -T Dirichlet value).
+//
+// Exactness: the causality test (t - tau > 0), the spread 4*alpha*dt and the
+// cull decision fl(r.r / spread) > cull reproduce the reference's discrete
+// choices bit for bit: r.r is formed with the reference's association and no
+// FMA, and the cull threshold thr_j is the largest double a with
+// fl(a / spread_j) <= cull, found with IEEE division in the prologue.
+#include <cmath>
+
+#include "common.cuh"
+#include "k1_superpose.cuh"
+
+namespace tgb {
+
+__constant__ double c_exp_table[kExpTableSize];
+
+__global__ void k1_prepare_sources(const double* __restrict__ src6, int n, double t,
+                                   double alpha4, double alpha2, double rcp, double cull,
+                                   SrcRec* __restrict__ out) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  const double* s = src6 + 6 * static_cast<size_t>(j);
+  SrcRec r;
+  r.sx = s[0];
+  r.sy = s[1];
+  r.sz = s[2];
+  r.pad = 0.0;
+  const double E = s[3];
+  const double dt = __dsub_rn(t, s[5]);  // analytic.cpp:97
+  bool active = dt > 0.0 && E > 0.0;     // E == 0 contributes exact zeros
+  double spread = 1.0, lnc = 0.0, thr = -1.0;
+  if (active) {
+    spread = __dmul_rn(alpha4, dt);  // 4.0 * alpha * dt
+    const double c = E / (rcp * pow(M_PI * spread, 1.5));
+    lnc = log(c);
+    // largest a with fl(a / spread) <= cull (exact cull decision)
+    double a = cull < 0.0 ? -1.0 : __dmul_rn(cull, spread);
+    if (a >= 0.0 && isfinite(a)) {
+      for (int it = 0; it < 16 && a > 0.0 && __ddiv_rn(a, spread) > cull; ++it)
+        a = __longlong_as_double(__double_as_longlong(a) - 1);  // next down (a > 0)
+      for (int it = 0; it < 16; ++it) {
+        const double b = __longlong_as_double(__double_as_longlong(a) + 1);  // next up
+        if (isfinite(b) && __ddiv_rn(b, spread) <= cull) a = b; else break;
+      }
+    }
+    // keep exp(lnc - r2/spread) in the normal range: contributions below
+    // 2^-1021 relative to nothing are flushed (only reachable without culling)
+    const double lim = (lnc + 707.0) * spread;
+    if (!(lim > 0.0) || !isfinite(lnc)) active = false;
+    thr = fmin(a, lim);
+  }
+  if (!active) {
+    spread = 1.0;
+    lnc = 0.0;
+    thr = -1.0;
+  }
+  r.nis = active ? -1.0 / spread : 0.0;
+  r.lnc = lnc;
+  r.gfac = active ? -1.0 / __dmul_rn(alpha2, dt) : 0.0;
+  r.thr = thr;
+  out[j] = r;
+}
+
+template <int P, bool GRAD>
+__global__ void __launch_bounds__(kK1Threads, 3)
+    k1_partial(const SrcRec* __restrict__ src, int n_src, int split_len,
+               const double* __restrict__ pts, const int* __restrict__ pt_index, int n_pts,
+               double* __restrict__ part) {
+  __shared__ __align__(16) SrcRec ring[kK1Stages][kK1Chunk];
+  __shared__ double tab[kExpTableSize];
+  __shared__ __align__(8) uint64_t bars[kK1Stages];
+
+  const int tid = threadIdx.x;
+  const int s = blockIdx.y;
+  const int begin = s * split_len;
+  const int len = max(0, min(n_src, begin + split_len) - begin);
+  const int n_chunks = (len + kK1Chunk - 1) / kK1Chunk;
+
+  if (tid < kExpTableSize) tab[tid] = c_exp_table[tid];
+  if (tid == 0) {
+    for (int b = 0; b < kK1Stages; ++b) mbar_init(&bars[b], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (tid == 0) {
+    for (int c = 0; c < kK1Stages && c < n_chunks; ++c) {
+      const int cnt = min(kK1Chunk, len - c * kK1Chunk);
+      const uint32_t bytes = static_cast<uint32_t>(cnt * sizeof(SrcRec));
+      mbar_arrive_expect_tx(&bars[c], bytes);
+      bulk_g2s(&ring[c][0], src + begin + c * kK1Chunk, bytes, &bars[c]);
+    }
+  }
+
+  // this thread's points
+  double px[P], py[P], pz[P], v[P], gx[P], gy[P], gz[P];
+  const int base = blockIdx.x * (kK1Threads * P) + tid;
+#pragma unroll
+  for (int k = 0; k < P; ++k) {
+    const int i = base + k * kK1Threads;
+    px[k] = py[k] = pz[k] = 0.0;
+    if (i < n_pts) {
+      const int pi = pt_index ? pt_index[i] : i;
+      px[k] = pts[3 * static_cast<size_t>(pi)];
+      py[k] = pts[3 * static_cast<size_t>(pi) + 1];
+      pz[k] = pts[3 * static_cast<size_t>(pi) + 2];
+    }
+    v[k] = gx[k] = gy[k] = gz[k] = 0.0;
+  }
+
+  for (int c = 0; c < n_chunks; ++c) {
+    const int buf = c % kK1Stages;
+    mbar_wait(&bars[buf], static_cast<uint32_t>((c / kK1Stages) & 1));
+    const int cnt = min(kK1Chunk, len - c * kK1Chunk);
+    const SrcRec* rb = ring[buf];
+#pragma unroll 2
+    for (int j = 0; j < cnt; ++j) {
+      const double4 a = *reinterpret_cast<const double4*>(&rb[j].sx);   // sx sy sz nis
+      const double4 b = *reinterpret_cast<const double4*>(&rb[j].lnc);  // lnc gfac thr pad
+#pragma unroll
+      for (int k = 0; k < P; ++k) {
+        const double rx = __dsub_rn(px[k], a.x);
+        const double ry = __dsub_rn(py[k], a.y);
+        const double rz = __dsub_rn(pz[k], a.z);
+        // r.r with the reference's association (core.hpp:27), no contraction
+        const double r2 =
+            __dadd_rn(__dadd_rn(__dmul_rn(rx, rx), __dmul_rn(ry, ry)), __dmul_rn(rz, rz));
+        const double e = fast_exp(__fma_rn(r2, a.w, b.x), tab);
+        const double T = (r2 <= b.z) ? e : 0.0;
+        v[k] = __dadd_rn(v[k], T);
+        if (GRAD) {
+          const double w = __dmul_rn(T, b.y);
+          gx[k] = __fma_rn(rx, w, gx[k]);
+          gy[k] = __fma_rn(ry, w, gy[k]);
+          gz[k] = __fma_rn(rz, w, gz[k]);
+        }
+      }
+    }
+    __syncthreads();  // everyone is done with ring[buf]
+    if (tid == 0 && c + kK1Stages < n_chunks) {
+      const int cn = c + kK1Stages;
+      const int cnt2 = min(kK1Chunk, len - cn * kK1Chunk);
+      const uint32_t bytes = static_cast<uint32_t>(cnt2 * sizeof(SrcRec));
+      mbar_arrive_expect_tx(&bars[buf], bytes);
+      bulk_g2s(&ring[buf][0], src + begin + cn * kK1Chunk, bytes, &bars[buf]);
+    }
+  }
+
+  const size_t plane = static_cast<size_t>(n_pts);
+  double* pv = part + static_cast<size_t>(s) * (GRAD ? 4 : 1) * plane;
+#pragma unroll
+  for (int k = 0; k < P; ++k) {
+    const int i = base + k * kK1Threads;
+    if (i < n_pts) {
+      pv[i] = v[k];
+      if (GRAD) {
+        pv[plane + i] = gx[k];
+        pv[2 * plane + i] = gy[k];
+        pv[3 * plane + i] = gz[k];
+      }
+    }
+  }
+}
+
+// plain field: val[i], grad[3i..3i+2]
+__global__ void k1_combine_field(const double* __restrict__ part, int S, int n,
+                                 double* __restrict__ val, double* __restrict__ grad) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const size_t plane = static_cast<size_t>(n);
+  double v = 0.0, x = 0.0, y = 0.0, z = 0.0;
+  for (int s = 0; s < S; ++s) {
+    const double* p = part + static_cast<size_t>(s) * 4 * plane;
+    v += p[i];
+    x += p[plane + i];
+    y += p[2 * plane + i];
+    z += p[3 * plane + i];
+  }
+  val[i] = v;
+  if (grad) {
+    grad[3 * static_cast<size_t>(i)] = x;
+    grad[3 * static_cast<size_t>(i) + 1] = y;
+    grad[3 * static_cast<size_t>(i) + 2] = z;
+  }
+}
+
+// Dirichlet values: out[i] = -T~ (mesh.cpp:261); partials are value-only.
+__global__ void k1_combine_dirichlet(const double* __restrict__ part, int S, int n,
+                                     double* __restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double v = 0.0;
+  for (int s = 0; s < S; ++s) v += part[static_cast<size_t>(s) * n + i];
+  out[i] = -v;
+}
+
+// Flux integrand at face quadrature points (assembly.cpp:161-164, :135):
+// g_q = (-k * grad.n) * w, with the qp addressed through pt_index.
+__global__ void k1_combine_flux(const double* __restrict__ part, int S, int n,
+                                const int* __restrict__ pt_index,
+                                const double* __restrict__ normals,
+                                const double* __restrict__ weights, double k,
+                                double* __restrict__ gq) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const size_t plane = static_cast<size_t>(n);
+  double x = 0.0, y = 0.0, z = 0.0;
+  for (int s = 0; s < S; ++s) {
+    const double* p = part + static_cast<size_t>(s) * 4 * plane;
+    x += p[plane + i];
+    y += p[2 * plane + i];
+    z += p[3 * plane + i];
+  }
+  const int q = pt_index ? pt_index[i] : i;
+  const double* nn = normals + 3 * static_cast<size_t>(q);
+  const double dot = __dadd_rn(__dadd_rn(__dmul_rn(x, nn[0]), __dmul_rn(y, nn[1])),
+                               __dmul_rn(z, nn[2]));
+  gq[i] = __dmul_rn(__dmul_rn(-k, dot), weights[q]);
+}
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+
+void k1_upload_exp_table(cudaStream_t stream) {
+  double tab[kExpTableSize];
+  for (int j = 0; j < kExpTableSize; ++j)
+    tab[j] = static_cast<double>(exp2l(static_cast<long double>(j) / kExpTableSize));
+  cudaMemcpyToSymbolAsync(c_exp_table, tab, sizeof(tab), 0, cudaMemcpyHostToDevice, stream);
+}
+
+int k1_choose_splits(int n_pts, int n_src, int sm_count, int points_per_cta) {
+  const int tiles = (n_pts + points_per_cta - 1) / points_per_cta;
+  const long target = static_cast<long>(sm_count) * 3 * 16;  // ~16 waves of 3 CTAs/SM
+  int S = static_cast<int>((target + tiles - 1) / tiles);
+  const int max_s = std::max(1, n_src / 256);  // keep >= 256 sources per split
+  S = std::max(1, std::min(S, max_s));
+  return S;
+}
+
+void k1_prepare(const double* d_src6, int n, double t, double alpha, double rcp, double cull,
+                SrcRec* d_rec, cudaStream_t stream) {
+  if (n <= 0) return;
+  const int threads = 256;
+  k1_prepare_sources<<<(n + threads - 1) / threads, threads, 0, stream>>>(
+      d_src6, n, t, 4.0 * alpha, 2.0 * alpha, rcp, cull, d_rec);
+}
+
+void k1_launch_partial(const SrcRec* d_rec, int n_src, const double* d_pts,
+                       const int* d_index, int n_pts, int S, bool grad, int P, double* d_part,
+                       cudaStream_t stream) {
+  const int split_len = (n_src + S - 1) / S;
+  const int ppc = kK1Threads * P;
+  dim3 grid((n_pts + ppc - 1) / ppc, S);
+  if (grad) {
+    if (P == 1)
+      k1_partial<1, true><<<grid, kK1Threads, 0, stream>>>(d_rec, n_src, split_len, d_pts, d_index, n_pts, d_part);
+    else if (P == 4)
+      k1_partial<4, true><<<grid, kK1Threads, 0, stream>>>(d_rec, n_src, split_len, d_pts, d_index, n_pts, d_part);
+    else
+      k1_partial<2, true><<<grid, kK1Threads, 0, stream>>>(d_rec, n_src, split_len, d_pts, d_index, n_pts, d_part);
+  } else {
+    if (P == 1)
+      k1_partial<1, false><<<grid, kK1Threads, 0, stream>>>(d_rec, n_src, split_len, d_pts, d_index, n_pts, d_part);
+    else if (P == 4)
+      k1_partial<4, false><<<grid, kK1Threads, 0, stream>>>(d_rec, n_src, split_len, d_pts, d_index, n_pts, d_part);
+    else
+      k1_partial<2, false><<<grid, kK1Threads, 0, stream>>>(d_rec, n_src, split_len, d_pts, d_index, n_pts, d_part);
+  }
+}
+
+void k1_launch_combine_field(const double* d_part, int S, int n, double* d_val, double* d_grad,
+                             cudaStream_t stream) {
+  k1_combine_field<<<(n + 255) / 256, 256, 0, stream>>>(d_part, S, n, d_val, d_grad);
+}
+
+void k1_launch_combine_dirichlet(const double* d_part, int S, int n, double* d_out,
+                                 cudaStream_t stream) {
+  k1_combine_dirichlet<<<(n + 255) / 256, 256, 0, stream>>>(d_part, S, n, d_out);
+}
+
+void k1_launch_combine_flux(const double* d_part, int S, int n, const int* d_index,
+                            const double* d_normals, const double* d_weights, double k,
+                            double* d_gq, cudaStream_t stream) {
+  k1_combine_flux<<<(n + 255) / 256, 256, 0, stream>>>(d_part, S, n, d_index, d_normals,
+                                                        d_weights, k, d_gq);
+}
+
+}  // namespace tgb

@@ -1,0 +1,38 @@
+// K1 — point-source superposition kernels (see k1_superpose.cu).
+#pragma once
+
+#include <algorithm>
+#include <cuda_runtime.h>
+
+namespace tgb {
+
+// Per-source, per-time constants; 64 bytes so one TMA bulk copy moves a tile.
+struct __align__(16) SrcRec {
+  double sx, sy, sz;  // position (m)
+  double nis;         // -1 / spread, spread = 4 alpha (t - tau)
+  double lnc;         // log(E / (rho c (pi spread)^1.5))
+  double gfac;        // -1 / (2 alpha (t - tau))
+  double thr;         // keep the pair iff r.r <= thr (cull and causality folded in)
+  double pad;
+};
+static_assert(sizeof(SrcRec) == 64, "SrcRec must stay 64 bytes");
+
+constexpr int kK1Threads = 256;
+constexpr int kK1Chunk = 128;  // sources per shared-memory stage (8 KB)
+constexpr int kK1Stages = 3;
+
+void k1_upload_exp_table(cudaStream_t stream);
+int k1_choose_splits(int n_pts, int n_src, int sm_count, int points_per_cta);
+void k1_prepare(const double* d_src6, int n, double t, double alpha, double rcp, double cull,
+                SrcRec* d_rec, cudaStream_t stream);
+void k1_launch_partial(const SrcRec* d_rec, int n_src, const double* d_pts, const int* d_index,
+                       int n_pts, int S, bool grad, int P, double* d_part, cudaStream_t stream);
+void k1_launch_combine_field(const double* d_part, int S, int n, double* d_val, double* d_grad,
+                             cudaStream_t stream);
+void k1_launch_combine_dirichlet(const double* d_part, int S, int n, double* d_out,
+                                 cudaStream_t stream);
+void k1_launch_combine_flux(const double* d_part, int S, int n, const int* d_index,
+                            const double* d_normals, const double* d_weights, double k,
+                            double* d_gq, cudaStream_t stream);
+
+}  // namespace tgb

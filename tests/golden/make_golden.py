@@ -1,0 +1,52 @@
+"""Regenerate the committed golden vectors from the UNMODIFIED reference
+library (oracle/_ref, built from /root/reference by oracle/Makefile).
+
+    python tests/golden/make_golden.py [k1] [cfg0]
+
+The fixtures let the GPU-side parity tests run on hosts where the reference
+sources are not mounted; tests/test_oracle_pins.py re-checks them against the
+live reference whenever it is available.
+"""
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, ROOT)
+
+from oracle import pyoracle  # noqa: E402
+from paper_2511_20432_b200 import workloads as W  # noqa: E402
+
+K1_SAMPLE = 2048
+
+
+def k1(R):
+    kw = dict(**W.MATERIAL, **W.LASER)
+    src = R.discretize_scan(W.config1_waypoints(), plane_z=1e-3, **kw)[:W.CONFIG1_SOURCES]
+    t = float(src[-1, 4])
+    pts = W.config1_points()[:K1_SAMPLE]
+    val, grad = R.superpose(src, pts, t, threads=os.cpu_count(), **kw)
+    # single dwell source probed around activation (causality, peak, cull)
+    dwell = R.discretize_scan([[1e-3, 1e-3]], plane_z=1e-3, **kw)
+    g = np.linspace(-2e-4, 2e-4, 9)
+    probe = np.array([[1e-3 + a, 1e-3 + b, 1e-3 + c] for a in g for b in g[::2] for c in g[::4]])
+    times = np.array([dwell[0, 5] - 1e-9, dwell[0, 5], dwell[0, 5] + 1e-9, dwell[0, 4], 1e-5,
+                      1e-4, 1e-3])
+    dv = np.zeros((len(times), len(probe)))
+    dg = np.zeros((len(times), len(probe), 3))
+    for i, tt in enumerate(times):
+        dv[i], dg[i] = R.superpose(dwell, probe, tt, **kw)
+    np.savez_compressed(os.path.join(HERE, "k1_cfg1.npz"), t=t, n_sources=len(src),
+                        sample=K1_SAMPLE, val=val, grad=grad, dwell=dwell, probe=probe,
+                        times=times, dwell_val=dv, dwell_grad=dg)
+    print("k1_cfg1.npz", val.shape)
+
+
+if __name__ == "__main__":
+    what = sys.argv[1:] or ["k1"]
+    pyoracle.build(ref=True)
+    R = pyoracle.RefLib()
+    if "k1" in what:
+        k1(R)
