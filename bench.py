@@ -215,7 +215,8 @@ def run_ours(args):
     val = torch.empty(n, dtype=torch.float64, device=dev)
     grad = torch.empty((n, 3), dtype=torch.float64, device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
-    stream = torch.cuda.current_stream(dev)
+    stream = torch.cuda.Stream(dev)  # a real stream: events and kernels share it
+    torch.cuda.set_stream(stream)
     sp = stream.cuda_stream
     pairs_per_step = float(n) * len(src)
 
@@ -236,7 +237,7 @@ def run_ours(args):
     barrier()
     with sampler:
         for i in range(args.steps):
-            flush.zero_()
+            flush.zero_()  # on `stream`, outside the step's events
             evs[i][0].record(stream)
             step()
             evs[i][1].record(stream)

@@ -10,7 +10,9 @@
  * Conventions
  *  - Plain pointers and sizes only. "host" arrays are caller-owned CPU memory;
  *    "_device" variants take CUDA device pointers and a cudaStream_t (as void*,
- *    NULL = the context's own stream) and do not synchronize.
+ *    NULL = the legacy default stream, as everywhere in CUDA) and do not
+ *    synchronize; host variants run on the context's own stream and return
+ *    after the results are in host memory.
  *  - Vectors over control points use the reference's flat order, first index
  *    fastest (ControlGrid::index, proj/include/thermiga/splines.hpp:73-75).
  *  - Points are xyz-interleaved doubles (Vec3, proj/include/thermiga/core.hpp:14).

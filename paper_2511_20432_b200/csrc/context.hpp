@@ -132,7 +132,8 @@ struct tg_ctx {
   tgb::DevBuf<double> pts, val, grad;
   int k1_points_per_thread = 2;
 
-  cudaStream_t pick(void* s) const { return s ? static_cast<cudaStream_t>(s) : stream; }
+  // device-pointer entry points run on the caller's stream (NULL = legacy default)
+  static cudaStream_t pick(void* s) { return static_cast<cudaStream_t>(s); }
 };
 
 namespace tgb {

@@ -1,0 +1,187 @@
+#include "mesh.hpp"
+
+#include <algorithm>
+#include <cmath>
+
+namespace tgb {
+
+FaceId BoundaryTags::bottom_face() const {
+  for (FaceId f : kFaces)
+    if (role_of(f) == FaceRole::bottom) return f;
+  throw config_error("boundary tags: no face tagged bottom");
+}
+
+void BoundaryTags::validate() const {
+  int nb = 0, nl = 0;
+  for (FaceId f : kFaces) {
+    nb += role_of(f) == FaceRole::bottom;
+    nl += role_of(f) == FaceRole::lateral;
+  }
+  if (nb != 1) throw config_error("boundary tags: exactly one face must be bottom");
+  if (nl < 1) throw config_error("boundary tags: at least one face must be lateral");
+}
+
+BoundaryTags BoundaryTags::extruded_default() {
+  BoundaryTags t;
+  t.role.fill(FaceRole::lateral);
+  t.role[static_cast<int>(FaceId::zetamin)] = FaceRole::bottom;
+  t.role[static_cast<int>(FaceId::zetamax)] = FaceRole::top;
+  return t;
+}
+
+DofMap make_dof_map(const NurbsVolume& vol, const BoundaryTags& tags) {
+  tags.validate();
+  const FaceId bottom = tags.bottom_face();
+  const int ax = face_axis(bottom);
+  const auto n = vol.basis_counts();
+  const int layer = face_is_min(bottom) ? 0 : n[ax] - 1;
+  DofMap m;
+  m.free_index.assign(vol.n_functions(), -1);
+  m.constrained_index.assign(vol.n_functions(), -1);
+  for (int k = 0; k < n[2]; ++k)
+    for (int j = 0; j < n[1]; ++j)
+      for (int i = 0; i < n[0]; ++i) {
+        const int ijk[3] = {i, j, k};
+        const int g = vol.grid().index(i, j, k);
+        if (ijk[ax] == layer) {
+          m.constrained_index[g] = m.n_constrained();
+          m.constrained_list.push_back(g);
+        } else {
+          m.free_index[g] = m.n_free();
+          m.free_list.push_back(g);
+        }
+      }
+  return m;
+}
+
+FaceSets build_face_sets(const NurbsVolume& vol, const BoundaryTags& tags, int fine_mult) {
+  tags.validate();
+  fine_mult = std::max(1, fine_mult);
+  const auto p = vol.degrees();
+  FaceSets fs;
+  std::vector<int> idx;
+  std::vector<double> val;
+  std::vector<Vec3> dv;
+  for (FaceId f : kFaces) {
+    if (tags.role_of(f) != FaceRole::lateral) continue;
+    const auto t = face_tangent_axes(f);
+    const auto bu = vol.knots(t[0]).breakpoints();
+    const auto bv = vol.knots(t[1]).breakpoints();
+    const int qu = p[t[0]] + 1, qv = p[t[1]] + 1;
+    fs.nq_base = qu * qv;
+    fs.nq_fine = fine_mult * qu * fine_mult * qv;
+    fs.n_dofs = (p[0] + 1) * (p[1] + 1) * (p[2] + 1);
+    for (std::size_t jv = 0; jv + 1 < bv.size(); ++jv)
+      for (std::size_t iu = 0; iu + 1 < bu.size(); ++iu) {
+        const double hu = 0.5 * (bu[iu + 1] - bu[iu]), mu = 0.5 * (bu[iu + 1] + bu[iu]);
+        const double hv = 0.5 * (bv[jv + 1] - bv[jv]), mv = 0.5 * (bv[jv + 1] + bv[jv]);
+        bool have_dofs = false;
+        auto rule = [&](int nu, int nv, std::vector<double>& X, std::vector<double>& Nn,
+                        std::vector<double>& Wt, std::vector<double>& Nt) {
+          const auto& gu = gauss_rule(nu);
+          const auto& gv = gauss_rule(nv);
+          for (int b = 0; b < nv; ++b)
+            for (int a = 0; a < nu; ++a) {
+              const double u = mu + hu * gu.nodes[a];
+              const double v = mv + hv * gv.nodes[b];
+              const auto sp = vol.face_point(f, u, v);
+              const int nbas = vol.basis_at(sp.xi, idx, val, dv);
+              if (!have_dofs) {
+                fs.dofs.insert(fs.dofs.end(), idx.begin(), idx.end());
+                have_dofs = true;
+              }
+              X.insert(X.end(), {sp.x.x, sp.x.y, sp.x.z});
+              Nn.insert(Nn.end(), {sp.normal.x, sp.normal.y, sp.normal.z});
+              Wt.push_back(gu.weights[a] * gv.weights[b] * hu * hv * sp.area_scale);
+              Nt.insert(Nt.end(), val.begin(), val.begin() + nbas);
+            }
+        };
+        rule(qu, qv, fs.xb, fs.nb, fs.wb, fs.Nb);
+        rule(fine_mult * qu, fine_mult * qv, fs.xf, fs.nf, fs.wf, fs.Nf);
+        const auto c = vol.face_point(f, mu, mv);
+        fs.centers.insert(fs.centers.end(), {c.x.x, c.x.y, c.x.z});
+        ++fs.n_elems;
+      }
+  }
+  return fs;
+}
+
+std::vector<double> greville_points(const NurbsVolume& vol, const DofMap& dofs,
+                                    const BoundaryTags& tags) {
+  const FaceId bottom = tags.bottom_face();
+  const auto t = face_tangent_axes(bottom);
+  const auto g0 = vol.knots(t[0]).greville();
+  const auto g1 = vol.knots(t[1]).greville();
+  const auto n = vol.basis_counts();
+  std::vector<double> out;
+  out.reserve(3 * dofs.n_constrained());
+  for (int c = 0; c < dofs.n_constrained(); ++c) {
+    const int g = dofs.constrained_list[c];
+    const int ijk[3] = {g % n[0], (g / n[0]) % n[1], g / (n[0] * n[1])};
+    const Vec3 x = vol.map_point(face_param(bottom, g0[ijk[t[0]]], g1[ijk[t[1]]])).x;
+    out.insert(out.end(), {x.x, x.y, x.z});
+  }
+  return out;
+}
+
+ElementGrid element_grid(const NurbsVolume& vol) {
+  ElementGrid eg;
+  for (int d = 0; d < 3; ++d) {
+    eg.bp[d] = vol.knots(d).breakpoints();
+    eg.n_el[d] = static_cast<int>(eg.bp[d].size()) - 1;
+  }
+  return eg;
+}
+
+void element_quad(const NurbsVolume& vol, const ElementGrid& eg, int e, std::array<int, 3> nq,
+                  ElementQuad& out) {
+  const int ei = e % eg.n_el[0];
+  const int ej = (e / eg.n_el[0]) % eg.n_el[1];
+  const int ek = e / (eg.n_el[0] * eg.n_el[1]);
+  const int el[3] = {ei, ej, ek};
+  double half[3], mid[3];
+  for (int d = 0; d < 3; ++d) {
+    half[d] = 0.5 * (eg.bp[d][el[d] + 1] - eg.bp[d][el[d]]);
+    mid[d] = 0.5 * (eg.bp[d][el[d] + 1] + eg.bp[d][el[d]]);
+  }
+  const double box = half[0] * half[1] * half[2];
+  const auto& g0 = gauss_rule(nq[0]);
+  const auto& g1 = gauss_rule(nq[1]);
+  const auto& g2 = gauss_rule(nq[2]);
+  out.n_qp = nq[0] * nq[1] * nq[2];
+  const auto p = vol.degrees();
+  out.n_basis = (p[0] + 1) * (p[1] + 1) * (p[2] + 1);
+  out.weight.assign(out.n_qp, 0.0);
+  out.N.assign(static_cast<size_t>(out.n_qp) * out.n_basis, 0.0);
+  out.dN.assign(static_cast<size_t>(out.n_qp) * out.n_basis, Vec3{});
+  std::vector<int> idx;
+  std::vector<double> val;
+  std::vector<Vec3> dv;
+  int q = 0;
+  for (int c = 0; c < nq[2]; ++c)
+    for (int b = 0; b < nq[1]; ++b)
+      for (int a = 0; a < nq[0]; ++a, ++q) {
+        const Vec3 xi{mid[0] + half[0] * g0.nodes[a], mid[1] + half[1] * g1.nodes[b],
+                      mid[2] + half[2] * g2.nodes[c]};
+        const int nb = vol.basis_at(xi, idx, val, dv);
+        if (nb != out.n_basis) throw numeric_error("basis block size mismatch");
+        if (q == 0) out.dofs = idx;
+        Mat3 J;
+        for (int m = 0; m < nb; ++m) {
+          const auto& cp = vol.grid().pts[idx[m]];
+          for (int r = 0; r < 3; ++r)
+            for (int s = 0; s < 3; ++s) J(r, s) += cp[r] * dv[m][s];
+        }
+        const double det = J.det();
+        if (!(det > 0.0))
+          throw numeric_error("non-positive Jacobian determinant at quadrature point");
+        const Mat3 inv = J.inverse();
+        out.weight[q] = g0.weights[a] * g1.weights[b] * g2.weights[c] * box * det;
+        for (int m = 0; m < nb; ++m) {
+          out.N[static_cast<size_t>(q) * nb + m] = val[m];
+          out.dN[static_cast<size_t>(q) * nb + m] = inv.apply_transposed(dv[m]);
+        }
+      }
+}
+
+}  // namespace tgb
