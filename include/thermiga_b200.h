@@ -100,6 +100,67 @@ int tg_superpose_batch(tg_ctx* ctx, const double* pts_xyz, long n, double t, dou
 int tg_superpose_batch_device(tg_ctx* ctx, const double* d_pts_xyz, long n, double t,
                               double cull, double* d_val, double* d_grad, void* stream);
 
+/* ---- simulation (K1 + K2 + K3 behind the reference's driver) ------------ */
+
+/* Overrides for a parsed config; zero fields keep the config's value. */
+typedef struct tg_sim_options {
+  double t_end;      /* [stepping] t_end */
+  double solver_tol; /* [stepping] solver_tol */
+  int max_iter;      /* [stepping] max_iter */
+  int device;        /* CUDA device ordinal */
+  int host_only;     /* 1: host setup only (no device; compute calls fail) */
+} tg_sim_options;
+
+/* parse_config + prepare_simulation (proj/src/config.cpp:253-416,
+ * proj/src/driver.cpp:66-95): the config format is the reference's. On
+ * failure *out is still set so tg_sim_last_error can be read; destroy it. */
+int tg_sim_create(const char* config_path, const tg_sim_options* opt, tg_sim** out);
+void tg_sim_destroy(tg_sim* sim);
+const char* tg_sim_last_error(const tg_sim* sim);
+/* The simulation's device context (profiling counters, K1 sources). */
+int tg_sim_context(tg_sim* sim, tg_ctx** out);
+/* out[18]: n_full, n_free, n_constrained, n_steps, n_sources, n_face_elements,
+ * nx, ny, nz, px, py, pz, kronecker(1)/assembled(0), max nq_base, max nq_fine,
+ * ndofs_kept, total base qps, total fine qps */
+int tg_sim_info(tg_sim* sim, long* out);
+/* out[10]: dt_solver, theta, solver_tol, elevate_radius, cull_exponent,
+ * conductivity, density, heat_capacity, platform_temperature, max_iter */
+int tg_sim_params(tg_sim* sim, double* out);
+int tg_sim_sources(tg_sim* sim, tg_point_source* out, int max_out);
+/* Lateral face quadrature sets as uploaded (classify_boundary,
+ * proj/src/mesh.cpp:158-236): per-element offsets into the base / fine rules
+ * (n_face_elements + 1 each), centers, kept DOF columns (-1 = pad), base then
+ * fine quadrature points, normals, weights and basis tables. */
+int tg_sim_face_sets(tg_sim* sim, int* qb_off, int* qf_off, double* centers, int* dofs,
+                     double* xq, double* nq, double* wq, double* Nb, double* Nf);
+int tg_sim_greville_points(tg_sim* sim, double* out_xyz);
+/* Banded 1D factors of the Kronecker operator for axis dir (n x (2p+1),
+ * [i][p + j - i]); TG_ERROR when the patch is not separable. */
+int tg_sim_kron_factors(tg_sim* sim, int dir, double* M, double* K);
+
+/* assemble_flux_load (proj/src/assembly.cpp:148-166): F (n_full) at time t;
+ * fine_radius < 0 uses the config's elevate_radius. */
+int tg_sim_flux_load(tg_sim* sim, double t, double fine_radius, double* out_F);
+/* dirichlet_values (proj/src/mesh.cpp:238-264): g (n_constrained) at time t. */
+int tg_sim_dirichlet_values(tg_sim* sim, double t, double* out_g);
+/* theta_step (proj/src/timestep.cpp:5-24) with pcg_jacobi
+ * (proj/src/sparse.cpp:41-100): warm-started from free_n. Returns TG_ENUMERIC
+ * with the reference's message on non-convergence or a non-SPD operator. */
+int tg_sim_theta_step(tg_sim* sim, const double* free_n, const double* g_n, const double* F_n,
+                      const double* F_np1, const double* g_np1, double tol, int max_iter,
+                      double* free_out, int* iters, double* rel);
+/* y = A_ff x, the reduced theta-step operator (DirichletSystem::reduced_operator,
+ * proj/include/thermiga/assembly.hpp:56). */
+int tg_sim_operator_apply(tg_sim* sim, const double* x_free, double* y_free);
+
+/* run_time_loop (proj/src/driver.cpp:105-146) with the state resident on the
+ * device: reset = step 0 (free = 0, g_0, F_0); advance = n steps. */
+int tg_sim_reset(tg_sim* sim);
+int tg_sim_advance(tg_sim* sim, int n_steps, long* cg_iterations, double* last_rel);
+/* Copy the current state to the host (any pointer may be NULL). */
+int tg_sim_state(tg_sim* sim, int* step, double* time, double* free_out, double* g_out,
+                 double* F_out);
+
 #ifdef __cplusplus
 }
 #endif

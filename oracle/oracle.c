@@ -220,14 +220,12 @@ int or_pcg_jacobi(int n, const int* rp, const int* col, const double* val, const
 /* src/assembly.cpp:117-166 — element-local accumulation in q order, then a
  * serial scatter in (face, element, a) order; the fine rule follows the newest
  * source with t_activate <= t (assembly.cpp:153-157). */
-void or_boundary_load(int n_fe, int nqb, int nqf, int nd, const int* dofs,
+void or_boundary_load(int n_fe, int nd, const int* nq_base, const int* nq_fine, const int* dofs,
                       const double* centers, const double* xb, const double* nb,
                       const double* wb, const double* Nb, const double* xf, const double* nf,
-                      const double* wf, const double* Nf, const int* face_of_elem, int n_src,
-                      const double* src6, int n_full, double t, double fine_radius, double cull,
-                      double k, double rho, double c, double unused, double* load) {
-  (void)face_of_elem;
-  (void)unused;
+                      const double* wf, const double* Nf, int n_src, const double* src6,
+                      int n_full, double t, double fine_radius, double cull, double k,
+                      double rho, double c, double* load) {
   const double alpha = k / (rho * c);
   const double rcp = rho * c;
   int have_focus = 0;
@@ -241,6 +239,7 @@ void or_boundary_load(int n_fe, int nqb, int nqf, int nd, const int* dofs,
   }
   memset(load, 0, sizeof(double) * (size_t)n_full);
   double* loc = (double*)malloc(sizeof(double) * (size_t)nd);
+  size_t ob = 0, of = 0;
   for (int e = 0; e < n_fe; ++e) {
     const double* ce = centers + 3 * (size_t)e;
     int fine = 0;
@@ -248,11 +247,12 @@ void or_boundary_load(int n_fe, int nqb, int nqf, int nd, const int* dofs,
       const double dx = ce[0] - focus[0], dy = ce[1] - focus[1], dz = ce[2] - focus[2];
       fine = sqrt(dx * dx + dy * dy + dz * dz) < fine_radius;
     }
-    const int nq = fine ? nqf : nqb;
-    const double* X = fine ? xf + 3 * (size_t)e * nqf : xb + 3 * (size_t)e * nqb;
-    const double* Nn = fine ? nf + 3 * (size_t)e * nqf : nb + 3 * (size_t)e * nqb;
-    const double* W = fine ? wf + (size_t)e * nqf : wb + (size_t)e * nqb;
-    const double* N = fine ? Nf + (size_t)e * nqf * nd : Nb + (size_t)e * nqb * nd;
+    const int nq = fine ? nq_fine[e] : nq_base[e];
+    const size_t o = fine ? of : ob;
+    const double* X = (fine ? xf : xb) + 3 * o;
+    const double* Nn = (fine ? nf : nb) + 3 * o;
+    const double* W = (fine ? wf : wb) + o;
+    const double* N = (fine ? Nf : Nb) + o * nd;
     for (int a = 0; a < nd; ++a) loc[a] = 0.0;
     for (int q = 0; q < nq; ++q) {
       double v, g[3];
@@ -263,6 +263,8 @@ void or_boundary_load(int n_fe, int nqb, int nqf, int nd, const int* dofs,
       for (int a = 0; a < nd; ++a) loc[a] += gq * N[(size_t)q * nd + a];
     }
     for (int a = 0; a < nd; ++a) load[dofs[(size_t)e * nd + a]] += loc[a];
+    ob += (size_t)nq_base[e];
+    of += (size_t)nq_fine[e];
   }
   free(loc);
 }

@@ -38,13 +38,14 @@ int or_pcg_jacobi(int n, const int* row_ptr, const int* col, const double* val, 
                   double* x, double tol, int max_iter, int* iters, double* rel);
 
 /* assemble_flux_load + assemble_boundary_load: src/assembly.cpp:117-166, on
- * face sets flattened in (face, element, q) order (mesh.hpp:84-113). */
-void or_boundary_load(int n_fe, int nq_base, int nq_fine, int n_dofs, const int* dofs,
-                      const double* centers, const double* xb, const double* nb,
+ * face sets flattened in (face, element, q) order (mesh.hpp:84-113) with
+ * per-element rule sizes nq_base[e], nq_fine[e]. */
+void or_boundary_load(int n_fe, int n_dofs, const int* nq_base, const int* nq_fine,
+                      const int* dofs, const double* centers, const double* xb, const double* nb,
                       const double* wb, const double* Nb, const double* xf, const double* nf,
-                      const double* wf, const double* Nf, const int* face_of_elem, int n_src,
-                      const double* src6, int n_full, double t, double fine_radius, double cull,
-                      double k, double rho, double c, double unused, double* load);
+                      const double* wf, const double* Nf, int n_src, const double* src6,
+                      int n_full, double t, double fine_radius, double cull, double k,
+                      double rho, double c, double* load);
 
 #ifdef __cplusplus
 }

@@ -70,7 +70,7 @@ class RefLib:
         L.ref_sim_info.argtypes = [C.c_void_p, _lp]
         L.ref_sim_params.argtypes = [C.c_void_p, _dp]
         L.ref_sim_sources.argtypes = [C.c_void_p, _dp]
-        L.ref_sim_face_sets.argtypes = [C.c_void_p, _lp, _dp, _ip] + [_dp] * 8
+        L.ref_sim_face_sets.argtypes = [C.c_void_p, _lp, _ip, _ip, _dp, _ip] + [_dp] * 8
         L.ref_sim_greville_points.argtypes = [C.c_void_p, _dp]
         L.ref_sim_knots.argtypes = [C.c_void_p, C.c_int, _dp]
         L.ref_sim_flux_load.argtypes = [C.c_void_p, C.c_double, _dp, C.c_int]
@@ -193,14 +193,18 @@ class RefSim:
         return out
 
     def face_sets(self):
+        """Flattened face sets: per-element rule sizes nqb/nqf, qps in
+        (face, element, q) order (xb: (total_base, 3), Nb: (total_base, nd), ...)."""
         cnt = np.zeros(4, dtype=np.int64)
-        self.L.ref_sim_face_sets(self.h, _ptr(cnt, _lp), None, None, *([None] * 8))
-        ne, nqb, nqf, nd = (int(c) for c in cnt)
-        d = dict(centers=np.zeros((ne, 3)), dofs=np.zeros((ne, nd), dtype=np.int32),
-                 xb=np.zeros((ne, nqb, 3)), nb=np.zeros((ne, nqb, 3)), wb=np.zeros((ne, nqb)),
-                 Nb=np.zeros((ne, nqb, nd)), xf=np.zeros((ne, nqf, 3)), nf=np.zeros((ne, nqf, 3)),
-                 wf=np.zeros((ne, nqf)), Nf=np.zeros((ne, nqf, nd)))
-        self.L.ref_sim_face_sets(self.h, _ptr(cnt, _lp), _ptr(d["centers"]), _ptr(d["dofs"], _ip),
+        self.L.ref_sim_face_sets(self.h, _ptr(cnt, _lp), None, None, None, None, *([None] * 8))
+        ne, tqb, tqf, nd = (int(c) for c in cnt)
+        d = dict(nqb=np.zeros(ne, dtype=np.int32), nqf=np.zeros(ne, dtype=np.int32),
+                 centers=np.zeros((ne, 3)), dofs=np.zeros((ne, nd), dtype=np.int32),
+                 xb=np.zeros((tqb, 3)), nb=np.zeros((tqb, 3)), wb=np.zeros(tqb),
+                 Nb=np.zeros((tqb, nd)), xf=np.zeros((tqf, 3)), nf=np.zeros((tqf, 3)),
+                 wf=np.zeros(tqf), Nf=np.zeros((tqf, nd)))
+        self.L.ref_sim_face_sets(self.h, _ptr(cnt, _lp), _ptr(d["nqb"], _ip), _ptr(d["nqf"], _ip),
+                                 _ptr(d["centers"]), _ptr(d["dofs"], _ip),
                                  _ptr(d["xb"]), _ptr(d["nb"]), _ptr(d["wb"]), _ptr(d["Nb"]),
                                  _ptr(d["xf"]), _ptr(d["nf"]), _ptr(d["wf"]), _ptr(d["Nf"]))
         return d
@@ -302,10 +306,10 @@ class COracle:
         L.or_csr_spmv.argtypes = [C.c_int, _ip, _ip, _dp, _dp, _dp]
         L.or_pcg_jacobi.restype = C.c_int
         L.or_pcg_jacobi.argtypes = [C.c_int, _ip, _ip, _dp, _dp, _dp, C.c_double, C.c_int, _ip, _dp]
-        L.or_boundary_load.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, _ip, _dp, _dp, _dp, _dp,
-                                       _dp, _dp, _dp, _dp, _dp, _ip, C.c_int, _dp, C.c_int,
+        L.or_boundary_load.argtypes = [C.c_int, C.c_int, _ip, _ip, _ip, _dp, _dp, _dp, _dp, _dp,
+                                       _dp, _dp, _dp, _dp, C.c_int, _dp, C.c_int, C.c_double,
                                        C.c_double, C.c_double, C.c_double, C.c_double, C.c_double,
-                                       C.c_double, C.c_double, _dp]
+                                       _dp]
 
     def discretize_scan(self, waypoints, *, start_time=0.0, plane_z=0.0, power, speed,
                         spot_radius, absorptivity, dt, conductivity, density, heat_capacity, **_):
@@ -359,19 +363,16 @@ class COracle:
         return x, it.value, rel.value, rc
 
     def boundary_load(self, fs, sources, t, *, fine_radius, n_full, conductivity, density,
-                      heat_capacity, cull=60.0, face_of_elem=None, **_):
+                      heat_capacity, cull=60.0, **_):
         """assemble_flux_load restated (face sets as exported by RefSim.face_sets)."""
-        ne, nqb, nd = fs["Nb"].shape
-        nqf = fs["Nf"].shape[1]
-        if face_of_elem is None:
-            face_of_elem = np.zeros(ne, dtype=np.int32)
+        ne, nd = fs["dofs"].shape
         arr = {k: np.ascontiguousarray(v) for k, v in fs.items()}
         s = np.ascontiguousarray(sources, dtype=np.float64)
         F = np.zeros(n_full)
-        foe = np.ascontiguousarray(face_of_elem, dtype=np.int32)
-        self.L.or_boundary_load(ne, nqb, nqf, nd, _ptr(arr["dofs"], _ip), _ptr(arr["centers"]),
+        self.L.or_boundary_load(ne, nd, _ptr(arr["nqb"], _ip), _ptr(arr["nqf"], _ip),
+                                _ptr(arr["dofs"], _ip), _ptr(arr["centers"]),
                                 _ptr(arr["xb"]), _ptr(arr["nb"]), _ptr(arr["wb"]), _ptr(arr["Nb"]),
                                 _ptr(arr["xf"]), _ptr(arr["nf"]), _ptr(arr["wf"]), _ptr(arr["Nf"]),
-                                _ptr(foe, _ip), len(s), _ptr(s), n_full, t, fine_radius, cull,
-                                conductivity, density, heat_capacity, 0.0, _ptr(F))
+                                len(s), _ptr(s), n_full, t, fine_radius, cull,
+                                conductivity, density, heat_capacity, _ptr(F))
         return F

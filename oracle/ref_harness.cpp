@@ -209,48 +209,47 @@ int ref_sim_sources(void* h, double* out6) {
 }
 
 // Lateral face quadrature sets (proj/src/mesh.cpp:158-236), flattened in
-// (face, element, q) order. counts: [n_fe, nq_base, nq_fine, n_dofs_per_fe].
-// Any output pointer may be null (then only counts are returned).
-int ref_sim_face_sets(void* h, long* counts, double* centers, int* dofs, double* xb,
-                      double* nb, double* wb, double* Nb, double* xf, double* nf, double* wf,
-                      double* Nf) {
+// (face, element, q) order; the rule sizes differ between faces when the
+// degrees differ per direction, so per-element counts are exported too.
+// counts: [n_fe, total base qps, total fine qps, n_dofs_per_fe].
+// With centers == null only counts are returned.
+int ref_sim_face_sets(void* h, long* counts, int* nq_base, int* nq_fine, double* centers,
+                      int* dofs, double* xb, double* nb, double* wb, double* Nb, double* xf,
+                      double* nf, double* wf, double* Nf) {
   const Simulation& s = static_cast<RefSim*>(h)->sim;
-  long n_fe = 0, nqb = 0, nqf = 0, nd = 0;
+  long n_fe = 0, tqb = 0, tqf = 0, nd = 0;
   for (const auto& f : s.boundary.lateral)
     for (const auto& fe : f.elements) {
       ++n_fe;
-      nqb = static_cast<long>(fe.qp_base.size());
-      nqf = static_cast<long>(fe.qp_fine.size());
+      tqb += static_cast<long>(fe.qp_base.size());
+      tqf += static_cast<long>(fe.qp_fine.size());
       nd = static_cast<long>(fe.dofs.size());
     }
   counts[0] = n_fe;
-  counts[1] = nqb;
-  counts[2] = nqf;
+  counts[1] = tqb;
+  counts[2] = tqf;
   counts[3] = nd;
   if (!centers) return 0;
-  long e = 0;
+  long e = 0, ob = 0, of = 0;
+  auto put = [nd](const FaceQuadPoint& qp, const double* N, long o, double* x, double* n,
+                  double* w, double* NN) {
+    x[3 * o] = qp.x.x; x[3 * o + 1] = qp.x.y; x[3 * o + 2] = qp.x.z;
+    n[3 * o] = qp.normal.x; n[3 * o + 1] = qp.normal.y; n[3 * o + 2] = qp.normal.z;
+    w[o] = qp.weight;
+    for (long a = 0; a < nd; ++a) NN[o * nd + a] = N[a];
+  };
   for (const auto& f : s.boundary.lateral)
     for (const auto& fe : f.elements) {
       centers[3 * e] = fe.center.x;
       centers[3 * e + 1] = fe.center.y;
       centers[3 * e + 2] = fe.center.z;
       for (long a = 0; a < nd; ++a) dofs[e * nd + a] = fe.dofs[a];
-      for (long q = 0; q < nqb; ++q) {
-        const auto& qp = fe.qp_base[q];
-        const long o = e * nqb + q;
-        xb[3 * o] = qp.x.x; xb[3 * o + 1] = qp.x.y; xb[3 * o + 2] = qp.x.z;
-        nb[3 * o] = qp.normal.x; nb[3 * o + 1] = qp.normal.y; nb[3 * o + 2] = qp.normal.z;
-        wb[o] = qp.weight;
-        for (long a = 0; a < nd; ++a) Nb[o * nd + a] = fe.N_base[q * nd + a];
-      }
-      for (long q = 0; q < nqf; ++q) {
-        const auto& qp = fe.qp_fine[q];
-        const long o = e * nqf + q;
-        xf[3 * o] = qp.x.x; xf[3 * o + 1] = qp.x.y; xf[3 * o + 2] = qp.x.z;
-        nf[3 * o] = qp.normal.x; nf[3 * o + 1] = qp.normal.y; nf[3 * o + 2] = qp.normal.z;
-        wf[o] = qp.weight;
-        for (long a = 0; a < nd; ++a) Nf[o * nd + a] = fe.N_fine[q * nd + a];
-      }
+      nq_base[e] = static_cast<int>(fe.qp_base.size());
+      nq_fine[e] = static_cast<int>(fe.qp_fine.size());
+      for (size_t q = 0; q < fe.qp_base.size(); ++q, ++ob)
+        put(fe.qp_base[q], &fe.N_base[q * nd], ob, xb, nb, wb, Nb);
+      for (size_t q = 0; q < fe.qp_fine.size(); ++q, ++of)
+        put(fe.qp_fine[q], &fe.N_fine[q * nd], of, xf, nf, wf, Nf);
       ++e;
     }
   return 0;

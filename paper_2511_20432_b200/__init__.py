@@ -5,7 +5,8 @@ behind the C ABI ``include/thermiga_b200.h``); this package is its Python
 binding and the seeded BASELINE workloads.
 """
 from .api import (ConfigError, Context, CudaError, LaserSpec, Material, NumericError, ScanPath,
+                  Simulation,
                   SuperposeOptions, ThermigaError, discretize_scan, lib, superpose)
 
 __all__ = ["ConfigError", "Context", "CudaError", "LaserSpec", "Material", "NumericError",
-           "ScanPath", "SuperposeOptions", "ThermigaError", "discretize_scan", "lib", "superpose"]
+           "ScanPath", "Simulation", "SuperposeOptions", "ThermigaError", "discretize_scan", "lib", "superpose"]

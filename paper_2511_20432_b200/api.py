@@ -263,3 +263,176 @@ def superpose(sources, mat: Material, x, t: float, opts: SuperposeOptions = Supe
     finally:
         if own:
             ctx.close()
+
+
+class _SimOptions(C.Structure):
+    _fields_ = [("t_end", C.c_double), ("solver_tol", C.c_double), ("max_iter", C.c_int),
+                ("device", C.c_int), ("host_only", C.c_int)]
+
+
+def _bind_sim(L):
+    if getattr(L, "_sim_bound", False):
+        return
+    L.tg_sim_create.argtypes = [C.c_char_p, C.POINTER(_SimOptions), C.POINTER(C.c_void_p)]
+    L.tg_sim_destroy.argtypes = [C.c_void_p]
+    L.tg_sim_last_error.restype = C.c_char_p
+    L.tg_sim_last_error.argtypes = [C.c_void_p]
+    L.tg_sim_context.argtypes = [C.c_void_p, C.POINTER(C.c_void_p)]
+    L.tg_sim_info.argtypes = [C.c_void_p, C.POINTER(C.c_long)]
+    L.tg_sim_params.argtypes = [C.c_void_p, _dp]
+    L.tg_sim_sources.argtypes = [C.c_void_p, _dp, C.c_int]
+    L.tg_sim_face_sets.argtypes = [C.c_void_p, _ip, _ip, _dp, _ip, _dp, _dp, _dp, _dp, _dp]
+    L.tg_sim_greville_points.argtypes = [C.c_void_p, _dp]
+    L.tg_sim_kron_factors.argtypes = [C.c_void_p, C.c_int, _dp, _dp]
+    L.tg_sim_flux_load.argtypes = [C.c_void_p, C.c_double, C.c_double, _dp]
+    L.tg_sim_dirichlet_values.argtypes = [C.c_void_p, C.c_double, _dp]
+    L.tg_sim_theta_step.argtypes = [C.c_void_p, _dp, _dp, _dp, _dp, _dp, C.c_double, C.c_int,
+                                    _dp, _ip, _dp]
+    L.tg_sim_operator_apply.argtypes = [C.c_void_p, _dp, _dp]
+    L.tg_sim_reset.argtypes = [C.c_void_p]
+    L.tg_sim_advance.argtypes = [C.c_void_p, C.c_int, C.POINTER(C.c_long), _dp]
+    L.tg_sim_state.argtypes = [C.c_void_p, _ip, _dp, _dp, _dp, _dp]
+    L._sim_bound = True
+
+
+class _BorrowedContext(Context):
+    """The context owned by a Simulation (not destroyed by Python)."""
+
+    def __init__(self, L, h):  # noqa: D401 - no base init: the handle is borrowed
+        self._L, self._h = L, h
+
+    def close(self):
+        self._h = None
+
+
+class Simulation:
+    """prepare_simulation + run_time_loop of the reference (driver.hpp:20-47) on the GPU.
+
+    The hot-path calls keep the reference's names: ``flux_load`` =
+    assemble_flux_load, ``dirichlet_values``, ``theta_step``; ``reset`` /
+    ``advance`` / ``state`` run the time loop with the state resident on the device.
+    """
+
+    INFO_KEYS = ["n_full", "n_free", "n_constrained", "n_steps", "n_sources", "n_face_elems",
+                 "nx", "ny", "nz", "px", "py", "pz", "kronecker", "nq_base", "nq_fine",
+                 "n_dofs_kept", "total_qb", "total_qf"]
+    PARAM_KEYS = ["dt", "theta", "solver_tol", "elevate_radius", "cull", "conductivity",
+                  "density", "heat_capacity", "platform_temperature", "max_iter"]
+
+    def __init__(self, config_path, t_end=0.0, solver_tol=0.0, max_iter=0, device=0,
+                 host_only=False):
+        L = self._L = lib()
+        _bind_sim(L)
+        opt = _SimOptions(t_end, solver_tol, max_iter, device, int(host_only))
+        h = C.c_void_p()
+        rc = L.tg_sim_create(str(config_path).encode(), C.byref(opt), C.byref(h))
+        self._h = h
+        if rc != TG_OK:
+            msg = L.tg_sim_last_error(h).decode() if h else "tg_sim_create failed"
+            L.tg_sim_destroy(h)
+            self._h = None
+            raise _ERRORS.get(rc, ThermigaError)(msg)
+        info = (C.c_long * 18)()
+        self._check(L.tg_sim_info(h, info))
+        self.info = {k: int(v) for k, v in zip(self.INFO_KEYS, info)}
+        par = np.zeros(10)
+        self._check(L.tg_sim_params(h, _p(par)))
+        self.params = dict(zip(self.PARAM_KEYS, par.tolist()))
+
+    def _check(self, rc):
+        if rc != TG_OK:
+            raise _ERRORS.get(rc, ThermigaError)(self._L.tg_sim_last_error(self._h).decode())
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._L.tg_sim_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def context(self) -> Context:
+        h = C.c_void_p()
+        self._check(self._L.tg_sim_context(self._h, C.byref(h)))
+        return _BorrowedContext(self._L, h)
+
+    def sources(self):
+        out = np.zeros((self.info["n_sources"], 6))
+        self._check(self._L.tg_sim_sources(self._h, _p(out), len(out)))
+        return out
+
+    def face_sets(self):
+        """Face sets as uploaded: qb_off/qf_off per-element offsets, xq/nq/wq all base
+        points then all fine points, Nb (total_qb, kept), Nf (total_qf, kept)."""
+        i = self.info
+        ne, nd, tqb, tqf = i["n_face_elems"], i["n_dofs_kept"], i["total_qb"], i["total_qf"]
+        d = dict(qb_off=np.zeros(ne + 1, dtype=np.int32), qf_off=np.zeros(ne + 1, dtype=np.int32),
+                 centers=np.zeros((ne, 3)), dofs=np.zeros((ne, nd), dtype=np.int32),
+                 xq=np.zeros((tqb + tqf, 3)), nq=np.zeros((tqb + tqf, 3)), wq=np.zeros(tqb + tqf),
+                 Nb=np.zeros((tqb, nd)), Nf=np.zeros((tqf, nd)))
+        ip = lambda a: a.ctypes.data_as(_ip)  # noqa: E731
+        self._check(self._L.tg_sim_face_sets(self._h, ip(d["qb_off"]), ip(d["qf_off"]),
+                                             _p(d["centers"]), ip(d["dofs"]), _p(d["xq"]),
+                                             _p(d["nq"]), _p(d["wq"]), _p(d["Nb"]), _p(d["Nf"])))
+        return d
+
+    def greville_points(self):
+        out = np.zeros((self.info["n_constrained"], 3))
+        self._check(self._L.tg_sim_greville_points(self._h, _p(out)))
+        return out
+
+    def kron_factors(self, d):
+        n, p = self.info["nx"] if d == 0 else self.info["ny"] if d == 1 else self.info["nz"], \
+            self.info["px"]
+        M = np.zeros((n, 2 * p + 1))
+        K = np.zeros((n, 2 * p + 1))
+        self._check(self._L.tg_sim_kron_factors(self._h, d, _p(M), _p(K)))
+        return M, K
+
+    def flux_load(self, t, fine_radius=-1.0):
+        F = np.zeros(self.info["n_full"])
+        self._check(self._L.tg_sim_flux_load(self._h, float(t), float(fine_radius), _p(F)))
+        return F
+
+    def dirichlet_values(self, t):
+        g = np.zeros(self.info["n_constrained"])
+        self._check(self._L.tg_sim_dirichlet_values(self._h, float(t), _p(g)))
+        return g
+
+    def theta_step(self, free_n, g_n, F_n, F_np1, g_np1, tol=None, max_iter=None):
+        tol = self.params["solver_tol"] if tol is None else tol
+        max_iter = int(self.params["max_iter"]) if max_iter is None else max_iter
+        a = [_f64(v) for v in (free_n, g_n, F_n, F_np1, g_np1)]
+        out = np.zeros(self.info["n_free"])
+        it = C.c_int(0)
+        rel = C.c_double(0.0)
+        self._check(self._L.tg_sim_theta_step(self._h, *[_p(v) for v in a], float(tol),
+                                              int(max_iter), _p(out), C.byref(it), C.byref(rel)))
+        return out, it.value, rel.value
+
+    def operator_apply(self, x):
+        xx = _f64(x)
+        y = np.zeros(self.info["n_free"])
+        self._check(self._L.tg_sim_operator_apply(self._h, _p(xx), _p(y)))
+        return y
+
+    def reset(self):
+        self._check(self._L.tg_sim_reset(self._h))
+
+    def advance(self, n_steps=1):
+        it = C.c_long(0)
+        rel = C.c_double(0.0)
+        self._check(self._L.tg_sim_advance(self._h, int(n_steps), C.byref(it), C.byref(rel)))
+        return it.value, rel.value
+
+    def state(self):
+        step = C.c_int(0)
+        t = C.c_double(0.0)
+        x = np.zeros(self.info["n_free"])
+        g = np.zeros(self.info["n_constrained"])
+        F = np.zeros(self.info["n_full"])
+        self._check(self._L.tg_sim_state(self._h, C.byref(step), C.byref(t), _p(x), _p(g), _p(F)))
+        return dict(step=step.value, time=t.value, free=x, g=g, F=F)

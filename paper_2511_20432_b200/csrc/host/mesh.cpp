@@ -59,6 +59,9 @@ FaceSets build_face_sets(const NurbsVolume& vol, const BoundaryTags& tags, int f
   fine_mult = std::max(1, fine_mult);
   const auto p = vol.degrees();
   FaceSets fs;
+  fs.n_dofs = (p[0] + 1) * (p[1] + 1) * (p[2] + 1);
+  fs.qb_off.push_back(0);
+  fs.qf_off.push_back(0);
   std::vector<int> idx;
   std::vector<double> val;
   std::vector<Vec3> dv;
@@ -68,9 +71,6 @@ FaceSets build_face_sets(const NurbsVolume& vol, const BoundaryTags& tags, int f
     const auto bu = vol.knots(t[0]).breakpoints();
     const auto bv = vol.knots(t[1]).breakpoints();
     const int qu = p[t[0]] + 1, qv = p[t[1]] + 1;
-    fs.nq_base = qu * qv;
-    fs.nq_fine = fine_mult * qu * fine_mult * qv;
-    fs.n_dofs = (p[0] + 1) * (p[1] + 1) * (p[2] + 1);
     for (std::size_t jv = 0; jv + 1 < bv.size(); ++jv)
       for (std::size_t iu = 0; iu + 1 < bu.size(); ++iu) {
         const double hu = 0.5 * (bu[iu + 1] - bu[iu]), mu = 0.5 * (bu[iu + 1] + bu[iu]);
@@ -100,6 +100,10 @@ FaceSets build_face_sets(const NurbsVolume& vol, const BoundaryTags& tags, int f
         rule(fine_mult * qu, fine_mult * qv, fs.xf, fs.nf, fs.wf, fs.Nf);
         const auto c = vol.face_point(f, mu, mv);
         fs.centers.insert(fs.centers.end(), {c.x.x, c.x.y, c.x.z});
+        fs.nqb.push_back(qu * qv);
+        fs.nqf.push_back(fine_mult * qu * fine_mult * qv);
+        fs.qb_off.push_back(fs.qb_off.back() + qu * qv);
+        fs.qf_off.push_back(fs.qf_off.back() + fine_mult * qu * fine_mult * qv);
         ++fs.n_elems;
       }
   }

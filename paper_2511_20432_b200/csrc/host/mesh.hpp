@@ -32,9 +32,13 @@ DofMap make_dof_map(const NurbsVolume& vol, const BoundaryTags& tags);
 
 // Lateral face quadrature, flattened in (face, element, q) order with q
 // v-outer / u-inner (mesh.cpp:158-205). Every face element carries the
-// (p+1)^3 volume DOFs active at its first quadrature point and both rules.
+// (p+1)^3 volume DOFs active at its first quadrature point and both rules;
+// rule sizes differ between faces when the degrees differ per direction, so
+// each element has its own counts and offsets into the flat arrays.
 struct FaceSets {
-  int n_elems = 0, nq_base = 0, nq_fine = 0, n_dofs = 0;
+  int n_elems = 0, n_dofs = 0;
+  std::vector<int> nqb, nqf;            // per element rule sizes
+  std::vector<long> qb_off, qf_off;     // per element offsets (n_elems + 1)
   std::vector<double> centers;          // 3 per element
   std::vector<int> dofs;                // n_dofs per element
   std::vector<double> xb, nb, wb, Nb;   // base rule: 3, 3, 1, n_dofs per qp

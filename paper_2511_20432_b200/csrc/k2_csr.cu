@@ -1,0 +1,210 @@
+// K2 general path — theta-step PCG on an assembled CSR operator, for patches
+// that are not separable (rational geometry such as the reference's
+// quarter-cylinder part, proj/src/splines.cpp:408-438). Same persistent
+// cooperative structure and reductions as the Kronecker path (k2_kron.cu); the
+// row products follow CsrMatrix::multiply (proj/src/sparse.cpp:25-31) term by
+// term without contraction, so each matvec row equals the reference's bit for
+// bit.
+#include <cooperative_groups.h>
+
+#include <algorithm>
+
+#include "context.hpp"
+#include "k2_csr.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace tgb {
+
+namespace {
+
+constexpr int kThreads = 256;
+
+__device__ __forceinline__ double row_dot(const DevCsr& A, int r, const double* __restrict__ x) {
+  double acc = 0.0;
+  for (int k = A.row_ptr[r]; k < A.row_ptr[r + 1]; ++k)
+    acc = __dadd_rn(acc, __dmul_rn(A.val[k], x[A.col[k]]));
+  return acc;
+}
+
+__device__ __forceinline__ void grid_reduce(cg::grid_group& grid, double (&acc)[4],
+                                            double* partials, int& buf, double* red,
+                                            double (&out)[4]) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    double v = acc[c];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    if (lane == 0) red[warp * 4 + c] = v;
+  }
+  __syncthreads();
+  double* pb = partials + static_cast<size_t>(buf) * 4 * gridDim.x;
+  if (tid < 4) {
+    double s = 0.0;
+    for (int w = 0; w < kThreads / 32; ++w) s += red[w * 4 + tid];
+    pb[blockIdx.x * 4 + tid] = s;
+  }
+  grid.sync();
+  if (warp == 0) {
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      double s = 0.0;
+      for (int b = lane; b < static_cast<int>(gridDim.x); b += 32) s += pb[b * 4 + c];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+      if (lane == 0) red[32 + c] = s;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int c = 0; c < 4; ++c) out[c] = red[32 + c];
+  __syncthreads();
+  buf ^= 1;
+}
+
+__global__ void __launch_bounds__(kThreads) csr_pcg_kernel(DevCsr A, const double* rhs,
+                                                           double* x, PcgWork w, double tol,
+                                                           int max_iter) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double red[64];
+  const int n = A.rows;
+  const int gtid = blockIdx.x * kThreads + threadIdx.x;
+  const int gstride = gridDim.x * kThreads;
+  int buf = 0;
+  double tot[4];
+  double acc[4] = {0, 0, 0, 0};
+  for (int f = gtid; f < n; f += gstride) {
+    const double bi = rhs[f];
+    const double ri = bi - row_dot(A, f, x);
+    const double zi = w.inv_diag[f] * ri;
+    w.r[f] = ri;
+    w.p[f] = zi;
+    acc[0] += ri * ri;
+    acc[1] += bi * bi;
+    acc[2] += ri * zi;
+  }
+  grid_reduce(grid, acc, w.partials, buf, red, tot);
+  double rr = tot[0], rz = tot[2];
+  const double bnorm = sqrt(tot[1]);
+  if (bnorm == 0.0) {
+    for (int f = gtid; f < n; f += gstride) x[f] = 0.0;
+    if (blockIdx.x == 0 && threadIdx.x == 0) *w.status = PcgStatus{0, 0, 0.0, 0.0};
+    return;
+  }
+  double rel = 0.0;
+  int it = 0, status = 3;
+  for (it = 0; it < max_iter; ++it) {
+    rel = sqrt(rr) / bnorm;
+    if (rel <= tol) {
+      status = 0;
+      break;
+    }
+    double a1[4] = {0, 0, 0, 0};
+    for (int f = gtid; f < n; f += gstride) {
+      const double y = row_dot(A, f, w.p);
+      w.Ap[f] = y;
+      a1[0] += w.p[f] * y;
+    }
+    grid_reduce(grid, a1, w.partials, buf, red, tot);
+    const double pAp = tot[0];
+    if (!(pAp > 0.0)) {
+      status = 4;
+      break;
+    }
+    const double alpha = rz / pAp;
+    double a2[4] = {0, 0, 0, 0};
+    for (int f = gtid; f < n; f += gstride) {
+      x[f] += alpha * w.p[f];
+      const double ri = w.r[f] - alpha * w.Ap[f];
+      w.r[f] = ri;
+      const double zi = w.inv_diag[f] * ri;
+      a2[0] += ri * zi;
+      a2[1] += ri * ri;
+    }
+    grid_reduce(grid, a2, w.partials, buf, red, tot);
+    const double beta = tot[0] / rz;
+    rz = tot[0];
+    rr = tot[1];
+    for (int f = gtid; f < n; f += gstride) w.p[f] = w.inv_diag[f] * w.r[f] + beta * w.p[f];
+    grid.sync();
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) *w.status = PcgStatus{it, status, rel, bnorm};
+}
+
+__global__ void csr_diag_kernel(DevCsr A, double* inv_diag, PcgStatus* st) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= A.rows) return;
+  double d = 0.0;
+  for (int k = A.row_ptr[r]; k < A.row_ptr[r + 1]; ++k)
+    if (A.col[k] == r) d = A.val[k];
+  if (!(d > 0.0)) st->status = 2;
+  inv_diag[r] = 1.0 / d;
+}
+
+// rhs_f = [B T]_f - [A g~]_f + theta F1 + (1 - theta) F0 (assembly.cpp:258-271)
+__global__ void csr_rhs_kernel(DevCsr Bf, DevCsr Ac, const double* T, const double* g1,
+                               const double* F0, const double* F1, const int* free_list,
+                               double theta, double* rhs) {
+  const int f = blockIdx.x * blockDim.x + threadIdx.x;
+  if (f >= Bf.rows) return;
+  const int g = free_list[f];
+  const double bt = row_dot(Bf, f, T);
+  const double ag = row_dot(Ac, f, g1);
+  rhs[f] = bt - ag + theta * F1[g] + (1.0 - theta) * F0[g];
+}
+
+}  // namespace
+
+int csr_pcg_max_blocks(int sm_count) {
+  int per_sm = 0;
+  TG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+      &per_sm, reinterpret_cast<const void*>(&csr_pcg_kernel), kThreads, 0));
+  return std::max(1, per_sm) * sm_count;
+}
+
+void csr_inverse_diagonal(const DevCsr& A, double* inv_diag, PcgStatus* st, cudaStream_t s) {
+  csr_diag_kernel<<<(A.rows + 255) / 256, 256, 0, s>>>(A, inv_diag, st);
+  TG_CUDA(cudaGetLastError());
+}
+
+void csr_theta_rhs(const DevCsr& Bf, const DevCsr& Ac, const double* T, const double* g1,
+                   const double* F0, const double* F1, const int* free_list, double theta,
+                   double* rhs, cudaStream_t s) {
+  if (Bf.rows <= 0) return;
+  csr_rhs_kernel<<<(Bf.rows + 255) / 256, 256, 0, s>>>(Bf, Ac, T, g1, F0, F1, free_list, theta,
+                                                       rhs);
+  TG_CUDA(cudaGetLastError());
+}
+
+void csr_pcg_solve(const DevCsr& A, const double* rhs, double* x, const PcgWork& w, double tol,
+                   int max_iter, int blocks, cudaStream_t s) {
+  const int need = (A.rows + kThreads - 1) / kThreads;
+  const int nb = std::max(1, std::min(blocks, need));
+  DevCsr AA = A;
+  PcgWork ww = w;
+  double tt = tol;
+  int mi = max_iter;
+  void* args[] = {&AA, const_cast<double**>(&rhs), &x, &ww, &tt, &mi};
+  TG_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(&csr_pcg_kernel), dim3(nb),
+                                      dim3(kThreads), args, 0, s));
+}
+
+}  // namespace tgb
+
+namespace tgb {
+
+namespace {
+__global__ void csr_apply_kernel(DevCsr A, const double* x, double* y) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < A.rows) y[r] = row_dot(A, r, x);
+}
+}  // namespace
+
+void csr_apply(const DevCsr& A, const double* x, double* y, cudaStream_t s) {
+  if (A.rows <= 0) return;
+  csr_apply_kernel<<<(A.rows + 255) / 256, 256, 0, s>>>(A, x, y);
+  TG_CUDA(cudaGetLastError());
+}
+
+}  // namespace tgb

@@ -1,0 +1,29 @@
+// K2 general (assembled CSR) path — see k2_csr.cu.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "k2_kron.cuh"
+
+namespace tgb {
+
+struct DevCsr {
+  int rows;
+  const int* row_ptr;
+  const int* col;
+  const double* val;
+};
+
+int csr_pcg_max_blocks(int sm_count);
+void csr_inverse_diagonal(const DevCsr& A, double* inv_diag, PcgStatus* st, cudaStream_t s);
+void csr_theta_rhs(const DevCsr& Bf, const DevCsr& Ac, const double* T, const double* g1,
+                   const double* F0, const double* F1, const int* free_list, double theta,
+                   double* rhs, cudaStream_t s);
+void csr_pcg_solve(const DevCsr& A, const double* rhs, double* x, const PcgWork& w, double tol,
+                   int max_iter, int blocks, cudaStream_t s);
+
+}  // namespace tgb
+
+namespace tgb {
+void csr_apply(const DevCsr& A, const double* x, double* y, cudaStream_t s);
+}  // namespace tgb

@@ -1,0 +1,71 @@
+// K2 — matrix-free theta-step operator and Jacobi-PCG for separable
+// (Kronecker) patches. See k2_kron.cu.
+#pragma once
+
+#include <cuda_runtime.h>
+
+namespace tgb {
+
+constexpr int kKronTX = 32;  // tile width along xi (one warp)
+constexpr int kKronTY = 8;   // tile height along eta
+constexpr int kKronMaxP = 3;
+
+// A grid of control points (possibly the free sub-grid) with the banded 1D
+// mass / stiffness factors of each direction: entry [i][P + (j - i)] of an
+// (n x (2P+1)) row-major band array is the (i, j) coupling.
+struct KronGrid {
+  int p;  // spline degree (1..3); band width 2p+1
+  int n[3];
+  const double* M[3];
+  const double* K[3];
+};
+
+// y = Op(a1, b1) v1 + Op(a2, b2) v2 with Op(a, b) = a (Mz x My x Mx) +
+//     b (Mz x My x Kx + Mz x Ky x Mx + Kz x My x Mx); v2 may be null.
+struct KronTerms {
+  double a1, b1, a2, b2;
+};
+
+// theta-step right-hand side on the free rows (assembly.cpp:245-272):
+//   rhs_f = [B T_n - A g~]_f + theta F_{n+1,f} + (1-theta) F_{n,f}
+struct RhsArgs {
+  const double* T_full;    // expanded state at level n (free + constrained)
+  const double* g_full;    // g_{n+1} on the constrained layer, zero elsewhere
+  const double* F_n;       // full-size loads
+  const double* F_np1;
+  double theta;
+  int bottom_axis, bottom_layer;  // constrained layer
+  double* rhs;             // n_free, free flat order
+};
+
+struct PcgStatus {
+  int iterations;
+  int status;  // 0 ok, 3 no convergence, 4 indefinite direction, 2 bad diagonal
+  double rel_residual;
+  double bnorm;
+};
+
+void k2_theta_rhs(const KronGrid& full, double a_b, double b_b, double a_a, double b_a,
+                  const RhsArgs& args, int sm_count, cudaStream_t s);
+
+// Jacobi-PCG on A = a Op_M + b Op_K over the free grid, one persistent
+// cooperative launch per solve; x holds the warm start on entry.
+struct PcgWork {
+  double* r;
+  double* p;
+  double* Ap;
+  double* inv_diag;
+  double* partials;  // >= 4 * max_blocks
+  PcgStatus* status;
+};
+void k2_inverse_diagonal(const KronGrid& g, double a, double b, double* inv_diag,
+                         PcgStatus* status, cudaStream_t s);
+int k2_pcg_max_blocks(int p, int sm_count);
+void k2_pcg_solve(const KronGrid& g, double a, double b, const double* rhs, double* x,
+                  const PcgWork& w, double tol, int max_iter, int blocks, cudaStream_t s);
+
+// plain y = Op(a, b) v on a grid (tests / benchmarks of the apply alone)
+void k2_apply(const KronGrid& g, double a, double b, const double* v, double* y, int sm_count,
+              cudaStream_t s);
+
+}  // namespace tgb

@@ -1,0 +1,441 @@
+// Simulation engine behind tg_sim_*: the host-side setup of the reference's
+// prepare_simulation (proj/src/driver.cpp:66-95) in C++, and the per-step hot
+// path of run_time_loop (driver.cpp:126-145) on the GPU:
+//   F_{n+1} = assemble_flux_load(t)   K1 (flux mode) + K3
+//   g_{n+1} = dirichlet_values(t)     K1 (value mode) at the Greville points
+//   theta_step                        K2: RHS kernel + persistent Jacobi-PCG
+// State (free coefficients, constrained values, loads) stays resident in HBM
+// between steps; the host only decides the fine-rule element set per step
+// (the reference's exact arithmetic) and reads back the PCG status.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+
+#include "context.hpp"
+#include "host/config.hpp"
+#include "host/operator.hpp"
+#include "k2_csr.cuh"
+#include "k2_kron.cuh"
+#include "k3_flux.cuh"
+#include "sim.hpp"
+
+namespace tgb {
+
+namespace {
+
+__global__ void expand_kernel(SimGeom g, const double* __restrict__ x,
+                              const double* __restrict__ gc, double* __restrict__ T) {
+  const long idx = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x;
+  const long n = static_cast<long>(g.n[0]) * g.n[1] * g.n[2];
+  if (idx >= n) return;
+  int ijk[3] = {static_cast<int>(idx % g.n[0]), static_cast<int>((idx / g.n[0]) % g.n[1]),
+                static_cast<int>(idx / (static_cast<long>(g.n[0]) * g.n[1]))};
+  if (ijk[g.ax] == g.layer) {
+    T[idx] = gc[ijk[g.t0] + g.n[g.t0] * ijk[g.t1]];
+  } else {
+    if (g.layer == 0) ijk[g.ax] -= 1;
+    int nf[3] = {g.n[0], g.n[1], g.n[2]};
+    nf[g.ax] -= 1;
+    T[idx] = x[ijk[0] + static_cast<long>(nf[0]) * (ijk[1] + static_cast<long>(nf[1]) * ijk[2])];
+  }
+}
+
+__global__ void scatter_layer_kernel(SimGeom g, const double* __restrict__ gc,
+                                     double* __restrict__ full) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  const int nc = g.n[g.t0] * g.n[g.t1];
+  if (c >= nc) return;
+  int ijk[3];
+  ijk[g.ax] = g.layer;
+  ijk[g.t0] = c % g.n[g.t0];
+  ijk[g.t1] = c / g.n[g.t0];
+  full[ijk[0] + static_cast<long>(g.n[0]) * (ijk[1] + static_cast<long>(g.n[1]) * ijk[2])] = gc[c];
+}
+
+template <typename T>
+void upload(DevBuf<T>& d, const std::vector<T>& h, cudaStream_t s) {
+  d.ensure(h.size());
+  if (!h.empty())
+    TG_CUDA(cudaMemcpyAsync(d.p, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice, s));
+}
+
+}  // namespace
+
+Sim::Sim(const std::string& path, const SimOptions& opt) {
+  RunConfig c = parse_config(path);
+  if (opt.t_end > 0.0) c.stepping.t_end = opt.t_end;
+  if (opt.solver_tol > 0.0) c.stepping.solver_tol = opt.solver_tol;
+  if (opt.max_iter > 0) c.stepping.max_iter = opt.max_iter;
+  cfg = std::move(c);
+  setup_host();
+  if (!opt.host_only) setup_device(opt.device);
+}
+
+Sim::~Sim() {
+  if (h_status) cudaFreeHost(h_status);
+  if (h_fine) cudaFreeHost(h_fine);
+  if (ctx) tg_ctx_destroy(ctx);
+}
+
+void Sim::setup_host() {
+  // prepare_simulation (driver.cpp:66-95)
+  vol = refine_for_spec(cfg.geometry, cfg.mesh);
+  const auto p = vol.degrees();
+  for (int d = 0; d < 3; ++d) quad[d] = cfg.mesh.quad_order > 0 ? cfg.mesh.quad_order : p[d] + 1;
+  dofs = make_dof_map(vol, cfg.tags);
+  sources = discretize_scan(cfg.scan, cfg.laser, cfg.material);
+  tact_max.resize(sources.size());
+  double m = -INFINITY;
+  for (size_t i = 0; i < sources.size(); ++i) tact_max[i] = m = std::max(m, sources[i].t_activate);
+  dt_solver = cfg.stepping.dt / cfg.stepping.substeps;
+  n_steps = static_cast<int>(std::ceil(cfg.stepping.t_end / dt_solver - 1e-9));
+
+  const auto n = vol.basis_counts();
+  const FaceId bottom = cfg.tags.bottom_face();
+  geom.n[0] = n[0];
+  geom.n[1] = n[1];
+  geom.n[2] = n[2];
+  geom.ax = face_axis(bottom);
+  geom.layer = face_is_min(bottom) ? 0 : n[geom.ax] - 1;
+  const auto t = face_tangent_axes(bottom);
+  geom.t0 = t[0];
+  geom.t1 = t[1];
+  n_full = vol.n_functions();
+  n_free = dofs.n_free();
+  n_con = dofs.n_constrained();
+
+  // lateral face sets, with the columns that are exactly zero on every
+  // quadrature point of an element dropped (their scatter adds +0, a no-op)
+  FaceSets fs = build_face_sets(vol, cfg.tags, cfg.mesh.boundary_quad_multiplier);
+  n_fe = fs.n_elems;
+  const int nd = fs.n_dofs;
+  const long tqb = fs.qb_off.back(), tqf = fs.qf_off.back();
+  if (tqb + tqf > (1L << 31) - 1) throw std::invalid_argument("face quadrature set too large");
+  h_qb_off.assign(fs.qb_off.begin(), fs.qb_off.end());
+  h_qf_off.assign(fs.qf_off.begin(), fs.qf_off.end());
+  nqb = nqf = 0;
+  for (int e = 0; e < n_fe; ++e) {
+    nqb = std::max(nqb, fs.nqb[e]);
+    nqf = std::max(nqf, fs.nqf[e]);
+  }
+  std::vector<std::vector<int>> keep(n_fe);
+  ndk = 0;
+  for (int e = 0; e < n_fe; ++e) {
+    for (int a = 0; a < nd; ++a) {
+      bool nz = false;
+      for (long q = fs.qb_off[e]; q < fs.qb_off[e + 1] && !nz; ++q) nz = fs.Nb[q * nd + a] != 0.0;
+      for (long q = fs.qf_off[e]; q < fs.qf_off[e + 1] && !nz; ++q) nz = fs.Nf[q * nd + a] != 0.0;
+      if (nz) keep[e].push_back(a);
+    }
+    ndk = std::max<int>(ndk, static_cast<int>(keep[e].size()));
+  }
+  ndk = std::max(ndk, 1);
+  centers = fs.centers;
+  h_qx = fs.xb;
+  h_qx.insert(h_qx.end(), fs.xf.begin(), fs.xf.end());
+  h_qn = fs.nb;
+  h_qn.insert(h_qn.end(), fs.nf.begin(), fs.nf.end());
+  h_qw = fs.wb;
+  h_qw.insert(h_qw.end(), fs.wf.begin(), fs.wf.end());
+  h_Nb.assign(static_cast<size_t>(tqb) * ndk, 0.0);
+  h_Nf.assign(static_cast<size_t>(tqf) * ndk, 0.0);
+  h_dofk.assign(static_cast<size_t>(n_fe) * ndk, -1);
+  std::vector<std::vector<int>> inc(n_full);
+  for (int e = 0; e < n_fe; ++e)
+    for (size_t kk = 0; kk < keep[e].size(); ++kk) {
+      const int a = keep[e][kk];
+      for (long q = fs.qb_off[e]; q < fs.qb_off[e + 1]; ++q) h_Nb[q * ndk + kk] = fs.Nb[q * nd + a];
+      for (long q = fs.qf_off[e]; q < fs.qf_off[e + 1]; ++q) h_Nf[q * ndk + kk] = fs.Nf[q * nd + a];
+      const int dof = fs.dofs[static_cast<size_t>(e) * nd + a];
+      h_dofk[static_cast<size_t>(e) * ndk + kk] = dof;
+      inc[dof].push_back(e * ndk + static_cast<int>(kk));
+    }
+  h_inc_ptr.assign(n_full + 1, 0);
+  for (int i = 0; i < n_full; ++i) h_inc_ptr[i + 1] = h_inc_ptr[i] + static_cast<int>(inc[i].size());
+  h_inc_src.reserve(h_inc_ptr[n_full]);
+  for (int i = 0; i < n_full; ++i) h_inc_src.insert(h_inc_src.end(), inc[i].begin(), inc[i].end());
+
+  grev = greville_points(vol, dofs, cfg.tags);
+
+  // operator: Kronecker factors when separable, else the assembled CSR pair
+  std::array<std::vector<double>, 3> coord;
+  kron = separable_coords(vol, coord);
+  const double dt = dt_solver, th = cfg.stepping.theta;
+  if (!(dt > 0.0)) throw std::invalid_argument("theta scheme: dt must be > 0");
+  if (!(th >= 0.0 && th <= 1.0)) throw std::invalid_argument("theta scheme: theta must be in [0,1]");
+  if (kron) {
+    for (int d = 0; d < 3; ++d) band[d] = assemble_band_1d(vol.knots(d), coord[d], quad[d]);
+    const double rc = cfg.material.volumetric_capacity(), k = cfg.material.conductivity;
+    coefA = {rc / dt, th * k};
+    coefB = {rc / dt, -(1.0 - th) * k};
+  } else {
+    Csr M, K;
+    assemble_mass_stiffness(vol, quad, cfg.material, M, K);
+    // A = M/dt + theta K, B = M/dt - (1-theta) K (assembly.cpp:194-199)
+    Csr A = M, B = M;
+    for (size_t i = 0; i < M.val.size(); ++i) {
+      A.val[i] = (1.0 / dt) * M.val[i] + th * K.val[i];
+      B.val[i] = (1.0 / dt) * M.val[i] + -(1.0 - th) * K.val[i];
+    }
+    auto extract = [&](const Csr& S, bool free_cols, Csr& out) {
+      out.rows = n_free;
+      out.row_ptr.assign(n_free + 1, 0);
+      out.col.clear();
+      out.val.clear();
+      for (int f = 0; f < n_free; ++f) {
+        const int r = dofs.free_list[f];
+        for (int q = S.row_ptr[r]; q < S.row_ptr[r + 1]; ++q) {
+          const int c = S.col[q];
+          if (free_cols) {
+            if (dofs.free_index[c] >= 0) {
+              out.col.push_back(dofs.free_index[c]);
+              out.val.push_back(S.val[q]);
+            }
+          } else if (dofs.constrained_index[c] >= 0) {
+            out.col.push_back(dofs.constrained_index[c]);
+            out.val.push_back(S.val[q]);
+          }
+        }
+        out.row_ptr[f + 1] = static_cast<int>(out.col.size());
+      }
+    };
+    extract(A, true, csrA);
+    extract(A, false, csrAc);
+    csrB.rows = n_free;  // free rows of B, all columns
+    csrB.row_ptr.assign(n_free + 1, 0);
+    for (int f = 0; f < n_free; ++f) {
+      const int r = dofs.free_list[f];
+      for (int q = B.row_ptr[r]; q < B.row_ptr[r + 1]; ++q) {
+        csrB.col.push_back(B.col[q]);
+        csrB.val.push_back(B.val[q]);
+      }
+      csrB.row_ptr[f + 1] = static_cast<int>(csrB.col.size());
+    }
+  }
+}
+
+void Sim::setup_device(int device) {
+  const int rc = tg_ctx_create(device, &ctx);
+  if (rc != TG_OK) {
+    const std::string msg = ctx ? ctx->err : std::string("context creation failed");
+    if (ctx) tg_ctx_destroy(ctx);
+    ctx = nullptr;
+    throw cuda_error(msg);
+  }
+  cudaStream_t s = ctx->stream;
+  ctx->mat = cfg.material;
+  ctx->n_src = static_cast<int>(sources.size());
+  double* d = ctx->src6.ensure(6 * sources.size());
+  if (!sources.empty())
+    TG_CUDA(cudaMemcpyAsync(d, sources.data(), sources.size() * sizeof(PointSource),
+                            cudaMemcpyHostToDevice, s));
+  upload(d_qx, h_qx, s);
+  upload(d_qn, h_qn, s);
+  upload(d_qw, h_qw, s);
+  upload(d_Nb, h_Nb, s);
+  upload(d_Nf, h_Nf, s);
+  upload(d_inc_ptr, h_inc_ptr, s);
+  upload(d_inc_src, h_inc_src, s);
+  upload(d_grev, grev, s);
+  upload(d_qb_off, h_qb_off, s);
+  upload(d_qf_off, h_qf_off, s);
+  const size_t max_pts = static_cast<size_t>(std::max(h_qb_off.back(), h_qf_off.back())) + 1;
+  d_pt_index.ensure(max_pts);
+  d_elem_off.ensure(n_fe + 1);
+  d_fine.ensure(2 * static_cast<size_t>(n_fe) + 2);
+  d_gq.ensure(max_pts);
+  d_loc.ensure(static_cast<size_t>(n_fe) * ndk + 1);
+  TG_CUDA(cudaMallocHost(&h_fine, sizeof(int) * (2 * static_cast<size_t>(n_fe) + 2)));
+  TG_CUDA(cudaMallocHost(&h_status, sizeof(PcgStatus)));
+
+  d_x.ensure(n_free);
+  d_r.ensure(n_free);
+  d_p.ensure(n_free);
+  d_Ap.ensure(n_free);
+  d_invd.ensure(n_free);
+  d_rhs.ensure(n_free);
+  d_gn.ensure(n_con);
+  d_g1.ensure(n_con);
+  d_Fn.ensure(n_full);
+  d_F1.ensure(n_full);
+  d_T.ensure(n_full);
+  d_gfull.ensure(n_full);
+  d_status.ensure(1);
+  TG_CUDA(cudaMemsetAsync(d_gfull.p, 0, sizeof(double) * n_full, s));
+  TG_CUDA(cudaMemsetAsync(d_status.p, 0, sizeof(PcgStatus), s));
+
+  if (kron) {
+    const int p = band[0].p;
+    if (band[1].p != p || band[2].p != p || p < 1 || p > kKronMaxP) {
+      kron = false;  // mixed or high degrees: fall back to the assembled operator
+      throw std::invalid_argument("kronecker path needs equal degrees 1..3 in all directions");
+    }
+    const int W = 2 * p + 1;
+    std::vector<double> all;
+    for (int d = 0; d < 3; ++d) {
+      all.insert(all.end(), band[d].M.begin(), band[d].M.end());
+      all.insert(all.end(), band[d].K.begin(), band[d].K.end());
+    }
+    upload(d_band, all, s);
+    size_t off = 0;
+    for (int d = 0; d < 3; ++d) {
+      const double* M = d_band.p + off;
+      off += band[d].M.size();
+      const double* K = d_band.p + off;
+      off += band[d].K.size();
+      gfull.M[d] = M;
+      gfull.K[d] = K;
+      gfull.n[d] = band[d].n;
+      gfree.M[d] = M;
+      gfree.K[d] = K;
+      gfree.n[d] = band[d].n;
+    }
+    gfull.p = gfree.p = p;
+    gfree.n[geom.ax] -= 1;
+    if (geom.layer == 0) {  // drop row/col 0 of the constrained direction
+      gfree.M[geom.ax] += W;
+      gfree.K[geom.ax] += W;
+    }
+    k2_inverse_diagonal(gfree, coefA[0], coefA[1], d_invd.p, d_status.p, s);
+    pcg_blocks = k2_pcg_max_blocks(p, ctx->sm_count);
+  } else {
+    auto up = [&](const Csr& C, DevBuf<int>& rp, DevBuf<int>& ci, DevBuf<double>& v, DevCsr& out) {
+      upload(rp, C.row_ptr, s);
+      upload(ci, C.col, s);
+      upload(v, C.val, s);
+      out = DevCsr{C.rows, rp.p, ci.p, v.p};
+    };
+    up(csrA, dA_rp, dA_ci, dA_v, devA);
+    up(csrAc, dAc_rp, dAc_ci, dAc_v, devAc);
+    up(csrB, dB_rp, dB_ci, dB_v, devB);
+    upload(d_free_list, dofs.free_list, s);
+    csr_inverse_diagonal(devA, d_invd.p, d_status.p, s);
+    pcg_blocks = csr_pcg_max_blocks(ctx->sm_count);
+  }
+  d_partials.ensure(8 * static_cast<size_t>(pcg_blocks) + 8);
+  TG_CUDA(cudaMemcpyAsync(h_status, d_status.p, sizeof(PcgStatus), cudaMemcpyDeviceToHost, s));
+  TG_CUDA(cudaStreamSynchronize(s));
+  diag_ok = h_status->status != 2;
+}
+
+// ---------------------------------------------------------------------------
+// hot path pieces
+
+bool Sim::focus_at(double t, Vec3& focus) const {
+  // the newest source with t_activate <= t, scanning in order and stopping at
+  // the first later one (assembly.cpp:153-157): first j with max(t_act[0..j]) > t
+  const size_t k = std::upper_bound(tact_max.begin(), tact_max.end(), t) - tact_max.begin();
+  if (k == 0) return false;
+  focus = sources[k - 1].position;
+  return true;
+}
+
+int Sim::fine_elements(double t, double radius) {
+  Vec3 f;
+  int nf = 0;
+  if (!focus_at(t, f)) return 0;
+  for (int e = 0; e < n_fe; ++e) {
+    const Vec3 c{centers[3 * e], centers[3 * e + 1], centers[3 * e + 2]};
+    if ((c - f).norm() < radius) h_fine[nf++] = e;
+  }
+  return nf;
+}
+
+void Sim::flux_load_device(double t, double radius, double* d_F) {
+  cudaStream_t s = ctx->stream;
+  // the pinned fine list is reused every step: order the last copy first
+  TG_CUDA(cudaStreamSynchronize(s));
+  const int nf = fine_elements(t, radius);
+  // extra[r]: added points of the first r fine elements (fine minus base rule)
+  int* extra = h_fine + n_fe + 1;
+  extra[0] = 0;
+  for (int r = 0; r < nf; ++r) {
+    const int e = h_fine[r];
+    extra[r + 1] = extra[r] + (h_qf_off[e + 1] - h_qf_off[e]) - (h_qb_off[e + 1] - h_qb_off[e]);
+  }
+  if (nf > 0) TG_CUDA(cudaMemcpyAsync(d_fine.p, h_fine, sizeof(int) * nf, cudaMemcpyHostToDevice, s));
+  TG_CUDA(cudaMemcpyAsync(d_fine.p + n_fe + 1, extra, sizeof(int) * (nf + 1),
+                          cudaMemcpyHostToDevice, s));
+  const long n_pts = static_cast<long>(h_qb_off.back()) + extra[nf];
+  const FaceTables ft{n_fe, ndk, d_qb_off.p, d_qf_off.p, d_Nb.p, d_Nf.p};
+  k3_point_index(ft, d_fine.p, d_fine.p + n_fe + 1, nf, d_pt_index.p, d_elem_off.p, s);
+  ++ctx->timer.launches;
+  K1Flux fl{d_pt_index.p, d_qn.p, d_qw.p, cfg.material.conductivity};
+  k1_run(ctx, ctx->src6.p, ctx->n_src, d_qx.p, d_pt_index.p, n_pts, t,
+         cfg.superpose.cull_exponent, K1Mode::flux, d_gq.p, nullptr, fl, s);
+  k3_local(ft, d_elem_off.p, d_gq.p, d_loc.p, s);
+  k3_gather(n_full, d_inc_ptr.p, d_inc_src.p, d_loc.p, d_F, s);
+  ctx->timer.launches += 2;
+  TG_CUDA(cudaGetLastError());
+}
+
+void Sim::dirichlet_device(double t, double* d_g) {
+  k1_run(ctx, ctx->src6.p, ctx->n_src, d_grev.p, nullptr, n_con, t, cfg.superpose.cull_exponent,
+         K1Mode::dirichlet, d_g, nullptr, {}, ctx->stream);
+}
+
+PcgStatus Sim::theta_step_device(double tol, int max_iter) {
+  cudaStream_t s = ctx->stream;
+  if (!diag_ok) throw numeric_error("pcg: non-positive diagonal, matrix not SPD");
+  const int threads = 256;
+  expand_kernel<<<static_cast<int>((n_full + threads - 1) / threads), threads, 0, s>>>(
+      geom, d_x.p, d_gn.p, d_T.p);
+  ++ctx->timer.launches;
+  PcgWork w{d_r.p, d_p.p, d_Ap.p, d_invd.p, d_partials.p, d_status.p};
+  const double th = cfg.stepping.theta;
+  if (kron) {
+    scatter_layer_kernel<<<(n_con + threads - 1) / threads, threads, 0, s>>>(geom, d_g1.p,
+                                                                             d_gfull.p);
+    RhsArgs ra{d_T.p, d_gfull.p, d_Fn.p, d_F1.p, th, geom.ax, geom.layer, d_rhs.p};
+    k2_theta_rhs(gfull, coefB[0], coefB[1], -coefA[0], -coefA[1], ra, ctx->sm_count, s);
+    ctx->timer.launches += 2;
+    ctx->timer.timed(2, s, [&] {
+      k2_pcg_solve(gfree, coefA[0], coefA[1], d_rhs.p, d_x.p, w, tol, max_iter, pcg_blocks, s);
+    });
+  } else {
+    csr_theta_rhs(devB, devAc, d_T.p, d_g1.p, d_Fn.p, d_F1.p, d_free_list.p, th, d_rhs.p, s);
+    ++ctx->timer.launches;
+    ctx->timer.timed(2, s, [&] {
+      csr_pcg_solve(devA, d_rhs.p, d_x.p, w, tol, max_iter, pcg_blocks, s);
+    });
+  }
+  ++ctx->timer.launches;
+  ++ctx->timer.k2_launches;
+  TG_CUDA(cudaMemcpyAsync(h_status, d_status.p, sizeof(PcgStatus), cudaMemcpyDeviceToHost, s));
+  TG_CUDA(cudaStreamSynchronize(s));
+  const PcgStatus st = *h_status;
+  ctx->timer.k2_bytes += 104.0 * n_free * st.iterations;  // SURVEY.md §8d algorithmic bytes
+  k2_iterations += st.iterations;
+  if (st.status == 4) throw numeric_error("pcg: indefinite direction, matrix not SPD");
+  if (st.status == 3) {
+    char buf[64];
+    std::snprintf(buf, sizeof(buf), "%.17g", st.rel_residual);
+    throw numeric_error("pcg: no convergence in " + std::to_string(max_iter) +
+                        " iterations, relative residual " + buf);
+  }
+  return st;
+}
+
+void Sim::reset() {
+  cudaStream_t s = ctx->stream;
+  TG_CUDA(cudaMemsetAsync(d_x.p, 0, sizeof(double) * n_free, s));
+  dirichlet_device(0.0, d_gn.p);
+  flux_load_device(0.0, cfg.mesh.elevate_radius, d_Fn.p);
+  step = 0;
+  TG_CUDA(cudaStreamSynchronize(s));
+}
+
+PcgStatus Sim::advance() {
+  const int s1 = step + 1;
+  const double t1 = s1 * dt_solver;  // driver.cpp:127
+  flux_load_device(t1, cfg.mesh.elevate_radius, d_F1.p);
+  dirichlet_device(t1, d_g1.p);
+  const PcgStatus st = theta_step_device(cfg.stepping.solver_tol, cfg.stepping.max_iter);
+  std::swap(d_Fn.p, d_F1.p);
+  std::swap(d_gn.p, d_g1.p);
+  step = s1;
+  return st;
+}
+
+}  // namespace tgb

@@ -1,0 +1,98 @@
+// Simulation engine (see sim.cu).
+#pragma once
+
+#include <array>
+#include <string>
+#include <vector>
+
+#include "context.hpp"
+#include "host/config.hpp"
+#include "host/operator.hpp"
+#include "k2_csr.cuh"
+#include "k2_kron.cuh"
+
+namespace tgb {
+
+// Control-grid geometry of the DOF split: grid dims, the constrained axis and
+// layer, and the two in-face axes that order the constrained values.
+struct SimGeom {
+  int n[3];
+  int ax, layer, t0, t1;
+};
+
+struct SimOptions {
+  double t_end = 0.0;       // > 0 overrides the config
+  double solver_tol = 0.0;  // > 0 overrides the config
+  int max_iter = 0;         // > 0 overrides the config
+  int device = 0;
+  bool host_only = false;
+};
+
+class Sim {
+ public:
+  Sim(const std::string& config_path, const SimOptions& opt);
+  ~Sim();
+  Sim(const Sim&) = delete;
+  Sim& operator=(const Sim&) = delete;
+
+  // run_time_loop pieces (driver.cpp:105-146)
+  void reset();          // state 0: free = 0, g_0, F_0
+  PcgStatus advance();   // one step: F_{n+1}, g_{n+1}, theta step
+
+  // drop-in pieces on device buffers
+  void flux_load_device(double t, double radius, double* d_F);
+  void dirichlet_device(double t, double* d_g);
+  PcgStatus theta_step_device(double tol, int max_iter);  // uses d_x, d_gn, d_g1, d_Fn, d_F1
+
+  bool focus_at(double t, Vec3& focus) const;
+  int fine_elements(double t, double radius);  // fills h_fine, returns the count
+
+  // ---- host setup
+  RunConfig cfg;
+  NurbsVolume vol;
+  DofMap dofs;
+  std::array<int, 3> quad{0, 0, 0};
+  std::vector<PointSource> sources;
+  std::vector<double> tact_max;
+  double dt_solver = 0.0;
+  int n_steps = 0;
+  SimGeom geom{};
+  int n_full = 0, n_free = 0, n_con = 0;
+  int n_fe = 0, nqb = 0, nqf = 0, ndk = 0;
+  std::vector<double> centers, h_qx, h_qn, h_qw, h_Nb, h_Nf, grev;
+  std::vector<int> h_dofk, h_inc_ptr, h_inc_src, h_qb_off, h_qf_off;
+  bool kron = false;
+  std::array<Band1D, 3> band;
+  std::array<double, 2> coefA{0, 0}, coefB{0, 0};
+  Csr csrA, csrAc, csrB;
+
+  // ---- device
+  tg_ctx* ctx = nullptr;
+  DevBuf<double> d_qx, d_qn, d_qw, d_Nb, d_Nf, d_gq, d_loc, d_grev, d_band;
+  DevBuf<int> d_inc_ptr, d_inc_src, d_pt_index, d_elem_off, d_fine, d_free_list, d_qb_off,
+      d_qf_off;
+  DevBuf<int> dA_rp, dA_ci, dAc_rp, dAc_ci, dB_rp, dB_ci;
+  DevBuf<double> dA_v, dAc_v, dB_v;
+  DevCsr devA{}, devAc{}, devB{};
+  KronGrid gfull{}, gfree{};
+  DevBuf<double> d_x, d_r, d_p, d_Ap, d_invd, d_rhs, d_gn, d_g1, d_Fn, d_F1, d_T, d_gfull,
+      d_partials;
+  DevBuf<PcgStatus> d_status;
+  PcgStatus* h_status = nullptr;
+  int* h_fine = nullptr;
+  int pcg_blocks = 1;
+  bool diag_ok = true;
+  int step = 0;
+  long k2_iterations = 0;
+
+ private:
+  void setup_host();
+  void setup_device(int device);
+};
+
+}  // namespace tgb
+
+struct tg_sim {
+  tgb::Sim* sim = nullptr;
+  std::string err;
+};

@@ -1,0 +1,232 @@
+// C ABI of the simulation engine: tg_sim_* (include/thermiga_b200.h).
+#include <cstring>
+
+#include "sim.hpp"
+
+using namespace tgb;
+
+namespace {
+
+template <typename F>
+int sim_guard(tg_sim* s, F&& body, bool needs_device = true) {
+  try {
+    if (!s || !s->sim) throw std::invalid_argument("null simulation handle");
+    if (needs_device) {
+      if (!s->sim->ctx) throw cuda_error("cuda: host-only simulation has no device context");
+      TG_CUDA(cudaSetDevice(s->sim->ctx->device));
+    }
+    body(*s->sim);
+    return TG_OK;
+  } catch (const config_error& e) {
+    if (s) s->err = e.what();
+    return TG_ECONFIG;
+  } catch (const io_error& e) {
+    if (s) s->err = e.what();
+    return TG_EIO;
+  } catch (const numeric_error& e) {
+    if (s) s->err = e.what();
+    return TG_ENUMERIC;
+  } catch (const cuda_error& e) {
+    if (s) s->err = e.what();
+    return TG_ECUDA;
+  } catch (const std::exception& e) {
+    if (s) s->err = e.what();
+    return TG_ERROR;
+  }
+}
+
+void d2h(double* h, const double* d, size_t n, cudaStream_t s) {
+  if (h && n) TG_CUDA(cudaMemcpyAsync(h, d, n * sizeof(double), cudaMemcpyDeviceToHost, s));
+}
+void h2d(double* d, const double* h, size_t n, cudaStream_t s) {
+  if (n) TG_CUDA(cudaMemcpyAsync(d, h, n * sizeof(double), cudaMemcpyHostToDevice, s));
+}
+
+}  // namespace
+
+extern "C" {
+
+int tg_sim_create(const char* config_path, const tg_sim_options* opt, tg_sim** out) {
+  if (!out) return TG_ERROR;
+  auto* h = new tg_sim();
+  *out = h;
+  try {
+    SimOptions o;
+    if (opt) {
+      o.t_end = opt->t_end;
+      o.solver_tol = opt->solver_tol;
+      o.max_iter = opt->max_iter;
+      o.device = opt->device;
+      o.host_only = opt->host_only != 0;
+    }
+    h->sim = new Sim(config_path ? config_path : "", o);
+    return TG_OK;
+  } catch (const config_error& e) {
+    h->err = e.what();
+    return TG_ECONFIG;
+  } catch (const io_error& e) {
+    h->err = e.what();
+    return TG_EIO;
+  } catch (const numeric_error& e) {
+    h->err = e.what();
+    return TG_ENUMERIC;
+  } catch (const cuda_error& e) {
+    h->err = e.what();
+    return TG_ECUDA;
+  } catch (const std::exception& e) {
+    h->err = e.what();
+    return TG_ERROR;
+  }
+}
+
+void tg_sim_destroy(tg_sim* s) {
+  if (!s) return;
+  delete s->sim;
+  delete s;
+}
+
+const char* tg_sim_last_error(const tg_sim* s) { return s ? s->err.c_str() : "null simulation"; }
+
+int tg_sim_kron_factors(tg_sim* s, int dir, double* M, double* K) {
+  return sim_guard(s, [&](Sim& m) {
+    if (!m.kron) throw std::invalid_argument("patch is not separable: no Kronecker factors");
+    if (dir < 0 || dir > 2) throw std::invalid_argument("dir must be 0, 1 or 2");
+    std::memcpy(M, m.band[dir].M.data(), m.band[dir].M.size() * sizeof(double));
+    std::memcpy(K, m.band[dir].K.data(), m.band[dir].K.size() * sizeof(double));
+  }, false);
+}
+
+int tg_sim_context(tg_sim* s, tg_ctx** out) {
+  return sim_guard(s, [&](Sim& m) { *out = m.ctx; });
+}
+
+int tg_sim_info(tg_sim* s, long* out) {
+  return sim_guard(s, [&](Sim& m) {
+    const auto n = m.vol.basis_counts();
+    const auto p = m.vol.degrees();
+    const long v[] = {m.n_full, m.n_free, m.n_con, m.n_steps, static_cast<long>(m.sources.size()),
+                      m.n_fe, n[0], n[1], n[2], p[0], p[1], p[2], m.kron ? 1 : 0, m.nqb, m.nqf,
+                      m.ndk, m.h_qb_off.back(), m.h_qf_off.back()};
+    std::memcpy(out, v, sizeof(v));
+  }, false);
+}
+
+int tg_sim_params(tg_sim* s, double* out) {
+  return sim_guard(s, [&](Sim& m) {
+    const double v[] = {m.dt_solver, m.cfg.stepping.theta, m.cfg.stepping.solver_tol,
+                        m.cfg.mesh.elevate_radius, m.cfg.superpose.cull_exponent,
+                        m.cfg.material.conductivity, m.cfg.material.density,
+                        m.cfg.material.heat_capacity, m.cfg.material.platform_temperature,
+                        static_cast<double>(m.cfg.stepping.max_iter)};
+    std::memcpy(out, v, sizeof(v));
+  }, false);
+}
+
+int tg_sim_sources(tg_sim* s, tg_point_source* out, int max_out) {
+  return sim_guard(s, [&](Sim& m) {
+    const int n = std::min<int>(max_out, static_cast<int>(m.sources.size()));
+    if (n > 0) std::memcpy(out, m.sources.data(), n * sizeof(tg_point_source));
+  }, false);
+}
+
+int tg_sim_face_sets(tg_sim* s, int* qb_off, int* qf_off, double* centers, int* dofs,
+                     double* xq, double* nq, double* wq, double* Nb, double* Nf) {
+  return sim_guard(s, [&](Sim& m) {
+    auto cp = [](auto* dst, const auto& v) {
+      if (dst) std::memcpy(dst, v.data(), v.size() * sizeof(v[0]));
+    };
+    cp(qb_off, m.h_qb_off);
+    cp(qf_off, m.h_qf_off);
+    cp(centers, m.centers);
+    cp(dofs, m.h_dofk);
+    cp(xq, m.h_qx);
+    cp(nq, m.h_qn);
+    cp(wq, m.h_qw);
+    cp(Nb, m.h_Nb);
+    cp(Nf, m.h_Nf);
+  }, false);
+}
+
+int tg_sim_greville_points(tg_sim* s, double* out) {
+  return sim_guard(s, [&](Sim& m) { std::memcpy(out, m.grev.data(), m.grev.size() * sizeof(double)); }, false);
+}
+
+int tg_sim_flux_load(tg_sim* s, double t, double fine_radius, double* out_F) {
+  return sim_guard(s, [&](Sim& m) {
+    const double r = fine_radius < 0.0 ? m.cfg.mesh.elevate_radius : fine_radius;
+    m.flux_load_device(t, r, m.d_T.p);
+    d2h(out_F, m.d_T.p, m.n_full, m.ctx->stream);
+    TG_CUDA(cudaStreamSynchronize(m.ctx->stream));
+  });
+}
+
+int tg_sim_dirichlet_values(tg_sim* s, double t, double* out_g) {
+  return sim_guard(s, [&](Sim& m) {
+    m.dirichlet_device(t, m.d_rhs.p);
+    d2h(out_g, m.d_rhs.p, m.n_con, m.ctx->stream);
+    TG_CUDA(cudaStreamSynchronize(m.ctx->stream));
+  });
+}
+
+int tg_sim_theta_step(tg_sim* s, const double* free_n, const double* g_n, const double* F_n,
+                      const double* F_np1, const double* g_np1, double tol, int max_iter,
+                      double* free_out, int* iters, double* rel) {
+  return sim_guard(s, [&](Sim& m) {
+    cudaStream_t st = m.ctx->stream;
+    h2d(m.d_x.p, free_n, m.n_free, st);
+    h2d(m.d_gn.p, g_n, m.n_con, st);
+    h2d(m.d_Fn.p, F_n, m.n_full, st);
+    h2d(m.d_F1.p, F_np1, m.n_full, st);
+    h2d(m.d_g1.p, g_np1, m.n_con, st);
+    const PcgStatus r = m.theta_step_device(tol, max_iter);
+    d2h(free_out, m.d_x.p, m.n_free, st);
+    TG_CUDA(cudaStreamSynchronize(st));
+    if (iters) *iters = r.iterations;
+    if (rel) *rel = r.rel_residual;
+  });
+}
+
+int tg_sim_reset(tg_sim* s) {
+  return sim_guard(s, [&](Sim& m) { m.reset(); });
+}
+
+int tg_sim_advance(tg_sim* s, int n_steps, long* cg_iterations, double* last_rel) {
+  return sim_guard(s, [&](Sim& m) {
+    long it = 0;
+    PcgStatus st{};
+    for (int k = 0; k < n_steps; ++k) {
+      st = m.advance();
+      it += st.iterations;
+    }
+    if (cg_iterations) *cg_iterations = it;
+    if (last_rel) *last_rel = st.rel_residual;
+  });
+}
+
+int tg_sim_state(tg_sim* s, int* step, double* time, double* free_out, double* g_out,
+                 double* F_out) {
+  return sim_guard(s, [&](Sim& m) {
+    cudaStream_t st = m.ctx->stream;
+    d2h(free_out, m.d_x.p, m.n_free, st);
+    d2h(g_out, m.d_gn.p, m.n_con, st);
+    d2h(F_out, m.d_Fn.p, m.n_full, st);
+    TG_CUDA(cudaStreamSynchronize(st));
+    if (step) *step = m.step;
+    if (time) *time = m.step * m.dt_solver;
+  });
+}
+
+int tg_sim_operator_apply(tg_sim* s, const double* x_free, double* y_free) {
+  return sim_guard(s, [&](Sim& m) {
+    cudaStream_t st = m.ctx->stream;
+    h2d(m.d_r.p, x_free, m.n_free, st);
+    if (m.kron)
+      k2_apply(m.gfree, m.coefA[0], m.coefA[1], m.d_r.p, m.d_Ap.p, m.ctx->sm_count, st);
+    else
+      csr_apply(m.devA, m.d_r.p, m.d_Ap.p, st);
+    d2h(y_free, m.d_Ap.p, m.n_free, st);
+    TG_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+}  // extern "C"

@@ -50,3 +50,41 @@ if __name__ == "__main__":
     R = pyoracle.RefLib()
     if "k1" in what:
         k1(R)
+
+
+SIM_STEPS = {"cfg0_parity": [1, 2, 3, 5, 10, 25, 50, 75, 100], "qc_small": [1, 2, 5, 12, 24]}
+
+
+def sim_run(R, name):
+    """Per-step F, g, free coefficients and CG iterations of run_time_loop."""
+    path = os.path.join(ROOT, "configs", name + ".cfg")
+    sim = R.sim(path)
+    F0, g0 = sim.reset()
+    keep = SIM_STEPS[name]
+    out = {"F0": F0, "g0": g0, "steps": np.array(keep)}
+    iters = []
+    for s in range(1, max(keep) + 1):
+        r = sim.step()
+        iters.append(r["iters"])
+        if s in keep:
+            out[f"F{s}"], out[f"g{s}"], out[f"x{s}"] = r["F"], r["g"], r["free"]
+    out["iters"] = np.array(iters)
+    # one flux load and Dirichlet vector at a mid time, and the operator on a probe vector
+    t = 0.37 * max(keep) * sim.params["dt"]
+    out["t_mid"] = t
+    out["F_mid"] = sim.flux_load(t)
+    out["g_mid"] = sim.dirichlet(t)
+    rp, ci, v = sim.csr(2)
+    x = np.random.default_rng(5).standard_normal(sim.info["n_free"])
+    out["Ax_probe"] = x
+    out["Ax"] = np.array([np.dot(v[rp[i]:rp[i + 1]], x[ci[rp[i]:rp[i + 1]]])
+                          for i in range(len(rp) - 1)])
+    np.savez_compressed(os.path.join(HERE, f"sim_{name}.npz"), **out)
+    print(f"sim_{name}.npz", sum(iters), "CG iterations")
+    sim.close()
+
+
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "sim":
+    R = pyoracle.RefLib()
+    for name in SIM_STEPS:
+        sim_run(R, name)

@@ -1,0 +1,155 @@
+"""K1 + K3 + K2 parity on the GPU through the C ABI (tg_sim_*), against the
+unmodified reference (live when oracle/_ref is present, else the committed
+golden vectors of tests/golden/make_golden.py).
+
+Tolerances (BASELINE.json north_star):
+  * loads F and Dirichlet values g: normwise max|a-b|/max|b| <= 1e-10, and
+    reference zeros reproduced exactly;
+  * correction-field coefficients: normwise <= 1e-8 at every compared step,
+    both sides run with solver_tol = 1e-12 (configs/*_parity.cfg, qc_small.cfg).
+"""
+import os
+
+import numpy as np
+import pytest
+
+import paper_2511_20432_b200 as tg
+from conftest import GOLDEN, ROOT
+
+pytestmark = pytest.mark.gpu
+NAMES = ["cfg0_parity", "qc_small"]
+
+
+def cfg(name):
+    return os.path.join(ROOT, "configs", name + ".cfg")
+
+
+def golden(name):
+    return np.load(os.path.join(GOLDEN, f"sim_{name}.npz"))
+
+
+def normwise(a, b):
+    m = np.abs(b).max()
+    return 0.0 if m == 0 else np.abs(a - b).max() / m
+
+
+@pytest.fixture(scope="module", params=NAMES)
+def sim(request):
+    s = tg.Simulation(cfg(request.param))
+    yield request.param, s
+    s.close()
+
+
+def test_operator_matches_assembled_reference(sim):
+    name, s = sim
+    g = golden(name)
+    y = s.operator_apply(g["Ax_probe"])
+    assert normwise(y, g["Ax"]) <= 1e-13
+
+
+def test_flux_load_and_dirichlet(sim):
+    name, s = sim
+    g = golden(name)
+    F = s.flux_load(float(g["t_mid"]))
+    assert normwise(F, g["F_mid"]) <= 1e-10
+    assert np.array_equal(F == 0.0, g["F_mid"] == 0.0)
+    d = s.dirichlet_values(float(g["t_mid"]))
+    assert normwise(d, g["g_mid"]) <= 1e-10
+    F0 = s.flux_load(0.0)
+    assert np.array_equal(F0, g["F0"])  # causal zero before activation
+
+
+def test_flux_load_live_reference_times(sim, ref):
+    """Several instants incl. ones where the fine rule engages (t = 1e-4, 2e-4)."""
+    name, s = sim
+    r = ref.sim(cfg(name))
+    for t in (1e-5, 5e-5, 1e-4, 2e-4, 2.4e-4):
+        F = s.flux_load(t)
+        Fr = r.flux_load(t)
+        assert normwise(F, Fr) <= 1e-10, t
+        assert np.array_equal(F == 0.0, Fr == 0.0), t
+        d, dr = s.dirichlet_values(t), r.dirichlet(t)
+        assert normwise(d, dr) <= 1e-10, t
+    # fine rule disabled / always on
+    for rad in (0.0, 1.0):
+        assert normwise(s.flux_load(1e-4, rad), r.flux_load_radius(1e-4, rad)) <= 1e-10
+    r.close()
+
+
+def test_theta_step_from_reference_inputs(sim):
+    name, s = sim
+    g = golden(name)
+    steps = list(g["steps"])
+    for a, b in zip(steps[:-1], steps[1:]):
+        if b != a + 1:
+            continue
+        x, it, rel = s.theta_step(g[f"x{a}"], g[f"g{a}"], g[f"F{a}"], g[f"F{b}"], g[f"g{b}"],
+                                  tol=1e-12)
+        assert rel <= 1e-12
+        assert normwise(x, g[f"x{b}"]) <= 1e-8, (a, b)
+        assert abs(it - g["iters"][b - 1]) <= max(3, 0.1 * g["iters"][b - 1])
+
+
+def test_full_time_loop(sim):
+    """run_time_loop on the device: every compared step within tolerance."""
+    name, s = sim
+    g = golden(name)
+    s.reset()
+    st = s.state()
+    assert st["step"] == 0 and not np.any(st["free"])
+    assert np.array_equal(st["F"], g["F0"]) and normwise(st["g"], g["g0"]) <= 1e-10
+    done = 0
+    total_it = 0
+    worst = 0.0
+    for k in g["steps"]:
+        it, rel = s.advance(int(k) - done)
+        total_it += it
+        done = int(k)
+        st = s.state()
+        assert st["step"] == k
+        assert normwise(st["F"], g[f"F{k}"]) <= 1e-10, k
+        assert normwise(st["g"], g[f"g{k}"]) <= 1e-10, k
+        err = normwise(st["free"], g[f"x{k}"])
+        worst = max(worst, err)
+        assert err <= 1e-8, (k, err)
+    ref_it = int(g["iters"][:done].sum())
+    assert abs(total_it - ref_it) <= 0.05 * ref_it, (total_it, ref_it)
+
+
+def test_deterministic_reruns(sim):
+    name, s = sim
+    s.reset()
+    s.advance(5)
+    a = s.state()
+    s.reset()
+    s.advance(5)
+    b = s.state()
+    for k in ("free", "g", "F"):
+        assert np.array_equal(a[k], b[k])
+
+
+def test_pcg_error_paths(sim):
+    name, s = sim
+    g = golden(name)
+    # iteration cap -> numeric error with the reference's message (sparse.cpp:98-99)
+    with pytest.raises(tg.NumericError, match=r"pcg: no convergence in 1 iterations, "
+                                              r"relative residual"):
+        s.theta_step(g["x1"], g["g1"], g["F1"], g["F2"], g["g2"], tol=1e-14, max_iter=1)
+    # zero right-hand side resets a warm start (sparse.cpp:57-60)
+    nf, nc, n = s.info["n_free"], s.info["n_constrained"], s.info["n_full"]
+    x, it, rel = s.theta_step(np.ones(nf) * 0.0, np.zeros(nc), np.zeros(n), np.zeros(n),
+                              np.zeros(nc))
+    assert it == 0 and not np.any(x)
+
+
+def test_zero_power_gives_platform_temperature(tmp_path):
+    # proj/tests/test_pipeline.cpp:66-78: P = 0 -> exactly T_c everywhere
+    txt = open(cfg("cfg0_parity")).read().replace("power = 150.0", "power = 0.0")
+    p = tmp_path / "zero.cfg"
+    p.write_text(txt)
+    s = tg.Simulation(str(p), t_end=1e-4)
+    s.reset()
+    s.advance(s.info["n_steps"])
+    st = s.state()
+    assert not np.any(st["free"]) and not np.any(st["g"]) and not np.any(st["F"])
+    s.close()
