@@ -60,6 +60,8 @@ def parse():
                     help="target CPU work for the bounded cpu_baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ncu", action="store_true", help="profiling run: no clocks/cpu legs")
+    ap.add_argument("--theta-steps", type=int, default=3,
+                    help="config-4 time steps for the theta-step section (0 = skip)")
     return ap.parse_args()
 
 
@@ -158,6 +160,86 @@ def cpu_baseline(src, t, budget_s, threads=None):
     return {"value": pairs / secs, "unit": "pairs/s", "cores": cores, "kind": kind,
             "sample": f"{len(pts)} of the 2^20 config-1 points (every {stride}th) x {len(src)} "
                       f"sources, value+grad at t_end, {secs:.2f} s"}
+
+
+THETA_CFG = os.path.join(ROOT, "configs", "cfg4_large.cfg")
+THETA_CPU_CFG = os.path.join(ROOT, "configs", "cfg2_raster_layer.cfg")
+HBM_PEAK_FALLBACK = 6555.2
+
+
+def hbm_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (measured)"
+    except Exception:
+        return HBM_PEAK_FALLBACK, "fallback 6555.2 GB/s (BASELINE.md copy measurement)"
+
+
+def theta_cpu_baseline():
+    """One reference theta_step on config 2 (78,408 DOF; serial PCG as shipped)."""
+    from oracle import pyoracle
+    if not pyoracle.ref_available():
+        return None
+    R = pyoracle.RefLib()
+    sim = R.sim(THETA_CPU_CFG)
+    n_free, n_con, n_full = (sim.info[k] for k in ("n_free", "n_constrained", "n_full"))
+    t = 0.02
+    F0, F1 = sim.flux_load(t - sim.params["dt"], threads=os.cpu_count()), sim.flux_load(t)
+    g0, g1 = sim.dirichlet(t - sim.params["dt"]), sim.dirichlet(t)
+    x0 = np.zeros(n_free)
+    t0 = time.perf_counter()
+    _, iters, _ = sim.theta_step(x0, g0, F0, F1, g1, sim.params["solver_tol"])
+    secs = time.perf_counter() - t0
+    sim.close()
+    dofs = n_free + n_con
+    return {"ms_per_step_per_mdof": secs * 1e3 / (dofs / 1e6), "cg_iterations": iters,
+            "cores": 1, "kind": "reference",
+            "sample": f"one theta_step of config 2 ({dofs} DOF) at t = 0.02 s, cold start"}
+
+
+def theta_section(steps, warmup, with_cpu):
+    """Config 4 (4.39M DOF, 1e5 sources): full run_time_loop steps on the device."""
+    import paper_2511_20432_b200 as tg
+    t0 = time.perf_counter()
+    sim = tg.Simulation(THETA_CFG)
+    setup_s = time.perf_counter() - t0
+    ctx = sim.context()
+    sim.reset()
+    if warmup:
+        sim.advance(warmup)
+    ctx.set_profiling(True)
+    ctx.profile(reset=True)
+    t0 = time.perf_counter()
+    iters, _ = sim.advance(steps)
+    wall = time.perf_counter() - t0
+    prof = ctx.profile()
+    ctx.set_profiling(False)
+    dofs = sim.info["n_full"]
+    k2_ms = prof["k2_ms"] / steps
+    peak, src = hbm_peak()
+    achieved = prof["k2_bytes"] / (prof["k2_ms"] * 1e-3) / 1e9 if prof["k2_ms"] else None
+    out = {
+        "workload": "config4: 256x256x64 degree-2 cuboid (4,393,224 DOF), 1e5 sources, "
+                    "theta = 0.5, dt = 1e-5, solver_tol 1e-10",
+        "steps": steps, "warmup": warmup, "setup_s": setup_s,
+        "ms_per_step": wall * 1e3 / steps,
+        "theta_ms_per_step": k2_ms,
+        "theta_ms_per_step_per_mdof": k2_ms / (dofs / 1e6),
+        "k1_ms_per_step": prof["k1_ms"] / steps,
+        "cg_iterations_per_step": iters / steps,
+        "roofline": {"kernel": "k2_pcg_kernel (persistent Jacobi-PCG)", "bound": "hbm",
+                     "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak if achieved else None, "traffic": None,
+                     "peak_source": src,
+                     "bytes_per_dof_per_iteration": 104},
+    }
+    if with_cpu:
+        try:
+            out["cpu_baseline"] = theta_cpu_baseline()
+        except Exception as e:
+            out["cpu_baseline"] = {"error": str(e)}
+    sim.close()
+    return out
 
 
 def run_reference(args):
@@ -313,6 +395,12 @@ def run_ours(args):
             line["cpu_baseline"] = cpu_baseline(src, t, args.cpu_seconds)
         except Exception as e:  # reported, not fatal
             line["cpu_baseline"] = {"value": None, "error": str(e)}
+    if world == 1 and args.theta_steps > 0:
+        try:
+            line["theta_step"] = theta_section(args.theta_steps, 1,
+                                               not args.no_cpu_baseline and not args.ncu)
+        except Exception as e:
+            line["theta_step"] = {"error": str(e)}
     print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist

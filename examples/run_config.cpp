@@ -1,0 +1,36 @@
+// Example host program: the reference's `thermiga simulate` hot loop through
+// the C++ shim (include/thermiga_b200.hpp). Build:
+//   g++ -std=c++17 -O2 -Iinclude examples/run_config.cpp \
+//       -Lpaper_2511_20432_b200/_lib -lthermiga_b200 -Wl,-rpath,$PWD/paper_2511_20432_b200/_lib
+#include <cstdio>
+
+#include "thermiga_b200.hpp"
+
+int main(int argc, char** argv) {
+  if (argc < 2) {
+    std::fprintf(stderr, "usage: %s config.cfg\n", argv[0]);
+    return 1;
+  }
+  try {
+    thermiga_b200::Simulation sim(argv[1]);
+    double peak = 0.0;
+    const long iters = sim.run_time_loop([&](const thermiga_b200::State& s) {
+      for (double v : s.free_coeffs) peak = v > peak ? v : peak;
+    });
+    std::printf("steps %d  cg iterations %ld  max correction coefficient %.6e\n", sim.n_steps,
+                iters, peak);
+  } catch (const thermiga_b200::config_error& e) {
+    std::fprintf(stderr, "%s\n", e.what());
+    return 2;
+  } catch (const thermiga_b200::io_error& e) {
+    std::fprintf(stderr, "%s\n", e.what());
+    return 4;
+  } catch (const thermiga_b200::numeric_error& e) {
+    std::fprintf(stderr, "%s\n", e.what());
+    return 3;
+  } catch (const std::exception& e) {
+    std::fprintf(stderr, "error: %s\n", e.what());
+    return 1;
+  }
+  return 0;
+}

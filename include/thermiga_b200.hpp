@@ -1,0 +1,221 @@
+// thermiga_b200.hpp — header-only C++ shim over the C ABI (thermiga_b200.h)
+// with the reference's hot-path signatures (proj/include/thermiga/*.hpp), so a
+// caller of the reference's run_time_loop can switch the hot path to the B200
+// kernels by swapping these calls. C ABI status codes are re-raised as the
+// reference's exception types (proj/include/thermiga/core.hpp:66-80).
+#pragma once
+
+#include <array>
+#include <functional>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "thermiga_b200.h"
+
+namespace thermiga_b200 {
+
+struct Vec3 {
+  double x = 0.0, y = 0.0, z = 0.0;
+};
+
+struct config_error : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct io_error : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct numeric_error : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct device_error : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+inline void raise(int rc, const char* msg) {
+  switch (rc) {
+    case TG_OK: return;
+    case TG_ECONFIG: throw config_error(msg);
+    case TG_EIO: throw io_error(msg);
+    case TG_ENUMERIC: throw numeric_error(msg);
+    case TG_ECUDA: throw device_error(msg);
+    default: throw std::invalid_argument(msg);
+  }
+}
+
+// analytic.hpp:10-40 (same layouts as the reference's records)
+using Material = tg_material;
+using LaserSpec = tg_laser;
+using PointSource = tg_point_source;
+struct ScanPath {
+  std::vector<std::array<double, 2>> waypoints;
+  double start_time = 0.0;
+  double plane_z = 0.0;
+};
+struct SuperposeOptions {
+  double cull_exponent = 60.0;
+};
+struct AnalyticField {
+  double value = 0.0;
+  Vec3 grad;
+};
+
+// discretize_scan (analytic.hpp:45-48)
+inline std::vector<PointSource> discretize_scan(const ScanPath& path, const LaserSpec& laser,
+                                                const Material& mat) {
+  std::vector<double> wp;
+  for (const auto& w : path.waypoints) wp.insert(wp.end(), {w[0], w[1]});
+  const int n = tg_discretize_scan(wp.data(), static_cast<int>(path.waypoints.size()),
+                                   path.start_time, path.plane_z, &laser, &mat, nullptr, 0);
+  if (n < 0) throw std::invalid_argument("discretize_scan: invalid laser, material or path");
+  std::vector<PointSource> out(n);
+  tg_discretize_scan(wp.data(), static_cast<int>(path.waypoints.size()), path.start_time,
+                     path.plane_z, &laser, &mat, out.data(), n);
+  return out;
+}
+
+// A device context: the scan history resident in HBM plus scratch.
+class Device {
+ public:
+  explicit Device(int device = 0) {
+    tg_ctx* c = nullptr;
+    const int rc = tg_ctx_create(device, &c);
+    ctx_.reset(c);
+    if (rc != TG_OK) raise(rc, tg_last_error(c));
+  }
+  tg_ctx* get() const { return ctx_.get(); }
+  void set_sources(const std::vector<PointSource>& s, const Material& m) {
+    raise(tg_set_sources(get(), s.data(), static_cast<int>(s.size()), &m), tg_last_error(get()));
+  }
+  // superpose (analytic.hpp:73-75) at many points: values and gradients
+  void superpose(const std::vector<Vec3>& x, double t, std::vector<AnalyticField>& out,
+                 const SuperposeOptions& opts = {}) {
+    std::vector<double> v(x.size()), g(3 * x.size());
+    raise(tg_superpose_batch(get(), &x[0].x, static_cast<long>(x.size()), t, opts.cull_exponent,
+                             v.data(), g.data()),
+          tg_last_error(get()));
+    out.resize(x.size());
+    for (size_t i = 0; i < x.size(); ++i) out[i] = {v[i], {g[3 * i], g[3 * i + 1], g[3 * i + 2]}};
+  }
+
+ private:
+  struct Del {
+    void operator()(tg_ctx* c) const { tg_ctx_destroy(c); }
+  };
+  std::unique_ptr<tg_ctx, Del> ctx_;
+};
+
+// superpose for one point (analytic.hpp:73-75); uploads the history each call,
+// use Device::superpose for batches.
+inline AnalyticField superpose(const std::vector<PointSource>& sources, const Material& mat,
+                               const Vec3& x, double t, const SuperposeOptions& opts = {}) {
+  thread_local Device dev;
+  dev.set_sources(sources, mat);
+  std::vector<AnalyticField> out;
+  dev.superpose({x}, t, out, opts);
+  return out[0];
+}
+
+struct PcgOptions {  // sparse.hpp:32-35
+  double tol = 1e-10;
+  int max_iter = 5000;
+};
+struct PcgResult {  // sparse.hpp:37-40
+  int iterations = 0;
+  double rel_residual = 0.0;
+};
+struct State {  // timestep.hpp:16-21
+  std::vector<double> free_coeffs;
+  std::vector<double> constrained_values;
+  int step = 0;
+  double time = 0.0;
+};
+
+// prepare_simulation (driver.hpp:49) + the hot-path calls of run_time_loop.
+class Simulation {
+ public:
+  explicit Simulation(const std::string& config_path, tg_sim_options opt = {}) {
+    tg_sim* s = nullptr;
+    const int rc = tg_sim_create(config_path.c_str(), &opt, &s);
+    sim_.reset(s);
+    if (rc != TG_OK) raise(rc, tg_sim_last_error(s));
+    long info[18];
+    check(tg_sim_info(get(), info));
+    n_full = info[0];
+    n_free = info[1];
+    n_constrained = info[2];
+    n_steps = static_cast<int>(info[3]);
+    double par[10];
+    check(tg_sim_params(get(), par));
+    dt_solver = par[0];
+    tol = par[2];
+    max_iter = static_cast<int>(par[9]);
+  }
+  tg_sim* get() const { return sim_.get(); }
+
+  // assemble_flux_load (assembly.hpp:37-40); fine_radius < 0: config value
+  void assemble_flux_load(double t, double fine_radius, std::vector<double>& load) {
+    load.resize(n_full);
+    check(tg_sim_flux_load(get(), t, fine_radius, load.data()));
+  }
+  // dirichlet_values (mesh.hpp:121-125)
+  std::vector<double> dirichlet_values(double t) {
+    std::vector<double> g(n_constrained);
+    check(tg_sim_dirichlet_values(get(), t, g.data()));
+    return g;
+  }
+  // theta_step (timestep.hpp:26-29)
+  State theta_step(const State& s, const std::vector<double>& load_n,
+                   const std::vector<double>& load_np1, const std::vector<double>& g_np1,
+                   const PcgOptions& o, PcgResult* stats = nullptr) {
+    State next;
+    next.free_coeffs.resize(n_free);
+    int it = 0;
+    double rel = 0.0;
+    check(tg_sim_theta_step(get(), s.free_coeffs.data(), s.constrained_values.data(),
+                            load_n.data(), load_np1.data(), g_np1.data(), o.tol, o.max_iter,
+                            next.free_coeffs.data(), &it, &rel));
+    if (stats) *stats = {it, rel};
+    next.constrained_values = g_np1;
+    next.step = s.step + 1;
+    next.time = next.step * dt_solver;
+    return next;
+  }
+  // run_time_loop (driver.hpp:45-47) with the state resident on the device;
+  // on_state sees the state after every step (and once with the initial one).
+  long run_time_loop(const std::function<void(const State&)>& on_state) {
+    check(tg_sim_reset(get()));
+    State st;
+    pull(st);
+    on_state(st);
+    long total = 0;
+    for (int s = 1; s <= n_steps; ++s) {
+      long it = 0;
+      check(tg_sim_advance(get(), 1, &it, nullptr));
+      total += it;
+      pull(st);
+      on_state(st);
+    }
+    return total;
+  }
+
+  long n_full = 0, n_free = 0, n_constrained = 0;
+  int n_steps = 0, max_iter = 5000;
+  double dt_solver = 0.0, tol = 1e-10;
+
+ private:
+  void check(int rc) { raise(rc, tg_sim_last_error(get())); }
+  void pull(State& st) {
+    st.free_coeffs.resize(n_free);
+    st.constrained_values.resize(n_constrained);
+    check(tg_sim_state(get(), &st.step, &st.time, st.free_coeffs.data(),
+                       st.constrained_values.data(), nullptr));
+  }
+  struct Del {
+    void operator()(tg_sim* s) const { tg_sim_destroy(s); }
+  };
+  std::unique_ptr<tg_sim, Del> sim_;
+};
+
+}  // namespace thermiga_b200

@@ -38,11 +38,13 @@ namespace {
 
 constexpr int kThreads = kKronTX * kKronTY;
 
-template <int P>
+template <int P, int NIN>
 struct TileSmem {
-  double v[2][kKronTY + 2 * P][kKronTX + 2 * P];
-  double u1[2][kKronTY + 2 * P][kKronTX];
-  double u2[2][kKronTY + 2 * P][kKronTX];
+  double v[NIN][kKronTY + 2 * P][kKronTX + 2 * P];
+  double u1[NIN][kKronTY + 2 * P][kKronTX];
+  double u2[NIN][kKronTY + 2 * P][kKronTX];
+  double cx[2][kKronTX][2 * P + 1];  // Mx, Kx rows of the tile's xi range
+  double cy[2][kKronTY][2 * P + 1];  // My, Ky rows of the tile's eta range
 };
 
 struct TileIdx {
@@ -50,17 +52,31 @@ struct TileIdx {
   __device__ __host__ int count() const { return ntx * nty * nzc; }
 };
 
-__host__ __device__ inline TileIdx make_tiles(const KronGrid& g, int want) {
-  TileIdx t;
-  t.ntx = (g.n[0] + kKronTX - 1) / kKronTX;
-  t.nty = (g.n[1] + kKronTY - 1) / kKronTY;
-  const int xy = t.ntx * t.nty;
-  int nzc = (want + xy - 1) / xy;
-  const int cap = g.n[2] / 4 > 1 ? g.n[2] / 4 : 1;  // keep >= 4 planes per chunk
-  nzc = nzc < 1 ? 1 : (nzc > cap ? cap : nzc);
-  t.zlen = (g.n[2] + nzc - 1) / nzc;
-  t.nzc = (g.n[2] + t.zlen - 1) / t.zlen;
-  return t;
+// Tile layout for `blocks` co-resident CTAs. Each tile is a 32 x 8 column
+// marching through zlen planes (+ P halo planes each side). With static
+// tile -> CTA assignment (deterministic reductions), the cost is
+// ceil(tiles / blocks) * (zlen + 2P); pick the z split that minimizes it.
+inline TileIdx make_tiles(const KronGrid& g, int blocks, int P) {
+  TileIdx best{};
+  double best_cost = 1e300;
+  const int ntx = (g.n[0] + kKronTX - 1) / kKronTX;
+  const int nty = (g.n[1] + kKronTY - 1) / kKronTY;
+  const int cap = std::max(1, g.n[2] / 4);  // >= 4 planes per chunk
+  for (int nzc = 1; nzc <= std::min(cap, 16); ++nzc) {
+    TileIdx t;
+    t.ntx = ntx;
+    t.nty = nty;
+    t.zlen = (g.n[2] + nzc - 1) / nzc;
+    t.nzc = (g.n[2] + t.zlen - 1) / t.zlen;
+    const int rounds = (t.count() + blocks - 1) / blocks;
+    const double cost = static_cast<double>(rounds) * (t.zlen + 2 * P) * 1.000001 +
+                        1e-9 * t.count();  // ties: fewer tiles
+    if (cost < best_cost) {
+      best_cost = cost;
+      best = t;
+    }
+  }
+  return best;
 }
 
 // Sweep one tile: for every output point (i, j, k) of the tile call
@@ -69,7 +85,7 @@ template <int P, int NIN, class Epi>
 __device__ __forceinline__ void kron_tile(const KronGrid& g, const KronTerms& c,
                                           const double* __restrict__ v1,
                                           const double* __restrict__ v2, const TileIdx& T,
-                                          int tile, TileSmem<P>& sm, Epi& epi) {
+                                          int tile, TileSmem<P, NIN>& sm, Epi& epi) {
   constexpr int W = 2 * P + 1;
   constexpr int RY = kKronTY + 2 * P;
   constexpr int RX = kKronTX + 2 * P;
@@ -81,14 +97,19 @@ __device__ __forceinline__ void kron_tile(const KronGrid& g, const KronTerms& c,
   const int nx = g.n[0], ny = g.n[1], nz = g.n[2];
   const int i = x0 + tx, j = y0 + ty;
 
-  // per-thread 1D rows (zero beyond the grid)
-  double mx[W], kx[W], my[W], ky[W];
-#pragma unroll
-  for (int d = 0; d < W; ++d) {
-    mx[d] = i < nx ? g.M[0][i * W + d] : 0.0;
-    kx[d] = i < nx ? g.K[0][i * W + d] : 0.0;
-    my[d] = j < ny ? g.M[1][j * W + d] : 0.0;
-    ky[d] = j < ny ? g.K[1][j * W + d] : 0.0;
+  // the tile's 1D rows in shared memory (zero beyond the grid); the barrier
+  // retires the previous tile's readers, the first plane's barrier orders
+  // these writes before any read
+  __syncthreads();
+  for (int q = ty * kKronTX + tx; q < kKronTX * W; q += kKronTX * kKronTY) {
+    const int r = q / W, d = q % W, gi = x0 + r;
+    sm.cx[0][r][d] = gi < nx ? g.M[0][gi * W + d] : 0.0;
+    sm.cx[1][r][d] = gi < nx ? g.K[0][gi * W + d] : 0.0;
+  }
+  for (int q = ty * kKronTX + tx; q < kKronTY * W; q += kKronTX * kKronTY) {
+    const int r = q / W, d = q % W, gj = y0 + r;
+    sm.cy[0][r][d] = gj < ny ? g.M[1][gj * W + d] : 0.0;
+    sm.cy[1][r][d] = gj < ny ? g.K[1][gj * W + d] : 0.0;
   }
   double win1[W], win2[W];
 #pragma unroll
@@ -122,8 +143,8 @@ __device__ __forceinline__ void kron_tile(const KronGrid& g, const KronTerms& c,
 #pragma unroll
           for (int d = 0; d < W; ++d) {
             const double vv = sm.v[q][r][tx + d];
-            a1 = fma(mx[d], vv, a1);
-            a2 = fma(kx[d], vv, a2);
+            a1 = fma(sm.cx[0][tx][d], vv, a1);
+            a2 = fma(sm.cx[1][tx][d], vv, a2);
           }
           sm.u1[q][r][tx] = a1;
           sm.u2[q][r][tx] = a2;
@@ -136,9 +157,10 @@ __device__ __forceinline__ void kron_tile(const KronGrid& g, const KronTerms& c,
 #pragma unroll
         for (int d = 0; d < W; ++d) {
           const double p1 = sm.u1[q][ty + d][tx];
-          w1 = fma(my[d], p1, w1);
-          w2 = fma(my[d], sm.u2[q][ty + d][tx], w2);
-          w3 = fma(ky[d], p1, w3);
+          const double my = sm.cy[0][ty][d];
+          w1 = fma(my, p1, w1);
+          w2 = fma(my, sm.u2[q][ty + d][tx], w2);
+          w3 = fma(sm.cy[1][ty][d], p1, w3);
         }
         const double a = q == 0 ? c.a1 : c.a2, b = q == 0 ? c.b1 : c.b2;
         s1 = fma(a, w1, fma(b, w2 + w3, s1));
@@ -177,7 +199,7 @@ template <int P>
 __global__ void __launch_bounds__(kThreads) k2_apply_kernel(KronGrid g, KronTerms c,
                                                             const double* v, double* y,
                                                             TileIdx T) {
-  __shared__ TileSmem<P> sm;
+  __shared__ TileSmem<P, 1> sm;
   EpiStore<P> epi{y};
   for (int t = blockIdx.x; t < T.count(); t += gridDim.x) kron_tile<P, 1>(g, c, v, nullptr, T, t, sm, epi);
 }
@@ -199,7 +221,7 @@ struct EpiRhs {
 template <int P>
 __global__ void __launch_bounds__(kThreads) k2_rhs_kernel(KronGrid g, KronTerms c, RhsArgs args,
                                                           TileIdx T) {
-  __shared__ TileSmem<P> sm;
+  __shared__ TileSmem<P, 2> sm;
   EpiRhs<P> epi{args, {g.n[0], g.n[1], g.n[2]}};
   epi.nfree[args.bottom_axis] -= 1;
   for (int t = blockIdx.x; t < T.count(); t += gridDim.x)
@@ -305,12 +327,12 @@ struct EpiAp {
 };
 
 template <int P>
-__global__ void __launch_bounds__(kThreads) k2_pcg_kernel(KronGrid g, double a, double b,
+__global__ void __launch_bounds__(kThreads, 3) k2_pcg_kernel(KronGrid g, double a, double b,
                                                           const double* rhs, double* x,
                                                           PcgWork w, double tol, int max_iter,
                                                           TileIdx T) {
   cg::grid_group grid = cg::this_grid();
-  __shared__ TileSmem<P> sm;
+  __shared__ TileSmem<P, 1> sm;
   __shared__ double red[64];
   const KronTerms c{a, b, 0.0, 0.0};
   const size_t n = static_cast<size_t>(g.n[0]) * g.n[1] * g.n[2];
@@ -387,8 +409,8 @@ const void* pcg_kernel_ptr() {
 
 void k2_apply(const KronGrid& g, double a, double b, const double* v, double* y, int sm_count,
               cudaStream_t s) {
-  const TileIdx T = make_tiles(g, 2 * sm_count);
-  const int blocks = std::min(T.count(), 4 * sm_count);
+  const TileIdx T = make_tiles(g, 3 * sm_count, g.p);
+  const int blocks = std::min(T.count(), 3 * sm_count);
   TG_KRON_DISPATCH(g.p, k2_apply_kernel<P><<<blocks, dim3(kKronTX, kKronTY), 0, s>>>(
                                  g, KronTerms{a, b, 0.0, 0.0}, v, y, T));
   TG_CUDA(cudaGetLastError());
@@ -396,8 +418,8 @@ void k2_apply(const KronGrid& g, double a, double b, const double* v, double* y,
 
 void k2_theta_rhs(const KronGrid& full, double a_b, double b_b, double a_a, double b_a,
                   const RhsArgs& args, int sm_count, cudaStream_t s) {
-  const TileIdx T = make_tiles(full, 2 * sm_count);
-  const int blocks = std::min(T.count(), 4 * sm_count);
+  const TileIdx T = make_tiles(full, 2 * sm_count, full.p);
+  const int blocks = std::min(T.count(), 2 * sm_count);
   TG_KRON_DISPATCH(full.p, k2_rhs_kernel<P><<<blocks, dim3(kKronTX, kKronTY), 0, s>>>(
                                  full, KronTerms{a_b, b_b, a_a, b_a}, args, T));
   TG_CUDA(cudaGetLastError());
@@ -418,7 +440,7 @@ int k2_pcg_max_blocks(int p, int sm_count) {
 
 void k2_pcg_solve(const KronGrid& g, double a, double b, const double* rhs, double* x,
                   const PcgWork& w, double tol, int max_iter, int blocks, cudaStream_t s) {
-  const TileIdx T = make_tiles(g, blocks);
+  const TileIdx T = make_tiles(g, blocks, g.p);
   int nb = std::max(1, std::min(blocks, T.count()));
   dim3 grid(nb), block(kKronTX, kKronTY);
   KronGrid gg = g;

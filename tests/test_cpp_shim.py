@@ -1,0 +1,37 @@
+"""The C++ shim (include/thermiga_b200.hpp) compiles against the C ABI and a
+host program built on it runs the reference's time loop on the GPU with the
+reference CLI's exit-code mapping (proj/tools/main.cpp:84-96)."""
+import os
+import subprocess
+
+import pytest
+
+from paper_2511_20432_b200 import _build
+from conftest import ROOT
+
+
+def _compile(tmp_path):
+    exe = tmp_path / "run_config"
+    cmd = ["g++", "-std=c++17", "-O2", "-I", os.path.join(ROOT, "include"),
+           os.path.join(ROOT, "examples", "run_config.cpp"), "-L", _build.LIBDIR,
+           "-lthermiga_b200", f"-Wl,-rpath,{_build.LIBDIR}", "-o", str(exe)]
+    subprocess.run(cmd, check=True, capture_output=True)
+    return exe
+
+
+def test_shim_compiles_and_maps_config_errors(tmp_path):
+    _build.build()
+    exe = _compile(tmp_path)
+    r = subprocess.run([str(exe), str(tmp_path / "missing.cfg")], capture_output=True, text=True)
+    assert r.returncode == 2 and "cannot open config file" in r.stderr
+    r = subprocess.run([str(exe)], capture_output=True, text=True)
+    assert r.returncode == 1
+
+
+@pytest.mark.gpu
+def test_shim_runs_time_loop(tmp_path):
+    exe = _compile(tmp_path)
+    r = subprocess.run([str(exe), os.path.join(ROOT, "configs", "cfg0_single_track.cfg")],
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr
+    assert "steps 100" in r.stdout

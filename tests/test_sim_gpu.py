@@ -55,8 +55,11 @@ def test_flux_load_and_dirichlet(sim):
     assert np.array_equal(F == 0.0, g["F_mid"] == 0.0)
     d = s.dirichlet_values(float(g["t_mid"]))
     assert normwise(d, g["g_mid"]) <= 1e-10
-    F0 = s.flux_load(0.0)
-    assert np.array_equal(F0, g["F0"])  # causal zero before activation
+    F0 = s.flux_load(0.0)  # the first source is already active at t = 0 (tau < 0)
+    assert normwise(F0, g["F0"]) <= 1e-10
+    assert np.array_equal(F0 == 0.0, g["F0"] == 0.0)
+    Fe = s.flux_load(-1.0)  # before every modified time: causal exact zero
+    assert not np.any(Fe)
 
 
 def test_flux_load_live_reference_times(sim, ref):
