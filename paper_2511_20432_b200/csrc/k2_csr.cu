@@ -64,7 +64,7 @@ __device__ __forceinline__ void grid_reduce(cg::grid_group& grid, double (&acc)[
 }
 
 __global__ void __launch_bounds__(kThreads) csr_pcg_kernel(DevCsr A, const double* rhs,
-                                                           double* x, PcgWork w, double tol,
+                                                           double* x, CsrWork w, double tol,
                                                            int max_iter) {
   cg::grid_group grid = cg::this_grid();
   __shared__ double red[64];
@@ -177,12 +177,12 @@ void csr_theta_rhs(const DevCsr& Bf, const DevCsr& Ac, const double* T, const do
   TG_CUDA(cudaGetLastError());
 }
 
-void csr_pcg_solve(const DevCsr& A, const double* rhs, double* x, const PcgWork& w, double tol,
+void csr_pcg_solve(const DevCsr& A, const double* rhs, double* x, const CsrWork& w, double tol,
                    int max_iter, int blocks, cudaStream_t s) {
   const int need = (A.rows + kThreads - 1) / kThreads;
   const int nb = std::max(1, std::min(blocks, need));
   DevCsr AA = A;
-  PcgWork ww = w;
+  CsrWork ww = w;
   double tt = tol;
   int mi = max_iter;
   void* args[] = {&AA, const_cast<double**>(&rhs), &x, &ww, &tt, &mi};

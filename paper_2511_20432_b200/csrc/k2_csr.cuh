@@ -14,12 +14,22 @@ struct DevCsr {
   const double* val;
 };
 
+// Work vectors of an assembled-operator solve (stored Jacobi diagonal).
+struct CsrWork {
+  double* r;
+  double* p;
+  double* Ap;
+  double* inv_diag;
+  double* partials;  // >= 8 * max_blocks
+  PcgStatus* status;
+};
+
 int csr_pcg_max_blocks(int sm_count);
 void csr_inverse_diagonal(const DevCsr& A, double* inv_diag, PcgStatus* st, cudaStream_t s);
 void csr_theta_rhs(const DevCsr& Bf, const DevCsr& Ac, const double* T, const double* g1,
                    const double* F0, const double* F1, const int* free_list, double theta,
                    double* rhs, cudaStream_t s);
-void csr_pcg_solve(const DevCsr& A, const double* rhs, double* x, const PcgWork& w, double tol,
+void csr_pcg_solve(const DevCsr& A, const double* rhs, double* x, const CsrWork& w, double tol,
                    int max_iter, int blocks, cudaStream_t s);
 
 }  // namespace tgb

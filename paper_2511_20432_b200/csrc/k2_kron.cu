@@ -7,24 +7,32 @@
 // the p+1-point Gauss quadrature factorizes exactly, so
 //   M = rho c (Mz x My x Mx),  K = k (Mz x My x Kx + Mz x Ky x Mx + Kz x My x Mx)
 // with banded 1D factors (2p+1 diagonals). The apply is sum-factorized:
-//   x-pass  u1 = Mx v, u2 = Kx v          (shared-memory tile with halo)
+//   x-pass  u1 = Mx v, u2 = Kx v          (shared-memory plane tile with halo)
 //   y-pass  w1 = My u1, w2 = My u2, w3 = Ky u1
 //           s1 = a w1 + b (w2 + w3),  s2 = b w1
 //   z-pass  y = Mz s1 + Kz s2            (2p+1-plane register window)
-// Each CTA owns a 32 x 8 column of the control grid and marches through a
-// z-range, so v is read from HBM once and y written once per apply
-// (16 B per DOF); the x/y halos come from L2.
+// A CTA owns a 32 x 8 column of the control grid and marches through a
+// z-range. Halo'd plane tiles arrive by TMA (cp.async.bulk.tensor.3d, zero
+// fill outside the grid) through a 3-stage mbarrier ring, so every vector is
+// read from HBM once and written once per pass; halos come from L2.
 //
-// The whole PCG solve is one persistent cooperative launch: phases separated
-// by grid-wide barriers, dot products reduced per CTA in a fixed tree and
-// then across CTAs in a fixed order (bitwise-deterministic reruns), the
-// convergence test evaluated on the device. The algorithm is the reference's:
-// warm start, Jacobi preconditioner, stop test ||r||/||b|| <= tol before the
-// matvec, b = 0 -> x = 0, failure on pAp <= 0 or after max_iter.
+// The PCG solve is one persistent cooperative launch with two grid barriers
+// per iteration:
+//   A'  p_new = D^-1 r + beta p_old  (computed on the loaded tiles, halo too)
+//       Ap = A p_new, pAp            (tile sweep; p_new and Ap written)
+//   B   x += alpha p, r -= alpha Ap, r.D^-1 r, r.r   (streaming pass)
+// The Jacobi diagonal is recomputed from the 1D factors instead of stored.
+// Dot products are reduced per CTA in a fixed tree and across CTAs in a fixed
+// order (bitwise-deterministic reruns). The algorithm is the reference's:
+// warm start, stop test ||r||/||b|| <= tol before the matvec, b = 0 -> x = 0,
+// failure on pAp <= 0 or after max_iter.
 #include <cooperative_groups.h>
+#include <cuda.h>
 
 #include <algorithm>
 #include <cmath>
+#include <cstring>
+#include <mutex>
 
 #include "common.cuh"
 #include "context.hpp"
@@ -37,14 +45,28 @@ namespace tgb {
 namespace {
 
 constexpr int kThreads = kKronTX * kKronTY;
+constexpr int kStages = 3;
 
-template <int P, int NIN>
-struct TileSmem {
-  double v[NIN][kKronTY + 2 * P][kKronTX + 2 * P];
-  double u1[NIN][kKronTY + 2 * P][kKronTX];
-  double u2[NIN][kKronTY + 2 * P][kKronTX];
-  double cx[2][kKronTX][2 * P + 1];  // Mx, Kx rows of the tile's xi range
-  double cy[2][kKronTY][2 * P + 1];  // My, Ky rows of the tile's eta range
+template <int P>
+struct Dims {
+  static constexpr int W = 2 * P + 1;
+  static constexpr int RY = kKronTY + 2 * P;
+  static constexpr int RX = kKronTX + 2 * P;
+  static constexpr int BUF = ((RY * RX * 8 + 127) / 128) * 128 / 8;  // 128-byte slots
+};
+
+// NIN loaded vectors; NPASS separate x/y passes (2 for the RHS, whose two
+// inputs carry different (a, b)); COMBINE: one pass over a pointwise
+// combination of the two inputs (the PCG direction update).
+template <int P, int NIN, int NPASS>
+struct KSmem {
+  double ring[NIN][kStages][Dims<P>::BUF];
+  double v[Dims<P>::RY][Dims<P>::RX];
+  double u1[NPASS][2][Dims<P>::RY][kKronTX];
+  double u2[NPASS][2][Dims<P>::RY][kKronTX];
+  double cx[2][kKronTX][Dims<P>::W];
+  double cy[2][kKronTY][Dims<P>::W];
+  uint64_t bar[NIN][kStages];
 };
 
 struct TileIdx {
@@ -52,25 +74,19 @@ struct TileIdx {
   __device__ __host__ int count() const { return ntx * nty * nzc; }
 };
 
-// Tile layout for `blocks` co-resident CTAs. Each tile is a 32 x 8 column
-// marching through zlen planes (+ P halo planes each side). With static
-// tile -> CTA assignment (deterministic reductions), the cost is
-// ceil(tiles / blocks) * (zlen + 2P); pick the z split that minimizes it.
-inline TileIdx make_tiles(const KronGrid& g, int blocks, int P) {
+// Tile layout for `blocks` co-resident CTAs; with a static tile -> CTA map
+// (deterministic reductions) the cost is ceil(tiles / blocks) * (zlen + 2P).
+TileIdx make_tiles(const KronGrid& g, int blocks, int P) {
   TileIdx best{};
   double best_cost = 1e300;
   const int ntx = (g.n[0] + kKronTX - 1) / kKronTX;
   const int nty = (g.n[1] + kKronTY - 1) / kKronTY;
   const int cap = std::max(1, g.n[2] / 4);  // >= 4 planes per chunk
   for (int nzc = 1; nzc <= std::min(cap, 16); ++nzc) {
-    TileIdx t;
-    t.ntx = ntx;
-    t.nty = nty;
-    t.zlen = (g.n[2] + nzc - 1) / nzc;
+    TileIdx t{ntx, nty, 0, (g.n[2] + nzc - 1) / nzc};
     t.nzc = (g.n[2] + t.zlen - 1) / t.zlen;
     const int rounds = (t.count() + blocks - 1) / blocks;
-    const double cost = static_cast<double>(rounds) * (t.zlen + 2 * P) * 1.000001 +
-                        1e-9 * t.count();  // ties: fewer tiles
+    const double cost = static_cast<double>(rounds) * (t.zlen + 2 * P) + 1e-9 * t.count();
     if (cost < best_cost) {
       best_cost = cost;
       best = t;
@@ -79,87 +95,172 @@ inline TileIdx make_tiles(const KronGrid& g, int blocks, int P) {
   return best;
 }
 
-// Sweep one tile: for every output point (i, j, k) of the tile call
-// epi(flat_index, i, j, k, y) with y = sum over inputs of Op(a, b) v.
-template <int P, int NIN, class Epi>
-__device__ __forceinline__ void kron_tile(const KronGrid& g, const KronTerms& c,
-                                          const double* __restrict__ v1,
-                                          const double* __restrict__ v2, const TileIdx& T,
-                                          int tile, TileSmem<P, NIN>& sm, Epi& epi) {
+// Jacobi diagonal of Op(a, b) at (i, j, k); the same arithmetic everywhere it
+// is needed, so D^-1 r is bit-identical across phases.
+template <int P>
+__device__ __forceinline__ double diag_at(const KronGrid& g, double a, double b, int i, int j,
+                                          int k) {
   constexpr int W = 2 * P + 1;
-  constexpr int RY = kKronTY + 2 * P;
-  constexpr int RX = kKronTX + 2 * P;
+  const double mx = g.M[0][i * W + P], kx = g.K[0][i * W + P];
+  const double my = g.M[1][j * W + P], ky = g.K[1][j * W + P];
+  const double mz = g.M[2][k * W + P], kz = g.K[2][k * W + P];
+  return a * (mx * my * mz) + b * (kx * my * mz + mx * ky * mz + mx * my * kz);
+}
+
+__device__ __forceinline__ void tma_load_plane(void* dst, const TensorMap3* map, int x, int y,
+                                               int z, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// Inputs of one sweep: NIN vectors, each with a TMA descriptor (or a plain
+// pointer when TMA is off).
+template <int NIN>
+struct Inputs {
+  const double* ptr[NIN];
+  const TensorMap3* map[NIN];
+};
+
+struct NoPrep {
+  double beta;
+};
+
+template <int P, int NIN, int NPASS>
+__device__ __forceinline__ void init_bars(KSmem<P, NIN, NPASS>& sm) {
+  if (threadIdx.x == 0 && threadIdx.y == 0) {
+    for (int q = 0; q < NIN; ++q)
+      for (int s = 0; s < kStages; ++s) mbar_init(&sm.bar[q][s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+}
+
+// Sweep one tile. For every output point (i, j, k) call
+// epi(flat, i, j, k, y, p_own) where y = sum over passes of Op(a_q, b_q) in_q
+// (COMBINE: one pass over v = D^-1 in0 + beta in1; p_own = v at the point).
+// The shared layout SM may hold more input rings than this sweep uses;
+// seqs[q] counts the planes ring q has delivered so far (mbarrier phases).
+template <int P, int NIN, int NPASS, bool COMBINE, bool TMA, class SM, class Epi>
+__device__ __forceinline__ void kron_tile(const KronGrid& g, const KronTerms& c,
+                                          const Inputs<NIN>& in, double beta, const TileIdx& T,
+                                          int tile, SM& sm, int* seqs, Epi& epi) {
+  constexpr int W = Dims<P>::W, RY = Dims<P>::RY, RX = Dims<P>::RX;
   const int tx = threadIdx.x, ty = threadIdx.y;
+  const bool leader = tx == 0 && ty == 0;
   const int txy = tile % (T.ntx * T.nty);
   const int zc = tile / (T.ntx * T.nty);
   const int x0 = (txy % T.ntx) * kKronTX, y0 = (txy / T.ntx) * kKronTY;
   const int k0 = zc * T.zlen, k1 = min(g.n[2], k0 + T.zlen);
   const int nx = g.n[0], ny = g.n[1], nz = g.n[2];
   const int i = x0 + tx, j = y0 + ty;
+  const int kb = max(0, k0 - P), ke = min(nz, k1 + P);
+  constexpr uint32_t kPlaneBytes = RY * RX * 8;
 
-  // the tile's 1D rows in shared memory (zero beyond the grid); the barrier
-  // retires the previous tile's readers, the first plane's barrier orders
-  // these writes before any read
-  __syncthreads();
-  for (int q = ty * kKronTX + tx; q < kKronTX * W; q += kKronTX * kKronTY) {
+  __syncthreads();  // the previous tile's readers of cx / cy / ring are done
+  for (int q = ty * kKronTX + tx; q < kKronTX * W; q += kThreads) {
     const int r = q / W, d = q % W, gi = x0 + r;
     sm.cx[0][r][d] = gi < nx ? g.M[0][gi * W + d] : 0.0;
     sm.cx[1][r][d] = gi < nx ? g.K[0][gi * W + d] : 0.0;
   }
-  for (int q = ty * kKronTX + tx; q < kKronTY * W; q += kKronTX * kKronTY) {
+  for (int q = ty * kKronTX + tx; q < kKronTY * W; q += kThreads) {
     const int r = q / W, d = q % W, gj = y0 + r;
     sm.cy[0][r][d] = gj < ny ? g.M[1][gj * W + d] : 0.0;
     sm.cy[1][r][d] = gj < ny ? g.K[1][gj * W + d] : 0.0;
   }
-  double win1[W], win2[W];
-#pragma unroll
-  for (int d = 0; d < W; ++d) win1[d] = win2[d] = 0.0;
+  if (TMA && leader) {
+    for (int s = 0; s < kStages && kb + s < ke; ++s)
+      for (int q = 0; q < NIN; ++q) {
+        const int slot = (seqs[q] + s) % kStages;
+        mbar_arrive_expect_tx(&sm.bar[q][slot], kPlaneBytes);
+        tma_load_plane(sm.ring[q][slot], in.map[q], x0 - P, y0 - P, kb + s, &sm.bar[q][slot]);
+      }
+  }
 
+  double win1[W], win2[W], pown[W];
+#pragma unroll
+  for (int d = 0; d < W; ++d) win1[d] = win2[d] = pown[d] = 0.0;
   const size_t plane = static_cast<size_t>(nx) * ny;
+
   for (int kin = k0 - P; kin < k1 + P; ++kin) {
-    double s1 = 0.0, s2 = 0.0;
-    if (kin >= 0 && kin < nz) {
-      // load the input plane tile(s) with a P-wide halo, zero outside the grid
+    double s1 = 0.0, s2 = 0.0, po = 0.0;
+    if (kin >= kb && kin < ke) {
+      int slot[NIN];
 #pragma unroll
       for (int q = 0; q < NIN; ++q) {
-        const double* v = q == 0 ? v1 : v2;
-        for (int r = ty; r < RY; r += kKronTY) {
-          const int gj = y0 + r - P;
-          for (int cc = tx; cc < RX; cc += kKronTX) {
-            const int gi = x0 + cc - P;
-            double val = 0.0;
-            if (gi >= 0 && gi < nx && gj >= 0 && gj < ny)
-              val = v[static_cast<size_t>(kin) * plane + static_cast<size_t>(gj) * nx + gi];
-            sm.v[q][r][cc] = val;
-          }
-        }
+        const int qn = seqs[q] + (kin - kb);
+        slot[q] = TMA ? qn % kStages : 0;
+        if (TMA) mbar_wait(&sm.bar[q][slot[q]], static_cast<uint32_t>((qn / kStages) & 1));
       }
-      __syncthreads();
-      // x-pass on the rows of the tile plus the y halo
+      if constexpr (!TMA) {
+        for (int q = 0; q < NIN; ++q)
+          for (int r = ty; r < RY; r += kKronTY) {
+            const int gj = y0 + r - P;
+            for (int cc = tx; cc < RX; cc += kKronTX) {
+              const int gi = x0 + cc - P;
+              double val = 0.0;
+              if (gi >= 0 && gi < nx && gj >= 0 && gj < ny)
+                val = in.ptr[q][static_cast<size_t>(kin) * plane + static_cast<size_t>(gj) * nx + gi];
+              sm.ring[q][0][r * RX + cc] = val;
+            }
+          }
+        __syncthreads();
+      }
+      if constexpr (COMBINE) {  // v = D^-1 r + beta p_old over the halo'd tile
+        for (int e = ty * kKronTX + tx; e < RY * RX; e += kThreads) {
+          const int r = e / RX, cc = e % RX;
+          const int gi = x0 + cc - P, gj = y0 + r - P;
+          double val = 0.0;
+          if (gi >= 0 && gi < nx && gj >= 0 && gj < ny) {
+            const double z = (1.0 / diag_at<P>(g, c.a1, c.b1, gi, gj, kin)) * sm.ring[0][slot[0]][e];
+            val = z + beta * sm.ring[1][slot[NIN - 1]][e];
+          }
+          sm.v[r][cc] = val;
+        }
+        __syncthreads();
+        po = sm.v[ty + P][tx + P];
+      }
+      // x-pass on the tile rows plus the y halo
 #pragma unroll
-      for (int q = 0; q < NIN; ++q)
+      for (int q = 0; q < NPASS; ++q) {
+        const double* src = COMBINE ? &sm.v[0][0] : sm.ring[q][slot[q < NIN ? q : 0]];
         for (int r = ty; r < RY; r += kKronTY) {
           double a1 = 0.0, a2 = 0.0;
 #pragma unroll
           for (int d = 0; d < W; ++d) {
-            const double vv = sm.v[q][r][tx + d];
+            const double vv = src[r * RX + tx + d];
             a1 = fma(sm.cx[0][tx][d], vv, a1);
             a2 = fma(sm.cx[1][tx][d], vv, a2);
           }
-          sm.u1[q][r][tx] = a1;
-          sm.u2[q][r][tx] = a2;
+          sm.u1[q][kin & 1][r][tx] = a1;
+          sm.u2[q][kin & 1][r][tx] = a2;
         }
+      }
       __syncthreads();
+      if (TMA && leader && kin + kStages < ke) {  // refill the slots just consumed
+        fence_proxy_async();
+        for (int q = 0; q < NIN; ++q) {
+          mbar_arrive_expect_tx(&sm.bar[q][slot[q]], kPlaneBytes);
+          tma_load_plane(sm.ring[q][slot[q]], in.map[q], x0 - P, y0 - P, kin + kStages,
+                         &sm.bar[q][slot[q]]);
+        }
+      }
       // y-pass and the z-pass inputs
 #pragma unroll
-      for (int q = 0; q < NIN; ++q) {
+      for (int q = 0; q < NPASS; ++q) {
         double w1 = 0.0, w2 = 0.0, w3 = 0.0;
 #pragma unroll
         for (int d = 0; d < W; ++d) {
-          const double p1 = sm.u1[q][ty + d][tx];
+          const double p1 = sm.u1[q][kin & 1][ty + d][tx];
           const double my = sm.cy[0][ty][d];
           w1 = fma(my, p1, w1);
-          w2 = fma(my, sm.u2[q][ty + d][tx], w2);
+          w2 = fma(my, sm.u2[q][kin & 1][ty + d][tx], w2);
           w3 = fma(sm.cy[1][ty][d], p1, w3);
         }
         const double a = q == 0 ? c.a1 : c.a2, b = q == 0 ? c.b1 : c.b2;
@@ -171,9 +272,11 @@ __device__ __forceinline__ void kron_tile(const KronGrid& g, const KronTerms& c,
     for (int d = 0; d < W - 1; ++d) {
       win1[d] = win1[d + 1];
       win2[d] = win2[d + 1];
+      pown[d] = pown[d + 1];
     }
     win1[W - 1] = s1;
     win2[W - 1] = s2;
+    pown[W - 1] = po;
     const int k = kin - P;
     if (k >= k0 && i < nx && j < ny) {
       const double* mz = g.M[2] + k * W;
@@ -181,34 +284,38 @@ __device__ __forceinline__ void kron_tile(const KronGrid& g, const KronTerms& c,
       double y = 0.0;
 #pragma unroll
       for (int d = 0; d < W; ++d) y = fma(mz[d], win1[d], fma(kz[d], win2[d], y));
-      epi(static_cast<size_t>(k) * plane + static_cast<size_t>(j) * nx + i, i, j, k, y);
+      epi(static_cast<size_t>(k) * plane + static_cast<size_t>(j) * nx + i, i, j, k, y, pown[P]);
     }
   }
+#pragma unroll
+  for (int q = 0; q < NIN; ++q) seqs[q] += ke - kb;
 }
 
 // ---------------------------------------------------------------------------
-// stand-alone applies
+// stand-alone applies (plain loads)
 
-template <int P>
 struct EpiStore {
   double* y;
-  __device__ void operator()(size_t idx, int, int, int, double v) { y[idx] = v; }
+  __device__ void operator()(size_t idx, int, int, int, double v, double) { y[idx] = v; }
 };
 
 template <int P>
 __global__ void __launch_bounds__(kThreads) k2_apply_kernel(KronGrid g, KronTerms c,
                                                             const double* v, double* y,
                                                             TileIdx T) {
-  __shared__ TileSmem<P, 1> sm;
-  EpiStore<P> epi{y};
-  for (int t = blockIdx.x; t < T.count(); t += gridDim.x) kron_tile<P, 1>(g, c, v, nullptr, T, t, sm, epi);
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  auto& sm = *reinterpret_cast<KSmem<P, 1, 1>*>(smem_raw);
+  EpiStore epi{y};
+  Inputs<1> in{{v}, {nullptr}};
+  int seq[1] = {0};
+  for (int t = blockIdx.x; t < T.count(); t += gridDim.x)
+    kron_tile<P, 1, 1, false, false>(g, c, in, 0.0, T, t, sm, seq, epi);
 }
 
-template <int P>
 struct EpiRhs {
   RhsArgs a;
   int nfree[3];
-  __device__ void operator()(size_t idx, int i, int j, int k, double y) {
+  __device__ void operator()(size_t idx, int i, int j, int k, double y, double) {
     int ijk[3] = {i, j, k};
     if (ijk[a.bottom_axis] == a.bottom_layer) return;
     if (a.bottom_layer == 0) ijk[a.bottom_axis] -= 1;
@@ -218,48 +325,43 @@ struct EpiRhs {
   }
 };
 
-template <int P>
+struct RhsMaps {
+  TensorMap3 T, g;
+};
+
+template <int P, bool TMA>
 __global__ void __launch_bounds__(kThreads) k2_rhs_kernel(KronGrid g, KronTerms c, RhsArgs args,
-                                                          TileIdx T) {
-  __shared__ TileSmem<P, 2> sm;
-  EpiRhs<P> epi{args, {g.n[0], g.n[1], g.n[2]}};
+                                                          TileIdx T,
+                                                          const __grid_constant__ RhsMaps maps) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  auto& sm = *reinterpret_cast<KSmem<P, 2, 2>*>(smem_raw);
+  if (TMA) init_bars(sm);
+  EpiRhs epi{args, {g.n[0], g.n[1], g.n[2]}};
   epi.nfree[args.bottom_axis] -= 1;
+  Inputs<2> in{{args.T_full, args.g_full}, {&maps.T, &maps.g}};
+  int seq[2] = {0, 0};
   for (int t = blockIdx.x; t < T.count(); t += gridDim.x)
-    kron_tile<P, 2>(g, c, args.T_full, args.g_full, T, t, sm, epi);
+    kron_tile<P, 2, 2, false, TMA>(g, c, in, 0.0, T, t, sm, seq, epi);
 }
 
-// ---------------------------------------------------------------------------
-// diagonal
-
 template <int P>
-__global__ void k2_diag_kernel(KronGrid g, double a, double b, double* inv_diag,
-                               PcgStatus* st) {
+__global__ void k2_diag_check_kernel(KronGrid g, double a, double b, PcgStatus* st) {
   const size_t n = static_cast<size_t>(g.n[0]) * g.n[1] * g.n[2];
-  constexpr int W = 2 * P + 1;
   for (size_t f = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; f < n;
        f += static_cast<size_t>(gridDim.x) * blockDim.x) {
     const int i = static_cast<int>(f % g.n[0]);
     const int j = static_cast<int>((f / g.n[0]) % g.n[1]);
     const int k = static_cast<int>(f / (static_cast<size_t>(g.n[0]) * g.n[1]));
-    const double mx = g.M[0][i * W + P], kx = g.K[0][i * W + P];
-    const double my = g.M[1][j * W + P], ky = g.K[1][j * W + P];
-    const double mz = g.M[2][k * W + P], kz = g.K[2][k * W + P];
-    const double d = a * (mx * my * mz) + b * (kx * my * mz + mx * ky * mz + mx * my * kz);
-    if (!(d > 0.0)) st->status = 2;
-    inv_diag[f] = 1.0 / d;
+    if (!(diag_at<P>(g, a, b, i, j, k) > 0.0)) st->status = 2;
   }
 }
 
 // ---------------------------------------------------------------------------
 // persistent Jacobi-PCG
 
-struct Acc4 {
-  double v[4];
-};
-
 // Block-reduce acc (fixed tree), store to partials[buf][block][4], grid sync,
 // then every CTA sums the per-block partials in the same fixed order.
-__device__ __forceinline__ void grid_reduce(cg::grid_group& grid, double (&acc)[4],
+__device__ __forceinline__ void grid_reduce(cg::grid_group& grid, const double (&acc)[4],
                                             double* partials, int& buf, double* red,
                                             double (&out)[4]) {
   const int tid = threadIdx.y * blockDim.x + threadIdx.x;
@@ -297,54 +399,62 @@ __device__ __forceinline__ void grid_reduce(cg::grid_group& grid, double (&acc)[
 }
 
 template <int P>
-struct EpiResidual {  // r = b - A x; z = D^-1 r; p = z; accumulate rr, bb, rz
+struct EpiResidual {  // r = b - A x; rr, bb, r.D^-1 r; p_old = 0
+  const KronGrid* g;
+  double a, b;
   const double* rhs;
-  const double* invd;
   double* r;
-  double* p;
+  double* p_old;
   double acc[4];
-  __device__ void operator()(size_t idx, int, int, int, double y) {
+  __device__ void operator()(size_t idx, int i, int j, int k, double y, double) {
     const double bi = rhs[idx];
     const double ri = bi - y;
-    const double zi = invd[idx] * ri;
+    const double zi = (1.0 / diag_at<P>(*g, a, b, i, j, k)) * ri;
     r[idx] = ri;
-    p[idx] = zi;
+    p_old[idx] = 0.0;
     acc[0] += ri * ri;
     acc[1] += bi * bi;
     acc[2] += ri * zi;
   }
 };
 
-template <int P>
-struct EpiAp {
-  const double* p;
+struct EpiDirection {  // p_new (own point), Ap, p.Ap
+  double* p_new;
   double* Ap;
   double acc[4];
-  __device__ void operator()(size_t idx, int, int, int, double y) {
+  __device__ void operator()(size_t idx, int, int, int, double y, double p) {
+    p_new[idx] = p;
     Ap[idx] = y;
-    acc[0] += p[idx] * y;
+    acc[0] += p * y;
   }
 };
 
-template <int P>
-__global__ void __launch_bounds__(kThreads, 3) k2_pcg_kernel(KronGrid g, double a, double b,
-                                                          const double* rhs, double* x,
-                                                          PcgWork w, double tol, int max_iter,
-                                                          TileIdx T) {
+template <int P, bool TMA>
+__global__ void __launch_bounds__(kThreads, 3)
+    k2_pcg_kernel(KronGrid g, double a, double b, const double* rhs, double* x, PcgWork w,
+                  double tol, int max_iter, TileIdx T, const __grid_constant__ PcgMaps maps) {
   cg::grid_group grid = cg::this_grid();
-  __shared__ TileSmem<P, 1> sm;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  auto& sm = *reinterpret_cast<KSmem<P, 2, 1>*>(smem_raw);
   __shared__ double red[64];
+  if (TMA) init_bars(sm);
   const KronTerms c{a, b, 0.0, 0.0};
-  const size_t n = static_cast<size_t>(g.n[0]) * g.n[1] * g.n[2];
+  const int nx = g.n[0], ny = g.n[1];
+  const size_t n = static_cast<size_t>(nx) * ny * g.n[2];
   const size_t gtid = static_cast<size_t>(blockIdx.x) * kThreads + threadIdx.y * kKronTX + threadIdx.x;
   const size_t gstride = static_cast<size_t>(gridDim.x) * kThreads;
   int buf = 0;
+  int seq[2] = {0, 0};
   double tot[4];
 
-  // r = b - A x, z = D^-1 r, p = z   (sparse.cpp:61-70)
-  EpiResidual<P> e0{rhs, w.inv_diag, w.r, w.p, {0, 0, 0, 0}};
-  for (int t = blockIdx.x; t < T.count(); t += gridDim.x) kron_tile<P, 1>(g, c, x, nullptr, T, t, sm, e0);
-  grid_reduce(grid, e0.acc, w.partials, buf, red, tot);
+  // r = b - A x (sparse.cpp:61-70); the first direction update sees p_old = 0
+  {
+    EpiResidual<P> e0{&g, a, b, rhs, w.r, w.pA, {0, 0, 0, 0}};
+    Inputs<1> in1{{x}, {&maps.x}};  // ring 0 of the two-ring layout
+    for (int t = blockIdx.x; t < T.count(); t += gridDim.x)
+      kron_tile<P, 1, 1, false, TMA>(g, c, in1, 0.0, T, t, sm, seq, e0);
+    grid_reduce(grid, e0.acc, w.partials, buf, red, tot);
+  }
   double rr = tot[0], rz = tot[2];
   const double bnorm = sqrt(tot[1]);
   if (bnorm == 0.0) {  // sparse.cpp:57-60: zero rhs resets even a warm start
@@ -353,16 +463,23 @@ __global__ void __launch_bounds__(kThreads, 3) k2_pcg_kernel(KronGrid g, double 
       *w.status = PcgStatus{0, 0, 0.0, 0.0};
     return;
   }
-  double rel = 0.0;
+  double rel = 0.0, beta = 0.0;
   int it = 0, status = 3;
+  double* p_old = w.pA;
+  double* p_new = w.pB;
+  const TensorMap3* m_old = &maps.pA;
+  const TensorMap3* m_new = &maps.pB;
   for (it = 0; it < max_iter; ++it) {
     rel = sqrt(rr) / bnorm;
     if (rel <= tol) {
       status = 0;
       break;
     }
-    EpiAp<P> e1{w.p, w.Ap, {0, 0, 0, 0}};
-    for (int t = blockIdx.x; t < T.count(); t += gridDim.x) kron_tile<P, 1>(g, c, w.p, nullptr, T, t, sm, e1);
+    // A': p_new = D^-1 r + beta p_old, Ap = A p_new
+    EpiDirection e1{p_new, w.Ap, {0, 0, 0, 0}};
+    Inputs<2> in{{w.r, p_old}, {&maps.r, m_old}};
+    for (int t = blockIdx.x; t < T.count(); t += gridDim.x)
+      kron_tile<P, 2, 1, true, TMA>(g, c, in, beta, T, t, sm, seq, e1);
     grid_reduce(grid, e1.acc, w.partials, buf, red, tot);
     const double pAp = tot[0];
     if (!(pAp > 0.0)) {
@@ -370,40 +487,98 @@ __global__ void __launch_bounds__(kThreads, 3) k2_pcg_kernel(KronGrid g, double 
       break;
     }
     const double alpha = rz / pAp;
+    // B: x, r updates and the two dot products (sparse.cpp:85-94)
     double acc[4] = {0, 0, 0, 0};
     for (size_t f = gtid; f < n; f += gstride) {
-      const double pi = w.p[f];
-      x[f] += alpha * pi;
+      const int i = static_cast<int>(f % nx);
+      const int j = static_cast<int>((f / nx) % ny);
+      const int k = static_cast<int>(f / (static_cast<size_t>(nx) * ny));
+      x[f] += alpha * p_new[f];
       const double ri = w.r[f] - alpha * w.Ap[f];
       w.r[f] = ri;
-      const double zi = w.inv_diag[f] * ri;
+      const double zi = (1.0 / diag_at<P>(g, a, b, i, j, k)) * ri;
       acc[0] += ri * zi;
       acc[1] += ri * ri;
     }
     grid_reduce(grid, acc, w.partials, buf, red, tot);
-    const double beta = tot[0] / rz;
+    beta = tot[0] / rz;
     rz = tot[0];
     rr = tot[1];
-    for (size_t f = gtid; f < n; f += gstride) w.p[f] = w.inv_diag[f] * w.r[f] + beta * w.p[f];
-    grid.sync();
+    double* tp = p_old;
+    p_old = p_new;
+    p_new = tp;
+    const TensorMap3* tm = m_old;
+    m_old = m_new;
+    m_new = tm;
   }
   if (blockIdx.x == 0 && threadIdx.x == 0 && threadIdx.y == 0)
     *w.status = PcgStatus{it, status, rel, bnorm};
 }
 
+// --------------------------------------------------------------------------
+// TMA descriptor encoding through the driver entry point (no -lcuda)
+
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                              const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                              const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                              CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeFn encoder() {
+  static EncodeFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeFn>(p);
+  });
+  return fn;
+}
+
 template <int P>
-const void* pcg_kernel_ptr() {
-  return reinterpret_cast<const void*>(&k2_pcg_kernel<P>);
+size_t smem_bytes(int nin, int npass) {
+  if (nin == 1) return sizeof(KSmem<P, 1, 1>);
+  if (npass == 2) return sizeof(KSmem<P, 2, 2>);
+  return sizeof(KSmem<P, 2, 1>);
+}
+
+template <typename K>
+void allow_smem(K kernel, size_t bytes) {
+  TG_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(bytes)));
 }
 
 }  // namespace
 
-// dispatch on the degree (stored in the band width)
-#define TG_KRON_DISPATCH(P_, ...)                                      \
-  switch (P_) {                                                        \
-    case 1: { constexpr int P = 1; __VA_ARGS__; break; }               \
-    case 2: { constexpr int P = 2; __VA_ARGS__; break; }               \
-    case 3: { constexpr int P = 3; __VA_ARGS__; break; }               \
+bool k2_make_map(const KronGrid& g, const double* base, TensorMap3* out) {
+  static_assert(sizeof(TensorMap3) == sizeof(CUtensorMap), "tensor map size");
+  EncodeFn enc = encoder();
+  const size_t pitch = static_cast<size_t>(g.n[0]) * sizeof(double);
+  if (!enc || pitch % 16 != 0 || reinterpret_cast<uintptr_t>(base) % 16 != 0) return false;
+  const cuuint64_t dims[3] = {static_cast<cuuint64_t>(g.n[0]), static_cast<cuuint64_t>(g.n[1]),
+                              static_cast<cuuint64_t>(g.n[2])};
+  const cuuint64_t strides[2] = {pitch, pitch * static_cast<cuuint64_t>(g.n[1])};
+  const cuuint32_t box[3] = {static_cast<cuuint32_t>(kKronTX + 2 * g.p),
+                             static_cast<cuuint32_t>(kKronTY + 2 * g.p), 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  CUtensorMap m;
+  const CUresult r = enc(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base), dims,
+                         strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                         CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return false;
+  std::memcpy(out, &m, sizeof(m));
+  return true;
+}
+
+// dispatch on the degree
+#define TG_KRON_DISPATCH(P_, ...)                                                \
+  switch (P_) {                                                                  \
+    case 1: { constexpr int P = 1; __VA_ARGS__; break; }                         \
+    case 2: { constexpr int P = 2; __VA_ARGS__; break; }                         \
+    case 3: { constexpr int P = 3; __VA_ARGS__; break; }                         \
     default: throw std::invalid_argument("kronecker path supports degree 1..3"); \
   }
 
@@ -411,46 +586,76 @@ void k2_apply(const KronGrid& g, double a, double b, const double* v, double* y,
               cudaStream_t s) {
   const TileIdx T = make_tiles(g, 3 * sm_count, g.p);
   const int blocks = std::min(T.count(), 3 * sm_count);
-  TG_KRON_DISPATCH(g.p, k2_apply_kernel<P><<<blocks, dim3(kKronTX, kKronTY), 0, s>>>(
-                                 g, KronTerms{a, b, 0.0, 0.0}, v, y, T));
+  TG_KRON_DISPATCH(g.p, {
+    const size_t sb = smem_bytes<P>(1, 1);
+    allow_smem(k2_apply_kernel<P>, sb);
+    k2_apply_kernel<P><<<blocks, dim3(kKronTX, kKronTY), sb, s>>>(g, KronTerms{a, b, 0.0, 0.0},
+                                                                  v, y, T);
+  });
   TG_CUDA(cudaGetLastError());
 }
 
 void k2_theta_rhs(const KronGrid& full, double a_b, double b_b, double a_a, double b_a,
-                  const RhsArgs& args, int sm_count, cudaStream_t s) {
+                  const RhsArgs& args, const TensorMap3* mT, const TensorMap3* mg, int sm_count,
+                  cudaStream_t s) {
   const TileIdx T = make_tiles(full, 2 * sm_count, full.p);
   const int blocks = std::min(T.count(), 2 * sm_count);
-  TG_KRON_DISPATCH(full.p, k2_rhs_kernel<P><<<blocks, dim3(kKronTX, kKronTY), 0, s>>>(
-                                 full, KronTerms{a_b, b_b, a_a, b_a}, args, T));
+  RhsMaps maps{};
+  const bool tma = mT && mg;
+  if (tma) {
+    maps.T = *mT;
+    maps.g = *mg;
+  }
+  const KronTerms c{a_b, b_b, a_a, b_a};
+  TG_KRON_DISPATCH(full.p, {
+    const size_t sb = smem_bytes<P>(2, 2);
+    if (tma) {
+      allow_smem(k2_rhs_kernel<P, true>, sb);
+      k2_rhs_kernel<P, true><<<blocks, dim3(kKronTX, kKronTY), sb, s>>>(full, c, args, T, maps);
+    } else {
+      allow_smem(k2_rhs_kernel<P, false>, sb);
+      k2_rhs_kernel<P, false><<<blocks, dim3(kKronTX, kKronTY), sb, s>>>(full, c, args, T, maps);
+    }
+  });
   TG_CUDA(cudaGetLastError());
 }
 
-void k2_inverse_diagonal(const KronGrid& g, double a, double b, double* inv_diag,
-                         PcgStatus* status, cudaStream_t s) {
-  TG_KRON_DISPATCH(g.p, k2_diag_kernel<P><<<256, 256, 0, s>>>(g, a, b, inv_diag, status));
+void k2_check_diagonal(const KronGrid& g, double a, double b, PcgStatus* status, cudaStream_t s) {
+  TG_KRON_DISPATCH(g.p, k2_diag_check_kernel<P><<<256, 256, 0, s>>>(g, a, b, status));
   TG_CUDA(cudaGetLastError());
 }
 
 int k2_pcg_max_blocks(int p, int sm_count) {
   int per_sm = 0;
-  TG_KRON_DISPATCH(p, TG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-                                 &per_sm, pcg_kernel_ptr<P>(), kThreads, 0)));
+  TG_KRON_DISPATCH(p, {
+    const size_t sb = smem_bytes<P>(2, 1);
+    allow_smem(k2_pcg_kernel<P, true>, sb);
+    allow_smem(k2_pcg_kernel<P, false>, sb);
+    TG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+        &per_sm, reinterpret_cast<const void*>(&k2_pcg_kernel<P, true>), kThreads, sb));
+  });
   return std::max(1, per_sm) * sm_count;
 }
 
 void k2_pcg_solve(const KronGrid& g, double a, double b, const double* rhs, double* x,
-                  const PcgWork& w, double tol, int max_iter, int blocks, cudaStream_t s) {
+                  const PcgWork& w, const PcgMaps& maps, double tol, int max_iter, int blocks,
+                  cudaStream_t s) {
   const TileIdx T = make_tiles(g, blocks, g.p);
-  int nb = std::max(1, std::min(blocks, T.count()));
+  const int nb = std::max(1, std::min(blocks, T.count()));
   dim3 grid(nb), block(kKronTX, kKronTY);
   KronGrid gg = g;
   PcgWork ww = w;
+  PcgMaps mm = maps;
   double aa = a, bb = b, tt = tol;
   int mi = max_iter;
   TileIdx TT = T;
-  void* args[] = {&gg, &aa, &bb, const_cast<double**>(&rhs), &x, &ww, &tt, &mi, &TT};
-  TG_KRON_DISPATCH(g.p, TG_CUDA(cudaLaunchCooperativeKernel(pcg_kernel_ptr<P>(), grid,
-                                                                  block, args, 0, s)));
+  void* args[] = {&gg, &aa, &bb, const_cast<double**>(&rhs), &x, &ww, &tt, &mi, &TT, &mm};
+  TG_KRON_DISPATCH(g.p, {
+    const size_t sb = smem_bytes<P>(2, 1);
+    const void* fn = maps.valid ? reinterpret_cast<const void*>(&k2_pcg_kernel<P, true>)
+                                : reinterpret_cast<const void*>(&k2_pcg_kernel<P, false>);
+    TG_CUDA(cudaLaunchCooperativeKernel(fn, grid, block, args, sb, s));
+  });
 }
 
 }  // namespace tgb

@@ -20,6 +20,17 @@ struct KronGrid {
   const double* K[3];
 };
 
+// Opaque CUtensorMap (128 bytes, 64-byte aligned): a 3D TMA descriptor of one
+// grid vector with a (32+2p) x (8+2p) x 1 box (a halo'd plane tile), zero
+// fill outside the grid.
+struct alignas(64) TensorMap3 {
+  unsigned char bytes[128];
+};
+// Encode the descriptor for `base` (a vector over g's grid). Returns false
+// when TMA cannot address the grid (row pitch not a multiple of 16 bytes);
+// the kernels then load planes with ordinary loads.
+bool k2_make_map(const KronGrid& g, const double* base, TensorMap3* out);
+
 // y = Op(a1, b1) v1 + Op(a2, b2) v2 with Op(a, b) = a (Mz x My x Mx) +
 //     b (Mz x My x Kx + Mz x Ky x Mx + Kz x My x Mx); v2 may be null.
 struct KronTerms {
@@ -45,26 +56,34 @@ struct PcgStatus {
   double bnorm;
 };
 
-void k2_theta_rhs(const KronGrid& full, double a_b, double b_b, double a_a, double b_a,
-                  const RhsArgs& args, int sm_count, cudaStream_t s);
-
-// Jacobi-PCG on A = a Op_M + b Op_K over the free grid, one persistent
-// cooperative launch per solve; x holds the warm start on entry.
+// Work vectors of a solve; pA/pB are the ping-pong search directions.
 struct PcgWork {
   double* r;
-  double* p;
+  double* pA;
+  double* pB;
   double* Ap;
-  double* inv_diag;
-  double* partials;  // >= 4 * max_blocks
+  double* partials;  // >= 8 * max_blocks
   PcgStatus* status;
 };
-void k2_inverse_diagonal(const KronGrid& g, double a, double b, double* inv_diag,
-                         PcgStatus* status, cudaStream_t s);
-int k2_pcg_max_blocks(int p, int sm_count);
-void k2_pcg_solve(const KronGrid& g, double a, double b, const double* rhs, double* x,
-                  const PcgWork& w, double tol, int max_iter, int blocks, cudaStream_t s);
 
-// plain y = Op(a, b) v on a grid (tests / benchmarks of the apply alone)
+// TMA descriptors of the vectors the PCG kernel streams (x, r, pA, pB), all
+// over the free grid; valid = false -> plain loads.
+struct PcgMaps {
+  bool valid;
+  TensorMap3 x, r, pA, pB;
+};
+
+void k2_theta_rhs(const KronGrid& full, double a_b, double b_b, double a_a, double b_a,
+                  const RhsArgs& args, const TensorMap3* mT, const TensorMap3* mg, int sm_count,
+                  cudaStream_t s);
+void k2_check_diagonal(const KronGrid& g, double a, double b, PcgStatus* status, cudaStream_t s);
+int k2_pcg_max_blocks(int p, int sm_count);
+// Jacobi-PCG on A = Op(a, b) over the free grid, one persistent cooperative
+// launch per solve; x holds the warm start on entry.
+void k2_pcg_solve(const KronGrid& g, double a, double b, const double* rhs, double* x,
+                  const PcgWork& w, const PcgMaps& maps, double tol, int max_iter, int blocks,
+                  cudaStream_t s);
+// plain y = Op(a, b) v (tests / the operator alone)
 void k2_apply(const KronGrid& g, double a, double b, const double* v, double* y, int sm_count,
               cudaStream_t s);
 

@@ -297,8 +297,13 @@ void Sim::setup_device(int device) {
       gfree.M[geom.ax] += W;
       gfree.K[geom.ax] += W;
     }
-    k2_inverse_diagonal(gfree, coefA[0], coefA[1], d_invd.p, d_status.p, s);
+    k2_check_diagonal(gfree, coefA[0], coefA[1], d_status.p, s);
     pcg_blocks = k2_pcg_max_blocks(p, ctx->sm_count);
+    d_p2.ensure(n_free);
+    // TMA descriptors of the streamed vectors (all persistent allocations)
+    maps.valid = k2_make_map(gfree, d_x.p, &maps.x) && k2_make_map(gfree, d_r.p, &maps.r) &&
+                 k2_make_map(gfree, d_p.p, &maps.pA) && k2_make_map(gfree, d_p2.p, &maps.pB);
+    rhs_tma = k2_make_map(gfull, d_T.p, &map_T) && k2_make_map(gfull, d_gfull.p, &map_g);
   } else {
     auto up = [&](const Csr& C, DevBuf<int>& rp, DevBuf<int>& ci, DevBuf<double>& v, DevCsr& out) {
       upload(rp, C.row_ptr, s);
@@ -382,20 +387,23 @@ PcgStatus Sim::theta_step_device(double tol, int max_iter) {
   expand_kernel<<<static_cast<int>((n_full + threads - 1) / threads), threads, 0, s>>>(
       geom, d_x.p, d_gn.p, d_T.p);
   ++ctx->timer.launches;
-  PcgWork w{d_r.p, d_p.p, d_Ap.p, d_invd.p, d_partials.p, d_status.p};
   const double th = cfg.stepping.theta;
   if (kron) {
     scatter_layer_kernel<<<(n_con + threads - 1) / threads, threads, 0, s>>>(geom, d_g1.p,
                                                                              d_gfull.p);
     RhsArgs ra{d_T.p, d_gfull.p, d_Fn.p, d_F1.p, th, geom.ax, geom.layer, d_rhs.p};
-    k2_theta_rhs(gfull, coefB[0], coefB[1], -coefA[0], -coefA[1], ra, ctx->sm_count, s);
+    k2_theta_rhs(gfull, coefB[0], coefB[1], -coefA[0], -coefA[1], ra, rhs_tma ? &map_T : nullptr,
+                 rhs_tma ? &map_g : nullptr, ctx->sm_count, s);
     ctx->timer.launches += 2;
+    const PcgWork w{d_r.p, d_p.p, d_p2.p, d_Ap.p, d_partials.p, d_status.p};
     ctx->timer.timed(2, s, [&] {
-      k2_pcg_solve(gfree, coefA[0], coefA[1], d_rhs.p, d_x.p, w, tol, max_iter, pcg_blocks, s);
+      k2_pcg_solve(gfree, coefA[0], coefA[1], d_rhs.p, d_x.p, w, maps, tol, max_iter,
+                   pcg_blocks, s);
     });
   } else {
     csr_theta_rhs(devB, devAc, d_T.p, d_g1.p, d_Fn.p, d_F1.p, d_free_list.p, th, d_rhs.p, s);
     ++ctx->timer.launches;
+    const CsrWork w{d_r.p, d_p.p, d_Ap.p, d_invd.p, d_partials.p, d_status.p};
     ctx->timer.timed(2, s, [&] {
       csr_pcg_solve(devA, d_rhs.p, d_x.p, w, tol, max_iter, pcg_blocks, s);
     });

@@ -75,8 +75,11 @@ class Sim {
   DevBuf<double> dA_v, dAc_v, dB_v;
   DevCsr devA{}, devAc{}, devB{};
   KronGrid gfull{}, gfree{};
-  DevBuf<double> d_x, d_r, d_p, d_Ap, d_invd, d_rhs, d_gn, d_g1, d_Fn, d_F1, d_T, d_gfull,
+  DevBuf<double> d_x, d_r, d_p, d_p2, d_Ap, d_invd, d_rhs, d_gn, d_g1, d_Fn, d_F1, d_T, d_gfull,
       d_partials;
+  PcgMaps maps{};
+  TensorMap3 map_T{}, map_g{};
+  bool rhs_tma = false;
   DevBuf<PcgStatus> d_status;
   PcgStatus* h_status = nullptr;
   int* h_fine = nullptr;

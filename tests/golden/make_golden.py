@@ -52,7 +52,8 @@ if __name__ == "__main__":
         k1(R)
 
 
-SIM_STEPS = {"cfg0_parity": [1, 2, 3, 5, 10, 25, 50, 75, 100], "qc_small": [1, 2, 5, 12, 24]}
+SIM_STEPS = {"cfg0_parity": [1, 2, 3, 5, 10, 25, 50, 75, 100], "qc_small": [1, 2, 5, 12, 24],
+             "cfg0_oddx": [1, 2, 10, 40]}
 
 
 def sim_run(R, name):

@@ -17,7 +17,7 @@ import paper_2511_20432_b200 as tg
 from conftest import GOLDEN, ROOT
 
 pytestmark = pytest.mark.gpu
-NAMES = ["cfg0_parity", "qc_small"]
+NAMES = ["cfg0_parity", "qc_small", "cfg0_oddx"]
 
 
 def cfg(name):
@@ -100,7 +100,7 @@ def test_full_time_loop(sim):
     s.reset()
     st = s.state()
     assert st["step"] == 0 and not np.any(st["free"])
-    assert np.array_equal(st["F"], g["F0"]) and normwise(st["g"], g["g0"]) <= 1e-10
+    assert normwise(st["F"], g["F0"]) <= 1e-10 and normwise(st["g"], g["g0"]) <= 1e-10
     done = 0
     total_it = 0
     worst = 0.0
