@@ -66,6 +66,7 @@ struct KSmem {
   double u2[NPASS][2][Dims<P>::RY][kKronTX];
   double cx[2][kKronTX][Dims<P>::W];
   double cy[2][kKronTY][Dims<P>::W];
+  double qr[2][Dims<P>::RY][Dims<P>::RX];  // diagonal factors Q, R of the halo'd tile
   uint64_t bar[NIN][kStages];
 };
 
@@ -95,16 +96,33 @@ TileIdx make_tiles(const KronGrid& g, int blocks, int P) {
   return best;
 }
 
-// Jacobi diagonal of Op(a, b) at (i, j, k); the same arithmetic everywhere it
-// is needed, so D^-1 r is bit-identical across phases.
+// Jacobi diagonal of Op(a, b) factored by columns:
+//   diag(i, j, k) = Mz_kk Q_ij + Kz_kk R_ij,
+//   Q_ij = a Mx_ii My_jj + b (Kx_ii My_jj + Mx_ii Ky_jj),  R_ij = b Mx_ii My_jj.
+// Written with explicit _rn operations so every phase (and the host check)
+// produces the same bits; the reciprocal is the correctly rounded
+// __drcp_rn, i.e. the reference's 1.0 / d (sparse.cpp:51).
+struct QR {
+  double q, r;
+};
+template <int P>
+__device__ __forceinline__ QR qr_at(const KronGrid& g, double a, double b, int i, int j) {
+  constexpr int W = 2 * P + 1;
+  const double mx = g.M[0][i * W + P], kx = g.K[0][i * W + P];
+  const double my = g.M[1][j * W + P], ky = g.K[1][j * W + P];
+  const double mm = __dmul_rn(mx, my);
+  const double km = __dadd_rn(__dmul_rn(kx, my), __dmul_rn(mx, ky));
+  return {__dadd_rn(__dmul_rn(a, mm), __dmul_rn(b, km)), __dmul_rn(b, mm)};
+}
+__device__ __forceinline__ double inv_diag(const QR& c, double mz, double kz) {
+  return __drcp_rn(__dadd_rn(__dmul_rn(mz, c.q), __dmul_rn(kz, c.r)));
+}
 template <int P>
 __device__ __forceinline__ double diag_at(const KronGrid& g, double a, double b, int i, int j,
                                           int k) {
   constexpr int W = 2 * P + 1;
-  const double mx = g.M[0][i * W + P], kx = g.K[0][i * W + P];
-  const double my = g.M[1][j * W + P], ky = g.K[1][j * W + P];
-  const double mz = g.M[2][k * W + P], kz = g.K[2][k * W + P];
-  return a * (mx * my * mz) + b * (kx * my * mz + mx * ky * mz + mx * my * kz);
+  const QR c = qr_at<P>(g, a, b, i, j);
+  return __dadd_rn(__dmul_rn(g.M[2][k * W + P], c.q), __dmul_rn(g.K[2][k * W + P], c.r));
 }
 
 __device__ __forceinline__ void tma_load_plane(void* dst, const TensorMap3* map, int x, int y,
@@ -174,6 +192,15 @@ __device__ __forceinline__ void kron_tile(const KronGrid& g, const KronTerms& c,
     sm.cy[0][r][d] = gj < ny ? g.M[1][gj * W + d] : 0.0;
     sm.cy[1][r][d] = gj < ny ? g.K[1][gj * W + d] : 0.0;
   }
+  if constexpr (COMBINE) {  // Jacobi factors of every point of the halo'd tile
+    for (int e = ty * kKronTX + tx; e < RY * RX; e += kThreads) {
+      const int r = e / RX, cc = e % RX, gi = x0 + cc - P, gj = y0 + r - P;
+      QR q{0.0, 0.0};
+      if (gi >= 0 && gi < nx && gj >= 0 && gj < ny) q = qr_at<P>(g, c.a1, c.b1, gi, gj);
+      sm.qr[0][r][cc] = q.q;
+      sm.qr[1][r][cc] = q.r;
+    }
+  }
   if (TMA && leader) {
     for (int s = 0; s < kStages && kb + s < ke; ++s)
       for (int q = 0; q < NIN; ++q) {
@@ -213,12 +240,14 @@ __device__ __forceinline__ void kron_tile(const KronGrid& g, const KronTerms& c,
         __syncthreads();
       }
       if constexpr (COMBINE) {  // v = D^-1 r + beta p_old over the halo'd tile
+        const double mz = g.M[2][kin * W + P], kz = g.K[2][kin * W + P];
         for (int e = ty * kKronTX + tx; e < RY * RX; e += kThreads) {
           const int r = e / RX, cc = e % RX;
           const int gi = x0 + cc - P, gj = y0 + r - P;
+          const QR q{sm.qr[0][r][cc], sm.qr[1][r][cc]};
           double val = 0.0;
-          if (gi >= 0 && gi < nx && gj >= 0 && gj < ny) {
-            const double z = (1.0 / diag_at<P>(g, c.a1, c.b1, gi, gj, kin)) * sm.ring[0][slot[0]][e];
+          if (gi >= 0 && gi < nx && gj >= 0 && gj < ny) {  // zero outside the grid
+            const double z = inv_diag(q, mz, kz) * sm.ring[0][slot[0]][e];
             val = z + beta * sm.ring[1][slot[NIN - 1]][e];
           }
           sm.v[r][cc] = val;
@@ -407,9 +436,11 @@ struct EpiResidual {  // r = b - A x; rr, bb, r.D^-1 r; p_old = 0
   double* p_old;
   double acc[4];
   __device__ void operator()(size_t idx, int i, int j, int k, double y, double) {
+    constexpr int W = 2 * P + 1;
     const double bi = rhs[idx];
     const double ri = bi - y;
-    const double zi = (1.0 / diag_at<P>(*g, a, b, i, j, k)) * ri;
+    const double zi =
+        inv_diag(qr_at<P>(*g, a, b, i, j), g->M[2][k * W + P], g->K[2][k * W + P]) * ri;
     r[idx] = ri;
     p_old[idx] = 0.0;
     acc[0] += ri * ri;
@@ -488,17 +519,25 @@ __global__ void __launch_bounds__(kThreads, 3)
     }
     const double alpha = rz / pAp;
     // B: x, r updates and the two dot products (sparse.cpp:85-94)
+    // (same tile -> CTA map as the sweeps; rows of 32 consecutive points per warp)
     double acc[4] = {0, 0, 0, 0};
-    for (size_t f = gtid; f < n; f += gstride) {
-      const int i = static_cast<int>(f % nx);
-      const int j = static_cast<int>((f / nx) % ny);
-      const int k = static_cast<int>(f / (static_cast<size_t>(nx) * ny));
-      x[f] += alpha * p_new[f];
-      const double ri = w.r[f] - alpha * w.Ap[f];
-      w.r[f] = ri;
-      const double zi = (1.0 / diag_at<P>(g, a, b, i, j, k)) * ri;
-      acc[0] += ri * zi;
-      acc[1] += ri * ri;
+    for (int t = blockIdx.x; t < T.count(); t += gridDim.x) {
+      const int txy = t % (T.ntx * T.nty), zc = t / (T.ntx * T.nty);
+      const int i = (txy % T.ntx) * kKronTX + threadIdx.x;
+      const int j = (txy / T.ntx) * kKronTY + threadIdx.y;
+      if (i >= nx || j >= ny) continue;
+      const QR q = qr_at<P>(g, a, b, i, j);
+      const int k0 = zc * T.zlen, k1 = min(g.n[2], k0 + T.zlen);
+      constexpr int W = 2 * P + 1;
+      for (int k = k0; k < k1; ++k) {
+        const size_t f = (static_cast<size_t>(k) * ny + j) * nx + i;
+        x[f] += alpha * p_new[f];
+        const double ri = w.r[f] - alpha * w.Ap[f];
+        w.r[f] = ri;
+        const double zi = inv_diag(q, g.M[2][k * W + P], g.K[2][k * W + P]) * ri;
+        acc[0] += ri * zi;
+        acc[1] += ri * ri;
+      }
     }
     grid_reduce(grid, acc, w.partials, buf, red, tot);
     beta = tot[0] / rz;
