@@ -529,14 +529,38 @@ __global__ void __launch_bounds__(kThreads, 3)
       const QR q = qr_at<P>(g, a, b, i, j);
       const int k0 = zc * T.zlen, k1 = min(g.n[2], k0 + T.zlen);
       constexpr int W = 2 * P + 1;
-      for (int k = k0; k < k1; ++k) {
-        const size_t f = (static_cast<size_t>(k) * ny + j) * nx + i;
-        x[f] += alpha * p_new[f];
-        const double ri = w.r[f] - alpha * w.Ap[f];
-        w.r[f] = ri;
-        const double zi = inv_diag(q, g.M[2][k * W + P], g.K[2][k * W + P]) * ri;
-        acc[0] += ri * zi;
-        acc[1] += ri * ri;
+      constexpr int U = 4;  // planes in flight per thread (memory-level parallelism)
+      const size_t pl = static_cast<size_t>(nx) * ny;
+      const size_t f0 = (static_cast<size_t>(k0) * ny + j) * nx + i;
+      double* __restrict__ xr = x;
+      double* __restrict__ rr_ = w.r;
+      const double* __restrict__ pr = p_new;
+      const double* __restrict__ apr = w.Ap;
+      for (int k = k0; k < k1; k += U) {
+        double xv[U], pv[U], rv[U], av[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          if (k + u < k1) {
+            const size_t f = f0 + (k - k0 + u) * pl;
+            xv[u] = xr[f];
+            pv[u] = pr[f];
+            rv[u] = rr_[f];
+            av[u] = apr[f];
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          if (k + u < k1) {
+            const size_t f = f0 + (k - k0 + u) * pl;
+            xr[f] = xv[u] + alpha * pv[u];
+            const double ri = rv[u] - alpha * av[u];
+            rr_[f] = ri;
+            const double zi =
+                inv_diag(q, g.M[2][(k + u) * W + P], g.K[2][(k + u) * W + P]) * ri;
+            acc[0] += ri * zi;
+            acc[1] += ri * ri;
+          }
+        }
       }
     }
     grid_reduce(grid, acc, w.partials, buf, red, tot);
