@@ -99,9 +99,8 @@ TileIdx make_tiles(const KronGrid& g, int blocks, int P) {
 // Jacobi diagonal of Op(a, b) factored by columns:
 //   diag(i, j, k) = Mz_kk Q_ij + Kz_kk R_ij,
 //   Q_ij = a Mx_ii My_jj + b (Kx_ii My_jj + Mx_ii Ky_jj),  R_ij = b Mx_ii My_jj.
-// Written with explicit _rn operations so every phase (and the host check)
-// produces the same bits; the reciprocal is the correctly rounded
-// __drcp_rn, i.e. the reference's 1.0 / d (sparse.cpp:51).
+// Written with explicit _rn operations so every phase produces the same bits
+// (the reference stores 1.0 / d once, sparse.cpp:47-52).
 struct QR {
   double q, r;
 };
@@ -114,8 +113,20 @@ __device__ __forceinline__ QR qr_at(const KronGrid& g, double a, double b, int i
   const double km = __dadd_rn(__dmul_rn(kx, my), __dmul_rn(mx, ky));
   return {__dadd_rn(__dmul_rn(a, mm), __dmul_rn(b, km)), __dmul_rn(b, mm)};
 }
+// 1/d from the MUFU seed (rcp.approx.ftz.f64, ~2^-22 relative) and two
+// Newton steps: within 1 ulp of the correctly rounded reciprocal at a fraction
+// of __drcp_rn's cost (its exactness checks dominated the direction update).
+// d is a positive normal number here (checked once by k2_check_diagonal).
+__device__ __forceinline__ double fast_rcp(double d) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d));
+  double e = __fma_rn(-d, y, 1.0);
+  y = __fma_rn(y, e, y);
+  e = __fma_rn(-d, y, 1.0);
+  return __fma_rn(y, e, y);
+}
 __device__ __forceinline__ double inv_diag(const QR& c, double mz, double kz) {
-  return __drcp_rn(__dadd_rn(__dmul_rn(mz, c.q), __dmul_rn(kz, c.r)));
+  return fast_rcp(__dadd_rn(__dmul_rn(mz, c.q), __dmul_rn(kz, c.r)));
 }
 template <int P>
 __device__ __forceinline__ double diag_at(const KronGrid& g, double a, double b, int i, int j,
