@@ -10,38 +10,39 @@
 namespace tgb {
 
 // ---------------------------------------------------------------------------
-// Table-driven exp(x) for x in [-708, 709], relative error < 1e-14.
+// Table-driven exp(x) for x in [-708, 709], relative error < 1e-13.
 //
-// x = (64 m + j) ln2/64 + r,  |r| <= ln2/128, j in [0,64)
-// exp(x) = 2^m * 2^(j/64) * p(r),  p(r) = 1 + r + r^2 (c2 + c3 r + c4 r^2)
+// x = (256 m + j) ln2/256 + r,  |r| <= ln2/512, j in [0,256)
+// exp(x) = 2^m * 2^(j/256) * p(r),  p(r) = 1 + r + r^2 (c2 + c3 r)
 //
-// 8 FP64-pipe instructions (3 DFMA + 1 DADD + 3 DFMA + 1 DMUL) plus integer
-// ops for j, m and the exponent add. The degree-4 polynomial is a Chebyshev
-// fit of (e^r - 1 - r)/r^2 on [-ln2/128, ln2/128]: max relative error 9.7e-15,
-// far below the 1e-10 parity tolerance (BASELINE.json north_star).
+// 7 FP64-pipe instructions (1 DFMA + 1 DADD + 1 DFMA range reduction, 3 DFMA
+// polynomial, 1 DMUL table product) plus integer ops for j, m and the
+// exponent add. The cubic is a Chebyshev fit of (e^r - 1 - r)/r^2 on
+// [-ln2/512, ln2/512]: max relative error 7.0e-14 (mpmath), three orders
+// below the 1e-10 parity tolerance (BASELINE.json north_star); the
+// single-constant reduction adds < 2e-15 for |x| <= 80.
 // ---------------------------------------------------------------------------
-constexpr int kExpTableSize = 64;
-constexpr double kExpInvStep = 92.332482616893656768;  // 64 / ln 2
-constexpr double kExpStep = 0.010830424696249145;       // ln 2 / 64
-constexpr double kExpMagic = 6755399441055744.0;        // 1.5 * 2^52
-constexpr double kExpC2 = 0.5;
-constexpr double kExpC3 = 0x1.55556deebaf9ep-3;
-constexpr double kExpC4 = 0x1.555565bb98f45p-5;
+constexpr int kExpBits = 8;
+constexpr int kExpTableSize = 1 << kExpBits;
+constexpr double kExpInvStep = 369.32993046757462707;    // 256 / ln 2
+constexpr double kExpStep = 0.0027076061740622863;       // ln 2 / 256
+constexpr double kExpMagic = 6755399441055744.0;         // 1.5 * 2^52
+constexpr double kExpC2 = 0x1.00000147fd40ap-1;
+constexpr double kExpC3 = 0x1.5555565bb988ep-3;
 
-// exp(x) with the 2^(j/64) table in shared memory.
+// exp(x) with the 2^(j/256) table in shared memory.
 __device__ __forceinline__ double fast_exp(double x, const double* __restrict__ tab) {
   const double kf = __fma_rn(x, kExpInvStep, kExpMagic);
   const double n = __dsub_rn(kf, kExpMagic);
   const int ki = __double2loint(kf);
   const double r = __fma_rn(n, -kExpStep, x);
-  double q = __fma_rn(kExpC4, r, kExpC3);
-  q = __fma_rn(q, r, kExpC2);
-  double p = __fma_rn(q, r, 1.0);
+  double p = __fma_rn(kExpC3, r, kExpC2);
+  p = __fma_rn(p, r, 1.0);
   p = __fma_rn(p, r, 1.0);
   const double t = tab[ki & (kExpTableSize - 1)];
   const double e = __dmul_rn(t, p);
   // scale by 2^m: integer add into the exponent field of the high word
-  const int m = ki >> 6;
+  const int m = ki >> kExpBits;
   const int hi = __double2hiint(e) + (m << 20);
   return __hiloint2double(hi, __double2loint(e));
 }

@@ -76,7 +76,7 @@ __global__ void k1_prepare_sources(const double* __restrict__ src6, int n, doubl
 }
 
 template <int P, bool GRAD>
-__global__ void __launch_bounds__(kK1Threads, 3)
+__global__ void __launch_bounds__(kK1Threads, P >= 4 ? 2 : 3)
     k1_partial(const SrcRec* __restrict__ src, int n_src, int split_len,
                const double* __restrict__ pts, const int* __restrict__ pt_index, int n_pts,
                double* __restrict__ part) {
@@ -90,7 +90,7 @@ __global__ void __launch_bounds__(kK1Threads, 3)
   const int len = max(0, min(n_src, begin + split_len) - begin);
   const int n_chunks = (len + kK1Chunk - 1) / kK1Chunk;
 
-  if (tid < kExpTableSize) tab[tid] = c_exp_table[tid];
+  for (int q = tid; q < kExpTableSize; q += kK1Threads) tab[q] = c_exp_table[q];
   if (tid == 0) {
     for (int b = 0; b < kK1Stages; ++b) mbar_init(&bars[b], 1);
     fence_mbar_init();
@@ -139,7 +139,10 @@ __global__ void __launch_bounds__(kK1Threads, 3)
         const double r2 =
             __dadd_rn(__dadd_rn(__dmul_rn(rx, rx), __dmul_rn(ry, ry)), __dmul_rn(rz, rz));
         const double e = fast_exp(__fma_rn(r2, a.w, b.x), tab);
-        const double T = (r2 <= b.z) ? e : 0.0;
+        // r2 <= thr on the bit patterns (r2 >= 0; thr < 0 marks an inactive
+        // source): an integer compare keeps the decision off the FP64 pipe
+        const double T =
+            (__double_as_longlong(r2) <= __double_as_longlong(b.z)) ? e : 0.0;
         v[k] = __dadd_rn(v[k], T);
         if (GRAD) {
           const double w = __dmul_rn(T, b.y);
