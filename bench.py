@@ -366,7 +366,8 @@ def run_ours(args):
     k1_mean_ms = prof["k1_ms"] / max(1, prof["k1_launches"])
     pairs_per_launch = prof["k1_pairs"] / max(1, prof["k1_launches"])
     achieved = FLOPS_PER_PAIR * pairs_per_launch / (k1_mean_ms * 1e-3) / 1e12 if k1_mean_ms else None
-    roof = {"kernel": "k1_partial<2,true>", "bound": "fp64", "achieved": achieved,
+    roof = {"kernel": f"k1_partial<{os.environ.get('TG_K1_P', '4')},true>", "bound": "fp64",
+            "achieved": achieved,
             "peak": fp64_peak, "unit": "TFLOP/s",
             "frac": (achieved / fp64_peak) if (achieved and fp64_peak) else None,
             "traffic": None,
