@@ -153,6 +153,11 @@ int tg_sim_theta_step(tg_sim* sim, const double* free_n, const double* g_n, cons
  * proj/include/thermiga/assembly.hpp:56). */
 int tg_sim_operator_apply(tg_sim* sim, const double* x_free, double* y_free);
 
+/* Diagnostics: %globaltimer stamps of CTA 0 at the K2 phase boundaries of the
+ * first 16 CG iterations of the last solve (5 per iteration; recorded only
+ * when TG_K2_TRACE is set in the environment at tg_sim_create). */
+int tg_sim_debug_trace(tg_sim* sim, unsigned long long* out, int n);
+
 /* run_time_loop (proj/src/driver.cpp:105-146) with the state resident on the
  * device: reset = step 0 (free = 0, g_0, F_0); advance = n steps. */
 int tg_sim_reset(tg_sim* sim);

@@ -517,12 +517,24 @@ __global__ void __launch_bounds__(kThreads, 3)
       status = 0;
       break;
     }
+    // optional phase trace of CTA 0 (tools/k2_trace.py)
+    const bool tr = w.trace && it < 16 && blockIdx.x == 0 && threadIdx.x == 0 && threadIdx.y == 0;
+    auto stamp = [&](int k) {
+      if (tr) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        w.trace[it * 5 + k] = t;
+      }
+    };
+    stamp(0);
     // A': p_new = D^-1 r + beta p_old, Ap = A p_new
     EpiDirection e1{p_new, w.Ap, {0, 0, 0, 0}};
     Inputs<2> in{{w.r, p_old}, {&maps.r, m_old}};
     for (int t = blockIdx.x; t < T.count(); t += gridDim.x)
       kron_tile<P, 2, 1, true, TMA>(g, c, in, beta, T, t, sm, seq, e1);
+    stamp(1);
     grid_reduce(grid, e1.acc, w.partials, buf, red, tot);
+    stamp(2);
     const double pAp = tot[0];
     if (!(pAp > 0.0)) {
       status = 4;
@@ -574,7 +586,9 @@ __global__ void __launch_bounds__(kThreads, 3)
         }
       }
     }
+    stamp(3);
     grid_reduce(grid, acc, w.partials, buf, red, tot);
+    stamp(4);
     beta = tot[0] / rz;
     rz = tot[0];
     rr = tot[1];

@@ -64,6 +64,7 @@ struct PcgWork {
   double* Ap;
   double* partials;  // >= 8 * max_blocks
   PcgStatus* status;
+  unsigned long long* trace;  // optional: per-phase %globaltimer stamps of CTA 0
 };
 
 // TMA descriptors of the vectors the PCG kernel streams (x, r, pA, pB), all

@@ -262,6 +262,8 @@ void Sim::setup_device(int device) {
   d_T.ensure(n_full);
   d_gfull.ensure(n_full);
   d_status.ensure(1);
+  d_trace.ensure(80);
+  trace_on = std::getenv("TG_K2_TRACE") != nullptr;
   TG_CUDA(cudaMemsetAsync(d_gfull.p, 0, sizeof(double) * n_full, s));
   TG_CUDA(cudaMemsetAsync(d_status.p, 0, sizeof(PcgStatus), s));
 
@@ -395,7 +397,8 @@ PcgStatus Sim::theta_step_device(double tol, int max_iter) {
     k2_theta_rhs(gfull, coefB[0], coefB[1], -coefA[0], -coefA[1], ra, rhs_tma ? &map_T : nullptr,
                  rhs_tma ? &map_g : nullptr, ctx->sm_count, s);
     ctx->timer.launches += 2;
-    const PcgWork w{d_r.p, d_p.p, d_p2.p, d_Ap.p, d_partials.p, d_status.p};
+    const PcgWork w{d_r.p, d_p.p, d_p2.p, d_Ap.p, d_partials.p, d_status.p,
+                    trace_on ? d_trace.p : nullptr};
     ctx->timer.timed(2, s, [&] {
       k2_pcg_solve(gfree, coefA[0], coefA[1], d_rhs.p, d_x.p, w, maps, tol, max_iter,
                    pcg_blocks, s);

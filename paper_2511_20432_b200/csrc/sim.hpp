@@ -81,6 +81,8 @@ class Sim {
   TensorMap3 map_T{}, map_g{};
   bool rhs_tma = false;
   DevBuf<PcgStatus> d_status;
+  DevBuf<unsigned long long> d_trace;  // K2 phase stamps (TG_K2_TRACE)
+  bool trace_on = false;
   PcgStatus* h_status = nullptr;
   int* h_fine = nullptr;
   int pcg_blocks = 1;

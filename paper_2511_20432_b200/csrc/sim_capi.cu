@@ -216,6 +216,13 @@ int tg_sim_state(tg_sim* s, int* step, double* time, double* free_out, double* g
   });
 }
 
+int tg_sim_debug_trace(tg_sim* s, unsigned long long* out, int n) {
+  return sim_guard(s, [&](Sim& m) {
+    TG_CUDA(cudaMemcpy(out, m.d_trace.p, sizeof(unsigned long long) * std::min(n, 80),
+                       cudaMemcpyDeviceToHost));
+  });
+}
+
 int tg_sim_operator_apply(tg_sim* s, const double* x_free, double* y_free) {
   return sim_guard(s, [&](Sim& m) {
     cudaStream_t st = m.ctx->stream;
