@@ -64,36 +64,36 @@ struct KSmem {
   double v[Dims<P>::RY][Dims<P>::RX];
   double u1[NPASS][2][Dims<P>::RY][kKronTX];
   double u2[NPASS][2][Dims<P>::RY][kKronTX];
-  double cx[2][kKronTX][Dims<P>::W];
-  double cy[2][kKronTY][Dims<P>::W];
   double qr[2][Dims<P>::RY][Dims<P>::RX];  // diagonal factors Q, R of the halo'd tile
   uint64_t bar[NIN][kStages];
 };
 
+// Work split: the grid is ntx x nty columns (32 x 8 control points each) of
+// nz planes. The column-planes, linearized column by column, are cut into
+// `blocks` equal contiguous ranges; a CTA sweeps its range as 1-2 column
+// segments (each costs P halo planes per side). Equal shares whatever the
+// column count (a static map keeps the reductions deterministic).
 struct TileIdx {
-  int ntx, nty, nzc, zlen;
-  __device__ __host__ int count() const { return ntx * nty * nzc; }
+  int ntx, nty, nz;
 };
-
-// Tile layout for `blocks` co-resident CTAs; with a static tile -> CTA map
-// (deterministic reductions) the cost is ceil(tiles / blocks) * (zlen + 2P).
-TileIdx make_tiles(const KronGrid& g, int blocks, int P) {
-  TileIdx best{};
-  double best_cost = 1e300;
-  const int ntx = (g.n[0] + kKronTX - 1) / kKronTX;
-  const int nty = (g.n[1] + kKronTY - 1) / kKronTY;
-  const int cap = std::max(1, g.n[2] / 4);  // >= 4 planes per chunk
-  for (int nzc = 1; nzc <= std::min(cap, 16); ++nzc) {
-    TileIdx t{ntx, nty, 0, (g.n[2] + nzc - 1) / nzc};
-    t.nzc = (g.n[2] + t.zlen - 1) / t.zlen;
-    const int rounds = (t.count() + blocks - 1) / blocks;
-    const double cost = static_cast<double>(rounds) * (t.zlen + 2 * P) + 1e-9 * t.count();
-    if (cost < best_cost) {
-      best_cost = cost;
-      best = t;
-    }
+struct Seg {
+  int x0, y0, k0, k1;
+};
+inline TileIdx make_tiles(const KronGrid& g) {
+  return {(g.n[0] + kKronTX - 1) / kKronTX, (g.n[1] + kKronTY - 1) / kKronTY, g.n[2]};
+}
+template <class F>
+__device__ __forceinline__ void for_segments(const TileIdx& T, int blocks, int b, F&& fn) {
+  const long total = static_cast<long>(T.ntx) * T.nty * T.nz;
+  long s = total * b / blocks;
+  const long e = total * (b + 1) / blocks;
+  while (s < e) {
+    const int col = static_cast<int>(s / T.nz);
+    const int k0 = static_cast<int>(s % T.nz);
+    const int k1 = static_cast<int>(min(static_cast<long>(T.nz), k0 + (e - s)));
+    fn(Seg{(col % T.ntx) * kKronTX, (col / T.ntx) * kKronTY, k0, k1});
+    s += k1 - k0;
   }
-  return best;
 }
 
 // Jacobi diagonal of Op(a, b) factored by columns:
@@ -171,37 +171,34 @@ __device__ __forceinline__ void init_bars(KSmem<P, NIN, NPASS>& sm) {
   __syncthreads();
 }
 
-// Sweep one tile. For every output point (i, j, k) call
+// Sweep one column segment. For every output point (i, j, k) call
 // epi(flat, i, j, k, y, p_own) where y = sum over passes of Op(a_q, b_q) in_q
 // (COMBINE: one pass over v = D^-1 in0 + beta in1; p_own = v at the point).
 // The shared layout SM may hold more input rings than this sweep uses;
 // seqs[q] counts the planes ring q has delivered so far (mbarrier phases).
 template <int P, int NIN, int NPASS, bool COMBINE, bool TMA, class SM, class Epi>
 __device__ __forceinline__ void kron_tile(const KronGrid& g, const KronTerms& c,
-                                          const Inputs<NIN>& in, double beta, const TileIdx& T,
-                                          int tile, SM& sm, int* seqs, Epi& epi) {
+                                          const Inputs<NIN>& in, double beta, const Seg& sg,
+                                          SM& sm, int* seqs, Epi& epi) {
   constexpr int W = Dims<P>::W, RY = Dims<P>::RY, RX = Dims<P>::RX;
   const int tx = threadIdx.x, ty = threadIdx.y;
   const bool leader = tx == 0 && ty == 0;
-  const int txy = tile % (T.ntx * T.nty);
-  const int zc = tile / (T.ntx * T.nty);
-  const int x0 = (txy % T.ntx) * kKronTX, y0 = (txy / T.ntx) * kKronTY;
-  const int k0 = zc * T.zlen, k1 = min(g.n[2], k0 + T.zlen);
+  const int x0 = sg.x0, y0 = sg.y0, k0 = sg.k0, k1 = sg.k1;
   const int nx = g.n[0], ny = g.n[1], nz = g.n[2];
   const int i = x0 + tx, j = y0 + ty;
   const int kb = max(0, k0 - P), ke = min(nz, k1 + P);
   constexpr uint32_t kPlaneBytes = RY * RX * 8;
 
-  __syncthreads();  // the previous tile's readers of cx / cy / ring are done
-  for (int q = ty * kKronTX + tx; q < kKronTX * W; q += kThreads) {
-    const int r = q / W, d = q % W, gi = x0 + r;
-    sm.cx[0][r][d] = gi < nx ? g.M[0][gi * W + d] : 0.0;
-    sm.cx[1][r][d] = gi < nx ? g.K[0][gi * W + d] : 0.0;
-  }
-  for (int q = ty * kKronTX + tx; q < kKronTY * W; q += kThreads) {
-    const int r = q / W, d = q % W, gj = y0 + r;
-    sm.cy[0][r][d] = gj < ny ? g.M[1][gj * W + d] : 0.0;
-    sm.cy[1][r][d] = gj < ny ? g.K[1][gj * W + d] : 0.0;
+  __syncthreads();  // the previous tile's readers of the ring / qr tables are done
+  // this thread's x and y rows of the 1D factors, in registers: the sweep is
+  // shared-memory-bandwidth bound, so coefficients must not come from smem
+  double mx[W], kx[W], my[W], ky[W];
+#pragma unroll
+  for (int d = 0; d < W; ++d) {
+    mx[d] = i < nx ? g.M[0][i * W + d] : 0.0;
+    kx[d] = i < nx ? g.K[0][i * W + d] : 0.0;
+    my[d] = j < ny ? g.M[1][j * W + d] : 0.0;
+    ky[d] = j < ny ? g.K[1][j * W + d] : 0.0;
   }
   if constexpr (COMBINE) {  // Jacobi factors of every point of the halo'd tile
     for (int e = ty * kKronTX + tx; e < RY * RX; e += kThreads) {
@@ -275,8 +272,8 @@ __device__ __forceinline__ void kron_tile(const KronGrid& g, const KronTerms& c,
 #pragma unroll
           for (int d = 0; d < W; ++d) {
             const double vv = src[r * RX + tx + d];
-            a1 = fma(sm.cx[0][tx][d], vv, a1);
-            a2 = fma(sm.cx[1][tx][d], vv, a2);
+            a1 = fma(mx[d], vv, a1);
+            a2 = fma(kx[d], vv, a2);
           }
           sm.u1[q][kin & 1][r][tx] = a1;
           sm.u2[q][kin & 1][r][tx] = a2;
@@ -298,10 +295,9 @@ __device__ __forceinline__ void kron_tile(const KronGrid& g, const KronTerms& c,
 #pragma unroll
         for (int d = 0; d < W; ++d) {
           const double p1 = sm.u1[q][kin & 1][ty + d][tx];
-          const double my = sm.cy[0][ty][d];
-          w1 = fma(my, p1, w1);
-          w2 = fma(my, sm.u2[q][kin & 1][ty + d][tx], w2);
-          w3 = fma(sm.cy[1][ty][d], p1, w3);
+          w1 = fma(my[d], p1, w1);
+          w2 = fma(my[d], sm.u2[q][kin & 1][ty + d][tx], w2);
+          w3 = fma(ky[d], p1, w3);
         }
         const double a = q == 0 ? c.a1 : c.a2, b = q == 0 ? c.b1 : c.b2;
         s1 = fma(a, w1, fma(b, w2 + w3, s1));
@@ -348,8 +344,9 @@ __global__ void __launch_bounds__(kThreads) k2_apply_kernel(KronGrid g, KronTerm
   EpiStore epi{y};
   Inputs<1> in{{v}, {nullptr}};
   int seq[1] = {0};
-  for (int t = blockIdx.x; t < T.count(); t += gridDim.x)
-    kron_tile<P, 1, 1, false, false>(g, c, in, 0.0, T, t, sm, seq, epi);
+  for_segments(T, gridDim.x, blockIdx.x, [&](const Seg& sg) {
+    kron_tile<P, 1, 1, false, false>(g, c, in, 0.0, sg, sm, seq, epi);
+  });
 }
 
 struct EpiRhs {
@@ -380,8 +377,9 @@ __global__ void __launch_bounds__(kThreads) k2_rhs_kernel(KronGrid g, KronTerms 
   epi.nfree[args.bottom_axis] -= 1;
   Inputs<2> in{{args.T_full, args.g_full}, {&maps.T, &maps.g}};
   int seq[2] = {0, 0};
-  for (int t = blockIdx.x; t < T.count(); t += gridDim.x)
-    kron_tile<P, 2, 2, false, TMA>(g, c, in, 0.0, T, t, sm, seq, epi);
+  for_segments(T, gridDim.x, blockIdx.x, [&](const Seg& sg) {
+    kron_tile<P, 2, 2, false, TMA>(g, c, in, 0.0, sg, sm, seq, epi);
+  });
 }
 
 template <int P>
@@ -472,7 +470,7 @@ struct EpiDirection {  // p_new (own point), Ap, p.Ap
 };
 
 template <int P, bool TMA>
-__global__ void __launch_bounds__(kThreads, 3)
+__global__ void __launch_bounds__(kThreads, 2)
     k2_pcg_kernel(KronGrid g, double a, double b, const double* rhs, double* x, PcgWork w,
                   double tol, int max_iter, TileIdx T, const __grid_constant__ PcgMaps maps) {
   cg::grid_group grid = cg::this_grid();
@@ -493,8 +491,9 @@ __global__ void __launch_bounds__(kThreads, 3)
   {
     EpiResidual<P> e0{&g, a, b, rhs, w.r, w.pA, {0, 0, 0, 0}};
     Inputs<1> in1{{x}, {&maps.x}};  // ring 0 of the two-ring layout
-    for (int t = blockIdx.x; t < T.count(); t += gridDim.x)
-      kron_tile<P, 1, 1, false, TMA>(g, c, in1, 0.0, T, t, sm, seq, e0);
+    for_segments(T, gridDim.x, blockIdx.x, [&](const Seg& sg) {
+      kron_tile<P, 1, 1, false, TMA>(g, c, in1, 0.0, sg, sm, seq, e0);
+    });
     grid_reduce(grid, e0.acc, w.partials, buf, red, tot);
   }
   double rr = tot[0], rz = tot[2];
@@ -530,8 +529,9 @@ __global__ void __launch_bounds__(kThreads, 3)
     // A': p_new = D^-1 r + beta p_old, Ap = A p_new
     EpiDirection e1{p_new, w.Ap, {0, 0, 0, 0}};
     Inputs<2> in{{w.r, p_old}, {&maps.r, m_old}};
-    for (int t = blockIdx.x; t < T.count(); t += gridDim.x)
-      kron_tile<P, 2, 1, true, TMA>(g, c, in, beta, T, t, sm, seq, e1);
+    for_segments(T, gridDim.x, blockIdx.x, [&](const Seg& sg) {
+      kron_tile<P, 2, 1, true, TMA>(g, c, in, beta, sg, sm, seq, e1);
+    });
     stamp(1);
     grid_reduce(grid, e1.acc, w.partials, buf, red, tot);
     stamp(2);
@@ -544,13 +544,12 @@ __global__ void __launch_bounds__(kThreads, 3)
     // B: x, r updates and the two dot products (sparse.cpp:85-94)
     // (same tile -> CTA map as the sweeps; rows of 32 consecutive points per warp)
     double acc[4] = {0, 0, 0, 0};
-    for (int t = blockIdx.x; t < T.count(); t += gridDim.x) {
-      const int txy = t % (T.ntx * T.nty), zc = t / (T.ntx * T.nty);
-      const int i = (txy % T.ntx) * kKronTX + threadIdx.x;
-      const int j = (txy / T.ntx) * kKronTY + threadIdx.y;
-      if (i >= nx || j >= ny) continue;
+    for_segments(T, gridDim.x, blockIdx.x, [&](const Seg& sg) {
+      const int i = sg.x0 + threadIdx.x;
+      const int j = sg.y0 + threadIdx.y;
+      if (i >= nx || j >= ny) return;
       const QR q = qr_at<P>(g, a, b, i, j);
-      const int k0 = zc * T.zlen, k1 = min(g.n[2], k0 + T.zlen);
+      const int k0 = sg.k0, k1 = sg.k1;
       constexpr int W = 2 * P + 1;
       constexpr int U = 4;  // planes in flight per thread (memory-level parallelism)
       const size_t pl = static_cast<size_t>(nx) * ny;
@@ -585,7 +584,7 @@ __global__ void __launch_bounds__(kThreads, 3)
           }
         }
       }
-    }
+    });
     stamp(3);
     grid_reduce(grid, acc, w.partials, buf, red, tot);
     stamp(4);
@@ -670,10 +669,17 @@ bool k2_make_map(const KronGrid& g, const double* base, TensorMap3* out) {
     default: throw std::invalid_argument("kronecker path supports degree 1..3"); \
   }
 
+// CTAs for a sweep: at most `max_blocks`, and >= ~16 planes per CTA so the
+// 2P halo planes of a segment stay a small overhead.
+static int seg_blocks(const TileIdx& T, int max_blocks) {
+  const long total = static_cast<long>(T.ntx) * T.nty * T.nz;
+  return static_cast<int>(std::max(1L, std::min<long>(max_blocks, total / 16)));
+}
+
 void k2_apply(const KronGrid& g, double a, double b, const double* v, double* y, int sm_count,
               cudaStream_t s) {
-  const TileIdx T = make_tiles(g, 3 * sm_count, g.p);
-  const int blocks = std::min(T.count(), 3 * sm_count);
+  const TileIdx T = make_tiles(g);
+  const int blocks = seg_blocks(T, 3 * sm_count);
   TG_KRON_DISPATCH(g.p, {
     const size_t sb = smem_bytes<P>(1, 1);
     allow_smem(k2_apply_kernel<P>, sb);
@@ -686,8 +692,8 @@ void k2_apply(const KronGrid& g, double a, double b, const double* v, double* y,
 void k2_theta_rhs(const KronGrid& full, double a_b, double b_b, double a_a, double b_a,
                   const RhsArgs& args, const TensorMap3* mT, const TensorMap3* mg, int sm_count,
                   cudaStream_t s) {
-  const TileIdx T = make_tiles(full, 2 * sm_count, full.p);
-  const int blocks = std::min(T.count(), 2 * sm_count);
+  const TileIdx T = make_tiles(full);
+  const int blocks = seg_blocks(T, 2 * sm_count);
   RhsMaps maps{};
   const bool tma = mT && mg;
   if (tma) {
@@ -728,8 +734,8 @@ int k2_pcg_max_blocks(int p, int sm_count) {
 void k2_pcg_solve(const KronGrid& g, double a, double b, const double* rhs, double* x,
                   const PcgWork& w, const PcgMaps& maps, double tol, int max_iter, int blocks,
                   cudaStream_t s) {
-  const TileIdx T = make_tiles(g, blocks, g.p);
-  const int nb = std::max(1, std::min(blocks, T.count()));
+  const TileIdx T = make_tiles(g);
+  const int nb = seg_blocks(T, blocks);
   dim3 grid(nb), block(kKronTX, kKronTY);
   KronGrid gg = g;
   PcgWork ww = w;
