@@ -11,21 +11,20 @@
 //   y-pass  w1 = My u1, w2 = My u2, w3 = Ky u1
 //           s1 = a w1 + b (w2 + w3),  s2 = b w1
 //   z-pass  y = Mz s1 + Kz s2            (2p+1-plane register window)
-// A CTA owns a 32 x 8 column of the control grid and marches through a
-// z-range. Halo'd plane tiles arrive by TMA (cp.async.bulk.tensor.3d, zero
-// fill outside the grid) through a 3-stage mbarrier ring, so every vector is
-// read from HBM once and written once per pass; halos come from L2.
+// A CTA owns 32 x 8 columns of the control grid and marches through z.
+// Halo'd plane tiles arrive by TMA (cp.async.bulk.tensor.3d, zero fill
+// outside the grid) through a 3-stage mbarrier ring, so every vector is read
+// from HBM once and written once per pass; the x/y halos come from L2.
 //
 // The PCG solve is one persistent cooperative launch with two grid barriers
 // per iteration:
-//   A'  p_new = D^-1 r + beta p_old  (computed on the loaded tiles, halo too)
-//       Ap = A p_new, pAp            (tile sweep; p_new and Ap written)
-//   B   x += alpha p, r -= alpha Ap, r.D^-1 r, r.r   (streaming pass)
-// The Jacobi diagonal is recomputed from the 1D factors instead of stored.
+//   A'  p_new = z + beta p_old  (on the loaded tiles, halo included)
+//       Ap = A p_new, p.Ap      (tile sweep; p_new and Ap written)
+//   B   x += alpha p, r -= alpha Ap, z = D^-1 r, r.z, r.r   (streaming pass)
 // Dot products are reduced per CTA in a fixed tree and across CTAs in a fixed
 // order (bitwise-deterministic reruns). The algorithm is the reference's:
-// warm start, stop test ||r||/||b|| <= tol before the matvec, b = 0 -> x = 0,
-// failure on pAp <= 0 or after max_iter.
+// inv_diag = 1.0 / d stored once, warm start, stop test ||r||/||b|| <= tol
+// before the matvec, b = 0 -> x = 0, failure on pAp <= 0 or after max_iter.
 #include <cooperative_groups.h>
 #include <cuda.h>
 
@@ -56,17 +55,22 @@ struct Dims {
 };
 
 // NIN loaded vectors; NPASS separate x/y passes (2 for the RHS, whose two
-// inputs carry different (a, b)); COMBINE: one pass over a pointwise
-// combination of the two inputs (the PCG direction update).
+// inputs carry different (a, b)); COMBINE: one pass over v = in0 + beta in1
+// (the PCG direction update). The z band (Mz, Kz rows) of the whole grid
+// follows the struct in dynamic shared memory.
 template <int P, int NIN, int NPASS>
 struct KSmem {
   double ring[NIN][kStages][Dims<P>::BUF];
   double v[Dims<P>::RY][Dims<P>::RX];
   double u1[NPASS][2][Dims<P>::RY][kKronTX];
   double u2[NPASS][2][Dims<P>::RY][kKronTX];
-  double qr[2][Dims<P>::RY][Dims<P>::RX];  // diagonal factors Q, R of the halo'd tile
   uint64_t bar[NIN][kStages];
 };
+
+template <int P, int NIN, int NPASS>
+__host__ __device__ constexpr size_t zband_offset() {
+  return (sizeof(KSmem<P, NIN, NPASS>) + 15) / 16 * 16;
+}
 
 // Work split: the grid is ntx x nty columns (32 x 8 control points each) of
 // nz planes. The column-planes, linearized column by column, are cut into
@@ -96,44 +100,15 @@ __device__ __forceinline__ void for_segments(const TileIdx& T, int blocks, int b
   }
 }
 
-// Jacobi diagonal of Op(a, b) factored by columns:
-//   diag(i, j, k) = Mz_kk Q_ij + Kz_kk R_ij,
-//   Q_ij = a Mx_ii My_jj + b (Kx_ii My_jj + Mx_ii Ky_jj),  R_ij = b Mx_ii My_jj.
-// Written with explicit _rn operations so every phase produces the same bits
-// (the reference stores 1.0 / d once, sparse.cpp:47-52).
-struct QR {
-  double q, r;
-};
-template <int P>
-__device__ __forceinline__ QR qr_at(const KronGrid& g, double a, double b, int i, int j) {
-  constexpr int W = 2 * P + 1;
-  const double mx = g.M[0][i * W + P], kx = g.K[0][i * W + P];
-  const double my = g.M[1][j * W + P], ky = g.K[1][j * W + P];
-  const double mm = __dmul_rn(mx, my);
-  const double km = __dadd_rn(__dmul_rn(kx, my), __dmul_rn(mx, ky));
-  return {__dadd_rn(__dmul_rn(a, mm), __dmul_rn(b, km)), __dmul_rn(b, mm)};
-}
-// 1/d from the MUFU seed (rcp.approx.ftz.f64, ~2^-22 relative) and two
-// Newton steps: within 1 ulp of the correctly rounded reciprocal at a fraction
-// of __drcp_rn's cost (its exactness checks dominated the direction update).
-// d is a positive normal number here (checked once by k2_check_diagonal).
-__device__ __forceinline__ double fast_rcp(double d) {
-  double y;
-  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d));
-  double e = __fma_rn(-d, y, 1.0);
-  y = __fma_rn(y, e, y);
-  e = __fma_rn(-d, y, 1.0);
-  return __fma_rn(y, e, y);
-}
-__device__ __forceinline__ double inv_diag(const QR& c, double mz, double kz) {
-  return fast_rcp(__dadd_rn(__dmul_rn(mz, c.q), __dmul_rn(kz, c.r)));
-}
+// Jacobi diagonal of Op(a, b) at (i, j, k).
 template <int P>
 __device__ __forceinline__ double diag_at(const KronGrid& g, double a, double b, int i, int j,
                                           int k) {
   constexpr int W = 2 * P + 1;
-  const QR c = qr_at<P>(g, a, b, i, j);
-  return __dadd_rn(__dmul_rn(g.M[2][k * W + P], c.q), __dmul_rn(g.K[2][k * W + P], c.r));
+  const double mx = g.M[0][i * W + P], kx = g.K[0][i * W + P];
+  const double my = g.M[1][j * W + P], ky = g.K[1][j * W + P];
+  const double mz = g.M[2][k * W + P], kz = g.K[2][k * W + P];
+  return a * (mx * my * mz) + b * (kx * my * mz + mx * ky * mz + mx * my * kz);
 }
 
 __device__ __forceinline__ void tma_load_plane(void* dst, const TensorMap3* map, int x, int y,
@@ -157,29 +132,32 @@ struct Inputs {
   const TensorMap3* map[NIN];
 };
 
-struct NoPrep {
-  double beta;
-};
-
 template <int P, int NIN, int NPASS>
-__device__ __forceinline__ void init_bars(KSmem<P, NIN, NPASS>& sm) {
-  if (threadIdx.x == 0 && threadIdx.y == 0) {
+__device__ __forceinline__ void init_smem(const KronGrid& g, KSmem<P, NIN, NPASS>& sm,
+                                          double* zb, bool tma) {
+  constexpr int W = 2 * P + 1;
+  const int tid = threadIdx.y * kKronTX + threadIdx.x;
+  if (tma && tid == 0) {
     for (int q = 0; q < NIN; ++q)
       for (int s = 0; s < kStages; ++s) mbar_init(&sm.bar[q][s], 1);
     fence_mbar_init();
+  }
+  for (int e = tid; e < g.n[2] * W; e += kThreads) {  // Mz, Kz rows: z-pass coefficients
+    zb[e] = g.M[2][e];
+    zb[g.n[2] * W + e] = g.K[2][e];
   }
   __syncthreads();
 }
 
 // Sweep one column segment. For every output point (i, j, k) call
 // epi(flat, i, j, k, y, p_own) where y = sum over passes of Op(a_q, b_q) in_q
-// (COMBINE: one pass over v = D^-1 in0 + beta in1; p_own = v at the point).
+// (COMBINE: one pass over v = in0 + beta in1; p_own = v at the point).
 // The shared layout SM may hold more input rings than this sweep uses;
 // seqs[q] counts the planes ring q has delivered so far (mbarrier phases).
 template <int P, int NIN, int NPASS, bool COMBINE, bool TMA, class SM, class Epi>
 __device__ __forceinline__ void kron_tile(const KronGrid& g, const KronTerms& c,
                                           const Inputs<NIN>& in, double beta, const Seg& sg,
-                                          SM& sm, int* seqs, Epi& epi) {
+                                          SM& sm, const double* zb, int* seqs, Epi& epi) {
   constexpr int W = Dims<P>::W, RY = Dims<P>::RY, RX = Dims<P>::RX;
   const int tx = threadIdx.x, ty = threadIdx.y;
   const bool leader = tx == 0 && ty == 0;
@@ -189,9 +167,9 @@ __device__ __forceinline__ void kron_tile(const KronGrid& g, const KronTerms& c,
   const int kb = max(0, k0 - P), ke = min(nz, k1 + P);
   constexpr uint32_t kPlaneBytes = RY * RX * 8;
 
-  __syncthreads();  // the previous tile's readers of the ring / qr tables are done
-  // this thread's x and y rows of the 1D factors, in registers: the sweep is
-  // shared-memory-bandwidth bound, so coefficients must not come from smem
+  __syncthreads();  // the previous segment's readers of the ring are done
+  // this thread's x and y rows of the 1D factors, in registers (the sweep is
+  // shared-memory-bandwidth bound: coefficients must not come from smem)
   double mx[W], kx[W], my[W], ky[W];
 #pragma unroll
   for (int d = 0; d < W; ++d) {
@@ -199,15 +177,6 @@ __device__ __forceinline__ void kron_tile(const KronGrid& g, const KronTerms& c,
     kx[d] = i < nx ? g.K[0][i * W + d] : 0.0;
     my[d] = j < ny ? g.M[1][j * W + d] : 0.0;
     ky[d] = j < ny ? g.K[1][j * W + d] : 0.0;
-  }
-  if constexpr (COMBINE) {  // Jacobi factors of every point of the halo'd tile
-    for (int e = ty * kKronTX + tx; e < RY * RX; e += kThreads) {
-      const int r = e / RX, cc = e % RX, gi = x0 + cc - P, gj = y0 + r - P;
-      QR q{0.0, 0.0};
-      if (gi >= 0 && gi < nx && gj >= 0 && gj < ny) q = qr_at<P>(g, c.a1, c.b1, gi, gj);
-      sm.qr[0][r][cc] = q.q;
-      sm.qr[1][r][cc] = q.r;
-    }
   }
   if (TMA && leader) {
     for (int s = 0; s < kStages && kb + s < ke; ++s)
@@ -247,19 +216,9 @@ __device__ __forceinline__ void kron_tile(const KronGrid& g, const KronTerms& c,
           }
         __syncthreads();
       }
-      if constexpr (COMBINE) {  // v = D^-1 r + beta p_old over the halo'd tile
-        const double mz = g.M[2][kin * W + P], kz = g.K[2][kin * W + P];
-        for (int e = ty * kKronTX + tx; e < RY * RX; e += kThreads) {
-          const int r = e / RX, cc = e % RX;
-          const int gi = x0 + cc - P, gj = y0 + r - P;
-          const QR q{sm.qr[0][r][cc], sm.qr[1][r][cc]};
-          double val = 0.0;
-          if (gi >= 0 && gi < nx && gj >= 0 && gj < ny) {  // zero outside the grid
-            const double z = inv_diag(q, mz, kz) * sm.ring[0][slot[0]][e];
-            val = z + beta * sm.ring[1][slot[NIN - 1]][e];
-          }
-          sm.v[r][cc] = val;
-        }
+      if constexpr (COMBINE) {  // v = z + beta p_old over the halo'd tile
+        for (int e = ty * kKronTX + tx; e < RY * RX; e += kThreads)
+          sm.v[0][e] = fma(beta, sm.ring[1][slot[NIN - 1]][e], sm.ring[0][slot[0]][e]);
         __syncthreads();
         po = sm.v[ty + P][tx + P];
       }
@@ -315,8 +274,8 @@ __device__ __forceinline__ void kron_tile(const KronGrid& g, const KronTerms& c,
     pown[W - 1] = po;
     const int k = kin - P;
     if (k >= k0 && i < nx && j < ny) {
-      const double* mz = g.M[2] + k * W;
-      const double* kz = g.K[2] + k * W;
+      const double* mz = zb + k * W;
+      const double* kz = zb + nz * W + k * W;
       double y = 0.0;
 #pragma unroll
       for (int d = 0; d < W; ++d) y = fma(mz[d], win1[d], fma(kz[d], win2[d], y));
@@ -341,11 +300,13 @@ __global__ void __launch_bounds__(kThreads) k2_apply_kernel(KronGrid g, KronTerm
                                                             TileIdx T) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   auto& sm = *reinterpret_cast<KSmem<P, 1, 1>*>(smem_raw);
+  double* zb = reinterpret_cast<double*>(smem_raw + zband_offset<P, 1, 1>());
+  init_smem(g, sm, zb, false);
   EpiStore epi{y};
   Inputs<1> in{{v}, {nullptr}};
   int seq[1] = {0};
   for_segments(T, gridDim.x, blockIdx.x, [&](const Seg& sg) {
-    kron_tile<P, 1, 1, false, false>(g, c, in, 0.0, sg, sm, seq, epi);
+    kron_tile<P, 1, 1, false, false>(g, c, in, 0.0, sg, sm, zb, seq, epi);
   });
 }
 
@@ -372,25 +333,29 @@ __global__ void __launch_bounds__(kThreads) k2_rhs_kernel(KronGrid g, KronTerms 
                                                           const __grid_constant__ RhsMaps maps) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   auto& sm = *reinterpret_cast<KSmem<P, 2, 2>*>(smem_raw);
-  if (TMA) init_bars(sm);
+  double* zb = reinterpret_cast<double*>(smem_raw + zband_offset<P, 2, 2>());
+  init_smem(g, sm, zb, TMA);
   EpiRhs epi{args, {g.n[0], g.n[1], g.n[2]}};
   epi.nfree[args.bottom_axis] -= 1;
   Inputs<2> in{{args.T_full, args.g_full}, {&maps.T, &maps.g}};
   int seq[2] = {0, 0};
   for_segments(T, gridDim.x, blockIdx.x, [&](const Seg& sg) {
-    kron_tile<P, 2, 2, false, TMA>(g, c, in, 0.0, sg, sm, seq, epi);
+    kron_tile<P, 2, 2, false, TMA>(g, c, in, 0.0, sg, sm, zb, seq, epi);
   });
 }
 
 template <int P>
-__global__ void k2_diag_check_kernel(KronGrid g, double a, double b, PcgStatus* st) {
+__global__ void k2_inv_diag_kernel(KronGrid g, double a, double b, double* inv,
+                                   PcgStatus* st) {
   const size_t n = static_cast<size_t>(g.n[0]) * g.n[1] * g.n[2];
   for (size_t f = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; f < n;
        f += static_cast<size_t>(gridDim.x) * blockDim.x) {
     const int i = static_cast<int>(f % g.n[0]);
     const int j = static_cast<int>((f / g.n[0]) % g.n[1]);
     const int k = static_cast<int>(f / (static_cast<size_t>(g.n[0]) * g.n[1]));
-    if (!(diag_at<P>(g, a, b, i, j, k) > 0.0)) st->status = 2;
+    const double d = diag_at<P>(g, a, b, i, j, k);
+    if (!(d > 0.0)) st->status = 2;  // sparse.cpp:50
+    inv[f] = 1.0 / d;
   }
 }
 
@@ -436,21 +401,19 @@ __device__ __forceinline__ void grid_reduce(cg::grid_group& grid, const double (
   buf ^= 1;
 }
 
-template <int P>
-struct EpiResidual {  // r = b - A x; rr, bb, r.D^-1 r; p_old = 0
-  const KronGrid* g;
-  double a, b;
+struct EpiResidual {  // r = b - A x; z = D^-1 r; p_old = 0; rr, bb, rz
   const double* rhs;
+  const double* inv;
   double* r;
+  double* z;
   double* p_old;
   double acc[4];
-  __device__ void operator()(size_t idx, int i, int j, int k, double y, double) {
-    constexpr int W = 2 * P + 1;
+  __device__ void operator()(size_t idx, int, int, int, double y, double) {
     const double bi = rhs[idx];
     const double ri = bi - y;
-    const double zi =
-        inv_diag(qr_at<P>(*g, a, b, i, j), g->M[2][k * W + P], g->K[2][k * W + P]) * ri;
+    const double zi = inv[idx] * ri;
     r[idx] = ri;
+    z[idx] = zi;
     p_old[idx] = 0.0;
     acc[0] += ri * ri;
     acc[1] += bi * bi;
@@ -476,30 +439,32 @@ __global__ void __launch_bounds__(kThreads, 2)
   cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(128) unsigned char smem_raw[];
   auto& sm = *reinterpret_cast<KSmem<P, 2, 1>*>(smem_raw);
+  double* zb = reinterpret_cast<double*>(smem_raw + zband_offset<P, 2, 1>());
   __shared__ double red[64];
-  if (TMA) init_bars(sm);
+  init_smem(g, sm, zb, TMA);
   const KronTerms c{a, b, 0.0, 0.0};
   const int nx = g.n[0], ny = g.n[1];
-  const size_t n = static_cast<size_t>(nx) * ny * g.n[2];
-  const size_t gtid = static_cast<size_t>(blockIdx.x) * kThreads + threadIdx.y * kKronTX + threadIdx.x;
-  const size_t gstride = static_cast<size_t>(gridDim.x) * kThreads;
   int buf = 0;
   int seq[2] = {0, 0};
   double tot[4];
 
-  // r = b - A x (sparse.cpp:61-70); the first direction update sees p_old = 0
+  // r = b - A x, z = D^-1 r (sparse.cpp:61-69); the first direction update
+  // sees p_old = 0, i.e. p = z
   {
-    EpiResidual<P> e0{&g, a, b, rhs, w.r, w.pA, {0, 0, 0, 0}};
+    EpiResidual e0{rhs, w.inv_diag, w.r, w.z, w.pA, {0, 0, 0, 0}};
     Inputs<1> in1{{x}, {&maps.x}};  // ring 0 of the two-ring layout
     for_segments(T, gridDim.x, blockIdx.x, [&](const Seg& sg) {
-      kron_tile<P, 1, 1, false, TMA>(g, c, in1, 0.0, sg, sm, seq, e0);
+      kron_tile<P, 1, 1, false, TMA>(g, c, in1, 0.0, sg, sm, zb, seq, e0);
     });
     grid_reduce(grid, e0.acc, w.partials, buf, red, tot);
   }
   double rr = tot[0], rz = tot[2];
   const double bnorm = sqrt(tot[1]);
   if (bnorm == 0.0) {  // sparse.cpp:57-60: zero rhs resets even a warm start
-    for (size_t f = gtid; f < n; f += gstride) x[f] = 0.0;
+    const size_t n = static_cast<size_t>(nx) * ny * g.n[2];
+    for (size_t f = static_cast<size_t>(blockIdx.x) * kThreads + threadIdx.y * kKronTX + threadIdx.x;
+         f < n; f += static_cast<size_t>(gridDim.x) * kThreads)
+      x[f] = 0.0;
     if (blockIdx.x == 0 && threadIdx.x == 0 && threadIdx.y == 0)
       *w.status = PcgStatus{0, 0, 0.0, 0.0};
     return;
@@ -526,11 +491,11 @@ __global__ void __launch_bounds__(kThreads, 2)
       }
     };
     stamp(0);
-    // A': p_new = D^-1 r + beta p_old, Ap = A p_new
+    // A': p_new = z + beta p_old (sparse.cpp:96), Ap = A p_new (sparse.cpp:81)
     EpiDirection e1{p_new, w.Ap, {0, 0, 0, 0}};
-    Inputs<2> in{{w.r, p_old}, {&maps.r, m_old}};
+    Inputs<2> in{{w.z, p_old}, {&maps.z, m_old}};
     for_segments(T, gridDim.x, blockIdx.x, [&](const Seg& sg) {
-      kron_tile<P, 2, 1, true, TMA>(g, c, in, beta, sg, sm, seq, e1);
+      kron_tile<P, 2, 1, true, TMA>(g, c, in, beta, sg, sm, zb, seq, e1);
     });
     stamp(1);
     grid_reduce(grid, e1.acc, w.partials, buf, red, tot);
@@ -541,44 +506,45 @@ __global__ void __launch_bounds__(kThreads, 2)
       break;
     }
     const double alpha = rz / pAp;
-    // B: x, r updates and the two dot products (sparse.cpp:85-94)
-    // (same tile -> CTA map as the sweeps; rows of 32 consecutive points per warp)
+    // B: x, r, z updates and the two dot products (sparse.cpp:85-94), on the
+    // same segment map; rows of 32 consecutive points per warp, U planes of
+    // loads in flight per thread
     double acc[4] = {0, 0, 0, 0};
     for_segments(T, gridDim.x, blockIdx.x, [&](const Seg& sg) {
       const int i = sg.x0 + threadIdx.x;
       const int j = sg.y0 + threadIdx.y;
       if (i >= nx || j >= ny) return;
-      const QR q = qr_at<P>(g, a, b, i, j);
-      const int k0 = sg.k0, k1 = sg.k1;
-      constexpr int W = 2 * P + 1;
-      constexpr int U = 4;  // planes in flight per thread (memory-level parallelism)
+      constexpr int U = 4;
       const size_t pl = static_cast<size_t>(nx) * ny;
-      const size_t f0 = (static_cast<size_t>(k0) * ny + j) * nx + i;
+      const size_t f0 = (static_cast<size_t>(sg.k0) * ny + j) * nx + i;
       double* __restrict__ xr = x;
       double* __restrict__ rr_ = w.r;
+      double* __restrict__ zr = w.z;
       const double* __restrict__ pr = p_new;
       const double* __restrict__ apr = w.Ap;
-      for (int k = k0; k < k1; k += U) {
-        double xv[U], pv[U], rv[U], av[U];
+      const double* __restrict__ ir = w.inv_diag;
+      for (int k = sg.k0; k < sg.k1; k += U) {
+        double xv[U], pv[U], rv[U], av[U], iv[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-          if (k + u < k1) {
-            const size_t f = f0 + (k - k0 + u) * pl;
+          if (k + u < sg.k1) {
+            const size_t f = f0 + (k - sg.k0 + u) * pl;
             xv[u] = xr[f];
             pv[u] = pr[f];
             rv[u] = rr_[f];
             av[u] = apr[f];
+            iv[u] = ir[f];
           }
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-          if (k + u < k1) {
-            const size_t f = f0 + (k - k0 + u) * pl;
+          if (k + u < sg.k1) {
+            const size_t f = f0 + (k - sg.k0 + u) * pl;
             xr[f] = xv[u] + alpha * pv[u];
             const double ri = rv[u] - alpha * av[u];
+            const double zi = iv[u] * ri;
             rr_[f] = ri;
-            const double zi =
-                inv_diag(q, g.M[2][(k + u) * W + P], g.K[2][(k + u) * W + P]) * ri;
+            zr[f] = zi;
             acc[0] += ri * zi;
             acc[1] += ri * ri;
           }
@@ -625,16 +591,24 @@ EncodeFn encoder() {
 }
 
 template <int P>
-size_t smem_bytes(int nin, int npass) {
-  if (nin == 1) return sizeof(KSmem<P, 1, 1>);
-  if (npass == 2) return sizeof(KSmem<P, 2, 2>);
-  return sizeof(KSmem<P, 2, 1>);
+size_t smem_bytes(int nin, int npass, int nz) {
+  const size_t band = 2 * static_cast<size_t>(nz) * (2 * P + 1) * sizeof(double);
+  if (nin == 1) return zband_offset<P, 1, 1>() + band;
+  if (npass == 2) return zband_offset<P, 2, 2>() + band;
+  return zband_offset<P, 2, 1>() + band;
 }
 
 template <typename K>
 void allow_smem(K kernel, size_t bytes) {
   TG_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                static_cast<int>(bytes)));
+}
+
+// CTAs for a sweep: at most `max_blocks`, and >= ~6 planes per CTA (small
+// grids are latency-bound: more CTAs beat the 2P halo-plane overhead).
+int seg_blocks(const TileIdx& T, int max_blocks) {
+  const long total = static_cast<long>(T.ntx) * T.nty * T.nz;
+  return static_cast<int>(std::max(1L, std::min<long>(max_blocks, total / 6)));
 }
 
 }  // namespace
@@ -669,19 +643,12 @@ bool k2_make_map(const KronGrid& g, const double* base, TensorMap3* out) {
     default: throw std::invalid_argument("kronecker path supports degree 1..3"); \
   }
 
-// CTAs for a sweep: at most `max_blocks`, and >= ~16 planes per CTA so the
-// 2P halo planes of a segment stay a small overhead.
-static int seg_blocks(const TileIdx& T, int max_blocks) {
-  const long total = static_cast<long>(T.ntx) * T.nty * T.nz;
-  return static_cast<int>(std::max(1L, std::min<long>(max_blocks, total / 16)));
-}
-
 void k2_apply(const KronGrid& g, double a, double b, const double* v, double* y, int sm_count,
               cudaStream_t s) {
   const TileIdx T = make_tiles(g);
   const int blocks = seg_blocks(T, 3 * sm_count);
   TG_KRON_DISPATCH(g.p, {
-    const size_t sb = smem_bytes<P>(1, 1);
+    const size_t sb = smem_bytes<P>(1, 1, g.n[2]);
     allow_smem(k2_apply_kernel<P>, sb);
     k2_apply_kernel<P><<<blocks, dim3(kKronTX, kKronTY), sb, s>>>(g, KronTerms{a, b, 0.0, 0.0},
                                                                   v, y, T);
@@ -702,7 +669,7 @@ void k2_theta_rhs(const KronGrid& full, double a_b, double b_b, double a_a, doub
   }
   const KronTerms c{a_b, b_b, a_a, b_a};
   TG_KRON_DISPATCH(full.p, {
-    const size_t sb = smem_bytes<P>(2, 2);
+    const size_t sb = smem_bytes<P>(2, 2, full.n[2]);
     if (tma) {
       allow_smem(k2_rhs_kernel<P, true>, sb);
       k2_rhs_kernel<P, true><<<blocks, dim3(kKronTX, kKronTY), sb, s>>>(full, c, args, T, maps);
@@ -714,15 +681,16 @@ void k2_theta_rhs(const KronGrid& full, double a_b, double b_b, double a_a, doub
   TG_CUDA(cudaGetLastError());
 }
 
-void k2_check_diagonal(const KronGrid& g, double a, double b, PcgStatus* status, cudaStream_t s) {
-  TG_KRON_DISPATCH(g.p, k2_diag_check_kernel<P><<<256, 256, 0, s>>>(g, a, b, status));
+void k2_inverse_diagonal(const KronGrid& g, double a, double b, double* inv_diag,
+                         PcgStatus* status, cudaStream_t s) {
+  TG_KRON_DISPATCH(g.p, k2_inv_diag_kernel<P><<<512, 256, 0, s>>>(g, a, b, inv_diag, status));
   TG_CUDA(cudaGetLastError());
 }
 
-int k2_pcg_max_blocks(int p, int sm_count) {
+int k2_pcg_max_blocks(int p, int sm_count, int nz) {
   int per_sm = 0;
   TG_KRON_DISPATCH(p, {
-    const size_t sb = smem_bytes<P>(2, 1);
+    const size_t sb = smem_bytes<P>(2, 1, nz);
     allow_smem(k2_pcg_kernel<P, true>, sb);
     allow_smem(k2_pcg_kernel<P, false>, sb);
     TG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
@@ -745,7 +713,7 @@ void k2_pcg_solve(const KronGrid& g, double a, double b, const double* rhs, doub
   TileIdx TT = T;
   void* args[] = {&gg, &aa, &bb, const_cast<double**>(&rhs), &x, &ww, &tt, &mi, &TT, &mm};
   TG_KRON_DISPATCH(g.p, {
-    const size_t sb = smem_bytes<P>(2, 1);
+    const size_t sb = smem_bytes<P>(2, 1, g.n[2]);
     const void* fn = maps.valid ? reinterpret_cast<const void*>(&k2_pcg_kernel<P, true>)
                                 : reinterpret_cast<const void*>(&k2_pcg_kernel<P, false>);
     TG_CUDA(cudaLaunchCooperativeKernel(fn, grid, block, args, sb, s));

@@ -56,29 +56,36 @@ struct PcgStatus {
   double bnorm;
 };
 
-// Work vectors of a solve; pA/pB are the ping-pong search directions.
+// Work vectors of a solve; pA/pB are the ping-pong search directions,
+// z = D^-1 r the preconditioned residual, inv_diag = 1 / diag(A) (set once
+// per operator by k2_inverse_diagonal).
 struct PcgWork {
   double* r;
+  double* z;
   double* pA;
   double* pB;
   double* Ap;
+  const double* inv_diag;
   double* partials;  // >= 8 * max_blocks
   PcgStatus* status;
   unsigned long long* trace;  // optional: per-phase %globaltimer stamps of CTA 0
 };
 
-// TMA descriptors of the vectors the PCG kernel streams (x, r, pA, pB), all
+// TMA descriptors of the vectors the PCG kernel sweeps (x, z, pA, pB), all
 // over the free grid; valid = false -> plain loads.
 struct PcgMaps {
   bool valid;
-  TensorMap3 x, r, pA, pB;
+  TensorMap3 x, z, pA, pB;
 };
 
 void k2_theta_rhs(const KronGrid& full, double a_b, double b_b, double a_a, double b_a,
                   const RhsArgs& args, const TensorMap3* mT, const TensorMap3* mg, int sm_count,
                   cudaStream_t s);
-void k2_check_diagonal(const KronGrid& g, double a, double b, PcgStatus* status, cudaStream_t s);
-int k2_pcg_max_blocks(int p, int sm_count);
+// inv_diag = 1.0 / diag(Op(a, b)) (sparse.cpp:47-52); status = 2 when a
+// diagonal entry is not positive.
+void k2_inverse_diagonal(const KronGrid& g, double a, double b, double* inv_diag,
+                         PcgStatus* status, cudaStream_t s);
+int k2_pcg_max_blocks(int p, int sm_count, int nz);
 // Jacobi-PCG on A = Op(a, b) over the free grid, one persistent cooperative
 // launch per solve; x holds the warm start on entry.
 void k2_pcg_solve(const KronGrid& g, double a, double b, const double* rhs, double* x,

@@ -299,11 +299,12 @@ void Sim::setup_device(int device) {
       gfree.M[geom.ax] += W;
       gfree.K[geom.ax] += W;
     }
-    k2_check_diagonal(gfree, coefA[0], coefA[1], d_status.p, s);
-    pcg_blocks = k2_pcg_max_blocks(p, ctx->sm_count);
+    k2_inverse_diagonal(gfree, coefA[0], coefA[1], d_invd.p, d_status.p, s);
+    pcg_blocks = k2_pcg_max_blocks(p, ctx->sm_count, gfree.n[2]);
     d_p2.ensure(n_free);
-    // TMA descriptors of the streamed vectors (all persistent allocations)
-    maps.valid = k2_make_map(gfree, d_x.p, &maps.x) && k2_make_map(gfree, d_r.p, &maps.r) &&
+    d_z.ensure(n_free);
+    // TMA descriptors of the swept vectors (all persistent allocations)
+    maps.valid = k2_make_map(gfree, d_x.p, &maps.x) && k2_make_map(gfree, d_z.p, &maps.z) &&
                  k2_make_map(gfree, d_p.p, &maps.pA) && k2_make_map(gfree, d_p2.p, &maps.pB);
     rhs_tma = k2_make_map(gfull, d_T.p, &map_T) && k2_make_map(gfull, d_gfull.p, &map_g);
   } else {
@@ -397,8 +398,9 @@ PcgStatus Sim::theta_step_device(double tol, int max_iter) {
     k2_theta_rhs(gfull, coefB[0], coefB[1], -coefA[0], -coefA[1], ra, rhs_tma ? &map_T : nullptr,
                  rhs_tma ? &map_g : nullptr, ctx->sm_count, s);
     ctx->timer.launches += 2;
-    const PcgWork w{d_r.p, d_p.p, d_p2.p, d_Ap.p, d_partials.p, d_status.p,
-                    trace_on ? d_trace.p : nullptr};
+    const PcgWork w{d_r.p,        d_z.p,      d_p.p,
+                    d_p2.p,       d_Ap.p,     d_invd.p,
+                    d_partials.p, d_status.p, trace_on ? d_trace.p : nullptr};
     ctx->timer.timed(2, s, [&] {
       k2_pcg_solve(gfree, coefA[0], coefA[1], d_rhs.p, d_x.p, w, maps, tol, max_iter,
                    pcg_blocks, s);

@@ -75,7 +75,7 @@ class Sim {
   DevBuf<double> dA_v, dAc_v, dB_v;
   DevCsr devA{}, devAc{}, devB{};
   KronGrid gfull{}, gfree{};
-  DevBuf<double> d_x, d_r, d_p, d_p2, d_Ap, d_invd, d_rhs, d_gn, d_g1, d_Fn, d_F1, d_T, d_gfull,
+  DevBuf<double> d_x, d_r, d_z, d_p, d_p2, d_Ap, d_invd, d_rhs, d_gn, d_g1, d_Fn, d_F1, d_T, d_gfull,
       d_partials;
   PcgMaps maps{};
   TensorMap3 map_T{}, map_g{};
