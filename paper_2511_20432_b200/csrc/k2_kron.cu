@@ -132,6 +132,11 @@ struct Inputs {
   const TensorMap3* map[NIN];
 };
 
+// Plane-level diagnostics (tools/k2_trace.py): %globaltimer stamps of CTA 0's
+// leader thread at the sub-steps of its first 64 direction-sweep planes.
+__device__ unsigned long long* g_plane_trace = nullptr;
+__device__ int g_plane_count = 0;
+
 template <int P, int NIN, int NPASS>
 __device__ __forceinline__ void init_smem(const KronGrid& g, KSmem<P, NIN, NPASS>& sm,
                                           double* zb, bool tma) {
@@ -192,8 +197,18 @@ __device__ __forceinline__ void kron_tile(const KronGrid& g, const KronTerms& c,
   for (int d = 0; d < W; ++d) win1[d] = win2[d] = pown[d] = 0.0;
   const size_t plane = static_cast<size_t>(nx) * ny;
 
+  // plane-level trace of CTA 0's direction sweeps (diagnostics only)
+  const bool ptr_on = COMBINE && g_plane_trace && blockIdx.x == 0 && leader;
+  auto pstamp = [&](int s) {
+    if (ptr_on && g_plane_count < 64) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      g_plane_trace[g_plane_count * 5 + s] = t;
+    }
+  };
   for (int kin = k0 - P; kin < k1 + P; ++kin) {
     double s1 = 0.0, s2 = 0.0, po = 0.0;
+    pstamp(0);
     if (kin >= kb && kin < ke) {
       int slot[NIN];
 #pragma unroll
@@ -202,6 +217,7 @@ __device__ __forceinline__ void kron_tile(const KronGrid& g, const KronTerms& c,
         slot[q] = TMA ? qn % kStages : 0;
         if (TMA) mbar_wait(&sm.bar[q][slot[q]], static_cast<uint32_t>((qn / kStages) & 1));
       }
+      pstamp(1);
       if constexpr (!TMA) {
         for (int q = 0; q < NIN; ++q)
           for (int r = ty; r < RY; r += kKronTY) {
@@ -222,6 +238,7 @@ __device__ __forceinline__ void kron_tile(const KronGrid& g, const KronTerms& c,
         __syncthreads();
         po = sm.v[ty + P][tx + P];
       }
+      pstamp(2);
       // x-pass on the tile rows plus the y halo
 #pragma unroll
       for (int q = 0; q < NPASS; ++q) {
@@ -239,6 +256,7 @@ __device__ __forceinline__ void kron_tile(const KronGrid& g, const KronTerms& c,
         }
       }
       __syncthreads();
+      pstamp(3);
       if (TMA && leader && kin + kStages < ke) {  // refill the slots just consumed
         fence_proxy_async();
         for (int q = 0; q < NIN; ++q) {
@@ -281,6 +299,8 @@ __device__ __forceinline__ void kron_tile(const KronGrid& g, const KronTerms& c,
       for (int d = 0; d < W; ++d) y = fma(mz[d], win1[d], fma(kz[d], win2[d], y));
       epi(static_cast<size_t>(k) * plane + static_cast<size_t>(j) * nx + i, i, j, k, y, pown[P]);
     }
+    pstamp(4);
+    if (ptr_on) ++g_plane_count;
   }
 #pragma unroll
   for (int q = 0; q < NIN; ++q) seqs[q] += ke - kb;
@@ -679,6 +699,12 @@ void k2_theta_rhs(const KronGrid& full, double a_b, double b_b, double a_a, doub
     }
   });
   TG_CUDA(cudaGetLastError());
+}
+
+void k2_plane_trace(unsigned long long* buf) {
+  int zero = 0;
+  TG_CUDA(cudaMemcpyToSymbol(g_plane_trace, &buf, sizeof(buf)));
+  TG_CUDA(cudaMemcpyToSymbol(g_plane_count, &zero, sizeof(zero)));
 }
 
 void k2_inverse_diagonal(const KronGrid& g, double a, double b, double* inv_diag,

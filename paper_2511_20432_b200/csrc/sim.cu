@@ -262,8 +262,12 @@ void Sim::setup_device(int device) {
   d_T.ensure(n_full);
   d_gfull.ensure(n_full);
   d_status.ensure(1);
-  d_trace.ensure(80);
+  d_trace.ensure(400);
   trace_on = std::getenv("TG_K2_TRACE") != nullptr;
+  if (trace_on) {
+    TG_CUDA(cudaMemsetAsync(d_trace.p, 0, 400 * sizeof(unsigned long long), s));
+    k2_plane_trace(d_trace.p + 80);
+  }
   TG_CUDA(cudaMemsetAsync(d_gfull.p, 0, sizeof(double) * n_full, s));
   TG_CUDA(cudaMemsetAsync(d_status.p, 0, sizeof(PcgStatus), s));
 

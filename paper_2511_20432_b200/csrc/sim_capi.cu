@@ -218,7 +218,7 @@ int tg_sim_state(tg_sim* s, int* step, double* time, double* free_out, double* g
 
 int tg_sim_debug_trace(tg_sim* s, unsigned long long* out, int n) {
   return sim_guard(s, [&](Sim& m) {
-    TG_CUDA(cudaMemcpy(out, m.d_trace.p, sizeof(unsigned long long) * std::min(n, 80),
+    TG_CUDA(cudaMemcpy(out, m.d_trace.p, sizeof(unsigned long long) * std::min(n, 400),
                        cudaMemcpyDeviceToHost));
   });
 }

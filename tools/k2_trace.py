@@ -13,7 +13,7 @@ import paper_2511_20432_b200 as tg  # noqa: E402
 cfg = sys.argv[1] if len(sys.argv) > 1 else os.path.join(ROOT, "configs", "cfg4_large.cfg")
 sim = tg.Simulation(cfg)
 sim.reset()
-sim.advance(2)
+sim.advance(1)
 L = sim._L
 L.tg_sim_debug_trace.argtypes = [C.c_void_p, C.POINTER(C.c_ulonglong), C.c_int]
 buf = (C.c_ulonglong * 80)()
@@ -30,3 +30,13 @@ for it in range(1, 15):
 rows = np.array(rows) / 1e3
 print("phase (us, CTA 0):", {n: round(float(v), 2) for n, v in zip(names, rows.mean(0))})
 print("iteration total (us):", round(float(rows.sum(1).mean()), 2))
+
+buf2 = (C.c_ulonglong * 400)()
+sim._check(L.tg_sim_debug_trace(sim._h, buf2, 400))
+pt = np.array(buf2[80:400], dtype=np.float64).reshape(64, 5)
+ok = pt[:, 4] > 0
+if ok.sum() > 2:
+    d = np.diff(pt[ok], axis=1) / 1e3
+    nxt = (pt[ok][1:, 0] - pt[ok][:-1, 4]) / 1e3
+    print("plane sub-steps (us): wait %.3f prep %.3f xpass %.3f ypass+z+epi %.3f gap %.3f" %
+          (d[:, 0].mean(), d[:, 1].mean(), d[:, 2].mean(), d[:, 3].mean(), nxt.mean()))
