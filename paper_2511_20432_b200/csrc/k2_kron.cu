@@ -200,11 +200,8 @@ __device__ __forceinline__ void kron_tile(const KronGrid& g, const KronTerms& c,
   // plane-level trace of CTA 0's direction sweeps (diagnostics only)
   const bool ptr_on = COMBINE && g_plane_trace && blockIdx.x == 0 && leader;
   auto pstamp = [&](int s) {
-    if (ptr_on && g_plane_count < 64) {
-      unsigned long long t;
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-      g_plane_trace[g_plane_count * 5 + s] = t;
-    }
+    if (ptr_on && g_plane_count < 64)  // SM cycles (globaltimer is too coarse here)
+      g_plane_trace[g_plane_count * 5 + s] = static_cast<unsigned long long>(clock64());
   };
   for (int kin = k0 - P; kin < k1 + P; ++kin) {
     double s1 = 0.0, s2 = 0.0, po = 0.0;

@@ -34,9 +34,13 @@ print("iteration total (us):", round(float(rows.sum(1).mean()), 2))
 buf2 = (C.c_ulonglong * 400)()
 sim._check(L.tg_sim_debug_trace(sim._h, buf2, 400))
 pt = np.array(buf2[80:400], dtype=np.float64).reshape(64, 5)
-ok = pt[:, 4] > 0
-if ok.sum() > 2:
-    d = np.diff(pt[ok], axis=1) / 1e3
-    nxt = (pt[ok][1:, 0] - pt[ok][:-1, 4]) / 1e3
-    print("plane sub-steps (us): wait %.3f prep %.3f xpass %.3f ypass+z+epi %.3f gap %.3f" %
-          (d[:, 0].mean(), d[:, 1].mean(), d[:, 2].mean(), d[:, 3].mean(), nxt.mean()))
+full = (pt > 0).all(axis=1)
+if full.sum() > 2:
+    d = np.diff(pt[full], axis=1)
+    print("plane sub-steps (SM cycles, CTA 0, %d planes): wait %.0f prep %.0f xpass %.0f "
+          "ypass+z+epi %.0f" % (full.sum(), d[:, 0].mean(), d[:, 1].mean(), d[:, 2].mean(),
+                                d[:, 3].mean()))
+    nz = pt[:, 4] > 0
+    idx = np.where(nz)[0]
+    per = np.diff(pt[idx, 4]) / np.maximum(1, np.diff(idx))
+    print("cycles per plane step: %.0f" % np.median(per))
