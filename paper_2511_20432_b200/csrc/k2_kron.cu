@@ -229,10 +229,21 @@ __device__ __forceinline__ void kron_tile(const KronGrid& g, const KronTerms& c,
           }
         __syncthreads();
       }
+      // refill the ring slots just consumed; the barrier before the issue
+      // orders every generic-proxy read of the slot before the TMA write
+      auto refill = [&] {
+        if (TMA && leader && kin + kStages < ke)
+          for (int q = 0; q < NIN; ++q) {
+            mbar_arrive_expect_tx(&sm.bar[q][slot[q]], kPlaneBytes);
+            tma_load_plane(sm.ring[q][slot[q]], in.map[q], x0 - P, y0 - P, kin + kStages,
+                           &sm.bar[q][slot[q]]);
+          }
+      };
       if constexpr (COMBINE) {  // v = z + beta p_old over the halo'd tile
         for (int e = ty * kKronTX + tx; e < RY * RX; e += kThreads)
           sm.v[0][e] = fma(beta, sm.ring[1][slot[NIN - 1]][e], sm.ring[0][slot[0]][e]);
         __syncthreads();
+        refill();  // the ring is only read by the update above
         po = sm.v[ty + P][tx + P];
       }
       pstamp(2);
@@ -254,14 +265,7 @@ __device__ __forceinline__ void kron_tile(const KronGrid& g, const KronTerms& c,
       }
       __syncthreads();
       pstamp(3);
-      if (TMA && leader && kin + kStages < ke) {  // refill the slots just consumed
-        fence_proxy_async();
-        for (int q = 0; q < NIN; ++q) {
-          mbar_arrive_expect_tx(&sm.bar[q][slot[q]], kPlaneBytes);
-          tma_load_plane(sm.ring[q][slot[q]], in.map[q], x0 - P, y0 - P, kin + kStages,
-                         &sm.bar[q][slot[q]]);
-        }
-      }
+      if constexpr (!COMBINE) refill();
       // y-pass and the z-pass inputs
 #pragma unroll
       for (int q = 0; q < NPASS; ++q) {
