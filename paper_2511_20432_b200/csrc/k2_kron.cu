@@ -11,10 +11,11 @@
 //   y-pass  w1 = My u1, w2 = My u2, w3 = Ky u1
 //           s1 = a w1 + b (w2 + w3),  s2 = b w1
 //   z-pass  y = Mz s1 + Kz s2            (2p+1-plane register window)
-// A CTA owns 32 x 8 columns of the control grid and marches through z.
-// Halo'd plane tiles arrive by TMA (cp.async.bulk.tensor.3d, zero fill
-// outside the grid) through a 3-stage mbarrier ring, so every vector is read
-// from HBM once and written once per pass; the x/y halos come from L2.
+// A CTA owns 32 x 8 columns of the control grid and marches through z, PL
+// planes per step (halving the barriers per plane). Halo'd (32+2p) x (8+2p)
+// x PL boxes arrive by TMA (cp.async.bulk.tensor.3d, zero fill outside the
+// grid) through a 3-stage mbarrier ring, so every vector is read from HBM
+// once and written once per pass; the x/y halos come from L2.
 //
 // The PCG solve is one persistent cooperative launch with two grid barriers
 // per iteration:
@@ -45,31 +46,33 @@ namespace {
 
 constexpr int kThreads = kKronTX * kKronTY;
 constexpr int kStages = 3;
+constexpr int kTmaPlanes = 2;  // planes per TMA box / per sweep step
 
-template <int P>
+template <int P, int PL>
 struct Dims {
   static constexpr int W = 2 * P + 1;
   static constexpr int RY = kKronTY + 2 * P;
   static constexpr int RX = kKronTX + 2 * P;
-  static constexpr int BUF = ((RY * RX * 8 + 127) / 128) * 128 / 8;  // 128-byte slots
+  static constexpr int PLANE = RY * RX;                                    // doubles
+  static constexpr int SLOT = ((PL * PLANE * 8 + 127) / 128) * 128 / 8;    // 128-byte slots
 };
 
 // NIN loaded vectors; NPASS separate x/y passes (2 for the RHS, whose two
 // inputs carry different (a, b)); COMBINE: one pass over v = in0 + beta in1
 // (the PCG direction update). The z band (Mz, Kz rows) of the whole grid
 // follows the struct in dynamic shared memory.
-template <int P, int NIN, int NPASS>
+template <int P, int PL, int NIN, int NPASS>
 struct KSmem {
-  double ring[NIN][kStages][Dims<P>::BUF];
-  double v[Dims<P>::RY][Dims<P>::RX];
-  double u1[NPASS][2][Dims<P>::RY][kKronTX];
-  double u2[NPASS][2][Dims<P>::RY][kKronTX];
+  double ring[NIN][kStages][Dims<P, PL>::SLOT];
+  double v[PL][Dims<P, PL>::PLANE];
+  double u1[NPASS][2][PL][Dims<P, PL>::RY][kKronTX];
+  double u2[NPASS][2][PL][Dims<P, PL>::RY][kKronTX];
   uint64_t bar[NIN][kStages];
 };
 
-template <int P, int NIN, int NPASS>
+template <int P, int PL, int NIN, int NPASS>
 __host__ __device__ constexpr size_t zband_offset() {
-  return (sizeof(KSmem<P, NIN, NPASS>) + 15) / 16 * 16;
+  return (sizeof(KSmem<P, PL, NIN, NPASS>) + 15) / 16 * 16;
 }
 
 // Work split: the grid is ntx x nty columns (32 x 8 control points each) of
@@ -111,17 +114,13 @@ __device__ __forceinline__ double diag_at(const KronGrid& g, double a, double b,
   return a * (mx * my * mz) + b * (kx * my * mz + mx * ky * mz + mx * my * kz);
 }
 
-__device__ __forceinline__ void tma_load_plane(void* dst, const TensorMap3* map, int x, int y,
-                                               int z, uint64_t* bar) {
+__device__ __forceinline__ void tma_load_box(void* dst, const TensorMap3* map, int x, int y,
+                                             int z, uint64_t* bar) {
   asm volatile(
       "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
       "[%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
       : "memory");
-}
-
-__device__ __forceinline__ void fence_proxy_async() {
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
 // Inputs of one sweep: NIN vectors, each with a TMA descriptor (or a plain
@@ -132,13 +131,8 @@ struct Inputs {
   const TensorMap3* map[NIN];
 };
 
-// Plane-level diagnostics (tools/k2_trace.py): %globaltimer stamps of CTA 0's
-// leader thread at the sub-steps of its first 64 direction-sweep planes.
-__device__ unsigned long long* g_plane_trace = nullptr;
-__device__ int g_plane_count = 0;
-
-template <int P, int NIN, int NPASS>
-__device__ __forceinline__ void init_smem(const KronGrid& g, KSmem<P, NIN, NPASS>& sm,
+template <int P, int PL, int NIN, int NPASS>
+__device__ __forceinline__ void init_smem(const KronGrid& g, KSmem<P, PL, NIN, NPASS>& sm,
                                           double* zb, bool tma) {
   constexpr int W = 2 * P + 1;
   const int tid = threadIdx.y * kKronTX + threadIdx.x;
@@ -154,23 +148,27 @@ __device__ __forceinline__ void init_smem(const KronGrid& g, KSmem<P, NIN, NPASS
   __syncthreads();
 }
 
-// Sweep one column segment. For every output point (i, j, k) call
-// epi(flat, i, j, k, y, p_own) where y = sum over passes of Op(a_q, b_q) in_q
-// (COMBINE: one pass over v = in0 + beta in1; p_own = v at the point).
-// The shared layout SM may hold more input rings than this sweep uses;
-// seqs[q] counts the planes ring q has delivered so far (mbarrier phases).
-template <int P, int NIN, int NPASS, bool COMBINE, bool TMA, class SM, class Epi>
+// Sweep one column segment, PL planes per step. For every output point
+// (i, j, k) call epi(flat, i, j, k, y, p_own) where y = sum over passes of
+// Op(a_q, b_q) in_q (COMBINE: one pass over v = in0 + beta in1; p_own = v at
+// the point). Step s covers input planes k0 - P + PL s .. + PL - 1 (planes
+// outside the grid arrive as zeros). The shared layout SM may hold more input
+// rings than this sweep uses; seqs[q] counts the boxes ring q has delivered
+// (mbarrier phases).
+template <int P, int PL, int NIN, int NPASS, bool COMBINE, bool TMA, class SM, class Epi>
 __device__ __forceinline__ void kron_tile(const KronGrid& g, const KronTerms& c,
                                           const Inputs<NIN>& in, double beta, const Seg& sg,
                                           SM& sm, const double* zb, int* seqs, Epi& epi) {
-  constexpr int W = Dims<P>::W, RY = Dims<P>::RY, RX = Dims<P>::RX;
+  using D = Dims<P, PL>;
+  constexpr int W = D::W, RY = D::RY, RX = D::RX, PLANE = D::PLANE;
   const int tx = threadIdx.x, ty = threadIdx.y;
   const bool leader = tx == 0 && ty == 0;
   const int x0 = sg.x0, y0 = sg.y0, k0 = sg.k0, k1 = sg.k1;
   const int nx = g.n[0], ny = g.n[1], nz = g.n[2];
   const int i = x0 + tx, j = y0 + ty;
-  const int kb = max(0, k0 - P), ke = min(nz, k1 + P);
-  constexpr uint32_t kPlaneBytes = RY * RX * 8;
+  const int kfirst = k0 - P;
+  const int nsteps = (k1 - k0 + 2 * P + PL - 1) / PL;
+  constexpr uint32_t kBoxBytes = PL * PLANE * 8;
 
   __syncthreads();  // the previous segment's readers of the ring are done
   // this thread's x and y rows of the 1D factors, in registers (the sweep is
@@ -184,11 +182,12 @@ __device__ __forceinline__ void kron_tile(const KronGrid& g, const KronTerms& c,
     ky[d] = j < ny ? g.K[1][j * W + d] : 0.0;
   }
   if (TMA && leader) {
-    for (int s = 0; s < kStages && kb + s < ke; ++s)
+    for (int s = 0; s < kStages && s < nsteps; ++s)
       for (int q = 0; q < NIN; ++q) {
         const int slot = (seqs[q] + s) % kStages;
-        mbar_arrive_expect_tx(&sm.bar[q][slot], kPlaneBytes);
-        tma_load_plane(sm.ring[q][slot], in.map[q], x0 - P, y0 - P, kb + s, &sm.bar[q][slot]);
+        mbar_arrive_expect_tx(&sm.bar[q][slot], kBoxBytes);
+        tma_load_box(sm.ring[q][slot], in.map[q], x0 - P, y0 - P, kfirst + PL * s,
+                     &sm.bar[q][slot]);
       }
   }
 
@@ -197,60 +196,54 @@ __device__ __forceinline__ void kron_tile(const KronGrid& g, const KronTerms& c,
   for (int d = 0; d < W; ++d) win1[d] = win2[d] = pown[d] = 0.0;
   const size_t plane = static_cast<size_t>(nx) * ny;
 
-  // plane-level trace of CTA 0's direction sweeps (diagnostics only)
-  const bool ptr_on = COMBINE && g_plane_trace && blockIdx.x == 0 && leader;
-  auto pstamp = [&](int s) {
-    if (ptr_on && g_plane_count < 64)  // SM cycles (globaltimer is too coarse here)
-      g_plane_trace[g_plane_count * 5 + s] = static_cast<unsigned long long>(clock64());
-  };
-  for (int kin = k0 - P; kin < k1 + P; ++kin) {
-    double s1 = 0.0, s2 = 0.0, po = 0.0;
-    pstamp(0);
-    if (kin >= kb && kin < ke) {
-      int slot[NIN];
+  for (int s = 0; s < nsteps; ++s) {
+    const int kin0 = kfirst + PL * s;
+    int slot[NIN];
 #pragma unroll
-      for (int q = 0; q < NIN; ++q) {
-        const int qn = seqs[q] + (kin - kb);
-        slot[q] = TMA ? qn % kStages : 0;
-        if (TMA) mbar_wait(&sm.bar[q][slot[q]], static_cast<uint32_t>((qn / kStages) & 1));
-      }
-      pstamp(1);
-      if constexpr (!TMA) {
-        for (int q = 0; q < NIN; ++q)
-          for (int r = ty; r < RY; r += kKronTY) {
-            const int gj = y0 + r - P;
-            for (int cc = tx; cc < RX; cc += kKronTX) {
-              const int gi = x0 + cc - P;
-              double val = 0.0;
-              if (gi >= 0 && gi < nx && gj >= 0 && gj < ny)
-                val = in.ptr[q][static_cast<size_t>(kin) * plane + static_cast<size_t>(gj) * nx + gi];
-              sm.ring[q][0][r * RX + cc] = val;
-            }
+    for (int q = 0; q < NIN; ++q) {
+      const int qn = seqs[q] + s;
+      slot[q] = TMA ? qn % kStages : 0;
+      if (TMA) mbar_wait(&sm.bar[q][slot[q]], static_cast<uint32_t>((qn / kStages) & 1));
+    }
+    if constexpr (!TMA) {
+      for (int q = 0; q < NIN; ++q)
+        for (int l = 0; l < PL; ++l) {
+          const int kin = kin0 + l;
+          for (int e = ty * kKronTX + tx; e < PLANE; e += kThreads) {
+            const int gi = x0 + e % RX - P, gj = y0 + e / RX - P;
+            double val = 0.0;
+            if (gi >= 0 && gi < nx && gj >= 0 && gj < ny && kin >= 0 && kin < nz)
+              val = in.ptr[q][static_cast<size_t>(kin) * plane + static_cast<size_t>(gj) * nx + gi];
+            sm.ring[q][0][l * PLANE + e] = val;
           }
-        __syncthreads();
-      }
-      // refill the ring slots just consumed; the barrier before the issue
-      // orders every generic-proxy read of the slot before the TMA write
-      auto refill = [&] {
-        if (TMA && leader && kin + kStages < ke)
-          for (int q = 0; q < NIN; ++q) {
-            mbar_arrive_expect_tx(&sm.bar[q][slot[q]], kPlaneBytes);
-            tma_load_plane(sm.ring[q][slot[q]], in.map[q], x0 - P, y0 - P, kin + kStages,
-                           &sm.bar[q][slot[q]]);
-          }
-      };
-      if constexpr (COMBINE) {  // v = z + beta p_old over the halo'd tile
-        for (int e = ty * kKronTX + tx; e < RY * RX; e += kThreads)
-          sm.v[0][e] = fma(beta, sm.ring[1][slot[NIN - 1]][e], sm.ring[0][slot[0]][e]);
-        __syncthreads();
-        refill();  // the ring is only read by the update above
-        po = sm.v[ty + P][tx + P];
-      }
-      pstamp(2);
-      // x-pass on the tile rows plus the y halo
+        }
+      __syncthreads();
+    }
+    // refill the ring slots just consumed; the barrier before the issue
+    // orders every generic-proxy read of the slot before the TMA write
+    auto refill = [&] {
+      if (TMA && leader && s + kStages < nsteps)
+        for (int q = 0; q < NIN; ++q) {
+          mbar_arrive_expect_tx(&sm.bar[q][slot[q]], kBoxBytes);
+          tma_load_box(sm.ring[q][slot[q]], in.map[q], x0 - P, y0 - P,
+                       kfirst + PL * (s + kStages), &sm.bar[q][slot[q]]);
+        }
+    };
+    double po[PL];
+    if constexpr (COMBINE) {  // v = z + beta p_old over the halo'd tiles
+      for (int e = ty * kKronTX + tx; e < PL * PLANE; e += kThreads)
+        (&sm.v[0][0])[e] = fma(beta, sm.ring[1][slot[NIN - 1]][e], sm.ring[0][slot[0]][e]);
+      __syncthreads();
+      refill();  // the ring is only read by the update above
 #pragma unroll
-      for (int q = 0; q < NPASS; ++q) {
-        const double* src = COMBINE ? &sm.v[0][0] : sm.ring[q][slot[q < NIN ? q : 0]];
+      for (int l = 0; l < PL; ++l) po[l] = sm.v[l][(ty + P) * RX + tx + P];
+    }
+    // x-pass on the tile rows plus the y halo, PL planes
+#pragma unroll
+    for (int q = 0; q < NPASS; ++q)
+#pragma unroll
+      for (int l = 0; l < PL; ++l) {
+        const double* src = COMBINE ? sm.v[l] : sm.ring[q][slot[q < NIN ? q : 0]] + l * PLANE;
         for (int r = ty; r < RY; r += kKronTY) {
           double a1 = 0.0, a2 = 0.0;
 #pragma unroll
@@ -259,52 +252,53 @@ __device__ __forceinline__ void kron_tile(const KronGrid& g, const KronTerms& c,
             a1 = fma(mx[d], vv, a1);
             a2 = fma(kx[d], vv, a2);
           }
-          sm.u1[q][kin & 1][r][tx] = a1;
-          sm.u2[q][kin & 1][r][tx] = a2;
+          sm.u1[q][s & 1][l][r][tx] = a1;
+          sm.u2[q][s & 1][l][r][tx] = a2;
         }
       }
-      __syncthreads();
-      pstamp(3);
-      if constexpr (!COMBINE) refill();
-      // y-pass and the z-pass inputs
+    __syncthreads();
+    if constexpr (!COMBINE) refill();
+    // y-pass, then the PL planes enter the z window one by one
+#pragma unroll
+    for (int l = 0; l < PL; ++l) {
+      double s1 = 0.0, s2 = 0.0;
 #pragma unroll
       for (int q = 0; q < NPASS; ++q) {
         double w1 = 0.0, w2 = 0.0, w3 = 0.0;
 #pragma unroll
         for (int d = 0; d < W; ++d) {
-          const double p1 = sm.u1[q][kin & 1][ty + d][tx];
+          const double p1 = sm.u1[q][s & 1][l][ty + d][tx];
           w1 = fma(my[d], p1, w1);
-          w2 = fma(my[d], sm.u2[q][kin & 1][ty + d][tx], w2);
+          w2 = fma(my[d], sm.u2[q][s & 1][l][ty + d][tx], w2);
           w3 = fma(ky[d], p1, w3);
         }
         const double a = q == 0 ? c.a1 : c.a2, b = q == 0 ? c.b1 : c.b2;
         s1 = fma(a, w1, fma(b, w2 + w3, s1));
         s2 = fma(b, w1, s2);
       }
-    }
 #pragma unroll
-    for (int d = 0; d < W - 1; ++d) {
-      win1[d] = win1[d + 1];
-      win2[d] = win2[d + 1];
-      pown[d] = pown[d + 1];
-    }
-    win1[W - 1] = s1;
-    win2[W - 1] = s2;
-    pown[W - 1] = po;
-    const int k = kin - P;
-    if (k >= k0 && i < nx && j < ny) {
-      const double* mz = zb + k * W;
-      const double* kz = zb + nz * W + k * W;
-      double y = 0.0;
+      for (int d = 0; d < W - 1; ++d) {
+        win1[d] = win1[d + 1];
+        win2[d] = win2[d + 1];
+        pown[d] = pown[d + 1];
+      }
+      win1[W - 1] = s1;
+      win2[W - 1] = s2;
+      pown[W - 1] = COMBINE ? po[l] : 0.0;
+      const int k = kin0 + l - P;
+      if (k >= k0 && k < k1 && i < nx && j < ny) {
+        const double* mz = zb + k * W;
+        const double* kz = zb + nz * W + k * W;
+        double y = 0.0;
 #pragma unroll
-      for (int d = 0; d < W; ++d) y = fma(mz[d], win1[d], fma(kz[d], win2[d], y));
-      epi(static_cast<size_t>(k) * plane + static_cast<size_t>(j) * nx + i, i, j, k, y, pown[P]);
+        for (int d = 0; d < W; ++d) y = fma(mz[d], win1[d], fma(kz[d], win2[d], y));
+        epi(static_cast<size_t>(k) * plane + static_cast<size_t>(j) * nx + i, i, j, k, y,
+            pown[P]);
+      }
     }
-    pstamp(4);
-    if (ptr_on) ++g_plane_count;
   }
 #pragma unroll
-  for (int q = 0; q < NIN; ++q) seqs[q] += ke - kb;
+  for (int q = 0; q < NIN; ++q) seqs[q] += nsteps;
 }
 
 // ---------------------------------------------------------------------------
@@ -320,14 +314,14 @@ __global__ void __launch_bounds__(kThreads) k2_apply_kernel(KronGrid g, KronTerm
                                                             const double* v, double* y,
                                                             TileIdx T) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  auto& sm = *reinterpret_cast<KSmem<P, 1, 1>*>(smem_raw);
-  double* zb = reinterpret_cast<double*>(smem_raw + zband_offset<P, 1, 1>());
+  auto& sm = *reinterpret_cast<KSmem<P, 1, 1, 1>*>(smem_raw);
+  double* zb = reinterpret_cast<double*>(smem_raw + zband_offset<P, 1, 1, 1>());
   init_smem(g, sm, zb, false);
   EpiStore epi{y};
   Inputs<1> in{{v}, {nullptr}};
   int seq[1] = {0};
   for_segments(T, gridDim.x, blockIdx.x, [&](const Seg& sg) {
-    kron_tile<P, 1, 1, false, false>(g, c, in, 0.0, sg, sm, zb, seq, epi);
+    kron_tile<P, 1, 1, 1, false, false>(g, c, in, 0.0, sg, sm, zb, seq, epi);
   });
 }
 
@@ -352,16 +346,17 @@ template <int P, bool TMA>
 __global__ void __launch_bounds__(kThreads) k2_rhs_kernel(KronGrid g, KronTerms c, RhsArgs args,
                                                           TileIdx T,
                                                           const __grid_constant__ RhsMaps maps) {
+  constexpr int PL = TMA ? kTmaPlanes : 1;
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  auto& sm = *reinterpret_cast<KSmem<P, 2, 2>*>(smem_raw);
-  double* zb = reinterpret_cast<double*>(smem_raw + zband_offset<P, 2, 2>());
+  auto& sm = *reinterpret_cast<KSmem<P, PL, 2, 2>*>(smem_raw);
+  double* zb = reinterpret_cast<double*>(smem_raw + zband_offset<P, PL, 2, 2>());
   init_smem(g, sm, zb, TMA);
   EpiRhs epi{args, {g.n[0], g.n[1], g.n[2]}};
   epi.nfree[args.bottom_axis] -= 1;
   Inputs<2> in{{args.T_full, args.g_full}, {&maps.T, &maps.g}};
   int seq[2] = {0, 0};
   for_segments(T, gridDim.x, blockIdx.x, [&](const Seg& sg) {
-    kron_tile<P, 2, 2, false, TMA>(g, c, in, 0.0, sg, sm, zb, seq, epi);
+    kron_tile<P, PL, 2, 2, false, TMA>(g, c, in, 0.0, sg, sm, zb, seq, epi);
   });
 }
 
@@ -457,10 +452,11 @@ template <int P, bool TMA>
 __global__ void __launch_bounds__(kThreads, 2)
     k2_pcg_kernel(KronGrid g, double a, double b, const double* rhs, double* x, PcgWork w,
                   double tol, int max_iter, TileIdx T, const __grid_constant__ PcgMaps maps) {
+  constexpr int PL = TMA ? kTmaPlanes : 1;
   cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  auto& sm = *reinterpret_cast<KSmem<P, 2, 1>*>(smem_raw);
-  double* zb = reinterpret_cast<double*>(smem_raw + zband_offset<P, 2, 1>());
+  auto& sm = *reinterpret_cast<KSmem<P, PL, 2, 1>*>(smem_raw);
+  double* zb = reinterpret_cast<double*>(smem_raw + zband_offset<P, PL, 2, 1>());
   __shared__ double red[64];
   init_smem(g, sm, zb, TMA);
   const KronTerms c{a, b, 0.0, 0.0};
@@ -475,7 +471,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     EpiResidual e0{rhs, w.inv_diag, w.r, w.z, w.pA, {0, 0, 0, 0}};
     Inputs<1> in1{{x}, {&maps.x}};  // ring 0 of the two-ring layout
     for_segments(T, gridDim.x, blockIdx.x, [&](const Seg& sg) {
-      kron_tile<P, 1, 1, false, TMA>(g, c, in1, 0.0, sg, sm, zb, seq, e0);
+      kron_tile<P, PL, 1, 1, false, TMA>(g, c, in1, 0.0, sg, sm, zb, seq, e0);
     });
     grid_reduce(grid, e0.acc, w.partials, buf, red, tot);
   }
@@ -516,7 +512,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     EpiDirection e1{p_new, w.Ap, {0, 0, 0, 0}};
     Inputs<2> in{{w.z, p_old}, {&maps.z, m_old}};
     for_segments(T, gridDim.x, blockIdx.x, [&](const Seg& sg) {
-      kron_tile<P, 2, 1, true, TMA>(g, c, in, beta, sg, sm, zb, seq, e1);
+      kron_tile<P, PL, 2, 1, true, TMA>(g, c, in, beta, sg, sm, zb, seq, e1);
     });
     stamp(1);
     grid_reduce(grid, e1.acc, w.partials, buf, red, tot);
@@ -611,12 +607,9 @@ EncodeFn encoder() {
   return fn;
 }
 
-template <int P>
-size_t smem_bytes(int nin, int npass, int nz) {
-  const size_t band = 2 * static_cast<size_t>(nz) * (2 * P + 1) * sizeof(double);
-  if (nin == 1) return zband_offset<P, 1, 1>() + band;
-  if (npass == 2) return zband_offset<P, 2, 2>() + band;
-  return zband_offset<P, 2, 1>() + band;
+template <int P, int PL, int NIN, int NPASS>
+size_t smem_bytes(int nz) {
+  return zband_offset<P, PL, NIN, NPASS>() + 2 * static_cast<size_t>(nz) * (2 * P + 1) * 8;
 }
 
 template <typename K>
@@ -643,7 +636,8 @@ bool k2_make_map(const KronGrid& g, const double* base, TensorMap3* out) {
                               static_cast<cuuint64_t>(g.n[2])};
   const cuuint64_t strides[2] = {pitch, pitch * static_cast<cuuint64_t>(g.n[1])};
   const cuuint32_t box[3] = {static_cast<cuuint32_t>(kKronTX + 2 * g.p),
-                             static_cast<cuuint32_t>(kKronTY + 2 * g.p), 1};
+                             static_cast<cuuint32_t>(kKronTY + 2 * g.p),
+                             static_cast<cuuint32_t>(kTmaPlanes)};
   const cuuint32_t estr[3] = {1, 1, 1};
   CUtensorMap m;
   const CUresult r = enc(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base), dims,
@@ -669,7 +663,7 @@ void k2_apply(const KronGrid& g, double a, double b, const double* v, double* y,
   const TileIdx T = make_tiles(g);
   const int blocks = seg_blocks(T, 3 * sm_count);
   TG_KRON_DISPATCH(g.p, {
-    const size_t sb = smem_bytes<P>(1, 1, g.n[2]);
+    const size_t sb = smem_bytes<P, 1, 1, 1>(g.n[2]);
     allow_smem(k2_apply_kernel<P>, sb);
     k2_apply_kernel<P><<<blocks, dim3(kKronTX, kKronTY), sb, s>>>(g, KronTerms{a, b, 0.0, 0.0},
                                                                   v, y, T);
@@ -690,11 +684,12 @@ void k2_theta_rhs(const KronGrid& full, double a_b, double b_b, double a_a, doub
   }
   const KronTerms c{a_b, b_b, a_a, b_a};
   TG_KRON_DISPATCH(full.p, {
-    const size_t sb = smem_bytes<P>(2, 2, full.n[2]);
     if (tma) {
+      const size_t sb = smem_bytes<P, kTmaPlanes, 2, 2>(full.n[2]);
       allow_smem(k2_rhs_kernel<P, true>, sb);
       k2_rhs_kernel<P, true><<<blocks, dim3(kKronTX, kKronTY), sb, s>>>(full, c, args, T, maps);
     } else {
+      const size_t sb = smem_bytes<P, 1, 2, 2>(full.n[2]);
       allow_smem(k2_rhs_kernel<P, false>, sb);
       k2_rhs_kernel<P, false><<<blocks, dim3(kKronTX, kKronTY), sb, s>>>(full, c, args, T, maps);
     }
@@ -702,11 +697,7 @@ void k2_theta_rhs(const KronGrid& full, double a_b, double b_b, double a_a, doub
   TG_CUDA(cudaGetLastError());
 }
 
-void k2_plane_trace(unsigned long long* buf) {
-  int zero = 0;
-  TG_CUDA(cudaMemcpyToSymbol(g_plane_trace, &buf, sizeof(buf)));
-  TG_CUDA(cudaMemcpyToSymbol(g_plane_count, &zero, sizeof(zero)));
-}
+void k2_plane_trace(unsigned long long*) {}  // plane-level stamps retired (see k2_trace.py)
 
 void k2_inverse_diagonal(const KronGrid& g, double a, double b, double* inv_diag,
                          PcgStatus* status, cudaStream_t s) {
@@ -717,11 +708,12 @@ void k2_inverse_diagonal(const KronGrid& g, double a, double b, double* inv_diag
 int k2_pcg_max_blocks(int p, int sm_count, int nz) {
   int per_sm = 0;
   TG_KRON_DISPATCH(p, {
-    const size_t sb = smem_bytes<P>(2, 1, nz);
-    allow_smem(k2_pcg_kernel<P, true>, sb);
-    allow_smem(k2_pcg_kernel<P, false>, sb);
+    const size_t sbt = smem_bytes<P, kTmaPlanes, 2, 1>(nz);
+    const size_t sbp = smem_bytes<P, 1, 2, 1>(nz);
+    allow_smem(k2_pcg_kernel<P, true>, sbt);
+    allow_smem(k2_pcg_kernel<P, false>, sbp);
     TG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-        &per_sm, reinterpret_cast<const void*>(&k2_pcg_kernel<P, true>), kThreads, sb));
+        &per_sm, reinterpret_cast<const void*>(&k2_pcg_kernel<P, true>), kThreads, sbt));
   });
   return std::max(1, per_sm) * sm_count;
 }
@@ -740,10 +732,13 @@ void k2_pcg_solve(const KronGrid& g, double a, double b, const double* rhs, doub
   TileIdx TT = T;
   void* args[] = {&gg, &aa, &bb, const_cast<double**>(&rhs), &x, &ww, &tt, &mi, &TT, &mm};
   TG_KRON_DISPATCH(g.p, {
-    const size_t sb = smem_bytes<P>(2, 1, g.n[2]);
-    const void* fn = maps.valid ? reinterpret_cast<const void*>(&k2_pcg_kernel<P, true>)
-                                : reinterpret_cast<const void*>(&k2_pcg_kernel<P, false>);
-    TG_CUDA(cudaLaunchCooperativeKernel(fn, grid, block, args, sb, s));
+    if (maps.valid)
+      TG_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(&k2_pcg_kernel<P, true>),
+                                          grid, block, args,
+                                          smem_bytes<P, kTmaPlanes, 2, 1>(g.n[2]), s));
+    else
+      TG_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(&k2_pcg_kernel<P, false>),
+                                          grid, block, args, smem_bytes<P, 1, 2, 1>(g.n[2]), s));
   });
 }
 
