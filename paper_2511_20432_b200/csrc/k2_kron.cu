@@ -235,7 +235,8 @@ __device__ __forceinline__ void kron_tile(const KronGrid& g, const KronTerms& c,
                        kfirst + PL * (s + kStages), &sm.bar[q][slot[q]]);
         }
     };
-    double po[PL];
+    double po[PL], xval[PL], xinc[PL];
+    size_t xown[PL];
     if constexpr (COMBINE) {  // v = z + beta p_old over the halo'd tiles
       double pold[PL];
 #pragma unroll
@@ -247,11 +248,15 @@ __device__ __forceinline__ void kron_tile(const KronGrid& g, const KronTerms& c,
 #pragma unroll
       for (int l = 0; l < PL; ++l) {
         po[l] = sm.v[l][(ty + P) * RX + tx + P];
-        // deferred x += alpha_prev p_old of the previous iteration (own points)
+        // deferred x += alpha_prev p_old of the previous iteration (own
+        // points): load now, update at the end of the step (latency hidden)
         const int kin = kin0 + l;
-        if (xd.x && kin >= k0 && kin < k1 && i < nx && j < ny) {
-          const size_t f = static_cast<size_t>(kin) * plane + static_cast<size_t>(j) * nx + i;
-          xd.x[f] += xd.alpha * pold[l];
+        xown[l] = (xd.x && kin >= k0 && kin < k1 && i < nx && j < ny)
+                      ? static_cast<size_t>(kin) * plane + static_cast<size_t>(j) * nx + i
+                      : ~size_t{0};
+        if (xown[l] != ~size_t{0}) {
+          xval[l] = xd.x[xown[l]];
+          xinc[l] = xd.alpha * pold[l];
         }
       }
     }
@@ -312,6 +317,11 @@ __device__ __forceinline__ void kron_tile(const KronGrid& g, const KronTerms& c,
         epi(static_cast<size_t>(k) * plane + static_cast<size_t>(j) * nx + i, i, j, k, y,
             pown[P]);
       }
+    }
+    if constexpr (COMBINE) {
+#pragma unroll
+      for (int l = 0; l < PL; ++l)
+        if (xown[l] != ~size_t{0}) xd.x[xown[l]] = xval[l] + xinc[l];
     }
   }
 #pragma unroll
