@@ -155,16 +155,10 @@ __device__ __forceinline__ void init_smem(const KronGrid& g, KSmem<P, PL, NIN, N
 // outside the grid arrive as zeros). The shared layout SM may hold more input
 // rings than this sweep uses; seqs[q] counts the boxes ring q has delivered
 // (mbarrier phases).
-struct XDefer {  // x += alpha p_old on the swept points (PCG); x == nullptr: off
-  double* x;
-  double alpha;
-};
-
 template <int P, int PL, int NIN, int NPASS, bool COMBINE, bool TMA, class SM, class Epi>
 __device__ __forceinline__ void kron_tile(const KronGrid& g, const KronTerms& c,
                                           const Inputs<NIN>& in, double beta, const Seg& sg,
-                                          SM& sm, const double* zb, int* seqs, Epi& epi,
-                                          XDefer xd = {nullptr, 0.0}) {
+                                          SM& sm, const double* zb, int* seqs, Epi& epi) {
   using D = Dims<P, PL>;
   constexpr int W = D::W, RY = D::RY, RX = D::RX, PLANE = D::PLANE;
   const int tx = threadIdx.x, ty = threadIdx.y;
@@ -235,30 +229,14 @@ __device__ __forceinline__ void kron_tile(const KronGrid& g, const KronTerms& c,
                        kfirst + PL * (s + kStages), &sm.bar[q][slot[q]]);
         }
     };
-    double po[PL], xval[PL], xinc[PL];
-    size_t xown[PL];
+    double po[PL];
     if constexpr (COMBINE) {  // v = z + beta p_old over the halo'd tiles
-      double pold[PL];
-#pragma unroll
-      for (int l = 0; l < PL; ++l) pold[l] = sm.ring[1][slot[NIN - 1]][l * PLANE + (ty + P) * RX + tx + P];
       for (int e = ty * kKronTX + tx; e < PL * PLANE; e += kThreads)
         (&sm.v[0][0])[e] = fma(beta, sm.ring[1][slot[NIN - 1]][e], sm.ring[0][slot[0]][e]);
       __syncthreads();
       refill();  // the ring is only read by the update above
 #pragma unroll
-      for (int l = 0; l < PL; ++l) {
-        po[l] = sm.v[l][(ty + P) * RX + tx + P];
-        // deferred x += alpha_prev p_old of the previous iteration (own
-        // points): load now, update at the end of the step (latency hidden)
-        const int kin = kin0 + l;
-        xown[l] = (xd.x && kin >= k0 && kin < k1 && i < nx && j < ny)
-                      ? static_cast<size_t>(kin) * plane + static_cast<size_t>(j) * nx + i
-                      : ~size_t{0};
-        if (xown[l] != ~size_t{0}) {
-          xval[l] = xd.x[xown[l]];
-          xinc[l] = xd.alpha * pold[l];
-        }
-      }
+      for (int l = 0; l < PL; ++l) po[l] = sm.v[l][(ty + P) * RX + tx + P];
     }
     // x-pass on the tile rows plus the y halo, PL planes
 #pragma unroll
@@ -317,11 +295,6 @@ __device__ __forceinline__ void kron_tile(const KronGrid& g, const KronTerms& c,
         epi(static_cast<size_t>(k) * plane + static_cast<size_t>(j) * nx + i, i, j, k, y,
             pown[P]);
       }
-    }
-    if constexpr (COMBINE) {
-#pragma unroll
-      for (int l = 0; l < PL; ++l)
-        if (xown[l] != ~size_t{0}) xd.x[xown[l]] = xval[l] + xinc[l];
     }
   }
 #pragma unroll
@@ -513,8 +486,7 @@ __global__ void __launch_bounds__(kThreads, 2)
       *w.status = PcgStatus{0, 0, 0.0, 0.0};
     return;
   }
-  double rel = 0.0, beta = 0.0, x_alpha = 0.0;
-  bool x_pending = false;
+  double rel = 0.0, beta = 0.0;
   int it = 0, status = 3;
   double* p_old = w.pA;
   double* p_new = w.pB;
@@ -537,14 +509,11 @@ __global__ void __launch_bounds__(kThreads, 2)
     };
     stamp(0);
     // A': p_new = z + beta p_old (sparse.cpp:96), Ap = A p_new (sparse.cpp:81)
-    // (the previous iteration's x += alpha p is applied on the way, sparse.cpp:86)
     EpiDirection e1{p_new, w.Ap, {0, 0, 0, 0}};
     Inputs<2> in{{w.z, p_old}, {&maps.z, m_old}};
-    const XDefer xd{x_pending ? x : nullptr, x_alpha};
     for_segments(T, gridDim.x, blockIdx.x, [&](const Seg& sg) {
-      kron_tile<P, PL, 2, 1, true, TMA>(g, c, in, beta, sg, sm, zb, seq, e1, xd);
+      kron_tile<P, PL, 2, 1, true, TMA>(g, c, in, beta, sg, sm, zb, seq, e1);
     });
-    x_pending = false;
     stamp(1);
     grid_reduce(grid, e1.acc, w.partials, buf, red, tot);
     stamp(2);
@@ -554,9 +523,7 @@ __global__ void __launch_bounds__(kThreads, 2)
       break;
     }
     const double alpha = rz / pAp;
-    x_alpha = alpha;  // x += alpha p is deferred to the next sweep (or the exit)
-    x_pending = true;
-    // B: r, z updates and the two dot products (sparse.cpp:87-94), on the
+    // B: x, r, z updates and the two dot products (sparse.cpp:85-94), on the
     // same segment map; rows of 32 consecutive points per warp, U planes of
     // loads in flight per thread
     double acc[4] = {0, 0, 0, 0};
@@ -567,16 +534,20 @@ __global__ void __launch_bounds__(kThreads, 2)
       constexpr int U = 4;
       const size_t pl = static_cast<size_t>(nx) * ny;
       const size_t f0 = (static_cast<size_t>(sg.k0) * ny + j) * nx + i;
+      double* __restrict__ xr = x;
       double* __restrict__ rr_ = w.r;
       double* __restrict__ zr = w.z;
+      const double* __restrict__ pr = p_new;
       const double* __restrict__ apr = w.Ap;
       const double* __restrict__ ir = w.inv_diag;
       for (int k = sg.k0; k < sg.k1; k += U) {
-        double rv[U], av[U], iv[U];
+        double xv[U], pv[U], rv[U], av[U], iv[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
           if (k + u < sg.k1) {
             const size_t f = f0 + (k - sg.k0 + u) * pl;
+            xv[u] = xr[f];
+            pv[u] = pr[f];
             rv[u] = rr_[f];
             av[u] = apr[f];
             iv[u] = ir[f];
@@ -586,6 +557,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         for (int u = 0; u < U; ++u) {
           if (k + u < sg.k1) {
             const size_t f = f0 + (k - sg.k0 + u) * pl;
+            xr[f] = xv[u] + alpha * pv[u];
             const double ri = rv[u] - alpha * av[u];
             const double zi = iv[u] * ri;
             rr_[f] = ri;
@@ -608,16 +580,6 @@ __global__ void __launch_bounds__(kThreads, 2)
     const TensorMap3* tm = m_old;
     m_old = m_new;
     m_new = tm;
-  }
-  if (x_pending && status != 4) {  // the last x += alpha p (own points, same map)
-    for_segments(T, gridDim.x, blockIdx.x, [&](const Seg& sg) {
-      const int i = sg.x0 + threadIdx.x, j = sg.y0 + threadIdx.y;
-      if (i >= nx || j >= ny) return;
-      for (int k = sg.k0; k < sg.k1; ++k) {
-        const size_t f = (static_cast<size_t>(k) * ny + j) * nx + i;
-        x[f] += x_alpha * p_old[f];
-      }
-    });
   }
   if (blockIdx.x == 0 && threadIdx.x == 0 && threadIdx.y == 0)
     *w.status = PcgStatus{it, status, rel, bnorm};
