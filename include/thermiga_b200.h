@@ -153,6 +153,23 @@ int tg_sim_theta_step(tg_sim* sim, const double* free_n, const double* g_n, cons
  * proj/include/thermiga/assembly.hpp:56). */
 int tg_sim_operator_apply(tg_sim* sim, const double* x_free, double* y_free);
 
+/* ---- sharding support (paper_2511_20432_b200/parallel.py) ---------------
+ * Face-element slabs: local loads loc[e][a] of elements [e0, e1) computed on
+ * this GPU ((e1 - e0) x n_dofs_kept doubles, device memory), and the
+ * deterministic gather of all elements' loads into F (reference scatter
+ * order, assembly.cpp:141-144), so all-gathered slabs reproduce the
+ * single-GPU load bit for bit. */
+int tg_sim_flux_local_device(tg_sim* sim, double t, double fine_radius, int e0, int e1,
+                             double* d_loc);
+int tg_sim_flux_gather_device(tg_sim* sim, const double* d_loc_all, double* d_F);
+/* z-slab of the reduced operator: y (planes [k0, k1) of the free grid) =
+ * A_ff x, with x given on planes [max(0, k0 - p), min(nz, k1 + p)) (ghost
+ * planes included). Kronecker patches only. Device pointers; synchronous. */
+int tg_sim_operator_apply_slab_device(tg_sim* sim, int k0, int k1, const double* d_x,
+                                      double* d_y);
+/* 1 / diag(A_ff) (the Jacobi preconditioner, sparse.cpp:47-52), host copy. */
+int tg_sim_inverse_diagonal(tg_sim* sim, double* out);
+
 /* Diagnostics: %globaltimer stamps of CTA 0 at the K2 phase boundaries of the
  * first 16 CG iterations of the last solve (5 per iteration; recorded only
  * when TG_K2_TRACE is set in the environment at tg_sim_create). */

@@ -268,3 +268,56 @@ void or_boundary_load(int n_fe, int nd, const int* nq_base, const int* nq_fine, 
   }
   free(loc);
 }
+
+/* The element-local half of assemble_boundary_load (src/assembly.cpp:126-139)
+ * for face elements [e0, e1): loc[(e - e0) * nd + a], without the scatter.
+ * (Test support for the sharded flux load: slabs of these, gathered in the
+ * reference's order, must reproduce or_boundary_load bit for bit.) */
+void or_boundary_local(int n_fe, int nd, const int* nq_base, const int* nq_fine,
+                       const double* centers, const double* xb, const double* nb,
+                       const double* wb, const double* Nb, const double* xf, const double* nf,
+                       const double* wf, const double* Nf, int n_src, const double* src6,
+                       double t, double fine_radius, double cull, double k, double rho, double c,
+                       int e0, int e1, double* loc) {
+  const double alpha = k / (rho * c);
+  const double rcp = rho * c;
+  int have_focus = 0;
+  double focus[3] = {0, 0, 0};
+  for (int j = 0; j < n_src; ++j) {
+    if (src6[6 * (size_t)j + 4] > t) break;
+    focus[0] = src6[6 * (size_t)j];
+    focus[1] = src6[6 * (size_t)j + 1];
+    focus[2] = src6[6 * (size_t)j + 2];
+    have_focus = 1;
+  }
+  size_t ob = 0, of = 0;
+  for (int e = 0; e < e0 && e < n_fe; ++e) {
+    ob += (size_t)nq_base[e];
+    of += (size_t)nq_fine[e];
+  }
+  for (int e = e0; e < e1 && e < n_fe; ++e) {
+    const double* ce = centers + 3 * (size_t)e;
+    int fine = 0;
+    if (have_focus) {
+      const double dx = ce[0] - focus[0], dy = ce[1] - focus[1], dz = ce[2] - focus[2];
+      fine = sqrt(dx * dx + dy * dy + dz * dz) < fine_radius;
+    }
+    const int nq = fine ? nq_fine[e] : nq_base[e];
+    const size_t o = fine ? of : ob;
+    const double* X = (fine ? xf : xb) + 3 * o;
+    const double* Nn = (fine ? nf : nb) + 3 * o;
+    const double* W = (fine ? wf : wb) + o;
+    const double* N = (fine ? Nf : Nb) + o * nd;
+    double* l = loc + (size_t)(e - e0) * nd;
+    for (int a = 0; a < nd; ++a) l[a] = 0.0;
+    for (int q = 0; q < nq; ++q) {
+      double v, g[3];
+      superpose_one(src6, n_src, alpha, rcp, X + 3 * q, t, cull, &v, g);
+      const double* n = Nn + 3 * q;
+      const double gq = -k * (g[0] * n[0] + g[1] * n[1] + g[2] * n[2]) * W[q];
+      for (int a = 0; a < nd; ++a) l[a] += gq * N[(size_t)q * nd + a];
+    }
+    ob += (size_t)nq_base[e];
+    of += (size_t)nq_fine[e];
+  }
+}

@@ -47,6 +47,15 @@ void or_boundary_load(int n_fe, int n_dofs, const int* nq_base, const int* nq_fi
                       int n_full, double t, double fine_radius, double cull, double k,
                       double rho, double c, double* load);
 
+/* Element-local loads of face elements [e0, e1) (assembly.cpp:126-139), no
+ * scatter: loc[(e - e0) * n_dofs + a]. */
+void or_boundary_local(int n_fe, int n_dofs, const int* nq_base, const int* nq_fine,
+                       const double* centers, const double* xb, const double* nb,
+                       const double* wb, const double* Nb, const double* xf, const double* nf,
+                       const double* wf, const double* Nf, int n_src, const double* src6,
+                       double t, double fine_radius, double cull, double k, double rho, double c,
+                       int e0, int e1, double* loc);
+
 #ifdef __cplusplus
 }
 #endif

@@ -362,6 +362,25 @@ class COracle:
                                   _ptr(x), tol, max_iter, C.byref(it), C.byref(rel))
         return x, it.value, rel.value, rc
 
+    def boundary_local(self, fs, sources, t, e0, e1, *, fine_radius, conductivity, density,
+                       heat_capacity, cull=60.0, **_):
+        """Local loads of face elements [e0, e1) ((e1 - e0), n_dofs) — no scatter."""
+        L = self.L
+        if not getattr(L, "_local_bound", False):
+            L.or_boundary_local.argtypes = [C.c_int, C.c_int, _ip, _ip] + [_dp] * 9 + [
+                C.c_int, _dp] + [C.c_double] * 6 + [C.c_int, C.c_int, _dp]
+            L._local_bound = True
+        ne, nd = fs["dofs"].shape
+        arr = {k: np.ascontiguousarray(v) for k, v in fs.items()}
+        s = np.ascontiguousarray(sources, dtype=np.float64)
+        loc = np.zeros((max(0, e1 - e0), nd))
+        L.or_boundary_local(ne, nd, _ptr(arr["nqb"], _ip), _ptr(arr["nqf"], _ip),
+                            _ptr(arr["centers"]), _ptr(arr["xb"]), _ptr(arr["nb"]),
+                            _ptr(arr["wb"]), _ptr(arr["Nb"]), _ptr(arr["xf"]), _ptr(arr["nf"]),
+                            _ptr(arr["wf"]), _ptr(arr["Nf"]), len(s), _ptr(s), t, fine_radius,
+                            cull, conductivity, density, heat_capacity, e0, e1, _ptr(loc))
+        return loc
+
     def boundary_load(self, fs, sources, t, *, fine_radius, n_full, conductivity, density,
                       heat_capacity, cull=60.0, **_):
         """assemble_flux_load restated (face sets as exported by RefSim.face_sets)."""

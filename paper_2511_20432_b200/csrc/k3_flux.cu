@@ -39,11 +39,13 @@ __global__ void k3_point_index_kernel(FaceTables ft, const int* __restrict__ fin
   elem_off[e] = is_fine ? -(off + 1) : off;  // the sign carries the rule
 }
 
-__global__ void k3_local_kernel(FaceTables ft, const int* __restrict__ elem_off,
+__global__ void k3_local_kernel(FaceTables ft, int e_begin, int e_end,
+                                const int* __restrict__ elem_off,
                                 const double* __restrict__ gq, double* __restrict__ loc) {
-  const long t = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x;
   const int ndk = ft.ndk;
-  if (t >= static_cast<long>(ft.n_fe) * ndk) return;
+  const long t = e_begin * static_cast<long>(ndk) + blockIdx.x * static_cast<long>(blockDim.x) +
+                 threadIdx.x;
+  if (t >= static_cast<long>(e_end) * ndk) return;
   const int e = static_cast<int>(t / ndk), a = static_cast<int>(t % ndk);
   const int eo = elem_off[e];
   const bool fine = eo < 0;
@@ -72,11 +74,12 @@ void k3_point_index(const FaceTables& ft, const int* d_fine, const int* d_extra,
                                                               d_pt_index, d_elem_off);
 }
 
-void k3_local(const FaceTables& ft, const int* d_elem_off, const double* d_gq, double* d_loc,
-              cudaStream_t s) {
-  const long n = static_cast<long>(ft.n_fe) * ft.ndk;
+void k3_local(const FaceTables& ft, int e_begin, int e_end, const int* d_elem_off,
+              const double* d_gq, double* d_loc, cudaStream_t s) {
+  const long n = static_cast<long>(e_end - e_begin) * ft.ndk;
   if (n <= 0) return;
-  k3_local_kernel<<<static_cast<int>((n + 255) / 256), 256, 0, s>>>(ft, d_elem_off, d_gq, d_loc);
+  k3_local_kernel<<<static_cast<int>((n + 255) / 256), 256, 0, s>>>(ft, e_begin, e_end,
+                                                                   d_elem_off, d_gq, d_loc);
 }
 
 void k3_gather(int n, const int* d_ptr, const int* d_src, const double* d_loc, double* d_F,

@@ -354,7 +354,7 @@ int Sim::fine_elements(double t, double radius) {
   return nf;
 }
 
-void Sim::flux_load_device(double t, double radius, double* d_F) {
+void Sim::flux_load_device(double t, double radius, double* d_F, int e0, int e1) {
   cudaStream_t s = ctx->stream;
   // the pinned fine list is reused every step: order the last copy first
   TG_CUDA(cudaStreamSynchronize(s));
@@ -369,16 +369,33 @@ void Sim::flux_load_device(double t, double radius, double* d_F) {
   if (nf > 0) TG_CUDA(cudaMemcpyAsync(d_fine.p, h_fine, sizeof(int) * nf, cudaMemcpyHostToDevice, s));
   TG_CUDA(cudaMemcpyAsync(d_fine.p + n_fe + 1, extra, sizeof(int) * (nf + 1),
                           cudaMemcpyHostToDevice, s));
-  const long n_pts = static_cast<long>(h_qb_off.back()) + extra[nf];
+  // compact-list offset of element e: its base offset plus the extra points
+  // of the fine elements before it
+  auto offset_of = [&](int e) {
+    const int r = static_cast<int>(std::lower_bound(h_fine, h_fine + nf, e) - h_fine);
+    return static_cast<long>(h_qb_off[e]) + extra[r];
+  };
+  e0 = std::max(0, std::min(e0, n_fe));
+  e1 = std::max(e0, std::min(e1, n_fe));
+  const long p0 = offset_of(e0), p1 = e1 == n_fe ? h_qb_off.back() + extra[nf] : offset_of(e1);
   const FaceTables ft{n_fe, ndk, d_qb_off.p, d_qf_off.p, d_Nb.p, d_Nf.p};
   k3_point_index(ft, d_fine.p, d_fine.p + n_fe + 1, nf, d_pt_index.p, d_elem_off.p, s);
   ++ctx->timer.launches;
-  K1Flux fl{d_pt_index.p, d_qn.p, d_qw.p, cfg.material.conductivity};
-  k1_run(ctx, ctx->src6.p, ctx->n_src, d_qx.p, d_pt_index.p, n_pts, t,
-         cfg.superpose.cull_exponent, K1Mode::flux, d_gq.p, nullptr, fl, s);
-  k3_local(ft, d_elem_off.p, d_gq.p, d_loc.p, s);
-  k3_gather(n_full, d_inc_ptr.p, d_inc_src.p, d_loc.p, d_F, s);
-  ctx->timer.launches += 2;
+  K1Flux fl{d_pt_index.p + p0, d_qn.p, d_qw.p, cfg.material.conductivity};
+  k1_run(ctx, ctx->src6.p, ctx->n_src, d_qx.p, d_pt_index.p + p0, p1 - p0, t,
+         cfg.superpose.cull_exponent, K1Mode::flux, d_gq.p + p0, nullptr, fl, s);
+  k3_local(ft, e0, e1, d_elem_off.p, d_gq.p, d_loc.p, s);
+  ++ctx->timer.launches;
+  if (d_F) {
+    k3_gather(n_full, d_inc_ptr.p, d_inc_src.p, d_loc.p, d_F, s);
+    ++ctx->timer.launches;
+  }
+  TG_CUDA(cudaGetLastError());
+}
+
+void Sim::flux_gather_device(const double* d_loc_all, double* d_F) {
+  k3_gather(n_full, d_inc_ptr.p, d_inc_src.p, d_loc_all, d_F, ctx->stream);
+  ++ctx->timer.launches;
   TG_CUDA(cudaGetLastError());
 }
 

@@ -40,7 +40,11 @@ class Sim {
   PcgStatus advance();   // one step: F_{n+1}, g_{n+1}, theta step
 
   // drop-in pieces on device buffers
-  void flux_load_device(double t, double radius, double* d_F);
+  // assemble_flux_load; with [e0, e1) only those face elements' local loads
+  // (d_loc) are computed, and d_F == nullptr skips the gather (sharded use)
+  void flux_load_device(double t, double radius, double* d_F, int e0 = 0,
+                        int e1 = 1 << 30);
+  void flux_gather_device(const double* d_loc_all, double* d_F);
   void dirichlet_device(double t, double* d_g);
   PcgStatus theta_step_device(double tol, int max_iter);  // uses d_x, d_gn, d_g1, d_Fn, d_F1
 

@@ -216,6 +216,53 @@ int tg_sim_state(tg_sim* s, int* step, double* time, double* free_out, double* g
   });
 }
 
+int tg_sim_flux_local_device(tg_sim* s, double t, double fine_radius, int e0, int e1,
+                             double* d_loc) {
+  return sim_guard(s, [&](Sim& m) {
+    const double r = fine_radius < 0.0 ? m.cfg.mesh.elevate_radius : fine_radius;
+    if (e0 < 0 || e1 < e0 || e1 > m.n_fe) throw std::invalid_argument("flux_local: bad range");
+    m.flux_load_device(t, r, nullptr, e0, e1);
+    if (e1 > e0)
+      TG_CUDA(cudaMemcpyAsync(d_loc, m.d_loc.p + static_cast<size_t>(e0) * m.ndk,
+                              sizeof(double) * (e1 - e0) * m.ndk, cudaMemcpyDeviceToDevice,
+                              m.ctx->stream));
+    TG_CUDA(cudaStreamSynchronize(m.ctx->stream));
+  });
+}
+
+int tg_sim_flux_gather_device(tg_sim* s, const double* d_loc_all, double* d_F) {
+  return sim_guard(s, [&](Sim& m) {
+    m.flux_gather_device(d_loc_all, d_F);
+    TG_CUDA(cudaStreamSynchronize(m.ctx->stream));
+  });
+}
+
+int tg_sim_operator_apply_slab_device(tg_sim* s, int k0, int k1, const double* d_x,
+                                      double* d_y) {
+  return sim_guard(s, [&](Sim& m) {
+    if (!m.kron) throw std::invalid_argument("slab apply needs the Kronecker operator");
+    const int p = m.gfree.p, W = 2 * p + 1, nz = m.gfree.n[2];
+    if (k0 < 0 || k1 > nz || k1 <= k0) throw std::invalid_argument("slab apply: bad planes");
+    const int g0 = std::max(0, k0 - p), g1 = std::min(nz, k1 + p);
+    KronGrid slab = m.gfree;
+    slab.n[2] = g1 - g0;
+    slab.M[2] += static_cast<size_t>(g0) * W;
+    slab.K[2] += static_cast<size_t>(g0) * W;
+    const size_t plane = static_cast<size_t>(slab.n[0]) * slab.n[1];
+    double* tmp = m.d_Ap.p;  // n_free >= slab size
+    k2_apply(slab, m.coefA[0], m.coefA[1], d_x, tmp, m.ctx->sm_count, m.ctx->stream);
+    TG_CUDA(cudaMemcpyAsync(d_y, tmp + (k0 - g0) * plane, sizeof(double) * (k1 - k0) * plane,
+                            cudaMemcpyDeviceToDevice, m.ctx->stream));
+    TG_CUDA(cudaStreamSynchronize(m.ctx->stream));
+  });
+}
+
+int tg_sim_inverse_diagonal(tg_sim* s, double* out) {
+  return sim_guard(s, [&](Sim& m) {
+    TG_CUDA(cudaMemcpy(out, m.d_invd.p, sizeof(double) * m.n_free, cudaMemcpyDeviceToHost));
+  });
+}
+
 int tg_sim_debug_trace(tg_sim* s, unsigned long long* out, int n) {
   return sim_guard(s, [&](Sim& m) {
     TG_CUDA(cudaMemcpy(out, m.d_trace.p, sizeof(unsigned long long) * std::min(n, 400),
