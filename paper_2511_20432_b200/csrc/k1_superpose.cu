@@ -76,7 +76,7 @@ __global__ void k1_prepare_sources(const double* __restrict__ src6, int n, doubl
 }
 
 template <int P, bool GRAD>
-__global__ void __launch_bounds__(kK1Threads, P >= 4 ? 2 : 3)
+__global__ void __launch_bounds__(kK1Threads, P >= 6 ? 1 : (P >= 4 ? 2 : 3))
     k1_partial(const SrcRec* __restrict__ src, int n_src, int split_len,
                const double* __restrict__ pts, const int* __restrict__ pt_index, int n_pts,
                double* __restrict__ part) {
@@ -268,21 +268,18 @@ void k1_launch_partial(const SrcRec* d_rec, int n_src, const double* d_pts,
   const int split_len = (n_src + S - 1) / S;
   const int ppc = kK1Threads * P;
   dim3 grid((n_pts + ppc - 1) / ppc, S);
-  if (grad) {
-    if (P == 1)
-      k1_partial<1, true><<<grid, kK1Threads, 0, stream>>>(d_rec, n_src, split_len, d_pts, d_index, n_pts, d_part);
-    else if (P == 4)
-      k1_partial<4, true><<<grid, kK1Threads, 0, stream>>>(d_rec, n_src, split_len, d_pts, d_index, n_pts, d_part);
-    else
-      k1_partial<2, true><<<grid, kK1Threads, 0, stream>>>(d_rec, n_src, split_len, d_pts, d_index, n_pts, d_part);
-  } else {
-    if (P == 1)
-      k1_partial<1, false><<<grid, kK1Threads, 0, stream>>>(d_rec, n_src, split_len, d_pts, d_index, n_pts, d_part);
-    else if (P == 4)
-      k1_partial<4, false><<<grid, kK1Threads, 0, stream>>>(d_rec, n_src, split_len, d_pts, d_index, n_pts, d_part);
-    else
-      k1_partial<2, false><<<grid, kK1Threads, 0, stream>>>(d_rec, n_src, split_len, d_pts, d_index, n_pts, d_part);
+#define TG_K1_LAUNCH(PP, GG)                                                              \
+  k1_partial<PP, GG><<<grid, kK1Threads, 0, stream>>>(d_rec, n_src, split_len, d_pts, d_index, \
+                                                      n_pts, d_part)
+  switch (P) {
+    case 1: if (grad) TG_K1_LAUNCH(1, true); else TG_K1_LAUNCH(1, false); break;
+    case 2: if (grad) TG_K1_LAUNCH(2, true); else TG_K1_LAUNCH(2, false); break;
+    case 3: if (grad) TG_K1_LAUNCH(3, true); else TG_K1_LAUNCH(3, false); break;
+    case 6: if (grad) TG_K1_LAUNCH(6, true); else TG_K1_LAUNCH(6, false); break;
+    case 8: if (grad) TG_K1_LAUNCH(8, true); else TG_K1_LAUNCH(8, false); break;
+    default: if (grad) TG_K1_LAUNCH(4, true); else TG_K1_LAUNCH(4, false); break;
   }
+#undef TG_K1_LAUNCH
 }
 
 void k1_launch_combine_field(const double* d_part, int S, int n, double* d_val, double* d_grad,
