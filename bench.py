@@ -46,6 +46,11 @@ sys.path.insert(0, ROOT)
 from paper_2511_20432_b200 import workloads as W  # noqa: E402
 
 FLOPS_PER_PAIR = 49.0  # value + gradient, exp counted at libdevice cost
+# FP64-pipe instructions per pair actually issued by k1_partial's fast path
+# (cuobjdump -sass of k1_partial<4,true>: 11 DFMA + 5 DADD + 3 DMUL; the table
+# exp costs 7 of them where libdevice costs 17, so the 49-flop accounting can
+# exceed the DFMA peak — fp64_pipe reports the issued-instruction fraction).
+PIPE_OPS_PER_PAIR = 19.0
 
 
 def parse():
@@ -374,6 +379,13 @@ def run_ours(args):
             "peak_source": "measured live: tg_fp64_peak DFMA-chain microbenchmark on this GPU",
             "flops_per_pair": FLOPS_PER_PAIR, "pairs_per_launch": pairs_per_launch,
             "mean_launch_ms": k1_mean_ms,
+            "fp64_pipe": {
+                "ops_per_pair": PIPE_OPS_PER_PAIR,
+                "achieved_gops": (PIPE_OPS_PER_PAIR * pairs_per_launch / (k1_mean_ms * 1e-3) / 1e9
+                                  if k1_mean_ms else None),
+                "peak_gops": fp64_peak * 1e3 / 2 if fp64_peak else None,
+                "frac": (PIPE_OPS_PER_PAIR * pairs_per_launch / (k1_mean_ms * 1e-3) /
+                         (fp64_peak * 1e12 / 2)) if (k1_mean_ms and fp64_peak) else None},
             "k1_share_of_step": prof["k1_ms"] / max(1e-9, float(sum(step_ms)))}
     line = {
         "metric": "source x point pair evals/s (superpose, value+grad)",

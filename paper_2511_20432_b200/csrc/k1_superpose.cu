@@ -16,9 +16,11 @@
 //
 // Exactness: the causality test (t - tau > 0), the spread 4*alpha*dt and the
 // cull decision fl(r.r / spread) > cull reproduce the reference's discrete
-// choices bit for bit: r.r is formed with the reference's association and no
-// FMA, and the cull threshold thr_j is the largest double a with
-// fl(a / spread_j) <= cull, found with IEEE division in the prologue.
+// choices bit for bit: the cull threshold thr_j is the largest double a with
+// fl(a / spread_j) <= cull, found with IEEE division in the prologue; the
+// per-pair decision compares the high words of an FMA-formed r.r with thr_j's
+// and, only inside the +-1 high-word band, re-forms r.r with the reference's
+// association and no FMA for the exact compare.
 #include <cmath>
 
 #include "common.cuh"
@@ -38,7 +40,6 @@ __global__ void k1_prepare_sources(const double* __restrict__ src6, int n, doubl
   r.sx = s[0];
   r.sy = s[1];
   r.sz = s[2];
-  r.pad = 0.0;
   const double E = s[3];
   const double dt = __dsub_rn(t, s[5]);  // analytic.cpp:97
   bool active = dt > 0.0 && E > 0.0;     // E == 0 contributes exact zeros
@@ -72,6 +73,8 @@ __global__ void k1_prepare_sources(const double* __restrict__ src6, int n, doubl
   r.lnc = lnc;
   r.gfac = active ? -1.0 / __dmul_rn(alpha2, dt) : 0.0;
   r.thr = thr;
+  r.thr_lo = __double2hiint(thr) - 1;
+  r.thr_hi = __double2hiint(thr) + 1;
   out[j] = r;
 }
 
@@ -129,26 +132,45 @@ __global__ void __launch_bounds__(kK1Threads, P >= 6 ? 1 : (P >= 4 ? 2 : 3))
 #pragma unroll 2
     for (int j = 0; j < cnt; ++j) {
       const double4 a = *reinterpret_cast<const double4*>(&rb[j].sx);   // sx sy sz nis
-      const double4 b = *reinterpret_cast<const double4*>(&rb[j].lnc);  // lnc gfac thr pad
+      const double4 b = *reinterpret_cast<const double4*>(&rb[j].lnc);  // lnc gfac thr band
+      const int lo = __double2loint(b.w), hi = __double2hiint(b.w);     // thr_lo, thr_hi
+      double rx[P], ry[P], rz[P], r2[P];
+      bool keep[P];
+      bool amb = false;
 #pragma unroll
       for (int k = 0; k < P; ++k) {
-        const double rx = __dsub_rn(px[k], a.x);
-        const double ry = __dsub_rn(py[k], a.y);
-        const double rz = __dsub_rn(pz[k], a.z);
-        // r.r with the reference's association (core.hpp:27), no contraction
-        const double r2 =
-            __dadd_rn(__dadd_rn(__dmul_rn(rx, rx), __dmul_rn(ry, ry)), __dmul_rn(rz, rz));
-        const double e = fast_exp(__fma_rn(r2, a.w, b.x), tab);
-        // r2 <= thr on the bit patterns (r2 >= 0; thr < 0 marks an inactive
-        // source): an integer compare keeps the decision off the FP64 pipe
-        const double T =
-            (__double_as_longlong(r2) <= __double_as_longlong(b.z)) ? e : 0.0;
+        rx[k] = __dsub_rn(px[k], a.x);
+        ry[k] = __dsub_rn(py[k], a.y);
+        rz[k] = __dsub_rn(pz[k], a.z);
+        // r.r with FMA (3 roundings of non-negative terms: within a few ulp of
+        // the reference's 5-rounding r.r, core.hpp:27)
+        r2[k] = __fma_rn(rz[k], rz[k], __fma_rn(ry[k], ry[k], __dmul_rn(rx[k], rx[k])));
+        // keep/cull decided on the high words (1 unit = 2^32 ulp >> the few-ulp
+        // gap): thr < 0 (inactive source) lands in the cull branch
+        const int h = __double2hiint(r2[k]);
+        keep[k] = h < lo;
+        amb |= (h >= lo) & (h <= hi);
+      }
+      if (__any_sync(0xffffffffu, amb)) {  // warp-uniform branch, no reconvergence stack
+        // rare band |hi32(r.r) - hi32(thr)| <= 1: the reference's exact r.r
+        // (association of core.hpp:27, no contraction) and its exact compare
+#pragma unroll
+        for (int k = 0; k < P; ++k) {
+          const double e2 = __dadd_rn(__dadd_rn(__dmul_rn(rx[k], rx[k]), __dmul_rn(ry[k], ry[k])),
+                                      __dmul_rn(rz[k], rz[k]));
+          keep[k] = __double_as_longlong(e2) <= __double_as_longlong(b.z);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < P; ++k) {
+        const double e = fast_exp(__fma_rn(r2[k], a.w, b.x), tab);
+        const double T = keep[k] ? e : 0.0;
         v[k] = __dadd_rn(v[k], T);
         if (GRAD) {
           const double w = __dmul_rn(T, b.y);
-          gx[k] = __fma_rn(rx, w, gx[k]);
-          gy[k] = __fma_rn(ry, w, gy[k]);
-          gz[k] = __fma_rn(rz, w, gz[k]);
+          gx[k] = __fma_rn(rx[k], w, gx[k]);
+          gy[k] = __fma_rn(ry[k], w, gy[k]);
+          gz[k] = __fma_rn(rz[k], w, gz[k]);
         }
       }
     }

@@ -13,7 +13,7 @@ struct __align__(16) SrcRec {
   double lnc;         // log(E / (rho c (pi spread)^1.5))
   double gfac;        // -1 / (2 alpha (t - tau))
   double thr;         // keep the pair iff r.r <= thr (cull and causality folded in)
-  double pad;
+  int thr_lo, thr_hi; // hi32(thr) - 1, hi32(thr) + 1: the fast-decision band
 };
 static_assert(sizeof(SrcRec) == 64, "SrcRec must stay 64 bytes");
 

@@ -98,6 +98,30 @@ def test_cull_boundary_and_zero_pattern(gpu_ctx, coracle):
         check_field(v, g, vo, go)
 
 
+def test_single_pair_cull_decision_ulp_exact(gpu_ctx, coracle):
+    """One source, points whose r.r lands within a few ulp of cull*spread: each
+    point's value is non-zero iff its single pair is kept, so the zero pattern
+    pins the per-pair decision fl(r.r / spread) > cull (analytic.cpp:103)
+    against the reference arithmetic, including the kernel's high-word band."""
+    src = coracle.discretize_scan([[1e-3, 1e-3], [1.1e-3, 1e-3]], plane_z=1e-3, **KW)[:1]
+    t = float(src[0, 5]) + 3e-5
+    alpha = MAT.diffusivity()
+    spread = 4.0 * alpha * (t - float(src[0, 5]))
+    rng = np.random.default_rng(3)
+    gpu_ctx.set_sources(src, MAT)
+    for cull in (60.0, 7.5, 1e-3):
+        r = np.sqrt(cull * spread) * (1 + rng.integers(-40, 41, 4096) * 2.0**-53)
+        d = rng.standard_normal((4096, 3))
+        d /= np.linalg.norm(d, axis=1, keepdims=True)
+        pts = src[0, :3] + d * r[:, None]
+        v, g = gpu_ctx.superpose(pts, t, tg.SuperposeOptions(cull))
+        vo, go = coracle.superpose(src, pts, t, cull=cull, **KW)
+        kept = vo != 0.0
+        assert 0 < kept.sum() < len(kept), "sample must straddle the threshold"
+        assert np.array_equal(v != 0.0, kept)
+        check_field(v, g, vo, go)
+
+
 def test_cull_invariance_and_no_cull(gpu_ctx, coracle):
     # proj/tests/test_analytic.cpp:178-189
     kw = dict(conductivity=42.0, density=4420.0, heat_capacity=990.0, power=82.5, speed=0.5,

@@ -26,7 +26,7 @@ p = ctx.profile()
 ms = p["k1_ms"] / p["k1_launches"]
 print(json.dumps({"P": os.environ.get("TG_K1_P"), "k1_ms": ms, "pairs_per_s": 2**20 * 2**16 / (ms * 1e-3)}))
 '''
-for P in ("3", "4", "6", "8"):
+for P in ("2", "3", "4", "6", "8"):
     env = dict(os.environ, TG_K1_P=P, ROOT=ROOT)
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True)
     print(r.stdout.strip() or r.stderr[-2000:])
