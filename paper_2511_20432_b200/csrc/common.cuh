@@ -1,5 +1,5 @@
 // Shared device helpers for the sm_100a kernels: exact-rounding arithmetic
-// wrappers, the table-driven fp64 exp used by the point-source kernels, and
+// wrappers, the table-driven fp64 exponential of the point-source kernels, and
 // the TMA bulk-copy / mbarrier primitives that stage source tiles in shared
 // memory.
 #pragma once
@@ -10,40 +10,48 @@
 namespace tgb {
 
 // ---------------------------------------------------------------------------
-// Table-driven exp(x) for x in [-708, 709], relative error < 1e-13.
+// Point-source exponential exp(lnc - r2 / spread), relative error < 1.7e-12.
 //
-// x = (256 m + j) ln2/256 + r,  |r| <= ln2/512, j in [0,256)
-// exp(x) = 2^m * 2^(j/256) * p(r),  p(r) = 1 + r + r^2 (c2 + c3 r)
+// In units of ln2/1024 the exponent is y = r2 * nis' + lnc' with
+// nis' = -(1024/ln2)/spread and lnc' = (1024/ln2) lnc, both per source.
+// Per source, lnc' = L + l with L an integer and |l| <= 1/2; the factor
+// C = 2^(l/1024) = exp(lnc - L ln2/1024) is folded into the polynomial:
 //
-// 7 FP64-pipe instructions (1 DFMA + 1 DADD + 1 DFMA range reduction, 3 DFMA
-// polynomial, 1 DMUL table product) plus integer ops for j, m and the
-// exponent add. The cubic is a Chebyshev fit of (e^r - 1 - r)/r^2 on
-// [-ln2/512, ln2/512]: max relative error 7.0e-14 (mpmath), three orders
-// below the 1e-10 parity tolerance (BASELINE.json north_star); the
-// single-constant reduction adds < 2e-15 for |x| <= 80.
+//   k  = rint(r2 nis' + L)            (one DFMA against A = L + 1.5*2^52)
+//   f  = r2 nis' + (L - k)            (exact integer L - k, one DFMA)
+//   exp(..) = 2^(k >> 10) * 2^((k & 1023)/1024) * C 2^(f/1024),  |f| <= 1/2
+//   C 2^(f/1024) ~= q0 + q1 f + q2 f^2 (q_i = C d_i, per source)
+//
+// 6 FP64-pipe instructions including the argument (3 DFMA + 1 DADD range
+// reduction, 2 DFMA quadratic) plus 1 DMUL by the 2^(j/1024) table entry;
+// 2^(k>>10) is an integer add into the exponent field. d_i is the relative
+// minimax quadratic of exp(u) on |u| <= ln2/2048 in the variable f = 1024 u/ln2
+// (Remez, mpmath): max relative error 1.62e-12, 60x below the 1e-10 parity
+// tolerance (BASELINE.json north_star); the folded per-source rounding adds
+// < 1e-15.
 // ---------------------------------------------------------------------------
-constexpr int kExpBits = 8;
+constexpr int kExpBits = 10;
 constexpr int kExpTableSize = 1 << kExpBits;
-constexpr double kExpInvStep = 369.32993046757462707;    // 256 / ln 2
-constexpr double kExpStep = 0.0027076061740622863;       // ln 2 / 256
-constexpr double kExpMagic = 6755399441055744.0;         // 1.5 * 2^52
-constexpr double kExpC2 = 0x1.00000147fd40ap-1;
-constexpr double kExpC3 = 0x1.5555565bb988ep-3;
+constexpr double kExpInvStep = 0x1.71547652b82fep+10;   // 1024 / ln2
+constexpr double kExpStepHi = 0x1.62e42fefa39efp-11;    // ln2 / 1024 (hi)
+constexpr double kExpStepLo = 0x1.abc9e3b39803fp-66;    // ln2 / 1024 (lo)
+constexpr double kExpMagic = 6755399441055744.0;        // 1.5 * 2^52
+constexpr double kExpD0 = 0x1.0000000000002p+0;
+constexpr double kExpD1 = 0x1.62e43044e4b97p-11;
+constexpr double kExpD2 = 0x1.ebfbdfbd1456bp-23;
 
-// exp(x) with the 2^(j/256) table in shared memory.
-__device__ __forceinline__ double fast_exp(double x, const double* __restrict__ tab) {
-  const double kf = __fma_rn(x, kExpInvStep, kExpMagic);
-  const double n = __dsub_rn(kf, kExpMagic);
+// e = exp(lnc - r2/spread) from the per-source constants (nisp = nis',
+// magicL = L + 1.5*2^52, q0..q2) and the shared 2^(j/1024) table.
+__device__ __forceinline__ double src_exp(double r2, double nisp, double magicL, double q0,
+                                          double q1, double q2,
+                                          const double* __restrict__ tab) {
+  const double kf = __fma_rn(r2, nisp, magicL);
+  const double d = __dsub_rn(magicL, kf);  // L - k, exact
+  const double f = __fma_rn(r2, nisp, d);
+  const double q = __fma_rn(__fma_rn(q2, f, q1), f, q0);
   const int ki = __double2loint(kf);
-  const double r = __fma_rn(n, -kExpStep, x);
-  double p = __fma_rn(kExpC3, r, kExpC2);
-  p = __fma_rn(p, r, 1.0);
-  p = __fma_rn(p, r, 1.0);
-  const double t = tab[ki & (kExpTableSize - 1)];
-  const double e = __dmul_rn(t, p);
-  // scale by 2^m: integer add into the exponent field of the high word
-  const int m = ki >> kExpBits;
-  const int hi = __double2hiint(e) + (m << 20);
+  const double e = __dmul_rn(tab[ki & (kExpTableSize - 1)], q);
+  const int hi = __double2hiint(e) + ((ki >> kExpBits) << 20);
   return __hiloint2double(hi, __double2loint(e));
 }
 

@@ -3,7 +3,7 @@
 //
 // Layout and schedule (sm_100a):
 //   * per call, k1_prepare_sources turns the history {x, y, z, E, t_act, tau}
-//     into 64-byte SrcRec records holding every per-source, per-time constant
+//     into 96-byte SrcRec records holding every per-source, per-time constant
 //     (the reference recomputes pow(pi*spread, 1.5) per pair, analytic.cpp:104);
 //   * k1_partial: one thread owns P points (registers), a CTA owns 256*P points
 //     and one contiguous source range; source records stream through a 3-stage
@@ -59,9 +59,9 @@ __global__ void k1_prepare_sources(const double* __restrict__ src6, int n, doubl
       }
     }
     // keep exp(lnc - r2/spread) in the normal range: contributions below
-    // 2^-1021 relative to nothing are flushed (only reachable without culling)
+    // e^-707 relative to nothing are flushed (only reachable without culling)
     const double lim = (lnc + 707.0) * spread;
-    if (!(lim > 0.0) || !isfinite(lnc)) active = false;
+    if (!(lim > 0.0) || !(lnc < 709.0)) active = false;
     thr = fmin(a, lim);
   }
   if (!active) {
@@ -69,12 +69,21 @@ __global__ void k1_prepare_sources(const double* __restrict__ src6, int n, doubl
     lnc = 0.0;
     thr = -1.0;
   }
-  r.nis = active ? -1.0 / spread : 0.0;
-  r.lnc = lnc;
+  // exponent constants of src_exp (common.cuh)
+  const double L = rint(__dmul_rn(lnc, kExpInvStep));
+  double u = __fma_rn(-L, kExpStepHi, lnc);
+  u = __fma_rn(-L, kExpStepLo, u);
+  const double C = exp(u);
+  r.nisp = active ? -kExpInvStep / spread : 0.0;
+  r.magicL = __dadd_rn(L, kExpMagic);
   r.gfac = active ? -1.0 / __dmul_rn(alpha2, dt) : 0.0;
   r.thr = thr;
   r.thr_lo = __double2hiint(thr) - 1;
   r.thr_hi = __double2hiint(thr) + 1;
+  r.q0 = __dmul_rn(C, kExpD0);
+  r.q1 = __dmul_rn(C, kExpD1);
+  r.q2 = __dmul_rn(C, kExpD2);
+  r.pad = 0.0;
   out[j] = r;
 }
 
@@ -83,7 +92,7 @@ __global__ void __launch_bounds__(kK1Threads, P >= 6 ? 1 : (P >= 4 ? 2 : 3))
     k1_partial(const SrcRec* __restrict__ src, int n_src, int split_len,
                const double* __restrict__ pts, const int* __restrict__ pt_index, int n_pts,
                double* __restrict__ part) {
-  __shared__ __align__(16) SrcRec ring[kK1Stages][kK1Chunk];
+  __shared__ __align__(128) SrcRec ring[kK1Stages][kK1Chunk];
   __shared__ double tab[kExpTableSize];
   __shared__ __align__(8) uint64_t bars[kK1Stages];
 
@@ -131,8 +140,9 @@ __global__ void __launch_bounds__(kK1Threads, P >= 6 ? 1 : (P >= 4 ? 2 : 3))
     const SrcRec* rb = ring[buf];
 #pragma unroll 2
     for (int j = 0; j < cnt; ++j) {
-      const double4 a = *reinterpret_cast<const double4*>(&rb[j].sx);   // sx sy sz nis
-      const double4 b = *reinterpret_cast<const double4*>(&rb[j].lnc);  // lnc gfac thr band
+      const double4 a = *reinterpret_cast<const double4*>(&rb[j].sx);      // sx sy sz nisp
+      const double4 b = *reinterpret_cast<const double4*>(&rb[j].magicL);  // magicL gfac thr band
+      const double4 q = *reinterpret_cast<const double4*>(&rb[j].q0);      // q0 q1 q2 -
       const int lo = __double2loint(b.w), hi = __double2hiint(b.w);     // thr_lo, thr_hi
       double rx[P], ry[P], rz[P], r2[P];
       bool keep[P];
@@ -163,7 +173,7 @@ __global__ void __launch_bounds__(kK1Threads, P >= 6 ? 1 : (P >= 4 ? 2 : 3))
       }
 #pragma unroll
       for (int k = 0; k < P; ++k) {
-        const double e = fast_exp(__fma_rn(r2[k], a.w, b.x), tab);
+        const double e = src_exp(r2[k], a.w, b.x, q.x, q.y, q.z, tab);
         const double T = keep[k] ? e : 0.0;
         v[k] = __dadd_rn(v[k], T);
         if (GRAD) {

@@ -6,19 +6,22 @@
 
 namespace tgb {
 
-// Per-source, per-time constants; 64 bytes so one TMA bulk copy moves a tile.
-struct __align__(16) SrcRec {
+// Per-source, per-time constants (see src_exp in common.cuh); 96 bytes, read
+// as three 32-byte broadcasts.
+struct __align__(32) SrcRec {
   double sx, sy, sz;  // position (m)
-  double nis;         // -1 / spread, spread = 4 alpha (t - tau)
-  double lnc;         // log(E / (rho c (pi spread)^1.5))
+  double nisp;        // -(1024/ln2) / spread, spread = 4 alpha (t - tau)
+  double magicL;      // L + 1.5*2^52, L = rint((1024/ln2) log c), c = E/(rho c (pi spread)^1.5)
   double gfac;        // -1 / (2 alpha (t - tau))
   double thr;         // keep the pair iff r.r <= thr (cull and causality folded in)
   int thr_lo, thr_hi; // hi32(thr) - 1, hi32(thr) + 1: the fast-decision band
+  double q0, q1, q2;  // C d_i, C = exp(log c - L ln2/1024)
+  double pad;
 };
-static_assert(sizeof(SrcRec) == 64, "SrcRec must stay 64 bytes");
+static_assert(sizeof(SrcRec) == 96, "SrcRec must stay 96 bytes");
 
 constexpr int kK1Threads = 256;
-constexpr int kK1Chunk = 128;  // sources per shared-memory stage (8 KB)
+constexpr int kK1Chunk = 128;  // sources per shared-memory stage (12 KB)
 constexpr int kK1Stages = 3;
 
 void k1_upload_exp_table(cudaStream_t stream);
