@@ -47,10 +47,11 @@ from paper_2511_20432_b200 import workloads as W  # noqa: E402
 
 FLOPS_PER_PAIR = 49.0  # value + gradient, exp counted at libdevice cost
 # FP64-pipe instructions per pair actually issued by k1_partial's fast path
-# (cuobjdump -sass of k1_partial<4,true>: 11 DFMA + 5 DADD + 3 DMUL; the table
-# exp costs 7 of them where libdevice costs 17, so the 49-flop accounting can
-# exceed the DFMA peak — fp64_pipe reports the issued-instruction fraction).
-PIPE_OPS_PER_PAIR = 19.0
+# (cuobjdump -sass of k1_partial<6,true>: 9 DFMA + 5 DADD + 3 DMUL; the
+# exponential costs 6 of them with its argument where libdevice costs 18, so
+# the 49-flop accounting exceeds the DFMA peak — fp64_pipe reports the
+# issued-instruction fraction).
+PIPE_OPS_PER_PAIR = 17.0
 
 
 def parse():
@@ -371,7 +372,7 @@ def run_ours(args):
     k1_mean_ms = prof["k1_ms"] / max(1, prof["k1_launches"])
     pairs_per_launch = prof["k1_pairs"] / max(1, prof["k1_launches"])
     achieved = FLOPS_PER_PAIR * pairs_per_launch / (k1_mean_ms * 1e-3) / 1e12 if k1_mean_ms else None
-    roof = {"kernel": f"k1_partial<{os.environ.get('TG_K1_P', '4')},true>", "bound": "fp64",
+    roof = {"kernel": f"k1_partial<{os.environ.get('TG_K1_P', '6')},true>", "bound": "fp64",
             "achieved": achieved,
             "peak": fp64_peak, "unit": "TFLOP/s",
             "frac": (achieved / fp64_peak) if (achieved and fp64_peak) else None,

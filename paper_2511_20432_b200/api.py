@@ -118,9 +118,10 @@ def lib(auto_build: bool = True):
         return _LIB
     if auto_build and (not os.path.exists(_build.LIB) or os.environ.get("TG_REBUILD")):
         _build.build()
-    if not os.path.exists(_build.LIB):
-        raise CudaError(f"native library missing: {_build.LIB}")
-    L = C.CDLL(_build.LIB)
+    path = os.environ.get("TG_LIB_VARIANT") or _build.LIB  # tuning builds (tools/k1_variants.py)
+    if not os.path.exists(path):
+        raise CudaError(f"native library missing: {path}")
+    L = C.CDLL(path)
     L.tg_abi_version.restype = C.c_int
     L.tg_ctx_create.argtypes = [C.c_int, C.POINTER(C.c_void_p)]
     L.tg_ctx_destroy.argtypes = [C.c_void_p]

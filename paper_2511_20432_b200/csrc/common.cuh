@@ -23,8 +23,8 @@ namespace tgb {
 //   C 2^(f/1024) ~= q0 + q1 f + q2 f^2 (q_i = C d_i, per source)
 //
 // 6 FP64-pipe instructions including the argument (3 DFMA + 1 DADD range
-// reduction, 2 DFMA quadratic) plus 1 DMUL by the 2^(j/1024) table entry;
-// 2^(k>>10) is an integer add into the exponent field. d_i is the relative
+// reduction, 2 DFMA quadratic) plus 1 DMUL by the table entry 2^(k/1024),
+// whose 2^(k>>10) part is an integer add into the exponent field. d_i is the relative
 // minimax quadratic of exp(u) on |u| <= ln2/2048 in the variable f = 1024 u/ln2
 // (Remez, mpmath): max relative error 1.62e-12, 60x below the 1e-10 parity
 // tolerance (BASELINE.json north_star); the folded per-source rounding adds
@@ -41,7 +41,9 @@ constexpr double kExpD1 = 0x1.62e43044e4b97p-11;
 constexpr double kExpD2 = 0x1.ebfbdfbd1456bp-23;
 
 // e = exp(lnc - r2/spread) from the per-source constants (nisp = nis',
-// magicL = L + 1.5*2^52, q0..q2) and the shared 2^(j/1024) table.
+// magicL = L + 1.5*2^52, q0..q2) and the shared table. Entry j holds 2^(j/1024)
+// with (j << 10) pre-subtracted from its high word, so that adding (k << 10)
+// scales it by 2^(k >> 10) exactly (one IMAD; the entry is a bit container).
 __device__ __forceinline__ double src_exp(double r2, double nisp, double magicL, double q0,
                                           double q1, double q2,
                                           const double* __restrict__ tab) {
@@ -50,9 +52,10 @@ __device__ __forceinline__ double src_exp(double r2, double nisp, double magicL,
   const double f = __fma_rn(r2, nisp, d);
   const double q = __fma_rn(__fma_rn(q2, f, q1), f, q0);
   const int ki = __double2loint(kf);
-  const double e = __dmul_rn(tab[ki & (kExpTableSize - 1)], q);
-  const int hi = __double2hiint(e) + ((ki >> kExpBits) << 20);
-  return __hiloint2double(hi, __double2loint(e));
+  const double t = tab[ki & (kExpTableSize - 1)];
+  const double s = __hiloint2double(__double2hiint(t) + static_cast<int>(static_cast<unsigned>(ki) << (20 - kExpBits)),
+                                    __double2loint(t));  // 2^(k/1024), exact
+  return __dmul_rn(s, q);
 }
 
 // ---------------------------------------------------------------------------

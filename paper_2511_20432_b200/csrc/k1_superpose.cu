@@ -22,6 +22,7 @@
 // and, only inside the +-1 high-word band, re-forms r.r with the reference's
 // association and no FMA for the exact compare.
 #include <cmath>
+#include <cstring>
 
 #include "common.cuh"
 #include "k1_superpose.cuh"
@@ -87,8 +88,20 @@ __global__ void k1_prepare_sources(const double* __restrict__ src6, int n, doubl
   out[j] = r;
 }
 
+// tuning knobs (tools/k1_variants.py builds and times the alternatives)
+#ifndef K1_UNROLL
+#define K1_UNROLL 4
+#endif
+#ifndef K1_MINB4
+#define K1_MINB4 2
+#endif
+#ifndef K1_VOTE_LATE  // 1: exponentials before the band vote, 0: after it
+#define K1_VOTE_LATE 1
+#endif
+constexpr int kK1Unroll = K1_UNROLL;
+
 template <int P, bool GRAD>
-__global__ void __launch_bounds__(kK1Threads, P >= 6 ? 1 : (P >= 4 ? 2 : 3))
+__global__ void __launch_bounds__(kK1Threads, P >= 6 ? 1 : (P >= 4 ? K1_MINB4 : 3))
     k1_partial(const SrcRec* __restrict__ src, int n_src, int split_len,
                const double* __restrict__ pts, const int* __restrict__ pt_index, int n_pts,
                double* __restrict__ part) {
@@ -138,15 +151,15 @@ __global__ void __launch_bounds__(kK1Threads, P >= 6 ? 1 : (P >= 4 ? 2 : 3))
     mbar_wait(&bars[buf], static_cast<uint32_t>((c / kK1Stages) & 1));
     const int cnt = min(kK1Chunk, len - c * kK1Chunk);
     const SrcRec* rb = ring[buf];
-#pragma unroll 2
+#pragma unroll kK1Unroll
     for (int j = 0; j < cnt; ++j) {
       const double4 a = *reinterpret_cast<const double4*>(&rb[j].sx);      // sx sy sz nisp
       const double4 b = *reinterpret_cast<const double4*>(&rb[j].magicL);  // magicL gfac thr band
       const double4 q = *reinterpret_cast<const double4*>(&rb[j].q0);      // q0 q1 q2 -
-      const int lo = __double2loint(b.w), hi = __double2hiint(b.w);     // thr_lo, thr_hi
-      double rx[P], ry[P], rz[P], r2[P];
+      const int lo = __double2loint(b.w);  // hi32(thr) - 1
+      double rx[P], ry[P], rz[P], r2[P], e[P];
       bool keep[P];
-      bool amb = false;
+      unsigned band = 0xffffffffu;
 #pragma unroll
       for (int k = 0; k < P; ++k) {
         rx[k] = __dsub_rn(px[k], a.x);
@@ -156,14 +169,16 @@ __global__ void __launch_bounds__(kK1Threads, P >= 6 ? 1 : (P >= 4 ? 2 : 3))
         // the reference's 5-rounding r.r, core.hpp:27)
         r2[k] = __fma_rn(rz[k], rz[k], __fma_rn(ry[k], ry[k], __dmul_rn(rx[k], rx[k])));
         // keep/cull decided on the high words (1 unit = 2^32 ulp >> the few-ulp
-        // gap): thr < 0 (inactive source) lands in the cull branch
+        // gap): thr < 0 (inactive source) lands in the cull branch; the band
+        // hi32(r.r) in [lo, lo + 2] is re-decided exactly below
         const int h = __double2hiint(r2[k]);
         keep[k] = h < lo;
-        amb |= (h >= lo) & (h <= hi);
+        band = min(band, static_cast<unsigned>(h - lo));
+        if (K1_VOTE_LATE) e[k] = src_exp(r2[k], a.w, b.x, q.x, q.y, q.z, tab);
       }
-      if (__any_sync(0xffffffffu, amb)) {  // warp-uniform branch, no reconvergence stack
-        // rare band |hi32(r.r) - hi32(thr)| <= 1: the reference's exact r.r
-        // (association of core.hpp:27, no contraction) and its exact compare
+      if (__any_sync(0xffffffffu, band <= 2u)) {  // warp-uniform, rare
+        // the reference's exact r.r (association of core.hpp:27, no
+        // contraction) and its exact compare, for every point of the warp
 #pragma unroll
         for (int k = 0; k < P; ++k) {
           const double e2 = __dadd_rn(__dadd_rn(__dmul_rn(rx[k], rx[k]), __dmul_rn(ry[k], ry[k])),
@@ -173,8 +188,8 @@ __global__ void __launch_bounds__(kK1Threads, P >= 6 ? 1 : (P >= 4 ? 2 : 3))
       }
 #pragma unroll
       for (int k = 0; k < P; ++k) {
-        const double e = src_exp(r2[k], a.w, b.x, q.x, q.y, q.z, tab);
-        const double T = keep[k] ? e : 0.0;
+        if (!K1_VOTE_LATE) e[k] = src_exp(r2[k], a.w, b.x, q.x, q.y, q.z, tab);
+        const double T = keep[k] ? e[k] : 0.0;
         v[k] = __dadd_rn(v[k], T);
         if (GRAD) {
           const double w = __dmul_rn(T, b.y);
@@ -271,9 +286,15 @@ __global__ void k1_combine_flux(const double* __restrict__ part, int S, int n,
 // ---------------------------------------------------------------------------
 
 void k1_upload_exp_table(cudaStream_t stream) {
+  // 2^(j/1024) with (j << 10) pre-subtracted from the high word (src_exp)
   double tab[kExpTableSize];
-  for (int j = 0; j < kExpTableSize; ++j)
-    tab[j] = static_cast<double>(exp2l(static_cast<long double>(j) / kExpTableSize));
+  for (int j = 0; j < kExpTableSize; ++j) {
+    const double v = static_cast<double>(exp2l(static_cast<long double>(j) / kExpTableSize));
+    uint64_t bits;
+    std::memcpy(&bits, &v, 8);
+    bits -= static_cast<uint64_t>(j) << (20 - kExpBits + 32);
+    std::memcpy(&tab[j], &bits, 8);
+  }
   cudaMemcpyToSymbolAsync(c_exp_table, tab, sizeof(tab), 0, cudaMemcpyHostToDevice, stream);
 }
 

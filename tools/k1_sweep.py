@@ -1,4 +1,4 @@
-"""K1 variant sweep: pairs/s of the config-1 superposition for TG_K1_P in {1,2,4}."""
+"""K1 sweep: pairs/s of the config-1 superposition for each TG_K1_P (or the\ncurrent environment only, with --one)."""
 import json
 import os
 import subprocess
@@ -26,6 +26,11 @@ p = ctx.profile()
 ms = p["k1_ms"] / p["k1_launches"]
 print(json.dumps({"P": os.environ.get("TG_K1_P"), "k1_ms": ms, "pairs_per_s": 2**20 * 2**16 / (ms * 1e-3)}))
 '''
+if "--one" in sys.argv:
+    r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, ROOT=ROOT),
+                       capture_output=True, text=True)
+    print(r.stdout.strip() or r.stderr[-2000:])
+    sys.exit(0)
 for P in ("2", "3", "4", "6", "8"):
     env = dict(os.environ, TG_K1_P=P, ROOT=ROOT)
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True)
