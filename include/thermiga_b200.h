@@ -120,7 +120,8 @@ const char* tg_sim_last_error(const tg_sim* sim);
 /* The simulation's device context (profiling counters, K1 sources). */
 int tg_sim_context(tg_sim* sim, tg_ctx** out);
 /* out[18]: n_full, n_free, n_constrained, n_steps, n_sources, n_face_elements,
- * nx, ny, nz, px, py, pz, kronecker(1)/assembled(0), max nq_base, max nq_fine,
+ * nx, ny, nz, px, py, pz, operator (0 assembled CSR, 1 Kronecker, 2 Kronecker with the
+ * single-sweep solver on the device), max nq_base, max nq_fine,
  * ndofs_kept, total base qps, total fine qps */
 int tg_sim_info(tg_sim* sim, long* out);
 /* out[10]: dt_solver, theta, solver_tol, elevate_radius, cull_exponent,

@@ -58,21 +58,23 @@ struct Dims {
 };
 
 // NIN loaded vectors; NPASS separate x/y passes (2 for the RHS, whose two
-// inputs carry different (a, b)); COMBINE: one pass over v = in0 + beta in1
-// (the PCG direction update). The z band (Mz, Kz rows) of the whole grid
-// follows the struct in dynamic shared memory.
-template <int P, int PL, int NIN, int NPASS>
+// inputs carry different (a, b)); a prologue functor may build one tile v
+// from the rings (the PCG direction update, the C-G residual update). The z
+// band (Mz, Kz rows) of the whole grid follows the struct in dynamic shared
+// memory.
+template <int P, int PL, int NIN, int NPASS, int ST = kStages>
 struct KSmem {
-  double ring[NIN][kStages][Dims<P, PL>::SLOT];
+  static constexpr int kSt = ST;  // TMA ring depth (boxes in flight per input)
+  double ring[NIN][ST][Dims<P, PL>::SLOT];
   double v[PL][Dims<P, PL>::PLANE];
   double u1[NPASS][2][PL][Dims<P, PL>::RY][kKronTX];
   double u2[NPASS][2][PL][Dims<P, PL>::RY][kKronTX];
-  uint64_t bar[NIN][kStages];
+  uint64_t bar[NIN][ST];
 };
 
-template <int P, int PL, int NIN, int NPASS>
+template <int P, int PL, int NIN, int NPASS, int ST = kStages>
 __host__ __device__ constexpr size_t zband_offset() {
-  return (sizeof(KSmem<P, PL, NIN, NPASS>) + 15) / 16 * 16;
+  return (sizeof(KSmem<P, PL, NIN, NPASS, ST>) + 15) / 16 * 16;
 }
 
 // Work split: the grid is ntx x nty columns (32 x 8 control points each) of
@@ -131,14 +133,14 @@ struct Inputs {
   const TensorMap3* map[NIN];
 };
 
-template <int P, int PL, int NIN, int NPASS>
-__device__ __forceinline__ void init_smem(const KronGrid& g, KSmem<P, PL, NIN, NPASS>& sm,
+template <int P, int PL, int NIN, int NPASS, int ST>
+__device__ __forceinline__ void init_smem(const KronGrid& g, KSmem<P, PL, NIN, NPASS, ST>& sm,
                                           double* zb, bool tma) {
   constexpr int W = 2 * P + 1;
   const int tid = threadIdx.y * kKronTX + threadIdx.x;
   if (tma && tid == 0) {
     for (int q = 0; q < NIN; ++q)
-      for (int s = 0; s < kStages; ++s) mbar_init(&sm.bar[q][s], 1);
+      for (int s = 0; s < ST; ++s) mbar_init(&sm.bar[q][s], 1);
     fence_mbar_init();
   }
   for (int e = tid; e < g.n[2] * W; e += kThreads) {  // Mz, Kz rows: z-pass coefficients
@@ -149,15 +151,22 @@ __device__ __forceinline__ void init_smem(const KronGrid& g, KSmem<P, PL, NIN, N
 }
 
 // Sweep one column segment, PL planes per step. For every output point
-// (i, j, k) call epi(flat, i, j, k, y, p_own) where y = sum over passes of
-// Op(a_q, b_q) in_q (COMBINE: one pass over v = in0 + beta in1; p_own = v at
-// the point). Step s covers input planes k0 - P + PL s .. + PL - 1 (planes
-// outside the grid arrive as zeros). The shared layout SM may hold more input
-// rings than this sweep uses; seqs[q] counts the boxes ring q has delivered
-// (mbarrier phases).
-template <int P, int PL, int NIN, int NPASS, bool COMBINE, bool TMA, class SM, class Epi>
+// (i, j, k) call epi(flat, i, j, k, y, v_own) where y = sum over passes of
+// Op(a_q, b_q) in_q. With a prologue (Pro::kV) the x-pass runs on the tile
+// v that pro(...) builds from the ring slots of the step (halo included), and
+// v_own is v at the point; otherwise each pass reads its ring directly. Step
+// s covers input planes k0 - P + PL s .. + PL - 1 (planes outside the grid
+// arrive as zeros). The shared layout SM may hold more input rings than this
+// sweep uses; seqs[q] counts the boxes ring q has delivered (mbarrier phases).
+struct NoPro {
+  static constexpr bool kV = false;
+  template <class SM>
+  __device__ void operator()(SM&, const int*, int, int, const Seg&) {}
+};
+
+template <int P, int PL, int NIN, int NPASS, bool TMA, class SM, class Pro, class Epi>
 __device__ __forceinline__ void kron_tile(const KronGrid& g, const KronTerms& c,
-                                          const Inputs<NIN>& in, double beta, const Seg& sg,
+                                          const Inputs<NIN>& in, Pro& pro, const Seg& sg,
                                           SM& sm, const double* zb, int* seqs, Epi& epi) {
   using D = Dims<P, PL>;
   constexpr int W = D::W, RY = D::RY, RX = D::RX, PLANE = D::PLANE;
@@ -182,9 +191,9 @@ __device__ __forceinline__ void kron_tile(const KronGrid& g, const KronTerms& c,
     ky[d] = j < ny ? g.K[1][j * W + d] : 0.0;
   }
   if (TMA && leader) {
-    for (int s = 0; s < kStages && s < nsteps; ++s)
+    for (int s = 0; s < SM::kSt && s < nsteps; ++s)
       for (int q = 0; q < NIN; ++q) {
-        const int slot = (seqs[q] + s) % kStages;
+        const int slot = (seqs[q] + s) % SM::kSt;
         mbar_arrive_expect_tx(&sm.bar[q][slot], kBoxBytes);
         tma_load_box(sm.ring[q][slot], in.map[q], x0 - P, y0 - P, kfirst + PL * s,
                      &sm.bar[q][slot]);
@@ -202,8 +211,8 @@ __device__ __forceinline__ void kron_tile(const KronGrid& g, const KronTerms& c,
 #pragma unroll
     for (int q = 0; q < NIN; ++q) {
       const int qn = seqs[q] + s;
-      slot[q] = TMA ? qn % kStages : 0;
-      if (TMA) mbar_wait(&sm.bar[q][slot[q]], static_cast<uint32_t>((qn / kStages) & 1));
+      slot[q] = TMA ? qn % SM::kSt : 0;
+      if (TMA) mbar_wait(&sm.bar[q][slot[q]], static_cast<uint32_t>((qn / SM::kSt) & 1));
     }
     if constexpr (!TMA) {
       for (int q = 0; q < NIN; ++q)
@@ -222,19 +231,18 @@ __device__ __forceinline__ void kron_tile(const KronGrid& g, const KronTerms& c,
     // refill the ring slots just consumed; the barrier before the issue
     // orders every generic-proxy read of the slot before the TMA write
     auto refill = [&] {
-      if (TMA && leader && s + kStages < nsteps)
+      if (TMA && leader && s + SM::kSt < nsteps)
         for (int q = 0; q < NIN; ++q) {
           mbar_arrive_expect_tx(&sm.bar[q][slot[q]], kBoxBytes);
           tma_load_box(sm.ring[q][slot[q]], in.map[q], x0 - P, y0 - P,
-                       kfirst + PL * (s + kStages), &sm.bar[q][slot[q]]);
+                       kfirst + PL * (s + SM::kSt), &sm.bar[q][slot[q]]);
         }
     };
     double po[PL];
-    if constexpr (COMBINE) {  // v = z + beta p_old over the halo'd tiles
-      for (int e = ty * kKronTX + tx; e < PL * PLANE; e += kThreads)
-        (&sm.v[0][0])[e] = fma(beta, sm.ring[1][slot[NIN - 1]][e], sm.ring[0][slot[0]][e]);
+    if constexpr (Pro::kV) {  // v over the halo'd tiles (and the prologue's own-point work)
+      pro(sm, slot, s, kin0, sg);
       __syncthreads();
-      refill();  // the ring is only read by the update above
+      refill();  // the ring is only read by the prologue
 #pragma unroll
       for (int l = 0; l < PL; ++l) po[l] = sm.v[l][(ty + P) * RX + tx + P];
     }
@@ -243,7 +251,7 @@ __device__ __forceinline__ void kron_tile(const KronGrid& g, const KronTerms& c,
     for (int q = 0; q < NPASS; ++q)
 #pragma unroll
       for (int l = 0; l < PL; ++l) {
-        const double* src = COMBINE ? sm.v[l] : sm.ring[q][slot[q < NIN ? q : 0]] + l * PLANE;
+        const double* src = Pro::kV ? sm.v[l] : sm.ring[q][slot[q < NIN ? q : 0]] + l * PLANE;
         for (int r = ty; r < RY; r += kKronTY) {
           double a1 = 0.0, a2 = 0.0;
 #pragma unroll
@@ -257,7 +265,7 @@ __device__ __forceinline__ void kron_tile(const KronGrid& g, const KronTerms& c,
         }
       }
     __syncthreads();
-    if constexpr (!COMBINE) refill();
+    if constexpr (!Pro::kV) refill();
     // y-pass, then the PL planes enter the z window one by one
 #pragma unroll
     for (int l = 0; l < PL; ++l) {
@@ -284,7 +292,7 @@ __device__ __forceinline__ void kron_tile(const KronGrid& g, const KronTerms& c,
       }
       win1[W - 1] = s1;
       win2[W - 1] = s2;
-      pown[W - 1] = COMBINE ? po[l] : 0.0;
+      pown[W - 1] = Pro::kV ? po[l] : 0.0;
       const int k = kin0 + l - P;
       if (k >= k0 && k < k1 && i < nx && j < ny) {
         const double* mz = zb + k * W;
@@ -320,8 +328,9 @@ __global__ void __launch_bounds__(kThreads) k2_apply_kernel(KronGrid g, KronTerm
   EpiStore epi{y};
   Inputs<1> in{{v}, {nullptr}};
   int seq[1] = {0};
+  NoPro np;
   for_segments(T, gridDim.x, blockIdx.x, [&](const Seg& sg) {
-    kron_tile<P, 1, 1, 1, false, false>(g, c, in, 0.0, sg, sm, zb, seq, epi);
+    kron_tile<P, 1, 1, 1, false>(g, c, in, np, sg, sm, zb, seq, epi);
   });
 }
 
@@ -355,8 +364,9 @@ __global__ void __launch_bounds__(kThreads) k2_rhs_kernel(KronGrid g, KronTerms 
   epi.nfree[args.bottom_axis] -= 1;
   Inputs<2> in{{args.T_full, args.g_full}, {&maps.T, &maps.g}};
   int seq[2] = {0, 0};
+  NoPro np;
   for_segments(T, gridDim.x, blockIdx.x, [&](const Seg& sg) {
-    kron_tile<P, PL, 2, 2, false, TMA>(g, c, in, 0.0, sg, sm, zb, seq, epi);
+    kron_tile<P, PL, 2, 2, TMA>(g, c, in, np, sg, sm, zb, seq, epi);
   });
 }
 
@@ -437,6 +447,17 @@ struct EpiResidual {  // r = b - A x; z = D^-1 r; p_old = 0; rr, bb, rz
   }
 };
 
+struct ProCombine {  // v = z + beta p_old over the halo'd tiles (ring 0: z, ring 1: p_old)
+  static constexpr bool kV = true;
+  double beta;
+  template <class SM>
+  __device__ void operator()(SM& sm, const int* slot, int, int, const Seg&) {
+    constexpr int N = sizeof(sm.v) / sizeof(double);
+    for (int e = threadIdx.y * kKronTX + threadIdx.x; e < N; e += kThreads)
+      (&sm.v[0][0])[e] = fma(beta, sm.ring[1][slot[1]][e], sm.ring[0][slot[0]][e]);
+  }
+};
+
 struct EpiDirection {  // p_new (own point), Ap, p.Ap
   double* p_new;
   double* Ap;
@@ -470,8 +491,9 @@ __global__ void __launch_bounds__(kThreads, 2)
   {
     EpiResidual e0{rhs, w.inv_diag, w.r, w.z, w.pA, {0, 0, 0, 0}};
     Inputs<1> in1{{x}, {&maps.x}};  // ring 0 of the two-ring layout
+    NoPro np;
     for_segments(T, gridDim.x, blockIdx.x, [&](const Seg& sg) {
-      kron_tile<P, PL, 1, 1, false, TMA>(g, c, in1, 0.0, sg, sm, zb, seq, e0);
+      kron_tile<P, PL, 1, 1, TMA>(g, c, in1, np, sg, sm, zb, seq, e0);
     });
     grid_reduce(grid, e0.acc, w.partials, buf, red, tot);
   }
@@ -511,8 +533,9 @@ __global__ void __launch_bounds__(kThreads, 2)
     // A': p_new = z + beta p_old (sparse.cpp:96), Ap = A p_new (sparse.cpp:81)
     EpiDirection e1{p_new, w.Ap, {0, 0, 0, 0}};
     Inputs<2> in{{w.z, p_old}, {&maps.z, m_old}};
+    ProCombine pc{beta};
     for_segments(T, gridDim.x, blockIdx.x, [&](const Seg& sg) {
-      kron_tile<P, PL, 2, 1, true, TMA>(g, c, in, beta, sg, sm, zb, seq, e1);
+      kron_tile<P, PL, 2, 1, TMA>(g, c, in, pc, sg, sm, zb, seq, e1);
     });
     stamp(1);
     grid_reduce(grid, e1.acc, w.partials, buf, red, tot);
@@ -585,6 +608,266 @@ __global__ void __launch_bounds__(kThreads, 2)
     *w.status = PcgStatus{it, status, rel, bnorm};
 }
 
+// ---------------------------------------------------------------------------
+// single-sweep Jacobi-PCG (Chronopoulos-Gear recurrences)
+//
+// Same Krylov iterates as the reference's PCG in exact arithmetic, with the
+// two dot-product phases merged: carrying w = A u and s = A p as vectors,
+//   p_i = u_i + b_i p_{i-1}     s_i = w_i + b_i s_{i-1}
+//   x  += a_i p_i               r_{i+1} = r_i - a_i s_i,  u_{i+1} = D^-1 r_{i+1}
+//   w_{i+1} = A u_{i+1};  g = r.u, d = w.u, rr = r.r (one grid reduction)
+//   b_{i+1} = g_{i+1} / g_i,  a_{i+1} = g_{i+1} / (d_{i+1} - b_{i+1} g_{i+1} / a_i)
+// (the denominator is p.Ap; <= 0 is the reference's indefinite-direction
+// failure). One tile sweep per iteration: the prologue forms s, r and u on the
+// halo'd TMA tiles of r, w, s_old and D^-1 (the stencil input u = D^-1 r_new),
+// updates p and x on the segment's own points, and the epilogue writes
+// w = A u. Vectors whose halos are read (r, w, s) ping-pong between two
+// buffers; x and p are point-local and update in place. HBM traffic: 6 reads
+// + 5 writes = 88 B per DOF per iteration, one grid barrier.
+
+constexpr int kCg1Stages = 2;  // ring depth: 4 inputs x 2 stages keeps 2 CTAs/SM
+
+template <int P, int PL>
+struct ProScale {  // init: v = D^-1 r0 (ring 0: r0, ring 1: D^-1); gamma0 on own points
+  static constexpr bool kV = true;
+  int nx, ny;
+  double gamma;
+  template <class SM>
+  __device__ void operator()(SM& sm, const int* slot, int, int kin0, const Seg& sg) {
+    using D = Dims<P, PL>;
+    constexpr int N = PL * D::PLANE;
+    const double* rr = sm.ring[0][slot[0]];
+    const double* dd = sm.ring[1][slot[1]];
+    const int tx = threadIdx.x, ty = threadIdx.y;
+    for (int e = ty * kKronTX + tx; e < N; e += kThreads) (&sm.v[0][0])[e] = dd[e] * rr[e];
+    if (sg.x0 + tx < nx && sg.y0 + ty < ny) {
+#pragma unroll
+      for (int l = 0; l < PL; ++l) {
+        const int kin = kin0 + l;
+        if (kin >= sg.k0 && kin < sg.k1) {
+          const int e = l * D::PLANE + (ty + P) * D::RX + tx + P;
+          gamma += rr[e] * (dd[e] * rr[e]);
+        }
+      }
+    }
+  }
+};
+
+// Point-local inputs of the C-G sweep (x, p_{i-1}): un-halo'd 32 x 8 x PL
+// TMA boxes through their own 2-slot ring, placed after the z band.
+template <int PL>
+struct CentreRing {
+  static constexpr int kBox = PL * kKronTY * kKronTX;  // doubles per box
+  double buf[2][2][kBox];                               // [vector][slot]
+  uint64_t bar[2][2];
+};
+
+template <int P, int PL>
+struct ProCg1 {  // rings: 0 r_i, 1 w_i, 2 s_{i-1}, 3 D^-1; centre ring: x, p_{i-1}
+  static constexpr bool kV = true;
+  double alpha, beta;
+  double* x;
+  double* p;
+  double* r_out;
+  double* s_out;
+  int nx, ny;
+  CentreRing<PL>* cr;
+  const TensorMap3* mx;
+  const TensorMap3* mp;
+  int* cseq;  // boxes the centre ring has delivered (persists across sweeps)
+  double gamma, rr;
+
+  __device__ void issue(const Seg& sg, int step) const {
+    const int q = *cseq + step, slot = q & 1;
+    constexpr uint32_t bytes = CentreRing<PL>::kBox * 8;
+    const int kin0 = sg.k0 - P + PL * step;
+    mbar_arrive_expect_tx(&cr->bar[0][slot], bytes);
+    tma_load_box(cr->buf[0][slot], mx, sg.x0, sg.y0, kin0, &cr->bar[0][slot]);
+    mbar_arrive_expect_tx(&cr->bar[1][slot], bytes);
+    tma_load_box(cr->buf[1][slot], mp, sg.x0, sg.y0, kin0, &cr->bar[1][slot]);
+  }
+  template <class SM>
+  __device__ void operator()(SM& sm, const int* slot, int s, int kin0, const Seg& sg) {
+    using D = Dims<P, PL>;
+    constexpr int N = PL * D::PLANE;
+    const int nsteps = (sg.k1 - sg.k0 + 2 * P + PL - 1) / PL;
+    const int tx = threadIdx.x, ty = threadIdx.y;
+    // the slot of step s + 1 was last read in step s - 1 (a barrier ago)
+    if (tx == 0 && ty == 0) {
+      if (s == 0) issue(sg, 0);
+      if (s + 1 < nsteps) issue(sg, s + 1);
+    }
+    const int q = *cseq + s, cs = q & 1;
+    const uint32_t par = static_cast<uint32_t>((q >> 1) & 1);
+    mbar_wait(&cr->bar[0][cs], par);
+    mbar_wait(&cr->bar[1][cs], par);
+    if (s + 1 == nsteps) *cseq += nsteps;
+    const double* r_ = sm.ring[0][slot[0]];
+    const double* w_ = sm.ring[1][slot[1]];
+    const double* s_ = sm.ring[2][slot[2]];
+    const double* d_ = sm.ring[3][slot[3]];
+    const int i = sg.x0 + tx, j = sg.y0 + ty;
+    if (i < nx && j < ny) {
+#pragma unroll
+      for (int l = 0; l < PL; ++l) {
+        const int kin = kin0 + l;
+        if (kin >= sg.k0 && kin < sg.k1) {
+          const int e = l * D::PLANE + (ty + P) * D::RX + tx + P;
+          const int c = (l * kKronTY + ty) * kKronTX + tx;
+          const size_t f = (static_cast<size_t>(kin) * ny + j) * nx + i;
+          const double ro = r_[e], dv = d_[e];
+          const double pnew = fma(beta, cr->buf[1][cs][c], dv * ro);  // p_i = u_i + beta p_{i-1}
+          p[f] = pnew;
+          x[f] = fma(alpha, pnew, cr->buf[0][cs][c]);                 // x_{i+1}
+          const double snew = fma(beta, s_[e], w_[e]);  // s_i = w_i + beta s_{i-1}
+          const double rnew = fma(-alpha, snew, ro);    // r_{i+1}
+          s_out[f] = snew;
+          r_out[f] = rnew;
+          gamma += rnew * (dv * rnew);
+          rr += rnew * rnew;
+        }
+      }
+    }
+    for (int e = ty * kKronTX + tx; e < N; e += kThreads)  // u_{i+1}, halo included
+      (&sm.v[0][0])[e] = d_[e] * fma(-alpha, fma(beta, s_[e], w_[e]), r_[e]);
+  }
+};
+
+struct EpiCg1 {  // w = A u and w.u
+  double* w_out;
+  double delta;
+  __device__ void operator()(size_t idx, int, int, int, double y, double u) {
+    w_out[idx] = y;
+    delta += y * u;
+  }
+};
+
+struct EpiCg1Init {  // r0 = b - A x0, s_{-1} = p_{-1} = 0; r.r, b.b
+  const double* rhs;
+  double* r;
+  double* s;
+  double* p;
+  double acc[4];
+  __device__ void operator()(size_t idx, int, int, int, double y, double) {
+    const double bi = rhs[idx];
+    const double ri = bi - y;
+    r[idx] = ri;
+    s[idx] = 0.0;
+    p[idx] = 0.0;
+    acc[0] += ri * ri;
+    acc[1] += bi * bi;
+  }
+};
+
+template <int P>
+__host__ __device__ constexpr size_t cg1_centre_offset(int nz) {
+  return (zband_offset<P, kTmaPlanes, 4, 1, kCg1Stages>() + 2 * static_cast<size_t>(nz) * (2 * P + 1) * 8 +
+          127) / 128 * 128;
+}
+template <int P>
+size_t cg1_smem_bytes(int nz) {
+  return cg1_centre_offset<P>(nz) + sizeof(CentreRing<kTmaPlanes>);
+}
+
+template <int P>
+__global__ void __launch_bounds__(kThreads, 2)
+    k2_cg1_kernel(KronGrid g, double a, double b, const double* rhs, double* x, Cg1Work w,
+                  double tol, int max_iter, TileIdx T, const __grid_constant__ Cg1Maps maps) {
+  constexpr int PL = kTmaPlanes;
+  using SMT = KSmem<P, PL, 4, 1, kCg1Stages>;
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  auto& sm = *reinterpret_cast<SMT*>(smem_raw);
+  double* zb = reinterpret_cast<double*>(smem_raw + zband_offset<P, PL, 4, 1, kCg1Stages>());
+  auto* cr = reinterpret_cast<CentreRing<PL>*>(smem_raw + cg1_centre_offset<P>(g.n[2]));
+  __shared__ double red[64];
+  if (threadIdx.x == 0 && threadIdx.y == 0)
+    for (int v = 0; v < 2; ++v)
+      for (int q = 0; q < 2; ++q) mbar_init(&cr->bar[v][q], 1);
+  init_smem(g, sm, zb, true);  // (its barrier also publishes the centre-ring init)
+  int cseq = 0;
+  const KronTerms c{a, b, 0.0, 0.0};
+  const int nx = g.n[0], ny = g.n[1];
+  int buf = 0;
+  int seq[4] = {0, 0, 0, 0};
+  double tot[4];
+  const bool lead = blockIdx.x == 0 && threadIdx.x == 0 && threadIdx.y == 0;
+
+  // r0 = b - A x0 (sparse.cpp:61-69)
+  {
+    EpiCg1Init e0{rhs, w.r[0], w.s[0], w.p, {0, 0, 0, 0}};
+    Inputs<1> in1{{x}, {&maps.x}};
+    NoPro np;
+    for_segments(T, gridDim.x, blockIdx.x, [&](const Seg& sg) {
+      kron_tile<P, PL, 1, 1, true>(g, c, in1, np, sg, sm, zb, seq, e0);
+    });
+    grid_reduce(grid, e0.acc, w.partials, buf, red, tot);
+  }
+  const double bnorm = sqrt(tot[1]);
+  if (bnorm == 0.0) {  // sparse.cpp:57-60: zero rhs resets even a warm start
+    const size_t n = static_cast<size_t>(nx) * ny * g.n[2];
+    for (size_t f = static_cast<size_t>(blockIdx.x) * kThreads + threadIdx.y * kKronTX + threadIdx.x;
+         f < n; f += static_cast<size_t>(gridDim.x) * kThreads)
+      x[f] = 0.0;
+    if (lead) *w.status = PcgStatus{0, 0, 0.0, 0.0};
+    return;
+  }
+  double rel = sqrt(tot[0]) / bnorm;
+  if (max_iter <= 0 || rel <= tol) {  // the reference tests before its first matvec
+    if (lead) *w.status = PcgStatus{0, max_iter <= 0 ? 3 : 0, rel, bnorm};
+    return;
+  }
+  // w0 = A u0, gamma0 = r0.u0, delta0 = w0.u0 = p0.Ap0
+  {
+    ProScale<P, PL> ps{nx, ny, 0.0};
+    EpiCg1 e1{w.w[0], 0.0};
+    Inputs<2> in2{{w.r[0], w.inv_diag}, {&maps.r[0], &maps.inv_diag}};
+    for_segments(T, gridDim.x, blockIdx.x, [&](const Seg& sg) {
+      kron_tile<P, PL, 2, 1, true>(g, c, in2, ps, sg, sm, zb, seq, e1);
+    });
+    const double acc[4] = {ps.gamma, e1.delta, 0.0, 0.0};
+    grid_reduce(grid, acc, w.partials, buf, red, tot);
+  }
+  double gamma = tot[0];
+  int it = 0, status = 3;
+  if (!(tot[1] > 0.0)) {
+    if (lead) *w.status = PcgStatus{0, 4, rel, bnorm};
+    return;
+  }
+  double alpha = gamma / tot[1], beta = 0.0;
+  int cur = 0;
+  while (it < max_iter) {
+    ProCg1<P, PL> pc{alpha, beta, x,          w.p,       w.r[cur ^ 1], w.s[cur ^ 1], nx,
+                     ny,    cr,   &maps.xc, &maps.pc, &cseq,        0.0,          0.0};
+    EpiCg1 e{w.w[cur ^ 1], 0.0};
+    Inputs<4> in{{w.r[cur], w.w[cur], w.s[cur], w.inv_diag},
+                 {&maps.r[cur], &maps.w[cur], &maps.s[cur], &maps.inv_diag}};
+    for_segments(T, gridDim.x, blockIdx.x, [&](const Seg& sg) {
+      kron_tile<P, PL, 4, 1, true>(g, c, in, pc, sg, sm, zb, seq, e);
+    });
+    const double acc[4] = {pc.gamma, e.delta, pc.rr, 0.0};
+    grid_reduce(grid, acc, w.partials, buf, red, tot);
+    ++it;
+    cur ^= 1;
+    if (it >= max_iter) break;  // the reference leaves after max_iter updates untested
+    rel = sqrt(tot[2]) / bnorm;
+    if (rel <= tol) {
+      status = 0;
+      break;
+    }
+    const double g1 = tot[0];
+    beta = g1 / gamma;
+    const double den = tot[1] - beta * g1 / alpha;  // p_{i+1}.A p_{i+1}
+    if (!(den > 0.0)) {
+      status = 4;
+      break;
+    }
+    alpha = g1 / den;
+    gamma = g1;
+  }
+  if (lead) *w.status = PcgStatus{it, status, rel, bnorm};
+}
+
 // --------------------------------------------------------------------------
 // TMA descriptor encoding through the driver entry point (no -lcuda)
 
@@ -607,9 +890,9 @@ EncodeFn encoder() {
   return fn;
 }
 
-template <int P, int PL, int NIN, int NPASS>
+template <int P, int PL, int NIN, int NPASS, int ST = kStages>
 size_t smem_bytes(int nz) {
-  return zband_offset<P, PL, NIN, NPASS>() + 2 * static_cast<size_t>(nz) * (2 * P + 1) * 8;
+  return zband_offset<P, PL, NIN, NPASS, ST>() + 2 * static_cast<size_t>(nz) * (2 * P + 1) * 8;
 }
 
 template <typename K>
@@ -627,7 +910,7 @@ int seg_blocks(const TileIdx& T, int max_blocks) {
 
 }  // namespace
 
-bool k2_make_map(const KronGrid& g, const double* base, TensorMap3* out) {
+bool k2_make_map(const KronGrid& g, const double* base, TensorMap3* out, bool halo) {
   static_assert(sizeof(TensorMap3) == sizeof(CUtensorMap), "tensor map size");
   EncodeFn enc = encoder();
   const size_t pitch = static_cast<size_t>(g.n[0]) * sizeof(double);
@@ -635,8 +918,9 @@ bool k2_make_map(const KronGrid& g, const double* base, TensorMap3* out) {
   const cuuint64_t dims[3] = {static_cast<cuuint64_t>(g.n[0]), static_cast<cuuint64_t>(g.n[1]),
                               static_cast<cuuint64_t>(g.n[2])};
   const cuuint64_t strides[2] = {pitch, pitch * static_cast<cuuint64_t>(g.n[1])};
-  const cuuint32_t box[3] = {static_cast<cuuint32_t>(kKronTX + 2 * g.p),
-                             static_cast<cuuint32_t>(kKronTY + 2 * g.p),
+  const int h = halo ? 2 * g.p : 0;
+  const cuuint32_t box[3] = {static_cast<cuuint32_t>(kKronTX + h),
+                             static_cast<cuuint32_t>(kKronTY + h),
                              static_cast<cuuint32_t>(kTmaPlanes)};
   const cuuint32_t estr[3] = {1, 1, 1};
   CUtensorMap m;
@@ -739,6 +1023,37 @@ void k2_pcg_solve(const KronGrid& g, double a, double b, const double* rhs, doub
     else
       TG_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(&k2_pcg_kernel<P, false>),
                                           grid, block, args, smem_bytes<P, 1, 2, 1>(g.n[2]), s));
+  });
+}
+
+int k2_cg1_max_blocks(int p, int sm_count, int nz) {
+  int per_sm = 0;
+  TG_KRON_DISPATCH(p, {
+    const size_t sb = cg1_smem_bytes<P>(nz);
+    allow_smem(k2_cg1_kernel<P>, sb);
+    TG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+        &per_sm, reinterpret_cast<const void*>(&k2_cg1_kernel<P>), kThreads, sb));
+  });
+  return std::max(1, per_sm) * sm_count;
+}
+
+void k2_cg1_solve(const KronGrid& g, double a, double b, const double* rhs, double* x,
+                  const Cg1Work& w, const Cg1Maps& maps, double tol, int max_iter, int blocks,
+                  cudaStream_t s) {
+  const TileIdx T = make_tiles(g);
+  const int nb = seg_blocks(T, blocks);
+  dim3 grid(nb), block(kKronTX, kKronTY);
+  KronGrid gg = g;
+  Cg1Work ww = w;
+  Cg1Maps mm = maps;
+  double aa = a, bb = b, tt = tol;
+  int mi = max_iter;
+  TileIdx TT = T;
+  void* args[] = {&gg, &aa, &bb, const_cast<double**>(&rhs), &x, &ww, &tt, &mi, &TT, &mm};
+  TG_KRON_DISPATCH(g.p, {
+    TG_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(&k2_cg1_kernel<P>), grid,
+                                        block, args,
+                                        cg1_smem_bytes<P>(g.n[2]), s));
   });
 }
 

@@ -21,15 +21,15 @@ struct KronGrid {
 };
 
 // Opaque CUtensorMap (128 bytes, 64-byte aligned): a 3D TMA descriptor of one
-// grid vector with a (32+2p) x (8+2p) x 1 box (a halo'd plane tile), zero
-// fill outside the grid.
+// grid vector with a (32+2p) x (8+2p) x 2 box (halo'd plane tiles; 32 x 8 x 2
+// with halo = false), zero fill outside the grid.
 struct alignas(64) TensorMap3 {
   unsigned char bytes[128];
 };
 // Encode the descriptor for `base` (a vector over g's grid). Returns false
 // when TMA cannot address the grid (row pitch not a multiple of 16 bytes);
 // the kernels then load planes with ordinary loads.
-bool k2_make_map(const KronGrid& g, const double* base, TensorMap3* out);
+bool k2_make_map(const KronGrid& g, const double* base, TensorMap3* out, bool halo = true);
 
 // y = Op(a1, b1) v1 + Op(a2, b2) v2 with Op(a, b) = a (Mz x My x Mx) +
 //     b (Mz x My x Kx + Mz x Ky x Mx + Kz x My x Mx); v2 may be null.
@@ -78,6 +78,23 @@ struct PcgMaps {
   TensorMap3 x, z, pA, pB;
 };
 
+// Work vectors of the single-sweep (Chronopoulos-Gear) solve: r, w = A u and
+// s = A p ping-pong between two buffers (their halos are read while the sweep
+// writes the next iterate); p is point-local. All over the free grid.
+struct Cg1Work {
+  double* p;
+  double* r[2];
+  double* w[2];
+  double* s[2];
+  const double* inv_diag;
+  double* partials;  // >= 8 * max_blocks
+  PcgStatus* status;
+};
+struct Cg1Maps {
+  TensorMap3 x, inv_diag, r[2], w[2], s[2];
+  TensorMap3 xc, pc;  // un-halo'd boxes of x and p (point-local inputs)
+};
+
 void k2_theta_rhs(const KronGrid& full, double a_b, double b_b, double a_a, double b_a,
                   const RhsArgs& args, const TensorMap3* mT, const TensorMap3* mg, int sm_count,
                   cudaStream_t s);
@@ -93,6 +110,13 @@ void k2_plane_trace(unsigned long long* buf);
 // launch per solve; x holds the warm start on entry.
 void k2_pcg_solve(const KronGrid& g, double a, double b, const double* rhs, double* x,
                   const PcgWork& w, const PcgMaps& maps, double tol, int max_iter, int blocks,
+                  cudaStream_t s);
+// The same solve with one tile sweep and one grid reduction per iteration
+// (TMA only; see k2_kron.cu). Stop test, failure codes and warm start as
+// k2_pcg_solve.
+int k2_cg1_max_blocks(int p, int sm_count, int nz);
+void k2_cg1_solve(const KronGrid& g, double a, double b, const double* rhs, double* x,
+                  const Cg1Work& w, const Cg1Maps& maps, double tol, int max_iter, int blocks,
                   cudaStream_t s);
 // plain y = Op(a, b) v (tests / the operator alone)
 void k2_apply(const KronGrid& g, double a, double b, const double* v, double* y, int sm_count,

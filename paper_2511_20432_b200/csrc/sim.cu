@@ -311,6 +311,19 @@ void Sim::setup_device(int device) {
     maps.valid = k2_make_map(gfree, d_x.p, &maps.x) && k2_make_map(gfree, d_z.p, &maps.z) &&
                  k2_make_map(gfree, d_p.p, &maps.pA) && k2_make_map(gfree, d_p2.p, &maps.pB);
     rhs_tma = k2_make_map(gfull, d_T.p, &map_T) && k2_make_map(gfull, d_gfull.p, &map_g);
+    const char* algo = std::getenv("TG_K2_ALGO");
+    if (maps.valid && !(algo && std::string(algo) == "pcg")) {
+      // buffers: r = {d_r, d_z}, w = {d_Ap, d_w2}, s = {d_p2, d_s2}, p = d_p
+      d_w2.ensure(n_free);
+      d_s2.ensure(n_free);
+      Cg1Maps& m = cg1maps;
+      use_cg1 = k2_make_map(gfree, d_x.p, &m.x) && k2_make_map(gfree, d_invd.p, &m.inv_diag) &&
+                k2_make_map(gfree, d_r.p, &m.r[0]) && k2_make_map(gfree, d_z.p, &m.r[1]) &&
+                k2_make_map(gfree, d_Ap.p, &m.w[0]) && k2_make_map(gfree, d_w2.p, &m.w[1]) &&
+                k2_make_map(gfree, d_p2.p, &m.s[0]) && k2_make_map(gfree, d_s2.p, &m.s[1]) &&
+                k2_make_map(gfree, d_x.p, &m.xc, false) && k2_make_map(gfree, d_p.p, &m.pc, false);
+      if (use_cg1) pcg_blocks = k2_cg1_max_blocks(p, ctx->sm_count, gfree.n[2]);
+    }
   } else {
     auto up = [&](const Csr& C, DevBuf<int>& rp, DevBuf<int>& ci, DevBuf<double>& v, DevCsr& out) {
       upload(rp, C.row_ptr, s);
@@ -419,13 +432,22 @@ PcgStatus Sim::theta_step_device(double tol, int max_iter) {
     k2_theta_rhs(gfull, coefB[0], coefB[1], -coefA[0], -coefA[1], ra, rhs_tma ? &map_T : nullptr,
                  rhs_tma ? &map_g : nullptr, ctx->sm_count, s);
     ctx->timer.launches += 2;
-    const PcgWork w{d_r.p,        d_z.p,      d_p.p,
-                    d_p2.p,       d_Ap.p,     d_invd.p,
-                    d_partials.p, d_status.p, trace_on ? d_trace.p : nullptr};
-    ctx->timer.timed(2, s, [&] {
-      k2_pcg_solve(gfree, coefA[0], coefA[1], d_rhs.p, d_x.p, w, maps, tol, max_iter,
-                   pcg_blocks, s);
-    });
+    if (use_cg1) {
+      const Cg1Work w{d_p.p,    {d_r.p, d_z.p}, {d_Ap.p, d_w2.p}, {d_p2.p, d_s2.p},
+                      d_invd.p, d_partials.p,   d_status.p};
+      ctx->timer.timed(2, s, [&] {
+        k2_cg1_solve(gfree, coefA[0], coefA[1], d_rhs.p, d_x.p, w, cg1maps, tol, max_iter,
+                     pcg_blocks, s);
+      });
+    } else {
+      const PcgWork w{d_r.p,        d_z.p,      d_p.p,
+                      d_p2.p,       d_Ap.p,     d_invd.p,
+                      d_partials.p, d_status.p, trace_on ? d_trace.p : nullptr};
+      ctx->timer.timed(2, s, [&] {
+        k2_pcg_solve(gfree, coefA[0], coefA[1], d_rhs.p, d_x.p, w, maps, tol, max_iter,
+                     pcg_blocks, s);
+      });
+    }
   } else {
     csr_theta_rhs(devB, devAc, d_T.p, d_g1.p, d_Fn.p, d_F1.p, d_free_list.p, th, d_rhs.p, s);
     ++ctx->timer.launches;

@@ -82,6 +82,11 @@ class Sim {
   DevBuf<double> d_x, d_r, d_z, d_p, d_p2, d_Ap, d_invd, d_rhs, d_gn, d_g1, d_Fn, d_F1, d_T, d_gfull,
       d_partials;
   PcgMaps maps{};
+  // single-sweep solve (k2_cg1_solve): the default when TMA can address the
+  // free grid; TG_K2_ALGO=pcg selects the two-phase kernel
+  bool use_cg1 = false;
+  Cg1Maps cg1maps{};
+  DevBuf<double> d_w2, d_s2;
   TensorMap3 map_T{}, map_g{};
   bool rhs_tma = false;
   DevBuf<PcgStatus> d_status;

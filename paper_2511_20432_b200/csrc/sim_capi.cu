@@ -105,7 +105,7 @@ int tg_sim_info(tg_sim* s, long* out) {
     const auto n = m.vol.basis_counts();
     const auto p = m.vol.degrees();
     const long v[] = {m.n_full, m.n_free, m.n_con, m.n_steps, static_cast<long>(m.sources.size()),
-                      m.n_fe, n[0], n[1], n[2], p[0], p[1], p[2], m.kron ? 1 : 0, m.nqb, m.nqf,
+                      m.n_fe, n[0], n[1], n[2], p[0], p[1], p[2], m.kron ? (m.use_cg1 ? 2 : 1) : 0, m.nqb, m.nqf,
                       m.ndk, m.h_qb_off.back(), m.h_qf_off.back()};
     std::memcpy(out, v, sizeof(v));
   }, false);

@@ -33,10 +33,21 @@ def normwise(a, b):
     return 0.0 if m == 0 else np.abs(a - b).max() / m
 
 
-@pytest.fixture(scope="module", params=NAMES)
+@pytest.fixture(scope="module", params=[(n, a) for n in NAMES for a in ("cg1", "pcg")],
+                ids=lambda p: f"{p[0]}-{p[1]}")
 def sim(request):
-    s = tg.Simulation(cfg(request.param))
-    yield request.param, s
+    """Each config with both Kronecker solvers: the single-sweep
+    Chronopoulos-Gear kernel (default with TMA) and the two-phase PCG kernel
+    (TG_K2_ALGO=pcg; the only one without TMA, e.g. cfg0_oddx's odd pitch)."""
+    name, algo = request.param
+    os.environ["TG_K2_ALGO"] = algo
+    try:
+        s = tg.Simulation(cfg(name))
+    finally:
+        os.environ.pop("TG_K2_ALGO")
+    if algo == "cg1" and name != "cfg0_oddx" and s.info["kronecker"]:
+        assert s.info["kronecker"] == 2
+    yield name, s
     s.close()
 
 
