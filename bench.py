@@ -221,6 +221,11 @@ def theta_section(steps, warmup, with_cpu):
     prof = ctx.profile()
     ctx.set_profiling(False)
     dofs = sim.info["n_full"]
+    solver = {2: "single-sweep Chronopoulos-Gear Jacobi-PCG (one tile sweep + one grid "
+                 "reduction per iteration)",
+              1: "two-phase Jacobi-PCG (direction sweep + streaming update)",
+              0: "assembled CSR Jacobi-PCG"}[sim.info["kronecker"]]
+    kernel = {2: "k2_cg1_kernel", 1: "k2_pcg_kernel", 0: "csr_pcg_kernel"}[sim.info["kronecker"]]
     k2_ms = prof["k2_ms"] / steps
     peak, src = hbm_peak()
     achieved = prof["k2_bytes"] / (prof["k2_ms"] * 1e-3) / 1e9 if prof["k2_ms"] else None
@@ -233,7 +238,8 @@ def theta_section(steps, warmup, with_cpu):
         "theta_ms_per_step_per_mdof": k2_ms / (dofs / 1e6),
         "k1_ms_per_step": prof["k1_ms"] / steps,
         "cg_iterations_per_step": iters / steps,
-        "roofline": {"kernel": "k2_pcg_kernel (persistent Jacobi-PCG)", "bound": "hbm",
+        "solver": solver,
+        "roofline": {"kernel": kernel, "bound": "hbm",
                      "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak if achieved else None, "traffic": None,
                      "peak_source": src,

@@ -11,7 +11,7 @@ import paper_2511_20432_b200 as tg  # noqa: E402
 
 cfg = sys.argv[1] if len(sys.argv) > 1 else os.path.join(ROOT, "configs", "cfg4_large.cfg")
 steps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
-for algo in ("cg1", "pcg"):
+for algo in os.environ.get("TG_K2_ALGOS", "cg1,pcg").split(","):
     os.environ["TG_K2_ALGO"] = algo
     sim = tg.Simulation(cfg)
     sim.reset()

@@ -11,5 +11,6 @@ cfg = sys.argv[1] if len(sys.argv) > 1 else os.path.join(ROOT, "configs", "cfg4_
 steps = int(sys.argv[2]) if len(sys.argv) > 2 else 2
 sim = tg.Simulation(cfg)
 sim.reset()
-it, rel = sim.advance(steps)
-print(f"steps {steps} cg iterations {it} last rel {rel:.3e}")
+for k in range(steps):
+    it, rel = sim.advance(1)
+    print(f"step {k + 1}: cg iterations {it} rel {rel:.3e}")
