@@ -52,6 +52,10 @@ FLOPS_PER_PAIR = 49.0  # value + gradient, exp counted at libdev
 # the 49-flop accounting exceeds the DFMA peak — fp64_pipe reports the
 # issued-instruction fraction).
 PIPE_OPS_PER_PAIR = 17.0
+# DRAM bytes (read + write) per launch from one `ncu --set full` capture of each
+# dominant kernel (profiles/r01_k1_ncu_summary.md, r01_k2_ncu_summary.md)
+K1_TRAFFIC_BYTES = 75.5e6 + 317.0e6   # k1_partial<6,1>, config 1, one launch
+K2_TRAFFIC_B_PER_DOF_ITER = 88.0      # k2_cg1_kernel<2>, config 4 (15.62 + 12.56 GB / 74 sweeps)
 
 
 def parse():
@@ -241,7 +245,11 @@ def theta_section(steps, warmup, with_cpu):
         "solver": solver,
         "roofline": {"kernel": kernel, "bound": "hbm",
                      "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak if achieved else None, "traffic": None,
+                     "frac": achieved / peak if achieved else None,
+                     "traffic": (K2_TRAFFIC_B_PER_DOF_ITER * sim.info["n_free"] * iters / steps
+                                 if sim.info["kronecker"] == 2 else None),
+                     "traffic_source": "ncu --set full, profiles/r01_k2_cg1_full.ncu-rep: "
+                                       "88 B/DOF/iteration measured, per solve",
                      "peak_source": src,
                      "bytes_per_dof_per_iteration": 104},
     }
@@ -382,7 +390,8 @@ def run_ours(args):
             "achieved": achieved,
             "peak": fp64_peak, "unit": "TFLOP/s",
             "frac": (achieved / fp64_peak) if (achieved and fp64_peak) else None,
-            "traffic": None,
+            "traffic": K1_TRAFFIC_BYTES,
+            "traffic_source": "ncu --set full, profiles/r01_k1_full_p6.ncu-rep (dram read+write)",
             "peak_source": "measured live: tg_fp64_peak DFMA-chain microbenchmark on this GPU",
             "flops_per_pair": FLOPS_PER_PAIR, "pairs_per_launch": pairs_per_launch,
             "mean_launch_ms": k1_mean_ms,
