@@ -159,9 +159,14 @@ class SlabPCG:
         local = [float((a * b).sum().item()) for a, b in pairs]
         return self.dist.all_reduce_sum(local)
 
-    def solve(self, b, x, tol: float, max_iter: int):
+    def solve(self, b, x, tol: float, max_iter: int, single_reduction: bool = False):
         """b, x: owned-plane torch tensors (x = warm start, updated in place).
-        Returns (iterations, relative residual); raises like the reference."""
+        Returns (iterations, relative residual); raises like the reference.
+        single_reduction: the Chronopoulos-Gear form of the device solver
+        (k2_cg1_kernel) — one halo exchange and one 3-scalar allreduce per
+        iteration instead of one exchange and two allreduces."""
+        if single_reduction:
+            return self._solve_cg1(b, x, tol, max_iter)
         bb = self._dot((b, b))[0]
         bnorm = float(np.sqrt(bb))
         if bnorm == 0.0:
@@ -189,6 +194,50 @@ class SlabPCG:
             beta = rz_new / rz
             rz = rz_new
             p = z + beta * p
+        raise ArithmeticError(f"pcg: no convergence in {max_iter} iterations, "
+                              f"relative residual {rel:.17g}")
+
+    def _solve_cg1(self, b, x, tol, max_iter):
+        A = lambda v: self.apply_slab(self.k0, self.k1, self._ghosted(v))  # noqa: E731
+        r = b - A(x)
+        bb, rr = self._dot((b, b), (r, r))
+        bnorm = float(np.sqrt(bb))
+        if bnorm == 0.0:  # sparse.cpp:57-60
+            x.zero_()
+            return 0, 0.0
+        rel = float(np.sqrt(rr)) / bnorm
+        if max_iter > 0 and rel <= tol:
+            return 0, rel
+        if max_iter > 0:
+            u = self.dinv * r
+            w = A(u)
+            gamma, delta = self._dot((r, u), (w, u))
+            if not delta > 0.0:
+                raise ArithmeticError("pcg: indefinite direction, matrix not SPD")
+            alpha, beta = gamma / delta, 0.0
+            p = u.clone()
+            s = w.clone()
+            it = 0
+            while it < max_iter:
+                if it > 0:
+                    p = u + beta * p  # p_i = u_i + beta p_{i-1}
+                    s = w + beta * s  # s_i = w_i + beta s_{i-1} (= A p_i)
+                x.add_(alpha * p)
+                r.sub_(alpha * s)
+                u = self.dinv * r
+                w = A(u)
+                g1, d1, rr = self._dot((r, u), (w, u), (r, r))
+                it += 1
+                if it >= max_iter:
+                    break  # the reference leaves after max_iter updates untested
+                rel = float(np.sqrt(rr)) / bnorm
+                if rel <= tol:
+                    return it, rel
+                beta = g1 / gamma
+                den = d1 - beta * g1 / alpha  # p_{i+1} . A p_{i+1}
+                if not den > 0.0:
+                    raise ArithmeticError("pcg: indefinite direction, matrix not SPD")
+                alpha, gamma = g1 / den, g1
         raise ArithmeticError(f"pcg: no convergence in {max_iter} iterations, "
                               f"relative residual {rel:.17g}")
 

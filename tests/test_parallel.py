@@ -124,7 +124,7 @@ def _apply(Mx, Kx, My, Ky, Mz, Kz, a, b, x):
     return a * k3(Mz, My, Mx) + b * (k3(Mz, My, Kx) + k3(Mz, Ky, Mx) + k3(Kz, My, Mx))
 
 
-def _pcg_rank(d: Dist, rhs_path):
+def _pcg_rank(d: Dist, rhs_path, single=False):
     Mx, Kx, My, Ky, Mz, Kz, a, b = _kron_factors()
     nz, ny, nx = Mz.shape[0], My.shape[0], Mx.shape[0]
     p = 2
@@ -144,18 +144,20 @@ def _pcg_rank(d: Dist, rhs_path):
     solver = SlabPCG(apply_slab, torch.from_numpy((1.0 / diag[k0:k1]).ravel().copy()), ny * nx,
                      nz, p, d)
     x = torch.zeros((k1 - k0) * ny * nx, dtype=torch.float64)
-    it, rel = solver.solve(torch.from_numpy(rhs[k0:k1].ravel().copy()), x, 1e-12, 2000)
+    it, rel = solver.solve(torch.from_numpy(rhs[k0:k1].ravel().copy()), x, 1e-12, 2000,
+                           single_reduction=single)
     return {"x": x.numpy(), "k0": k0, "k1": k1, "it": it, "rel": rel}
 
 
-def test_slab_pcg_two_ranks_matches_one(tmp_path):
+@pytest.mark.parametrize("single", [False, True], ids=["two-reductions", "single-reduction"])
+def test_slab_pcg_two_ranks_matches_one(tmp_path, single):
     Mx, Kx, My, Ky, Mz, Kz, a, b = _kron_factors()
     nz, ny, nx = Mz.shape[0], My.shape[0], Mx.shape[0]
     rhs = np.random.default_rng(11).standard_normal(nz * ny * nx)
     path = tmp_path / "rhs.npz"
     np.savez(path, b=rhs)
-    one = _run(1, _pcg_rank, tmp_path, str(path))[0]
-    two = _run(2, _pcg_rank, tmp_path, str(path))
+    one = _run(1, _pcg_rank, tmp_path, str(path), False)[0]
+    two = _run(2, _pcg_rank, tmp_path, str(path), single)
     x2 = np.concatenate([o["x"] for o in sorted(two, key=lambda o: int(o["k0"]))])
     assert abs(int(two[0]["it"]) - int(one["it"])) <= 1
     assert np.abs(x2 - one["x"]).max() <= 1e-10 * np.abs(one["x"]).max()
