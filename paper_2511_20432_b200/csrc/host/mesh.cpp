@@ -3,6 +3,8 @@
 #include <algorithm>
 #include <cmath>
 
+#include "parallel.hpp"
+
 namespace tgb {
 
 FaceId BoundaryTags::bottom_face() const {
@@ -59,12 +61,18 @@ FaceSets build_face_sets(const NurbsVolume& vol, const BoundaryTags& tags, int f
   fine_mult = std::max(1, fine_mult);
   const auto p = vol.degrees();
   FaceSets fs;
-  fs.n_dofs = (p[0] + 1) * (p[1] + 1) * (p[2] + 1);
+  const int nd = (p[0] + 1) * (p[1] + 1) * (p[2] + 1);
+  fs.n_dofs = nd;
+  // element list in the reference's order (face, then v-interval, then
+  // u-interval; mesh.cpp:158-236) with its rule offsets
+  struct Elem {
+    FaceId f;
+    double mu, hu, mv, hv;
+    int qu, qv;
+  };
+  std::vector<Elem> el;
   fs.qb_off.push_back(0);
   fs.qf_off.push_back(0);
-  std::vector<int> idx;
-  std::vector<double> val;
-  std::vector<Vec3> dv;
   for (FaceId f : kFaces) {
     if (tags.role_of(f) != FaceRole::lateral) continue;
     const auto t = face_tangent_axes(f);
@@ -73,40 +81,67 @@ FaceSets build_face_sets(const NurbsVolume& vol, const BoundaryTags& tags, int f
     const int qu = p[t[0]] + 1, qv = p[t[1]] + 1;
     for (std::size_t jv = 0; jv + 1 < bv.size(); ++jv)
       for (std::size_t iu = 0; iu + 1 < bu.size(); ++iu) {
-        const double hu = 0.5 * (bu[iu + 1] - bu[iu]), mu = 0.5 * (bu[iu + 1] + bu[iu]);
-        const double hv = 0.5 * (bv[jv + 1] - bv[jv]), mv = 0.5 * (bv[jv + 1] + bv[jv]);
-        bool have_dofs = false;
-        auto rule = [&](int nu, int nv, std::vector<double>& X, std::vector<double>& Nn,
-                        std::vector<double>& Wt, std::vector<double>& Nt) {
-          const auto& gu = gauss_rule(nu);
-          const auto& gv = gauss_rule(nv);
-          for (int b = 0; b < nv; ++b)
-            for (int a = 0; a < nu; ++a) {
-              const double u = mu + hu * gu.nodes[a];
-              const double v = mv + hv * gv.nodes[b];
-              const auto sp = vol.face_point(f, u, v);
-              const int nbas = vol.basis_at(sp.xi, idx, val, dv);
-              if (!have_dofs) {
-                fs.dofs.insert(fs.dofs.end(), idx.begin(), idx.end());
-                have_dofs = true;
-              }
-              X.insert(X.end(), {sp.x.x, sp.x.y, sp.x.z});
-              Nn.insert(Nn.end(), {sp.normal.x, sp.normal.y, sp.normal.z});
-              Wt.push_back(gu.weights[a] * gv.weights[b] * hu * hv * sp.area_scale);
-              Nt.insert(Nt.end(), val.begin(), val.begin() + nbas);
-            }
-        };
-        rule(qu, qv, fs.xb, fs.nb, fs.wb, fs.Nb);
-        rule(fine_mult * qu, fine_mult * qv, fs.xf, fs.nf, fs.wf, fs.Nf);
-        const auto c = vol.face_point(f, mu, mv);
-        fs.centers.insert(fs.centers.end(), {c.x.x, c.x.y, c.x.z});
+        el.push_back({f, 0.5 * (bu[iu + 1] + bu[iu]), 0.5 * (bu[iu + 1] - bu[iu]),
+                      0.5 * (bv[jv + 1] + bv[jv]), 0.5 * (bv[jv + 1] - bv[jv]), qu, qv});
         fs.nqb.push_back(qu * qv);
         fs.nqf.push_back(fine_mult * qu * fine_mult * qv);
         fs.qb_off.push_back(fs.qb_off.back() + qu * qv);
         fs.qf_off.push_back(fs.qf_off.back() + fine_mult * qu * fine_mult * qv);
-        ++fs.n_elems;
       }
   }
+  fs.n_elems = static_cast<int>(el.size());
+  const size_t tqb = fs.qb_off.back(), tqf = fs.qf_off.back();
+  fs.centers.assign(3 * el.size(), 0.0);
+  fs.dofs.assign(nd * el.size(), 0);
+  fs.xb.assign(3 * tqb, 0.0);
+  fs.nb.assign(3 * tqb, 0.0);
+  fs.wb.assign(tqb, 0.0);
+  fs.Nb.assign(nd * tqb, 0.0);
+  fs.xf.assign(3 * tqf, 0.0);
+  fs.nf.assign(3 * tqf, 0.0);
+  fs.wf.assign(tqf, 0.0);
+  fs.Nf.assign(nd * tqf, 0.0);
+  for (const Elem& e : el) {  // warm the (mutex-guarded) rule cache
+    gauss_rule(e.qu);
+    gauss_rule(e.qv);
+    gauss_rule(fine_mult * e.qu);
+    gauss_rule(fine_mult * e.qv);
+  }
+  parallel_for(static_cast<long>(el.size()), [&](long ei) {
+    const Elem& e = el[ei];
+    std::vector<int> idx;
+    std::vector<double> val;
+    std::vector<Vec3> dv;
+    auto rule = [&](int nu, int nv, long q0, double* X, double* Nn, double* Wt, double* Nt,
+                    bool first) {
+      const auto& gu = gauss_rule(nu);
+      const auto& gv = gauss_rule(nv);
+      long q = q0;
+      for (int b = 0; b < nv; ++b)
+        for (int a = 0; a < nu; ++a, ++q) {
+          const double u = e.mu + e.hu * gu.nodes[a];
+          const double v = e.mv + e.hv * gv.nodes[b];
+          const auto sp = vol.face_point(e.f, u, v);
+          const int nbas = vol.basis_at(sp.xi, idx, val, dv);
+          if (first && q == q0) std::copy(idx.begin(), idx.begin() + nbas, &fs.dofs[ei * nd]);
+          X[3 * q] = sp.x.x;
+          X[3 * q + 1] = sp.x.y;
+          X[3 * q + 2] = sp.x.z;
+          Nn[3 * q] = sp.normal.x;
+          Nn[3 * q + 1] = sp.normal.y;
+          Nn[3 * q + 2] = sp.normal.z;
+          Wt[q] = gu.weights[a] * gv.weights[b] * e.hu * e.hv * sp.area_scale;
+          std::copy(val.begin(), val.begin() + nbas, Nt + q * nd);
+        }
+    };
+    rule(e.qu, e.qv, fs.qb_off[ei], fs.xb.data(), fs.nb.data(), fs.wb.data(), fs.Nb.data(), true);
+    rule(fine_mult * e.qu, fine_mult * e.qv, fs.qf_off[ei], fs.xf.data(), fs.nf.data(),
+         fs.wf.data(), fs.Nf.data(), false);
+    const auto c = vol.face_point(e.f, e.mu, e.mv);
+    fs.centers[3 * ei] = c.x.x;
+    fs.centers[3 * ei + 1] = c.x.y;
+    fs.centers[3 * ei + 2] = c.x.z;
+  });
   return fs;
 }
 

@@ -8,12 +8,15 @@
 // between steps; the host only decides the fine-rule element set per step
 // (the reference's exact arithmetic) and reads back the PCG status.
 #include <algorithm>
+#include <chrono>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <numeric>
 
 #include "context.hpp"
 #include "host/config.hpp"
+#include "host/parallel.hpp"
 #include "host/operator.hpp"
 #include "k2_csr.cuh"
 #include "k2_kron.cuh"
@@ -78,7 +81,23 @@ Sim::~Sim() {
   if (ctx) tg_ctx_destroy(ctx);
 }
 
+namespace {
+// TG_SETUP_TIMING=1: per-phase wall times of the setup on stderr
+struct PhaseClock {
+  bool on = std::getenv("TG_SETUP_TIMING") != nullptr;
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  void mark(const char* what) {
+    if (!on) return;
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[setup] %-28s %8.3f s\n", what,
+                 std::chrono::duration<double>(now - t).count());
+    t = now;
+  }
+};
+}  // namespace
+
 void Sim::setup_host() {
+  PhaseClock clk;
   // prepare_simulation (driver.cpp:66-95)
   vol = refine_for_spec(cfg.geometry, cfg.mesh);
   const auto p = vol.degrees();
@@ -107,7 +126,9 @@ void Sim::setup_host() {
 
   // lateral face sets, with the columns that are exactly zero on every
   // quadrature point of an element dropped (their scatter adds +0, a no-op)
+  clk.mark("volume, dofs, sources");
   FaceSets fs = build_face_sets(vol, cfg.tags, cfg.mesh.boundary_quad_multiplier);
+  clk.mark("face sets");
   n_fe = fs.n_elems;
   const int nd = fs.n_dofs;
   const long tqb = fs.qb_off.back(), tqf = fs.qf_off.back();
@@ -120,17 +141,16 @@ void Sim::setup_host() {
     nqf = std::max(nqf, fs.nqf[e]);
   }
   std::vector<std::vector<int>> keep(n_fe);
-  ndk = 0;
-  for (int e = 0; e < n_fe; ++e) {
+  parallel_for(n_fe, [&](long e) {
     for (int a = 0; a < nd; ++a) {
       bool nz = false;
       for (long q = fs.qb_off[e]; q < fs.qb_off[e + 1] && !nz; ++q) nz = fs.Nb[q * nd + a] != 0.0;
       for (long q = fs.qf_off[e]; q < fs.qf_off[e + 1] && !nz; ++q) nz = fs.Nf[q * nd + a] != 0.0;
       if (nz) keep[e].push_back(a);
     }
-    ndk = std::max<int>(ndk, static_cast<int>(keep[e].size()));
-  }
-  ndk = std::max(ndk, 1);
+  });
+  ndk = 1;
+  for (int e = 0; e < n_fe; ++e) ndk = std::max<int>(ndk, static_cast<int>(keep[e].size()));
   centers = fs.centers;
   h_qx = fs.xb;
   h_qx.insert(h_qx.end(), fs.xf.begin(), fs.xf.end());
@@ -141,22 +161,30 @@ void Sim::setup_host() {
   h_Nb.assign(static_cast<size_t>(tqb) * ndk, 0.0);
   h_Nf.assign(static_cast<size_t>(tqf) * ndk, 0.0);
   h_dofk.assign(static_cast<size_t>(n_fe) * ndk, -1);
-  std::vector<std::vector<int>> inc(n_full);
-  for (int e = 0; e < n_fe; ++e)
+  parallel_for(n_fe, [&](long e) {
     for (size_t kk = 0; kk < keep[e].size(); ++kk) {
       const int a = keep[e][kk];
       for (long q = fs.qb_off[e]; q < fs.qb_off[e + 1]; ++q) h_Nb[q * ndk + kk] = fs.Nb[q * nd + a];
       for (long q = fs.qf_off[e]; q < fs.qf_off[e + 1]; ++q) h_Nf[q * ndk + kk] = fs.Nf[q * nd + a];
-      const int dof = fs.dofs[static_cast<size_t>(e) * nd + a];
-      h_dofk[static_cast<size_t>(e) * ndk + kk] = dof;
-      inc[dof].push_back(e * ndk + static_cast<int>(kk));
+      h_dofk[static_cast<size_t>(e) * ndk + kk] = fs.dofs[static_cast<size_t>(e) * nd + a];
     }
+  });
+  // incidence lists per DOF in the reference's scatter order (face, element, a):
+  // a stable counting sort of the kept (element, column) slots by DOF
   h_inc_ptr.assign(n_full + 1, 0);
-  for (int i = 0; i < n_full; ++i) h_inc_ptr[i + 1] = h_inc_ptr[i] + static_cast<int>(inc[i].size());
-  h_inc_src.reserve(h_inc_ptr[n_full]);
-  for (int i = 0; i < n_full; ++i) h_inc_src.insert(h_inc_src.end(), inc[i].begin(), inc[i].end());
+  for (size_t s2 = 0; s2 < h_dofk.size(); ++s2)
+    if (h_dofk[s2] >= 0) ++h_inc_ptr[h_dofk[s2] + 1];
+  for (int i = 0; i < n_full; ++i) h_inc_ptr[i + 1] += h_inc_ptr[i];
+  h_inc_src.assign(h_inc_ptr[n_full], 0);
+  {
+    std::vector<int> fill(h_inc_ptr.begin(), h_inc_ptr.end() - 1);
+    for (size_t s2 = 0; s2 < h_dofk.size(); ++s2)
+      if (h_dofk[s2] >= 0) h_inc_src[fill[h_dofk[s2]]++] = static_cast<int>(s2);
+  }
 
+  clk.mark("face tables, incidence");
   grev = greville_points(vol, dofs, cfg.tags);
+  clk.mark("greville points");
 
   // operator: Kronecker factors when separable, else the assembled CSR pair
   std::array<std::vector<double>, 3> coord;
@@ -169,6 +197,7 @@ void Sim::setup_host() {
     const double rc = cfg.material.volumetric_capacity(), k = cfg.material.conductivity;
     coefA = {rc / dt, th * k};
     coefB = {rc / dt, -(1.0 - th) * k};
+    clk.mark("kronecker factors");
   } else {
     Csr M, K;
     assemble_mass_stiffness(vol, quad, cfg.material, M, K);
