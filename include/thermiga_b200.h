@@ -184,6 +184,28 @@ int tg_sim_advance(tg_sim* sim, int n_steps, long* cg_iterations, double* last_r
 int tg_sim_state(tg_sim* sim, int* step, double* time, double* free_out, double* g_out,
                  double* F_out);
 
+/* ---- observers (proj/src/postproc.cpp, driver.cpp:226-254) --
+ * The current state (after reset/advance, time = step * dt) at parametric
+ * points xi (n x 3, each coordinate in [0, 1]; others fail like
+ * total_temperature, postproc.cpp:12-14): out (n x 12) per point =
+ *   x, y, z (map_point), T_total = T_c + T_tilde + T_hat (total_temperature),
+ *   T_tilde (superpose), T_hat (field_at), grad T_tilde (3), grad T_hat (3).
+ * The probes, export_field and boundary_flux_profile read these columns. */
+int tg_sim_probe(tg_sim* sim, const double* xi, long n, double* out);
+/* Same on device buffers (synchronous; runs on the simulation's stream). */
+int tg_sim_probe_device(tg_sim* sim, const double* d_xi, long n, double* d_out);
+/* map_point / field_at (proj/src/splines.cpp:257-303) with caller
+ * coefficients (n_full, host, flat order): out_x (n x 3), out_f (n x 4 =
+ * value, physical gradient). coeffs and out_f may be NULL (geometry only). */
+int tg_sim_field_eval(tg_sim* sim, const double* coeffs, const double* xi, long n,
+                      double* out_x, double* out_f);
+/* boundary_flux_profile (postproc.cpp:21-79) of the current state on face
+ * `face` (0 ximin, 1 ximax, 2 etamin, 3 etamax, 4 zetamin, 5 zetamax) at edge
+ * parameter edge_v: out (n_samples x 5) = s, theta (NaN without theta_axis),
+ * q_tilde, q_hat, q_net. theta_axis: NULL or 2 doubles. */
+int tg_sim_flux_profile(tg_sim* sim, int face, int n_samples, double edge_v,
+                        const double* theta_axis, double* out);
+
 #ifdef __cplusplus
 }
 #endif

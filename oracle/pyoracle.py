@@ -87,6 +87,13 @@ class RefLib:
         L.ref_pcg_csr.argtypes = [C.c_int, _ip, _ip, _dp, _dp, _dp, C.c_double, C.c_int, _ip, _dp,
                                   C.c_char_p, C.c_int]
         L.ref_sim_run.argtypes = [C.c_void_p, C.c_int, _dp, C.c_char_p, C.c_int]
+        L.ref_sim_total_temperature.argtypes = [C.c_void_p, _dp, _dp, C.c_double, _dp,
+                                                C.c_char_p, C.c_int]
+        L.ref_sim_flux_profile.argtypes = [C.c_void_p, _dp, C.c_int, C.c_int, C.c_double, _dp,
+                                           C.c_double, _dp, _dp, C.c_char_p, C.c_int]
+        L.ref_sim_export_field.argtypes = [C.c_void_p, _dp, _ip, C.c_double, C.c_char_p,
+                                           C.c_char_p, C.c_int]
+        L.ref_export_profile_csv.argtypes = [_dp, C.c_int, C.c_char_p, C.c_char_p, C.c_int]
 
     # -- analytic ---------------------------------------------------------
     def discretize_scan(self, waypoints, *, start_time=0.0, plane_z=0.0, power, speed,
@@ -281,6 +288,43 @@ class RefSim:
         x = np.ascontiguousarray(xi, dtype=np.float64)
         self.L.ref_sim_map_point(self.h, _ptr(x), _ptr(out))
         return out
+
+    def total_temperature(self, full, xi, t):
+        """total_temperature (postproc.cpp:9-19) with caller coefficients."""
+        out = np.zeros(1)
+        err = C.create_string_buffer(1024)
+        f = np.ascontiguousarray(full, dtype=np.float64)
+        x = np.ascontiguousarray(xi, dtype=np.float64)
+        if self.L.ref_sim_total_temperature(self.h, _ptr(f), _ptr(x), t, _ptr(out), err, 1024):
+            raise RefError(err.value.decode())
+        return float(out[0])
+
+    def flux_profile(self, full, face, n, t, theta_axis=None, edge_v=1.0):
+        """boundary_flux_profile + integrated_abs_flux: (rows (n x 5), metrics[3])."""
+        out = np.zeros((n, 5))
+        met = np.zeros(3)
+        err = C.create_string_buffer(1024)
+        f = np.ascontiguousarray(full, dtype=np.float64)
+        ax = None if theta_axis is None else np.ascontiguousarray(theta_axis, dtype=np.float64)
+        if self.L.ref_sim_flux_profile(self.h, _ptr(f), int(face), int(n), t,
+                                       _ptr(ax) if ax is not None else None, edge_v, _ptr(out),
+                                       _ptr(met), err, 1024):
+            raise RefError(err.value.decode())
+        return out, met
+
+    def export_field(self, full, dims, t, path):
+        err = C.create_string_buffer(1024)
+        f = np.ascontiguousarray(full, dtype=np.float64)
+        d = np.ascontiguousarray(dims, dtype=np.int32)
+        if self.L.ref_sim_export_field(self.h, _ptr(f), _ptr(d, _ip), t, str(path).encode(), err,
+                                       1024):
+            raise RefError(err.value.decode())
+
+    def export_profile_csv(self, rows, path):
+        err = C.create_string_buffer(1024)
+        r = np.ascontiguousarray(rows, dtype=np.float64)
+        if self.L.ref_export_profile_csv(_ptr(r), len(r), str(path).encode(), err, 1024):
+            raise RefError(err.value.decode())
 
     def run(self, n_steps=0):
         t = np.zeros(8)

@@ -9,6 +9,8 @@
 // reference's arithmetic.
 
 #include <chrono>
+#include <cmath>
+#include <optional>
 #include <cstdio>
 #include <cstring>
 #include <exception>
@@ -20,6 +22,7 @@
 #include "thermiga/config.hpp"
 #include "thermiga/driver.hpp"
 #include "thermiga/mesh.hpp"
+#include "thermiga/postproc.hpp"
 #include "thermiga/sparse.hpp"
 #include "thermiga/timestep.hpp"
 
@@ -434,6 +437,78 @@ int ref_sim_field_at(void* h, const double* full, const double* xi, double* out4
   out4[2] = f.grad.y;
   out4[3] = f.grad.z;
   return 0;
+}
+
+// total_temperature (proj/src/postproc.cpp:9-19) at t with caller coefficients.
+int ref_sim_total_temperature(void* h, const double* full, const double* xi, double t,
+                              double* out, char* err, int errlen) {
+  try {
+    const Simulation& s = static_cast<RefSim*>(h)->sim;
+    *out = total_temperature(s.volume(), std::span<const double>(full, s.mesh.n_functions()),
+                             s.sources, s.cfg.material, Vec3{xi[0], xi[1], xi[2]}, t,
+                             s.cfg.superpose);
+    return 0;
+  } catch (const std::exception& e) {
+    put_err(err, errlen, e.what());
+    return 1;
+  }
+}
+
+// boundary_flux_profile (postproc.cpp:21-79) + integrated_abs_flux (:81-95):
+// out (n x 5) = s, theta, q_tilde, q_hat, q_net; metrics[3] = integral_net,
+// integral_analytic, ratio (NaN when absent).
+int ref_sim_flux_profile(void* h, const double* full, int face, int n, double t,
+                         const double* theta_axis, double edge_v, double* out, double* metrics,
+                         char* err, int errlen) {
+  try {
+    const Simulation& s = static_cast<RefSim*>(h)->sim;
+    std::optional<std::array<double, 2>> ax;
+    if (theta_axis) ax = std::array<double, 2>{theta_axis[0], theta_axis[1]};
+    const FluxProfile p = boundary_flux_profile(
+        s.volume(), std::span<const double>(full, s.mesh.n_functions()), s.sources,
+        s.cfg.material, static_cast<FaceId>(face), n, t, ax, edge_v, s.cfg.superpose);
+    for (int i = 0; i < n; ++i) {
+      const auto& q = p.samples[i];
+      const double row[5] = {q.s, q.theta, q.q_tilde, q.q_hat, q.q_net};
+      std::memcpy(out + 5 * i, row, sizeof(row));
+    }
+    const FluxMetrics m = integrated_abs_flux(p);
+    metrics[0] = m.integral_net;
+    metrics[1] = m.integral_analytic;
+    metrics[2] = m.ratio ? *m.ratio : std::nan("");
+    return 0;
+  } catch (const std::exception& e) {
+    put_err(err, errlen, e.what());
+    return 1;
+  }
+}
+
+// export_field (postproc.cpp:101-147) and export_profile_csv (:149-159) to a path.
+int ref_sim_export_field(void* h, const double* full, const int* dims, double t,
+                         const char* path, char* err, int errlen) {
+  try {
+    const Simulation& s = static_cast<RefSim*>(h)->sim;
+    export_field(s.volume(), std::span<const double>(full, s.mesh.n_functions()), s.sources,
+                 s.cfg.material, {dims[0], dims[1], dims[2]}, t, path, s.cfg.superpose);
+    return 0;
+  } catch (const std::exception& e) {
+    put_err(err, errlen, e.what());
+    return 1;
+  }
+}
+
+int ref_export_profile_csv(const double* rows, int n, const char* path, char* err, int errlen) {
+  try {
+    FluxProfile p;
+    for (int i = 0; i < n; ++i)
+      p.samples.push_back({rows[5 * i], rows[5 * i + 1], rows[5 * i + 2], rows[5 * i + 3],
+                           rows[5 * i + 4]});
+    export_profile_csv(p, path);
+    return 0;
+  } catch (const std::exception& e) {
+    put_err(err, errlen, e.what());
+    return 1;
+  }
 }
 
 // map_point (proj/src/splines.cpp:257-278).

@@ -6,7 +6,9 @@ binding and the seeded BASELINE workloads.
 """
 from .api import (ConfigError, Context, CudaError, LaserSpec, Material, NumericError, ScanPath,
                   Simulation,
-                  SuperposeOptions, ThermigaError, discretize_scan, lib, superpose)
+                  SuperposeOptions, ThermigaError, discretize_scan, export_profile_csv,
+                  integrated_abs_flux, lib, superpose)
 
 __all__ = ["ConfigError", "Context", "CudaError", "LaserSpec", "Material", "NumericError",
-           "ScanPath", "Simulation", "SuperposeOptions", "ThermigaError", "discretize_scan", "lib", "superpose"]
+           "ScanPath", "Simulation", "SuperposeOptions", "ThermigaError", "discretize_scan",
+           "export_profile_csv", "integrated_abs_flux", "lib", "superpose"]

@@ -26,6 +26,11 @@ COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler",
           "-I", os.path.join(ROOT, "include"), "-I", CSRC]
 
 
+# files whose arithmetic must round every product and sum separately (the
+# host / reference association, no FMA contraction)
+NO_FMAD = {"k4_eval.cu"}
+
+
 def _sources():
     srcs = sorted(glob.glob(os.path.join(CSRC, "**", "*.cu"), recursive=True))
     srcs += sorted(glob.glob(os.path.join(CSRC, "**", "*.cpp"), recursive=True))
@@ -48,7 +53,8 @@ def _obj_for(src):
 def _compile(src, verbose):
     obj = _obj_for(src)
     if src.endswith(".cu"):
-        cmd = [NVCC, *ARCH, *COMMON, "-Xptxas", "-warn-spills", "-c", src, "-o", obj]
+        extra = ["-fmad=false"] if os.path.basename(src) in NO_FMAD else []
+        cmd = [NVCC, *ARCH, *COMMON, *extra, "-Xptxas", "-warn-spills", "-c", src, "-o", obj]
     else:
         # host C++: compiled by the host compiler through nvcc, no FMA contraction
         # (bit-exact setup arithmetic with the reference's x86-64 build)

@@ -293,6 +293,10 @@ def _bind_sim(L):
     L.tg_sim_reset.argtypes = [C.c_void_p]
     L.tg_sim_advance.argtypes = [C.c_void_p, C.c_int, C.POINTER(C.c_long), _dp]
     L.tg_sim_state.argtypes = [C.c_void_p, _ip, _dp, _dp, _dp, _dp]
+    L.tg_sim_probe.argtypes = [C.c_void_p, _dp, C.c_long, _dp]
+    L.tg_sim_probe_device.argtypes = [C.c_void_p, C.c_void_p, C.c_long, C.c_void_p]
+    L.tg_sim_field_eval.argtypes = [C.c_void_p, _dp, _dp, C.c_long, _dp, _dp]
+    L.tg_sim_flux_profile.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_double, _dp, _dp]
     L._sim_bound = True
 
 
@@ -437,3 +441,127 @@ class Simulation:
         F = np.zeros(self.info["n_full"])
         self._check(self._L.tg_sim_state(self._h, C.byref(step), C.byref(t), _p(x), _p(g), _p(F)))
         return dict(step=step.value, time=t.value, free=x, g=g, F=F)
+
+    # -- observers (proj/src/postproc.cpp, driver.cpp:226-254) --
+    PROBE_COLUMNS = ["x", "y", "z", "T_total", "T_tilde", "T_hat", "gx_tilde", "gy_tilde",
+                     "gz_tilde", "gx_hat", "gy_hat", "gz_hat"]
+
+    def probe(self, xi):
+        """The current state (time = step * dt) at parametric points xi (n x 3
+        in [0, 1]^3): an (n x 12) array with the columns PROBE_COLUMNS —
+        map_point, total_temperature, superpose value/gradient, field_at
+        value/gradient (postproc.cpp:9-19, splines.cpp:257-303). A torch CUDA
+        tensor input stays on the device (tg_sim_probe_device)."""
+        try:
+            import torch
+            if isinstance(xi, torch.Tensor) and xi.is_cuda:
+                x = xi.to(torch.float64).contiguous()
+                out = torch.empty((x.numel() // 3, 12), dtype=torch.float64, device=x.device)
+                torch.cuda.current_stream().synchronize()
+                self._check(self._L.tg_sim_probe_device(self._h, x.data_ptr(), x.numel() // 3,
+                                                        out.data_ptr()))
+                return out
+        except ImportError:
+            pass
+        x = _f64(np.asarray(xi, dtype=np.float64).reshape(-1, 3))
+        out = np.zeros((len(x), 12))
+        self._check(self._L.tg_sim_probe(self._h, _p(x), len(x), _p(out)))
+        return out
+
+    def total_temperature(self, xi):
+        """total_temperature (postproc.cpp:9-19) of the current state: T_c +
+        T_tilde + T_hat at each parametric point."""
+        return self.probe(xi)[:, 3]
+
+    def field_eval(self, coeffs, xi):
+        """map_point and field_at with caller coefficients (n_full, flat
+        order): (x (n x 3), f (n x 4: value, physical gradient)); coeffs=None
+        evaluates the geometry only."""
+        x = _f64(np.asarray(xi, dtype=np.float64).reshape(-1, 3))
+        xo = np.zeros((len(x), 3))
+        if coeffs is None:
+            self._check(self._L.tg_sim_field_eval(self._h, None, _p(x), len(x), _p(xo), None))
+            return xo, None
+        c = _f64(coeffs)
+        fo = np.zeros((len(x), 4))
+        self._check(self._L.tg_sim_field_eval(self._h, _p(c), _p(x), len(x), _p(xo), _p(fo)))
+        return xo, fo
+
+    FACES = {"ximin": 0, "ximax": 1, "etamin": 2, "etamax": 3, "zetamin": 4, "zetamax": 5}
+
+    def boundary_flux_profile(self, face, n_samples, theta_axis=None, edge_v=1.0):
+        """boundary_flux_profile (postproc.cpp:21-79) of the current state:
+        (n_samples x 5) array of s, theta, q_tilde, q_hat, q_net (theta NaN
+        without theta_axis)."""
+        f = self.FACES[face] if isinstance(face, str) else int(face)
+        out = np.zeros((int(n_samples), 5))
+        ax = None if theta_axis is None else _f64(theta_axis)
+        self._check(self._L.tg_sim_flux_profile(self._h, f, int(n_samples), float(edge_v),
+                                                _p(ax) if ax is not None else None, _p(out)))
+        return out
+
+    def export_field(self, path, grid_dims):
+        """export_field (postproc.cpp:101-147) of the current state: legacy
+        ASCII VTK structured grid of T_total / T_tilde / T_hat on a parametric
+        grid, byte-identical to the reference writer for the same values."""
+        nx, ny, nz = (int(d) for d in grid_dims)
+        if min(nx, ny, nz) < 2:
+            raise ValueError("field grid needs >= 2 per direction")
+        k, j, i = np.meshgrid(np.arange(nz), np.arange(ny), np.arange(nx), indexing="ij")
+        xi = np.stack([i.ravel() / (nx - 1), j.ravel() / (ny - 1), k.ravel() / (nz - 1)], axis=1)
+        pr = self.probe(xi)
+        t = self.state_time()
+        tc = self.params["platform_temperature"]
+        n = len(xi)
+        g = "%.17g"
+        lines = ["# vtk DataFile Version 3.0",
+                 f"thermiga temperature field at t={g % t} s", "ASCII",
+                 "DATASET STRUCTURED_GRID", f"DIMENSIONS {nx} {ny} {nz}", f"POINTS {n} double"]
+        lines += [f"{g % a} {g % b} {g % c}" for a, b, c in pr[:, :3]]
+        lines.append(f"POINT_DATA {n}")
+        for name, col in (("T_total", None), ("T_tilde", 4), ("T_hat", 5)):
+            lines += [f"SCALARS {name} double 1", "LOOKUP_TABLE default"]
+            vals = (tc + pr[:, 4] + pr[:, 5]) if col is None else pr[:, col]
+            lines += [g % v for v in vals]
+        try:
+            with open(path, "w") as fh:
+                fh.write("\n".join(lines) + "\n")
+        except OSError as e:
+            raise IOError_(f"cannot open {path}") from e
+
+    def state_time(self):
+        step = C.c_int(0)
+        t = C.c_double(0.0)
+        self._check(self._L.tg_sim_state(self._h, C.byref(step), C.byref(t), None, None, None))
+        return t.value
+
+
+def integrated_abs_flux(profile):
+    """integrated_abs_flux (postproc.cpp:81-95): composite-trapezoid integrals
+    of |q_net| and |q_tilde| over arc length; ratio None when the analytic
+    integral is zero."""
+    p = np.asarray(profile, dtype=np.float64)
+    if len(p) < 2:
+        raise ValueError("flux metrics need >= 2 samples")
+    net = ana = 0.0
+    for i in range(1, len(p)):
+        ds = p[i, 0] - p[i - 1, 0]
+        net += 0.5 * ds * (abs(p[i - 1, 4]) + abs(p[i, 4]))
+        ana += 0.5 * ds * (abs(p[i - 1, 2]) + abs(p[i, 2]))
+    return {"integral_net": float(net), "integral_analytic": float(ana),
+            "ratio": float(net / ana) if ana > 0.0 else None}
+
+
+def export_profile_csv(profile, path):
+    """export_profile_csv (postproc.cpp:149-159)."""
+    p = np.asarray(profile, dtype=np.float64)
+    if len(p) == 0:
+        raise ValueError("refusing to write an empty flux profile")
+    g = "%.17g"
+    try:
+        with open(path, "w") as fh:
+            fh.write("s_m,theta_rad,q_tilde_W_m2,q_hat_W_m2,q_net_W_m2\n")
+            for r in p:
+                fh.write(",".join(g % v for v in r) + "\n")
+    except OSError as e:
+        raise IOError_(f"cannot open {path}") from e

@@ -12,6 +12,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <limits>
 #include <numeric>
 
 #include "context.hpp"
@@ -521,6 +522,144 @@ PcgStatus Sim::advance() {
   std::swap(d_gn.p, d_g1.p);
   step = s1;
   return st;
+}
+
+// ---------------------------------------------------------------------------
+// observers: K4 NURBS evaluation + K1 on the device
+
+void Sim::upload_nurbs() {
+  if (nurbs_up) return;
+  cudaStream_t s = ctx->stream;
+  std::vector<double> kn;
+  size_t off[3];
+  for (int d = 0; d < 3; ++d) {
+    off[d] = kn.size();
+    const auto& U = vol.knots(d).values();
+    kn.insert(kn.end(), U.begin(), U.end());
+  }
+  upload(d_knots, kn, s);
+  const ControlGrid& g = vol.grid();
+  std::vector<double> cp(4 * static_cast<size_t>(g.count()));
+  for (int i = 0; i < g.count(); ++i)
+    for (int c = 0; c < 4; ++c) cp[4 * static_cast<size_t>(i) + c] = g.pts[i][c];
+  upload(d_cpts, cp, s);
+  const auto n = vol.basis_counts();
+  for (int d = 0; d < 3; ++d) {
+    nurbs.p[d] = vol.knots(d).degree();
+    nurbs.n[d] = n[d];
+    nurbs.U[d] = d_knots.p + off[d];
+  }
+  nurbs.pts = d_cpts.p;
+  d_eflags.ensure(1);
+  TG_CUDA(cudaStreamSynchronize(s));
+  nurbs_up = true;
+}
+
+void Sim::field_eval_device(const double* d_coeffs, const double* d_xi, long n, double* d_xo,
+                            double* d_f, cudaStream_t s) {
+  if (n <= 0) return;
+  upload_nurbs();
+  TG_CUDA(cudaMemsetAsync(d_eflags.p, 0, sizeof(int), s));
+  k4_eval(nurbs, d_xi, n, d_coeffs, d_xo, d_f, d_eflags.p, s);
+  ++ctx->timer.launches;
+  int flags = 0;
+  TG_CUDA(cudaMemcpyAsync(&flags, d_eflags.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+  TG_CUDA(cudaStreamSynchronize(s));
+  if (flags & kEvalOutside)  // postproc.cpp:12-14
+    throw std::domain_error("probe parametric coordinates outside the patch");
+  if (flags & kEvalDomain) throw std::domain_error("parameter outside knot range");
+  if (flags & kEvalJacobian)
+    throw numeric_error("non-positive Jacobian determinant in field evaluation");
+}
+
+void Sim::probe_device(const double* d_xi, long n, double* d_out, cudaStream_t s) {
+  if (n <= 0) return;
+  upload_nurbs();
+  // full coefficients of the current state (DirichletSystem::expand,
+  // assembly.cpp:274-281); d_T is rebuilt by every theta step
+  const int threads = 256;
+  expand_kernel<<<static_cast<int>((n_full + threads - 1) / threads), threads, 0, s>>>(
+      geom, d_x.p, d_gn.p, d_T.p);
+  ++ctx->timer.launches;
+  double* xo = d_px.ensure(3 * static_cast<size_t>(n));
+  double* fo = d_pf.ensure(4 * static_cast<size_t>(n));
+  TG_CUDA(cudaMemsetAsync(d_eflags.p, 0, sizeof(int), s));
+  k4_eval(nurbs, d_xi, n, d_T.p, xo, fo, d_eflags.p, s, true);
+  ++ctx->timer.launches;
+  int flags = 0;
+  TG_CUDA(cudaMemcpyAsync(&flags, d_eflags.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+  TG_CUDA(cudaStreamSynchronize(s));
+  if (flags & kEvalOutside)
+    throw std::domain_error("probe parametric coordinates outside the patch");
+  if (flags & kEvalDomain) throw std::domain_error("parameter outside knot range");
+  if (flags & kEvalJacobian)
+    throw numeric_error("non-positive Jacobian determinant in field evaluation");
+  const double t = step * dt_solver;  // State::time (timestep.cpp:22)
+  double* val = d_pval.ensure(n);
+  double* grad = d_pgrad.ensure(3 * static_cast<size_t>(n));
+  k1_run(ctx, ctx->src6.p, ctx->n_src, xo, nullptr, n, t, cfg.superpose.cull_exponent,
+         K1Mode::field, val, grad, {}, s);
+  k4_assemble_probe(n, cfg.material.platform_temperature, xo, fo, val, grad, d_out, s);
+  ++ctx->timer.launches;
+}
+
+void Sim::flux_profile(FaceId face, int ns, double edge_v, const double* theta_axis,
+                       double* out) {
+  if (ns < 2) throw std::invalid_argument("flux profile needs >= 2 samples");
+  const double k = cfg.material.conductivity;
+  const auto tang = face_tangent_axes(face);
+  // arc length along the edge: 4-point Gauss per interval, split at the
+  // tangent direction's breakpoints (postproc.cpp:33-52)
+  const GaussRule& quadr = gauss_rule(4);
+  const auto breaks = vol.knots(tang[0]).breakpoints();
+  auto segment_length = [&](double a, double b) {
+    std::vector<double> cuts{a};
+    for (double bp : breaks)
+      if (bp > a && bp < b) cuts.push_back(bp);
+    cuts.push_back(b);
+    double len = 0.0;
+    for (size_t c = 0; c + 1 < cuts.size(); ++c) {
+      const double h = 0.5 * (cuts[c + 1] - cuts[c]), m = 0.5 * (cuts[c + 1] + cuts[c]);
+      for (size_t q = 0; q < quadr.nodes.size(); ++q) {
+        const auto pm = vol.map_point(face_param(face, m + h * quadr.nodes[q], edge_v));
+        const Vec3 du{pm.jac(0, tang[0]), pm.jac(1, tang[0]), pm.jac(2, tang[0])};
+        len += quadr.weights[q] * h * du.norm();
+      }
+    }
+    return len;
+  };
+  std::vector<double> xi(3 * static_cast<size_t>(ns)), arc(ns);
+  std::vector<Vec3> xs(ns), nrm(ns);
+  double sacc = 0.0, u_prev = 0.0;
+  for (int i = 0; i < ns; ++i) {
+    const double u = static_cast<double>(i) / (ns - 1);
+    if (i > 0) sacc += segment_length(u_prev, u);
+    u_prev = u;
+    const auto sp = vol.face_point(face, u, edge_v);
+    for (int d = 0; d < 3; ++d) xi[3 * i + d] = sp.xi[d];
+    xs[i] = sp.x;
+    nrm[i] = sp.normal;
+    arc[i] = sacc;
+  }
+  cudaStream_t s = ctx->stream;
+  DevBuf<double> d_xi, d_o;
+  upload(d_xi, xi, s);
+  d_o.ensure(12 * static_cast<size_t>(ns));
+  probe_device(d_xi.p, ns, d_o.p, s);
+  std::vector<double> o(12 * static_cast<size_t>(ns));
+  TG_CUDA(cudaMemcpyAsync(o.data(), d_o.p, sizeof(double) * o.size(), cudaMemcpyDeviceToHost, s));
+  TG_CUDA(cudaStreamSynchronize(s));
+  for (int i = 0; i < ns; ++i) {
+    const double* r = &o[12 * static_cast<size_t>(i)];
+    const Vec3 gt{r[6], r[7], r[8]}, gh{r[9], r[10], r[11]};
+    double* row = out + 5 * static_cast<size_t>(i);
+    row[0] = arc[i];
+    row[1] = theta_axis ? std::atan2(-(xs[i].x - theta_axis[0]), xs[i].y - theta_axis[1])
+                        : std::numeric_limits<double>::quiet_NaN();
+    row[2] = -k * gt.dot(nrm[i]);
+    row[3] = -k * gh.dot(nrm[i]);
+    row[4] = row[2] + row[3];
+  }
 }
 
 }  // namespace tgb

@@ -10,6 +10,7 @@
 #include "host/operator.hpp"
 #include "k2_csr.cuh"
 #include "k2_kron.cuh"
+#include "k4_eval.cuh"
 
 namespace tgb {
 
@@ -47,6 +48,17 @@ class Sim {
   void flux_gather_device(const double* d_loc_all, double* d_F);
   void dirichlet_device(double t, double* d_g);
   PcgStatus theta_step_device(double tol, int max_iter);  // uses d_x, d_gn, d_g1, d_Fn, d_F1
+
+  // observers: the current state at parametric points, on
+  // device buffers: d_out (n x 12) = x, T_total, T_tilde, T_hat, grad T_tilde,
+  // grad T_hat (k4_eval.cuh); map_point / field_at with caller coefficients
+  void probe_device(const double* d_xi, long n, double* d_out, cudaStream_t s);
+  void field_eval_device(const double* d_coeffs, const double* d_xi, long n, double* d_x,
+                         double* d_f, cudaStream_t s);
+  // boundary_flux_profile (postproc.cpp:21-79): out (n_samples x 5) = s,
+  // theta, q_tilde, q_hat, q_net
+  void flux_profile(FaceId face, int n_samples, double edge_v, const double* theta_axis,
+                    double* out);
 
   bool focus_at(double t, Vec3& focus) const;
   int fine_elements(double t, double radius);  // fills h_fine, returns the count
@@ -87,6 +99,12 @@ class Sim {
   bool use_cg1 = false;
   Cg1Maps cg1maps{};
   DevBuf<double> d_w2, d_s2;
+  // observers: the patch on the device (uploaded on first use) and scratch
+  NurbsDev nurbs{};
+  bool nurbs_up = false;
+  DevBuf<double> d_knots, d_cpts, d_px, d_pf, d_pval, d_pgrad;
+  DevBuf<int> d_eflags;
+  void upload_nurbs();
   TensorMap3 map_T{}, map_g{};
   bool rhs_tma = false;
   DevBuf<PcgStatus> d_status;

@@ -283,4 +283,60 @@ int tg_sim_operator_apply(tg_sim* s, const double* x_free, double* y_free) {
   });
 }
 
+int tg_sim_probe(tg_sim* s, const double* xi, long n, double* out) {
+  return sim_guard(s, [&](Sim& m) {
+    if (n < 0 || (n > 0 && (!xi || !out))) throw std::invalid_argument("probe: bad args");
+    if (n == 0) return;
+    cudaStream_t st = m.ctx->stream;
+    DevBuf<double> d_xi, d_o;
+    d_xi.ensure(3 * static_cast<size_t>(n));
+    d_o.ensure(12 * static_cast<size_t>(n));
+    h2d(d_xi.p, xi, 3 * n, st);
+    m.probe_device(d_xi.p, n, d_o.p, st);
+    d2h(out, d_o.p, 12 * n, st);
+    TG_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+int tg_sim_probe_device(tg_sim* s, const double* d_xi, long n, double* d_out) {
+  return sim_guard(s, [&](Sim& m) {
+    if (n < 0 || (n > 0 && (!d_xi || !d_out))) throw std::invalid_argument("probe: bad args");
+    m.probe_device(d_xi, n, d_out, m.ctx->stream);
+    TG_CUDA(cudaStreamSynchronize(m.ctx->stream));
+  });
+}
+
+int tg_sim_field_eval(tg_sim* s, const double* coeffs, const double* xi, long n, double* out_x,
+                      double* out_f) {
+  return sim_guard(s, [&](Sim& m) {
+    if (n < 0 || (n > 0 && (!xi || !out_x)) || (out_f && !coeffs))
+      throw std::invalid_argument("field_eval: bad args");
+    if (n == 0) return;
+    cudaStream_t st = m.ctx->stream;
+    DevBuf<double> d_c, d_xi, d_x, d_f;
+    d_xi.ensure(3 * static_cast<size_t>(n));
+    d_x.ensure(3 * static_cast<size_t>(n));
+    h2d(d_xi.p, xi, 3 * n, st);
+    const double* dc = nullptr;
+    if (out_f) {
+      d_c.ensure(m.n_full);
+      h2d(d_c.p, coeffs, m.n_full, st);
+      d_f.ensure(4 * static_cast<size_t>(n));
+      dc = d_c.p;
+    }
+    m.field_eval_device(dc, d_xi.p, n, d_x.p, out_f ? d_f.p : nullptr, st);
+    d2h(out_x, d_x.p, 3 * n, st);
+    if (out_f) d2h(out_f, d_f.p, 4 * n, st);
+    TG_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+int tg_sim_flux_profile(tg_sim* s, int face, int n_samples, double edge_v,
+                        const double* theta_axis, double* out) {
+  return sim_guard(s, [&](Sim& m) {
+    if (face < 0 || face > 5 || !out) throw std::invalid_argument("flux_profile: bad args");
+    m.flux_profile(static_cast<FaceId>(face), n_samples, edge_v, theta_axis, out);
+  });
+}
+
 }  // extern "C"
