@@ -109,6 +109,9 @@ typedef struct tg_sim_options {
   int max_iter;      /* [stepping] max_iter */
   int device;        /* CUDA device ordinal */
   int host_only;     /* 1: host setup only (no device; compute calls fail) */
+  int preconditioner; /* 0: Jacobi, the reference's pcg_jacobi (default);
+                         1: fast diagonalization (separable patches; the
+                         same PCG loop converges in 1-2 iterations) */
 } tg_sim_options;
 
 /* parse_config + prepare_simulation (proj/src/config.cpp:253-416,
@@ -121,7 +124,8 @@ const char* tg_sim_last_error(const tg_sim* sim);
 int tg_sim_context(tg_sim* sim, tg_ctx** out);
 /* out[18]: n_full, n_free, n_constrained, n_steps, n_sources, n_face_elements,
  * nx, ny, nz, px, py, pz, operator (0 assembled CSR, 1 Kronecker, 2 Kronecker with the
- * single-sweep solver on the device), max nq_base, max nq_fine,
+ * single-sweep solver on the device, 3 Kronecker with the fast-diagonalization
+ * preconditioner), max nq_base, max nq_fine,
  * ndofs_kept, total base qps, total fine qps */
 int tg_sim_info(tg_sim* sim, long* out);
 /* out[10]: dt_solver, theta, solver_tol, elevate_radius, cull_exponent,
@@ -183,6 +187,13 @@ int tg_sim_advance(tg_sim* sim, int n_steps, long* cg_iterations, double* last_r
 /* Copy the current state to the host (any pointer may be NULL). */
 int tg_sim_state(tg_sim* sim, int* step, double* time, double* free_out, double* g_out,
                  double* F_out);
+
+/* Host helper behind the fast-diagonalization preconditioner (exposed for
+ * tests): K_d V = M_d V diag(lam), V^T M_d V = I for rows/cols
+ * [first, first + n) of banded 1D factors (n_band x (2p+1), [i][p + j - i]).
+ * V: n x n column-major. */
+int tg_fdm_factor(const double* Mband, const double* Kband, int n_band, int p, int first, int n,
+                  double* V, double* lam);
 
 /* ---- observers (proj/src/postproc.cpp, driver.cpp:226-254) --
  * The current state (after reset/advance, time = step * dt) at parametric

@@ -31,6 +31,12 @@ COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler",
 NO_FMAD = {"k4_eval.cu"}
 
 
+# cuBLAS (plain library GEMMs of the fast-diagonalization preconditioner)
+CUDA_LIB = os.path.join(os.path.dirname(os.path.dirname(os.path.realpath(
+    __import__("shutil").which(NVCC) or "/usr/local/cuda/bin/nvcc"))), "lib64")
+LINK = ["-L" + CUDA_LIB, "-lcublas", "-Xlinker", "-rpath=" + CUDA_LIB]
+
+
 def _sources():
     srcs = sorted(glob.glob(os.path.join(CSRC, "**", "*.cu"), recursive=True))
     srcs += sorted(glob.glob(os.path.join(CSRC, "**", "*.cpp"), recursive=True))
@@ -87,7 +93,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         list(ex.map(lambda s: _compile(s, verbose), todo))
     objs = [_obj_for(s) for s in _sources()]
     if force or todo or not os.path.exists(LIB):
-        cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", LIB, *objs]
+        cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", LIB, *objs, *LINK]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")

@@ -268,7 +268,7 @@ def superpose(sources, mat: Material, x, t: float, opts: SuperposeOptions = Supe
 
 class _SimOptions(C.Structure):
     _fields_ = [("t_end", C.c_double), ("solver_tol", C.c_double), ("max_iter", C.c_int),
-                ("device", C.c_int), ("host_only", C.c_int)]
+                ("device", C.c_int), ("host_only", C.c_int), ("preconditioner", C.c_int)]
 
 
 def _bind_sim(L):
@@ -324,11 +324,14 @@ class Simulation:
     PARAM_KEYS = ["dt", "theta", "solver_tol", "elevate_radius", "cull", "conductivity",
                   "density", "heat_capacity", "platform_temperature", "max_iter"]
 
+    PRECONDITIONERS = {"jacobi": 0, "fdm": 1}
+
     def __init__(self, config_path, t_end=0.0, solver_tol=0.0, max_iter=0, device=0,
-                 host_only=False):
+                 host_only=False, preconditioner="jacobi"):
         L = self._L = lib()
         _bind_sim(L)
-        opt = _SimOptions(t_end, solver_tol, max_iter, device, int(host_only))
+        opt = _SimOptions(t_end, solver_tol, max_iter, device, int(host_only),
+                          self.PRECONDITIONERS[preconditioner])
         h = C.c_void_p()
         rc = L.tg_sim_create(str(config_path).encode(), C.byref(opt), C.byref(h))
         self._h = h

@@ -17,6 +17,7 @@
 
 #include "context.hpp"
 #include "host/config.hpp"
+#include "host/fdm.hpp"
 #include "host/parallel.hpp"
 #include "host/operator.hpp"
 #include "k2_csr.cuh"
@@ -73,10 +74,12 @@ Sim::Sim(const std::string& path, const SimOptions& opt) {
   if (opt.max_iter > 0) c.stepping.max_iter = opt.max_iter;
   cfg = std::move(c);
   setup_host();
-  if (!opt.host_only) setup_device(opt.device);
+  if (!opt.host_only) setup_device(opt.device, opt.preconditioner);
 }
 
 Sim::~Sim() {
+  if (cublas) cublasDestroy(cublas);
+  if (h_dots) cudaFreeHost(h_dots);
   if (h_status) cudaFreeHost(h_status);
   if (h_fine) cudaFreeHost(h_fine);
   if (ctx) tg_ctx_destroy(ctx);
@@ -245,7 +248,7 @@ void Sim::setup_host() {
   }
 }
 
-void Sim::setup_device(int device) {
+void Sim::setup_device(int device, int preconditioner) {
   const int rc = tg_ctx_create(device, &ctx);
   if (rc != TG_OK) {
     const std::string msg = ctx ? ctx->err : std::string("context creation failed");
@@ -354,6 +357,35 @@ void Sim::setup_device(int device) {
                 k2_make_map(gfree, d_x.p, &m.xc, false) && k2_make_map(gfree, d_p.p, &m.pc, false);
       if (use_cg1) pcg_blocks = k2_cg1_max_blocks(p, ctx->sm_count, gfree.n[2]);
     }
+    if (preconditioner == 1) {
+      // V_d, lambda_d per direction on the free grid (host/fdm.cpp)
+      std::vector<double> Vall, Lall;
+      size_t offV[3], offL[3];
+      for (int d = 0; d < 3; ++d) {
+        const int first = (d == geom.ax && geom.layer == 0) ? 1 : 0;
+        const Fdm1D f = fdm_factor(band[d].M, band[d].K, band[d].n, p, first, gfree.n[d]);
+        offV[d] = Vall.size();
+        offL[d] = Lall.size();
+        Vall.insert(Vall.end(), f.V.begin(), f.V.end());
+        Lall.insert(Lall.end(), f.lam.begin(), f.lam.end());
+      }
+      upload(d_fdmV, Vall, s);
+      upload(d_fdmL, Lall, s);
+      d_fdmDinv.ensure(n_free);
+      fdm_inverse_eigs(gfree.n, d_fdmL.p + offL[0], d_fdmL.p + offL[1], d_fdmL.p + offL[2],
+                       coefA[0], coefA[1], d_fdmDinv.p, s);
+      for (int d = 0; d < 3; ++d) {
+        fdm.n[d] = gfree.n[d];
+        fdm.V[d] = d_fdmV.p + offV[d];
+      }
+      fdm.dinv = d_fdmDinv.p;
+      if (cublasCreate(&cublas) != CUBLAS_STATUS_SUCCESS) throw cuda_error("cublas: create failed");
+      d_w2.ensure(n_free);
+      d_dots.ensure(2);
+      TG_CUDA(cudaMallocHost(&h_dots, 2 * sizeof(double)));
+      use_fdm = true;
+      use_cg1 = false;
+    }
   } else {
     auto up = [&](const Csr& C, DevBuf<int>& rp, DevBuf<int>& ci, DevBuf<double>& v, DevCsr& out) {
       upload(rp, C.row_ptr, s);
@@ -368,7 +400,7 @@ void Sim::setup_device(int device) {
     csr_inverse_diagonal(devA, d_invd.p, d_status.p, s);
     pcg_blocks = csr_pcg_max_blocks(ctx->sm_count);
   }
-  d_partials.ensure(8 * static_cast<size_t>(pcg_blocks) + 8);
+  d_partials.ensure(std::max<size_t>(8 * static_cast<size_t>(pcg_blocks) + 8, 1024));
   TG_CUDA(cudaMemcpyAsync(h_status, d_status.p, sizeof(PcgStatus), cudaMemcpyDeviceToHost, s));
   TG_CUDA(cudaStreamSynchronize(s));
   diag_ok = h_status->status != 2;
@@ -462,7 +494,14 @@ PcgStatus Sim::theta_step_device(double tol, int max_iter) {
     k2_theta_rhs(gfull, coefB[0], coefB[1], -coefA[0], -coefA[1], ra, rhs_tma ? &map_T : nullptr,
                  rhs_tma ? &map_g : nullptr, ctx->sm_count, s);
     ctx->timer.launches += 2;
-    if (use_cg1) {
+    if (use_fdm) {
+      const FdmWork w{d_r.p, d_z.p, d_p.p, d_Ap.p, d_p2.p, d_w2.p, d_partials.p, d_dots.p, h_dots};
+      ctx->timer.timed(2, s, [&] {
+        *h_status = fdm_pcg_solve(cublas, gfree, coefA[0], coefA[1], fdm, d_rhs.p, d_x.p, w, tol,
+                                  max_iter, ctx->sm_count, s);
+      });
+      TG_CUDA(cudaMemcpyAsync(d_status.p, h_status, sizeof(PcgStatus), cudaMemcpyHostToDevice, s));
+    } else if (use_cg1) {
       const Cg1Work w{d_p.p,    {d_r.p, d_z.p}, {d_Ap.p, d_w2.p}, {d_p2.p, d_s2.p},
                       d_invd.p, d_partials.p,   d_status.p};
       ctx->timer.timed(2, s, [&] {

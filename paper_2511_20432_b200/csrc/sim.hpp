@@ -9,6 +9,7 @@
 #include "host/config.hpp"
 #include "host/operator.hpp"
 #include "k2_csr.cuh"
+#include "k2_fdm.cuh"
 #include "k2_kron.cuh"
 #include "k4_eval.cuh"
 
@@ -27,6 +28,7 @@ struct SimOptions {
   int max_iter = 0;         // > 0 overrides the config
   int device = 0;
   bool host_only = false;
+  int preconditioner = 0;  // 0 Jacobi (reference), 1 fast diagonalization
 };
 
 class Sim {
@@ -97,6 +99,12 @@ class Sim {
   // single-sweep solve (k2_cg1_solve): the default when TMA can address the
   // free grid; TG_K2_ALGO=pcg selects the two-phase kernel
   bool use_cg1 = false;
+  // fast-diagonalization preconditioner (k2_fdm.cuh), opt-in
+  bool use_fdm = false;
+  FdmDev fdm{};
+  DevBuf<double> d_fdmV, d_fdmL, d_fdmDinv, d_dots;
+  double* h_dots = nullptr;
+  cublasHandle_t cublas = nullptr;
   Cg1Maps cg1maps{};
   DevBuf<double> d_w2, d_s2;
   // observers: the patch on the device (uploaded on first use) and scratch
@@ -119,7 +127,7 @@ class Sim {
 
  private:
   void setup_host();
-  void setup_device(int device);
+  void setup_device(int device, int preconditioner);
 };
 
 }  // namespace tgb

@@ -1,6 +1,7 @@
 // C ABI of the simulation engine: tg_sim_* (include/thermiga_b200.h).
 #include <cstring>
 
+#include "host/fdm.hpp"
 #include "sim.hpp"
 
 using namespace tgb;
@@ -58,6 +59,7 @@ int tg_sim_create(const char* config_path, const tg_sim_options* opt, tg_sim** o
       o.max_iter = opt->max_iter;
       o.device = opt->device;
       o.host_only = opt->host_only != 0;
+      o.preconditioner = opt->preconditioner;
     }
     h->sim = new Sim(config_path ? config_path : "", o);
     return TG_OK;
@@ -105,7 +107,7 @@ int tg_sim_info(tg_sim* s, long* out) {
     const auto n = m.vol.basis_counts();
     const auto p = m.vol.degrees();
     const long v[] = {m.n_full, m.n_free, m.n_con, m.n_steps, static_cast<long>(m.sources.size()),
-                      m.n_fe, n[0], n[1], n[2], p[0], p[1], p[2], m.kron ? (m.use_cg1 ? 2 : 1) : 0, m.nqb, m.nqf,
+                      m.n_fe, n[0], n[1], n[2], p[0], p[1], p[2], m.kron ? (m.use_fdm ? 3 : (m.use_cg1 ? 2 : 1)) : 0, m.nqb, m.nqf,
                       m.ndk, m.h_qb_off.back(), m.h_qf_off.back()};
     std::memcpy(out, v, sizeof(v));
   }, false);
@@ -281,6 +283,20 @@ int tg_sim_operator_apply(tg_sim* s, const double* x_free, double* y_free) {
     d2h(y_free, m.d_Ap.p, m.n_free, st);
     TG_CUDA(cudaStreamSynchronize(st));
   });
+}
+
+int tg_fdm_factor(const double* Mband, const double* Kband, int n_band, int p, int first, int n,
+                  double* V, double* lam) {
+  try {
+    const size_t nb = static_cast<size_t>(n_band) * (2 * p + 1);
+    const Fdm1D f = fdm_factor(std::vector<double>(Mband, Mband + nb),
+                               std::vector<double>(Kband, Kband + nb), n_band, p, first, n);
+    std::memcpy(V, f.V.data(), sizeof(double) * f.V.size());
+    std::memcpy(lam, f.lam.data(), sizeof(double) * f.lam.size());
+    return TG_OK;
+  } catch (const std::exception&) {
+    return TG_ERROR;
+  }
 }
 
 int tg_sim_probe(tg_sim* s, const double* xi, long n, double* out) {

@@ -194,3 +194,29 @@ def test_sharding_entry_points_single_gpu():
         parts.append(apply(k0, k1, xt[g0 * plane:g1 * plane].contiguous()))
     assert np.array_equal(torch.cat(parts).cpu().numpy(), y)
     s.close()
+
+
+@pytest.mark.parametrize("name", ["cfg0_parity", "cfg0_oddx"])
+def test_fdm_preconditioner_time_loop(name):
+    """The fast-diagonalization preconditioner (opt-in): the
+    same run_time_loop within the correction-field tolerance of the
+    reference's Jacobi-PCG solution, in 1-2 CG iterations per step, with
+    bitwise-deterministic reruns."""
+    g = golden(name)
+    s = tg.Simulation(cfg(name), preconditioner="fdm")
+    assert s.info["kronecker"] == 3
+    s.reset()
+    done = 0
+    for k in g["steps"]:
+        it, rel = s.advance(int(k) - done)
+        assert it <= 2 * (int(k) - done), (k, it)
+        done = int(k)
+        st = s.state()
+        assert normwise(st["free"], g[f"x{k}"]) <= 1e-8, k
+    a = s.state()["free"]
+    s.reset()
+    s.advance(done)
+    assert np.array_equal(s.state()["free"], a)
+    with pytest.raises(tg.NumericError, match=r"pcg: no convergence in 1 iterations"):
+        s.theta_step(g["x1"], g["g1"], g["F1"], g["F2"], g["g2"], tol=1e-30, max_iter=1)
+    s.close()

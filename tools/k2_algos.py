@@ -11,9 +11,9 @@ import paper_2511_20432_b200 as tg  # noqa: E402
 
 cfg = sys.argv[1] if len(sys.argv) > 1 else os.path.join(ROOT, "configs", "cfg4_large.cfg")
 steps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
-for algo in os.environ.get("TG_K2_ALGOS", "cg1,pcg").split(","):
-    os.environ["TG_K2_ALGO"] = algo
-    sim = tg.Simulation(cfg)
+for algo in os.environ.get("TG_K2_ALGOS", "cg1,pcg,fdm").split(","):
+    os.environ["TG_K2_ALGO"] = "pcg" if algo == "pcg" else "cg1"
+    sim = tg.Simulation(cfg, preconditioner="fdm" if algo == "fdm" else "jacobi")
     sim.reset()
     sim.advance(1)
     ctx = sim.context()
