@@ -259,7 +259,34 @@ def theta_section(steps, warmup, with_cpu):
         except Exception as e:
             out["cpu_baseline"] = {"error": str(e)}
     sim.close()
+    try:
+        out["fdm_option"] = theta_fdm(steps, warmup)
+    except Exception as e:  # reported, not fatal
+        out["fdm_option"] = {"error": str(e)}
     return out
+
+
+def theta_fdm(steps, warmup):
+    """The opt-in fast-diagonalization preconditioner on the
+    same config-4 steps: θ-step solve time and CG iterations."""
+    import paper_2511_20432_b200 as tg
+    sim = tg.Simulation(THETA_CFG, preconditioner="fdm")
+    ctx = sim.context()
+    sim.reset()
+    if warmup:
+        sim.advance(warmup)
+    ctx.set_profiling(True)
+    ctx.profile(reset=True)
+    iters, rel = sim.advance(steps)
+    prof = ctx.profile()
+    ctx.set_profiling(False)
+    dofs = sim.info["n_full"]
+    k2_ms = prof["k2_ms"] / steps
+    sim.close()
+    return {"preconditioner": "fast diagonalization (V diag(1/(a + b(lx+ly+lz))) V^T, "
+                              "cuBLAS DGEMM mode products), same PCG stop test",
+            "theta_ms_per_step": k2_ms, "theta_ms_per_step_per_mdof": k2_ms / (dofs / 1e6),
+            "cg_iterations_per_step": iters / steps, "last_rel_residual": rel}
 
 
 def run_reference(args):

@@ -174,7 +174,8 @@ void fdm_apply(cublasHandle_t h, const FdmDev& F, const double* r, double* z, do
 
 PcgStatus fdm_pcg_solve(cublasHandle_t h, const KronGrid& g, double a, double b, const FdmDev& F,
                         const double* rhs, double* x, const FdmWork& w, double tol, int max_iter,
-                        int sm_count, cudaStream_t s) {
+                        int sm_count, cudaStream_t s, const TensorMap3* x_map,
+                        const TensorMap3* p_map) {
   const long n = static_cast<long>(g.n[0]) * g.n[1] * g.n[2];
   const int G = grid_for(n);
   double bb = 0.0, unused = 0.0;
@@ -187,7 +188,7 @@ PcgStatus fdm_pcg_solve(cublasHandle_t h, const KronGrid& g, double a, double b,
   // r = b - A x (sparse.cpp:61-69); the preconditioned residual z = P r is
   // formed lazily after the stop test (same iterates as the reference's
   // order, one preconditioner apply fewer on the converged iteration)
-  k2_apply(g, a, b, x, w.Ap, sm_count, s);
+  k2_apply(g, a, b, x, w.Ap, sm_count, s, x_map);
   residual_kernel<<<G, 256, 0, s>>>(n, rhs, w.Ap, w.r);
   double rr = 0.0, rz = 0.0, rz_old = 0.0;
   dot2(n, w.r, w.r, nullptr, nullptr, w, s, rr, unused);
@@ -203,7 +204,7 @@ PcgStatus fdm_pcg_solve(cublasHandle_t h, const KronGrid& g, double a, double b,
       direction_kernel<<<G, 256, 0, s>>>(n, rz / rz_old, w.z, w.p);  // p = z + beta p
     }
     rz_old = rz;
-    k2_apply(g, a, b, w.p, w.Ap, sm_count, s);
+    k2_apply(g, a, b, w.p, w.Ap, sm_count, s, p_map);
     double pAp = 0.0;
     dot2(n, w.p, w.Ap, nullptr, nullptr, w, s, pAp, unused);
     if (!(pAp > 0.0)) return PcgStatus{it, 4, rel, bnorm};

@@ -41,8 +41,10 @@ struct FdmWork {
   double* dots;      // device, 2
   double* h_dots;    // pinned host, 2
 };
+// x_map / p_map: TMA descriptors of x and w.p for the operator applies (or null)
 PcgStatus fdm_pcg_solve(cublasHandle_t h, const KronGrid& g, double a, double b, const FdmDev& F,
                         const double* rhs, double* x, const FdmWork& w, double tol, int max_iter,
-                        int sm_count, cudaStream_t s);
+                        int sm_count, cudaStream_t s, const TensorMap3* x_map = nullptr,
+                        const TensorMap3* p_map = nullptr);
 
 }  // namespace tgb

@@ -334,20 +334,26 @@ struct EpiStore {
   __device__ void operator()(size_t idx, int, int, int, double v, double) { y[idx] = v; }
 };
 
-template <int P>
+struct ApplyMap {
+  TensorMap3 v;
+};
+
+template <int P, bool TMA>
 __global__ void __launch_bounds__(kThreads) k2_apply_kernel(KronGrid g, KronTerms c,
                                                             const double* v, double* y,
-                                                            TileIdx T) {
+                                                            TileIdx T,
+                                                            const __grid_constant__ ApplyMap m) {
+  constexpr int PL = TMA ? kTmaPlanes : 1;
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  auto& sm = *reinterpret_cast<KSmem<P, 1, 1, 1>*>(smem_raw);
-  double* zb = reinterpret_cast<double*>(smem_raw + zband_offset<P, 1, 1, 1>());
-  init_smem(g, sm, zb, false);
+  auto& sm = *reinterpret_cast<KSmem<P, PL, 1, 1>*>(smem_raw);
+  double* zb = reinterpret_cast<double*>(smem_raw + zband_offset<P, PL, 1, 1>());
+  init_smem(g, sm, zb, TMA);
   EpiStore epi{y};
-  Inputs<1> in{{v}, {nullptr}};
+  Inputs<1> in{{v}, {&m.v}};
   int seq[1] = {0};
   NoPro np;
   for_segments(T, gridDim.x, blockIdx.x, [&](const Seg& sg) {
-    kron_tile<P, 1, 1, 1, false>(g, c, in, np, sg, sm, zb, seq, epi);
+    kron_tile<P, PL, 1, 1, TMA>(g, c, in, np, sg, sm, zb, seq, epi);
   });
 }
 
@@ -970,14 +976,23 @@ bool k2_make_map(const KronGrid& g, const double* base, TensorMap3* out, bool ha
   }
 
 void k2_apply(const KronGrid& g, double a, double b, const double* v, double* y, int sm_count,
-              cudaStream_t s) {
+              cudaStream_t s, const TensorMap3* v_map) {
   const TileIdx T = make_tiles(g);
   const int blocks = seg_blocks(T, 3 * sm_count);
+  ApplyMap m{};
+  if (v_map) m.v = *v_map;
   TG_KRON_DISPATCH(g.p, {
-    const size_t sb = smem_bytes<P, 1, 1, 1>(g.n[2]);
-    allow_smem(k2_apply_kernel<P>, sb);
-    k2_apply_kernel<P><<<blocks, dim3(kKronTX, kKronTY), sb, s>>>(g, KronTerms{a, b, 0.0, 0.0},
-                                                                  v, y, T);
+    if (v_map) {
+      const size_t sb = smem_bytes<P, kTmaPlanes, 1, 1>(g.n[2]);
+      allow_smem(k2_apply_kernel<P, true>, sb);
+      k2_apply_kernel<P, true><<<blocks, dim3(kKronTX, kKronTY), sb, s>>>(
+          g, KronTerms{a, b, 0.0, 0.0}, v, y, T, m);
+    } else {
+      const size_t sb = smem_bytes<P, 1, 1, 1>(g.n[2]);
+      allow_smem(k2_apply_kernel<P, false>, sb);
+      k2_apply_kernel<P, false><<<blocks, dim3(kKronTX, kKronTY), sb, s>>>(
+          g, KronTerms{a, b, 0.0, 0.0}, v, y, T, m);
+    }
   });
   TG_CUDA(cudaGetLastError());
 }

@@ -119,7 +119,8 @@ void k2_cg1_solve(const KronGrid& g, double a, double b, const double* rhs, doub
                   const Cg1Work& w, const Cg1Maps& maps, double tol, int max_iter, int blocks,
                   cudaStream_t s);
 // plain y = Op(a, b) v (tests / the operator alone)
+// v_map: TMA descriptor of v (k2_make_map) or null for plain loads
 void k2_apply(const KronGrid& g, double a, double b, const double* v, double* y, int sm_count,
-              cudaStream_t s);
+              cudaStream_t s, const TensorMap3* v_map = nullptr);
 
 }  // namespace tgb

@@ -498,7 +498,8 @@ PcgStatus Sim::theta_step_device(double tol, int max_iter) {
       const FdmWork w{d_r.p, d_z.p, d_p.p, d_Ap.p, d_p2.p, d_w2.p, d_partials.p, d_dots.p, h_dots};
       ctx->timer.timed(2, s, [&] {
         *h_status = fdm_pcg_solve(cublas, gfree, coefA[0], coefA[1], fdm, d_rhs.p, d_x.p, w, tol,
-                                  max_iter, ctx->sm_count, s);
+                                  max_iter, ctx->sm_count, s, maps.valid ? &maps.x : nullptr,
+                                  maps.valid ? &maps.pA : nullptr);
       });
       TG_CUDA(cudaMemcpyAsync(d_status.p, h_status, sizeof(PcgStatus), cudaMemcpyHostToDevice, s));
     } else if (use_cg1) {
