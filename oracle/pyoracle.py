@@ -94,6 +94,8 @@ class RefLib:
         L.ref_sim_export_field.argtypes = [C.c_void_p, _dp, _ip, C.c_double, C.c_char_p,
                                            C.c_char_p, C.c_int]
         L.ref_export_profile_csv.argtypes = [_dp, C.c_int, C.c_char_p, C.c_char_p, C.c_int]
+        L.ref_sim_face_point.argtypes = [C.c_void_p, C.c_int, C.c_double, C.c_double, _dp]
+        L.ref_sim_face_points.argtypes = [C.c_void_p, C.c_int, C.c_int, _dp, _dp]
 
     # -- analytic ---------------------------------------------------------
     def discretize_scan(self, waypoints, *, start_time=0.0, plane_z=0.0, power, speed,
@@ -282,6 +284,19 @@ class RefSim:
         x = np.ascontiguousarray(xi, dtype=np.float64)
         self.L.ref_sim_field_at(self.h, _ptr(f), _ptr(x), _ptr(out))
         return out[0], out[1:]
+
+    def face_point(self, face, u, v):
+        """face_point: (x (3), normal (3), area scale)."""
+        out = np.zeros(7)
+        self.L.ref_sim_face_point(self.h, int(face), u, v, _ptr(out))
+        return out[:3], out[3:6], out[6]
+
+    def face_points(self, face, uv):
+        """face_point at many (u, v): (n x 7) = x, normal, area scale."""
+        p = np.ascontiguousarray(uv, dtype=np.float64).reshape(-1, 2)
+        out = np.zeros((len(p), 7))
+        self.L.ref_sim_face_points(self.h, int(face), len(p), _ptr(p), _ptr(out))
+        return out
 
     def map_point(self, xi):
         out = np.zeros(3)

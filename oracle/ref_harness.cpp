@@ -511,6 +511,22 @@ int ref_export_profile_csv(const double* rows, int n, const char* path, char* er
   }
 }
 
+// face_point (proj/src/splines.cpp:305-321): out = x (3), normal (3), area scale.
+int ref_sim_face_point(void* h, int face, double u, double v, double* out) {
+  const Simulation& s = static_cast<RefSim*>(h)->sim;
+  const auto sp = s.volume().face_point(static_cast<FaceId>(face), u, v);
+  const double o[7] = {sp.x.x, sp.x.y, sp.x.z, sp.normal.x, sp.normal.y, sp.normal.z,
+                       sp.area_scale};
+  std::memcpy(out, o, sizeof(o));
+  return 0;
+}
+
+// face_point at n (u, v) pairs: out (n x 7).
+int ref_sim_face_points(void* h, int face, int n, const double* uv, double* out) {
+  for (int i = 0; i < n; ++i) ref_sim_face_point(h, face, uv[2 * i], uv[2 * i + 1], out + 7 * i);
+  return 0;
+}
+
 // map_point (proj/src/splines.cpp:257-278).
 int ref_sim_map_point(void* h, const double* xi, double* x) {
   const Simulation& s = static_cast<RefSim*>(h)->sim;
