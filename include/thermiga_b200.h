@@ -188,6 +188,20 @@ int tg_sim_advance(tg_sim* sim, int n_steps, long* cg_iterations, double* last_r
 int tg_sim_state(tg_sim* sim, int* step, double* time, double* free_out, double* g_out,
                  double* F_out);
 
+/* ---- sparse LA on a caller matrix (proj/include/thermiga/sparse.hpp) ------
+ * CSR: rows x rows, 0-based row_ptr (rows + 1) / col / val, host arrays.
+ * tg_pcg_jacobi = pcg_jacobi (sparse.cpp:41-100) on this context's GPU: x
+ * holds the warm start and receives the solution; the reference's options
+ * default to tol = 1e-10, max_iter = 5000 (sparse.hpp:32-35). TG_ENUMERIC with
+ * the reference's messages on a non-positive diagonal, an indefinite
+ * direction, or the iteration cap (iterations / rel_residual still set).
+ * tg_csr_multiply = CsrMatrix::multiply (sparse.cpp:25-31). */
+int tg_pcg_jacobi(tg_ctx* ctx, int rows, const int* row_ptr, const int* col, const double* val,
+                  const double* b, double* x, double tol, int max_iter, int* iterations,
+                  double* rel_residual);
+int tg_csr_multiply(tg_ctx* ctx, int rows, const int* row_ptr, const int* col, const double* val,
+                    const double* x, double* y);
+
 /* Host helper behind the fast-diagonalization preconditioner (exposed for
  * tests): K_d V = M_d V diag(lam), V^T M_d V = I for rows/cols
  * [first, first + n) of banded 1D factors (n_band x (2p+1), [i][p + j - i]).

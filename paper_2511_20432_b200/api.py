@@ -130,6 +130,9 @@ def lib(auto_build: bool = True):
     L.tg_set_profiling.argtypes = [C.c_void_p, C.c_int]
     L.tg_profile_read.argtypes = [C.c_void_p, _dp, C.c_int]
     L.tg_fp64_peak.argtypes = [C.c_void_p, _dp]
+    L.tg_pcg_jacobi.argtypes = [C.c_void_p, C.c_int, _ip, _ip, _dp, _dp, _dp, C.c_double, C.c_int,
+                                _ip, _dp]
+    L.tg_csr_multiply.argtypes = [C.c_void_p, C.c_int, _ip, _ip, _dp, _dp, _dp]
     L.tg_discretize_scan.argtypes = [_dp, C.c_int, C.c_double, C.c_double,
                                      C.POINTER(_Laser), C.POINTER(_Material), _dp, C.c_int]
     L.tg_set_sources.argtypes = [C.c_void_p, _dp, C.c_int, C.POINTER(_Material)]
@@ -204,6 +207,54 @@ class Context:
         self._check(self._L.tg_profile_read(self._h, _p(out), int(reset)))
         return dict(k1_ms=out[0], k1_launches=int(out[1]), k1_pairs=out[2], k2_ms=out[3],
                     k2_launches=int(out[4]), k2_bytes=out[5], launches=int(out[6]))
+
+    @staticmethod
+    def _csr(A):
+        """(row_ptr, col, val) int32/int32/float64 from a scipy sparse matrix,
+        a dense array or a (row_ptr, col, val) tuple."""
+        if isinstance(A, tuple):
+            rp, ci, v = A
+        elif hasattr(A, "tocsr"):
+            M = A.tocsr()
+            M.sort_indices()
+            rp, ci, v = M.indptr, M.indices, M.data
+        else:
+            D = np.asarray(A, dtype=np.float64)
+            rp, ci, v = [0], [], []
+            for row in D:
+                nz = np.nonzero(row)[0]
+                ci += nz.tolist()
+                v += row[nz].tolist()
+                rp.append(len(ci))
+        return (np.ascontiguousarray(rp, dtype=np.int32), np.ascontiguousarray(ci, dtype=np.int32),
+                _f64(v))
+
+    def pcg_jacobi(self, A, b, x=None, tol: float = 1e-10, max_iter: int = 5000):
+        """pcg_jacobi (proj/include/thermiga/sparse.hpp:45-46) on this GPU:
+        returns (x, iterations, rel_residual); NumericError with the
+        reference's message on the cap or a non-SPD matrix."""
+        rp, ci, v = self._csr(A)
+        n = len(rp) - 1
+        bb = _f64(b)
+        xx = np.zeros(n) if x is None else _f64(x).copy()
+        it = C.c_int(0)
+        rel = C.c_double(0.0)
+        ip = C.POINTER(C.c_int)
+        self._check(self._L.tg_pcg_jacobi(self._h, n, rp.ctypes.data_as(ip), ci.ctypes.data_as(ip),
+                                          _p(v), _p(bb), _p(xx), float(tol), int(max_iter),
+                                          C.byref(it), C.byref(rel)))
+        return xx, it.value, rel.value
+
+    def csr_multiply(self, A, x):
+        """CsrMatrix::multiply (sparse.cpp:25-31) on this GPU."""
+        rp, ci, v = self._csr(A)
+        n = len(rp) - 1
+        xx = _f64(x)
+        y = np.zeros(n)
+        ip = C.POINTER(C.c_int)
+        self._check(self._L.tg_csr_multiply(self._h, n, rp.ctypes.data_as(ip),
+                                            ci.ctypes.data_as(ip), _p(v), _p(xx), _p(y)))
+        return y
 
     def fp64_peak_tflops(self) -> float:
         out = C.c_double(0.0)
