@@ -648,7 +648,10 @@ __global__ void __launch_bounds__(kThreads, 2)
 // buffers; x and p are point-local and update in place. HBM traffic: 6 reads
 // + 5 writes = 88 B per DOF per iteration, one grid barrier.
 
-constexpr int kCg1Stages = 2;  // ring depth: 4 inputs x 2 stages keeps 2 CTAs/SM
+#ifndef K2_CG1_STAGES
+#define K2_CG1_STAGES 2
+#endif
+constexpr int kCg1Stages = K2_CG1_STAGES;  // 2 keeps 2 CTAs/SM: 93.0 us/iter; 3 or 4 (1 CTA/SM): 134-136
 
 template <int P, int PL>
 struct ProScale {  // init: v = D^-1 r0 (ring 0: r0, ring 1: D^-1); gamma0 on own points

@@ -39,7 +39,7 @@ def build():
         d = [f"-D{k}={v}" for k, v in defs.items()]
         subprocess.run([B.NVCC, *B.ARCH, *B.COMMON, *d, "-c", k1, "-o", obj], check=True)
         subprocess.run([B.NVCC, *B.ARCH, "-shared", "-cudart", "static", "-o",
-                        os.path.join(VDIR, f"{name}.so"), obj, *others], check=True)
+                        os.path.join(VDIR, f"{name}.so"), obj, *others, *B.LINK], check=True)
         print("built", name)
 
 

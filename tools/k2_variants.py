@@ -15,10 +15,9 @@ sys.path.insert(0, ROOT)
 VDIR = os.path.join(ROOT, "paper_2511_20432_b200", "_lib", "variants_k2")
 
 VARIANTS = {
-    "l2a0": dict(K2_L2_AHEAD=0),
-    "l2a1": dict(K2_L2_AHEAD=1),
-    "l2a2": dict(K2_L2_AHEAD=2),
-    "l2a4": dict(K2_L2_AHEAD=4),
+    "st2": dict(K2_CG1_STAGES=2),
+    "st3": dict(K2_CG1_STAGES=3),
+    "st4": dict(K2_CG1_STAGES=4),
 }
 
 
@@ -33,7 +32,7 @@ def build():
         d = [f"-D{k}={v}" for k, v in defs.items()]
         subprocess.run([B.NVCC, *B.ARCH, *B.COMMON, *d, "-c", src, "-o", obj], check=True)
         subprocess.run([B.NVCC, *B.ARCH, "-shared", "-cudart", "static", "-o",
-                        os.path.join(VDIR, f"{name}.so"), obj, *others], check=True)
+                        os.path.join(VDIR, f"{name}.so"), obj, *others, *B.LINK], check=True)
         print("built", name)
 
 
