@@ -207,6 +207,53 @@ def theta_cpu_baseline():
             "sample": f"one theta_step of config 2 ({dofs} DOF) at t = 0.02 s, cold start"}
 
 
+def config2_run(with_cpu):
+    """End to end: config 2's whole run_time_loop (2000 θ-steps, 64x64x16
+    degree-2 cuboid, one raster layer) on the device, against one reference
+    step at mid-run (flux load on all host cores + Dirichlet values + θ-step)."""
+    import paper_2511_20432_b200 as tg
+    sim = tg.Simulation(THETA_CPU_CFG)
+    n = sim.info["n_steps"]
+    sim.reset()
+    sim.advance(5)  # warm-up (module load, first launches)
+    sim.reset()
+    t0 = time.perf_counter()
+    iters, rel = sim.advance(n)
+    wall = time.perf_counter() - t0
+    out = {"workload": "config2: 64x64x16 degree-2 cuboid (78,408 DOF), one-layer raster "
+                       f"({sim.info['n_sources']} sources), {n} theta steps, solver_tol "
+                       f"{sim.params['solver_tol']:g}",
+           "steps": n, "run_s": wall, "ms_per_step": wall * 1e3 / n,
+           "cg_iterations_per_step": iters / n, "timing": "wall clock around the "
+           "synchronous tg_sim_advance(n) call (device-resident state)"}
+    sim.close()
+    if with_cpu:
+        from oracle import pyoracle
+        if pyoracle.ref_available():
+            R = pyoracle.RefLib()
+            rs = R.sim(THETA_CPU_CFG)
+            dt = rs.params["dt"]
+            k = n // 2
+            t1 = k * dt
+            x0 = np.zeros(rs.info["n_free"])
+            F0 = rs.flux_load(t1 - dt, threads=os.cpu_count())
+            g0 = rs.dirichlet(t1 - dt)
+            c0 = time.perf_counter()
+            F1 = rs.flux_load(t1, threads=os.cpu_count())
+            g1 = rs.dirichlet(t1)
+            rs.theta_step(x0, g0, F0, F1, g1, rs.params["solver_tol"])
+            secs = time.perf_counter() - c0
+            rs.close()
+            out["cpu_baseline"] = {"ms_per_step": secs * 1e3, "kind": "reference",
+                                   "cores": os.cpu_count(),
+                                   "sample": f"one step at step {k} (t = {t1:g} s): "
+                                             "assemble_flux_load (threaded), "
+                                             "dirichlet_values, theta_step (serial PCG, "
+                                             "cold start)",
+                                   "run_s_estimate": secs * n}
+    return out
+
+
 def theta_section(steps, warmup, with_cpu):
     """Config 4 (4.39M DOF, 1e5 sources): full run_time_loop steps on the device."""
     import paper_2511_20432_b200 as tg
@@ -263,6 +310,10 @@ def theta_section(steps, warmup, with_cpu):
         out["fdm_option"] = theta_fdm(steps, warmup)
     except Exception as e:  # reported, not fatal
         out["fdm_option"] = {"error": str(e)}
+    try:
+        out["config2_run"] = config2_run(with_cpu)
+    except Exception as e:  # reported, not fatal
+        out["config2_run"] = {"error": str(e)}
     return out
 
 
