@@ -939,9 +939,12 @@ void allow_smem(K kernel, size_t bytes) {
 
 // CTAs for a sweep: at most `max_blocks`, and >= ~6 planes per CTA (small
 // grids are latency-bound: more CTAs beat the 2P halo-plane overhead).
+#ifndef K2_MIN_PLANES
+#define K2_MIN_PLANES 3  // config 2 per CG iteration: 2 -> 16.6 us, 3 -> 15.5, 4 -> 16.2, 6 -> 17.4
+#endif
 int seg_blocks(const TileIdx& T, int max_blocks) {
   const long total = static_cast<long>(T.ntx) * T.nty * T.nz;
-  return static_cast<int>(std::max(1L, std::min<long>(max_blocks, total / 6)));
+  return static_cast<int>(std::max(1L, std::min<long>(max_blocks, total / K2_MIN_PLANES)));
 }
 
 }  // namespace

@@ -15,9 +15,10 @@ sys.path.insert(0, ROOT)
 VDIR = os.path.join(ROOT, "paper_2511_20432_b200", "_lib", "variants_k2")
 
 VARIANTS = {
-    "st2": dict(K2_CG1_STAGES=2),
-    "st3": dict(K2_CG1_STAGES=3),
-    "st4": dict(K2_CG1_STAGES=4),
+    "mp2": dict(K2_MIN_PLANES=2),
+    "mp3": dict(K2_MIN_PLANES=3),
+    "mp4": dict(K2_MIN_PLANES=4),
+    "mp6": dict(K2_MIN_PLANES=6),
 }
 
 
@@ -39,7 +40,8 @@ def build():
 def run():
     for so in sorted(glob.glob(os.path.join(VDIR, "*.so"))):
         env = dict(os.environ, TG_LIB_VARIANT=so, TG_K2_ALGOS="cg1")
-        r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "k2_algos.py")],
+        r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "k2_algos.py"),
+                            *sys.argv[2:]],
                            env=env, capture_output=True, text=True)
         for line in (r.stdout.strip() or r.stderr[-1500:]).splitlines():
             print(os.path.basename(so)[:-3], line, flush=True)
