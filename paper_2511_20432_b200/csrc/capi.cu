@@ -55,6 +55,8 @@ void k1_run(tg_ctx* ctx, const double* d_src6, int n_src, const double* d_pts,
   const double rcp = m.volumetric_capacity();
   const bool grad = mode != K1Mode::dirichlet;
   const int P = ctx->k1_points_per_thread;
+  if (d_src6 == ctx->src6.p && static_cast<int>(ctx->tau_sufmin.size()) == n_src)
+    n_src = ctx->active_prefix(t);  // trailing inactive sources contribute exact zeros
   int S = 1;
   if (n_src > 0) {
     k1_prepare(d_src6, n_src, t, alpha, rcp, cull, ctx->rec.ensure(n_src), stream);
@@ -194,6 +196,7 @@ int tg_set_sources(tg_ctx* ctx, const tg_point_source* src, int n, const tg_mate
     TG_CUDA(cudaSetDevice(ctx->device));
     ctx->mat = m;
     ctx->n_src = n;
+    ctx->set_tau(reinterpret_cast<const double*>(src), n);
     double* d = ctx->src6.ensure(static_cast<size_t>(n) * 6);
     if (n > 0)
       TG_CUDA(cudaMemcpyAsync(d, src, sizeof(tg_point_source) * n, cudaMemcpyHostToDevice,

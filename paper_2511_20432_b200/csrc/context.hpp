@@ -4,6 +4,8 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
+#include <cmath>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -126,6 +128,19 @@ struct tg_ctx {
   // K1 state
   tgb::Material mat;
   int n_src = 0;
+  // suffix minima of the sources' modified times tau: sources [j, n) are all
+  // causally inactive at t (t - tau <= 0) iff tau_sufmin[j] >= t, so K1 runs
+  // over the active prefix only (the skipped pairs are exact zeros)
+  std::vector<double> tau_sufmin;
+  int active_prefix(double t) const {
+    const auto it = std::lower_bound(tau_sufmin.begin(), tau_sufmin.end(), t);
+    return static_cast<int>(it - tau_sufmin.begin());
+  }
+  void set_tau(const double* src6_host, int n) {
+    tau_sufmin.assign(n, 0.0);
+    double m = INFINITY;
+    for (int j = n - 1; j >= 0; --j) tau_sufmin[j] = m = std::min(m, src6_host[6 * j + 5]);
+  }
   tgb::DevBuf<double> src6;
   tgb::DevBuf<tgb::SrcRec> rec;
   tgb::DevBuf<double> part;

@@ -259,6 +259,8 @@ void Sim::setup_device(int device, int preconditioner) {
   cudaStream_t s = ctx->stream;
   ctx->mat = cfg.material;
   ctx->n_src = static_cast<int>(sources.size());
+  static_assert(sizeof(PointSource) == 6 * sizeof(double), "PointSource layout");
+  ctx->set_tau(reinterpret_cast<const double*>(sources.data()), ctx->n_src);
   double* d = ctx->src6.ensure(6 * sources.size());
   if (!sources.empty())
     TG_CUDA(cudaMemcpyAsync(d, sources.data(), sources.size() * sizeof(PointSource),
