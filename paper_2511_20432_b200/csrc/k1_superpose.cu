@@ -298,13 +298,13 @@ void k1_upload_exp_table(cudaStream_t stream) {
   cudaMemcpyToSymbolAsync(c_exp_table, tab, sizeof(tab), 0, cudaMemcpyHostToDevice, stream);
 }
 
-int k1_choose_splits(int n_pts, int n_src, int sm_count, int points_per_cta) {
-  const int tiles = (n_pts + points_per_cta - 1) / points_per_cta;
-  const long target = static_cast<long>(sm_count) * 3 * 16;  // ~16 waves of 3 CTAs/SM
-  int S = static_cast<int>((target + tiles - 1) / tiles);
-  const int max_s = std::max(1, n_src / 256);  // keep >= 256 sources per split
-  S = std::max(1, std::min(S, max_s));
-  return S;
+// The source splits depend on the source count only — never on the points —
+// so every point's sum has the same association whichever subset of points a
+// launch (or a shard of a multi-GPU run) evaluates: sharded loads reproduce
+// the single-launch result bit for bit. >= 128 sources per split, <= 16 splits
+// (enough CTAs for small point sets, few partial planes for large ones).
+int k1_choose_splits(int, int n_src, int, int) {
+  return std::max(1, std::min(16, n_src / 128));
 }
 
 void k1_prepare(const double* d_src6, int n, double t, double alpha, double rcp, double cull,
