@@ -2,7 +2,7 @@
  * thermal solver (reference: "thermiga", /root/reference/proj).
  *
  * The reference has no FFI of its own: its boundary for this path is the C++
- * API in proj/include/thermiga/*.hpp, called by run_time_loop
+ * API in the headers under proj/include/thermiga/, called by run_time_loop
  * (proj/src/driver.cpp:105-146). Each entry point below replaces one of those
  * calls; the citation says which. The C++ shim include/thermiga_b200.hpp
  * re-exposes them with the reference's signatures.

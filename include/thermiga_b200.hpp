@@ -5,7 +5,9 @@
 // reference's exception types (proj/include/thermiga/core.hpp:66-80).
 #pragma once
 
+#include <algorithm>
 #include <array>
+#include <cmath>
 #include <functional>
 #include <memory>
 #include <stdexcept>
@@ -32,6 +34,12 @@ struct numeric_error : std::runtime_error {
 struct device_error : std::runtime_error {
   using std::runtime_error::runtime_error;
 };
+
+// rc first, then the context's message (read only after the call returned)
+inline void raise(int rc, const char* msg);
+inline void check_ctx(int rc, tg_ctx* c) {
+  if (rc != TG_OK) raise(rc, tg_last_error(c));
+}
 
 inline void raise(int rc, const char* msg) {
   switch (rc) {
@@ -86,15 +94,15 @@ class Device {
   }
   tg_ctx* get() const { return ctx_.get(); }
   void set_sources(const std::vector<PointSource>& s, const Material& m) {
-    raise(tg_set_sources(get(), s.data(), static_cast<int>(s.size()), &m), tg_last_error(get()));
+    check_ctx(tg_set_sources(get(), s.data(), static_cast<int>(s.size()), &m), get());
   }
   // superpose (analytic.hpp:73-75) at many points: values and gradients
   void superpose(const std::vector<Vec3>& x, double t, std::vector<AnalyticField>& out,
                  const SuperposeOptions& opts = {}) {
     std::vector<double> v(x.size()), g(3 * x.size());
-    raise(tg_superpose_batch(get(), &x[0].x, static_cast<long>(x.size()), t, opts.cull_exponent,
-                             v.data(), g.data()),
-          tg_last_error(get()));
+    check_ctx(tg_superpose_batch(get(), &x[0].x, static_cast<long>(x.size()), t,
+                                 opts.cull_exponent, v.data(), g.data()),
+              get());
     out.resize(x.size());
     for (size_t i = 0; i < x.size(); ++i) out[i] = {v[i], {g[3 * i], g[3 * i + 1], g[3 * i + 2]}};
   }
@@ -125,6 +133,73 @@ struct PcgResult {  // sparse.hpp:37-40
   int iterations = 0;
   double rel_residual = 0.0;
 };
+
+namespace detail {
+inline Device& thread_device() {
+  thread_local Device dev;
+  return dev;
+}
+}  // namespace detail
+
+// CsrMatrix (sparse.hpp:14-30): same fields; multiply runs on the GPU.
+struct CsrMatrix {
+  int rows = 0, cols = 0;
+  std::vector<int> row_ptr, col_idx;
+  std::vector<double> vals;
+  void multiply(const std::vector<double>& x, std::vector<double>& y) const {
+    if (static_cast<int>(x.size()) != cols) throw std::invalid_argument("spmv: size mismatch");
+    y.resize(rows);
+    Device& d = detail::thread_device();
+    check_ctx(tg_csr_multiply(d.get(), rows, row_ptr.data(), col_idx.data(), vals.data(),
+                              x.data(), y.data()),
+              d.get());
+  }
+};
+
+// pcg_jacobi (sparse.hpp:45-46) on the GPU: x is the warm start and the result.
+inline PcgResult pcg_jacobi(const CsrMatrix& A, const std::vector<double>& b,
+                            std::vector<double>& x, const PcgOptions& opts = {}) {
+  if (A.cols != A.rows || static_cast<int>(b.size()) != A.rows ||
+      static_cast<int>(x.size()) != A.rows)
+    throw std::invalid_argument("pcg: dimension mismatch");
+  Device& d = detail::thread_device();
+  PcgResult r;
+  check_ctx(tg_pcg_jacobi(d.get(), A.rows, A.row_ptr.data(), A.col_idx.data(), A.vals.data(),
+                          b.data(), x.data(), opts.tol, opts.max_iter, &r.iterations,
+                          &r.rel_residual),
+            d.get());
+  return r;
+}
+
+// postproc.hpp:17-44
+struct FluxProfile {
+  struct Sample {
+    double s, theta, q_tilde, q_hat, q_net;
+  };
+  std::vector<Sample> samples;
+};
+struct FluxMetrics {
+  double integral_net = 0.0, integral_analytic = 0.0;
+  bool has_ratio = false;
+  double ratio = 0.0;
+};
+// integrated_abs_flux (postproc.cpp:81-95)
+inline FluxMetrics integrated_abs_flux(const FluxProfile& p) {
+  if (p.samples.size() < 2) throw std::invalid_argument("flux metrics need >= 2 samples");
+  FluxMetrics m;
+  for (size_t i = 1; i < p.samples.size(); ++i) {
+    const auto& a = p.samples[i - 1];
+    const auto& b = p.samples[i];
+    const double ds = b.s - a.s;
+    m.integral_net += 0.5 * ds * (std::abs(a.q_net) + std::abs(b.q_net));
+    m.integral_analytic += 0.5 * ds * (std::abs(a.q_tilde) + std::abs(b.q_tilde));
+  }
+  if (m.integral_analytic > 0.0) {
+    m.has_ratio = true;
+    m.ratio = m.integral_net / m.integral_analytic;
+  }
+  return m;
+}
 struct State {  // timestep.hpp:16-21
   std::vector<double> free_coeffs;
   std::vector<double> constrained_values;
@@ -198,6 +273,25 @@ class Simulation {
       on_state(st);
     }
     return total;
+  }
+
+  // observers on the current device state (postproc.cpp:9-79):
+  // total_temperature at parametric points, boundary_flux_profile of a face
+  std::vector<double> total_temperature(const std::vector<Vec3>& xi) {
+    std::vector<double> out(12 * xi.size()), T(xi.size());
+    if (!xi.empty()) check(tg_sim_probe(get(), &xi[0].x, static_cast<long>(xi.size()), out.data()));
+    for (size_t i = 0; i < xi.size(); ++i) T[i] = out[12 * i + 3];
+    return T;
+  }
+  FluxProfile boundary_flux_profile(int face, int n_samples, const double* theta_axis = nullptr,
+                                    double edge_v = 1.0) {
+    std::vector<double> rows(5 * static_cast<size_t>(std::max(0, n_samples)));
+    check(tg_sim_flux_profile(get(), face, n_samples, edge_v, theta_axis, rows.data()));
+    FluxProfile p;
+    for (int i = 0; i < n_samples; ++i)
+      p.samples.push_back({rows[5 * i], rows[5 * i + 1], rows[5 * i + 2], rows[5 * i + 3],
+                           rows[5 * i + 4]});
+    return p;
   }
 
   long n_full = 0, n_free = 0, n_constrained = 0;

@@ -35,3 +35,16 @@ def test_shim_runs_time_loop(tmp_path):
                        capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stderr
     assert "steps 100" in r.stdout
+
+
+@pytest.mark.gpu
+def test_shim_sparse_and_observers(tmp_path):
+    exe = tmp_path / "sparse_and_observers"
+    cmd = ["g++", "-std=c++17", "-O2", "-I", os.path.join(ROOT, "include"),
+           os.path.join(ROOT, "examples", "sparse_and_observers.cpp"), "-L", _build.LIBDIR,
+           "-lthermiga_b200", f"-Wl,-rpath,{_build.LIBDIR}", "-o", str(exe)]
+    subprocess.run(cmd, check=True, capture_output=True)
+    r = subprocess.run([str(exe), os.path.join(ROOT, "configs", "cfg0_parity.cfg")],
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert r.stdout.count(" ok") == 3
