@@ -47,14 +47,14 @@ from paper_2511_20432_b200 import workloads as W  # noqa: E402
 
 FLOPS_PER_PAIR = 49.0  # value + gradient, exp counted at libdevice cost
 # FP64-pipe instructions per pair actually issued by k1_partial's fast path
-# (cuobjdump -sass of k1_partial<6,true>: 9 DFMA + 5 DADD + 3 DMUL; the
+# (cuobjdump -sass of k1_partial<7,true>: 9 DFMA + 5 DADD + 3 DMUL; the
 # exponential costs 6 of them with its argument where libdevice costs 18, so
 # the 49-flop accounting exceeds the DFMA peak — fp64_pipe reports the
 # issued-instruction fraction).
 PIPE_OPS_PER_PAIR = 17.0
 # DRAM bytes (read + write) per launch from one `ncu --set full` capture of each
 # dominant kernel (profiles/r01_k1_ncu_summary.md, r01_k2_ncu_summary.md)
-K1_TRAFFIC_BYTES = 75.5e6 + 317.0e6   # k1_partial<6,1>, config 1, one launch
+K1_TRAFFIC_BYTES = 90.9e6 + 486.6e6   # k1_partial<7,1>, config 1, one launch
 K2_TRAFFIC_B_PER_DOF_ITER = 88.0      # k2_cg1_kernel<2>, config 4 (15.62 + 12.56 GB / 74 sweeps)
 
 
@@ -464,12 +464,12 @@ def run_ours(args):
     k1_mean_ms = prof["k1_ms"] / max(1, prof["k1_launches"])
     pairs_per_launch = prof["k1_pairs"] / max(1, prof["k1_launches"])
     achieved = FLOPS_PER_PAIR * pairs_per_launch / (k1_mean_ms * 1e-3) / 1e12 if k1_mean_ms else None
-    roof = {"kernel": f"k1_partial<{os.environ.get('TG_K1_P', '6')},true>", "bound": "fp64",
+    roof = {"kernel": f"k1_partial<{os.environ.get('TG_K1_P', '7')},true>", "bound": "fp64",
             "achieved": achieved,
             "peak": fp64_peak, "unit": "TFLOP/s",
             "frac": (achieved / fp64_peak) if (achieved and fp64_peak) else None,
             "traffic": K1_TRAFFIC_BYTES,
-            "traffic_source": "ncu --set full, profiles/r01_k1_full_p6.ncu-rep (dram read+write)",
+            "traffic_source": "ncu --set full, profiles/r01_k1_full_p7.ncu-rep (dram read+write)",
             "peak_source": "measured live: tg_fp64_peak DFMA-chain microbenchmark on this GPU",
             "flops_per_pair": FLOPS_PER_PAIR, "pairs_per_launch": pairs_per_launch,
             "mean_launch_ms": k1_mean_ms,

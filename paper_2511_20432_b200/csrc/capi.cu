@@ -114,9 +114,9 @@ int tg_ctx_create(int device, tg_ctx** out) {
     ctx->device = device;
     ctx->sm_count = prop.multiProcessorCount;
     TG_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
-    if (const char* p = std::getenv("TG_K1_P")) {  // points per thread: 1, 2, 3, 4, 6, 8
+    if (const char* p = std::getenv("TG_K1_P")) {  // points per thread: 1..8
       const int v = std::atoi(p);
-      if (v == 1 || v == 2 || v == 3 || v == 4 || v == 6 || v == 8) ctx->k1_points_per_thread = v;
+      if (v >= 1 && v <= 8) ctx->k1_points_per_thread = v;
     }
     k1_upload_exp_table(ctx->stream);
     TG_CUDA(cudaStreamSynchronize(ctx->stream));

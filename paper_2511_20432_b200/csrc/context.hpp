@@ -145,8 +145,8 @@ struct tg_ctx {
   tgb::DevBuf<tgb::SrcRec> rec;
   tgb::DevBuf<double> part;
   tgb::DevBuf<double> pts, val, grad;
-  // measured (config 1, 17 FP64 ops/pair, unroll 4): P=6 83.6 ms, P=8 89.7, P=2 90.0, P=4 90.8
-  int k1_points_per_thread = 6;
+  // measured (config 1, 17 FP64 ops/pair, unroll 4): P=7 82.4 ms, P=6 83.9, P=8 89.7, P=5 94.6
+  int k1_points_per_thread = 7;
 
   // device-pointer entry points run on the caller's stream (NULL = legacy default)
   static cudaStream_t pick(void* s) { return static_cast<cudaStream_t>(s); }

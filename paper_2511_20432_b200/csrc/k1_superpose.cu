@@ -328,7 +328,9 @@ void k1_launch_partial(const SrcRec* d_rec, int n_src, const double* d_pts,
     case 1: if (grad) TG_K1_LAUNCH(1, true); else TG_K1_LAUNCH(1, false); break;
     case 2: if (grad) TG_K1_LAUNCH(2, true); else TG_K1_LAUNCH(2, false); break;
     case 3: if (grad) TG_K1_LAUNCH(3, true); else TG_K1_LAUNCH(3, false); break;
+    case 5: if (grad) TG_K1_LAUNCH(5, true); else TG_K1_LAUNCH(5, false); break;
     case 6: if (grad) TG_K1_LAUNCH(6, true); else TG_K1_LAUNCH(6, false); break;
+    case 7: if (grad) TG_K1_LAUNCH(7, true); else TG_K1_LAUNCH(7, false); break;
     case 8: if (grad) TG_K1_LAUNCH(8, true); else TG_K1_LAUNCH(8, false); break;
     default: if (grad) TG_K1_LAUNCH(4, true); else TG_K1_LAUNCH(4, false); break;
   }

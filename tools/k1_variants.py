@@ -18,13 +18,8 @@ sys.path.insert(0, ROOT)
 VDIR = os.path.join(ROOT, "paper_2511_20432_b200", "_lib", "variants")
 
 VARIANTS = {
-    "u3_late": dict(K1_UNROLL=3, K1_VOTE_LATE=1),
-    "u4_late": dict(K1_UNROLL=4, K1_VOTE_LATE=1),
-    "u4_early": dict(K1_UNROLL=4, K1_VOTE_LATE=0),
-    "u6_late": dict(K1_UNROLL=6, K1_VOTE_LATE=1),
-    "u8_late": dict(K1_UNROLL=8, K1_VOTE_LATE=1),
-    "u4_late_mb1": dict(K1_UNROLL=4, K1_VOTE_LATE=1, K1_MINB4=1),
-    "u8_late_mb1": dict(K1_UNROLL=8, K1_VOTE_LATE=1, K1_MINB4=1),
+    "u4": dict(K1_UNROLL=4),
+    "u6": dict(K1_UNROLL=6),
 }
 
 
