@@ -1029,8 +1029,6 @@ void k2_theta_rhs(const KronGrid& full, double a_b, double b_b, double a_a, doub
   TG_CUDA(cudaGetLastError());
 }
 
-void k2_plane_trace(unsigned long long*) {}  // plane-level stamps retired (see k2_trace.py)
-
 void k2_inverse_diagonal(const KronGrid& g, double a, double b, double* inv_diag,
                          PcgStatus* status, cudaStream_t s) {
   TG_KRON_DISPATCH(g.p, k2_inv_diag_kernel<P><<<512, 256, 0, s>>>(g, a, b, inv_diag, status));

@@ -103,9 +103,6 @@ void k2_theta_rhs(const KronGrid& full, double a_b, double b_b, double a_a, doub
 void k2_inverse_diagonal(const KronGrid& g, double a, double b, double* inv_diag,
                          PcgStatus* status, cudaStream_t s);
 int k2_pcg_max_blocks(int p, int sm_count, int nz);
-// Diagnostics: route CTA 0's plane-level stamps (64 planes x 5) to buf
-// (nullptr disables) and restart the plane counter.
-void k2_plane_trace(unsigned long long* buf);
 // Jacobi-PCG on A = Op(a, b) over the free grid, one persistent cooperative
 // launch per solve; x holds the warm start on entry.
 void k2_pcg_solve(const KronGrid& g, double a, double b, const double* rhs, double* x,

@@ -301,7 +301,6 @@ void Sim::setup_device(int device, int preconditioner) {
   trace_on = std::getenv("TG_K2_TRACE") != nullptr;
   if (trace_on) {
     TG_CUDA(cudaMemsetAsync(d_trace.p, 0, 400 * sizeof(unsigned long long), s));
-    k2_plane_trace(d_trace.p + 80);
   }
   TG_CUDA(cudaMemsetAsync(d_gfull.p, 0, sizeof(double) * n_full, s));
   TG_CUDA(cudaMemsetAsync(d_status.p, 0, sizeof(PcgStatus), s));
