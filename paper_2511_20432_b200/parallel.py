@@ -292,6 +292,18 @@ def gpu_apply_slab(sim):
     return apply
 
 
+def gpu_inverse_diagonal(sim):
+    """1 / diag(A_ff) of the simulation's operator as a CUDA tensor (the Jacobi
+    preconditioner of SlabPCG on this GPU)."""
+    import ctypes as C
+    import torch
+    L = sim._L
+    L.tg_sim_inverse_diagonal.argtypes = [C.c_void_p, C.POINTER(C.c_double)]
+    out = np.zeros(sim.info["n_free"])
+    sim._check(L.tg_sim_inverse_diagonal(sim._h, out.ctypes.data_as(C.POINTER(C.c_double))))
+    return torch.from_numpy(out).cuda()
+
+
 def init_from_env(backend: Optional[str] = None) -> Dist:
     """torchrun-style initialization (MASTER_ADDR/PORT, RANK, WORLD_SIZE)."""
     import torch

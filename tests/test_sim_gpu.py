@@ -220,3 +220,35 @@ def test_fdm_preconditioner_time_loop(name):
     with pytest.raises(tg.NumericError, match=r"pcg: no convergence in 1 iterations"):
         s.theta_step(g["x1"], g["g1"], g["F1"], g["F2"], g["g2"], tol=1e-30, max_iter=1)
     s.close()
+
+
+@pytest.mark.parametrize("single", [False, True], ids=["two-reductions", "single-reduction"])
+def test_slab_pcg_on_the_gpu_single_rank(single):
+    """parallel.SlabPCG driven by the device bindings (operator slabs, Jacobi
+    diagonal) on one rank over NCCL: the same solution as the device solver."""
+    import socket
+    import torch
+    import torch.distributed as dist
+    from paper_2511_20432_b200 import parallel
+    s = tg.Simulation(cfg("cfg0_parity"))
+    sock = socket.socket()
+    sock.bind(("127.0.0.1", 0))
+    port = sock.getsockname()[1]
+    sock.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1)
+    try:
+        d = parallel.Dist(0, 1, "cuda")
+        nz, plane = s.info["nz"] - 1, s.info["nx"] * s.info["ny"]
+        solver = parallel.SlabPCG(parallel.gpu_apply_slab(s), parallel.gpu_inverse_diagonal(s),
+                                  plane, nz, 2, d)
+        b = np.random.default_rng(21).standard_normal(s.info["n_free"])
+        x = torch.zeros(s.info["n_free"], dtype=torch.float64, device="cuda")
+        it, rel = solver.solve(torch.from_numpy(b).cuda(), x, 1e-12, 5000,
+                               single_reduction=single)
+        xs = x.cpu().numpy()
+        assert rel <= 1e-12
+        assert np.linalg.norm(s.operator_apply(xs) - b) <= 1e-11 * np.linalg.norm(b)
+    finally:
+        dist.destroy_process_group()
+        s.close()
