@@ -45,6 +45,9 @@ namespace tgb {
 namespace {
 
 constexpr int kThreads = kKronTX * kKronTY;
+#ifndef K2_MINB
+#define K2_MINB (kKronTY > 8 ? 1 : 2)  // resident CTAs per SM of the persistent solvers
+#endif
 constexpr int kStages = 3;
 constexpr int kTmaPlanes = 2;  // planes per TMA box / per sweep step
 #ifndef K2_L2_AHEAD
@@ -493,7 +496,7 @@ struct EpiDirection {  // p_new (own point), Ap, p.Ap
 };
 
 template <int P, bool TMA>
-__global__ void __launch_bounds__(kThreads, 2)
+__global__ void __launch_bounds__(kThreads, K2_MINB)
     k2_pcg_kernel(KronGrid g, double a, double b, const double* rhs, double* x, PcgWork w,
                   double tol, int max_iter, TileIdx T, const __grid_constant__ PcgMaps maps) {
   constexpr int PL = TMA ? kTmaPlanes : 1;
@@ -806,7 +809,7 @@ size_t cg1_smem_bytes(int nz) {
 }
 
 template <int P>
-__global__ void __launch_bounds__(kThreads, 2)
+__global__ void __launch_bounds__(kThreads, K2_MINB)
     k2_cg1_kernel(KronGrid g, double a, double b, const double* rhs, double* x, Cg1Work w,
                   double tol, int max_iter, TileIdx T, const __grid_constant__ Cg1Maps maps) {
   constexpr int PL = kTmaPlanes;

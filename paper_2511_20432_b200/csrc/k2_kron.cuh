@@ -7,7 +7,10 @@
 namespace tgb {
 
 constexpr int kKronTX = 32;  // tile width along xi (one warp)
-constexpr int kKronTY = 8;   // tile height along eta
+#ifndef K2_TY
+#define K2_TY 8
+#endif
+constexpr int kKronTY = K2_TY;  // tile height along eta; 16 (1 CTA/SM): 105 us/iter vs 93 (cfg 4)
 constexpr int kKronMaxP = 3;
 
 // A grid of control points (possibly the free sub-grid) with the banded 1D

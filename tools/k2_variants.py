@@ -15,10 +15,9 @@ sys.path.insert(0, ROOT)
 VDIR = os.path.join(ROOT, "paper_2511_20432_b200", "_lib", "variants_k2")
 
 VARIANTS = {
-    "mp2": dict(K2_MIN_PLANES=2),
-    "mp3": dict(K2_MIN_PLANES=3),
-    "mp4": dict(K2_MIN_PLANES=4),
-    "mp6": dict(K2_MIN_PLANES=6),
+    "ty8": dict(K2_TY=8),
+    "ty16": dict(K2_TY=16),
+    "ty16_st3": dict(K2_TY=16, K2_CG1_STAGES=3),
 }
 
 
