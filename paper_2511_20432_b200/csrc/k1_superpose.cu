@@ -248,13 +248,14 @@ __global__ void k1_combine_field(const double* __restrict__ part, int S, int n,
 }
 
 // Dirichlet values: out[i] = -T~ (mesh.cpp:261); partials are value-only.
+// (negate = false: plain values, the field without its gradient)
 __global__ void k1_combine_dirichlet(const double* __restrict__ part, int S, int n,
-                                     double* __restrict__ out) {
+                                     double* __restrict__ out, bool negate) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   double v = 0.0;
   for (int s = 0; s < S; ++s) v += part[static_cast<size_t>(s) * n + i];
-  out[i] = -v;
+  out[i] = negate ? -v : v;
 }
 
 // Flux integrand at face quadrature points (assembly.cpp:161-164, :135):
@@ -343,8 +344,8 @@ void k1_launch_combine_field(const double* d_part, int S, int n, double* d_val, 
 }
 
 void k1_launch_combine_dirichlet(const double* d_part, int S, int n, double* d_out,
-                                 cudaStream_t stream) {
-  k1_combine_dirichlet<<<(n + 255) / 256, 256, 0, stream>>>(d_part, S, n, d_out);
+                                 cudaStream_t stream, bool negate) {
+  k1_combine_dirichlet<<<(n + 255) / 256, 256, 0, stream>>>(d_part, S, n, d_out, negate);
 }
 
 void k1_launch_combine_flux(const double* d_part, int S, int n, const int* d_index,

@@ -33,7 +33,7 @@ void k1_launch_partial(const SrcRec* d_rec, int n_src, const double* d_pts, cons
 void k1_launch_combine_field(const double* d_part, int S, int n, double* d_val, double* d_grad,
                              cudaStream_t stream);
 void k1_launch_combine_dirichlet(const double* d_part, int S, int n, double* d_out,
-                                 cudaStream_t stream);
+                                 cudaStream_t stream, bool negate = true);
 void k1_launch_combine_flux(const double* d_part, int S, int n, const int* d_index,
                             const double* d_normals, const double* d_weights, double k,
                             double* d_gq, cudaStream_t stream);

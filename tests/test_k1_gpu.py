@@ -171,3 +171,14 @@ def test_device_path_matches_host_path(gpu_ctx, cfg1_sources):
     dv, dg = gpu_ctx.superpose(dp, t)
     torch.cuda.synchronize()
     assert np.array_equal(dv.cpu().numpy(), v) and np.array_equal(dg.cpu().numpy(), g)
+
+
+def test_value_only_launch_matches_value_of_gradient_launch(gpu_ctx, cfg1_sources):
+    """Without a gradient output the value-only kernel runs (13 instead of 17
+    FP64 ops per pair); the values are the same bits."""
+    src, t = cfg1_sources
+    gpu_ctx.set_sources(src, MAT)
+    pts = W.config1_points()[:50000]
+    v, g = gpu_ctx.superpose(pts, t)
+    v0, g0 = gpu_ctx.superpose(pts, t, grad=False)
+    assert g0 is None and np.array_equal(v0, v)

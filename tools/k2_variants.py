@@ -16,8 +16,8 @@ VDIR = os.path.join(ROOT, "paper_2511_20432_b200", "_lib", "variants_k2")
 
 VARIANTS = {
     "ty8": dict(K2_TY=8),
-    "ty16": dict(K2_TY=16),
-    "ty16_st3": dict(K2_TY=16, K2_CG1_STAGES=3),
+    "ty4_b3": dict(K2_TY=4, K2_MINB=3),
+    "ty4_b4": dict(K2_TY=4, K2_MINB=4),
 }
 
 
