@@ -56,7 +56,7 @@ void k1_run(tg_ctx* ctx, const double* d_src6, int n_src, const double* d_pts,
   // gradients only where a caller reads them (flux integrand, or a field call
   // with a gradient output): value-only launches skip 4 of 17 FP64 ops per pair
   const bool grad = mode == K1Mode::flux || (mode == K1Mode::field && d_out_b != nullptr);
-  const int P = ctx->k1_points_per_thread;
+  const int P = grad ? ctx->k1_points_per_thread : ctx->k1_points_per_thread_value;
   if (d_src6 == ctx->src6.p && static_cast<int>(ctx->tau_sufmin.size()) == n_src)
     n_src = ctx->active_prefix(t);  // trailing inactive sources contribute exact zeros
   int S = 1;
@@ -122,6 +122,10 @@ int tg_ctx_create(int device, tg_ctx** out) {
     if (const char* p = std::getenv("TG_K1_P")) {  // points per thread: 1..8
       const int v = std::atoi(p);
       if (v >= 1 && v <= 8) ctx->k1_points_per_thread = v;
+    }
+    if (const char* p = std::getenv("TG_K1_P0")) {  // value-only launches: 1..8
+      const int v = std::atoi(p);
+      if (v >= 1 && v <= 8) ctx->k1_points_per_thread_value = v;
     }
     k1_upload_exp_table(ctx->stream);
     TG_CUDA(cudaStreamSynchronize(ctx->stream));

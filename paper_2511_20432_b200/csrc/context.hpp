@@ -147,6 +147,8 @@ struct tg_ctx {
   tgb::DevBuf<double> pts, val, grad;
   // measured (config 1, 17 FP64 ops/pair, unroll 4): P=7 82.4 ms, P=6 83.9, P=8 89.7, P=5 94.6
   int k1_points_per_thread = 7;
+  // value-only launches (Dirichlet, field without grad), config 1: P=5 64.7 ms, 4 65.5, 7 67.2
+  int k1_points_per_thread_value = 5;
 
   // device-pointer entry points run on the caller's stream (NULL = legacy default)
   static cudaStream_t pick(void* s) { return static_cast<cudaStream_t>(s); }

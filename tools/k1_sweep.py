@@ -17,14 +17,16 @@ t = float(src[-1, 4])
 ctx.set_sources(src, mat)
 pts = torch.from_numpy(W.config1_points()).cuda()
 s = torch.cuda.Stream(); torch.cuda.set_stream(s)
-for _ in range(2): ctx.superpose(pts, t, stream=s.cuda_stream)
+grad = os.environ.get("TG_SWEEP_NOGRAD") is None
+for _ in range(2): ctx.superpose(pts, t, grad=grad, stream=s.cuda_stream)
 torch.cuda.synchronize()
 ctx.set_profiling(True); ctx.profile(reset=True)
-for _ in range(3): ctx.superpose(pts, t, stream=s.cuda_stream)
+for _ in range(3): ctx.superpose(pts, t, grad=grad, stream=s.cuda_stream)
 torch.cuda.synchronize()
 p = ctx.profile()
 ms = p["k1_ms"] / p["k1_launches"]
-print(json.dumps({"P": os.environ.get("TG_K1_P"), "k1_ms": ms, "pairs_per_s": 2**20 * 2**16 / (ms * 1e-3)}))
+print(json.dumps({"P": os.environ.get("TG_K1_P"), "P0": os.environ.get("TG_K1_P0"), "grad": grad,
+                  "k1_ms": ms, "pairs_per_s": 2**20 * 2**16 / (ms * 1e-3)}))
 '''
 if "--one" in sys.argv:
     r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, ROOT=ROOT),
