@@ -14,18 +14,21 @@
 // A CTA owns 32 x 8 columns of the control grid and marches through z, PL
 // planes per step (halving the barriers per plane). Halo'd (32+2p) x (8+2p)
 // x PL boxes arrive by TMA (cp.async.bulk.tensor.3d, zero fill outside the
-// grid) through a 3-stage mbarrier ring, so every vector is read from HBM
-// once and written once per pass; the x/y halos come from L2.
+// grid) through mbarrier rings, so every vector is read from HBM once and
+// written once per pass; the x/y halos come from L2. A prologue functor may
+// build the tile the passes read from several rings (direction update,
+// Chronopoulos-Gear residual update).
 //
-// The PCG solve is one persistent cooperative launch with two grid barriers
-// per iteration:
-//   A'  p_new = z + beta p_old  (on the loaded tiles, halo included)
-//       Ap = A p_new, p.Ap      (tile sweep; p_new and Ap written)
-//   B   x += alpha p, r -= alpha Ap, z = D^-1 r, r.z, r.r   (streaming pass)
+// Two persistent cooperative Jacobi-PCG solvers (one launch per solve):
+//   k2_cg1_kernel (default): the Chronopoulos-Gear form, one tile sweep and
+//     one grid reduction per iteration (see the section below);
+//   k2_pcg_kernel: the reference's recurrences, two grid barriers per
+//     iteration: A' p_new = z + beta p_old on the loaded tiles and Ap, p.Ap;
+//     B x += alpha p, r -= alpha Ap, z = D^-1 r, r.z, r.r (streaming pass).
 // Dot products are reduced per CTA in a fixed tree and across CTAs in a fixed
-// order (bitwise-deterministic reruns). The algorithm is the reference's:
-// inv_diag = 1.0 / d stored once, warm start, stop test ||r||/||b|| <= tol
-// before the matvec, b = 0 -> x = 0, failure on pAp <= 0 or after max_iter.
+// order (bitwise-deterministic reruns). Reference semantics: inv_diag = 1.0 /
+// d stored once, warm start, stop test ||r||/||b|| <= tol before the matvec,
+// b = 0 -> x = 0, failure on pAp <= 0 or after max_iter.
 #include <cooperative_groups.h>
 #include <cuda.h>
 
