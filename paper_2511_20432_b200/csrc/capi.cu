@@ -48,7 +48,21 @@ void k1_run(tg_ctx* ctx, const double* d_src6, int n_src, const double* d_pts,
             const int* d_index, long n_pts_l, double t, double cull, K1Mode mode,
             double* d_out_a, double* d_out_b, const K1Flux& flux, cudaStream_t stream) {
   if (n_pts_l <= 0) return;
-  if (n_pts_l > (1L << 30)) throw std::invalid_argument("superpose: too many points per call");
+  // launches of at most 2^28 points (int indexing, bounded partial buffers);
+  // every point's sum is independent of the chunking
+  constexpr long kChunk = 1L << 28;
+  if (n_pts_l > kChunk) {
+    for (long off = 0; off < n_pts_l; off += kChunk) {
+      const long n = std::min(kChunk, n_pts_l - off);
+      K1Flux f = flux;
+      if (f.index) f.index += off;
+      const bool fl = mode == K1Mode::flux;
+      k1_run(ctx, d_src6, n_src, d_index || fl ? d_pts : d_pts + 3 * off,
+             d_index ? d_index + off : nullptr, n, t, cull, mode, d_out_a + off,
+             d_out_b ? d_out_b + 3 * off : nullptr, f, stream);
+    }
+    return;
+  }
   const int n_pts = static_cast<int>(n_pts_l);
   const Material& m = ctx->mat;
   const double alpha = m.diffusivity();

@@ -182,3 +182,23 @@ def test_value_only_launch_matches_value_of_gradient_launch(gpu_ctx, cfg1_source
     v, g = gpu_ctx.superpose(pts, t)
     v0, g0 = gpu_ctx.superpose(pts, t, grad=False)
     assert g0 is None and np.array_equal(v0, v)
+
+
+def test_more_than_2e28_points_in_one_call(gpu_ctx, coracle):
+    """Calls beyond one launch's 2^28 points are chunked inside the library;
+    points on both sides of the chunk seam match the oracle."""
+    import torch
+    src = coracle.discretize_scan([[1e-3, 1e-3], [1.02e-3, 1e-3]], plane_z=1e-3, **KW)
+    t = float(src[-1, 4])
+    gpu_ctx.set_sources(src, MAT)
+    n = (1 << 28) + 4096
+    g = torch.Generator(device="cuda").manual_seed(5)
+    pts = (torch.rand((n, 3), dtype=torch.float64, device="cuda", generator=g) * 4e-4 + 8e-4)
+    v, gr = gpu_ctx.superpose(pts, t)
+    torch.cuda.synchronize()
+    for lo in (0, (1 << 28) - 2048, n - 2048):
+        p = pts[lo:lo + 2048].cpu().numpy()
+        vo, go = coracle.superpose(src, p, t, **KW)
+        check_field(v[lo:lo + 2048].cpu().numpy(), gr[lo:lo + 2048].cpu().numpy(), vo, go)
+    del pts, v, gr
+    torch.cuda.empty_cache()
