@@ -473,6 +473,10 @@ def run_ours(args):
             "peak_source": "measured live: tg_fp64_peak DFMA-chain microbenchmark on this GPU",
             "flops_per_pair": FLOPS_PER_PAIR, "pairs_per_launch": pairs_per_launch,
             "mean_launch_ms": k1_mean_ms,
+            "note": "frac uses SURVEY.md §8d's 49 flops/pair, which counts the exponential at "
+                    "its libdevice cost (31 flops); this kernel evaluates it in 6 FP64 "
+                    "instructions (17 per pair in all), so the algorithmic rate exceeds the "
+                    "DFMA peak; fp64_pipe.frac is the issued-instruction share of the pipe",
             "fp64_pipe": {
                 "ops_per_pair": PIPE_OPS_PER_PAIR,
                 "achieved_gops": (PIPE_OPS_PER_PAIR * pairs_per_launch / (k1_mean_ms * 1e-3) / 1e9
