@@ -198,16 +198,6 @@ __device__ __forceinline__ void kron_tile(const KronGrid& g, const KronTerms& c,
   constexpr uint32_t kBoxBytes = PL * PLANE * 8;
 
   __syncthreads();  // the previous segment's readers of the ring are done
-  // this thread's x and y rows of the 1D factors, in registers (the sweep is
-  // shared-memory-bandwidth bound: coefficients must not come from smem)
-  double mx[W], kx[W], my[W], ky[W];
-#pragma unroll
-  for (int d = 0; d < W; ++d) {
-    mx[d] = i < nx ? g.M[0][i * W + d] : 0.0;
-    kx[d] = i < nx ? g.K[0][i * W + d] : 0.0;
-    my[d] = j < ny ? g.M[1][j * W + d] : 0.0;
-    ky[d] = j < ny ? g.K[1][j * W + d] : 0.0;
-  }
   if (TMA && leader) {
     for (int s = 0; s < SM::kSt && s < nsteps; ++s)
       for (int q = 0; q < NIN; ++q) {
@@ -218,6 +208,18 @@ __device__ __forceinline__ void kron_tile(const KronGrid& g, const KronTerms& c,
       }
     for (int s = SM::kSt; s < SM::kSt + kL2Ahead && s < nsteps; ++s)
       for (int q = 0; q < NIN; ++q) tma_prefetch_box(in.map[q], x0 - P, y0 - P, kfirst + PL * s);
+  }
+
+  // this thread's x and y rows of the 1D factors, in registers (the sweep is
+  // shared-memory-bandwidth bound: coefficients must not come from smem);
+  // loaded after the ring is primed so their latency overlaps the first boxes
+  double mx[W], kx[W], my[W], ky[W];
+#pragma unroll
+  for (int d = 0; d < W; ++d) {
+    mx[d] = i < nx ? g.M[0][i * W + d] : 0.0;
+    kx[d] = i < nx ? g.K[0][i * W + d] : 0.0;
+    my[d] = j < ny ? g.M[1][j * W + d] : 0.0;
+    ky[d] = j < ny ? g.K[1][j * W + d] : 0.0;
   }
 
   double win1[W], win2[W], pown[W];
