@@ -115,6 +115,19 @@ __device__ __forceinline__ void for_segments(const TileIdx& T, int blocks, int b
   }
 }
 
+// The first segment for_segments hands CTA b (false when its range is empty).
+__device__ __forceinline__ bool first_segment(const TileIdx& T, int blocks, int b, Seg& out) {
+  const long total = static_cast<long>(T.ntx) * T.nty * T.nz;
+  const long s = total * b / blocks;
+  const long e = total * (b + 1) / blocks;
+  if (s >= e) return false;
+  const int col = static_cast<int>(s / T.nz);
+  const int k0 = static_cast<int>(s % T.nz);
+  const int k1 = static_cast<int>(min(static_cast<long>(T.nz), k0 + (e - s)));
+  out = Seg{(col % T.ntx) * kKronTX, (col / T.ntx) * kKronTY, k0, k1};
+  return true;
+}
+
 // Jacobi diagonal of Op(a, b) at (i, j, k).
 template <int P>
 __device__ __forceinline__ double diag_at(const KronGrid& g, double a, double b, int i, int j,
@@ -185,7 +198,8 @@ struct NoPro {
 template <int P, int PL, int NIN, int NPASS, bool TMA, class SM, class Pro, class Epi>
 __device__ __forceinline__ void kron_tile(const KronGrid& g, const KronTerms& c,
                                           const Inputs<NIN>& in, Pro& pro, const Seg& sg,
-                                          SM& sm, const double* zb, int* seqs, Epi& epi) {
+                                          SM& sm, const double* zb, int* seqs, Epi& epi,
+                                          bool primed = false) {
   using D = Dims<P, PL>;
   constexpr int W = D::W, RY = D::RY, RX = D::RX, PLANE = D::PLANE;
   const int tx = threadIdx.x, ty = threadIdx.y;
@@ -198,7 +212,7 @@ __device__ __forceinline__ void kron_tile(const KronGrid& g, const KronTerms& c,
   constexpr uint32_t kBoxBytes = PL * PLANE * 8;
 
   __syncthreads();  // the previous segment's readers of the ring are done
-  if (TMA && leader) {
+  if (TMA && leader && !primed) {  // (primed: prime_ring already issued these boxes)
     for (int s = 0; s < SM::kSt && s < nsteps; ++s)
       for (int q = 0; q < NIN; ++q) {
         const int slot = (seqs[q] + s) % SM::kSt;
@@ -419,11 +433,43 @@ __global__ void k2_inv_diag_kernel(KronGrid g, double a, double b, double* inv,
 // ---------------------------------------------------------------------------
 // persistent Jacobi-PCG
 
+// Issue the first ring boxes kron_tile would issue for segment sg (one thread).
+template <int P, int PL, int NIN, class SM>
+__device__ __forceinline__ void prime_ring(const Inputs<NIN>& in, const Seg& sg, SM& sm,
+                                           const int* seqs) {
+  constexpr uint32_t kBoxBytes = PL * Dims<P, PL>::PLANE * 8;
+  const int nsteps = (sg.k1 - sg.k0 + 2 * P + PL - 1) / PL;
+  for (int s = 0; s < SM::kSt && s < nsteps; ++s)
+    for (int q = 0; q < NIN; ++q) {
+      const int slot = (seqs[q] + s) % SM::kSt;
+      mbar_arrive_expect_tx(&sm.bar[q][slot], kBoxBytes);
+      tma_load_box(sm.ring[q][slot], in.map[q], sg.x0 - P, sg.y0 - P, sg.k0 - P + PL * s,
+                   &sm.bar[q][slot]);
+    }
+}
+
+// Wait for primed boxes nobody will consume (the solve ended after priming),
+// so no bulk copy into this CTA's shared memory is in flight at exit.
+template <int P, int PL, int NIN, class SM>
+__device__ __forceinline__ void drain_ring(const Seg& sg, SM& sm, const int* seqs) {
+  const int nsteps = (sg.k1 - sg.k0 + 2 * P + PL - 1) / PL;
+  for (int s = 0; s < SM::kSt && s < nsteps; ++s)
+    for (int q = 0; q < NIN; ++q) {
+      const int qn = seqs[q] + s;
+      mbar_wait(&sm.bar[q][qn % SM::kSt], static_cast<uint32_t>((qn / SM::kSt) & 1));
+    }
+}
+
+struct NoAfterSync {
+  __device__ void operator()() const {}
+};
+
 // Block-reduce acc (fixed tree), store to partials[buf][block][4], grid sync,
 // then every CTA sums the per-block partials in the same fixed order.
+template <class AfterSync = NoAfterSync>
 __device__ __forceinline__ void grid_reduce(cg::grid_group& grid, const double (&acc)[4],
                                             double* partials, int& buf, double* red,
-                                            double (&out)[4]) {
+                                            double (&out)[4], AfterSync after = {}) {
   const int tid = threadIdx.y * blockDim.x + threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
 #pragma unroll
@@ -441,6 +487,7 @@ __device__ __forceinline__ void grid_reduce(cg::grid_group& grid, const double (
     pb[blockIdx.x * 4 + tid] = s;
   }
   grid.sync();
+  if (warp == 1 && lane == 0) after();  // e.g. prime the next sweep's TMA ring
   if (warp == 0) {
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
@@ -880,23 +927,44 @@ __global__ void __launch_bounds__(kThreads, K2_MINB)
   }
   double alpha = gamma / tot[1], beta = 0.0;
   int cur = 0;
+  // the next sweep's first ring boxes are issued as soon as the grid barrier
+  // of the reduction has passed (its inputs are final), overlapping the
+  // partial sums and the scalar updates
+  Seg seg0{};
+  const bool has_seg = first_segment(T, gridDim.x, blockIdx.x, seg0);
+  auto inputs = [&](int k) {
+    return Inputs<4>{{w.r[k], w.w[k], w.s[k], w.inv_diag},
+                     {&maps.r[k], &maps.w[k], &maps.s[k], &maps.inv_diag}};
+  };
+  bool primed = false;
   while (it < max_iter) {
     ProCg1<P, PL> pc{alpha, beta, x,          w.p,       w.r[cur ^ 1], w.s[cur ^ 1], nx,
                      ny,    cr,   &maps.xc, &maps.pc, &cseq,        0.0,          0.0};
     EpiCg1 e{w.w[cur ^ 1], 0.0};
-    Inputs<4> in{{w.r[cur], w.w[cur], w.s[cur], w.inv_diag},
-                 {&maps.r[cur], &maps.w[cur], &maps.s[cur], &maps.inv_diag}};
+    const Inputs<4> in = inputs(cur);
+    bool first = true;
     for_segments(T, gridDim.x, blockIdx.x, [&](const Seg& sg) {
-      kron_tile<P, PL, 4, 1, true>(g, c, in, pc, sg, sm, zb, seq, e);
+      kron_tile<P, PL, 4, 1, true>(g, c, in, pc, sg, sm, zb, seq, e, first && primed);
+      first = false;
     });
     const double acc[4] = {pc.gamma, e.delta, pc.rr, 0.0};
-    grid_reduce(grid, acc, w.partials, buf, red, tot);
+    const Inputs<4> next = inputs(cur ^ 1);
+    grid_reduce(grid, acc, w.partials, buf, red, tot, [&] {
+      if (has_seg) prime_ring<P, PL, 4>(next, seg0, sm, seq);
+    });
+    primed = has_seg;
     ++it;
     cur ^= 1;
-    if (it >= max_iter) break;  // the reference leaves after max_iter updates untested
-    rel = sqrt(tot[2]) / bnorm;
-    if (rel <= tol) {
-      status = 0;
+    bool stop = it >= max_iter;  // the reference leaves after max_iter updates untested
+    if (!stop) {
+      rel = sqrt(tot[2]) / bnorm;
+      if (rel <= tol) {
+        status = 0;
+        stop = true;
+      }
+    }
+    if (stop) {
+      if (primed) drain_ring<P, PL, 4>(seg0, sm, seq);
       break;
     }
     const double g1 = tot[0];
@@ -904,6 +972,7 @@ __global__ void __launch_bounds__(kThreads, K2_MINB)
     const double den = tot[1] - beta * g1 / alpha;  // p_{i+1}.A p_{i+1}
     if (!(den > 0.0)) {
       status = 4;
+      if (primed) drain_ring<P, PL, 4>(seg0, sm, seq);
       break;
     }
     alpha = g1 / den;
