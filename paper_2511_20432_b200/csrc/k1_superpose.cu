@@ -101,7 +101,8 @@ __global__ void k1_prepare_sources(const double* __restrict__ src6, int n, doubl
 constexpr int kK1Unroll = K1_UNROLL;
 
 template <int P, bool GRAD>
-__global__ void __launch_bounds__(kK1Threads, P >= 6 ? 1 : (P >= 4 ? K1_MINB4 : 3))
+__global__ void __launch_bounds__(kK1Threads,
+                                  P >= 6 ? 256 / kK1Threads : (P >= 4 ? K1_MINB4 : 3))
     k1_partial(const SrcRec* __restrict__ src, int n_src, int split_len,
                const double* __restrict__ pts, const int* __restrict__ pt_index, int n_pts,
                double* __restrict__ part) {

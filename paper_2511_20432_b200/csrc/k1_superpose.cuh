@@ -20,8 +20,14 @@ struct __align__(32) SrcRec {
 };
 static_assert(sizeof(SrcRec) == 96, "SrcRec must stay 96 bytes");
 
-constexpr int kK1Threads = 256;
-constexpr int kK1Chunk = 128;  // sources per shared-memory stage (12 KB)
+#ifndef K1_THREADS
+#define K1_THREADS 256
+#endif
+#ifndef K1_CHUNK
+#define K1_CHUNK 128
+#endif
+constexpr int kK1Threads = K1_THREADS;
+constexpr int kK1Chunk = K1_CHUNK;  // sources per shared-memory stage (12 KB)
 constexpr int kK1Stages = 3;
 
 void k1_upload_exp_table(cudaStream_t stream);

@@ -18,8 +18,8 @@ sys.path.insert(0, ROOT)
 VDIR = os.path.join(ROOT, "paper_2511_20432_b200", "_lib", "variants")
 
 VARIANTS = {
-    "u4": dict(K1_UNROLL=4),
-    "u6": dict(K1_UNROLL=6),
+    "t128_c128": dict(K1_THREADS=128, K1_CHUNK=128),
+    "t128_c64": dict(K1_THREADS=128, K1_CHUNK=64),
 }
 
 
