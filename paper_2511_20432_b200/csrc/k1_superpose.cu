@@ -233,12 +233,15 @@ __global__ void k1_combine_field(const double* __restrict__ part, int S, int n,
   if (i >= n) return;
   const size_t plane = static_cast<size_t>(n);
   double v = 0.0, x = 0.0, y = 0.0, z = 0.0;
-  for (int s = 0; s < S; ++s) {
-    const double* p = part + static_cast<size_t>(s) * 4 * plane;
-    v += p[i];
-    x += p[plane + i];
-    y += p[2 * plane + i];
-    z += p[3 * plane + i];
+#pragma unroll  // S <= kMaxSplits: all loads in flight, sums in split order
+  for (int s = 0; s < kMaxSplits; ++s) {
+    if (s < S) {
+      const double* p = part + static_cast<size_t>(s) * 4 * plane;
+      v += p[i];
+      x += p[plane + i];
+      y += p[2 * plane + i];
+      z += p[3 * plane + i];
+    }
   }
   val[i] = v;
   if (grad) {
@@ -255,7 +258,9 @@ __global__ void k1_combine_dirichlet(const double* __restrict__ part, int S, int
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   double v = 0.0;
-  for (int s = 0; s < S; ++s) v += part[static_cast<size_t>(s) * n + i];
+#pragma unroll
+  for (int s = 0; s < kMaxSplits; ++s)
+    if (s < S) v += part[static_cast<size_t>(s) * n + i];
   out[i] = negate ? -v : v;
 }
 
@@ -270,11 +275,14 @@ __global__ void k1_combine_flux(const double* __restrict__ part, int S, int n,
   if (i >= n) return;
   const size_t plane = static_cast<size_t>(n);
   double x = 0.0, y = 0.0, z = 0.0;
-  for (int s = 0; s < S; ++s) {
-    const double* p = part + static_cast<size_t>(s) * 4 * plane;
-    x += p[plane + i];
-    y += p[2 * plane + i];
-    z += p[3 * plane + i];
+#pragma unroll
+  for (int s = 0; s < kMaxSplits; ++s) {
+    if (s < S) {
+      const double* p = part + static_cast<size_t>(s) * 4 * plane;
+      x += p[plane + i];
+      y += p[2 * plane + i];
+      z += p[3 * plane + i];
+    }
   }
   const int q = pt_index ? pt_index[i] : i;
   const double* nn = normals + 3 * static_cast<size_t>(q);
@@ -306,7 +314,7 @@ void k1_upload_exp_table(cudaStream_t stream) {
 // the single-launch result bit for bit. >= 128 sources per split, <= 16 splits
 // (enough CTAs for small point sets, few partial planes for large ones).
 int k1_choose_splits(int, int n_src, int, int) {
-  return std::max(1, std::min(16, n_src / 128));
+  return std::max(1, std::min(kMaxSplits, n_src / 128));
 }
 
 void k1_prepare(const double* d_src6, int n, double t, double alpha, double rcp, double cull,

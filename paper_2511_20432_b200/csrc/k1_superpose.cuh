@@ -29,6 +29,7 @@ static_assert(sizeof(SrcRec) == 96, "SrcRec must stay 96 bytes");
 constexpr int kK1Threads = K1_THREADS;
 constexpr int kK1Chunk = K1_CHUNK;  // sources per shared-memory stage (12 KB)
 constexpr int kK1Stages = 3;
+constexpr int kMaxSplits = 16;  // source splits of one launch (k1_choose_splits)
 
 void k1_upload_exp_table(cudaStream_t stream);
 int k1_choose_splits(int n_pts, int n_src, int sm_count, int points_per_cta);
