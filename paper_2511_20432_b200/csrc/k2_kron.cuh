@@ -6,7 +6,10 @@
 
 namespace tgb {
 
-constexpr int kKronTX = 32;  // tile width along xi (one warp)
+#ifndef K2_TX
+#define K2_TX 32
+#endif
+constexpr int kKronTX = K2_TX;  // tile width along xi; 16x16 tiles: 100 us/iter (cfg 4) vs 93
 #ifndef K2_TY
 #define K2_TY 8
 #endif
