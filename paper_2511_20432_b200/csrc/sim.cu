@@ -192,7 +192,13 @@ void Sim::setup_host() {
 
   // operator: Kronecker factors when separable, else the assembled CSR pair
   std::array<std::vector<double>, 3> coord;
-  kron = separable_coords(vol, coord);
+  // the Kronecker kernels take equal degrees 1..kKronMaxP; mixed or higher
+  // degrees use the assembled operator like any non-separable patch
+  {
+    const auto pd = vol.degrees();
+    const bool eq = pd[0] == pd[1] && pd[1] == pd[2] && pd[0] >= 1 && pd[0] <= kKronMaxP;
+    kron = eq && separable_coords(vol, coord);
+  }
   const double dt = dt_solver, th = cfg.stepping.theta;
   if (!(dt > 0.0)) throw std::invalid_argument("theta scheme: dt must be > 0");
   if (!(th >= 0.0 && th <= 1.0)) throw std::invalid_argument("theta scheme: theta must be in [0,1]");
@@ -307,10 +313,8 @@ void Sim::setup_device(int device, int preconditioner) {
 
   if (kron) {
     const int p = band[0].p;
-    if (band[1].p != p || band[2].p != p || p < 1 || p > kKronMaxP) {
-      kron = false;  // mixed or high degrees: fall back to the assembled operator
-      throw std::invalid_argument("kronecker path needs equal degrees 1..3 in all directions");
-    }
+    if (band[1].p != p || band[2].p != p || p < 1 || p > kKronMaxP)  // excluded in setup_host
+      throw std::logic_error("kronecker path needs equal degrees 1..3 in all directions");
     const int W = 2 * p + 1;
     std::vector<double> all;
     for (int d = 0; d < 3; ++d) {

@@ -293,3 +293,48 @@ def test_other_bottom_faces_against_live_reference(bottom, precond, ref, tmp_pat
         assert normwise(st["free"], o["free"]) <= 1e-8, (bottom, k)
     s.close()
     r.close()
+
+
+def box_geometry(degrees, size=(2e-3, 1e-3, 0.5e-3)):
+    """[geometry] block of an axis-aligned box as a single Bezier patch of the
+    given degrees (control points equally spaced: the exact linear map)."""
+    lines = ["[geometry]", "degrees = " + " ".join(map(str, degrees))]
+    for name, p in zip(("xi", "eta", "zeta"), degrees):
+        lines.append(f"knots_{name} = " + " ".join(["0"] * (p + 1) + ["1"] * (p + 1)))
+    lines.append("grid_dims = " + " ".join(str(p + 1) for p in degrees))
+    px, py, pz = degrees
+    for k in range(pz + 1):
+        for j in range(py + 1):
+            for i in range(px + 1):
+                x, y, z = (size[0] * i / px, size[1] * j / py, size[2] * k / pz)
+                lines.append(f"cp = {x!r} {y!r} {z!r} 1")
+    return "\n".join(lines) + "\n"
+
+
+@pytest.mark.parametrize("degrees", [(1, 1, 1), (3, 3, 3), (2, 2, 1)],
+                         ids=["p1", "p3", "mixed221"])
+def test_other_degrees_against_live_reference(degrees, ref, tmp_path):
+    """Degree 1 and 3 Kronecker paths, and a mixed-degree cuboid (separable
+    but unequal degrees: the assembled-operator path), stepped against the
+    unmodified reference."""
+    txt = open(cfg("cfg0_parity")).read()
+    head, rest = txt.split("[geometry]", 1)
+    rest = rest[rest.index("\n\n"):]
+    p = tmp_path / "deg.cfg"
+    p.write_text(head + box_geometry(degrees) + rest)
+    s = tg.Simulation(str(p), t_end=1.5e-4)
+    r = ref.sim(str(p), t_end=1.5e-4)
+    kron = len(set(degrees)) == 1
+    assert (s.info["kronecker"] > 0) == kron
+    s.reset()
+    F0, g0 = r.reset()
+    assert normwise(s.state()["F"], F0) <= 1e-10
+    for k in range(1, 16):
+        s.advance(1)
+        st = s.state()
+        o = r.step()
+        assert normwise(st["F"], o["F"]) <= 1e-10, (degrees, k)
+        assert normwise(st["g"], o["g"]) <= 1e-10, (degrees, k)
+        assert normwise(st["free"], o["free"]) <= 1e-8, (degrees, k)
+    s.close()
+    r.close()
