@@ -362,3 +362,32 @@ def test_graded_cuboid_against_live_reference(ref, tmp_path):
         assert normwise(st["free"], o["free"]) <= 1e-8, k
     s.close()
     r.close()
+
+
+@pytest.mark.parametrize("edit", [
+    ("theta = 0.5", "theta = 1.0"),
+    ("theta = 0.5", "theta = 0.0"),
+    ("dt = 1e-5\nt_end", "dt = 1e-5\nsubsteps = 2\nt_end"),
+    ("zeta_elements = 4", "zeta_elements = 4\nquad_order = 4"),
+], ids=["theta1", "theta0", "substeps2", "quad4"])
+def test_stepping_and_quadrature_variants_against_live_reference(edit, ref, tmp_path):
+    """Backward Euler, the explicit theta = 0 scheme, solver substeps and an
+    explicit quadrature order change the operator and the step sequence: each
+    against the unmodified reference."""
+    txt = open(cfg("cfg0_parity")).read()
+    assert edit[0] in txt
+    p = tmp_path / "variant.cfg"
+    p.write_text(txt.replace(edit[0], edit[1], 1))
+    s = tg.Simulation(str(p), t_end=1.2e-4)
+    r = ref.sim(str(p), t_end=1.2e-4)
+    assert s.info["n_steps"] == r.info["n_steps"]
+    s.reset()
+    r.reset()
+    for k in range(1, s.info["n_steps"] + 1):
+        s.advance(1)
+        st = s.state()
+        o = r.step()
+        assert normwise(st["F"], o["F"]) <= 1e-10, k
+        assert normwise(st["free"], o["free"]) <= 1e-8, k
+    s.close()
+    r.close()
