@@ -52,6 +52,9 @@ FLOPS_PER_PAIR = 49.0  # value + gradient, exp counted at libdev
 # the 49-flop accounting exceeds the DFMA peak — fp64_pipe reports the
 # issued-instruction fraction).
 PIPE_OPS_PER_PAIR = 17.0
+# with every source on one plane (a layer's scan paths; config 1 is one) the
+# PLANAR variant takes rz and rz^2 per point: 8 DFMA + 5 DADD + 2 DMUL
+PIPE_OPS_PER_PAIR_PLANAR = 15.0
 # DRAM bytes (read + write) per launch from one `ncu --set full` capture of each
 # dominant kernel (profiles/r01_k1_ncu_summary.md, r01_k2_ncu_summary.md)
 K1_TRAFFIC_BYTES = 90.9e6 + 486.6e6   # k1_partial<7,1>, config 1, one launch
@@ -464,7 +467,11 @@ def run_ours(args):
     k1_mean_ms = prof["k1_ms"] / max(1, prof["k1_launches"])
     pairs_per_launch = prof["k1_pairs"] / max(1, prof["k1_launches"])
     achieved = FLOPS_PER_PAIR * pairs_per_launch / (k1_mean_ms * 1e-3) / 1e12 if k1_mean_ms else None
-    roof = {"kernel": f"k1_partial<{os.environ.get('TG_K1_P', '7')},true>", "bound": "fp64",
+    planar = bool(len(src)) and bool(np.all(src[:, 2] == src[0, 2])) and \
+        not os.environ.get("TG_K1_NO_PLANAR")
+    ops = PIPE_OPS_PER_PAIR_PLANAR if planar else PIPE_OPS_PER_PAIR
+    roof = {"kernel": f"k1_partial<{os.environ.get('TG_K1_P', '7')},true,{str(planar).lower()}>",
+            "bound": "fp64",
             "achieved": achieved,
             "peak": fp64_peak, "unit": "TFLOP/s",
             "frac": (achieved / fp64_peak) if (achieved and fp64_peak) else None,
@@ -475,14 +482,14 @@ def run_ours(args):
             "mean_launch_ms": k1_mean_ms,
             "note": "frac uses SURVEY.md §8d's 49 flops/pair, which counts the exponential at "
                     "its libdevice cost (31 flops); this kernel evaluates it in 6 FP64 "
-                    "instructions (17 per pair in all), so the algorithmic rate exceeds the "
+                    "instructions (15-17 per pair in all), so the algorithmic rate exceeds the "
                     "DFMA peak; fp64_pipe.frac is the issued-instruction share of the pipe",
             "fp64_pipe": {
-                "ops_per_pair": PIPE_OPS_PER_PAIR,
-                "achieved_gops": (PIPE_OPS_PER_PAIR * pairs_per_launch / (k1_mean_ms * 1e-3) / 1e9
+                "ops_per_pair": ops,
+                "achieved_gops": (ops * pairs_per_launch / (k1_mean_ms * 1e-3) / 1e9
                                   if k1_mean_ms else None),
                 "peak_gops": fp64_peak * 1e3 / 2 if fp64_peak else None,
-                "frac": (PIPE_OPS_PER_PAIR * pairs_per_launch / (k1_mean_ms * 1e-3) /
+                "frac": (ops * pairs_per_launch / (k1_mean_ms * 1e-3) /
                          (fp64_peak * 1e12 / 2)) if (k1_mean_ms and fp64_peak) else None},
             "k1_share_of_step": prof["k1_ms"] / max(1e-9, float(sum(step_ms)))}
     line = {

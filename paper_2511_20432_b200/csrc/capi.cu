@@ -71,8 +71,9 @@ void k1_run(tg_ctx* ctx, const double* d_src6, int n_src, const double* d_pts,
   // with a gradient output): value-only launches skip 4 of 17 FP64 ops per pair
   const bool grad = mode == K1Mode::flux || (mode == K1Mode::field && d_out_b != nullptr);
   const int P = grad ? ctx->k1_points_per_thread : ctx->k1_points_per_thread_value;
-  if (d_src6 == ctx->src6.p && static_cast<int>(ctx->tau_sufmin.size()) == n_src)
-    n_src = ctx->active_prefix(t);  // trailing inactive sources contribute exact zeros
+  const bool own_src = d_src6 == ctx->src6.p && static_cast<int>(ctx->tau_sufmin.size()) == n_src;
+  if (own_src) n_src = ctx->active_prefix(t);  // trailing inactive sources: exact zeros
+  const bool planar = own_src && ctx->planar && !std::getenv("TG_K1_NO_PLANAR");
   int S = 1;
   if (n_src > 0) {
     k1_prepare(d_src6, n_src, t, alpha, rcp, cull, ctx->rec.ensure(n_src), stream);
@@ -82,7 +83,8 @@ void k1_run(tg_ctx* ctx, const double* d_src6, int n_src, const double* d_pts,
   double* part = ctx->part.ensure(static_cast<size_t>(S) * (grad ? 4 : 1) * n_pts);
   if (n_src > 0) {
     ctx->timer.timed(1, stream, [&] {
-      k1_launch_partial(ctx->rec.p, n_src, d_pts, d_index, n_pts, S, grad, P, part, stream);
+      k1_launch_partial(ctx->rec.p, n_src, d_pts, d_index, n_pts, S, grad, P, part, stream,
+                        planar, ctx->planar_z);
     });
     ++ctx->timer.launches;
     ++ctx->timer.k1_launches;

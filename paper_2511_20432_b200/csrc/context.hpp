@@ -136,7 +136,14 @@ struct tg_ctx {
     const auto it = std::lower_bound(tau_sufmin.begin(), tau_sufmin.end(), t);
     return static_cast<int>(it - tau_sufmin.begin());
   }
+  // all sources on one plane z = planar_z (k1_partial's PLANAR variant)
+  bool planar = false;
+  double planar_z = 0.0;
   void set_tau(const double* src6_host, int n) {
+    planar = n > 0;
+    planar_z = n > 0 ? src6_host[2] : 0.0;
+    for (int j = 1; j < n && planar; ++j)
+      planar = __builtin_memcmp(&src6_host[6 * j + 2], &planar_z, sizeof(double)) == 0;
     tau_sufmin.assign(n, 0.0);
     double m = INFINITY;
     for (int j = n - 1; j >= 0; --j) tau_sufmin[j] = m = std::min(m, src6_host[6 * j + 5]);

@@ -100,12 +100,16 @@ __global__ void k1_prepare_sources(const double* __restrict__ src6, int n, doubl
 #endif
 constexpr int kK1Unroll = K1_UNROLL;
 
-template <int P, bool GRAD>
+// PLANAR: every source of the history lies on one plane z = zs (a layer's
+// scan paths; k1_run checks it). Then rz = z - zs and fl(rz * rz) are per
+// point — the reference's own values for every pair of that point — and the
+// z-gradient is rz * sum_j w_j: two FP64 instructions fewer per pair.
+template <int P, bool GRAD, bool PLANAR>
 __global__ void __launch_bounds__(kK1Threads,
                                   P >= 6 ? 256 / kK1Threads : (P >= 4 ? K1_MINB4 : 3))
     k1_partial(const SrcRec* __restrict__ src, int n_src, int split_len,
                const double* __restrict__ pts, const int* __restrict__ pt_index, int n_pts,
-               double* __restrict__ part) {
+               double* __restrict__ part, double zs) {
   __shared__ __align__(128) SrcRec ring[kK1Stages][kK1Chunk];
   __shared__ double tab[kExpTableSize];
   __shared__ __align__(8) uint64_t bars[kK1Stages];
@@ -146,6 +150,15 @@ __global__ void __launch_bounds__(kK1Threads,
     }
     v[k] = gx[k] = gy[k] = gz[k] = 0.0;
   }
+  // PLANAR: pz holds rz = z - zs and gz accumulates sum_j w_j; rz2 = fl(rz rz)
+  double rz2[PLANAR ? P : 1];
+  if (PLANAR) {
+#pragma unroll
+    for (int k = 0; k < P; ++k) {
+      pz[k] = __dsub_rn(pz[k], zs);
+      rz2[k] = __dmul_rn(pz[k], pz[k]);
+    }
+  }
 
   for (int c = 0; c < n_chunks; ++c) {
     const int buf = c % kK1Stages;
@@ -165,10 +178,13 @@ __global__ void __launch_bounds__(kK1Threads,
       for (int k = 0; k < P; ++k) {
         rx[k] = __dsub_rn(px[k], a.x);
         ry[k] = __dsub_rn(py[k], a.y);
-        rz[k] = __dsub_rn(pz[k], a.z);
+        rz[k] = PLANAR ? pz[k] : __dsub_rn(pz[k], a.z);
         // r.r with FMA (3 roundings of non-negative terms: within a few ulp of
         // the reference's 5-rounding r.r, core.hpp:27)
-        r2[k] = __fma_rn(rz[k], rz[k], __fma_rn(ry[k], ry[k], __dmul_rn(rx[k], rx[k])));
+        if (PLANAR)
+          r2[k] = __fma_rn(ry[k], ry[k], __fma_rn(rx[k], rx[k], rz2[PLANAR ? k : 0]));
+        else
+          r2[k] = __fma_rn(rz[k], rz[k], __fma_rn(ry[k], ry[k], __dmul_rn(rx[k], rx[k])));
         // keep/cull decided on the high words (1 unit = 2^32 ulp >> the few-ulp
         // gap): thr < 0 (inactive source) lands in the cull branch; the band
         // hi32(r.r) in [lo, lo + 2] is re-decided exactly below
@@ -182,8 +198,9 @@ __global__ void __launch_bounds__(kK1Threads,
         // contraction) and its exact compare, for every point of the warp
 #pragma unroll
         for (int k = 0; k < P; ++k) {
-          const double e2 = __dadd_rn(__dadd_rn(__dmul_rn(rx[k], rx[k]), __dmul_rn(ry[k], ry[k])),
-                                      __dmul_rn(rz[k], rz[k]));
+          const double zz = PLANAR ? rz2[PLANAR ? k : 0] : __dmul_rn(rz[k], rz[k]);
+          const double e2 =
+              __dadd_rn(__dadd_rn(__dmul_rn(rx[k], rx[k]), __dmul_rn(ry[k], ry[k])), zz);
           keep[k] = __double_as_longlong(e2) <= __double_as_longlong(b.z);
         }
       }
@@ -196,7 +213,7 @@ __global__ void __launch_bounds__(kK1Threads,
           const double w = __dmul_rn(T, b.y);
           gx[k] = __fma_rn(rx[k], w, gx[k]);
           gy[k] = __fma_rn(ry[k], w, gy[k]);
-          gz[k] = __fma_rn(rz[k], w, gz[k]);
+          gz[k] = PLANAR ? __dadd_rn(gz[k], w) : __fma_rn(rz[k], w, gz[k]);
         }
       }
     }
@@ -220,7 +237,7 @@ __global__ void __launch_bounds__(kK1Threads,
       if (GRAD) {
         pv[plane + i] = gx[k];
         pv[2 * plane + i] = gy[k];
-        pv[3 * plane + i] = gz[k];
+        pv[3 * plane + i] = PLANAR ? __dmul_rn(pz[k], gz[k]) : gz[k];
       }
     }
   }
@@ -327,22 +344,31 @@ void k1_prepare(const double* d_src6, int n, double t, double alpha, double rcp,
 
 void k1_launch_partial(const SrcRec* d_rec, int n_src, const double* d_pts,
                        const int* d_index, int n_pts, int S, bool grad, int P, double* d_part,
-                       cudaStream_t stream) {
+                       cudaStream_t stream, bool planar, double zs) {
   const int split_len = (n_src + S - 1) / S;
   const int ppc = kK1Threads * P;
   dim3 grid((n_pts + ppc - 1) / ppc, S);
-#define TG_K1_LAUNCH(PP, GG)                                                              \
-  k1_partial<PP, GG><<<grid, kK1Threads, 0, stream>>>(d_rec, n_src, split_len, d_pts, d_index, \
-                                                      n_pts, d_part)
+#define TG_K1_LAUNCH(PP, GG, PLN)                                                         \
+  k1_partial<PP, GG, PLN><<<grid, kK1Threads, 0, stream>>>(d_rec, n_src, split_len, d_pts,     \
+                                                          d_index, n_pts, d_part, zs)
+  // planar-history variants for the default shapes (P = 7 with gradient, 5 value-only)
+  if (planar && grad && P == 7) {
+    TG_K1_LAUNCH(7, true, true);
+    return;
+  }
+  if (planar && !grad && P == 5) {
+    TG_K1_LAUNCH(5, false, true);
+    return;
+  }
   switch (P) {
-    case 1: if (grad) TG_K1_LAUNCH(1, true); else TG_K1_LAUNCH(1, false); break;
-    case 2: if (grad) TG_K1_LAUNCH(2, true); else TG_K1_LAUNCH(2, false); break;
-    case 3: if (grad) TG_K1_LAUNCH(3, true); else TG_K1_LAUNCH(3, false); break;
-    case 5: if (grad) TG_K1_LAUNCH(5, true); else TG_K1_LAUNCH(5, false); break;
-    case 6: if (grad) TG_K1_LAUNCH(6, true); else TG_K1_LAUNCH(6, false); break;
-    case 7: if (grad) TG_K1_LAUNCH(7, true); else TG_K1_LAUNCH(7, false); break;
-    case 8: if (grad) TG_K1_LAUNCH(8, true); else TG_K1_LAUNCH(8, false); break;
-    default: if (grad) TG_K1_LAUNCH(4, true); else TG_K1_LAUNCH(4, false); break;
+    case 1: if (grad) TG_K1_LAUNCH(1, true, false); else TG_K1_LAUNCH(1, false, false); break;
+    case 2: if (grad) TG_K1_LAUNCH(2, true, false); else TG_K1_LAUNCH(2, false, false); break;
+    case 3: if (grad) TG_K1_LAUNCH(3, true, false); else TG_K1_LAUNCH(3, false, false); break;
+    case 5: if (grad) TG_K1_LAUNCH(5, true, false); else TG_K1_LAUNCH(5, false, false); break;
+    case 6: if (grad) TG_K1_LAUNCH(6, true, false); else TG_K1_LAUNCH(6, false, false); break;
+    case 7: if (grad) TG_K1_LAUNCH(7, true, false); else TG_K1_LAUNCH(7, false, false); break;
+    case 8: if (grad) TG_K1_LAUNCH(8, true, false); else TG_K1_LAUNCH(8, false, false); break;
+    default: if (grad) TG_K1_LAUNCH(4, true, false); else TG_K1_LAUNCH(4, false, false); break;
   }
 #undef TG_K1_LAUNCH
 }

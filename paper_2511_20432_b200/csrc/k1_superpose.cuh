@@ -35,8 +35,10 @@ void k1_upload_exp_table(cudaStream_t stream);
 int k1_choose_splits(int n_pts, int n_src, int sm_count, int points_per_cta);
 void k1_prepare(const double* d_src6, int n, double t, double alpha, double rcp, double cull,
                 SrcRec* d_rec, cudaStream_t stream);
+// planar: all sources lie on z = zs (k1_partial's PLANAR variant)
 void k1_launch_partial(const SrcRec* d_rec, int n_src, const double* d_pts, const int* d_index,
-                       int n_pts, int S, bool grad, int P, double* d_part, cudaStream_t stream);
+                       int n_pts, int S, bool grad, int P, double* d_part, cudaStream_t stream,
+                       bool planar = false, double zs = 0.0);
 void k1_launch_combine_field(const double* d_part, int S, int n, double* d_val, double* d_grad,
                              cudaStream_t stream);
 void k1_launch_combine_dirichlet(const double* d_part, int S, int n, double* d_out,
