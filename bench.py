@@ -57,7 +57,7 @@ PIPE_OPS_PER_PAIR = 17.0
 PIPE_OPS_PER_PAIR_PLANAR = 15.0
 # DRAM bytes (read + write) per launch from one `ncu --set full` capture of each
 # dominant kernel (profiles/r01_k1_ncu_summary.md, r01_k2_ncu_summary.md)
-K1_TRAFFIC_BYTES = 90.9e6 + 486.6e6   # k1_partial<7,1>, config 1, one launch
+K1_TRAFFIC_BYTES = 92.2e6 + 484.4e6   # k1_partial<7,1,1>, config 1, one launch
 K2_TRAFFIC_B_PER_DOF_ITER = 88.0      # k2_cg1_kernel<2>, config 4 (15.62 + 12.56 GB / 74 sweeps)
 
 
@@ -476,7 +476,8 @@ def run_ours(args):
             "peak": fp64_peak, "unit": "TFLOP/s",
             "frac": (achieved / fp64_peak) if (achieved and fp64_peak) else None,
             "traffic": K1_TRAFFIC_BYTES,
-            "traffic_source": "ncu --set full, profiles/r01_k1_full_p7.ncu-rep (dram read+write)",
+            "traffic_source": "ncu --set full, profiles/r01_k1_full_p7_planar.ncu-rep (dram "
+                              "read+write)",
             "peak_source": "measured live: tg_fp64_peak DFMA-chain microbenchmark on this GPU",
             "flops_per_pair": FLOPS_PER_PAIR, "pairs_per_launch": pairs_per_launch,
             "mean_launch_ms": k1_mean_ms,
