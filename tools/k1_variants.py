@@ -18,8 +18,7 @@ sys.path.insert(0, ROOT)
 VDIR = os.path.join(ROOT, "paper_2511_20432_b200", "_lib", "variants")
 
 VARIANTS = {
-    "t128_c128": dict(K1_THREADS=128, K1_CHUNK=128),
-    "t128_c64": dict(K1_THREADS=128, K1_CHUNK=64),
+    "planar_sweep": dict(K1_PLANAR_SWEEP=1),
 }
 
 
