@@ -38,13 +38,17 @@ struct DevBuf {
   ~DevBuf() {
     if (p) cudaFree(p);
   }
+  // grows with 25 % headroom once a buffer has been sized (per-step sizes
+  // such as the flux-load point count vary by a few percent; a reallocation
+  // synchronizes the device and costs milliseconds at config-4 sizes)
   T* ensure(size_t n) {
     if (n > cap) {
+      const size_t want = cap > 0 ? n + n / 4 : n;
       if (p) TG_CUDA(cudaFree(p));
       p = nullptr;
       cap = 0;
-      TG_CUDA(cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(T)));
-      cap = n;
+      TG_CUDA(cudaMalloc(&p, std::max<size_t>(want, 1) * sizeof(T)));
+      cap = want;
     }
     return p;
   }

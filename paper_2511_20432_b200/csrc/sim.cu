@@ -560,9 +560,23 @@ void Sim::reset() {
 PcgStatus Sim::advance() {
   const int s1 = step + 1;
   const double t1 = s1 * dt_solver;  // driver.cpp:127
+  static const bool timing = std::getenv("TG_STEP_TIMING") != nullptr;
+  auto now = [&] {
+    if (timing) TG_CUDA(cudaStreamSynchronize(ctx->stream));
+    return std::chrono::steady_clock::now();
+  };
+  const auto t0 = now();
   flux_load_device(t1, cfg.mesh.elevate_radius, d_F1.p);
+  const auto ta = now();
   dirichlet_device(t1, d_g1.p);
+  const auto tb = now();
   const PcgStatus st = theta_step_device(cfg.stepping.solver_tol, cfg.stepping.max_iter);
+  if (timing) {
+    const auto tc = now();
+    auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+    std::fprintf(stderr, "[step %d] flux %.3f ms, dirichlet %.3f ms, theta %.3f ms\n", s1,
+                 ms(t0, ta), ms(ta, tb), ms(tb, tc));
+  }
   std::swap(d_Fn.p, d_F1.p);
   std::swap(d_gn.p, d_g1.p);
   step = s1;
