@@ -75,6 +75,9 @@ def parse():
     ap.add_argument("--ncu", action="store_true", help="profiling run: no clocks/cpu legs")
     ap.add_argument("--theta-steps", type=int, default=3,
                     help="config-4 time steps for the theta-step section (0 = skip)")
+    ap.add_argument("--theta-sharded", type=int, default=0,
+                    help="config-4 time steps on all ranks with parallel.ShardedTimeLoop "
+                         "(sharded superposition + all-gathered loads; 0 = skip)")
     return ap.parse_args()
 
 
@@ -320,6 +323,47 @@ def theta_section(steps, warmup, with_cpu):
     return out
 
 
+def theta_sharded_section(steps, rank, world, local):
+    """Config-4 time steps on all ranks: the superposition work (flux-load
+    element slabs, Dirichlet point slabs) split across GPUs and all-gathered,
+    the theta step replicated (strong scaling of the whole step).
+    Wall time per step between barriers, max over ranks."""
+    import torch
+    import paper_2511_20432_b200 as tg
+    from paper_2511_20432_b200 import parallel
+    import torch.distributed as dist
+    own_pg = world == 1 and not dist.is_initialized()
+    if own_pg:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29631")
+        dist.init_process_group("nccl", rank=0, world_size=1)
+    try:
+        sim = tg.Simulation(THETA_CFG, device=local)
+        loop = parallel.ShardedTimeLoop(sim, parallel.Dist(rank, world, f"cuda:{local}"))
+        loop.reset()
+        loop.step()
+        dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        its = 0
+        for _ in range(steps):
+            its += loop.step()[0]
+        torch.cuda.synchronize()
+        dist.barrier()
+        ms = torch.tensor([(time.perf_counter() - t0) * 1e3 / steps], dtype=torch.float64,
+                          device=f"cuda:{local}")
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+        sim.close()
+        return {"workload": "config4 time steps, superposition sharded over "
+                            f"{world} GPU(s), loads all-gathered, theta step replicated",
+                "n_gpus": world, "steps": steps, "ms_per_step": float(ms.item()),
+                "cg_iterations_per_step": its / steps,
+                "timing": "wall clock between barriers, max over ranks"}
+    finally:
+        if own_pg:
+            dist.destroy_process_group()
+
+
 def theta_fdm(steps, warmup):
     """The opt-in fast-diagonalization preconditioner on the
     same config-4 steps: θ-step solve time and CG iterations."""
@@ -457,6 +501,13 @@ def run_ours(args):
         e2e_s = float(tt.item())
     e2e = world * pairs_per_step * args.steps / e2e_s
 
+    sharded = None
+    if args.theta_sharded > 0:  # collective: every rank takes part
+        try:
+            sharded = theta_sharded_section(args.theta_sharded, rank, world, local)
+        except Exception as e:
+            sharded = {"error": str(e)}
+
     if rank != 0:
         if world > 1:
             import torch.distributed as dist
@@ -520,6 +571,8 @@ def run_ours(args):
                                                not args.no_cpu_baseline and not args.ncu)
         except Exception as e:
             line["theta_step"] = {"error": str(e)}
+    if sharded is not None:
+        line["theta_step_sharded"] = sharded
     print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist

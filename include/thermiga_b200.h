@@ -172,6 +172,16 @@ int tg_sim_flux_gather_device(tg_sim* sim, const double* d_loc_all, double* d_F)
  * planes included). Kronecker patches only. Device pointers; synchronous. */
 int tg_sim_operator_apply_slab_device(tg_sim* sim, int k0, int k1, const double* d_x,
                                       double* d_y);
+/* Dirichlet values of the constrained DOFs [c0, c1) at t (device output of
+ * c1 - c0 values, synchronous); ranges of a point split reproduce the full
+ * call bit for bit. */
+int tg_sim_dirichlet_range_device(tg_sim* sim, double t, int c0, int c1, double* d_g);
+/* One time step with F_{n+1} (n_full) and g_{n+1} (n_constrained) supplied as
+ * device arrays — the step of a driver that assembles the loads sharded and
+ * all-gathers them; otherwise as tg_sim_advance(sim, 1, ...). */
+int tg_sim_advance_with_loads_device(tg_sim* sim, const double* d_F1, const double* d_g1,
+                                     long* cg_iterations, double* rel);
+
 /* 1 / diag(A_ff) (the Jacobi preconditioner, sparse.cpp:47-52), host copy. */
 int tg_sim_inverse_diagonal(tg_sim* sim, double* out);
 

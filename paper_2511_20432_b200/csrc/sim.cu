@@ -479,9 +479,14 @@ void Sim::flux_gather_device(const double* d_loc_all, double* d_F) {
   TG_CUDA(cudaGetLastError());
 }
 
-void Sim::dirichlet_device(double t, double* d_g) {
-  k1_run(ctx, ctx->src6.p, ctx->n_src, d_grev.p, nullptr, n_con, t, cfg.superpose.cull_exponent,
-         K1Mode::dirichlet, d_g, nullptr, {}, ctx->stream);
+void Sim::dirichlet_device(double t, double* d_g, int c0, int c1) {
+  // constrained DOFs [c0, c1) (all by default): each value depends on its
+  // Greville point only, so a range is the same bits as the full call
+  if (c1 < 0) c1 = n_con;
+  c0 = std::max(0, std::min(c0, n_con));
+  c1 = std::max(c0, std::min(c1, n_con));
+  k1_run(ctx, ctx->src6.p, ctx->n_src, d_grev.p + 3 * static_cast<size_t>(c0), nullptr, c1 - c0,
+         t, cfg.superpose.cull_exponent, K1Mode::dirichlet, d_g, nullptr, {}, ctx->stream);
 }
 
 PcgStatus Sim::theta_step_device(double tol, int max_iter) {
@@ -580,6 +585,17 @@ PcgStatus Sim::advance() {
   std::swap(d_Fn.p, d_F1.p);
   std::swap(d_gn.p, d_g1.p);
   step = s1;
+  return st;
+}
+
+PcgStatus Sim::advance_with_loads(const double* d_F1_in, const double* d_g1_in) {
+  cudaStream_t s = ctx->stream;
+  TG_CUDA(cudaMemcpyAsync(d_F1.p, d_F1_in, sizeof(double) * n_full, cudaMemcpyDeviceToDevice, s));
+  TG_CUDA(cudaMemcpyAsync(d_g1.p, d_g1_in, sizeof(double) * n_con, cudaMemcpyDeviceToDevice, s));
+  const PcgStatus st = theta_step_device(cfg.stepping.solver_tol, cfg.stepping.max_iter);
+  std::swap(d_Fn.p, d_F1.p);
+  std::swap(d_gn.p, d_g1.p);
+  step += 1;
   return st;
 }
 

@@ -41,6 +41,9 @@ class Sim {
   // run_time_loop pieces (driver.cpp:105-146)
   void reset();          // state 0: free = 0, g_0, F_0
   PcgStatus advance();   // one step: F_{n+1}, g_{n+1}, theta step
+  // one step with F_{n+1}, g_{n+1} supplied on the device (a multi-GPU driver
+  // assembles them sharded, all-gathers, and every rank steps)
+  PcgStatus advance_with_loads(const double* d_F1_in, const double* d_g1_in);
 
   // drop-in pieces on device buffers
   // assemble_flux_load; with [e0, e1) only those face elements' local loads
@@ -48,7 +51,7 @@ class Sim {
   void flux_load_device(double t, double radius, double* d_F, int e0 = 0,
                         int e1 = 1 << 30);
   void flux_gather_device(const double* d_loc_all, double* d_F);
-  void dirichlet_device(double t, double* d_g);
+  void dirichlet_device(double t, double* d_g, int c0 = 0, int c1 = -1);
   PcgStatus theta_step_device(double tol, int max_iter);  // uses d_x, d_gn, d_g1, d_Fn, d_F1
 
   // observers: the current state at parametric points, on

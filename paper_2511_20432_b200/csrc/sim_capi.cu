@@ -205,6 +205,23 @@ int tg_sim_advance(tg_sim* s, int n_steps, long* cg_iterations, double* last_rel
   });
 }
 
+int tg_sim_dirichlet_range_device(tg_sim* s, double t, int c0, int c1, double* d_g) {
+  return sim_guard(s, [&](Sim& m) {
+    if (c0 < 0 || c1 < c0 || c1 > m.n_con) throw std::invalid_argument("dirichlet: bad range");
+    m.dirichlet_device(t, d_g, c0, c1);
+    TG_CUDA(cudaStreamSynchronize(m.ctx->stream));
+  });
+}
+
+int tg_sim_advance_with_loads_device(tg_sim* s, const double* d_F1, const double* d_g1,
+                                     long* cg_iterations, double* rel) {
+  return sim_guard(s, [&](Sim& m) {
+    const PcgStatus st = m.advance_with_loads(d_F1, d_g1);
+    if (cg_iterations) *cg_iterations = st.iterations;
+    if (rel) *rel = st.rel_residual;
+  });
+}
+
 int tg_sim_state(tg_sim* s, int* step, double* time, double* free_out, double* g_out,
                  double* F_out) {
   return sim_guard(s, [&](Sim& m) {

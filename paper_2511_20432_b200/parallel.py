@@ -304,6 +304,63 @@ def gpu_inverse_diagonal(sim):
     return torch.from_numpy(out).cuda()
 
 
+def gpu_dirichlet_range(sim, t: float):
+    """fn(c0, c1) -> Dirichlet values of constrained DOFs [c0, c1) at t (CUDA
+    tensor) for sharded_points."""
+    import ctypes as C
+    import torch
+    L = sim._L
+    L.tg_sim_dirichlet_range_device.argtypes = [C.c_void_p, C.c_double, C.c_int, C.c_int,
+                                                C.c_void_p]
+
+    def fn(c0, c1):
+        out = torch.empty(max(0, c1 - c0), dtype=torch.float64, device="cuda")
+        if c1 > c0:
+            sim._check(L.tg_sim_dirichlet_range_device(sim._h, float(t), c0, c1,
+                                                       C.c_void_p(out.data_ptr())))
+        return out
+    return fn
+
+
+class ShardedTimeLoop:
+    """run_time_loop (proj/src/driver.cpp:105-146) on `dist.world` GPUs, one
+    Simulation per rank. Per step the superposition work — the flux load over
+    face-element slabs and the Dirichlet values over point slabs, >90 % of a
+    config-4 step — is split across ranks and all-gathered (two collectives);
+    the theta step then runs on every rank from the same loads, so every rank
+    holds the same state (bit for bit: all pieces are deterministic and
+    shard-independent)."""
+
+    def __init__(self, sim, dist: Dist):
+        import ctypes as C
+        self.sim, self.dist = sim, dist
+        self.L = sim._L
+        self.L.tg_sim_advance_with_loads_device.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p,
+                                                           C.POINTER(C.c_long),
+                                                           C.POINTER(C.c_double)]
+        self.dt = sim.params["dt"]
+        self.step_index = 0
+
+    def reset(self):
+        self.sim.reset()
+        self.step_index = 0
+
+    def step(self):
+        import ctypes as C
+        s, d = self.sim, self.dist
+        t1 = (self.step_index + 1) * self.dt  # driver.cpp:127
+        F1 = sharded_flux_load(gpu_flux_local(s, t1), gpu_flux_gather(s), s.info["n_face_elems"],
+                               s.info["n_dofs_kept"], d)
+        g1 = sharded_points(gpu_dirichlet_range(s, t1), s.info["n_constrained"], d)
+        it = C.c_long(0)
+        rel = C.c_double(0.0)
+        s._check(self.L.tg_sim_advance_with_loads_device(s._h, C.c_void_p(F1.data_ptr()),
+                                                         C.c_void_p(g1.data_ptr()),
+                                                         C.byref(it), C.byref(rel)))
+        self.step_index += 1
+        return it.value, rel.value
+
+
 def init_from_env(backend: Optional[str] = None) -> Dist:
     """torchrun-style initialization (MASTER_ADDR/PORT, RANK, WORLD_SIZE)."""
     import torch

@@ -166,3 +166,21 @@ def test_slab_pcg_two_ranks_matches_one(tmp_path, single):
          b * (np.kron(Mz, np.kron(My, Kx)) + np.kron(Mz, np.kron(Ky, Mx)) +
               np.kron(Kz, np.kron(My, Mx))))
     assert np.linalg.norm(A @ x2 - rhs) / np.linalg.norm(rhs) <= 1e-11
+
+
+def _points_rank(d: Dist, n):
+    from paper_2511_20432_b200.parallel import sharded_points
+    f = lambda b, e: torch.arange(b, e, dtype=torch.float64) * 0.5 + 1.0  # noqa: E731
+    return {"all": sharded_points(f, n, d).numpy(), "own": sharded_points(f, n, d, gather=False).numpy()}
+
+
+@pytest.mark.parametrize("n", [0, 7, 66564])
+def test_sharded_points_two_ranks(tmp_path, n):
+    """Point slabs (the Dirichlet values of ShardedTimeLoop) all-gathered in
+    rank order reproduce the single evaluation."""
+    outs = _run(2, _points_rank, tmp_path, n)
+    ref = np.arange(n, dtype=np.float64) * 0.5 + 1.0
+    for r, o in enumerate(outs):
+        assert np.array_equal(o["all"], ref)
+        b, e = partition(n, 2, r)
+        assert np.array_equal(o["own"], ref[b:e])

@@ -391,3 +391,36 @@ def test_stepping_and_quadrature_variants_against_live_reference(edit, ref, tmp_
         assert normwise(st["free"], o["free"]) <= 1e-8, k
     s.close()
     r.close()
+
+
+def test_sharded_time_loop_single_rank_matches_advance():
+    """parallel.ShardedTimeLoop (sharded flux/Dirichlet + all-gather + the
+    replicated theta step) on one rank over NCCL reproduces advance() bit for
+    bit over 20 steps (the multi-rank logic is the gloo-tested sharding)."""
+    import socket
+    import torch.distributed as dist
+    from paper_2511_20432_b200 import parallel
+    a = tg.Simulation(cfg("cfg0_parity"))
+    b = tg.Simulation(cfg("cfg0_parity"))
+    sock = socket.socket()
+    sock.bind(("127.0.0.1", 0))
+    port = sock.getsockname()[1]
+    sock.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1)
+    try:
+        loop = parallel.ShardedTimeLoop(a, parallel.Dist(0, 1, "cuda"))
+        loop.reset()
+        b.reset()
+        for _ in range(20):
+            it_a, _ = loop.step()
+            it_b, _ = b.advance(1)
+            assert it_a == it_b
+        sa, sb = a.state(), b.state()
+        assert sa["step"] == sb["step"] == 20
+        for k in ("free", "g", "F"):
+            assert np.array_equal(sa[k], sb[k]), k
+    finally:
+        dist.destroy_process_group()
+        a.close()
+        b.close()
