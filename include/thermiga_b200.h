@@ -73,7 +73,9 @@ void tg_ctx_destroy(tg_ctx* ctx);
 const char* tg_last_error(const tg_ctx* ctx);
 /* Kernel-level profiling: when on, the main K1/K2 kernels are bracketed by
  * CUDA events; tg_profile_read returns the summed milliseconds since the last
- * reset, the number of this library's kernel launches, and the work counted. */
+ * reset, the number of this library's kernel launches, and the work counted:
+ * out = {k1_ms, k1_launches, k1_pairs, k2_ms (solve), k2_launches, k2_bytes,
+ *        launches, theta_step_ms (expand + RHS + solve)}. */
 int tg_set_profiling(tg_ctx* ctx, int on);
 int tg_profile_read(tg_ctx* ctx, double* out /* [8] */, int reset);
 /* FP64 issue-rate microbenchmark (independent DFMA chains over every SM);

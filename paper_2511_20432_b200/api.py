@@ -206,7 +206,8 @@ class Context:
         out = np.zeros(8)
         self._check(self._L.tg_profile_read(self._h, _p(out), int(reset)))
         return dict(k1_ms=out[0], k1_launches=int(out[1]), k1_pairs=out[2], k2_ms=out[3],
-                    k2_launches=int(out[4]), k2_bytes=out[5], launches=int(out[6]))
+                    k2_launches=int(out[4]), k2_bytes=out[5], launches=int(out[6]),
+                    theta_step_ms=out[7])
 
     @staticmethod
     def _csr(A):

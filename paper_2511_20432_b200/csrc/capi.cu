@@ -184,7 +184,7 @@ int tg_profile_read(tg_ctx* ctx, double* out, int reset) {
     out[4] = static_cast<double>(ctx->timer.k2_launches);
     out[5] = ctx->timer.k2_bytes;
     out[6] = static_cast<double>(ctx->timer.launches);
-    out[7] = 0.0;
+    out[7] = ctx->timer.step_ms;  // whole theta steps (expand + RHS + solve)
     if (reset) ctx->timer.reset();
   });
 }

@@ -492,6 +492,25 @@ void Sim::dirichlet_device(double t, double* d_g, int c0, int c1) {
 PcgStatus Sim::theta_step_device(double tol, int max_iter) {
   cudaStream_t s = ctx->stream;
   if (!diag_ok) throw numeric_error("pcg: non-positive diagonal, matrix not SPD");
+  ctx->timer.timed(3, s, [&] { theta_step_launch(tol, max_iter); });
+  TG_CUDA(cudaMemcpyAsync(h_status, d_status.p, sizeof(PcgStatus), cudaMemcpyDeviceToHost, s));
+  TG_CUDA(cudaStreamSynchronize(s));
+  const PcgStatus st = *h_status;
+  ctx->timer.k2_bytes += 104.0 * n_free * st.iterations;  // SURVEY.md §8d algorithmic bytes
+  k2_iterations += st.iterations;
+  if (st.status == 4) throw numeric_error("pcg: indefinite direction, matrix not SPD");
+  if (st.status == 3) {
+    char buf[64];
+    std::snprintf(buf, sizeof(buf), "%.17g", st.rel_residual);
+    throw numeric_error("pcg: no convergence in " + std::to_string(max_iter) +
+                        " iterations, relative residual " + buf);
+  }
+  return st;
+}
+
+// expand, RHS and the solve on the stream (theta_step, timestep.cpp:5-24)
+void Sim::theta_step_launch(double tol, int max_iter) {
+  cudaStream_t s = ctx->stream;
   const int threads = 256;
   expand_kernel<<<static_cast<int>((n_full + threads - 1) / threads), threads, 0, s>>>(
       geom, d_x.p, d_gn.p, d_T.p);
@@ -538,19 +557,6 @@ PcgStatus Sim::theta_step_device(double tol, int max_iter) {
   }
   ++ctx->timer.launches;
   ++ctx->timer.k2_launches;
-  TG_CUDA(cudaMemcpyAsync(h_status, d_status.p, sizeof(PcgStatus), cudaMemcpyDeviceToHost, s));
-  TG_CUDA(cudaStreamSynchronize(s));
-  const PcgStatus st = *h_status;
-  ctx->timer.k2_bytes += 104.0 * n_free * st.iterations;  // SURVEY.md §8d algorithmic bytes
-  k2_iterations += st.iterations;
-  if (st.status == 4) throw numeric_error("pcg: indefinite direction, matrix not SPD");
-  if (st.status == 3) {
-    char buf[64];
-    std::snprintf(buf, sizeof(buf), "%.17g", st.rel_residual);
-    throw numeric_error("pcg: no convergence in " + std::to_string(max_iter) +
-                        " iterations, relative residual " + buf);
-  }
-  return st;
 }
 
 void Sim::reset() {

@@ -53,6 +53,7 @@ class Sim {
   void flux_gather_device(const double* d_loc_all, double* d_F);
   void dirichlet_device(double t, double* d_g, int c0 = 0, int c1 = -1);
   PcgStatus theta_step_device(double tol, int max_iter);  // uses d_x, d_gn, d_g1, d_Fn, d_F1
+  void theta_step_launch(double tol, int max_iter);      // its launches (no status read)
 
   // observers: the current state at parametric points, on
   // device buffers: d_out (n x 12) = x, T_total, T_tilde, T_hat, grad T_tilde,

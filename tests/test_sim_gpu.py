@@ -142,6 +142,21 @@ def test_deterministic_reruns(sim):
         assert np.array_equal(a[k], b[k])
 
 
+def test_step_profile_counters(sim):
+    """Profiling brackets the solve (kind 2) inside the whole theta step (kind 3)."""
+    name, s = sim
+    ctx = s.context()
+    s.reset()
+    ctx.set_profiling(True)
+    ctx.profile(reset=True)
+    s.advance(3)
+    p = ctx.profile()
+    ctx.set_profiling(False)
+    assert p["k2_launches"] == 3
+    assert 0.0 < p["k2_ms"] <= p["theta_step_ms"]
+    assert p["k1_ms"] > 0.0
+
+
 def test_pcg_error_paths(sim):
     name, s = sim
     g = golden(name)
