@@ -58,7 +58,7 @@ PIPE_OPS_PER_PAIR_PLANAR = 15.0
 # DRAM bytes (read + write) per launch from one `ncu --set full` capture of each
 # dominant kernel (profiles/r01_k1_ncu_summary.md, r01_k2_ncu_summary.md)
 K1_TRAFFIC_BYTES = 92.2e6 + 484.4e6   # k1_partial<7,1,1>, config 1, one launch
-K2_TRAFFIC_B_PER_DOF_ITER = 88.0      # k2_cg1_kernel<2>, config 4 (15.62 + 12.56 GB / 74 sweeps)
+K2_TRAFFIC_B_PER_DOF_ITER = 80.0      # k2_cg1_kernel<2> (scaled), config 4 (13.06 + 12.56 GB / 74 sweeps)
 
 
 def parse():
@@ -304,8 +304,8 @@ def theta_section(steps, warmup, with_cpu):
                      "frac": achieved / peak if achieved else None,
                      "traffic": (K2_TRAFFIC_B_PER_DOF_ITER * sim.info["n_free"] * iters / steps
                                  if sim.info["kronecker"] == 2 else None),
-                     "traffic_source": "ncu --set full, profiles/r01_k2_cg1_full.ncu-rep: "
-                                       "88 B/DOF/iteration measured, per solve",
+                     "traffic_source": "ncu --set full, profiles/r01_k2_cg1s_full.ncu-rep: "
+                                       "80 B/DOF/iteration measured, per solve",
                      "peak_source": src,
                      "bytes_per_dof_per_iteration": 104},
     }

@@ -15,8 +15,8 @@ sys.path.insert(0, ROOT)
 VDIR = os.path.join(ROOT, "paper_2511_20432_b200", "_lib", "variants_k2")
 
 VARIANTS = {
-    "tx32_ty8": dict(K2_TX=32, K2_TY=8),
-    "tx16_ty16": dict(K2_TX=16, K2_TY=16, K2_MINB=2),
+    "base": dict(),
+    "zsplit": dict(K2_ZSPLIT=1),
 }
 
 
