@@ -144,6 +144,12 @@ int tg_sim_greville_points(tg_sim* sim, double* out_xyz);
 /* Banded 1D factors of the Kronecker operator for axis dir (n x (2p+1),
  * [i][p + j - i]); TG_ERROR when the patch is not separable. */
 int tg_sim_kron_factors(tg_sim* sim, int dir, double* M, double* K);
+/* DirichletSystem::reduced_operator() (proj/include/thermiga/assembly.hpp:56,
+ * proj/src/assembly.cpp:201-228) of a non-separable patch as assembled on the
+ * host (bit-identical to the reference's): returns nnz (pass NULL arrays to
+ * query), or -status (TG_ERROR for separable patches, whose operator is never
+ * assembled). */
+long tg_sim_reduced_operator(tg_sim* sim, int* rows, int* row_ptr, int* col, double* val);
 
 /* assemble_flux_load (proj/src/assembly.cpp:148-166): F (n_full) at time t;
  * fine_radius < 0 uses the config's elevate_radius. */
@@ -220,6 +226,17 @@ int tg_csr_multiply(tg_ctx* ctx, int rows, const int* row_ptr, const int* col, c
  * V: n x n column-major. */
 int tg_fdm_factor(const double* Mband, const double* Kband, int n_band, int p, int first, int n,
                   double* V, double* lam);
+
+/* Geometry tooling (not in the reference):
+ * read a geometry file (the reference's [geometry] format or `case =`,
+ * proj/src/config.cpp:171-215), scale the control coordinates per axis
+ * (scale[3], NULL = none), elevate the degree exactly by elevate[3] per
+ * direction (Bezier extraction + Bernstein elevation on homogeneous points;
+ * interior breakpoints end with multiplicity p + t, i.e. C0), and write the
+ * result as a geometry file the reference reads. On failure the message is
+ * copied to err (err_len bytes). */
+int tg_geometry_elevate(const char* in_path, const int* elevate, const double* scale,
+                        const char* out_path, char* err, int err_len);
 
 /* ---- observers (proj/src/postproc.cpp, driver.cpp:226-254) --
  * The current state (after reset/advance, time = step * dt) at parametric

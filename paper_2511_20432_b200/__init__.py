@@ -6,9 +6,11 @@ binding and the seeded BASELINE workloads.
 """
 from .api import (ConfigError, Context, CudaError, LaserSpec, Material, NumericError, ScanPath,
                   Simulation,
-                  SuperposeOptions, ThermigaError, discretize_scan, export_profile_csv,
+                  SuperposeOptions, ThermigaError, discretize_scan, elevate_geometry,
+                  export_profile_csv,
                   integrated_abs_flux, lib, superpose)
 
 __all__ = ["ConfigError", "Context", "CudaError", "LaserSpec", "Material", "NumericError",
            "ScanPath", "Simulation", "SuperposeOptions", "ThermigaError", "discretize_scan",
+           "elevate_geometry",
            "export_profile_csv", "integrated_abs_flux", "lib", "superpose"]

@@ -139,6 +139,7 @@ def lib(auto_build: bool = True):
     L.tg_superpose_batch.argtypes = [C.c_void_p, _dp, C.c_long, C.c_double, C.c_double, _dp, _dp]
     L.tg_superpose_batch_device.argtypes = [C.c_void_p, C.c_void_p, C.c_long, C.c_double,
                                             C.c_double, C.c_void_p, C.c_void_p, C.c_void_p]
+    L.tg_geometry_elevate.argtypes = [C.c_char_p, _ip, _dp, C.c_char_p, C.c_char_p, C.c_int]
     _LIB = L
     return L
 
@@ -164,6 +165,21 @@ def discretize_scan(path: ScanPath, laser: LaserSpec, mat: Material) -> np.ndarr
     L.tg_discretize_scan(_p(wp), len(wp), path.start_time, path.plane_z, C.byref(las),
                          C.byref(m), _p(out), n)
     return out
+
+
+def elevate_geometry(in_path: str, out_path: str, elevate=(0, 0, 0), scale=None) -> None:
+    """Geometry tooling for config 3 (SURVEY.md §8f item 4, Appendix C option A):
+    read a geometry file in the reference's format, scale the control
+    coordinates per axis, elevate the degree exactly, write a geometry file
+    (tg_geometry_elevate)."""
+    L = lib()
+    t = np.ascontiguousarray(elevate, dtype=np.int32)
+    sc = None if scale is None else _f64(scale)
+    err = C.create_string_buffer(512)
+    rc = L.tg_geometry_elevate(os.fsencode(in_path), t.ctypes.data_as(_ip), _p(sc),
+                               os.fsencode(out_path), err, len(err))
+    if rc != 0:
+        raise _ERRORS.get(rc, ThermigaError)(err.value.decode())
 
 
 class Context:
@@ -337,6 +353,8 @@ def _bind_sim(L):
     L.tg_sim_face_sets.argtypes = [C.c_void_p, _ip, _ip, _dp, _ip, _dp, _dp, _dp, _dp, _dp]
     L.tg_sim_greville_points.argtypes = [C.c_void_p, _dp]
     L.tg_sim_kron_factors.argtypes = [C.c_void_p, C.c_int, _dp, _dp]
+    L.tg_sim_reduced_operator.argtypes = [C.c_void_p, _ip, _ip, _ip, _dp]
+    L.tg_sim_reduced_operator.restype = C.c_long
     L.tg_sim_flux_load.argtypes = [C.c_void_p, C.c_double, C.c_double, _dp]
     L.tg_sim_dirichlet_values.argtypes = [C.c_void_p, C.c_double, _dp]
     L.tg_sim_theta_step.argtypes = [C.c_void_p, _dp, _dp, _dp, _dp, _dp, C.c_double, C.c_int,
@@ -472,6 +490,20 @@ class Simulation:
         self._check(self._L.tg_sim_theta_step(self._h, *[_p(v) for v in a], float(tol),
                                               int(max_iter), _p(out), C.byref(it), C.byref(rel)))
         return out, it.value, rel.value
+
+    def reduced_operator(self):
+        """(row_ptr, col, val) of the assembled reduced operator A_ff
+        (non-separable patches; DirichletSystem::reduced_operator)."""
+        rows = C.c_int(0)
+        nnz = self._L.tg_sim_reduced_operator(self._h, C.byref(rows), None, None, None)
+        if nnz < 0:
+            raise _ERRORS.get(-nnz, ThermigaError)(self._L.tg_sim_last_error(self._h).decode())
+        rp = np.zeros(rows.value + 1, dtype=np.int32)
+        ci = np.zeros(nnz, dtype=np.int32)
+        v = np.zeros(nnz)
+        self._L.tg_sim_reduced_operator(self._h, None, rp.ctypes.data_as(_ip),
+                                        ci.ctypes.data_as(_ip), _p(v))
+        return rp, ci, v
 
     def operator_apply(self, x):
         xx = _f64(x)

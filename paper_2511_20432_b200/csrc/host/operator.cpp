@@ -1,7 +1,12 @@
 #include "operator.hpp"
 
+#include "parallel.hpp"
+
 #include <algorithm>
+#include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 
 namespace tgb {
 
@@ -109,51 +114,131 @@ Csr tensor_pattern(const NurbsVolume& vol) {
   return m;
 }
 
-double& at(Csr& m, int r, int c) {
-  auto b = m.col.begin() + m.row_ptr[r], e = m.col.begin() + m.row_ptr[r + 1];
-  auto it = std::lower_bound(b, e, c);
-  if (it == e || *it != c) throw std::out_of_range("entry not in sparsity pattern");
-  return m.val[it - m.col.begin()];
-}
 
 }  // namespace
 
+// Element matrices are formed in parallel in batches of consecutive elements;
+// the scatter is parallel over the tensor index i of the row (each worker owns
+// a range of i and walks the batch in element order), so every entry still
+// receives its element contributions in element order, with the reference's
+// per-element arithmetic (assembly.cpp:59-101): the values are bit-identical
+// to a serial assembly for any thread count. CSR slots come from the tensor
+// pattern directly (no search).
 void assemble_mass_stiffness(const NurbsVolume& vol, std::array<int, 3> nq, const Material& mat,
                              Csr& M, Csr& K) {
   M = tensor_pattern(vol);
   K = M;
   const ElementGrid eg = element_grid(vol);
-  ElementQuad quad;
-  std::vector<double> lm, lk;
-  for (int e = 0; e < eg.count(); ++e) {
-    element_quad(vol, eg, e, nq, quad);
-    const int nb = quad.n_basis;
-    lm.assign(static_cast<size_t>(nb) * nb, 0.0);
-    lk.assign(static_cast<size_t>(nb) * nb, 0.0);
-    for (int q = 0; q < quad.n_qp; ++q) {
-      const double wm = mat.volumetric_capacity() * quad.weight[q];
-      const double wk = mat.conductivity * quad.weight[q];
-      const double* N = &quad.N[static_cast<size_t>(q) * nb];
-      const Vec3* G = &quad.dN[static_cast<size_t>(q) * nb];
-      for (int a = 0; a < nb; ++a)
-        for (int b = 0; b <= a; ++b) {
-          lm[static_cast<size_t>(a) * nb + b] += wm * N[a] * N[b];
-          lk[static_cast<size_t>(a) * nb + b] += wk * G[a].dot(G[b]);
+  const auto n = vol.basis_counts();
+  const auto pd = vol.degrees();
+  const int ne = eg.count();
+  constexpr int kBatch = 2048;
+  struct Local {
+    int nb = 0;
+    std::vector<int> dofs;
+    std::vector<std::array<int, 3>> ijk;
+    std::vector<double> lm, lk;  // nb x nb, lower triangle used
+  };
+  std::vector<Local> loc(std::min(kBatch, std::max(ne, 1)));
+  const int nth = std::max(1, std::min(host_threads(), n[0]));
+  double t_loc = 0.0, t_sc = 0.0;
+  for (int e0 = 0; e0 < ne; e0 += kBatch) {
+    auto c0 = std::chrono::steady_clock::now();
+    const int nbt = std::min(kBatch, ne - e0);
+    parallel_for(nbt, [&](long t) {
+      thread_local ElementQuad quad;
+      element_quad(vol, eg, e0 + static_cast<int>(t), nq, quad);
+      Local& L = loc[t];
+      const int nb = L.nb = quad.n_basis;
+      L.dofs.assign(quad.dofs.begin(), quad.dofs.end());
+      L.ijk.resize(nb);
+      for (int a = 0; a < nb; ++a) {
+        const int f = L.dofs[a];
+        L.ijk[a] = {f % n[0], (f / n[0]) % n[1], f / (n[0] * n[1])};
+      }
+      L.lm.assign(static_cast<size_t>(nb) * nb, 0.0);
+      L.lk.assign(static_cast<size_t>(nb) * nb, 0.0);
+      // the reference's expressions, wm * N[a] * N[b] and wk * (G[a].dot(G[b])),
+      // with (wm * N[a]) hoisted and G split by component so the b loop
+      // vectorizes; same roundings in the same order
+      thread_local std::vector<double> gx, gy, gz;
+      gx.resize(nb);
+      gy.resize(nb);
+      gz.resize(nb);
+      double* __restrict lm = L.lm.data();
+      double* __restrict lk = L.lk.data();
+      for (int q = 0; q < quad.n_qp; ++q) {
+        const double wm = mat.volumetric_capacity() * quad.weight[q];
+        const double wk = mat.conductivity * quad.weight[q];
+        const double* __restrict N = &quad.N[static_cast<size_t>(q) * nb];
+        const Vec3* G = &quad.dN[static_cast<size_t>(q) * nb];
+        for (int a = 0; a < nb; ++a) {
+          gx[a] = G[a].x;
+          gy[a] = G[a].y;
+          gz[a] = G[a].z;
         }
-    }
-    // deterministic scatter in element order, symmetric by construction
-    for (int a = 0; a < nb; ++a)
-      for (int b = 0; b <= a; ++b) {
-        const double vm = lm[static_cast<size_t>(a) * nb + b];
-        const double vk = lk[static_cast<size_t>(a) * nb + b];
-        at(M, quad.dofs[a], quad.dofs[b]) += vm;
-        at(K, quad.dofs[a], quad.dofs[b]) += vk;
-        if (a != b) {
-          at(M, quad.dofs[b], quad.dofs[a]) += vm;
-          at(K, quad.dofs[b], quad.dofs[a]) += vk;
+        const double* __restrict X = gx.data();
+        const double* __restrict Y = gy.data();
+        const double* __restrict Z = gz.data();
+        for (int a = 0; a < nb; ++a) {
+          const double ma = wm * N[a];
+          const double xa = X[a], ya = Y[a], za = Z[a];
+          double* __restrict rm = lm + static_cast<size_t>(a) * nb;
+          double* __restrict rk = lk + static_cast<size_t>(a) * nb;
+          for (int b = 0; b <= a; ++b) {
+            rm[b] += ma * N[b];
+            rk[b] += wk * (xa * X[b] + ya * Y[b] + za * Z[b]);
+          }
         }
       }
+    }, 8);
+    auto c1 = std::chrono::steady_clock::now();
+    t_loc += std::chrono::duration<double>(c1 - c0).count();
+    parallel_for(nth, [&](long T) {
+      const int i0 = static_cast<int>(static_cast<long>(n[0]) * T / nth);
+      const int i1 = static_cast<int>(static_cast<long>(n[0]) * (T + 1) / nth);
+      // slot of column c in the pattern row of r (tensor_pattern's order)
+      auto slot = [&](int r, const std::array<int, 3>& ri, const std::array<int, 3>& ci) {
+        int lo[3], w[3];
+        for (int d = 0; d < 3; ++d) {
+          lo[d] = std::max(0, ri[d] - pd[d]);
+          w[d] = std::min(n[d] - 1, ri[d] + pd[d]) - lo[d] + 1;
+        }
+        return M.row_ptr[r] + ((ci[2] - lo[2]) * w[1] + (ci[1] - lo[1])) * w[0] + (ci[0] - lo[0]);
+      };
+      for (int t = 0; t < nbt; ++t) {
+        const Local& L = loc[t];
+        const int nb = L.nb;
+        int imin = n[0], imax = -1;
+        for (int a = 0; a < nb; ++a) {
+          imin = std::min(imin, L.ijk[a][0]);
+          imax = std::max(imax, L.ijk[a][0]);
+        }
+        if (imax < i0 || imin >= i1) continue;
+        for (int a = 0; a < nb; ++a) {
+          const bool own_a = L.ijk[a][0] >= i0 && L.ijk[a][0] < i1;
+          for (int b = 0; b <= a; ++b) {
+            const bool own_b = L.ijk[b][0] >= i0 && L.ijk[b][0] < i1;
+            if (!own_a && !own_b) continue;
+            const double vm = L.lm[static_cast<size_t>(a) * nb + b];
+            const double vk = L.lk[static_cast<size_t>(a) * nb + b];
+            if (own_a) {
+              const int sl = slot(L.dofs[a], L.ijk[a], L.ijk[b]);
+              M.val[sl] += vm;
+              K.val[sl] += vk;
+            }
+            if (a != b && own_b) {
+              const int sl = slot(L.dofs[b], L.ijk[b], L.ijk[a]);
+              M.val[sl] += vm;
+              K.val[sl] += vk;
+            }
+          }
+        }
+      }
+    }, 1);
+    t_sc += std::chrono::duration<double>(std::chrono::steady_clock::now() - c1).count();
   }
+  if (std::getenv("TG_SETUP_TIMING")) std::fprintf(stderr, "[setup]   element matrices %.3f s, scatter %.3f s\n", t_loc, t_sc);
 }
 
 }  // namespace tgb

@@ -108,6 +108,14 @@ class NurbsVolume {
 
 NurbsVolume quarter_cylinder_part();
 
+// Geometry tooling (not in the reference): exact degree
+// elevation by t[d] per direction, an optional per-axis scaling of the control
+// coordinates, and the reference's geometry-file text ([geometry] degrees,
+// knots_*, grid_dims, cp lines; proj/src/config.cpp:171-215).
+NurbsVolume elevate_degree(const NurbsVolume& vol, std::array<int, 3> t);
+NurbsVolume scaled(const NurbsVolume& vol, std::array<double, 3> s);
+std::string geometry_text(const NurbsVolume& vol);
+
 std::vector<double> graded_refinement_knots(const KnotVector& kv, int target_elements,
                                             double ratio, double focus);
 

@@ -211,46 +211,48 @@ void Sim::setup_host() {
   } else {
     Csr M, K;
     assemble_mass_stiffness(vol, quad, cfg.material, M, K);
+    clk.mark("csr assembly (M, K)");
     // A = M/dt + theta K, B = M/dt - (1-theta) K (assembly.cpp:194-199)
-    Csr A = M, B = M;
-    for (size_t i = 0; i < M.val.size(); ++i) {
-      A.val[i] = (1.0 / dt) * M.val[i] + th * K.val[i];
-      B.val[i] = (1.0 / dt) * M.val[i] + -(1.0 - th) * K.val[i];
-    }
-    auto extract = [&](const Csr& S, bool free_cols, Csr& out) {
+    const long nnz = static_cast<long>(M.val.size());
+    std::vector<double> Av(nnz), Bv(nnz);
+    parallel_for((nnz + 4095) / 4096, [&](long blk) {
+      const long e = std::min(nnz, (blk + 1) * 4096);
+      for (long i2 = blk * 4096; i2 < e; ++i2) {
+        Av[i2] = (1.0 / dt) * M.val[i2] + th * K.val[i2];
+        Bv[i2] = (1.0 / dt) * M.val[i2] + -(1.0 - th) * K.val[i2];
+      }
+    }, 1);
+    // free rows of the pattern with values v; columns renumbered by `map`
+    // (entries with map < 0 dropped; all kept when map is null): count,
+    // prefix, fill, row-parallel
+    auto extract = [&](const std::vector<double>& v, const std::vector<int>* map, Csr& out) {
+      const Csr& S = M;  // the shared pattern
       out.rows = n_free;
       out.row_ptr.assign(n_free + 1, 0);
-      out.col.clear();
-      out.val.clear();
-      for (int f = 0; f < n_free; ++f) {
+      parallel_for(n_free, [&](long f) {
         const int r = dofs.free_list[f];
+        int c = 0;
+        for (int q = S.row_ptr[r]; q < S.row_ptr[r + 1]; ++q) c += !map || (*map)[S.col[q]] >= 0;
+        out.row_ptr[f + 1] = c;
+      }, 256);
+      for (int f = 0; f < n_free; ++f) out.row_ptr[f + 1] += out.row_ptr[f];
+      out.col.resize(out.row_ptr[n_free]);
+      out.val.resize(out.row_ptr[n_free]);
+      parallel_for(n_free, [&](long f) {
+        const int r = dofs.free_list[f];
+        int o = out.row_ptr[f];
         for (int q = S.row_ptr[r]; q < S.row_ptr[r + 1]; ++q) {
-          const int c = S.col[q];
-          if (free_cols) {
-            if (dofs.free_index[c] >= 0) {
-              out.col.push_back(dofs.free_index[c]);
-              out.val.push_back(S.val[q]);
-            }
-          } else if (dofs.constrained_index[c] >= 0) {
-            out.col.push_back(dofs.constrained_index[c]);
-            out.val.push_back(S.val[q]);
-          }
+          const int c = map ? (*map)[S.col[q]] : S.col[q];
+          if (c < 0) continue;
+          out.col[o] = c;
+          out.val[o++] = v[q];
         }
-        out.row_ptr[f + 1] = static_cast<int>(out.col.size());
-      }
+      }, 256);
     };
-    extract(A, true, csrA);
-    extract(A, false, csrAc);
-    csrB.rows = n_free;  // free rows of B, all columns
-    csrB.row_ptr.assign(n_free + 1, 0);
-    for (int f = 0; f < n_free; ++f) {
-      const int r = dofs.free_list[f];
-      for (int q = B.row_ptr[r]; q < B.row_ptr[r + 1]; ++q) {
-        csrB.col.push_back(B.col[q]);
-        csrB.val.push_back(B.val[q]);
-      }
-      csrB.row_ptr[f + 1] = static_cast<int>(csrB.col.size());
-    }
+    extract(Av, &dofs.free_index, csrA);
+    extract(Av, &dofs.constrained_index, csrAc);
+    extract(Bv, nullptr, csrB);  // free rows of B, all columns
+    clk.mark("csr theta operators");
   }
 }
 

@@ -1,6 +1,8 @@
 // C ABI of the simulation engine: tg_sim_* (include/thermiga_b200.h).
 #include <cstring>
+#include <fstream>
 
+#include "host/config.hpp"
 #include "host/fdm.hpp"
 #include "sim.hpp"
 
@@ -96,6 +98,20 @@ int tg_sim_kron_factors(tg_sim* s, int dir, double* M, double* K) {
     std::memcpy(M, m.band[dir].M.data(), m.band[dir].M.size() * sizeof(double));
     std::memcpy(K, m.band[dir].K.data(), m.band[dir].K.size() * sizeof(double));
   }, false);
+}
+
+long tg_sim_reduced_operator(tg_sim* s, int* rows, int* row_ptr, int* col, double* val) {
+  long nnz = -TG_ERROR;
+  const int rc = sim_guard(s, [&](Sim& m) {
+    if (m.kron) throw std::invalid_argument("separable patch: the operator is not assembled");
+    const Csr& A = m.csrA;
+    if (rows) *rows = A.rows;
+    if (row_ptr) std::memcpy(row_ptr, A.row_ptr.data(), A.row_ptr.size() * sizeof(int));
+    if (col) std::memcpy(col, A.col.data(), A.col.size() * sizeof(int));
+    if (val) std::memcpy(val, A.val.data(), A.val.size() * sizeof(double));
+    nnz = static_cast<long>(A.val.size());
+  }, false);
+  return rc == TG_OK ? nnz : -rc;
 }
 
 int tg_sim_context(tg_sim* s, tg_ctx** out) {
@@ -313,6 +329,34 @@ int tg_fdm_factor(const double* Mband, const double* Kband, int n_band, int p, i
     return TG_OK;
   } catch (const std::exception&) {
     return TG_ERROR;
+  }
+}
+
+int tg_geometry_elevate(const char* in_path, const int* elevate, const double* scale,
+                        const char* out_path, char* err, int err_len) {
+  auto fail = [&](int code, const char* msg) {
+    if (err && err_len > 0) {
+      std::strncpy(err, msg, static_cast<size_t>(err_len) - 1);
+      err[err_len - 1] = '\0';
+    }
+    return code;
+  };
+  try {
+    if (!in_path || !out_path) throw std::invalid_argument("geometry_elevate: null path");
+    NurbsVolume v = read_geometry_file(in_path);
+    if (scale) v = scaled(v, {scale[0], scale[1], scale[2]});
+    if (elevate) v = elevate_degree(v, {elevate[0], elevate[1], elevate[2]});
+    std::ofstream out(out_path);
+    if (!out) throw io_error(std::string("cannot write '") + out_path + "'");
+    out << "# written by tg_geometry_elevate (exact degree elevation)\n" << geometry_text(v);
+    if (!out) throw io_error(std::string("cannot write '") + out_path + "'");
+    return TG_OK;
+  } catch (const config_error& e) {
+    return fail(TG_ECONFIG, e.what());
+  } catch (const io_error& e) {
+    return fail(TG_EIO, e.what());
+  } catch (const std::exception& e) {
+    return fail(TG_ERROR, e.what());
   }
 }
 

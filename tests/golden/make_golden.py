@@ -53,7 +53,7 @@ if __name__ == "__main__":
 
 
 SIM_STEPS = {"cfg0_parity": [1, 2, 3, 5, 10, 25, 50, 75, 100], "qc_small": [1, 2, 5, 12, 24],
-             "cfg0_oddx": [1, 2, 10, 40]}
+             "cfg0_oddx": [1, 2, 10, 40], "cfg3_parity": [1, 2, 5, 10, 20, 40]}
 
 
 def sim_run(R, name):
@@ -87,5 +87,5 @@ def sim_run(R, name):
 
 if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "sim":
     R = pyoracle.RefLib()
-    for name in SIM_STEPS:
+    for name in (sys.argv[2:] or SIM_STEPS):
         sim_run(R, name)

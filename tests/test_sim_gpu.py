@@ -17,7 +17,7 @@ import paper_2511_20432_b200 as tg
 from conftest import GOLDEN, ROOT
 
 pytestmark = pytest.mark.gpu
-NAMES = ["cfg0_parity", "qc_small", "cfg0_oddx"]
+NAMES = ["cfg0_parity", "qc_small", "cfg0_oddx", "cfg3_parity"]
 
 
 def cfg(name):
