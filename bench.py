@@ -180,6 +180,7 @@ def cpu_baseline(src, t, budget_s, threads=None):
 
 THETA_CFG = os.path.join(ROOT, "configs", "cfg4_large.cfg")
 THETA_CPU_CFG = os.path.join(ROOT, "configs", "cfg2_raster_layer.cfg")
+CFG3 = os.path.join(ROOT, "configs", "cfg3_contour_hatch.cfg")
 HBM_PEAK_FALLBACK = 6555.2
 
 
@@ -211,6 +212,73 @@ def theta_cpu_baseline():
     return {"ms_per_step_per_mdof": secs * 1e3 / (dofs / 1e6), "cg_iterations": iters,
             "cores": 1, "kind": "reference",
             "sample": f"one theta_step of config 2 ({dofs} DOF) at t = 0.02 s, cold start"}
+
+
+def config3_steps(with_cpu, steps=10):
+    """Config 3 (degree-3 rational plate-with-hole part, 128x64x32 elements,
+    302,974 free DOF; SURVEY.md Appendix C option A): the assembled-operator
+    path. `steps` time steps from the start (contour scan) on the device; the
+    reference's own pcg_jacobi timed beside it on the identical A_ff for a
+    bounded number of iterations."""
+    import paper_2511_20432_b200 as tg
+    t0 = time.perf_counter()
+    sim = tg.Simulation(CFG3)
+    setup_s = time.perf_counter() - t0
+    ctx = sim.context()
+    sim.reset()
+    sim.advance(1)
+    ctx.set_profiling(True)
+    ctx.profile(reset=True)
+    t0 = time.perf_counter()
+    iters, rel = sim.advance(steps)
+    wall = time.perf_counter() - t0
+    prof = ctx.profile()
+    ctx.set_profiling(False)
+    rp, ci, v = sim.reduced_operator()
+    n, nnz = len(rp) - 1, len(v)
+    peak, src = hbm_peak()
+    us_it = 1e3 * prof["k2_ms"] / max(1, iters)
+    # per CG iteration: A_ff once (8 B value + 4 B column per entry) and the
+    # vectors p (r), Ap (w, r), x (r, w), r (r, w), D^-1 (r, twice), p (r, w)
+    alg_bytes = 12.0 * nnz + 8.0 * n * 11
+    achieved = alg_bytes / (us_it * 1e-6) / 1e9
+    out = {"workload": "config3: degree-(3,3,3) rational plate-with-hole part (Appendix C "
+                       "option A), 128x64x32 elements, 311,885 DOF (302,974 free), contour + "
+                       f"hatch path; steps 2..{steps + 1} of the 5000-step run",
+           "setup_s": setup_s, "steps": steps, "ms_per_step": wall * 1e3 / steps,
+           "theta_ms_per_step": prof["k2_ms"] / steps,
+           "theta_step_total_ms_per_step": prof["theta_step_ms"] / steps,
+           "theta_ms_per_step_per_mdof": prof["k2_ms"] / steps / (sim.info["n_full"] / 1e6),
+           "cg_iterations_per_step": iters / steps, "us_per_cg_iteration": us_it,
+           "operator": "assembled A_ff in sliced ELL (32-row slices), one thread per row, "
+                       "row sums in the reference's CSR order (bit-exact rows)",
+           "nnz": nnz,
+           "roofline": {"kernel": "csr_pcg_kernel<DevSell>", "bound": "hbm",
+                        "achieved": achieved, "peak": peak, "unit": "GB/s",
+                        "frac": achieved / peak, "peak_source": src,
+                        "bytes_per_iteration": alg_bytes,
+                        "bytes_note": "12 B per A_ff entry + 11 vector streams of 8 B/DOF"}}
+    sim.close()
+    if with_cpu:
+        from oracle import pyoracle
+        if pyoracle.ref_available():
+            R = pyoracle.RefLib()
+            b = np.random.default_rng(3).standard_normal(n)
+            k = 8
+            c0 = time.perf_counter()
+            try:
+                R.pcg(rp, ci, v, b, np.zeros(n), tol=1e-30, max_iter=k)
+            except pyoracle.RefError:
+                pass  # the cap: k iterations done
+            secs = time.perf_counter() - c0
+            ms_it = secs * 1e3 / (k + 1)  # k iterations + the initial residual matvec
+            out["cpu_baseline"] = {"ms_per_cg_iteration": ms_it, "kind": "reference",
+                                   "cores": 1,
+                                   "sample": f"pcg_jacobi (proj/src/sparse.cpp:41-100, serial "
+                                             f"as shipped) on the identical A_ff, capped at {k} "
+                                             "iterations (time / (k + 1))",
+                                   "theta_ms_per_step_estimate": ms_it * iters / steps}
+    return out
 
 
 def config2_run(with_cpu):
@@ -323,6 +391,10 @@ def theta_section(steps, warmup, with_cpu):
         out["config2_run"] = config2_run(with_cpu)
     except Exception as e:  # reported, not fatal
         out["config2_run"] = {"error": str(e)}
+    try:
+        out["config3_steps"] = config3_steps(with_cpu)
+    except Exception as e:  # reported, not fatal
+        out["config3_steps"] = {"error": str(e)}
     return out
 
 

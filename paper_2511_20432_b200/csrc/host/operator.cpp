@@ -117,6 +117,35 @@ Csr tensor_pattern(const NurbsVolume& vol) {
 
 }  // namespace
 
+Sell to_sell(const Csr& m) {
+  Sell s;
+  s.rows = m.rows;
+  const int ns = (m.rows + 31) / 32;
+  s.row_len.assign(m.rows, 0);
+  s.slice_ptr.assign(ns + 1, 0);
+  for (int sl = 0; sl < ns; ++sl) {
+    int w = 0;
+    for (int r = sl * 32; r < std::min(m.rows, sl * 32 + 32); ++r) {
+      s.row_len[r] = m.row_ptr[r + 1] - m.row_ptr[r];
+      w = std::max(w, s.row_len[r]);
+    }
+    s.slice_ptr[sl + 1] = s.slice_ptr[sl] + 32LL * w;
+  }
+  s.col.assign(s.slice_ptr[ns], 0);
+  s.val.assign(s.slice_ptr[ns], 0.0);
+  parallel_for(ns, [&](long sl) {
+    for (int r = static_cast<int>(sl) * 32; r < std::min(m.rows, static_cast<int>(sl) * 32 + 32);
+         ++r) {
+      const long long base = s.slice_ptr[sl] + (r & 31);
+      for (int k = m.row_ptr[r]; k < m.row_ptr[r + 1]; ++k) {
+        s.col[base + 32LL * (k - m.row_ptr[r])] = m.col[k];
+        s.val[base + 32LL * (k - m.row_ptr[r])] = m.val[k];
+      }
+    }
+  }, 64);
+  return s;
+}
+
 // Element matrices are formed in parallel in batches of consecutive elements;
 // the scatter is parallel over the tensor index i of the row (each worker owns
 // a range of i and walks the batch in element order), so every entry still

@@ -29,6 +29,17 @@ struct Csr {
   std::vector<int> row_ptr, col;
   std::vector<double> val;
 };
+// Sliced ELL copy (32-row slices, entry k of a slice's rows contiguous,
+// padded to the slice's longest row) for coalesced one-thread-per-row
+// products on the GPU (k2_csr.cu DevSell).
+struct Sell {
+  int rows = 0;
+  std::vector<long long> slice_ptr;
+  std::vector<int> row_len, col;
+  std::vector<double> val;
+};
+Sell to_sell(const Csr& m);
+
 // M (coefficient rho c) and K (coefficient k) on the full tensor pattern
 // (assembly.cpp:8-101), element contributions scattered in element order.
 void assemble_mass_stiffness(const NurbsVolume& vol, std::array<int, 3> nq, const Material& mat,

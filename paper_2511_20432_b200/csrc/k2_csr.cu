@@ -22,9 +22,65 @@ constexpr int kThreads = 256;
 
 __device__ __forceinline__ double row_dot(const DevCsr& A, int r, const double* __restrict__ x) {
   double acc = 0.0;
-  for (int k = A.row_ptr[r]; k < A.row_ptr[r + 1]; ++k)
-    acc = __dadd_rn(acc, __dmul_rn(A.val[k], x[A.col[k]]));
+  int k = A.row_ptr[r];
+  const int e = A.row_ptr[r + 1];
+  for (; k + 4 <= e; k += 4) {  // loads batched, adds in order
+    double vv[4], xx[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) vv[u] = A.val[k + u];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) xx[u] = x[A.col[k + u]];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) acc = __dadd_rn(acc, __dmul_rn(vv[u], xx[u]));
+  }
+  for (; k < e; ++k) acc = __dadd_rn(acc, __dmul_rn(A.val[k], x[A.col[k]]));
   return acc;
+}
+
+// the same sum over the sliced layout (coalesced across the 32 rows of a
+// slice). The row's terms are added strictly in order, so the loads are
+// batched (kBatch values, columns and gathered x in flight per thread) to
+// hide memory latency behind the sequential add chain.
+#ifndef K2_SELL_BATCH
+#define K2_SELL_BATCH 16  // config 3 (302,974 rows): 4 -> 335, 8 -> 215, 16 -> 199 us per CG iteration
+#endif
+constexpr int kBatch = K2_SELL_BATCH;
+__device__ __forceinline__ double row_dot(const DevSell& A, int r, const double* __restrict__ x) {
+  const long long base = A.slice_ptr[r >> 5] + (r & 31);
+  const int len = A.row_len[r];
+  const double* __restrict__ v = A.val + base;
+  const int* __restrict__ c = A.col + base;
+  double acc = 0.0;
+  int k = 0;
+  for (; k + kBatch <= len; k += kBatch) {
+    double vv[kBatch], xx[kBatch];
+    int cc[kBatch];
+#pragma unroll
+    for (int u = 0; u < kBatch; ++u) {
+      vv[u] = __ldcs(v + 32 * (k + u));
+      cc[u] = __ldcs(c + 32 * (k + u));
+    }
+#pragma unroll
+    for (int u = 0; u < kBatch; ++u) xx[u] = x[cc[u]];  // (x is written in-kernel: no .nc)
+#pragma unroll
+    for (int u = 0; u < kBatch; ++u) acc = __dadd_rn(acc, __dmul_rn(vv[u], xx[u]));
+  }
+  for (; k < len; ++k) acc = __dadd_rn(acc, __dmul_rn(__ldcs(v + 32 * k), x[__ldcs(c + 32 * k)]));
+  return acc;
+}
+
+__device__ __forceinline__ double diag_of(const DevCsr& A, int r) {
+  double d = 0.0;
+  for (int k = A.row_ptr[r]; k < A.row_ptr[r + 1]; ++k)
+    if (A.col[k] == r) d = A.val[k];
+  return d;
+}
+__device__ __forceinline__ double diag_of(const DevSell& A, int r) {
+  const long long base = A.slice_ptr[r >> 5] + (r & 31);
+  double d = 0.0;
+  for (int k = 0; k < A.row_len[r]; ++k)
+    if (A.col[base + 32 * k] == r) d = A.val[base + 32 * k];
+  return d;
 }
 
 __device__ __forceinline__ void grid_reduce(cg::grid_group& grid, double (&acc)[4],
@@ -63,9 +119,9 @@ __device__ __forceinline__ void grid_reduce(cg::grid_group& grid, double (&acc)[
   buf ^= 1;
 }
 
-__global__ void __launch_bounds__(kThreads) csr_pcg_kernel(DevCsr A, const double* rhs,
-                                                           double* x, CsrWork w, double tol,
-                                                           int max_iter) {
+template <class Mat>
+__global__ void __launch_bounds__(kThreads) csr_pcg_kernel(Mat A, const double* rhs, double* x,
+                                                           CsrWork w, double tol, int max_iter) {
   cg::grid_group grid = cg::this_grid();
   __shared__ double red[64];
   const int n = A.rows;
@@ -132,18 +188,17 @@ __global__ void __launch_bounds__(kThreads) csr_pcg_kernel(DevCsr A, const doubl
   if (blockIdx.x == 0 && threadIdx.x == 0) *w.status = PcgStatus{it, status, rel, bnorm};
 }
 
-__global__ void csr_diag_kernel(DevCsr A, double* inv_diag, PcgStatus* st) {
+template <class Mat>
+__global__ void csr_diag_kernel(Mat A, double* inv_diag, PcgStatus* st) {
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= A.rows) return;
-  double d = 0.0;
-  for (int k = A.row_ptr[r]; k < A.row_ptr[r + 1]; ++k)
-    if (A.col[k] == r) d = A.val[k];
+  const double d = diag_of(A, r);
   if (!(d > 0.0)) st->status = 2;
   inv_diag[r] = 1.0 / d;
 }
 
 // rhs_f = [B T]_f - [A g~]_f + theta F1 + (1 - theta) F0 (assembly.cpp:258-271)
-__global__ void csr_rhs_kernel(DevCsr Bf, DevCsr Ac, const double* T, const double* g1,
+__global__ void csr_rhs_kernel(DevSell Bf, DevSell Ac, const double* T, const double* g1,
                                const double* F0, const double* F1, const int* free_list,
                                double theta, double* rhs) {
   const int f = blockIdx.x * blockDim.x + threadIdx.x;
@@ -157,18 +212,28 @@ __global__ void csr_rhs_kernel(DevCsr Bf, DevCsr Ac, const double* T, const doub
 }  // namespace
 
 int csr_pcg_max_blocks(int sm_count) {
-  int per_sm = 0;
+  int a = 0, b = 0;
   TG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-      &per_sm, reinterpret_cast<const void*>(&csr_pcg_kernel), kThreads, 0));
-  return std::max(1, per_sm) * sm_count;
+      &a, reinterpret_cast<const void*>(&csr_pcg_kernel<DevCsr>), kThreads, 0));
+  TG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+      &b, reinterpret_cast<const void*>(&csr_pcg_kernel<DevSell>), kThreads, 0));
+  return std::max(1, std::min(a, b)) * sm_count;
 }
 
-void csr_inverse_diagonal(const DevCsr& A, double* inv_diag, PcgStatus* st, cudaStream_t s) {
+template <class Mat>
+void inverse_diagonal(const Mat& A, double* inv_diag, PcgStatus* st, cudaStream_t s) {
+  if (A.rows <= 0) return;
   csr_diag_kernel<<<(A.rows + 255) / 256, 256, 0, s>>>(A, inv_diag, st);
   TG_CUDA(cudaGetLastError());
 }
+void csr_inverse_diagonal(const DevCsr& A, double* inv_diag, PcgStatus* st, cudaStream_t s) {
+  inverse_diagonal(A, inv_diag, st, s);
+}
+void csr_inverse_diagonal(const DevSell& A, double* inv_diag, PcgStatus* st, cudaStream_t s) {
+  inverse_diagonal(A, inv_diag, st, s);
+}
 
-void csr_theta_rhs(const DevCsr& Bf, const DevCsr& Ac, const double* T, const double* g1,
+void csr_theta_rhs(const DevSell& Bf, const DevSell& Ac, const double* T, const double* g1,
                    const double* F0, const double* F1, const int* free_list, double theta,
                    double* rhs, cudaStream_t s) {
   if (Bf.rows <= 0) return;
@@ -177,34 +242,43 @@ void csr_theta_rhs(const DevCsr& Bf, const DevCsr& Ac, const double* T, const do
   TG_CUDA(cudaGetLastError());
 }
 
-void csr_pcg_solve(const DevCsr& A, const double* rhs, double* x, const CsrWork& w, double tol,
-                   int max_iter, int blocks, cudaStream_t s) {
+template <class Mat>
+void pcg_solve(const Mat& A, const double* rhs, double* x, const CsrWork& w, double tol,
+               int max_iter, int blocks, cudaStream_t s) {
   const int need = (A.rows + kThreads - 1) / kThreads;
   const int nb = std::max(1, std::min(blocks, need));
-  DevCsr AA = A;
+  Mat AA = A;
   CsrWork ww = w;
   double tt = tol;
   int mi = max_iter;
   void* args[] = {&AA, const_cast<double**>(&rhs), &x, &ww, &tt, &mi};
-  TG_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(&csr_pcg_kernel), dim3(nb),
-                                      dim3(kThreads), args, 0, s));
+  TG_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(&csr_pcg_kernel<Mat>),
+                                      dim3(nb), dim3(kThreads), args, 0, s));
+}
+void csr_pcg_solve(const DevCsr& A, const double* rhs, double* x, const CsrWork& w, double tol,
+                   int max_iter, int blocks, cudaStream_t s) {
+  pcg_solve(A, rhs, x, w, tol, max_iter, blocks, s);
+}
+void csr_pcg_solve(const DevSell& A, const double* rhs, double* x, const CsrWork& w, double tol,
+                   int max_iter, int blocks, cudaStream_t s) {
+  pcg_solve(A, rhs, x, w, tol, max_iter, blocks, s);
 }
 
-}  // namespace tgb
-
-namespace tgb {
-
 namespace {
-__global__ void csr_apply_kernel(DevCsr A, const double* x, double* y) {
+template <class Mat>
+__global__ void csr_apply_kernel(Mat A, const double* x, double* y) {
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r < A.rows) y[r] = row_dot(A, r, x);
 }
-}  // namespace
-
-void csr_apply(const DevCsr& A, const double* x, double* y, cudaStream_t s) {
+template <class Mat>
+void apply(const Mat& A, const double* x, double* y, cudaStream_t s) {
   if (A.rows <= 0) return;
   csr_apply_kernel<<<(A.rows + 255) / 256, 256, 0, s>>>(A, x, y);
   TG_CUDA(cudaGetLastError());
 }
+}  // namespace
+
+void csr_apply(const DevCsr& A, const double* x, double* y, cudaStream_t s) { apply(A, x, y, s); }
+void csr_apply(const DevSell& A, const double* x, double* y, cudaStream_t s) { apply(A, x, y, s); }
 
 }  // namespace tgb

@@ -394,15 +394,18 @@ void Sim::setup_device(int device, int preconditioner) {
       use_cg1 = false;
     }
   } else {
-    auto up = [&](const Csr& C, DevBuf<int>& rp, DevBuf<int>& ci, DevBuf<double>& v, DevCsr& out) {
-      upload(rp, C.row_ptr, s);
-      upload(ci, C.col, s);
-      upload(v, C.val, s);
-      out = DevCsr{C.rows, rp.p, ci.p, v.p};
+    auto up = [&](const Csr& C, SellBufs& b, DevSell& out) {
+      const Sell h = to_sell(C);
+      upload(b.sp, h.slice_ptr, s);
+      upload(b.len, h.row_len, s);
+      upload(b.col, h.col, s);
+      upload(b.val, h.val, s);
+      TG_CUDA(cudaStreamSynchronize(s));  // h dies here
+      out = DevSell{C.rows, b.sp.p, b.len.p, b.col.p, b.val.p};
     };
-    up(csrA, dA_rp, dA_ci, dA_v, devA);
-    up(csrAc, dAc_rp, dAc_ci, dAc_v, devAc);
-    up(csrB, dB_rp, dB_ci, dB_v, devB);
+    up(csrA, sA, devA);
+    up(csrAc, sAc, devAc);
+    up(csrB, sB, devB);
     upload(d_free_list, dofs.free_list, s);
     csr_inverse_diagonal(devA, d_invd.p, d_status.p, s);
     pcg_blocks = csr_pcg_max_blocks(ctx->sm_count);

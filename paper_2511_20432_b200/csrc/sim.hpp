@@ -93,9 +93,13 @@ class Sim {
   DevBuf<double> d_qx, d_qn, d_qw, d_Nb, d_Nf, d_gq, d_loc, d_grev, d_band;
   DevBuf<int> d_inc_ptr, d_inc_src, d_pt_index, d_elem_off, d_fine, d_free_list, d_qb_off,
       d_qf_off;
-  DevBuf<int> dA_rp, dA_ci, dAc_rp, dAc_ci, dB_rp, dB_ci;
-  DevBuf<double> dA_v, dAc_v, dB_v;
-  DevCsr devA{}, devAc{}, devB{};
+  struct SellBufs {
+    DevBuf<long long> sp;
+    DevBuf<int> len, col;
+    DevBuf<double> val;
+  };
+  SellBufs sA, sAc, sB;
+  DevSell devA{}, devAc{}, devB{};
   KronGrid gfull{}, gfree{};
   DevBuf<double> d_x, d_r, d_z, d_p, d_p2, d_Ap, d_invd, d_rhs, d_gn, d_g1, d_Fn, d_F1, d_T, d_gfull,
       d_partials;

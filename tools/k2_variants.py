@@ -15,8 +15,9 @@ sys.path.insert(0, ROOT)
 VDIR = os.path.join(ROOT, "paper_2511_20432_b200", "_lib", "variants_k2")
 
 VARIANTS = {
-    "base": dict(),
-    "zsplit": dict(K2_ZSPLIT=1),
+    "sell_b4": dict(K2_SELL_BATCH=4),
+    "sell_b8": dict(K2_SELL_BATCH=8),
+    "sell_b16": dict(K2_SELL_BATCH=16),
 }
 
 
@@ -24,7 +25,7 @@ def build():
     from paper_2511_20432_b200 import _build as B
     B.build()
     os.makedirs(VDIR, exist_ok=True)
-    src = os.path.join(B.CSRC, "k2_kron.cu")
+    src = os.path.join(B.CSRC, os.environ.get("TG_VARIANT_SRC", "k2_kron.cu"))
     others = [B._obj_for(s) for s in B._sources() if s != src]
     for name, defs in VARIANTS.items():
         obj = os.path.join(B.OBJDIR, f"k2_{name}.o")
