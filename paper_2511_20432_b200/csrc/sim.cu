@@ -406,6 +406,8 @@ void Sim::setup_device(int device, int preconditioner) {
     up(csrA, sA, devA);
     up(csrAc, sAc, devAc);
     up(csrB, sB, devB);
+    csrAc = Csr{};  // host copies no longer needed (csrA stays: tg_sim_reduced_operator)
+    csrB = Csr{};
     upload(d_free_list, dofs.free_list, s);
     csr_inverse_diagonal(devA, d_invd.p, d_status.p, s);
     pcg_blocks = csr_pcg_max_blocks(ctx->sm_count);
