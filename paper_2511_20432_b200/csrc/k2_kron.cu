@@ -1045,22 +1045,24 @@ struct EpiCg1InitS {  // r0 = b - A x0; u0 = D^-1 r0; s^_{-1} = p_{-1} = 0; r.r,
   }
 };
 
-template <int P>
+template <int P, int PL>
 __host__ __device__ constexpr size_t cg1_centre_offset(int nz) {
-  return (zband_offset<P, kTmaPlanes, kCg1Nin, 1, kCg1Stages, kCg1Ub>() +
+  return (zband_offset<P, PL, kCg1Nin, 1, kCg1Stages, kCg1Ub>() +
           2 * static_cast<size_t>(nz) * (2 * P + 1) * 8 +
           127) / 128 * 128;
 }
-template <int P>
+template <int P, int PL>
 size_t cg1_smem_bytes(int nz) {
-  return cg1_centre_offset<P>(nz) + sizeof(CentreRing<kTmaPlanes>);
+  return cg1_centre_offset<P, PL>(nz) + sizeof(CentreRing<PL>);
 }
 
-template <int P>
+// PL planes per sweep step (TMA box depth): 2 for large grids (2 CTAs/SM), 4
+// for grids too small to fill the GPU at 2 CTAs/SM (1 CTA/SM, half the steps
+// per segment: the per-iteration time there is pipeline latency, not bytes)
+template <int P, int PL>
 __global__ void __launch_bounds__(kThreads, K2_MINB)
     k2_cg1_kernel(KronGrid g, double a, double b, const double* rhs, double* x, Cg1Work w,
                   double tol, int max_iter, TileIdx T, const __grid_constant__ Cg1Maps maps) {
-  constexpr int PL = kTmaPlanes;
   constexpr int NIN = kCg1Nin;
   using SMT = KSmem<P, PL, NIN, 1, kCg1Stages, kCg1Ub>;
   cg::grid_group grid = cg::this_grid();
@@ -1068,7 +1070,7 @@ __global__ void __launch_bounds__(kThreads, K2_MINB)
   auto& sm = *reinterpret_cast<SMT*>(smem_raw);
   double* zb =
       reinterpret_cast<double*>(smem_raw + zband_offset<P, PL, NIN, 1, kCg1Stages, kCg1Ub>());
-  auto* cr = reinterpret_cast<CentreRing<PL>*>(smem_raw + cg1_centre_offset<P>(g.n[2]));
+  auto* cr = reinterpret_cast<CentreRing<PL>*>(smem_raw + cg1_centre_offset<P, PL>(g.n[2]));
   __shared__ double red[64];
   if (threadIdx.x == 0 && threadIdx.y == 0)
     for (int v = 0; v < 2; ++v)
@@ -1319,7 +1321,7 @@ int seg_blocks(const TileIdx& T, int max_blocks) {
 
 }  // namespace
 
-bool k2_make_map(const KronGrid& g, const double* base, TensorMap3* out, bool halo) {
+bool k2_make_map(const KronGrid& g, const double* base, TensorMap3* out, bool halo, int planes) {
   static_assert(sizeof(TensorMap3) == sizeof(CUtensorMap), "tensor map size");
   EncodeFn enc = encoder();
   const size_t pitch = static_cast<size_t>(g.n[0]) * sizeof(double);
@@ -1330,7 +1332,7 @@ bool k2_make_map(const KronGrid& g, const double* base, TensorMap3* out, bool ha
   const int h = halo ? 2 * g.p : 0;
   const cuuint32_t box[3] = {static_cast<cuuint32_t>(kKronTX + h),
                              static_cast<cuuint32_t>(kKronTY + h),
-                             static_cast<cuuint32_t>(kTmaPlanes)};
+                             static_cast<cuuint32_t>(planes)};
   const cuuint32_t estr[3] = {1, 1, 1};
   CUtensorMap m;
   const CUresult r = enc(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base), dims,
@@ -1442,20 +1444,36 @@ void k2_pcg_solve(const KronGrid& g, double a, double b, const double* rhs, doub
   });
 }
 
-int k2_cg1_max_blocks(int p, int sm_count, int nz) {
+#define TG_CG1_PL_DISPATCH(PL_, ...)                                          \
+  switch (PL_) {                                                              \
+    case 2: { constexpr int PL = 2; __VA_ARGS__; break; }                     \
+    case 4: { constexpr int PL = 4; __VA_ARGS__; break; }                     \
+    default: throw std::invalid_argument("cg1: planes per step must be 2 or 4"); \
+  }
+
+#ifndef K2_SMALL_PL
+#define K2_SMALL_PL 4
+#endif
+int k2_cg1_planes(const KronGrid& g, int sm_count) {
+  const TileIdx T = make_tiles(g);
+  const long colplanes = static_cast<long>(T.ntx) * T.nty * T.nz;
+  return colplanes / K2_MIN_PLANES < 2L * sm_count ? K2_SMALL_PL : 2;
+}
+
+int k2_cg1_max_blocks(int p, int sm_count, int nz, int pl) {
   int per_sm = 0;
-  TG_KRON_DISPATCH(p, {
-    const size_t sb = cg1_smem_bytes<P>(nz);
-    allow_smem(k2_cg1_kernel<P>, sb);
+  TG_KRON_DISPATCH(p, TG_CG1_PL_DISPATCH(pl, {
+    const size_t sb = cg1_smem_bytes<P, PL>(nz);
+    allow_smem(k2_cg1_kernel<P, PL>, sb);
     TG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-        &per_sm, reinterpret_cast<const void*>(&k2_cg1_kernel<P>), kThreads, sb));
-  });
+        &per_sm, reinterpret_cast<const void*>(&k2_cg1_kernel<P, PL>), kThreads, sb));
+  }));
   return std::max(1, per_sm) * sm_count;
 }
 
 void k2_cg1_solve(const KronGrid& g, double a, double b, const double* rhs, double* x,
                   const Cg1Work& w, const Cg1Maps& maps, double tol, int max_iter, int blocks,
-                  cudaStream_t s) {
+                  cudaStream_t s, int pl) {
   const TileIdx T = make_tiles(g);
   const int nb = seg_blocks(T, blocks);
   dim3 grid(nb), block(kKronTX, kKronTY);
@@ -1466,11 +1484,10 @@ void k2_cg1_solve(const KronGrid& g, double a, double b, const double* rhs, doub
   int mi = max_iter;
   TileIdx TT = T;
   void* args[] = {&gg, &aa, &bb, const_cast<double**>(&rhs), &x, &ww, &tt, &mi, &TT, &mm};
-  TG_KRON_DISPATCH(g.p, {
-    TG_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(&k2_cg1_kernel<P>), grid,
-                                        block, args,
-                                        cg1_smem_bytes<P>(g.n[2]), s));
-  });
+  TG_KRON_DISPATCH(g.p, TG_CG1_PL_DISPATCH(pl, {
+    TG_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(&k2_cg1_kernel<P, PL>),
+                                        grid, block, args, cg1_smem_bytes<P, PL>(g.n[2]), s));
+  }));
 }
 
 }  // namespace tgb

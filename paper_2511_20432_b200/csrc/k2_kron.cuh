@@ -35,7 +35,8 @@ struct alignas(64) TensorMap3 {
 // Encode the descriptor for `base` (a vector over g's grid). Returns false
 // when TMA cannot address the grid (row pitch not a multiple of 16 bytes);
 // the kernels then load planes with ordinary loads.
-bool k2_make_map(const KronGrid& g, const double* base, TensorMap3* out, bool halo = true);
+bool k2_make_map(const KronGrid& g, const double* base, TensorMap3* out, bool halo = true,
+                 int planes = 2);
 
 // y = Op(a1, b1) v1 + Op(a2, b2) v2 with Op(a, b) = a (Mz x My x Mx) +
 //     b (Mz x My x Kx + Mz x Ky x Mx + Kz x My x Mx); v2 may be null.
@@ -117,10 +118,13 @@ void k2_pcg_solve(const KronGrid& g, double a, double b, const double* rhs, doub
 // The same solve with one tile sweep and one grid reduction per iteration
 // (TMA only; see k2_kron.cu). Stop test, failure codes and warm start as
 // k2_pcg_solve.
-int k2_cg1_max_blocks(int p, int sm_count, int nz);
+// planes per sweep step for this grid (2, or 4 for grids that cannot fill the
+// GPU at 2 CTAs/SM); the maps of the solve must be made with that box depth
+int k2_cg1_planes(const KronGrid& g, int sm_count);
+int k2_cg1_max_blocks(int p, int sm_count, int nz, int pl);
 void k2_cg1_solve(const KronGrid& g, double a, double b, const double* rhs, double* x,
                   const Cg1Work& w, const Cg1Maps& maps, double tol, int max_iter, int blocks,
-                  cudaStream_t s);
+                  cudaStream_t s, int pl);
 // plain y = Op(a, b) v (tests / the operator alone)
 // v_map: TMA descriptor of v (k2_make_map) or null for plain loads
 void k2_apply(const KronGrid& g, double a, double b, const double* v, double* y, int sm_count,

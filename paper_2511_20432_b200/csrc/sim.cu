@@ -357,12 +357,20 @@ void Sim::setup_device(int device, int preconditioner) {
       d_w2.ensure(n_free);
       d_s2.ensure(n_free);
       Cg1Maps& m = cg1maps;
-      use_cg1 = k2_make_map(gfree, d_x.p, &m.x) && k2_make_map(gfree, d_invd.p, &m.inv_diag) &&
-                k2_make_map(gfree, d_r.p, &m.r[0]) && k2_make_map(gfree, d_z.p, &m.r[1]) &&
-                k2_make_map(gfree, d_Ap.p, &m.w[0]) && k2_make_map(gfree, d_w2.p, &m.w[1]) &&
-                k2_make_map(gfree, d_p2.p, &m.s[0]) && k2_make_map(gfree, d_s2.p, &m.s[1]) &&
-                k2_make_map(gfree, d_x.p, &m.xc, false) && k2_make_map(gfree, d_p.p, &m.pc, false);
-      if (use_cg1) pcg_blocks = k2_cg1_max_blocks(p, ctx->sm_count, gfree.n[2]);
+      cg1_pl = k2_cg1_planes(gfree, ctx->sm_count);
+      if (const char* e = std::getenv("TG_K2_PL")) cg1_pl = std::atoi(e);
+      const int L = cg1_pl;
+      use_cg1 = k2_make_map(gfree, d_x.p, &m.x, true, L) &&
+                k2_make_map(gfree, d_invd.p, &m.inv_diag, true, L) &&
+                k2_make_map(gfree, d_r.p, &m.r[0], true, L) &&
+                k2_make_map(gfree, d_z.p, &m.r[1], true, L) &&
+                k2_make_map(gfree, d_Ap.p, &m.w[0], true, L) &&
+                k2_make_map(gfree, d_w2.p, &m.w[1], true, L) &&
+                k2_make_map(gfree, d_p2.p, &m.s[0], true, L) &&
+                k2_make_map(gfree, d_s2.p, &m.s[1], true, L) &&
+                k2_make_map(gfree, d_x.p, &m.xc, false, L) &&
+                k2_make_map(gfree, d_p.p, &m.pc, false, L);
+      if (use_cg1) pcg_blocks = k2_cg1_max_blocks(p, ctx->sm_count, gfree.n[2], cg1_pl);
     }
     if (preconditioner == 1) {
       // V_d, lambda_d per direction on the free grid (host/fdm.cpp)
@@ -543,7 +551,7 @@ void Sim::theta_step_launch(double tol, int max_iter) {
                       d_invd.p, d_partials.p,   d_status.p};
       ctx->timer.timed(2, s, [&] {
         k2_cg1_solve(gfree, coefA[0], coefA[1], d_rhs.p, d_x.p, w, cg1maps, tol, max_iter,
-                     pcg_blocks, s);
+                     pcg_blocks, s, cg1_pl);
       });
     } else {
       const PcgWork w{d_r.p,        d_z.p,      d_p.p,

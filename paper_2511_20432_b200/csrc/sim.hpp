@@ -106,6 +106,7 @@ class Sim {
   PcgMaps maps{};
   // single-sweep solve (k2_cg1_solve): the default when TMA can address the
   // free grid; TG_K2_ALGO=pcg selects the two-phase kernel
+  int cg1_pl = 2;  // planes per sweep step of the single-sweep solver
   bool use_cg1 = false;
   // fast-diagonalization preconditioner (k2_fdm.cuh), opt-in
   bool use_fdm = false;
