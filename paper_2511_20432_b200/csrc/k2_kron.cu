@@ -739,6 +739,9 @@ constexpr int kCg1Nin = K2_CG1_SCALED ? 3 : 4;
 #ifndef K2_CG1_UB
 #define K2_CG1_UB 1
 #endif
+#ifndef K2_STUDY_NOSWEEP
+#define K2_STUDY_NOSWEEP 0
+#endif
 constexpr int kCg1Ub = K2_CG1_SCALED ? K2_CG1_UB : 2;  // every scaled sweep has a prologue
 
 template <int P, int PL>
@@ -1236,6 +1239,14 @@ __global__ void __launch_bounds__(kThreads, K2_MINB)
                       &maps.pc, &cseq, &g, a,   b,            {{}, zb, g.n[2]}, 0.0, 0.0};
     EpiCg1S<P, ProCg1S<P, PL>> e{w.w[cur ^ 1], &pc, a, b, 0.0};
     const Inputs<NIN> in = inputs(cur);
+#if K2_STUDY_NOSWEEP  // latency study only (tools/k2_iter_time.py): barrier + reduction alone
+    {
+      const double acc0[4] = {1.0, 1.0, 1.0, 0.0};
+      grid_reduce(grid, acc0, w.partials, buf, red, tot);
+      ++it;
+      continue;
+    }
+#endif
     bool first = true;
     for_segments(T, gridDim.x, blockIdx.x, [&](const Seg& sg) {
       kron_tile<P, PL, NIN, 1, true>(g, c, in, pc, sg, sm, zb, seq, e, first && primed);

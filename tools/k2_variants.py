@@ -15,9 +15,8 @@ sys.path.insert(0, ROOT)
 VDIR = os.path.join(ROOT, "paper_2511_20432_b200", "_lib", "variants_k2")
 
 VARIANTS = {
-    "sell_b4": dict(K2_SELL_BATCH=4),
-    "sell_b8": dict(K2_SELL_BATCH=8),
-    "sell_b16": dict(K2_SELL_BATCH=16),
+    "base": dict(),
+    "nosweep": dict(K2_STUDY_NOSWEEP=1),
 }
 
 
