@@ -171,6 +171,16 @@ inline PcgResult pcg_jacobi(const CsrMatrix& A, const std::vector<double>& b,
   return r;
 }
 
+// Geometry tooling (config 3; not in the reference): exact degree elevation of
+// a geometry file, written in the reference's format.
+inline void elevate_geometry(const std::string& in_path, const std::string& out_path,
+                             const int elevate[3], const double* scale = nullptr) {
+  char err[512] = {0};
+  const int rc =
+      tg_geometry_elevate(in_path.c_str(), elevate, scale, out_path.c_str(), err, sizeof(err));
+  if (rc != TG_OK) raise(rc, err);
+}
+
 // postproc.hpp:17-44
 struct FluxProfile {
   struct Sample {
@@ -292,6 +302,21 @@ class Simulation {
       p.samples.push_back({rows[5 * i], rows[5 * i + 1], rows[5 * i + 2], rows[5 * i + 3],
                            rows[5 * i + 4]});
     return p;
+  }
+
+  // DirichletSystem::reduced_operator() (assembly.hpp:56) of a non-separable
+  // patch, as the reference's CsrMatrix (bit-identical values)
+  CsrMatrix reduced_operator() {
+    int rows = 0;
+    const long nnz = tg_sim_reduced_operator(get(), &rows, nullptr, nullptr, nullptr);
+    if (nnz < 0) raise(static_cast<int>(-nnz), tg_sim_last_error(get()));
+    CsrMatrix A;
+    A.rows = A.cols = rows;
+    A.row_ptr.resize(rows + 1);
+    A.col_idx.resize(nnz);
+    A.vals.resize(nnz);
+    tg_sim_reduced_operator(get(), nullptr, A.row_ptr.data(), A.col_idx.data(), A.vals.data());
+    return A;
   }
 
   long n_full = 0, n_free = 0, n_constrained = 0;

@@ -44,7 +44,8 @@ def test_shim_sparse_and_observers(tmp_path):
            os.path.join(ROOT, "examples", "sparse_and_observers.cpp"), "-L", _build.LIBDIR,
            "-lthermiga_b200", f"-Wl,-rpath,{_build.LIBDIR}", "-o", str(exe)]
     subprocess.run(cmd, check=True, capture_output=True)
-    r = subprocess.run([str(exe), os.path.join(ROOT, "configs", "cfg0_parity.cfg")],
+    r = subprocess.run([str(exe), os.path.join(ROOT, "configs", "cfg0_parity.cfg"),
+                        os.path.join(ROOT, "configs", "qc_small.cfg"), str(tmp_path)],
                        capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
-    assert r.stdout.count(" ok") == 3
+    assert r.stdout.count(" ok") == 4
