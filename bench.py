@@ -249,6 +249,8 @@ def config3_steps(with_cpu, steps=10):
            "theta_ms_per_step": prof["k2_ms"] / steps,
            "theta_step_total_ms_per_step": prof["theta_step_ms"] / steps,
            "theta_ms_per_step_per_mdof": prof["k2_ms"] / steps / (sim.info["n_full"] / 1e6),
+           "theta_step_total_ms_per_mdof": prof["theta_step_ms"] / steps
+                                           / (sim.info["n_full"] / 1e6),
            "cg_iterations_per_step": iters / steps, "us_per_cg_iteration": us_it,
            "operator": "assembled A_ff in sliced ELL (32-row slices), one thread per row, "
                        "row sums in the reference's CSR order (bit-exact rows)",
@@ -362,8 +364,10 @@ def theta_section(steps, warmup, with_cpu):
         "theta_ms_per_step": k2_ms,
         "theta_ms_per_step_per_mdof": k2_ms / (dofs / 1e6),
         "theta_step_total_ms_per_step": prof["theta_step_ms"] / steps,
-        "theta_step_total_note": "expand + theta RHS + solve (theta_step, timestep.cpp:5-24); "
-                                 "theta_ms_per_step is the solve alone",
+        "theta_step_total_ms_per_mdof": prof["theta_step_ms"] / steps / (dofs / 1e6),
+        "theta_step_total_note": "SURVEY.md §8d's 'theta-step time per 1M DOF' is the whole "
+                                 "step: expand + theta RHS + solve (theta_step, "
+                                 "timestep.cpp:5-24); theta_ms_* are the solve alone",
         "k1_ms_per_step": prof["k1_ms"] / steps,
         "cg_iterations_per_step": iters / steps,
         "solver": solver,
@@ -460,6 +464,7 @@ def theta_fdm(steps, warmup):
                               "cuBLAS DGEMM mode products), same PCG stop test",
             "theta_ms_per_step": k2_ms, "theta_ms_per_step_per_mdof": k2_ms / (dofs / 1e6),
             "theta_step_total_ms_per_step": prof["theta_step_ms"] / steps,
+            "theta_step_total_ms_per_mdof": prof["theta_step_ms"] / steps / (dofs / 1e6),
             "cg_iterations_per_step": iters / steps, "last_rel_residual": rel}
 
 
