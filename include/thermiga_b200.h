@@ -260,6 +260,17 @@ int tg_sim_field_eval(tg_sim* sim, const double* coeffs, const double* xi, long 
 int tg_sim_flux_profile(tg_sim* sim, int face, int n_samples, double edge_v,
                         const double* theta_axis, double* out);
 
+/* K5 sum-factorised superposition (no reference counterpart: an evaluation
+ * strategy for assemble_flux_load, proj/src/assembly.cpp:148-166, and
+ * dirichlet_values, proj/src/mesh.cpp:238-264, on axis-aligned patches whose
+ * face quadrature / Greville points are tensor grids). On by default where
+ * available; on = 0 makes every superposition a K1 pair loop. */
+int tg_sim_set_sumfact(tg_sim* sim, int on);
+/* out[8]: on, faces gridded, Greville grid, source prefix J of the last flux
+ * call, of the last Dirichlet call, GEMM flops issued, point x source pairs
+ * taken off K1, sources per GEMM chunk */
+int tg_sim_sumfact_stats(tg_sim* sim, double* out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -367,6 +367,8 @@ def _bind_sim(L):
     L.tg_sim_probe_device.argtypes = [C.c_void_p, C.c_void_p, C.c_long, C.c_void_p]
     L.tg_sim_field_eval.argtypes = [C.c_void_p, _dp, _dp, C.c_long, _dp, _dp]
     L.tg_sim_flux_profile.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_double, _dp, _dp]
+    L.tg_sim_set_sumfact.argtypes = [C.c_void_p, C.c_int]
+    L.tg_sim_sumfact_stats.argtypes = [C.c_void_p, _dp]
     L._sim_bound = True
 
 
@@ -456,6 +458,19 @@ class Simulation:
                                              _p(d["centers"]), ip(d["dofs"]), _p(d["xq"]),
                                              _p(d["nq"]), _p(d["wq"]), _p(d["Nb"]), _p(d["Nf"])))
         return d
+
+    def set_sumfact(self, on: bool = True):
+        """K5: superposition on the gridded face / Greville point sets as a DGEMM over
+        the sources no cull can reach there (default on where the sets are grids);
+        off = every pair through K1."""
+        self._check(self._L.tg_sim_set_sumfact(self._h, int(on)))
+
+    def sumfact_stats(self) -> dict:
+        out = np.zeros(8)
+        self._check(self._L.tg_sim_sumfact_stats(self._h, _p(out)))
+        return dict(on=bool(out[0]), faces_gridded=bool(out[1]), greville_gridded=bool(out[2]),
+                    last_j_flux=int(out[3]), last_j_dirichlet=int(out[4]), gemm_flops=out[5],
+                    pairs_off_k1=out[6], chunk=int(out[7]))
 
     def greville_points(self):
         out = np.zeros((self.info["n_constrained"], 3))

@@ -46,7 +46,8 @@ Material to_material(const tg_material* m) {
 
 void k1_run(tg_ctx* ctx, const double* d_src6, int n_src, const double* d_pts,
             const int* d_index, long n_pts_l, double t, double cull, K1Mode mode,
-            double* d_out_a, double* d_out_b, const K1Flux& flux, cudaStream_t stream) {
+            double* d_out_a, double* d_out_b, const K1Flux& flux, cudaStream_t stream,
+            int src_begin, int src_end) {
   if (n_pts_l <= 0) return;
   // launches of at most 2^28 points (int indexing, bounded partial buffers);
   // every point's sum is independent of the chunking
@@ -59,7 +60,7 @@ void k1_run(tg_ctx* ctx, const double* d_src6, int n_src, const double* d_pts,
       const bool fl = mode == K1Mode::flux;
       k1_run(ctx, d_src6, n_src, d_index || fl ? d_pts : d_pts + 3 * off,
              d_index ? d_index + off : nullptr, n, t, cull, mode, d_out_a + off,
-             d_out_b ? d_out_b + 3 * off : nullptr, f, stream);
+             d_out_b ? d_out_b + 3 * off : nullptr, f, stream, src_begin, src_end);
     }
     return;
   }
@@ -73,6 +74,11 @@ void k1_run(tg_ctx* ctx, const double* d_src6, int n_src, const double* d_pts,
   const int P = grad ? ctx->k1_points_per_thread : ctx->k1_points_per_thread_value;
   const bool own_src = d_src6 == ctx->src6.p && static_cast<int>(ctx->tau_sufmin.size()) == n_src;
   if (own_src) n_src = ctx->active_prefix(t);  // trailing inactive sources: exact zeros
+  // sources [src_begin, src_end) only (the K5 split hands the rest to a GEMM)
+  if (src_end >= 0) n_src = std::min(n_src, src_end);
+  src_begin = std::max(0, std::min(src_begin, n_src));
+  d_src6 += 6 * static_cast<size_t>(src_begin);
+  n_src -= src_begin;
   const bool planar = own_src && ctx->planar && !std::getenv("TG_K1_NO_PLANAR");
   int S = 1;
   if (n_src > 0) {

@@ -180,6 +180,7 @@ struct K1Flux {
 
 void k1_run(tg_ctx* ctx, const double* d_src6, int n_src, const double* d_pts,
             const int* d_index, long n_pts, double t, double cull, K1Mode mode, double* d_out_a,
-            double* d_out_b, const K1Flux& flux, cudaStream_t stream);
+            double* d_out_b, const K1Flux& flux, cudaStream_t stream, int src_begin = 0,
+            int src_end = -1);
 
 }  // namespace tgb

@@ -82,6 +82,7 @@ Sim::~Sim() {
   if (h_dots) cudaFreeHost(h_dots);
   if (h_status) cudaFreeHost(h_status);
   if (h_fine) cudaFreeHost(h_fine);
+  if (h_sf_fine) cudaFreeHost(h_sf_fine);
   if (ctx) tg_ctx_destroy(ctx);
 }
 
@@ -424,6 +425,148 @@ void Sim::setup_device(int device, int preconditioner) {
   TG_CUDA(cudaMemcpyAsync(h_status, d_status.p, sizeof(PcgStatus), cudaMemcpyDeviceToHost, s));
   TG_CUDA(cudaStreamSynchronize(s));
   diag_ok = h_status->status != 2;
+  sf_setup();
+}
+
+// K5 setup: are the lateral faces' base quadrature points and the Greville
+// points tensor grids (up to coordinate rounding) with axis-aligned normals?
+void Sim::sf_setup() {
+  cudaStream_t s = ctx->stream;
+  if (const char* e = std::getenv("TG_SF_KC")) sf_kc = std::max(64, std::atoi(e));
+  const int tqb = h_qb_off.empty() ? 0 : h_qb_off.back();
+  // faces: base points grouped by the normal's axis and sign
+  double ext = 0.0;
+  for (int ax = 0; ax < 3; ++ax) {
+    double lo = 1e300, hi = -1e300;
+    for (int q = 0; q < tqb; ++q) {
+      lo = std::min(lo, h_qx[3 * q + ax]);
+      hi = std::max(hi, h_qx[3 * q + ax]);
+    }
+    ext = std::max(ext, hi - lo);
+  }
+  const double tol = 1e-12 * ext;
+  std::vector<int> gcell(tqb, -1), gaxn(tqb, 0);
+  sf_flux_ok = tqb > 0;
+  std::vector<std::vector<int>> groups(6);
+  for (int q = 0; q < tqb && sf_flux_ok; ++q) {
+    const double* n = &h_qn[3 * q];
+    int ax = 0;
+    for (int d = 1; d < 3; ++d)
+      if (std::fabs(n[d]) > std::fabs(n[ax])) ax = d;
+    const bool axis = std::fabs(std::fabs(n[ax]) - 1.0) <= 1e-12 &&
+                      std::fabs(n[(ax + 1) % 3]) <= 1e-12 && std::fabs(n[(ax + 2) % 3]) <= 1e-12;
+    if (!axis) sf_flux_ok = false;
+    groups[2 * ax + (n[ax] > 0.0)].push_back(q);
+  }
+  int off = 0;
+  for (int k = 0; k < 6 && sf_flux_ok; ++k) {
+    if (groups[k].empty()) continue;
+    std::vector<double> pts(3 * groups[k].size());
+    for (size_t i = 0; i < groups[k].size(); ++i)
+      for (int d = 0; d < 3; ++d) pts[3 * i + d] = h_qx[3 * groups[k][i] + d];
+    SfGrid g;
+    if (!sf_make_grid(pts.data(), static_cast<long>(groups[k].size()), tol, g) || g.axn != k / 2) {
+      sf_flux_ok = false;
+      break;
+    }
+    for (size_t i = 0; i < groups[k].size(); ++i) {
+      gcell[groups[k][i]] = off + g.cell[i];
+      gaxn[groups[k][i]] = g.axn;
+    }
+    sf_faces_off.push_back(off);
+    off += static_cast<int>(g.U.size() * g.V.size());
+    sf_faces.push_back(std::move(g));
+  }
+  if (sf_flux_ok) {
+    for (int ax = 0; ax < 3; ++ax) {
+      sf_lo[ax] = 1e300;
+      sf_hi[ax] = -1e300;
+    }
+    for (const SfGrid& g : sf_faces) {
+      for (int ax = 0; ax < 3; ++ax) {
+        sf_lo[ax] = std::min(sf_lo[ax], g.lo[ax]);
+        sf_hi[ax] = std::max(sf_hi[ax], g.hi[ax]);
+      }
+      sf_delta = std::max(sf_delta, g.delta);
+    }
+  } else {
+    sf_faces.clear();
+    sf_faces_off.clear();
+  }
+  sf_dir_ok = n_con > 0 && sf_make_grid(grev.data(), n_con, tol, sf_dir);
+  // grid lines on the device: faces then the Greville grid
+  std::vector<double> uv;
+  std::vector<size_t> at;
+  auto push = [&](const SfGrid& g) {
+    at.push_back(uv.size());
+    uv.insert(uv.end(), g.U.begin(), g.U.end());
+    uv.insert(uv.end(), g.V.begin(), g.V.end());
+  };
+  for (const SfGrid& g : sf_faces) push(g);
+  if (sf_dir_ok) push(sf_dir);
+  if (uv.empty()) return;
+  upload(d_sf_uv, uv, s);
+  auto dev = [&](const SfGrid& g, size_t a) {
+    const int na = static_cast<int>(g.U.size()), nb = static_cast<int>(g.V.size());
+    return SfDev{g.axn, g.axu, g.axv, na, nb, g.xf, d_sf_uv.p + a, d_sf_uv.p + a + na};
+  };
+  for (size_t k = 0; k < sf_faces.size(); ++k) sf_faces_dev.push_back(dev(sf_faces[k], at[k]));
+  if (sf_dir_ok) {
+    sf_dir_dev = dev(sf_dir, at.back());
+    upload(d_sf_dcell, sf_dir.cell, s);
+    d_sf_Gdir.ensure(sf_dir.U.size() * sf_dir.V.size());
+  }
+  if (sf_flux_ok) {
+    upload(d_sf_gcell, gcell, s);
+    upload(d_sf_gaxn, gaxn, s);
+    d_sf_G.ensure(off);
+    const size_t tqf = h_qf_off.back();
+    d_sf_fine.ensure(2 * tqf + 2);
+    d_sf_tmp.ensure(tqf + 1);
+    TG_CUDA(cudaMallocHost(&h_sf_fine, sizeof(int) * (2 * tqf + 2)));
+  }
+  if (!cublas && cublasCreate(&cublas) != CUBLAS_STATUS_SUCCESS)
+    throw cuda_error("cublas: create failed");
+  const char* e = std::getenv("TG_SUMFACT");
+  sf_on = !(e && std::string(e) == "0");
+  set_sumfact(sf_on);
+  TG_CUDA(cudaStreamSynchronize(s));
+}
+
+// longest prefix [0, J) of the sources that sf_source_eligible admits for the
+// box at t; a prefix of sources all active at an earlier t stays eligible
+// (their spreads only grow), so the scan resumes there
+int Sim::sf_prefix(double t, const double lo[3], const double hi[3], double delta, SfPrefix& c) {
+  const double alpha = ctx->mat.diffusivity();
+  const double cull = cfg.superpose.cull_exponent;
+  const double* src = reinterpret_cast<const double*>(sources.data());
+  const int n = static_cast<int>(sources.size());
+  int j = (c.valid && t >= c.t) ? c.J : 0;
+  bool active = true;
+  for (; j < n; ++j) {
+    const double* p = src + 6 * static_cast<size_t>(j);
+    if (!sf_source_eligible(p, t, alpha, cull, lo, hi, delta)) break;
+    if (!(t - p[5] > 0.0)) active = false;
+  }
+  c = SfPrefix{j, t, active};
+  return j;
+}
+
+SfScratch Sim::sf_scratch(int na, int nb, int J) {
+  const int C = (J + sf_kc - 1) / sf_kc;
+  const size_t Jpad = static_cast<size_t>(C) * sf_kc;
+  // sized for every source at once: the prefix only grows during a run
+  const size_t Jmax = (sources.size() + sf_kc - 1) / sf_kc * static_cast<size_t>(sf_kc);
+  const size_t Jcap = std::max(Jpad, Jmax);
+  SfScratch w{};
+  w.fac = d_sf_vec.ensure(4 * Jcap);
+  w.inv_s = w.fac + Jcap;
+  w.su = w.inv_s + Jcap;
+  w.sv = w.su + Jcap;
+  w.A = d_sf_A.ensure(static_cast<size_t>(na) * Jcap);
+  w.B = d_sf_B.ensure(static_cast<size_t>(nb) * Jcap);
+  w.Cpart = d_sf_C.ensure(static_cast<size_t>(na) * nb * (Jcap / sf_kc));
+  return w;
 }
 
 // ---------------------------------------------------------------------------
@@ -477,8 +620,50 @@ void Sim::flux_load_device(double t, double radius, double* d_F, int e0, int e1)
   k3_point_index(ft, d_fine.p, d_fine.p + n_fe + 1, nf, d_pt_index.p, d_elem_off.p, s);
   ++ctx->timer.launches;
   K1Flux fl{d_pt_index.p + p0, d_qn.p, d_qw.p, cfg.material.conductivity};
+  // K5 split (full-range calls): sources [0, J) by DGEMM on the face grids
+  // (plus K1 on the fine-rule points, which are not on the grids), [J, n) by K1
+  const bool full = e0 == 0 && e1 == n_fe;
+  const int J = (sf_on && sf_flux_ok && full) ? sf_prefix(t, sf_lo, sf_hi, sf_delta, sf_pf_flux) : 0;
+  sf_last_j[0] = J;
   k1_run(ctx, ctx->src6.p, ctx->n_src, d_qx.p, d_pt_index.p + p0, p1 - p0, t,
-         cfg.superpose.cull_exponent, K1Mode::flux, d_gq.p + p0, nullptr, fl, s);
+         cfg.superpose.cull_exponent, K1Mode::flux, d_gq.p + p0, nullptr, fl, s, J);
+  if (J > 0) {
+    const double alpha = ctx->mat.diffusivity(), rcp = ctx->mat.volumetric_capacity();
+    const int tqb = h_qb_off.back();
+    if (nf > 0) {
+      int nfp = 0;
+      for (int r = 0; r < nf; ++r) nfp += h_qf_off[h_fine[r] + 1] - h_qf_off[h_fine[r]];
+      int* pos = h_sf_fine;
+      int* ids = h_sf_fine + nfp;
+      int m = 0;
+      for (int r = 0; r < nf; ++r) {
+        const int e = h_fine[r];
+        const int o = h_qb_off[e] + extra[r], nq = h_qf_off[e + 1] - h_qf_off[e];
+        for (int l = 0; l < nq; ++l, ++m) {
+          pos[m] = o + l;
+          ids[m] = tqb + h_qf_off[e] + l;
+        }
+      }
+      TG_CUDA(cudaMemcpyAsync(d_sf_fine.p, h_sf_fine, sizeof(int) * 2 * nfp,
+                              cudaMemcpyHostToDevice, s));
+      K1Flux ff{d_sf_fine.p + nfp, d_qn.p, d_qw.p, cfg.material.conductivity};
+      k1_run(ctx, ctx->src6.p, ctx->n_src, d_qx.p, d_sf_fine.p + nfp, nfp, t,
+             cfg.superpose.cull_exponent, K1Mode::flux, d_sf_tmp.p, nullptr, ff, s, 0, J);
+      sf_scatter_add(nfp, d_sf_fine.p, d_sf_tmp.p, d_gq.p, s);
+      ctx->timer.launches += 1;
+      sf_pairs -= static_cast<double>(nfp) * J;
+    }
+    for (size_t k = 0; k < sf_faces_dev.size(); ++k) {
+      const SfDev& g = sf_faces_dev[k];
+      sf_flops += sf_contract(cublas, g, true, ctx->src6.p, J, sf_kc, t, alpha, rcp,
+                              sf_scratch(g.na, g.nb, J), d_sf_G.p + sf_faces_off[k], s);
+      ctx->timer.launches += 5;
+    }
+    sf_add_flux(static_cast<int>(p1 - p0), d_pt_index.p, tqb, d_sf_gcell.p, d_sf_gaxn.p,
+                d_sf_G.p, d_qn.p, d_qw.p, cfg.material.conductivity, d_gq.p, s);
+    ++ctx->timer.launches;
+    sf_pairs += static_cast<double>(p1 - p0) * J;
+  }
   k3_local(ft, e0, e1, d_elem_off.p, d_gq.p, d_loc.p, s);
   ++ctx->timer.launches;
   if (d_F) {
@@ -500,8 +685,21 @@ void Sim::dirichlet_device(double t, double* d_g, int c0, int c1) {
   if (c1 < 0) c1 = n_con;
   c0 = std::max(0, std::min(c0, n_con));
   c1 = std::max(c0, std::min(c1, n_con));
+  const int J = (sf_on && sf_dir_ok && c0 == 0 && c1 == n_con)
+                    ? sf_prefix(t, sf_dir.lo, sf_dir.hi, sf_dir.delta, sf_pf_dir)
+                    : 0;
+  sf_last_j[1] = J;
   k1_run(ctx, ctx->src6.p, ctx->n_src, d_grev.p + 3 * static_cast<size_t>(c0), nullptr, c1 - c0,
-         t, cfg.superpose.cull_exponent, K1Mode::dirichlet, d_g, nullptr, {}, ctx->stream);
+         t, cfg.superpose.cull_exponent, K1Mode::dirichlet, d_g, nullptr, {}, ctx->stream, J);
+  if (J > 0) {  // g = -(K1 part) - (GEMM part)
+    const SfDev& g = sf_dir_dev;
+    sf_flops += sf_contract(cublas, g, false, ctx->src6.p, J, sf_kc, t, ctx->mat.diffusivity(),
+                            ctx->mat.volumetric_capacity(), sf_scratch(g.na, g.nb, J),
+                            d_sf_Gdir.p, ctx->stream);
+    sf_add_dirichlet(n_con, d_sf_dcell.p, d_sf_Gdir.p, d_g, ctx->stream);
+    ctx->timer.launches += 6;
+    sf_pairs += static_cast<double>(n_con) * J;
+  }
 }
 
 PcgStatus Sim::theta_step_device(double tol, int max_iter) {

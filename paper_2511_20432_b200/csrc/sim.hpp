@@ -12,6 +12,7 @@
 #include "k2_fdm.cuh"
 #include "k2_kron.cuh"
 #include "k4_eval.cuh"
+#include "k5_sumfact.cuh"
 
 namespace tgb {
 
@@ -65,6 +66,18 @@ class Sim {
   // theta, q_tilde, q_hat, q_net
   void flux_profile(FaceId face, int n_samples, double edge_v, const double* theta_axis,
                     double* out);
+
+  // K5 (k5_sumfact.cuh): the superposition on the gridded face / Greville
+  // point sets of an axis-aligned patch as a DGEMM over the sources that no
+  // cull can touch there; K1 keeps the rest. On by default where the sets are
+  // grids (TG_SUMFACT=0 or set_sumfact(false) turns it off). Only the
+  // full-range flux / Dirichlet calls use it (the sharded range calls are K1).
+  void set_sumfact(bool on) { sf_on = on && (sf_flux_ok || sf_dir_ok); }
+  bool sf_on = false, sf_flux_ok = false, sf_dir_ok = false;
+  double sf_flops = 0.0;   // GEMM flops issued (2 na nb Jpad per set)
+  double sf_pairs = 0.0;   // point x source pairs taken off K1
+  int sf_last_j[2] = {0, 0};  // source prefix of the last flux / Dirichlet call
+  int sf_kc = 2048;           // sources per GEMM chunk (one batch entry; TG_SF_KC)
 
   bool focus_at(double t, Vec3& focus) const;
   int fine_elements(double t, double radius);  // fills h_fine, returns the count
@@ -137,6 +150,24 @@ class Sim {
  private:
   void setup_host();
   void setup_device(int device, int preconditioner);
+  void sf_setup();
+  struct SfPrefix {
+    int J = 0;
+    double t = 0.0;
+    bool valid = false;  // [0, J) were all causally active at t (reusable at later t)
+  };
+  int sf_prefix(double t, const double lo[3], const double hi[3], double delta, SfPrefix& c);
+  std::vector<SfGrid> sf_faces;
+  std::vector<SfDev> sf_faces_dev;
+  std::vector<int> sf_faces_off;
+  SfGrid sf_dir;
+  SfDev sf_dir_dev{};
+  double sf_lo[3] = {0, 0, 0}, sf_hi[3] = {0, 0, 0}, sf_delta = 0.0;
+  SfPrefix sf_pf_flux, sf_pf_dir;
+  DevBuf<double> d_sf_uv, d_sf_G, d_sf_Gdir, d_sf_vec, d_sf_A, d_sf_B, d_sf_C, d_sf_tmp;
+  DevBuf<int> d_sf_gcell, d_sf_gaxn, d_sf_dcell, d_sf_fine;
+  int* h_sf_fine = nullptr;  // pinned: fine compact positions, then their qp ids
+  SfScratch sf_scratch(int na, int nb, int J);
 };
 
 }  // namespace tgb

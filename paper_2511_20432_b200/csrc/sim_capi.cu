@@ -129,6 +129,19 @@ int tg_sim_info(tg_sim* s, long* out) {
   }, false);
 }
 
+int tg_sim_set_sumfact(tg_sim* s, int on) {
+  return sim_guard(s, [&](Sim& m) { m.set_sumfact(on != 0); });
+}
+
+int tg_sim_sumfact_stats(tg_sim* s, double* out) {
+  return sim_guard(s, [&](Sim& m) {
+    const double v[] = {m.sf_on ? 1.0 : 0.0, m.sf_flux_ok ? 1.0 : 0.0, m.sf_dir_ok ? 1.0 : 0.0,
+                        static_cast<double>(m.sf_last_j[0]), static_cast<double>(m.sf_last_j[1]),
+                        m.sf_flops, m.sf_pairs, static_cast<double>(m.sf_kc)};
+    std::memcpy(out, v, sizeof(v));
+  });
+}
+
 int tg_sim_params(tg_sim* s, double* out) {
   return sim_guard(s, [&](Sim& m) {
     const double v[] = {m.dt_solver, m.cfg.stepping.theta, m.cfg.stepping.solver_tol,

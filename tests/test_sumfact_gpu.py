@@ -1,0 +1,134 @@
+"""K5 (sum-factorised superposition, csrc/k5_sumfact.cu) against the unmodified
+reference and against the K1 pair loop.
+
+K5 evaluates the superposition at the lateral-face quadrature points and the
+bottom Greville points of an axis-aligned patch as a DGEMM over the sources
+that no cull can reach there (old sources of a long scan), K1 keeping the
+young ones with the reference's exact cull. Tolerances are the hot path's
+(BASELINE.json north_star): loads and Dirichlet values normwise <= 1e-10 with
+the reference's exact zeros reproduced (the Dirichlet values also pointwise),
+correction-field coefficients normwise <= 1e-8 every step.
+"""
+import os
+
+import numpy as np
+import pytest
+
+import paper_2511_20432_b200 as tg
+from conftest import ROOT
+
+pytestmark = pytest.mark.gpu
+
+
+def normwise(a, b):
+    m = np.abs(b).max()
+    return 0.0 if m == 0 else np.abs(a - b).max() / m
+
+
+def pointwise(a, b):
+    nz = b != 0.0
+    assert np.array_equal(a == 0.0, ~nz)
+    return 0.0 if not nz.any() else float((np.abs(a - b)[nz] / np.abs(b[nz])).max())
+
+
+def long_history_cfg(tmp_path, start_time=-0.015):
+    """config 0's cuboid under a 9-track raster (2125 sources, 21 ms) that started
+    15 ms before t = 0: at t = 0 the oldest ~1500 sources are GEMM-eligible, a few
+    hundred active young ones stay on K1 (with culled pairs), the rest are not yet
+    active; the fine rule engages (every track is within 0.5 mm of a y face)."""
+    txt = open(os.path.join(ROOT, "configs", "cfg0_parity.cfg")).read()
+    head, rest = txt.split("[scan]", 1)
+    tail = rest[rest.index("[faces]"):]
+    wp = []
+    for i, y in enumerate(np.arange(1, 10) * 1e-4):
+        xs = (1e-4, 1.9e-3) if i % 2 == 0 else (1.9e-3, 1e-4)
+        wp += [(xs[0], y), (xs[1], y)]
+    scan = ["[scan]", f"start_time = {start_time!r}", "plane_z = 0.0005"]
+    scan += [f"waypoint = {float(x)!r} {float(y)!r}" for x, y in wp]
+    p = tmp_path / "long_history.cfg"
+    p.write_text(head + "\n".join(scan) + "\n\n" + tail)
+    return str(p)
+
+
+def test_sumfact_against_live_reference(ref, tmp_path):
+    path = long_history_cfg(tmp_path)
+    s = tg.Simulation(path, t_end=2e-4)
+    st = s.sumfact_stats()
+    assert st["on"] and st["faces_gridded"] and st["greville_gridded"]
+    n_src = s.info["n_sources"]
+    r = ref.sim(path, t_end=2e-4)
+    for t in (0.0, 5e-5, 1e-4, 2e-4):
+        F, Fr = s.flux_load(t), r.flux_load(t)
+        j = s.sumfact_stats()["last_j_flux"]
+        assert 0 < j < n_src, j  # both paths carry sources
+        assert normwise(F, Fr) <= 1e-10, t
+        assert np.array_equal(F == 0.0, Fr == 0.0), t
+        d, dr = s.dirichlet_values(t), r.dirichlet(t)
+        assert 0 < s.sumfact_stats()["last_j_dirichlet"] < n_src
+        assert normwise(d, dr) <= 1e-10, t
+        assert pointwise(d, dr) <= 1e-10, t
+    for rad in (0.0, 1.0):  # fine rule off / on everywhere
+        assert normwise(s.flux_load(1e-4, rad), r.flux_load_radius(1e-4, rad)) <= 1e-10
+    s.close()
+    r.close()
+
+
+def test_sumfact_time_loop_against_live_reference(ref, tmp_path):
+    path = long_history_cfg(tmp_path)
+    s = tg.Simulation(path, t_end=2e-4)
+    r = ref.sim(path, t_end=2e-4)
+    s.reset()
+    F0, g0 = r.reset()
+    st = s.state()
+    assert normwise(st["F"], F0) <= 1e-10 and normwise(st["g"], g0) <= 1e-10
+    for k in range(1, 21):
+        s.advance(1)
+        st = s.state()
+        o = r.step()
+        assert normwise(st["F"], o["F"]) <= 1e-10, k
+        assert normwise(st["g"], o["g"]) <= 1e-10, k
+        assert normwise(st["free"], o["free"]) <= 1e-8, k
+    assert s.sumfact_stats()["gemm_flops"] > 0
+    s.close()
+    r.close()
+
+
+def test_sumfact_on_off_and_causal_zero(tmp_path):
+    s = tg.Simulation(long_history_cfg(tmp_path), t_end=2e-4)
+    for t in (0.0, 1.5e-4):
+        F1, d1 = s.flux_load(t), s.dirichlet_values(t)
+        s.set_sumfact(False)
+        F0, d0 = s.flux_load(t), s.dirichlet_values(t)
+        assert s.sumfact_stats()["last_j_flux"] == 0
+        s.set_sumfact(True)
+        assert normwise(F1, F0) <= 1e-12 and np.array_equal(F1 == 0.0, F0 == 0.0)
+        assert pointwise(d1, d0) <= 1e-12
+    # before every modified time: every source is eligible and contributes exactly 0
+    assert not np.any(s.flux_load(-1.0)) and not np.any(s.dirichlet_values(-1.0))
+    s.close()
+
+
+def test_sumfact_not_used_on_curved_patch():
+    s = tg.Simulation(os.path.join(ROOT, "configs", "qc_small.cfg"))
+    st = s.sumfact_stats()
+    assert not st["faces_gridded"]
+    s.flux_load(1e-4)
+    assert s.sumfact_stats()["last_j_flux"] == 0
+    s.close()
+
+
+def test_sumfact_config4_full_size():
+    """Config 4 (1e5 sources, 99,000 already active at t = 0): K5 against the
+    K1 pair loop over every point at two instants of the run."""
+    s = tg.Simulation(os.path.join(ROOT, "configs", "cfg4_large.cfg"))
+    for t in (1e-5, 2.5e-3):
+        F1, d1 = s.flux_load(t), s.dirichlet_values(t)
+        st = s.sumfact_stats()
+        assert st["last_j_flux"] > 80000 and st["last_j_dirichlet"] > 80000, st
+        s.set_sumfact(False)
+        F0, d0 = s.flux_load(t), s.dirichlet_values(t)
+        s.set_sumfact(True)
+        assert normwise(F1, F0) <= 1e-12, t
+        assert np.array_equal(F1 == 0.0, F0 == 0.0)
+        assert pointwise(d1, d0) <= 1e-12, t
+    s.close()
