@@ -347,6 +347,13 @@ def theta_section(steps, warmup, with_cpu):
     wall = time.perf_counter() - t0
     prof = ctx.profile()
     ctx.set_profiling(False)
+    sf = sim.sumfact_stats()
+    # the same steps with every superposition pair on K1 (K5 off), for the split
+    sim.set_sumfact(False)
+    t1 = time.perf_counter()
+    sim.advance(steps)
+    wall_k1 = time.perf_counter() - t1
+    sim.set_sumfact(True)
     dofs = sim.info["n_full"]
     solver = {2: "single-sweep Chronopoulos-Gear Jacobi-PCG (one tile sweep + one grid "
                  "reduction per iteration)",
@@ -369,6 +376,14 @@ def theta_section(steps, warmup, with_cpu):
                                  "step: expand + theta RHS + solve (theta_step, "
                                  "timestep.cpp:5-24); theta_ms_* are the solve alone",
         "k1_ms_per_step": prof["k1_ms"] / steps,
+        "k5": {"note": "sum-factorised superposition (csrc/k5_sumfact.cu): flux load and "
+                       "Dirichlet values over the sources no cull reaches on the face / "
+                       "Greville grids as cuBLAS DGEMMs (FP64 tensor cores); K1 keeps the "
+                       "rest (k1_ms_per_step)",
+               "sources_on_gemm": sf["last_j_flux"], "sources": sim.info["n_sources"],
+               "gemm_flops_per_step": sf["gemm_flops"] / (warmup + steps + 1),
+               "ms_per_step_with_k1_only": wall_k1 * 1e3 / steps,
+               "k1_pairs_per_step_moved": sf["pairs_off_k1"] / (warmup + steps + 1)},
         "cg_iterations_per_step": iters / steps,
         "solver": solver,
         "roofline": {"kernel": kernel, "bound": "hbm",

@@ -151,6 +151,24 @@ __global__ void sf_add_dirichlet_kernel(int n, const int* __restrict__ gcell,
   g[i] = __dsub_rn(g[i], G[gcell[i]]);
 }
 
+__global__ void sf_add_fine_kernel(int n, const int* __restrict__ pos,
+                                   const int* __restrict__ ids, int n_base,
+                                   const int* __restrict__ fa, const int* __restrict__ fb,
+                                   const int* __restrict__ ff, const int* __restrict__ rect,
+                                   const double* __restrict__ G,
+                                   const double* __restrict__ normals,
+                                   const double* __restrict__ weights, double k,
+                                   double* __restrict__ gq) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int q = ids[i];
+  const int* r = rect + 5 * ff[q];
+  const double gv = G[r[3] + (fa[q] - r[0]) + r[2] * (fb[q] - r[1])];
+  const size_t qq = static_cast<size_t>(n_base) + q;
+  const double dot = __dmul_rn(gv, normals[3 * qq + r[4]]);
+  gq[pos[i]] = __dadd_rn(gq[pos[i]], __dmul_rn(__dmul_rn(-k, dot), weights[qq]));
+}
+
 __global__ void sf_scatter_add_kernel(int n, const int* __restrict__ pos,
                                       const double* __restrict__ tmp, double* __restrict__ gq) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -256,6 +274,15 @@ void sf_add_flux(int n, const int* d_pt_index, int n_base, const int* d_gcell, c
 void sf_add_dirichlet(int n, const int* d_gcell, const double* d_G, double* d_g, cudaStream_t s) {
   if (n <= 0) return;
   sf_add_dirichlet_kernel<<<(n + 255) / 256, 256, 0, s>>>(n, d_gcell, d_G, d_g);
+}
+
+void sf_add_fine(int n, const int* d_pos, const int* d_ids, int n_base, const int* d_fa,
+                 const int* d_fb, const int* d_ff, const int* d_rect, const double* d_G,
+                 const double* d_normals, const double* d_weights, double k, double* d_gq,
+                 cudaStream_t s) {
+  if (n <= 0) return;
+  sf_add_fine_kernel<<<(n + 255) / 256, 256, 0, s>>>(n, d_pos, d_ids, n_base, d_fa, d_fb, d_ff,
+                                                      d_rect, d_G, d_normals, d_weights, k, d_gq);
 }
 
 void sf_scatter_add(int n, const int* d_pos, const double* d_tmp, double* d_gq, cudaStream_t s) {

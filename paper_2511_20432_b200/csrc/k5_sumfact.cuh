@@ -68,6 +68,14 @@ void sf_add_flux(int n, const int* d_pt_index, int n_base, const int* d_gcell, c
                  double* d_gq, cudaStream_t s);
 // g[c] -= G[gcell[c]] (g = -T~ at the Greville points)
 void sf_add_dirichlet(int n, const int* d_gcell, const double* d_G, double* d_g, cudaStream_t s);
+// fine-rule points: i < n, q = ids[i] (fine point index), face f = ff[q] with
+// rect[5 f..] = a0, b0, na, G offset, normal axis of the step's rectangle:
+//   gq[pos[i]] += (-k (G[off + (fa[q] - a0) + na (fb[q] - b0)] n[axn])) w
+// (normals / weights indexed by n_base + q)
+void sf_add_fine(int n, const int* d_pos, const int* d_ids, int n_base, const int* d_fa,
+                 const int* d_fb, const int* d_ff, const int* d_rect, const double* d_G,
+                 const double* d_normals, const double* d_weights, double k, double* d_gq,
+                 cudaStream_t s);
 // gq[pos[i]] += tmp[i]
 void sf_scatter_add(int n, const int* d_pos, const double* d_tmp, double* d_gq, cudaStream_t s);
 

@@ -83,6 +83,7 @@ Sim::~Sim() {
   if (h_status) cudaFreeHost(h_status);
   if (h_fine) cudaFreeHost(h_fine);
   if (h_sf_fine) cudaFreeHost(h_sf_fine);
+  if (h_sf_rect) cudaFreeHost(h_sf_rect);
   if (ctx) tg_ctx_destroy(ctx);
 }
 
@@ -448,19 +449,26 @@ void Sim::sf_setup() {
   std::vector<int> gcell(tqb, -1), gaxn(tqb, 0);
   sf_flux_ok = tqb > 0;
   std::vector<std::vector<int>> groups(6);
-  for (int q = 0; q < tqb && sf_flux_ok; ++q) {
-    const double* n = &h_qn[3 * q];
+  auto normal_key = [&](int q) {  // 2 axis + (sign > 0), or -1 off the axes
+    const double* n = &h_qn[3 * static_cast<size_t>(q)];
     int ax = 0;
     for (int d = 1; d < 3; ++d)
       if (std::fabs(n[d]) > std::fabs(n[ax])) ax = d;
     const bool axis = std::fabs(std::fabs(n[ax]) - 1.0) <= 1e-12 &&
                       std::fabs(n[(ax + 1) % 3]) <= 1e-12 && std::fabs(n[(ax + 2) % 3]) <= 1e-12;
-    if (!axis) sf_flux_ok = false;
-    groups[2 * ax + (n[ax] > 0.0)].push_back(q);
+    return axis ? 2 * ax + (n[ax] > 0.0) : -1;
+  };
+  std::vector<int> qkey(tqb, -1);
+  for (int q = 0; q < tqb && sf_flux_ok; ++q) {
+    qkey[q] = normal_key(q);
+    if (qkey[q] < 0) sf_flux_ok = false;
+    else groups[qkey[q]].push_back(q);
   }
+  int face_of_key[6] = {-1, -1, -1, -1, -1, -1};
   int off = 0;
   for (int k = 0; k < 6 && sf_flux_ok; ++k) {
     if (groups[k].empty()) continue;
+    face_of_key[k] = static_cast<int>(sf_faces.size());
     std::vector<double> pts(3 * groups[k].size());
     for (size_t i = 0; i < groups[k].size(); ++i)
       for (int d = 0; d < 3; ++d) pts[3 * i + d] = h_qx[3 * groups[k][i] + d];
@@ -477,10 +485,68 @@ void Sim::sf_setup() {
     off += static_cast<int>(g.U.size() * g.V.size());
     sf_faces.push_back(std::move(g));
   }
+  // fine-rule points: per face, the fine points of all its elements form a
+  // finer grid; a step's fine elements take a rectangle of it
+  const int tqf = h_qf_off.empty() ? 0 : h_qf_off.back();
+  sf_fine_ok = sf_flux_ok && tqf > 0;
+  std::vector<int> fa(tqf), fb(tqf), ff(tqf);
+  if (sf_fine_ok) {
+    sf_elem_face.assign(n_fe, -1);
+    sf_erect.assign(4 * static_cast<size_t>(n_fe), 0);
+    std::vector<std::vector<int>> felems(sf_faces.size());
+    for (int e = 0; e < n_fe && sf_fine_ok; ++e) {
+      const int f = face_of_key[qkey[h_qb_off[e]]];
+      for (int q = h_qb_off[e]; q < h_qb_off[e + 1]; ++q)
+        if (face_of_key[qkey[q]] != f) sf_fine_ok = false;
+      for (int l = h_qf_off[e]; l < h_qf_off[e + 1]; ++l)
+        if (face_of_key[std::max(0, normal_key(tqb + l))] != f || normal_key(tqb + l) < 0)
+          sf_fine_ok = false;
+      sf_elem_face[e] = f;
+      felems[f].push_back(e);
+    }
+    for (size_t f = 0; f < felems.size() && sf_fine_ok; ++f) {
+      std::vector<double> pts;
+      for (int e : felems[f])
+        for (int l = h_qf_off[e]; l < h_qf_off[e + 1]; ++l)
+          for (int d = 0; d < 3; ++d) pts.push_back(h_qx[3 * static_cast<size_t>(tqb + l) + d]);
+      SfGrid g;
+      if (!sf_make_grid(pts.data(), static_cast<long>(pts.size() / 3), tol, g) ||
+          g.axn != sf_faces[f].axn) {
+        sf_fine_ok = false;
+        break;
+      }
+      const int na = static_cast<int>(g.U.size());
+      size_t i = 0;
+      for (int e : felems[f]) {
+        int* r = &sf_erect[4 * static_cast<size_t>(e)];
+        r[0] = r[1] = 1 << 30;
+        r[2] = r[3] = -1;
+        for (int l = h_qf_off[e]; l < h_qf_off[e + 1]; ++l, ++i) {
+          const int a = g.cell[i] % na, b = g.cell[i] / na;
+          fa[l] = a;
+          fb[l] = b;
+          ff[l] = static_cast<int>(f);
+          r[0] = std::min(r[0], a);
+          r[1] = std::min(r[1], b);
+          r[2] = std::max(r[2], a);
+          r[3] = std::max(r[3], b);
+        }
+      }
+      sf_fine.push_back(std::move(g));
+    }
+    if (!sf_fine_ok) sf_fine.clear();
+  }
   if (sf_flux_ok) {
     for (int ax = 0; ax < 3; ++ax) {
       sf_lo[ax] = 1e300;
       sf_hi[ax] = -1e300;
+    }
+    for (const SfGrid& g : sf_fine) {  // the eligibility box covers the fine points too
+      for (int ax = 0; ax < 3; ++ax) {
+        sf_lo[ax] = std::min(sf_lo[ax], g.lo[ax]);
+        sf_hi[ax] = std::max(sf_hi[ax], g.hi[ax]);
+      }
+      sf_delta = std::max(sf_delta, g.delta);
     }
     for (const SfGrid& g : sf_faces) {
       for (int ax = 0; ax < 3; ++ax) {
@@ -503,6 +569,7 @@ void Sim::sf_setup() {
     uv.insert(uv.end(), g.V.begin(), g.V.end());
   };
   for (const SfGrid& g : sf_faces) push(g);
+  for (const SfGrid& g : sf_fine) push(g);
   if (sf_dir_ok) push(sf_dir);
   if (uv.empty()) return;
   upload(d_sf_uv, uv, s);
@@ -511,6 +578,15 @@ void Sim::sf_setup() {
     return SfDev{g.axn, g.axu, g.axv, na, nb, g.xf, d_sf_uv.p + a, d_sf_uv.p + a + na};
   };
   for (size_t k = 0; k < sf_faces.size(); ++k) sf_faces_dev.push_back(dev(sf_faces[k], at[k]));
+  for (size_t k = 0; k < sf_fine.size(); ++k)
+    sf_fine_dev.push_back(dev(sf_fine[k], at[sf_faces.size() + k]));
+  if (sf_fine_ok) {
+    upload(d_sf_fa, fa, s);
+    upload(d_sf_fb, fb, s);
+    upload(d_sf_ff, ff, s);
+    d_sf_rect.ensure(5 * sf_fine.size());
+    TG_CUDA(cudaMallocHost(&h_sf_rect, sizeof(int) * 5 * sf_fine.size()));
+  }
   if (sf_dir_ok) {
     sf_dir_dev = dev(sf_dir, at.back());
     upload(d_sf_dcell, sf_dir.cell, s);
@@ -630,7 +706,68 @@ void Sim::flux_load_device(double t, double radius, double* d_F, int e0, int e1)
   if (J > 0) {
     const double alpha = ctx->mat.diffusivity(), rcp = ctx->mat.volumetric_capacity();
     const int tqb = h_qb_off.back();
-    if (nf > 0) {
+    if (nf > 0 && sf_fine_ok) {
+      // the step's fine elements: per face the bounding rectangle of their
+      // cells in the face's fine grid, one GEMM each
+      const size_t nF = sf_fine.size();
+      std::vector<int> rc(4 * nF);
+      for (size_t f = 0; f < nF; ++f) {
+        rc[4 * f] = rc[4 * f + 1] = 1 << 30;
+        rc[4 * f + 2] = rc[4 * f + 3] = -1;
+      }
+      int nfp = 0;
+      for (int r = 0; r < nf; ++r) {
+        const int e = h_fine[r], f = sf_elem_face[e];
+        const int* er = &sf_erect[4 * static_cast<size_t>(e)];
+        rc[4 * f] = std::min(rc[4 * f], er[0]);
+        rc[4 * f + 1] = std::min(rc[4 * f + 1], er[1]);
+        rc[4 * f + 2] = std::max(rc[4 * f + 2], er[2]);
+        rc[4 * f + 3] = std::max(rc[4 * f + 3], er[3]);
+        nfp += h_qf_off[e + 1] - h_qf_off[e];
+      }
+      size_t gtot = 0;
+      for (size_t f = 0; f < nF; ++f) {
+        int* hr = h_sf_rect + 5 * f;
+        const bool any = rc[4 * f + 2] >= 0;
+        hr[0] = rc[4 * f];
+        hr[1] = rc[4 * f + 1];
+        hr[2] = any ? rc[4 * f + 2] - rc[4 * f] + 1 : 0;
+        hr[3] = static_cast<int>(gtot);
+        hr[4] = sf_fine[f].axn;
+        if (any) gtot += static_cast<size_t>(hr[2]) * (rc[4 * f + 3] - rc[4 * f + 1] + 1);
+      }
+      double* Gf = d_sf_Gf.ensure(gtot);
+      for (size_t f = 0; f < nF; ++f) {
+        const int* hr = h_sf_rect + 5 * f;
+        if (hr[2] == 0) continue;
+        SfDev g = sf_fine_dev[f];
+        g.U += hr[0];
+        g.V += hr[1];
+        g.na = hr[2];
+        g.nb = rc[4 * f + 3] - rc[4 * f + 1] + 1;
+        sf_flops += sf_contract(cublas, g, true, ctx->src6.p, J, sf_kc, t, alpha, rcp,
+                                sf_scratch(g.na, g.nb, J), Gf + hr[3], s);
+        ctx->timer.launches += 5;
+      }
+      int* pos = h_sf_fine;
+      int* ids = h_sf_fine + nfp;
+      int m = 0;
+      for (int r = 0; r < nf; ++r) {
+        const int e = h_fine[r];
+        const int o = h_qb_off[e] + extra[r], nq = h_qf_off[e + 1] - h_qf_off[e];
+        for (int l = 0; l < nq; ++l, ++m) {
+          pos[m] = o + l;
+          ids[m] = h_qf_off[e] + l;
+        }
+      }
+      TG_CUDA(cudaMemcpyAsync(d_sf_fine.p, h_sf_fine, sizeof(int) * 2 * nfp,
+                              cudaMemcpyHostToDevice, s));
+      TG_CUDA(cudaMemcpyAsync(d_sf_rect.p, h_sf_rect, sizeof(int) * 5 * nF,
+                              cudaMemcpyHostToDevice, s));
+      sf_add_fine(nfp, d_sf_fine.p, d_sf_fine.p + nfp, tqb, d_sf_fa.p, d_sf_fb.p, d_sf_ff.p,
+                  d_sf_rect.p, Gf, d_qn.p, d_qw.p, cfg.material.conductivity, d_gq.p, s);
+      ++ctx->timer.launches;
+    } else if (nf > 0) {
       int nfp = 0;
       for (int r = 0; r < nf; ++r) nfp += h_qf_off[h_fine[r] + 1] - h_qf_off[h_fine[r]];
       int* pos = h_sf_fine;

@@ -160,6 +160,13 @@ class Sim {
   std::vector<SfGrid> sf_faces;
   std::vector<SfDev> sf_faces_dev;
   std::vector<int> sf_faces_off;
+  bool sf_fine_ok = false;  // fine-rule points gridded per face too
+  std::vector<SfGrid> sf_fine;
+  std::vector<SfDev> sf_fine_dev;
+  std::vector<int> sf_elem_face, sf_erect;  // per face element: face, fine-cell rectangle
+  DevBuf<int> d_sf_fa, d_sf_fb, d_sf_ff, d_sf_rect;
+  DevBuf<double> d_sf_Gf;
+  int* h_sf_rect = nullptr;
   SfGrid sf_dir;
   SfDev sf_dir_dev{};
   double sf_lo[3] = {0, 0, 0}, sf_hi[3] = {0, 0, 0}, sf_delta = 0.0;
