@@ -267,8 +267,8 @@ int tg_sim_flux_profile(tg_sim* sim, int face, int n_samples, double edge_v,
  * available; on = 0 makes every superposition a K1 pair loop. */
 int tg_sim_set_sumfact(tg_sim* sim, int on);
 /* out[8]: on, faces gridded, Greville grid, source prefix J of the last flux
- * call, of the last Dirichlet call, GEMM flops issued, point x source pairs
- * taken off K1, sources per GEMM chunk */
+ * call (the smallest over the faces), of the last Dirichlet call, GEMM flops
+ * issued, point x source pairs evaluated by the GEMMs, sources per GEMM chunk */
 int tg_sim_sumfact_stats(tg_sim* sim, double* out);
 
 #ifdef __cplusplus

@@ -91,31 +91,42 @@ __global__ void sf_prep_kernel(const double* __restrict__ src6, int J, int Jpad,
   sv[j] = v;
 }
 
-// A (na x Jpad, column-major): fac_j e^{-(U_a - u_j)^2 / s_j}
-__global__ void sf_build_a_kernel(SfDev g, size_t total, const double* __restrict__ fac,
+// A (na x Jpad, column-major): fac_j e^{-(U_a - u_j)^2 / s_j}; x: rows a,
+// y: groups of kJA sources (2D grid, no 64-bit index division)
+constexpr int kJA = 16;
+__global__ void sf_build_a_kernel(SfDev g, int Jpad, const double* __restrict__ fac,
                                   const double* __restrict__ inv_s, const double* __restrict__ su,
                                   double* __restrict__ A) {
-  for (size_t e = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; e < total;
-       e += static_cast<size_t>(gridDim.x) * blockDim.x) {
-    const size_t j = e / g.na;
-    const int a = static_cast<int>(e - j * g.na);
-    const double d = g.U[a] - su[j];
-    A[e] = fac[j] * exp(-(d * d) * inv_s[j]);
+  const int a = blockIdx.x * blockDim.x + threadIdx.x;
+  if (a >= g.na) return;
+  const double ua = g.U[a];
+  const int j0 = blockIdx.y * kJA;
+#pragma unroll 4
+  for (int jj = 0; jj < kJA; ++jj) {
+    const int j = j0 + jj;
+    if (j >= Jpad) break;
+    const double d = ua - su[j];
+    A[static_cast<size_t>(j) * g.na + a] = fac[j] * exp(-(d * d) * inv_s[j]);
   }
 }
 
-// B, chunk c of Kc sources as a (Kc x nb) column-major block: e^{-(V_b - v_j)^2 / s_j}
-__global__ void sf_build_b_kernel(SfDev g, size_t total, int Kc, const double* __restrict__ inv_s,
+// B, chunk c of Kc sources as a (Kc x nb) column-major block: e^{-(V_b - v_j)^2 / s_j};
+// x: sources, y: groups of kBB rows b
+constexpr int kBB = 8;
+__global__ void sf_build_b_kernel(SfDev g, int Jpad, int Kc, const double* __restrict__ inv_s,
                                   const double* __restrict__ sv, double* __restrict__ B) {
-  const size_t blk = static_cast<size_t>(Kc) * g.nb;
-  for (size_t e = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; e < total;
-       e += static_cast<size_t>(gridDim.x) * blockDim.x) {
-    const size_t c = e / blk;
-    const size_t rem = e - c * blk;
-    const size_t b = rem / Kc;
-    const size_t j = c * Kc + (rem - b * Kc);
-    const double d = g.V[b] - sv[j];
-    B[e] = exp(-(d * d) * inv_s[j]);
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= Jpad) return;
+  const int c = j / Kc, jj = j - c * Kc;
+  const double is = inv_s[j], v = sv[j];
+  double* out = B + static_cast<size_t>(c) * Kc * g.nb + jj;
+  const int b0 = blockIdx.y * kBB;
+#pragma unroll 4
+  for (int bb = 0; bb < kBB; ++bb) {
+    const int b = b0 + bb;
+    if (b >= g.nb) break;
+    const double d = g.V[b] - v;
+    out[static_cast<size_t>(b) * Kc] = exp(-(d * d) * is);
   }
 }
 
@@ -174,10 +185,6 @@ __global__ void sf_scatter_add_kernel(int n, const int* __restrict__ pos,
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   gq[pos[i]] = __dadd_rn(gq[pos[i]], tmp[i]);
-}
-
-int blocks_for(size_t n, int threads, int cap = 148 * 16) {
-  return static_cast<int>(std::min<size_t>((n + threads - 1) / threads, cap));
 }
 
 }  // namespace
@@ -242,14 +249,21 @@ bool sf_source_eligible(const double* p, double t, double alpha, double cull, co
 double sf_contract(cublasHandle_t h, const SfDev& g, bool grad, const double* d_src6, int J,
                    int Kc, double t, double alpha, double rcp, const SfScratch& w, double* d_G,
                    cudaStream_t s) {
+  if (J <= 0) {  // nothing eligible: the callers add G
+    TG_CUDA(cudaMemsetAsync(d_G, 0, sizeof(double) * g.na * g.nb, s));
+    return 0.0;
+  }
   const int C = (J + Kc - 1) / Kc;
   const int Jpad = C * Kc;
   constexpr int T = 256;
   sf_prep_kernel<<<(Jpad + T - 1) / T, T, 0, s>>>(d_src6, J, Jpad, t, alpha, rcp, g, grad, w.fac,
                                                    w.inv_s, w.su, w.sv);
-  const size_t na_tot = static_cast<size_t>(g.na) * Jpad, nb_tot = static_cast<size_t>(g.nb) * Jpad;
-  sf_build_a_kernel<<<blocks_for(na_tot, T), T, 0, s>>>(g, na_tot, w.fac, w.inv_s, w.su, w.A);
-  sf_build_b_kernel<<<blocks_for(nb_tot, T), T, 0, s>>>(g, nb_tot, Kc, w.inv_s, w.sv, w.B);
+  // (grid.y <= 65535: up to ~1e6 sources per contraction)
+  const int TA = g.na >= 256 ? 256 : 128;
+  sf_build_a_kernel<<<dim3((g.na + TA - 1) / TA, (Jpad + kJA - 1) / kJA), TA, 0, s>>>(
+      g, Jpad, w.fac, w.inv_s, w.su, w.A);
+  sf_build_b_kernel<<<dim3((Jpad + T - 1) / T, (g.nb + kBB - 1) / kBB), T, 0, s>>>(
+      g, Jpad, Kc, w.inv_s, w.sv, w.B);
   const double one = 1.0, zero = 0.0;
   cublas_ok(cublasSetStream(h, s), "set stream");
   cublas_ok(cublasDgemmStridedBatched(h, CUBLAS_OP_N, CUBLAS_OP_N, g.na, g.nb, Kc, &one, w.A,

@@ -536,6 +536,28 @@ void Sim::sf_setup() {
     }
     if (!sf_fine_ok) sf_fine.clear();
   }
+  // per-face source prefixes need each face's elements contiguous (one K1
+  // launch per face) and its fine points gridded (the GEMM covers them)
+  sf_face_split = sf_fine_ok;
+  if (sf_face_split) {
+    const size_t nfc = sf_faces.size();
+    sf_face_e.assign(2 * nfc, -1);
+    for (int e = 0; e < n_fe; ++e) {
+      const int f = sf_elem_face[e];
+      if (sf_face_e[2 * f] < 0) sf_face_e[2 * f] = e;
+      else if (sf_face_e[2 * f + 1] != e) sf_face_split = false;
+      sf_face_e[2 * f + 1] = e + 1;
+    }
+    sf_face_box.assign(6 * nfc, 0.0);
+    sf_face_delta.assign(nfc, 0.0);
+    sf_pf_face.assign(nfc, SfPrefix{});
+    for (size_t f = 0; f < nfc; ++f)
+      for (int ax = 0; ax < 3; ++ax) {
+        sf_face_box[6 * f + ax] = std::min(sf_faces[f].lo[ax], sf_fine[f].lo[ax]);
+        sf_face_box[6 * f + 3 + ax] = std::max(sf_faces[f].hi[ax], sf_fine[f].hi[ax]);
+        sf_face_delta[f] = std::max(sf_faces[f].delta, sf_fine[f].delta);
+      }
+  }
   if (sf_flux_ok) {
     for (int ax = 0; ax < 3; ++ax) {
       sf_lo[ax] = 1e300;
@@ -616,7 +638,8 @@ int Sim::sf_prefix(double t, const double lo[3], const double hi[3], double delt
   const double alpha = ctx->mat.diffusivity();
   const double cull = cfg.superpose.cull_exponent;
   const double* src = reinterpret_cast<const double*>(sources.data());
-  const int n = static_cast<int>(sources.size());
+  // (the GEMM builders' 2D grids address up to ~1e6 sources; later ones stay on K1)
+  const int n = std::min(static_cast<int>(sources.size()), 1000000);
   int j = (c.valid && t >= c.t) ? c.J : 0;
   bool active = true;
   for (; j < n; ++j) {
@@ -699,11 +722,40 @@ void Sim::flux_load_device(double t, double radius, double* d_F, int e0, int e1)
   // K5 split (full-range calls): sources [0, J) by DGEMM on the face grids
   // (plus K1 on the fine-rule points, which are not on the grids), [J, n) by K1
   const bool full = e0 == 0 && e1 == n_fe;
-  const int J = (sf_on && sf_flux_ok && full) ? sf_prefix(t, sf_lo, sf_hi, sf_delta, sf_pf_flux) : 0;
+  // per face the longest eligible prefix for that face's box (faces whose
+  // elements are contiguous and gridded with their fine points), else one
+  // prefix for the box of all faces
+  const size_t nfc = sf_faces.size();
+  std::vector<int> Jf(nfc, 0);
+  int J = 0, Jmax = 0;
+  if (sf_on && sf_flux_ok && full) {
+    if (sf_face_split) {
+      J = 1 << 30;
+      for (size_t f = 0; f < nfc; ++f) {
+        Jf[f] = sf_prefix(t, &sf_face_box[6 * f], &sf_face_box[6 * f + 3], sf_face_delta[f],
+                          sf_pf_face[f]);
+        J = std::min(J, Jf[f]);
+        Jmax = std::max(Jmax, Jf[f]);
+      }
+    } else {
+      J = Jmax = sf_prefix(t, sf_lo, sf_hi, sf_delta, sf_pf_flux);
+      std::fill(Jf.begin(), Jf.end(), J);
+    }
+  }
   sf_last_j[0] = J;
-  k1_run(ctx, ctx->src6.p, ctx->n_src, d_qx.p, d_pt_index.p + p0, p1 - p0, t,
-         cfg.superpose.cull_exponent, K1Mode::flux, d_gq.p + p0, nullptr, fl, s, J);
-  if (J > 0) {
+  if (Jmax > 0 && sf_face_split) {
+    auto pos_of = [&](int e) { return e == n_fe ? p1 : offset_of(e); };
+    for (size_t f = 0; f < nfc; ++f) {
+      const long a = pos_of(sf_face_e[2 * f]), b = pos_of(sf_face_e[2 * f + 1]);
+      K1Flux ff{d_pt_index.p + a, d_qn.p, d_qw.p, cfg.material.conductivity};
+      k1_run(ctx, ctx->src6.p, ctx->n_src, d_qx.p, d_pt_index.p + a, b - a, t,
+             cfg.superpose.cull_exponent, K1Mode::flux, d_gq.p + a, nullptr, ff, s, Jf[f]);
+    }
+  } else {
+    k1_run(ctx, ctx->src6.p, ctx->n_src, d_qx.p, d_pt_index.p + p0, p1 - p0, t,
+           cfg.superpose.cull_exponent, K1Mode::flux, d_gq.p + p0, nullptr, fl, s, J);
+  }
+  if (Jmax > 0) {
     const double alpha = ctx->mat.diffusivity(), rcp = ctx->mat.volumetric_capacity();
     const int tqb = h_qb_off.back();
     if (nf > 0 && sf_fine_ok) {
@@ -745,8 +797,9 @@ void Sim::flux_load_device(double t, double radius, double* d_F, int e0, int e1)
         g.V += hr[1];
         g.na = hr[2];
         g.nb = rc[4 * f + 3] - rc[4 * f + 1] + 1;
-        sf_flops += sf_contract(cublas, g, true, ctx->src6.p, J, sf_kc, t, alpha, rcp,
-                                sf_scratch(g.na, g.nb, J), Gf + hr[3], s);
+        sf_flops += sf_contract(cublas, g, true, ctx->src6.p, Jf[f], sf_kc, t, alpha, rcp,
+                                sf_scratch(g.na, g.nb, Jf[f]), Gf + hr[3], s);
+        sf_pairs += static_cast<double>(g.na) * g.nb * Jf[f];
         ctx->timer.launches += 5;
       }
       int* pos = h_sf_fine;
@@ -788,18 +841,17 @@ void Sim::flux_load_device(double t, double radius, double* d_F, int e0, int e1)
              cfg.superpose.cull_exponent, K1Mode::flux, d_sf_tmp.p, nullptr, ff, s, 0, J);
       sf_scatter_add(nfp, d_sf_fine.p, d_sf_tmp.p, d_gq.p, s);
       ctx->timer.launches += 1;
-      sf_pairs -= static_cast<double>(nfp) * J;
     }
     for (size_t k = 0; k < sf_faces_dev.size(); ++k) {
       const SfDev& g = sf_faces_dev[k];
-      sf_flops += sf_contract(cublas, g, true, ctx->src6.p, J, sf_kc, t, alpha, rcp,
-                              sf_scratch(g.na, g.nb, J), d_sf_G.p + sf_faces_off[k], s);
+      sf_flops += sf_contract(cublas, g, true, ctx->src6.p, Jf[k], sf_kc, t, alpha, rcp,
+                              sf_scratch(g.na, g.nb, Jf[k]), d_sf_G.p + sf_faces_off[k], s);
+      sf_pairs += static_cast<double>(g.na) * g.nb * Jf[k];
       ctx->timer.launches += 5;
     }
     sf_add_flux(static_cast<int>(p1 - p0), d_pt_index.p, tqb, d_sf_gcell.p, d_sf_gaxn.p,
                 d_sf_G.p, d_qn.p, d_qw.p, cfg.material.conductivity, d_gq.p, s);
     ++ctx->timer.launches;
-    sf_pairs += static_cast<double>(p1 - p0) * J;
   }
   k3_local(ft, e0, e1, d_elem_off.p, d_gq.p, d_loc.p, s);
   ++ctx->timer.launches;

@@ -161,6 +161,10 @@ class Sim {
   std::vector<SfDev> sf_faces_dev;
   std::vector<int> sf_faces_off;
   bool sf_fine_ok = false;  // fine-rule points gridded per face too
+  bool sf_face_split = false;  // per-face source prefixes (face boxes)
+  std::vector<int> sf_face_e;  // per face: element range [begin, end)
+  std::vector<double> sf_face_box, sf_face_delta;
+  std::vector<SfPrefix> sf_pf_face;
   std::vector<SfGrid> sf_fine;
   std::vector<SfDev> sf_fine_dev;
   std::vector<int> sf_elem_face, sf_erect;  // per face element: face, fine-cell rectangle
