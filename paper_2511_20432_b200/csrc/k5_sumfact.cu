@@ -246,6 +246,19 @@ bool sf_source_eligible(const double* p, double t, double alpha, double cull, co
   return 36.0 * cull * delta * delta <= 1e-24 * spread;
 }
 
+bool sf_source_culled(const double* p, double t, double alpha, double cull, const double lo[3],
+                      const double hi[3]) {
+  const double dt = t - p[5];
+  if (!(dt > 0.0)) return true;
+  const double spread = 4.0 * alpha * dt;
+  double r2 = 0.0;  // squared distance from the source to the box
+  for (int ax = 0; ax < 3; ++ax) {
+    const double d = std::max({lo[ax] - p[ax], p[ax] - hi[ax], 0.0});
+    r2 += d * d;
+  }
+  return r2 * (1.0 - 1e-9) > cull * spread;
+}
+
 double sf_contract(cublasHandle_t h, const SfDev& g, bool grad, const double* d_src6, int J,
                    int Kc, double t, double alpha, double rcp, const SfScratch& w, double* d_G,
                    cudaStream_t s) {

@@ -34,6 +34,12 @@ bool sf_make_grid(const double* pts, long n, double tol, SfGrid& out);
 bool sf_source_eligible(const double* src6, double t, double alpha, double cull,
                         const double lo[3], const double hi[3], double delta);
 
+// Every pair of the source with a point in [lo, hi] is culled by the
+// reference (or the source is causally inactive at t): its terms are exact
+// zeros there, and K1 may skip it.
+bool sf_source_culled(const double* src6, double t, double alpha, double cull,
+                      const double lo[3], const double hi[3]);
+
 struct SfDev {
   int axn, axu, axv, na, nb;
   double xf;

@@ -651,6 +651,17 @@ int Sim::sf_prefix(double t, const double lo[3], const double hi[3], double delt
   return j;
 }
 
+int Sim::sf_suffix_end(double t, const double lo[3], const double hi[3], int begin) {
+  const double alpha = ctx->mat.diffusivity();
+  const double cull = cfg.superpose.cull_exponent;
+  const double* src = reinterpret_cast<const double*>(sources.data());
+  int end = ctx->active_prefix(t);
+  while (end > begin &&
+         sf_source_culled(src + 6 * static_cast<size_t>(end - 1), t, alpha, cull, lo, hi))
+    --end;
+  return end;
+}
+
 SfScratch Sim::sf_scratch(int na, int nb, int J) {
   const int C = (J + sf_kc - 1) / sf_kc;
   const size_t Jpad = static_cast<size_t>(C) * sf_kc;
@@ -748,8 +759,9 @@ void Sim::flux_load_device(double t, double radius, double* d_F, int e0, int e1)
     for (size_t f = 0; f < nfc; ++f) {
       const long a = pos_of(sf_face_e[2 * f]), b = pos_of(sf_face_e[2 * f + 1]);
       K1Flux ff{d_pt_index.p + a, d_qn.p, d_qw.p, cfg.material.conductivity};
+      const int end = sf_suffix_end(t, &sf_face_box[6 * f], &sf_face_box[6 * f + 3], Jf[f]);
       k1_run(ctx, ctx->src6.p, ctx->n_src, d_qx.p, d_pt_index.p + a, b - a, t,
-             cfg.superpose.cull_exponent, K1Mode::flux, d_gq.p + a, nullptr, ff, s, Jf[f]);
+             cfg.superpose.cull_exponent, K1Mode::flux, d_gq.p + a, nullptr, ff, s, Jf[f], end);
     }
   } else {
     k1_run(ctx, ctx->src6.p, ctx->n_src, d_qx.p, d_pt_index.p + p0, p1 - p0, t,
@@ -878,8 +890,10 @@ void Sim::dirichlet_device(double t, double* d_g, int c0, int c1) {
                     ? sf_prefix(t, sf_dir.lo, sf_dir.hi, sf_dir.delta, sf_pf_dir)
                     : 0;
   sf_last_j[1] = J;
+  const int end = J > 0 ? sf_suffix_end(t, sf_dir.lo, sf_dir.hi, J) : -1;
   k1_run(ctx, ctx->src6.p, ctx->n_src, d_grev.p + 3 * static_cast<size_t>(c0), nullptr, c1 - c0,
-         t, cfg.superpose.cull_exponent, K1Mode::dirichlet, d_g, nullptr, {}, ctx->stream, J);
+         t, cfg.superpose.cull_exponent, K1Mode::dirichlet, d_g, nullptr, {}, ctx->stream, J,
+         end);
   if (J > 0) {  // g = -(K1 part) - (GEMM part)
     const SfDev& g = sf_dir_dev;
     sf_flops += sf_contract(cublas, g, false, ctx->src6.p, J, sf_kc, t, ctx->mat.diffusivity(),

@@ -157,6 +157,8 @@ class Sim {
     bool valid = false;  // [0, J) were all causally active at t (reusable at later t)
   };
   int sf_prefix(double t, const double lo[3], const double hi[3], double delta, SfPrefix& c);
+  // end of the K1 source range [begin, end): trailing sources culled on the whole box drop out
+  int sf_suffix_end(double t, const double lo[3], const double hi[3], int begin);
   std::vector<SfGrid> sf_faces;
   std::vector<SfDev> sf_faces_dev;
   std::vector<int> sf_faces_off;
