@@ -270,6 +270,9 @@ int tg_sim_set_sumfact(tg_sim* sim, int on);
  * call (the smallest over the faces), of the last Dirichlet call, GEMM flops
  * issued, point x source pairs evaluated by the GEMMs, sources per GEMM chunk */
 int tg_sim_sumfact_stats(tg_sim* sim, double* out);
+/* out[2]: the K5 source prefixes at time t (host arithmetic only): sources
+ * [0, J) take the GEMMs — flux (the smallest over the faces), Dirichlet */
+int tg_sim_sumfact_prefix(tg_sim* sim, double t, int* out);
 
 #ifdef __cplusplus
 }

@@ -369,6 +369,7 @@ def _bind_sim(L):
     L.tg_sim_flux_profile.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_double, _dp, _dp]
     L.tg_sim_set_sumfact.argtypes = [C.c_void_p, C.c_int]
     L.tg_sim_sumfact_stats.argtypes = [C.c_void_p, _dp]
+    L.tg_sim_sumfact_prefix.argtypes = [C.c_void_p, C.c_double, _ip]
     L._sim_bound = True
 
 
@@ -471,6 +472,12 @@ class Simulation:
         return dict(on=bool(out[0]), faces_gridded=bool(out[1]), greville_gridded=bool(out[2]),
                     last_j_flux=int(out[3]), last_j_dirichlet=int(out[4]), gemm_flops=out[5],
                     pairs_off_k1=out[6], chunk=int(out[7]))
+
+    def sumfact_prefix(self, t: float):
+        """(J_flux, J_dirichlet): sources [0, J) that K5 puts on the GEMMs at t."""
+        out = np.zeros(2, dtype=np.int32)
+        self._check(self._L.tg_sim_sumfact_prefix(self._h, t, out.ctypes.data_as(_ip)))
+        return int(out[0]), int(out[1])
 
     def greville_points(self):
         out = np.zeros((self.info["n_constrained"], 3))

@@ -74,6 +74,7 @@ Sim::Sim(const std::string& path, const SimOptions& opt) {
   if (opt.max_iter > 0) c.stepping.max_iter = opt.max_iter;
   cfg = std::move(c);
   setup_host();
+  sf_setup_host();
   if (!opt.host_only) setup_device(opt.device, opt.preconditioner);
 }
 
@@ -426,13 +427,12 @@ void Sim::setup_device(int device, int preconditioner) {
   TG_CUDA(cudaMemcpyAsync(h_status, d_status.p, sizeof(PcgStatus), cudaMemcpyDeviceToHost, s));
   TG_CUDA(cudaStreamSynchronize(s));
   diag_ok = h_status->status != 2;
-  sf_setup();
+  sf_setup_device();
 }
 
 // K5 setup: are the lateral faces' base quadrature points and the Greville
 // points tensor grids (up to coordinate rounding) with axis-aligned normals?
-void Sim::sf_setup() {
-  cudaStream_t s = ctx->stream;
+void Sim::sf_setup_host() {
   if (const char* e = std::getenv("TG_SF_KC")) sf_kc = std::max(64, std::atoi(e));
   const int tqb = h_qb_off.empty() ? 0 : h_qb_off.back();
   // faces: base points grouped by the normal's axis and sign
@@ -446,7 +446,10 @@ void Sim::sf_setup() {
     ext = std::max(ext, hi - lo);
   }
   const double tol = 1e-12 * ext;
-  std::vector<int> gcell(tqb, -1), gaxn(tqb, 0);
+  auto& gcell = sf_h_gcell;
+  auto& gaxn = sf_h_gaxn;
+  gcell.assign(tqb, -1);
+  gaxn.assign(tqb, 0);
   sf_flux_ok = tqb > 0;
   std::vector<std::vector<int>> groups(6);
   auto normal_key = [&](int q) {  // 2 axis + (sign > 0), or -1 off the axes
@@ -489,7 +492,12 @@ void Sim::sf_setup() {
   // finer grid; a step's fine elements take a rectangle of it
   const int tqf = h_qf_off.empty() ? 0 : h_qf_off.back();
   sf_fine_ok = sf_flux_ok && tqf > 0;
-  std::vector<int> fa(tqf), fb(tqf), ff(tqf);
+  auto& fa = sf_h_fa;
+  auto& fb = sf_h_fb;
+  auto& ff = sf_h_ff;
+  fa.assign(tqf, 0);
+  fb.assign(tqf, 0);
+  ff.assign(tqf, 0);
   if (sf_fine_ok) {
     sf_elem_face.assign(n_fe, -1);
     sf_erect.assign(4 * static_cast<size_t>(n_fe), 0);
@@ -582,6 +590,16 @@ void Sim::sf_setup() {
     sf_faces_off.clear();
   }
   sf_dir_ok = n_con > 0 && sf_make_grid(grev.data(), n_con, tol, sf_dir);
+  sf_g_total = off;
+  const char* e = std::getenv("TG_SUMFACT");
+  set_sumfact(!(e && std::string(e) == "0"));
+}
+
+void Sim::sf_setup_device() {
+  cudaStream_t s = ctx->stream;
+  const int off = sf_g_total;
+  auto& gcell = sf_h_gcell;
+  auto& gaxn = sf_h_gaxn;
   // grid lines on the device: faces then the Greville grid
   std::vector<double> uv;
   std::vector<size_t> at;
@@ -603,9 +621,9 @@ void Sim::sf_setup() {
   for (size_t k = 0; k < sf_fine.size(); ++k)
     sf_fine_dev.push_back(dev(sf_fine[k], at[sf_faces.size() + k]));
   if (sf_fine_ok) {
-    upload(d_sf_fa, fa, s);
-    upload(d_sf_fb, fb, s);
-    upload(d_sf_ff, ff, s);
+    upload(d_sf_fa, sf_h_fa, s);
+    upload(d_sf_fb, sf_h_fb, s);
+    upload(d_sf_ff, sf_h_ff, s);
     d_sf_rect.ensure(5 * sf_fine.size());
     TG_CUDA(cudaMallocHost(&h_sf_rect, sizeof(int) * 5 * sf_fine.size()));
   }
@@ -625,17 +643,37 @@ void Sim::sf_setup() {
   }
   if (!cublas && cublasCreate(&cublas) != CUBLAS_STATUS_SUCCESS)
     throw cuda_error("cublas: create failed");
-  const char* e = std::getenv("TG_SUMFACT");
-  sf_on = !(e && std::string(e) == "0");
-  set_sumfact(sf_on);
   TG_CUDA(cudaStreamSynchronize(s));
+  for (auto* v : {&sf_h_gcell, &sf_h_gaxn, &sf_h_fa, &sf_h_fb, &sf_h_ff}) std::vector<int>().swap(*v);
+}
+
+void Sim::sf_prefixes(double t, int* out) {
+  if (!sf_on) {
+    out[0] = out[1] = 0;
+    return;
+  }
+  out[0] = 0;
+  if (sf_flux_ok) {
+    SfPrefix c;
+    out[0] = sf_prefix(t, sf_lo, sf_hi, sf_delta, c);
+    if (sf_face_split) {
+      out[0] = 1 << 30;
+      for (size_t f = 0; f < sf_faces.size(); ++f) {
+        c = SfPrefix{};
+        out[0] = std::min(out[0], sf_prefix(t, &sf_face_box[6 * f], &sf_face_box[6 * f + 3],
+                                            sf_face_delta[f], c));
+      }
+    }
+  }
+  SfPrefix c;
+  out[1] = sf_dir_ok ? sf_prefix(t, sf_dir.lo, sf_dir.hi, sf_dir.delta, c) : 0;
 }
 
 // longest prefix [0, J) of the sources that sf_source_eligible admits for the
 // box at t; a prefix of sources all active at an earlier t stays eligible
 // (their spreads only grow), so the scan resumes there
 int Sim::sf_prefix(double t, const double lo[3], const double hi[3], double delta, SfPrefix& c) {
-  const double alpha = ctx->mat.diffusivity();
+  const double alpha = cfg.material.diffusivity();  // = ctx->mat's
   const double cull = cfg.superpose.cull_exponent;
   const double* src = reinterpret_cast<const double*>(sources.data());
   // (the GEMM builders' 2D grids address up to ~1e6 sources; later ones stay on K1)

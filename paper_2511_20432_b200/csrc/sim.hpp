@@ -73,6 +73,8 @@ class Sim {
   // grids (TG_SUMFACT=0 or set_sumfact(false) turns it off). Only the
   // full-range flux / Dirichlet calls use it (the sharded range calls are K1).
   void set_sumfact(bool on) { sf_on = on && (sf_flux_ok || sf_dir_ok); }
+  // the GEMM source prefixes at t (flux: smallest over the faces; Dirichlet), host only
+  void sf_prefixes(double t, int* out);
   bool sf_on = false, sf_flux_ok = false, sf_dir_ok = false;
   double sf_flops = 0.0;   // GEMM flops issued (2 na nb Jpad per set)
   double sf_pairs = 0.0;   // point x source pairs taken off K1
@@ -150,7 +152,10 @@ class Sim {
  private:
   void setup_host();
   void setup_device(int device, int preconditioner);
-  void sf_setup();
+  void sf_setup_host();    // grids, face boxes (host only)
+  void sf_setup_device();  // uploads
+  std::vector<int> sf_h_gcell, sf_h_gaxn, sf_h_fa, sf_h_fb, sf_h_ff;  // until uploaded
+  int sf_g_total = 0;
   struct SfPrefix {
     int J = 0;
     double t = 0.0;

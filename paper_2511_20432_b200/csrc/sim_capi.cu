@@ -130,7 +130,7 @@ int tg_sim_info(tg_sim* s, long* out) {
 }
 
 int tg_sim_set_sumfact(tg_sim* s, int on) {
-  return sim_guard(s, [&](Sim& m) { m.set_sumfact(on != 0); });
+  return sim_guard(s, [&](Sim& m) { m.set_sumfact(on != 0); }, false);
 }
 
 int tg_sim_sumfact_stats(tg_sim* s, double* out) {
@@ -139,7 +139,11 @@ int tg_sim_sumfact_stats(tg_sim* s, double* out) {
                         static_cast<double>(m.sf_last_j[0]), static_cast<double>(m.sf_last_j[1]),
                         m.sf_flops, m.sf_pairs, static_cast<double>(m.sf_kc)};
     std::memcpy(out, v, sizeof(v));
-  });
+  }, false);
+}
+
+int tg_sim_sumfact_prefix(tg_sim* s, double t, int* out) {
+  return sim_guard(s, [&](Sim& m) { m.sf_prefixes(t, out); }, false);
 }
 
 int tg_sim_params(tg_sim* s, double* out) {
