@@ -350,6 +350,7 @@ def theta_section(steps, warmup, with_cpu):
     sf = sim.sumfact_stats()
     # the same steps with every superposition pair on K1 (K5 off), for the split
     sim.set_sumfact(False)
+    sim.advance(1)  # untimed: K1-only buffer sizes
     t1 = time.perf_counter()
     sim.advance(steps)
     wall_k1 = time.perf_counter() - t1

@@ -434,6 +434,7 @@ void Sim::setup_device(int device, int preconditioner) {
 // points tensor grids (up to coordinate rounding) with axis-aligned normals?
 void Sim::sf_setup_host() {
   if (const char* e = std::getenv("TG_SF_KC")) sf_kc = std::max(64, std::atoi(e));
+  if (const char* e = std::getenv("TG_SF_MIN_PAIRS")) sf_min_pairs = std::atof(e);
   const int tqb = h_qb_off.empty() ? 0 : h_qb_off.back();
   // faces: base points grouped by the normal's axis and sign
   double ext = 0.0;
@@ -791,6 +792,25 @@ void Sim::flux_load_device(double t, double radius, double* d_F, int e0, int e1)
       std::fill(Jf.begin(), Jf.end(), J);
     }
   }
+  // profitability: a face's GEMM (a few launches, ~25 us) must save more K1
+  // pair work than it costs (TG_SF_MIN_PAIRS moved pairs, default 3e7 ~ 30 us)
+  if (Jmax > 0 && sf_face_split) {
+    J = 1 << 30;
+    Jmax = 0;
+    for (size_t f = 0; f < nfc; ++f) {
+      const double pts = static_cast<double>(sf_faces[f].U.size()) * sf_faces[f].V.size();
+      if (static_cast<double>(Jf[f]) * pts < sf_min_pairs) Jf[f] = 0;
+      J = std::min(J, Jf[f]);
+      Jmax = std::max(Jmax, Jf[f]);
+    }
+  } else if (Jmax > 0) {  // one prefix for all faces: all kept or all dropped
+    double pts = 0.0;
+    for (const SfGrid& g : sf_faces) pts += static_cast<double>(g.U.size()) * g.V.size();
+    if (static_cast<double>(J) * pts < sf_min_pairs) {
+      J = Jmax = 0;
+      std::fill(Jf.begin(), Jf.end(), 0);
+    }
+  }
   sf_last_j[0] = J;
   if (Jmax > 0 && sf_face_split) {
     auto pos_of = [&](int e) { return e == n_fe ? p1 : offset_of(e); };
@@ -924,9 +944,10 @@ void Sim::dirichlet_device(double t, double* d_g, int c0, int c1) {
   if (c1 < 0) c1 = n_con;
   c0 = std::max(0, std::min(c0, n_con));
   c1 = std::max(c0, std::min(c1, n_con));
-  const int J = (sf_on && sf_dir_ok && c0 == 0 && c1 == n_con)
-                    ? sf_prefix(t, sf_dir.lo, sf_dir.hi, sf_dir.delta, sf_pf_dir)
-                    : 0;
+  int J = (sf_on && sf_dir_ok && c0 == 0 && c1 == n_con)
+              ? sf_prefix(t, sf_dir.lo, sf_dir.hi, sf_dir.delta, sf_pf_dir)
+              : 0;
+  if (static_cast<double>(J) * n_con < sf_min_pairs) J = 0;  // not worth the launches
   sf_last_j[1] = J;
   const int end = J > 0 ? sf_suffix_end(t, sf_dir.lo, sf_dir.hi, J) : -1;
   k1_run(ctx, ctx->src6.p, ctx->n_src, d_grev.p + 3 * static_cast<size_t>(c0), nullptr, c1 - c0,

@@ -80,6 +80,7 @@ class Sim {
   double sf_pairs = 0.0;   // point x source pairs taken off K1
   int sf_last_j[2] = {0, 0};  // source prefix of the last flux / Dirichlet call
   int sf_kc = 2048;           // sources per GEMM chunk (one batch entry; TG_SF_KC)
+  double sf_min_pairs = 3e7;  // smallest J x points worth a GEMM (TG_SF_MIN_PAIRS)
 
   bool focus_at(double t, Vec3& focus) const;
   int fine_elements(double t, double radius);  // fills h_fine, returns the count

@@ -20,6 +20,13 @@ from conftest import ROOT
 pytestmark = pytest.mark.gpu
 
 
+@pytest.fixture(autouse=True)
+def _gemm_even_when_small(monkeypatch):
+    # the small parity configs move fewer pairs than K5's profitability
+    # threshold (3e7 per face); force the GEMM path so it is what gets checked
+    monkeypatch.setenv("TG_SF_MIN_PAIRS", "0")
+
+
 def normwise(a, b):
     m = np.abs(b).max()
     return 0.0 if m == 0 else np.abs(a - b).max() / m
