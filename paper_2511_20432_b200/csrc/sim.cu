@@ -435,6 +435,7 @@ void Sim::setup_device(int device, int preconditioner) {
 void Sim::sf_setup_host() {
   if (const char* e = std::getenv("TG_SF_KC")) sf_kc = std::max(64, std::atoi(e));
   if (const char* e = std::getenv("TG_SF_MIN_PAIRS")) sf_min_pairs = std::atof(e);
+  if (const char* e = std::getenv("TG_SF_BANDS")) sf_bands = std::max(1, std::atoi(e));
   const int tqb = h_qb_off.empty() ? 0 : h_qb_off.back();
   // faces: base points grouped by the normal's axis and sign
   double ext = 0.0;
@@ -452,7 +453,6 @@ void Sim::sf_setup_host() {
   gcell.assign(tqb, -1);
   gaxn.assign(tqb, 0);
   sf_flux_ok = tqb > 0;
-  std::vector<std::vector<int>> groups(6);
   auto normal_key = [&](int q) {  // 2 axis + (sign > 0), or -1 off the axes
     const double* n = &h_qn[3 * static_cast<size_t>(q)];
     int ax = 0;
@@ -466,28 +466,76 @@ void Sim::sf_setup_host() {
   for (int q = 0; q < tqb && sf_flux_ok; ++q) {
     qkey[q] = normal_key(q);
     if (qkey[q] < 0) sf_flux_ok = false;
-    else groups[qkey[q]].push_back(q);
   }
-  int face_of_key[6] = {-1, -1, -1, -1, -1, -1};
+  // elements by face (normal key), each face cut into up to sf_bands bands of
+  // whole element rows (a band's box is smaller than the face's, so more of the
+  // history is cull-free there and takes the GEMM); every band is a grid
+  std::vector<int> ekey(n_fe, -1), eband(n_fe, -1);
+  std::vector<std::vector<int>> kelems(6);
+  for (int e = 0; e < n_fe && sf_flux_ok; ++e) {
+    ekey[e] = qkey[h_qb_off[e]];
+    for (int q = h_qb_off[e]; q < h_qb_off[e + 1]; ++q)
+      if (qkey[q] != ekey[e]) sf_flux_ok = false;
+    if (sf_flux_ok) kelems[ekey[e]].push_back(e);
+  }
   int off = 0;
+  auto grid_of = [&](const std::vector<int>& els, SfGrid& g) {
+    std::vector<double> pts;
+    for (int e : els)
+      for (int q = h_qb_off[e]; q < h_qb_off[e + 1]; ++q)
+        for (int d = 0; d < 3; ++d) pts.push_back(h_qx[3 * static_cast<size_t>(q) + d]);
+    return sf_make_grid(pts.data(), static_cast<long>(pts.size() / 3), tol, g);
+  };
   for (int k = 0; k < 6 && sf_flux_ok; ++k) {
-    if (groups[k].empty()) continue;
-    face_of_key[k] = static_cast<int>(sf_faces.size());
-    std::vector<double> pts(3 * groups[k].size());
-    for (size_t i = 0; i < groups[k].size(); ++i)
-      for (int d = 0; d < 3; ++d) pts[3 * i + d] = h_qx[3 * groups[k][i] + d];
-    SfGrid g;
-    if (!sf_make_grid(pts.data(), static_cast<long>(groups[k].size()), tol, g) || g.axn != k / 2) {
-      sf_flux_ok = false;
+    const std::vector<int>& E = kelems[k];
+    if (E.empty()) continue;
+    // row starts: where the slower-varying in-face centre coordinate changes
+    const int ax = k / 2, u = ax == 0 ? 1 : 0, v = ax == 2 ? 1 : 2;
+    auto changes = [&](int d) {
+      int c = 0;
+      for (size_t i = 1; i < E.size(); ++i)
+        c += std::fabs(centers[3 * E[i] + d] - centers[3 * E[i - 1] + d]) > tol;
+      return c;
+    };
+    const int slow = changes(u) <= changes(v) ? u : v;
+    std::vector<size_t> rows{0};
+    for (size_t i = 1; i < E.size(); ++i)
+      if (std::fabs(centers[3 * E[i] + slow] - centers[3 * E[i - 1] + slow]) > tol)
+        rows.push_back(i);
+    std::vector<std::vector<int>> bands;
+    for (int nb = std::max(1, std::min<int>(sf_bands, static_cast<int>(rows.size()))); nb >= 1;
+         nb = nb > 1 ? 1 : 0) {
+      bands.clear();
+      size_t prev = 0;
+      for (int b = 1; b <= nb; ++b) {
+        const size_t end = b == nb ? E.size() : rows[rows.size() * b / nb];
+        if (end > prev) bands.emplace_back(E.begin() + prev, E.begin() + end);
+        prev = end;
+      }
+      std::vector<SfGrid> gs(bands.size());
+      bool ok = true;
+      for (size_t i = 0; i < bands.size() && ok; ++i)
+        ok = grid_of(bands[i], gs[i]) && gs[i].axn == ax;
+      if (!ok) {
+        if (nb == 1) sf_flux_ok = false;
+        continue;
+      }
+      for (size_t i = 0; i < bands.size(); ++i) {
+        const int f = static_cast<int>(sf_faces.size());
+        size_t c = 0;
+        for (int e : bands[i]) {
+          eband[e] = f;
+          for (int q = h_qb_off[e]; q < h_qb_off[e + 1]; ++q, ++c) {
+            gcell[q] = off + gs[i].cell[c];
+            gaxn[q] = gs[i].axn;
+          }
+        }
+        sf_faces_off.push_back(off);
+        off += static_cast<int>(gs[i].U.size() * gs[i].V.size());
+        sf_faces.push_back(std::move(gs[i]));
+      }
       break;
     }
-    for (size_t i = 0; i < groups[k].size(); ++i) {
-      gcell[groups[k][i]] = off + g.cell[i];
-      gaxn[groups[k][i]] = g.axn;
-    }
-    sf_faces_off.push_back(off);
-    off += static_cast<int>(g.U.size() * g.V.size());
-    sf_faces.push_back(std::move(g));
   }
   // fine-rule points: per face, the fine points of all its elements form a
   // finer grid; a step's fine elements take a rectangle of it
@@ -504,12 +552,9 @@ void Sim::sf_setup_host() {
     sf_erect.assign(4 * static_cast<size_t>(n_fe), 0);
     std::vector<std::vector<int>> felems(sf_faces.size());
     for (int e = 0; e < n_fe && sf_fine_ok; ++e) {
-      const int f = face_of_key[qkey[h_qb_off[e]]];
-      for (int q = h_qb_off[e]; q < h_qb_off[e + 1]; ++q)
-        if (face_of_key[qkey[q]] != f) sf_fine_ok = false;
+      const int f = eband[e];
       for (int l = h_qf_off[e]; l < h_qf_off[e + 1]; ++l)
-        if (face_of_key[std::max(0, normal_key(tqb + l))] != f || normal_key(tqb + l) < 0)
-          sf_fine_ok = false;
+        if (normal_key(tqb + l) != ekey[e]) sf_fine_ok = false;
       sf_elem_face[e] = f;
       felems[f].push_back(e);
     }
@@ -592,6 +637,9 @@ void Sim::sf_setup_host() {
   }
   sf_dir_ok = n_con > 0 && sf_make_grid(grev.data(), n_con, tol, sf_dir);
   sf_g_total = off;
+  if (std::getenv("TG_SF_DEBUG"))
+    std::fprintf(stderr, "[k5] flux %d fine %d split %d groups %zu dir %d\n", sf_flux_ok,
+                 sf_fine_ok, sf_face_split, sf_faces.size(), sf_dir_ok);
   const char* e = std::getenv("TG_SUMFACT");
   set_sumfact(!(e && std::string(e) == "0"));
 }

@@ -81,6 +81,7 @@ class Sim {
   int sf_last_j[2] = {0, 0};  // source prefix of the last flux / Dirichlet call
   int sf_kc = 2048;           // sources per GEMM chunk (one batch entry; TG_SF_KC)
   double sf_min_pairs = 3e7;  // smallest J x points worth a GEMM (TG_SF_MIN_PAIRS)
+  int sf_bands = 1;           // bands of element rows per face (TG_SF_BANDS; see DESIGN K5)
 
   bool focus_at(double t, Vec3& focus) const;
   int fine_elements(double t, double radius);  // fills h_fine, returns the count

@@ -66,8 +66,11 @@ def _face_boxes(s):
 
 
 @pytest.mark.parametrize("t", [-1.0, 0.0, 1e-4, 3e-3])
-def test_prefix_matches_restatement(tmp_path, t):
-    s = host_sim(long_history_cfg(tmp_path))
+def test_prefix_matches_restatement(tmp_path, monkeypatch, t):
+    path = long_history_cfg(tmp_path)
+    banded = host_sim(path)  # default: faces cut into bands of element rows
+    monkeypatch.setenv("TG_SF_BANDS", "1")  # whole faces: the restatement's boxes
+    s = host_sim(path)
     src = s.sources()
     k, rho, c = (s.params[n] for n in ("conductivity", "density", "heat_capacity"))
     alpha, cull = k / (rho * c), s.params["cull"]
@@ -76,6 +79,9 @@ def test_prefix_matches_restatement(tmp_path, t):
     jd = _prefix(src, t, alpha, cull, g.min(axis=0), g.max(axis=0))
     got = s.sumfact_prefix(t)
     assert got == (jf, jd)
+    jb = banded.sumfact_prefix(t)  # smaller boxes: never a shorter prefix
+    assert jb[0] >= jf and jb[1] == jd
+    banded.close()
     if t == -1.0:  # every source still inactive: all eligible (exact zero columns)
         assert got == (len(src), len(src))
     if t == 0.0:  # the long history: both paths carry sources
