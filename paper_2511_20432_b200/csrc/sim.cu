@@ -85,6 +85,9 @@ Sim::~Sim() {
   if (h_fine) cudaFreeHost(h_fine);
   if (h_sf_fine) cudaFreeHost(h_sf_fine);
   if (h_sf_rect) cudaFreeHost(h_sf_rect);
+  for (auto& ev : sf_ev)
+    if (ev) cudaEventDestroy(ev);
+  if (sf_stream) cudaStreamDestroy(sf_stream);
   if (ctx) tg_ctx_destroy(ctx);
 }
 
@@ -692,6 +695,11 @@ void Sim::sf_setup_device() {
   }
   if (!cublas && cublasCreate(&cublas) != CUBLAS_STATUS_SUCCESS)
     throw cuda_error("cublas: create failed");
+  const char* ser = std::getenv("TG_SF_SERIAL");
+  if (sf_face_split && !(ser && std::string(ser) == "1")) {
+    TG_CUDA(cudaStreamCreateWithFlags(&sf_stream, cudaStreamNonBlocking));
+    for (auto& ev : sf_ev) TG_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  }
   TG_CUDA(cudaStreamSynchronize(s));
   for (auto* v : {&sf_h_gcell, &sf_h_gaxn, &sf_h_fa, &sf_h_fb, &sf_h_ff}) std::vector<int>().swap(*v);
 }
@@ -860,6 +868,13 @@ void Sim::flux_load_device(double t, double radius, double* d_F, int e0, int e1)
     }
   }
   sf_last_j[0] = J;
+  // the K1 remainder (FP64 pipe) runs on a side stream beside the GEMMs (DMMA)
+  const bool conc = Jmax > 0 && sf_face_split && sf_stream != nullptr;
+  cudaStream_t ks = conc ? sf_stream : s;
+  if (conc) {
+    TG_CUDA(cudaEventRecord(sf_ev[0], s));
+    TG_CUDA(cudaStreamWaitEvent(sf_stream, sf_ev[0], 0));
+  }
   if (Jmax > 0 && sf_face_split) {
     auto pos_of = [&](int e) { return e == n_fe ? p1 : offset_of(e); };
     for (size_t f = 0; f < nfc; ++f) {
@@ -867,12 +882,15 @@ void Sim::flux_load_device(double t, double radius, double* d_F, int e0, int e1)
       K1Flux ff{d_pt_index.p + a, d_qn.p, d_qw.p, cfg.material.conductivity};
       const int end = sf_suffix_end(t, &sf_face_box[6 * f], &sf_face_box[6 * f + 3], Jf[f]);
       k1_run(ctx, ctx->src6.p, ctx->n_src, d_qx.p, d_pt_index.p + a, b - a, t,
-             cfg.superpose.cull_exponent, K1Mode::flux, d_gq.p + a, nullptr, ff, s, Jf[f], end);
+             cfg.superpose.cull_exponent, K1Mode::flux, d_gq.p + a, nullptr, ff, ks, Jf[f], end);
     }
+    if (conc) TG_CUDA(cudaEventRecord(sf_ev[1], sf_stream));
   } else {
     k1_run(ctx, ctx->src6.p, ctx->n_src, d_qx.p, d_pt_index.p + p0, p1 - p0, t,
            cfg.superpose.cull_exponent, K1Mode::flux, d_gq.p + p0, nullptr, fl, s, J);
   }
+  int fine_n = 0;
+  double* fine_G = nullptr;
   if (Jmax > 0) {
     const double alpha = ctx->mat.diffusivity(), rcp = ctx->mat.volumetric_capacity();
     const int tqb = h_qb_off.back();
@@ -935,9 +953,8 @@ void Sim::flux_load_device(double t, double radius, double* d_F, int e0, int e1)
                               cudaMemcpyHostToDevice, s));
       TG_CUDA(cudaMemcpyAsync(d_sf_rect.p, h_sf_rect, sizeof(int) * 5 * nF,
                               cudaMemcpyHostToDevice, s));
-      sf_add_fine(nfp, d_sf_fine.p, d_sf_fine.p + nfp, tqb, d_sf_fa.p, d_sf_fb.p, d_sf_ff.p,
-                  d_sf_rect.p, Gf, d_qn.p, d_qw.p, cfg.material.conductivity, d_gq.p, s);
-      ++ctx->timer.launches;
+      fine_n = nfp;  // added after the join with the K1 stream
+      fine_G = Gf;
     } else if (nf > 0) {
       int nfp = 0;
       for (int r = 0; r < nf; ++r) nfp += h_qf_off[h_fine[r] + 1] - h_qf_off[h_fine[r]];
@@ -966,6 +983,13 @@ void Sim::flux_load_device(double t, double radius, double* d_F, int e0, int e1)
                               sf_scratch(g.na, g.nb, Jf[k]), d_sf_G.p + sf_faces_off[k], s);
       sf_pairs += static_cast<double>(g.na) * g.nb * Jf[k];
       ctx->timer.launches += 5;
+    }
+    if (conc) TG_CUDA(cudaStreamWaitEvent(s, sf_ev[1], 0));  // K1 wrote gq
+    if (fine_n > 0) {
+      sf_add_fine(fine_n, d_sf_fine.p, d_sf_fine.p + fine_n, tqb, d_sf_fa.p, d_sf_fb.p,
+                  d_sf_ff.p, d_sf_rect.p, fine_G, d_qn.p, d_qw.p, cfg.material.conductivity,
+                  d_gq.p, s);
+      ++ctx->timer.launches;
     }
     sf_add_flux(static_cast<int>(p1 - p0), d_pt_index.p, tqb, d_sf_gcell.p, d_sf_gaxn.p,
                 d_sf_G.p, d_qn.p, d_qw.p, cfg.material.conductivity, d_gq.p, s);

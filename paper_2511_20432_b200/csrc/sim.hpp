@@ -180,6 +180,8 @@ class Sim {
   DevBuf<int> d_sf_fa, d_sf_fb, d_sf_ff, d_sf_rect;
   DevBuf<double> d_sf_Gf;
   int* h_sf_rect = nullptr;
+  cudaStream_t sf_stream = nullptr;  // K1 remainder beside the GEMMs (TG_SF_SERIAL=1: one stream)
+  cudaEvent_t sf_ev[2] = {nullptr, nullptr};
   SfGrid sf_dir;
   SfDev sf_dir_dev{};
   double sf_lo[3] = {0, 0, 0}, sf_hi[3] = {0, 0, 0}, sf_delta = 0.0;
