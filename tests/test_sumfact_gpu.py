@@ -132,6 +132,8 @@ def test_sumfact_config4_full_size():
         F1, d1 = s.flux_load(t), s.dirichlet_values(t)
         st = s.sumfact_stats()
         assert st["last_j_flux"] > 80000 and st["last_j_dirichlet"] > 80000, st
+        # deterministic: fixed chunking and chunk-reduction order, K1 on its own stream
+        assert np.array_equal(s.flux_load(t), F1) and np.array_equal(s.dirichlet_values(t), d1)
         s.set_sumfact(False)
         F0, d0 = s.flux_load(t), s.dirichlet_values(t)
         s.set_sumfact(True)
