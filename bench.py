@@ -43,7 +43,19 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-from paper_2511_20432_b200 import workloads as W  # noqa: E402
+
+def _load_workloads():
+    """workloads.py by file path: the seeded inputs without importing the
+    product package (the reference arm must not load any of it)."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location(
+        "tg_workloads", os.path.join(ROOT, "paper_2511_20432_b200", "workloads.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    return mod
+
+
+W = _load_workloads()
 
 FLOPS_PER_PAIR = 49.0  # SURVEY.md §8d: value + gradient, exp counted at libdevice cost
 # FP64-pipe instructions per pair actually issued by k1_partial's fast path
@@ -86,6 +98,14 @@ def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return rank, world, local
+
+
+def config1_dict(n_points, n_src, world):
+    """The `config` object of both arms (identical by construction)."""
+    return {"workload": "config1: 2^20 points x 2^16 raster sources, superpose at t_end",
+            "points_per_gpu": n_points, "sources": n_src, "cull_exponent": 60.0,
+            "parallelism": f"point slabs x{world}, sources replicated",
+            "l2": "flushed between steps (256 MiB write outside the step events)"}
 
 
 def workload(n_src):
@@ -192,28 +212,6 @@ def hbm_peak():
         return HBM_PEAK_FALLBACK, "fallback 6555.2 GB/s (BASELINE.md copy measurement)"
 
 
-def theta_cpu_baseline():
-    """One reference theta_step on config 2 (78,408 DOF; serial PCG as shipped)."""
-    from oracle import pyoracle
-    if not pyoracle.ref_available():
-        return None
-    R = pyoracle.RefLib()
-    sim = R.sim(THETA_CPU_CFG)
-    n_free, n_con, n_full = (sim.info[k] for k in ("n_free", "n_constrained", "n_full"))
-    t = 0.02
-    F0, F1 = sim.flux_load(t - sim.params["dt"], threads=os.cpu_count()), sim.flux_load(t)
-    g0, g1 = sim.dirichlet(t - sim.params["dt"]), sim.dirichlet(t)
-    x0 = np.zeros(n_free)
-    t0 = time.perf_counter()
-    _, iters, _ = sim.theta_step(x0, g0, F0, F1, g1, sim.params["solver_tol"])
-    secs = time.perf_counter() - t0
-    sim.close()
-    dofs = n_free + n_con
-    return {"ms_per_step_per_mdof": secs * 1e3 / (dofs / 1e6), "cg_iterations": iters,
-            "cores": 1, "kind": "reference",
-            "sample": f"one theta_step of config 2 ({dofs} DOF) at t = 0.02 s, cold start"}
-
-
 def config3_steps(with_cpu, steps=10):
     """Config 3 (degree-3 rational plate-with-hole part, 128x64x32 elements,
     302,974 free DOF; SURVEY.md Appendix C option A): the assembled-operator
@@ -285,48 +283,64 @@ def config3_steps(with_cpu, steps=10):
 
 def config2_run(with_cpu):
     """End to end: config 2's whole run_time_loop (2000 θ-steps, 64x64x16
-    degree-2 cuboid, one raster layer) on the device, against one reference
-    step at mid-run (flux load on all host cores + Dirichlet values + θ-step)."""
+    degree-2 cuboid, one raster layer) on the device, against the reference's
+    own step at mid-run, warm-started from the same state (flux load on all
+    host cores + Dirichlet values + θ-step with its serial PCG)."""
     import paper_2511_20432_b200 as tg
     sim = tg.Simulation(THETA_CPU_CFG)
     n = sim.info["n_steps"]
     sim.reset()
     sim.advance(5)  # warm-up (module load, first launches)
     sim.reset()
+    ctx = sim.context()
+    ctx.set_profiling(True)
+    ctx.profile(reset=True)
     t0 = time.perf_counter()
     iters, rel = sim.advance(n)
     wall = time.perf_counter() - t0
+    prof = ctx.profile()
+    ctx.set_profiling(False)
+    dofs = sim.info["n_full"]
     out = {"workload": "config2: 64x64x16 degree-2 cuboid (78,408 DOF), one-layer raster "
                        f"({sim.info['n_sources']} sources), {n} theta steps, solver_tol "
                        f"{sim.params['solver_tol']:g}",
            "steps": n, "run_s": wall, "ms_per_step": wall * 1e3 / n,
+           "theta_step_total_ms_per_step": prof["theta_step_ms"] / n,
+           "theta_step_total_ms_per_mdof": prof["theta_step_ms"] / n / (dofs / 1e6),
            "cg_iterations_per_step": iters / n, "timing": "wall clock around the "
            "synchronous tg_sim_advance(n) call (device-resident state)"}
-    sim.close()
+    k = n // 2
     if with_cpu:
         from oracle import pyoracle
         if pyoracle.ref_available():
+            sim.reset()
+            sim.advance(k - 1)
+            st = sim.state()  # the step k-1 state both sides continue from
             R = pyoracle.RefLib()
             rs = R.sim(THETA_CPU_CFG)
             dt = rs.params["dt"]
-            k = n // 2
-            t1 = k * dt
-            x0 = np.zeros(rs.info["n_free"])
-            F0 = rs.flux_load(t1 - dt, threads=os.cpu_count())
-            g0 = rs.dirichlet(t1 - dt)
+            t0_, t1 = (k - 1) * dt, k * dt
+            F0 = rs.flux_load(t0_, threads=os.cpu_count())
+            g0 = rs.dirichlet(t0_)
             c0 = time.perf_counter()
             F1 = rs.flux_load(t1, threads=os.cpu_count())
+            c1 = time.perf_counter()
             g1 = rs.dirichlet(t1)
-            rs.theta_step(x0, g0, F0, F1, g1, rs.params["solver_tol"])
-            secs = time.perf_counter() - c0
+            c2 = time.perf_counter()
+            _, its, _ = rs.theta_step(st["free"], g0, F0, F1, g1, rs.params["solver_tol"])
+            c3 = time.perf_counter()
             rs.close()
-            out["cpu_baseline"] = {"ms_per_step": secs * 1e3, "kind": "reference",
-                                   "cores": os.cpu_count(),
-                                   "sample": f"one step at step {k} (t = {t1:g} s): "
-                                             "assemble_flux_load (threaded), "
-                                             "dirichlet_values, theta_step (serial PCG, "
-                                             "cold start)",
-                                   "run_s_estimate": secs * n}
+            out["cpu_baseline"] = {
+                "ms_per_step": (c3 - c0) * 1e3, "kind": "reference", "cores": os.cpu_count(),
+                "flux_load_ms": (c1 - c0) * 1e3, "dirichlet_ms": (c2 - c1) * 1e3,
+                "theta_step_ms": (c3 - c2) * 1e3,
+                "theta_step_ms_per_mdof": (c3 - c2) * 1e3 / (dofs / 1e6),
+                "cg_iterations": its,
+                "sample": f"the reference's step {k} (t = {t1:g} s), warm-started from the "
+                          "device run's step-(k-1) state: assemble_flux_load (threaded over "
+                          "all cores), dirichlet_values and theta_step (serial, as shipped)",
+                "run_s_estimate": (c3 - c0) * n}
+    sim.close()
     return out
 
 
@@ -348,9 +362,12 @@ def theta_section(steps, warmup, with_cpu):
     prof = ctx.profile()
     ctx.set_profiling(False)
     sf = sim.sumfact_stats()
-    # the same steps with every superposition pair on K1 (K5 off), for the split
+    # the same steps (same step indices, from a reset) with every
+    # superposition pair on K1 (K5 off), for the split
     sim.set_sumfact(False)
-    sim.advance(1)  # untimed: K1-only buffer sizes
+    sim.reset()
+    if warmup:
+        sim.advance(warmup)
     t1 = time.perf_counter()
     sim.advance(steps)
     wall_k1 = time.perf_counter() - t1
@@ -397,11 +414,10 @@ def theta_section(steps, warmup, with_cpu):
                      "peak_source": src,
                      "bytes_per_dof_per_iteration": 104},
     }
-    if with_cpu:
-        try:
-            out["cpu_baseline"] = theta_cpu_baseline()
-        except Exception as e:
-            out["cpu_baseline"] = {"error": str(e)}
+    out["cpu_baseline"] = {
+        "note": "the reference cannot be timed per step on config 4 inside this bench (its "
+                "setup assembles ~57 GB of CSR / element matrices in minutes); the "
+                "reference's warm-started step on config 2 is config2_run.cpu_baseline"}
     sim.close()
     try:
         out["fdm_option"] = theta_fdm(steps, warmup)
@@ -485,27 +501,63 @@ def theta_fdm(steps, warmup):
 
 
 def run_reference(args):
+    """The reference's own CPU implementation of the path: the unmodified
+    reference library's superpose (oracle/_ref, its parallel_for over every
+    host core), on the same workload. Nothing of the product package is
+    imported or loaded here. Each step evaluates a fixed strided sample of
+    the 2^20 points against all 2^16 sources (the full set would take ~80 s
+    per step on 16 cores); value and ms_per_step are the sample's measured
+    rate and time."""
     rank, world, _ = dist_env()
     if rank != 0:
         return 0
-    import paper_2511_20432_b200 as tg  # host-only use: discretize_scan for the inputs
-    src, t = make_sources(tg, args.sources)
-    per_step = max(1.0, min(30.0, 120.0 / max(1, args.steps + args.warmup)))
+    from oracle import pyoracle
+    threads = os.cpu_count() or 1
+    kw = dict(**W.MATERIAL, **W.LASER)
+    if pyoracle.ref_available():
+        impl, kind, cores = pyoracle.RefLib(), "reference", threads
+        call = lambda pts: impl.superpose(src, pts, t, threads=threads, **kw)  # noqa: E731
+    else:  # the pinned C port (oracle/oracle.c), one thread
+        impl, kind, cores = pyoracle.COracle(), "port", 1
+        call = lambda pts: impl.superpose(src, pts, t, **kw)  # noqa: E731
+    src = impl.discretize_scan(W.config1_waypoints(), start_time=0.0, plane_z=1e-3,
+                               **W.LASER, **W.MATERIAL)[:args.sources]
+    t = float(src[-1, 4])
+    all_pts = W.config1_points(args.points)
+    # one step ~ per_step seconds so that the whole --steps/--warmup run ends
+    # within a few minutes
+    per_step = max(0.5, min(10.0, 100.0 / max(1, args.steps + args.warmup)))
+    n0 = max(64, 8 * cores)
+    call(all_pts[:n0])  # thread / page warm-up, then calibrate
+    c0 = time.perf_counter()
+    call(all_pts[:n0])
+    dt0 = time.perf_counter() - c0
+    n = int(min(len(all_pts), max(n0, n0 * per_step / max(dt0, 1e-6))))
+    stride = max(1, len(all_pts) // n)
+    sample = np.ascontiguousarray(all_pts[::stride][:n])
     for _ in range(args.warmup):
-        cpu_baseline(src, t, per_step / 4)
-    vals = [cpu_baseline(src, t, per_step) for _ in range(args.steps)]
-    v = float(np.mean([x["value"] for x in vals]))
-    cb = dict(vals[-1])
-    cb["value"] = v
+        call(sample)
+    secs = []
+    for _ in range(args.steps):
+        c0 = time.perf_counter()
+        call(sample)
+        secs.append(time.perf_counter() - c0)
+    pairs = float(len(sample)) * len(src)
+    v = pairs * len(secs) / sum(secs)
+    desc = (f"{len(sample)} of the 2^20 config-1 points (every {stride}th) x {len(src)} sources "
+            f"per step, value+grad at t_end")
     line = {
         "impl": "reference", "metric": "source x point pair evals/s (superpose, value+grad)",
         "value": v, "unit": "pairs/s", "n_gpus": args.gpus, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": float(W.CONFIG1_POINTS) * len(src) / v * 1e3,
+        "warmup": args.warmup, "ms_per_step": 1e3 * sum(secs) / len(secs),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded, SURVEY.md §8d)",
-        "config": {"workload": "config1: 2^20 points x 2^16 raster sources, superpose at t_end",
-                   "points": W.CONFIG1_POINTS, "sources": len(src), "cull_exponent": 60.0},
-        "cpu_baseline": cb,
+        "config": config1_dict(W.CONFIG1_POINTS, len(src), args.gpus),
+        "sample": {"sample_points": len(sample), "sample_fraction": len(sample) / len(all_pts),
+                   "pairs_per_step": pairs,
+                   "note": "ms_per_step is the measured time of the sampled step actually run"},
+        "cpu_baseline": {"value": v, "unit": "pairs/s", "cores": cores, "kind": kind,
+                         "sample": desc},
         "e2e": {"value": v, "unit": "pairs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -614,32 +666,37 @@ def run_ours(args):
 
     k1_mean_ms = prof["k1_ms"] / max(1, prof["k1_launches"])
     pairs_per_launch = prof["k1_pairs"] / max(1, prof["k1_launches"])
-    achieved = FLOPS_PER_PAIR * pairs_per_launch / (k1_mean_ms * 1e-3) / 1e12 if k1_mean_ms else None
     planar = bool(len(src)) and bool(np.all(src[:, 2] == src[0, 2])) and \
         not os.environ.get("TG_K1_NO_PLANAR")
     ops = PIPE_OPS_PER_PAIR_PLANAR if planar else PIPE_OPS_PER_PAIR
+    # the roofline: FP64 instructions the kernel must issue per pair x pairs
+    # per launch / mean launch time, against the FP64 pipe's DFMA issue rate
+    # (peak TFLOP/s / 2 instructions per second); MEASURED_PEAKS.json and the
+    # profiling recipe carry no FP64 figure, so the peak is the DFMA-chain
+    # microbenchmark run live on this GPU
+    pipe_peak = fp64_peak * 1e12 / 2 if fp64_peak else None
+    achieved_ops = ops * pairs_per_launch / (k1_mean_ms * 1e-3) if k1_mean_ms else None
+    alg = FLOPS_PER_PAIR * pairs_per_launch / (k1_mean_ms * 1e-3) / 1e12 if k1_mean_ms else None
     roof = {"kernel": f"k1_partial<{os.environ.get('TG_K1_P', '7')},true,{str(planar).lower()}>",
             "bound": "fp64",
-            "achieved": achieved,
-            "peak": fp64_peak, "unit": "TFLOP/s",
-            "frac": (achieved / fp64_peak) if (achieved and fp64_peak) else None,
+            "achieved": achieved_ops / 1e12 if achieved_ops else None,
+            "peak": pipe_peak / 1e12 if pipe_peak else None,
+            "unit": "T FP64 instr/s",
+            "frac": (achieved_ops / pipe_peak) if (achieved_ops and pipe_peak) else None,
             "traffic": K1_TRAFFIC_BYTES,
             "traffic_source": "ncu --set full, profiles/r01_k1_full_p7_planar.ncu-rep (dram "
                               "read+write)",
-            "peak_source": "measured live: tg_fp64_peak DFMA-chain microbenchmark on this GPU",
-            "flops_per_pair": FLOPS_PER_PAIR, "pairs_per_launch": pairs_per_launch,
+            "peak_source": "measured live: tg_fp64_peak DFMA-chain microbenchmark on this GPU "
+                           "(no FP64 entry in MEASURED_PEAKS.json or the recipe's fallback)",
+            "ops_per_pair": ops, "pairs_per_launch": pairs_per_launch,
             "mean_launch_ms": k1_mean_ms,
-            "note": "frac uses SURVEY.md §8d's 49 flops/pair, which counts the exponential at "
-                    "its libdevice cost (31 flops); this kernel evaluates it in 6 FP64 "
-                    "instructions (15-17 per pair in all), so the algorithmic rate exceeds the "
-                    "DFMA peak; fp64_pipe.frac is the issued-instruction share of the pipe",
-            "fp64_pipe": {
-                "ops_per_pair": ops,
-                "achieved_gops": (ops * pairs_per_launch / (k1_mean_ms * 1e-3) / 1e9
-                                  if k1_mean_ms else None),
-                "peak_gops": fp64_peak * 1e3 / 2 if fp64_peak else None,
-                "frac": (ops * pairs_per_launch / (k1_mean_ms * 1e-3) /
-                         (fp64_peak * 1e12 / 2)) if (k1_mean_ms and fp64_peak) else None},
+            "note": "frac = issued FP64-pipe instructions per pair (cuobjdump -sass of the "
+                    "kernel: 15 planar / 17 general) x pair rate / the pipe's issue rate. "
+                    "flops_49 restates it with SURVEY.md §8d's 49 flops/pair, which counts the "
+                    "exponential at its libdevice cost (31 flops) where this kernel spends 6 "
+                    "instructions, so that figure exceeds 1 and is not a roofline",
+            "flops_49": {"achieved_tflops": alg, "peak_tflops": fp64_peak,
+                         "frac": (alg / fp64_peak) if (alg and fp64_peak) else None},
             "k1_share_of_step": prof["k1_ms"] / max(1e-9, float(sum(step_ms)))}
     line = {
         "metric": "source x point pair evals/s (superpose, value+grad)",
@@ -647,10 +704,7 @@ def run_ours(args):
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded, SURVEY.md §8d)",
-        "config": {"workload": "config1: 2^20 points x 2^16 raster sources, superpose at t_end",
-                   "points_per_gpu": n, "sources": len(src), "cull_exponent": 60.0,
-                   "parallelism": f"point slabs x{world}, sources replicated",
-                   "l2": "flushed between steps (256 MiB write outside the step events)"},
+        "config": config1_dict(n, len(src), world),
         "e2e": {"value": e2e, "unit": "pairs/s", "h2d_bytes_per_step": int(pp.nbytes),
                 "d2h_bytes_per_step": int(pv.nbytes + pg.nbytes)},
         "gpu_launches": prof["launches"],
