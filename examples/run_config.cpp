@@ -2,7 +2,9 @@
 // the C++ shim (include/thermiga_b200.hpp). Build:
 //   g++ -std=c++17 -O2 -Iinclude examples/run_config.cpp \
 //       -Lpaper_2511_20432_b200/_lib -lthermiga_b200 -Wl,-rpath,$PWD/paper_2511_20432_b200/_lib
+#include <cmath>
 #include <cstdio>
+#include <vector>
 
 #include "thermiga_b200.hpp"
 
@@ -14,11 +16,19 @@ int main(int argc, char** argv) {
   try {
     thermiga_b200::Simulation sim(argv[1]);
     double peak = 0.0;
+    std::vector<double> last;
     const long iters = sim.run_time_loop([&](const thermiga_b200::State& s) {
       for (double v : s.free_coeffs) peak = v > peak ? v : peak;
+      last = s.free_coeffs;
     });
+    double amax = 0.0, l2 = 0.0;
+    for (double v : last) {
+      amax = std::fmax(amax, std::fabs(v));
+      l2 += v * v;
+    }
     std::printf("steps %d  cg iterations %ld  max correction coefficient %.6e\n", sim.n_steps,
                 iters, peak);
+    std::printf("final free coefficients: max|x| %.17g  |x|_2 %.17g\n", amax, std::sqrt(l2));
   } catch (const thermiga_b200::config_error& e) {
     std::fprintf(stderr, "%s\n", e.what());
     return 2;

@@ -141,6 +141,10 @@ int tg_sim_sources(tg_sim* sim, tg_point_source* out, int max_out);
 int tg_sim_face_sets(tg_sim* sim, int* qb_off, int* qf_off, double* centers, int* dofs,
                      double* xq, double* nq, double* wq, double* Nb, double* Nf);
 int tg_sim_greville_points(tg_sim* sim, double* out_xyz);
+/* The per-element local loads of the last flux-load call (n_face_elements x
+ * ndofs_kept, the columns of tg_sim_face_sets' dofs): assemble_boundary_load's
+ * `local` (proj/src/assembly.cpp:123-137) before the scatter. */
+int tg_sim_last_local_loads(tg_sim* sim, double* out);
 /* Banded 1D factors of the Kronecker operator for axis dir (n x (2p+1),
  * [i][p + j - i]); TG_ERROR when the patch is not separable. */
 int tg_sim_kron_factors(tg_sim* sim, int dir, double* M, double* K);

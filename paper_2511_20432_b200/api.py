@@ -352,6 +352,7 @@ def _bind_sim(L):
     L.tg_sim_sources.argtypes = [C.c_void_p, _dp, C.c_int]
     L.tg_sim_face_sets.argtypes = [C.c_void_p, _ip, _ip, _dp, _ip, _dp, _dp, _dp, _dp, _dp]
     L.tg_sim_greville_points.argtypes = [C.c_void_p, _dp]
+    L.tg_sim_last_local_loads.argtypes = [C.c_void_p, _dp]
     L.tg_sim_kron_factors.argtypes = [C.c_void_p, C.c_int, _dp, _dp]
     L.tg_sim_reduced_operator.argtypes = [C.c_void_p, _ip, _ip, _ip, _dp]
     L.tg_sim_reduced_operator.restype = C.c_long
@@ -478,6 +479,13 @@ class Simulation:
         out = np.zeros(2, dtype=np.int32)
         self._check(self._L.tg_sim_sumfact_prefix(self._h, t, out.ctypes.data_as(_ip)))
         return int(out[0]), int(out[1])
+
+    def last_local_loads(self):
+        """Per face element local loads of the last flux_load ((n_face_elems,
+        n_dofs_kept), columns as face_sets()['dofs'])."""
+        out = np.zeros((self.info["n_face_elems"], self.info["n_dofs_kept"]))
+        self._check(self._L.tg_sim_last_local_loads(self._h, _p(out)))
+        return out
 
     def greville_points(self):
         out = np.zeros((self.info["n_constrained"], 3))

@@ -182,6 +182,13 @@ int tg_sim_face_sets(tg_sim* s, int* qb_off, int* qf_off, double* centers, int* 
   }, false);
 }
 
+int tg_sim_last_local_loads(tg_sim* s, double* out) {
+  return sim_guard(s, [&](Sim& m) {
+    d2h(out, m.d_loc.p, static_cast<size_t>(m.n_fe) * m.ndk, m.ctx->stream);
+    TG_CUDA(cudaStreamSynchronize(m.ctx->stream));
+  });
+}
+
 int tg_sim_greville_points(tg_sim* s, double* out) {
   return sim_guard(s, [&](Sim& m) { std::memcpy(out, m.grev.data(), m.grev.size() * sizeof(double)); }, false);
 }
