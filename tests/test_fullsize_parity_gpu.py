@@ -15,15 +15,13 @@ compared step, both sides at solver_tol = 1e-12.
     own loads (assemble_flux_load, dirichlet_values, theta_step);
   * config 3 (302,974 free DOF, degree-3 rational part): the reference's
     first 2 steps and step 401 (the reference needs ~50 s per step);
-  * config 4 (4,393,224 DOF, 1e5 sources, K5 on): flux loads and Dirichlet
-    values at 3 instants against the reference's superpose on the face
-    quadrature / Greville points with the reference's assembly rules
-    (assembly.cpp:117-166, mesh.cpp:238-264) restated in numpy — the full
-    point set at one instant, an element sample holding the fine-rule
-    elements at the others. The reference's prepare_simulation for config 4
-    (~57 GB of CSR / element matrices) and its serial step do not fit this
-    suite's time budget; tools/cfg4_ref_probe.py runs that comparison
-    (profiles/r02_cfg4_ref_theta.md).
+  * config 4 (4,393,224 DOF, 1e5 sources, K5 on): one full step (flux load,
+    Dirichlet values, θ-step) against the reference's own prepare_simulation
+    / assemble_flux_load / theta_step, and the loads at two later instants
+    against the reference's superpose on the face quadrature / Greville
+    points with the reference's assembly rules (assembly.cpp:117-166,
+    mesh.cpp:238-264) restated in numpy, on an element sample holding the
+    fine-rule elements.
 """
 import os
 
@@ -225,26 +223,36 @@ def test_config4_sources_are_the_references(cfg4, ref):
     assert np.array_equal(src, cfg4.sources())
 
 
-def test_config4_loads_full_point_set(cfg4, ref):
-    """Step 1 (t = 1e-5 s): every lateral face quadrature point (589,824 plus
-    the fine rules) and every Greville point, K5 on (the GEMMs carry the
-    ~99k sources no cull reaches)."""
+def test_config4_step_against_reference(cfg4, ref):
+    """Step 3 (t = 3e-5 s) at full size against the reference's own
+    prepare_simulation / assemble_flux_load / theta_step (~5 min of host time:
+    138 s setup, 85 s threaded flux load, 66 s serial PCG on the box's 16
+    cores; profiles/r02_cfg4_ref_theta.md). The device's loads use K5 (the
+    GEMMs carry the ~99k sources no cull reaches); the Dirichlet values are
+    checked against the reference's superpose at its own Greville points
+    (dirichlet_values' serial loop would take ~4 min)."""
     s = cfg4
     s.set_sumfact(True)
-    fs = s.face_sets()
-    src = s.sources()
-    t = s.params["dt"]
-    F = s.flux_load(t)
+    s.reset()
+    s.advance(2)
+    st = s.state()
+    t3 = st["time"] + s.params["dt"]
+    F3 = s.flux_load(t3)
     assert s.sumfact_stats()["last_j_flux"] > 90000  # the K5 path really ran
-    Fr, _, fine = ref_flux_load(ref, fs, src, t, s.params["elevate_radius"], MAT["conductivity"],
-                                s.info["n_full"])
-    assert fine.any()
-    assert normwise(F, Fr) <= 1e-10, normwise(F, Fr)
-    assert np.array_equal(F == 0.0, Fr == 0.0)
-    g = s.dirichlet_values(t)
+    g3 = s.dirichlet_values(t3)
     assert s.sumfact_stats()["last_j_dirichlet"] > 90000
-    vr, _ = ref.superpose(src, s.greville_points(), t, threads=THREADS, grad=False, **MAT)
-    assert normwise(g, -vr) <= 1e-10
+    x3, it, _ = s.theta_step(st["free"], st["g"], st["F"], F3, g3, tol=1e-12)
+    r = ref.sim(CFG[4], threads=THREADS, solver_tol=1e-12)
+    Fr = r.flux_load(t3, threads=THREADS)
+    assert normwise(F3, Fr) <= 1e-10, normwise(F3, Fr)
+    assert np.array_equal(F3 == 0.0, Fr == 0.0)
+    vr, _ = ref.superpose(r.sources(), r.greville_points(), t3, threads=THREADS, grad=False,
+                          **MAT)
+    assert normwise(g3, -vr) <= 1e-10
+    xr, itr, _ = r.theta_step(st["free"], st["g"], st["F"], Fr, -vr, 1e-12)
+    r.close()
+    assert normwise(x3, xr) <= 1e-8, normwise(x3, xr)
+    assert abs(it - itr) <= max(3, 0.1 * itr), (it, itr)
 
 
 @pytest.mark.parametrize("step", [250, 1000])
