@@ -75,9 +75,10 @@ const char* tg_last_error(const tg_ctx* ctx);
  * CUDA events; tg_profile_read returns the summed milliseconds since the last
  * reset, the number of this library's kernel launches, and the work counted:
  * out = {k1_ms, k1_launches, k1_pairs, k2_ms (solve), k2_launches, k2_bytes,
- *        launches, theta_step_ms (expand + RHS + solve)}. */
+ *        launches, theta_step_ms (expand + RHS + solve), k5_ms (contraction),
+ *        k5_launches}. */
 int tg_set_profiling(tg_ctx* ctx, int on);
-int tg_profile_read(tg_ctx* ctx, double* out /* [8] */, int reset);
+int tg_profile_read(tg_ctx* ctx, double* out /* [10] */, int reset);
 /* FP64 issue-rate microbenchmark (independent DFMA chains over every SM);
  * the K1 roofline denominator. */
 int tg_fp64_peak(tg_ctx* ctx, double* out_tflops);
@@ -270,13 +271,19 @@ int tg_sim_flux_profile(tg_sim* sim, int face, int n_samples, double edge_v,
  * face quadrature / Greville points are tensor grids). On by default where
  * available; on = 0 makes every superposition a K1 pair loop. */
 int tg_sim_set_sumfact(tg_sim* sim, int on);
-/* out[8]: on, faces gridded, Greville grid, source prefix J of the last flux
- * call (the smallest over the faces), of the last Dirichlet call, GEMM flops
- * issued, point x source pairs evaluated by the GEMMs, sources per GEMM chunk */
+/* out[8]: on, faces gridded, Greville grid, the last call's contraction
+ * prefix J (the smallest over the flux regions; over the Greville regions),
+ * contraction flops issued since setup, regions, sources per work item */
 int tg_sim_sumfact_stats(tg_sim* sim, double* out);
-/* out[2]: the K5 source prefixes at time t (host arithmetic only): sources
- * [0, J) take the GEMMs — flux (the smallest over the faces), Dirichlet */
-int tg_sim_sumfact_prefix(tg_sim* sim, double t, int* out);
+/* K5 regions (one per contraction tile of the face grids, then of the
+ * Greville grid): out (n_regions x 8) = lo[3], hi[3], delta, points. */
+int tg_sim_sumfact_regions(tg_sim* sim, double* out);
+/* The K5 plan at time t restated on the host (no device needed): per region
+ * the contraction prefix J (sources [0, J)) and the end E of the pair-wise
+ * remainder [J, E) (later sources are culled on the whole region box). */
+int tg_sim_sumfact_plan(tg_sim* sim, double t, int* J, int* E);
+/* The plan the device computed in the last flux-load / Dirichlet call. */
+int tg_sim_sumfact_last_plan(tg_sim* sim, int* J, int* E);
 
 #ifdef __cplusplus
 }

@@ -219,11 +219,11 @@ class Context:
         self._check(self._L.tg_set_profiling(self._h, int(on)))
 
     def profile(self, reset: bool = False) -> dict:
-        out = np.zeros(8)
+        out = np.zeros(10)
         self._check(self._L.tg_profile_read(self._h, _p(out), int(reset)))
         return dict(k1_ms=out[0], k1_launches=int(out[1]), k1_pairs=out[2], k2_ms=out[3],
                     k2_launches=int(out[4]), k2_bytes=out[5], launches=int(out[6]),
-                    theta_step_ms=out[7])
+                    theta_step_ms=out[7], k5_ms=out[8], k5_launches=int(out[9]))
 
     @staticmethod
     def _csr(A):
@@ -370,7 +370,9 @@ def _bind_sim(L):
     L.tg_sim_flux_profile.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_double, _dp, _dp]
     L.tg_sim_set_sumfact.argtypes = [C.c_void_p, C.c_int]
     L.tg_sim_sumfact_stats.argtypes = [C.c_void_p, _dp]
-    L.tg_sim_sumfact_prefix.argtypes = [C.c_void_p, C.c_double, _ip]
+    L.tg_sim_sumfact_regions.argtypes = [C.c_void_p, _dp]
+    L.tg_sim_sumfact_plan.argtypes = [C.c_void_p, C.c_double, _ip, _ip]
+    L.tg_sim_sumfact_last_plan.argtypes = [C.c_void_p, _ip, _ip]
     L._sim_bound = True
 
 
@@ -472,13 +474,32 @@ class Simulation:
         self._check(self._L.tg_sim_sumfact_stats(self._h, _p(out)))
         return dict(on=bool(out[0]), faces_gridded=bool(out[1]), greville_gridded=bool(out[2]),
                     last_j_flux=int(out[3]), last_j_dirichlet=int(out[4]), gemm_flops=out[5],
-                    pairs_off_k1=out[6], chunk=int(out[7]))
+                    regions=int(out[6]), item=int(out[7]))
 
-    def sumfact_prefix(self, t: float):
-        """(J_flux, J_dirichlet): sources [0, J) that K5 puts on the GEMMs at t."""
-        out = np.zeros(2, dtype=np.int32)
-        self._check(self._L.tg_sim_sumfact_prefix(self._h, t, out.ctypes.data_as(_ip)))
-        return int(out[0]), int(out[1])
+    def sumfact_regions(self):
+        """K5 regions (flux tiles, then Greville tiles): (n, 8) = lo[3], hi[3],
+        delta, points."""
+        out = np.zeros((self.sumfact_stats()["regions"], 8))
+        self._check(self._L.tg_sim_sumfact_regions(self._h, _p(out)))
+        return out
+
+    def sumfact_plan(self, t: float):
+        """The K5 plan at t restated on the host: per region (J, E)."""
+        n = self.sumfact_stats()["regions"]
+        J = np.zeros(n, dtype=np.int32)
+        E = np.zeros(n, dtype=np.int32)
+        self._check(self._L.tg_sim_sumfact_plan(self._h, float(t), J.ctypes.data_as(_ip),
+                                                E.ctypes.data_as(_ip)))
+        return J, E
+
+    def sumfact_last_plan(self):
+        """The plan the device computed in the last flux-load / Dirichlet call."""
+        n = self.sumfact_stats()["regions"]
+        J = np.zeros(n, dtype=np.int32)
+        E = np.zeros(n, dtype=np.int32)
+        self._check(self._L.tg_sim_sumfact_last_plan(self._h, J.ctypes.data_as(_ip),
+                                                     E.ctypes.data_as(_ip)))
+        return J, E
 
     def last_local_loads(self):
         """Per face element local loads of the last flux_load ((n_face_elems,

@@ -191,6 +191,8 @@ int tg_profile_read(tg_ctx* ctx, double* out, int reset) {
     out[5] = ctx->timer.k2_bytes;
     out[6] = static_cast<double>(ctx->timer.launches);
     out[7] = ctx->timer.step_ms;  // whole theta steps (expand + RHS + solve)
+    out[8] = ctx->timer.k5_ms;    // K5 contraction launches
+    out[9] = static_cast<double>(ctx->timer.k5_launches);
     if (reset) ctx->timer.reset();
   });
 }

@@ -64,10 +64,11 @@ struct KernelTimer {
   bool on = false;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> live;  // pending pairs
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pool;
-  double k1_ms = 0.0, k2_ms = 0.0, step_ms = 0.0;  // kinds 1, 2, 3 (whole theta step)
+  // kinds 1 (K1 main), 2 (K2 main), 3 (whole theta step), 5 (K5 contraction)
+  double k1_ms = 0.0, k2_ms = 0.0, step_ms = 0.0, k5_ms = 0.0;
   std::vector<int> kinds;
   double k1_pairs = 0.0, k2_bytes = 0.0;
-  long launches = 0, k1_launches = 0, k2_launches = 0;
+  long launches = 0, k1_launches = 0, k2_launches = 0, k5_launches = 0;
 
   std::pair<cudaEvent_t, cudaEvent_t> get() {
     if (!pool.empty()) {
@@ -99,7 +100,7 @@ struct KernelTimer {
       TG_CUDA(cudaEventSynchronize(live[i].second));
       float ms = 0.f;
       TG_CUDA(cudaEventElapsedTime(&ms, live[i].first, live[i].second));
-      (kinds[i] == 1 ? k1_ms : kinds[i] == 2 ? k2_ms : step_ms) += ms;
+      (kinds[i] == 1 ? k1_ms : kinds[i] == 2 ? k2_ms : kinds[i] == 5 ? k5_ms : step_ms) += ms;
       pool.push_back(live[i]);
     }
     live.clear();
@@ -107,9 +108,9 @@ struct KernelTimer {
   }
   void reset() {
     collect();
-    k1_ms = k2_ms = step_ms = 0.0;
+    k1_ms = k2_ms = step_ms = k5_ms = 0.0;
     k1_pairs = k2_bytes = 0.0;
-    launches = k1_launches = k2_launches = 0;
+    launches = k1_launches = k2_launches = k5_launches = 0;
   }
   ~KernelTimer() {
     for (auto& e : live) pool.push_back(e);

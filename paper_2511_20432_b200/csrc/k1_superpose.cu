@@ -109,15 +109,22 @@ __global__ void __launch_bounds__(kK1Threads,
                                   P >= 6 ? 256 / kK1Threads : (P >= 4 ? K1_MINB4 : 3))
     k1_partial(const SrcRec* __restrict__ src, int n_src, int split_len,
                const double* __restrict__ pts, const int* __restrict__ pt_index, int n_pts,
-               double* __restrict__ part, double zs) {
+               double* __restrict__ part, double zs, K1Ranges rg) {
   __shared__ __align__(128) SrcRec ring[kK1Stages][kK1Chunk];
   __shared__ double tab[kExpTableSize];
   __shared__ __align__(8) uint64_t bars[kK1Stages];
 
   const int tid = threadIdx.x;
   const int s = blockIdx.y;
-  const int begin = s * split_len;
-  const int len = max(0, min(n_src, begin + split_len) - begin);
+  int begin = s * split_len;
+  int len = max(0, min(n_src, begin + split_len) - begin);
+  if (rg.cta_region) {  // this CTA's points take their region's range [J, E) only
+    const int r = rg.cta_region[blockIdx.x];
+    const int J = rg.J[r], E = min(rg.E[r], n_src);
+    const int L = (max(0, E - J) + gridDim.y - 1) / gridDim.y;
+    begin = J + s * L;
+    len = max(0, min(E, begin + L) - begin);
+  }
   const int n_chunks = (len + kK1Chunk - 1) / kK1Chunk;
 
   for (int q = tid; q < kExpTableSize; q += kK1Threads) tab[q] = c_exp_table[q];
@@ -312,9 +319,8 @@ __global__ void k1_combine_flux(const double* __restrict__ part, int S, int n,
 // host side
 // ---------------------------------------------------------------------------
 
-void k1_upload_exp_table(cudaStream_t stream) {
+void k1_exp_table_host(double* tab) {
   // 2^(j/1024) with (j << 10) pre-subtracted from the high word (src_exp)
-  double tab[kExpTableSize];
   for (int j = 0; j < kExpTableSize; ++j) {
     const double v = static_cast<double>(exp2l(static_cast<long double>(j) / kExpTableSize));
     uint64_t bits;
@@ -322,6 +328,11 @@ void k1_upload_exp_table(cudaStream_t stream) {
     bits -= static_cast<uint64_t>(j) << (20 - kExpBits + 32);
     std::memcpy(&tab[j], &bits, 8);
   }
+}
+
+void k1_upload_exp_table(cudaStream_t stream) {
+  static double tab[kExpTableSize];
+  k1_exp_table_host(tab);
   cudaMemcpyToSymbolAsync(c_exp_table, tab, sizeof(tab), 0, cudaMemcpyHostToDevice, stream);
 }
 
@@ -344,13 +355,13 @@ void k1_prepare(const double* d_src6, int n, double t, double alpha, double rcp,
 
 void k1_launch_partial(const SrcRec* d_rec, int n_src, const double* d_pts,
                        const int* d_index, int n_pts, int S, bool grad, int P, double* d_part,
-                       cudaStream_t stream, bool planar, double zs) {
+                       cudaStream_t stream, bool planar, double zs, const K1Ranges& rg) {
   const int split_len = (n_src + S - 1) / S;
   const int ppc = kK1Threads * P;
   dim3 grid((n_pts + ppc - 1) / ppc, S);
 #define TG_K1_LAUNCH(PP, GG, PLN)                                                         \
   k1_partial<PP, GG, PLN><<<grid, kK1Threads, 0, stream>>>(d_rec, n_src, split_len, d_pts,     \
-                                                          d_index, n_pts, d_part, zs)
+                                                          d_index, n_pts, d_part, zs, rg)
   // planar-history variants for the default shapes (P = 7 with gradient, 5 value-only;
   // measured best: gradient P=6/7/8 76.8/75.3/78.7 ms, value-only P=4/5/6 62.2/59.2/61.8)
   if (planar && grad && P == 7) {

@@ -31,14 +31,25 @@ constexpr int kK1Chunk = K1_CHUNK;  // sources per shared-memory stage (12 KB)
 constexpr int kK1Stages = 3;
 constexpr int kMaxSplits = 16;  // source splits of one launch (k1_choose_splits)
 
+// Per-CTA source ranges (K5's remainder launch): CTA x takes only the sources
+// [J[r], E[r]) of its region r = cta_region[x], split over grid.y; null =
+// the launch's one range.
+struct K1Ranges {
+  const int* cta_region = nullptr;
+  const int* J = nullptr;
+  const int* E = nullptr;
+};
+
 void k1_upload_exp_table(cudaStream_t stream);
+// the src_exp table (common.cuh) on the host: kExpTableSize doubles
+void k1_exp_table_host(double* tab);
 int k1_choose_splits(int n_pts, int n_src, int sm_count, int points_per_cta);
 void k1_prepare(const double* d_src6, int n, double t, double alpha, double rcp, double cull,
                 SrcRec* d_rec, cudaStream_t stream);
 // planar: all sources lie on z = zs (k1_partial's PLANAR variant)
 void k1_launch_partial(const SrcRec* d_rec, int n_src, const double* d_pts, const int* d_index,
                        int n_pts, int S, bool grad, int P, double* d_part, cudaStream_t stream,
-                       bool planar = false, double zs = 0.0);
+                       bool planar = false, double zs = 0.0, const K1Ranges& rg = K1Ranges{});
 void k1_launch_combine_field(const double* d_part, int S, int n, double* d_val, double* d_grad,
                              cudaStream_t stream);
 void k1_launch_combine_dirichlet(const double* d_part, int S, int n, double* d_out,

@@ -938,6 +938,7 @@ struct ProCg1S {  // rings: 0 u_i, 1 w^_i, 2 s^_{i-1}; centre ring: x, p_{i-1}
   double a, b;
   OwnDiag<P> od;
   double gamma, rr;
+  int zo0 = -(1 << 30), zo1 = 1 << 30;  // planes whose points enter the dot products
 
   __device__ void issue(const Seg& sg, int step) const {
     const int q = *cseq + step, slot = q & 1;
@@ -985,9 +986,11 @@ struct ProCg1S {  // rings: 0 u_i, 1 w^_i, 2 s^_{i-1}; centre ring: x, p_{i-1}
           const double unew = fma(-alpha, snew, uo);               // u_{i+1}
           s_out[f] = snew;
           u_out[f] = unew;
-          const double ru = od.at(kin, a, b) * unew;               // r_{i+1} = D u_{i+1}
-          gamma = fma(ru, unew, gamma);
-          rr = fma(ru, ru, rr);
+          if (kin >= zo0 && kin < zo1) {
+            const double ru = od.at(kin, a, b) * unew;             // r_{i+1} = D u_{i+1}
+            gamma = fma(ru, unew, gamma);
+            rr = fma(ru, ru, rr);
+          }
         }
       }
     }
@@ -1013,9 +1016,10 @@ struct EpiCg1S {  // w^ = D^-1 (A u), delta = (A u).u; own diagonal from the pro
   const Own* own;
   double a, b;
   double delta;
+  int zo0 = -(1 << 30), zo1 = 1 << 30;
   __device__ void operator()(size_t idx, int, int, int k, double y, double u) {
     w_out[idx] = y * recip(own->od.at(k, a, b));
-    delta = fma(y, u, delta);
+    if (k >= zo0 && k < zo1) delta = fma(y, u, delta);
   }
 };
 
@@ -1030,6 +1034,7 @@ struct EpiCg1InitS {  // r0 = b - A x0; u0 = D^-1 r0; s^_{-1} = p_{-1} = 0; r.r,
   OwnDiag<P> od;
   int ci, cj;
   double acc[4];
+  int zo0 = -(1 << 30), zo1 = 1 << 30;
   __device__ void operator()(size_t idx, int i, int j, int k, double y, double) {
     if (i != ci || j != cj) {
       od.set(*g, i, j);
@@ -1042,9 +1047,11 @@ struct EpiCg1InitS {  // r0 = b - A x0; u0 = D^-1 r0; s^_{-1} = p_{-1} = 0; r.r,
     u[idx] = ui;
     s[idx] = 0.0;
     p[idx] = 0.0;
-    acc[0] += ri * ri;
-    acc[1] += bi * bi;
-    acc[2] += ri * ui;
+    if (k >= zo0 && k < zo1) {
+      acc[0] += ri * ri;
+      acc[1] += bi * bi;
+      acc[2] += ri * ui;
+    }
   }
 };
 
@@ -1288,6 +1295,181 @@ __global__ void __launch_bounds__(kThreads, K2_MINB)
 }
 
 // --------------------------------------------------------------------------
+// The single-sweep solve on one z-slab of the free grid (multi-GPU: one slab
+// per rank). The slab holds its own planes plus P ghost planes per interior
+// side; each launch is ONE sweep of the persistent kernel above (the same
+// prologue / epilogue functors) with the dot products restricted to the own
+// planes, and the scalar recurrences advanced at the start of the next launch
+// from the ranks' partial sums (summed in rank order, so every rank computes
+// the same alpha, beta and stop decision). Between launches the caller
+// exchanges the P ghost planes of the vector the sweep wrote (u_0, w^_0, then
+// w^ each iteration: the only halo the next prologue reads that the rank
+// cannot recompute) and all-gathers the 4 partials (NCCL over NVLink, or
+// device copies between slabs of one GPU).
+template <int P, int PL>
+__global__ void __launch_bounds__(kThreads, K2_MINB)
+    k2_slab_kernel(KronGrid g, double a, double b, const double* rhs, double* x, Cg1Work w,
+                   double tol, int max_iter, TileIdx T, const __grid_constant__ Cg1Maps maps,
+                   SlabCtl ctl) {
+  constexpr int NIN = kCg1Nin;
+  using SMT = KSmem<P, PL, NIN, 1, kCg1Stages, kCg1Ub>;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  auto& sm = *reinterpret_cast<SMT*>(smem_raw);
+  double* zb =
+      reinterpret_cast<double*>(smem_raw + zband_offset<P, PL, NIN, 1, kCg1Stages, kCg1Ub>());
+  auto* cr = reinterpret_cast<CentreRing<PL>*>(smem_raw + cg1_centre_offset<P, PL>(g.n[2]));
+  __shared__ double red[64];
+  __shared__ int last_block;
+  const int tid = threadIdx.y * kKronTX + threadIdx.x;
+  const bool lead = blockIdx.x == 0 && tid == 0;
+
+  // ---- the scalars (identical in every CTA of every rank)
+  SlabState st = *ctl.sin;
+  double tot[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int r = 0; r < ctl.world; ++r)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) tot[c] += ctl.gath[4 * r + c];
+  double beta = 0.0;
+  bool zero_x = false;
+  if (ctl.phase == 0) {
+    st = SlabState{0.0, 0.0, 0.0, 0.0, 0.0, 0, 3, 1, 0};
+  } else if (!st.done && ctl.phase == 1) {  // r.r, b.b, r.u of the initial residual
+    st.bnorm = sqrt(tot[1]);
+    if (st.bnorm == 0.0) {  // sparse.cpp:57-60: zero rhs resets even a warm start
+      zero_x = true;
+      st.status = 0;
+      st.rel = 0.0;
+      st.done = 1;
+    } else {
+      st.rel = sqrt(tot[0]) / st.bnorm;
+      if (max_iter <= 0 || st.rel <= tol) {
+        st.status = max_iter <= 0 ? 3 : 0;
+        st.done = 1;
+      }
+      st.gamma = tot[2];
+    }
+    st.stage = 2;
+  } else if (!st.done && st.stage == 2) {  // delta_0 = (A u0).u0
+    if (!(tot[0] > 0.0)) {
+      st.status = 4;
+      st.done = 1;
+    } else {
+      st.alpha = st.gamma / tot[0];
+      beta = 0.0;
+    }
+    st.stage = 3;
+  } else if (!st.done) {  // the previous sweep's gamma', delta', r.r
+    ++st.it;
+    bool stop = st.it >= max_iter;  // the reference leaves after max_iter updates untested
+    if (!stop) {
+      st.rel = sqrt(tot[2]) / st.bnorm;
+      if (st.rel <= tol) {
+        st.status = 0;
+        stop = true;
+      }
+    }
+    if (stop) {
+      st.done = 1;
+    } else {
+      const double g1 = tot[0];
+      beta = g1 / st.gamma;
+      const double den = tot[1] - beta * g1 / st.alpha;  // p_{i+1}.A p_{i+1}
+      if (!(den > 0.0)) {
+        st.status = 4;
+        st.done = 1;
+      } else {
+        st.alpha = g1 / den;
+        st.gamma = g1;
+      }
+    }
+  }
+  st.beta = beta;
+  if (lead) *ctl.sout = st;
+  const int nx = g.n[0], ny = g.n[1];
+  if (zero_x) {
+    const size_t n = static_cast<size_t>(nx) * ny * g.n[2];
+    for (size_t f = static_cast<size_t>(blockIdx.x) * kThreads + tid; f < n;
+         f += static_cast<size_t>(gridDim.x) * kThreads)
+      x[f] = 0.0;
+  }
+  if (st.done) return;
+
+  // ---- one sweep
+  if (threadIdx.x == 0 && threadIdx.y == 0)
+    for (int v = 0; v < 2; ++v)
+      for (int q = 0; q < 2; ++q) mbar_init(&cr->bar[v][q], 1);
+  init_smem(g, sm, zb, true);
+  int cseq = 0;
+  int seq[4] = {0, 0, 0, 0};
+  const KronTerms c{a, b, 0.0, 0.0};
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  if (ctl.phase == 0) {  // r0 = b - A x0, u0 = D^-1 r0, s = p = 0
+    EpiCg1InitS<P> e0{rhs, w.r[0], w.s[0], w.p, &g, a, b, {{}, zb, g.n[2]}, -1, -1,
+                      {0, 0, 0, 0}, ctl.zo0, ctl.zo1};
+    Inputs<1> in1{{x}, {&maps.x}};
+    ProCopy<P, PL> pcp{&g, nx, ny, {{}, zb, g.n[2]}};
+    for_segments(T, gridDim.x, blockIdx.x, [&](const Seg& sg) {
+      kron_tile<P, PL, 1, 1, true>(g, c, in1, pcp, sg, sm, zb, seq, e0);
+    });
+    for (int q = 0; q < 4; ++q) acc[q] = e0.acc[q];
+  } else if (ctl.phase == 1) {  // w^0 = D^-1 A u0, delta0
+    ProCopy<P, PL> pcp{&g, nx, ny, {{}, zb, g.n[2]}};
+    EpiCg1S<P, ProCopy<P, PL>> e1{w.w[0], &pcp, a, b, 0.0, ctl.zo0, ctl.zo1};
+    Inputs<1> in1{{w.r[0]}, {&maps.r[0]}};
+    for_segments(T, gridDim.x, blockIdx.x, [&](const Seg& sg) {
+      kron_tile<P, PL, 1, 1, true>(g, c, in1, pcp, sg, sm, zb, seq, e1);
+    });
+    acc[0] = e1.delta;
+  } else {
+    const int cur = ctl.cur;
+    ProCg1S<P, PL> pc{st.alpha, beta, x, w.p, w.r[cur ^ 1], w.s[cur ^ 1], nx, ny, cr, &maps.xc,
+                      &maps.pc, &cseq, &g, a, b, {{}, zb, g.n[2]}, 0.0, 0.0, ctl.zo0, ctl.zo1};
+    EpiCg1S<P, ProCg1S<P, PL>> e{w.w[cur ^ 1], &pc, a, b, 0.0, ctl.zo0, ctl.zo1};
+    const Inputs<NIN> in{{w.r[cur], w.w[cur], w.s[cur]}, {&maps.r[cur], &maps.w[cur], &maps.s[cur]}};
+    for_segments(T, gridDim.x, blockIdx.x, [&](const Seg& sg) {
+      kron_tile<P, PL, NIN, 1, true>(g, c, in, pc, sg, sm, zb, seq, e);
+    });
+    acc[0] = pc.gamma;
+    acc[1] = e.delta;
+    acc[2] = pc.rr;
+  }
+
+  // ---- this rank's partial sums: a fixed tree per CTA, then the last CTA to
+  // arrive sums the CTA partials in block order (deterministic)
+  const int lane = tid & 31, warp = tid >> 5;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    double v = acc[q];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    if (lane == 0) red[warp * 4 + q] = v;
+  }
+  __syncthreads();
+  if (tid < 4) {
+    double v = 0.0;
+    for (int q = 0; q < kThreads / 32; ++q) v += red[q * 4 + tid];
+    ctl.cta_part[blockIdx.x * 4 + tid] = v;
+  }
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) last_block = atomicAdd(ctl.ticket, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (last_block && warp == 0) {
+    __threadfence();
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      double v = 0.0;
+      for (int bb = lane; bb < static_cast<int>(gridDim.x); bb += 32)
+        v += ctl.cta_part[bb * 4 + q];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+      if (lane == 0) ctl.mine[q] = v;
+    }
+    if (lane == 0) *ctl.ticket = 0u;
+  }
+}
+
+// --------------------------------------------------------------------------
 // TMA descriptor encoding through the driver entry point (no -lcuda)
 
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
@@ -1499,6 +1681,30 @@ void k2_cg1_solve(const KronGrid& g, double a, double b, const double* rhs, doub
     TG_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(&k2_cg1_kernel<P, PL>),
                                         grid, block, args, cg1_smem_bytes<P, PL>(g.n[2]), s));
   }));
+}
+
+int k2_slab_max_blocks(int p, int sm_count, int nz, int pl) {
+  int per_sm = 0;
+  TG_KRON_DISPATCH(p, TG_CG1_PL_DISPATCH(pl, {
+    const size_t sb = cg1_smem_bytes<P, PL>(nz);
+    allow_smem(k2_slab_kernel<P, PL>, sb);
+    TG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+        &per_sm, reinterpret_cast<const void*>(&k2_slab_kernel<P, PL>), kThreads, sb));
+  }));
+  return std::max(1, per_sm) * sm_count;
+}
+
+void k2_slab_launch(const KronGrid& g, double a, double b, const double* rhs, double* x,
+                    const Cg1Work& w, const Cg1Maps& maps, double tol, int max_iter, int blocks,
+                    const SlabCtl& ctl, cudaStream_t s, int pl) {
+  const TileIdx T = make_tiles(g);
+  const int nb = seg_blocks(T, blocks);
+  dim3 grid(nb), block(kKronTX, kKronTY);
+  TG_KRON_DISPATCH(g.p, TG_CG1_PL_DISPATCH(pl, {
+    k2_slab_kernel<P, PL><<<grid, block, cg1_smem_bytes<P, PL>(g.n[2]), s>>>(
+        g, a, b, rhs, x, w, tol, max_iter, T, maps, ctl);
+  }));
+  TG_CUDA(cudaGetLastError());
 }
 
 }  // namespace tgb

@@ -130,4 +130,27 @@ void k2_cg1_solve(const KronGrid& g, double a, double b, const double* rhs, doub
 void k2_apply(const KronGrid& g, double a, double b, const double* v, double* y, int sm_count,
               cudaStream_t s, const TensorMap3* v_map = nullptr);
 
+// ---- the single-sweep solve on one z-slab (multi-GPU; k2_kron.cu)
+// Scalars carried from launch to launch (double-buffered by the caller).
+struct SlabState {
+  double alpha, beta, gamma, bnorm, rel;
+  int it, status, stage, done;  // stage 1: init sums pending, 2: delta_0 pending, 3: iterating
+};
+struct SlabCtl {
+  int phase;            // 0: r0 / u0 sweep, 1: w^0 sweep, 2: an iteration sweep
+  int cur;              // the ping-pong buffers an iteration sweep reads
+  int zo0, zo1;         // own planes (local indices) of the dot products
+  int world;
+  const double* gath;   // world x 4 partial sums of the previous launch, rank order
+  double* mine;         // this launch's 4 partial sums
+  const SlabState* sin;
+  SlabState* sout;
+  double* cta_part;     // >= 4 per CTA
+  unsigned int* ticket; // zero between launches
+};
+int k2_slab_max_blocks(int p, int sm_count, int nz, int pl);
+void k2_slab_launch(const KronGrid& g, double a, double b, const double* rhs, double* x,
+                    const Cg1Work& w, const Cg1Maps& maps, double tol, int max_iter, int blocks,
+                    const SlabCtl& ctl, cudaStream_t s, int pl);
+
 }  // namespace tgb

@@ -1,0 +1,131 @@
+// K5 — sum-factorised superposition on tensor-grid point sets, fused
+// (see k5_fused.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <vector>
+
+#include "k1_superpose.cuh"
+
+namespace tgb {
+
+// CTA output tile of the contraction (a rows x b columns of one grid) and the
+// sources per shared-memory stage / per stream-K work item.
+constexpr int kSfTA = 64;
+constexpr int kSfTB = 96;
+constexpr int kSfKS = 32;
+constexpr int kSfItem = 1024;
+constexpr int kSfThreads = 256;  // 8 warps (2 x 4 of 32 x 24), 2 CTAs per SM
+
+// A point set that is a tensor grid up to coordinate rounding: point (a, b)
+// sits at (xf on axis axn, U[a] on axu, V[b] on axv).
+struct SfGridDesc {
+  int axn, axu, axv, na, nb;
+  int flux;     // 1: the normal derivative (flux integrand), 0: the value (Dirichlet)
+  int vplane;   // 1: every source has V coordinate vs: the B exponent is cb[b] * nisp
+  double xf;
+  const double* U;
+  const double* V;
+  const double* cb;  // (V[b] - vs)^2 when vplane
+};
+
+// A CTA tile: rows [a0, a0 + na) x columns [b0, b0 + nb) of grid `grid`, whose
+// sources come from region `region` (J = the contraction's prefix).
+struct SfTile {
+  int grid, a0, b0, na, nb, region;
+};
+
+// A region: points whose box [lo, hi] (+- delta per axis) decides which
+// sources no cull can reach anywhere in it (the contraction's prefix [0, J))
+// and which are culled everywhere in it (dropped from the pair-wise
+// remainder [J, E)). npts: its point count (profitability).
+struct SfRegion {
+  double lo[3], hi[3];
+  double delta;
+  double npts;
+};
+
+struct SfPlanArgs {
+  const double* src6;
+  int n_act;           // the causally active prefix (later sources are exact zeros)
+  double t, alpha, cull;
+  double min_pairs;    // J * npts below this: no contraction for the region (K1 is cheaper)
+  bool gemm;           // false: J = 0 everywhere (every pair on K1)
+};
+
+// Per (grid, source) constants of the factors (64 bytes): u, v, nisp =
+// -(1024/ln2)/spread, magicL = L + 1.5*2^52 and the folded cubic q0..q2, pad
+// (= q3) of the A factor (src_exp's representation, common.cuh; zero for
+// inactive sources).
+struct SfConst {
+  double u, v, nisp, magicL, q0, q1, q2, pad;
+};
+
+// Which regions a call computes: static flux tiles [0, nt_flux), Greville
+// tiles [nt_flux, nt_static), the step's fine regions after n_static_regions;
+// parts not requested, and (multi-GPU) regions r with r % world != rank, get
+// J = E = 0 (no work; their outputs come out as zeros).
+struct SfPlanMask {
+  bool flux, dir;
+  int nt_flux, nt_static;
+  int rank, world;
+};
+// regions' J, E (the computed static regions' also into Jlast / Elast, kept
+// across calls for queries); tiles' item prefix (n_tiles + 1) and the call's
+// contraction flops (2 na nb J summed over the tiles) added to stats[0]
+void sf_plan(const SfPlanArgs& a, const SfRegion* d_regions, int n_regions, int* d_J, int* d_E,
+             const SfPlanMask& mask, int n_static_regions, int* d_Jlast, int* d_Elast,
+             cudaStream_t s);
+void sf_items(const SfTile* d_tiles, int n_tiles, const int* d_J, int* d_prefix, double* stats,
+              cudaStream_t s);
+void sf_prep(const double* d_src6, int n_act, double t, double alpha, double rcp,
+             const SfGridDesc* d_grids, int n_grids, int max_src, SfConst* d_cst, cudaStream_t s);
+
+// The persistent stream-K contraction: the items (tile, 1024-source chunk) of
+// all tiles split evenly over `ctas` CTAs; each CTA accumulates its run of
+// items per tile in registers (DMMA m8n8k4) and writes one partial tile per
+// (tile t, CTA c) to slot t + c of `scratch` (kSfTA * kSfTB doubles each, cell
+// (a, b) at a + kSfTA * b). Deterministic: the split depends only on the item
+// count and `ctas`.
+void sf_contract_fused(const SfGridDesc* d_grids, const SfTile* d_tiles, int n_tiles,
+                       const int* d_prefix, const int* d_J, const SfConst* d_cst, int max_src,
+                       const double* d_tab, double* d_scratch, int ctas, cudaStream_t s);
+int sf_contract_max_ctas(int sm_count);
+
+// Entries of the pair-wise remainder launch (K1 with per-region ranges): one
+// per point, grouped by region and padded to whole K1 CTAs.
+struct SfEntries {
+  const int* q;      // point id (into the flux quadrature points, Greville after them)
+  const int* pos;    // output slot (compact flux point / constrained DOF), -1 = none
+  const int* tile;   // the point's contraction tile, -1 = none
+  const int* cell;   // its cell in the tile
+};
+
+// positions of the static flux entries: pos = elem_off[e] + (q - qb_off[e])
+// unless element e takes its fine rule this step (elem_off < 0, k3_flux.cu),
+// or the entry is padding (tile < 0): then -1
+void sf_base_positions(int n, const int* d_q, const int* d_tile, const int* d_qelem,
+                       const int* d_qb_off, const int* d_elem_off, int* d_pos, cudaStream_t s);
+
+// gq[pos] = (-k (grad.n)) w from the remainder's partials + (-k (G n_axn)) w,
+// over entries [e0, e1) (flux); g[pos] = -v - G over [d0, d1) (Dirichlet).
+// G = the sum over the tile's segments in CTA order (sf_contract_fused).
+struct SfAddArgs {
+  SfEntries ent;
+  const double* part;  // K1 partial planes: S x 4 x n_entries
+  int S, n_entries;
+  const SfGridDesc* grids;
+  const SfTile* tiles;
+  const int* prefix;
+  int n_tiles, ctas;
+  const double* scratch;
+  const double* normals;
+  const double* weights;
+  double k;
+  double* gq;
+  double* g;
+};
+void sf_add(const SfAddArgs& a, int e0, int e1, bool flux, cudaStream_t s);
+
+}  // namespace tgb

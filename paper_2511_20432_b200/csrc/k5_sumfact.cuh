@@ -1,7 +1,6 @@
-// K5 — sum-factorised superposition on tensor-grid point sets (see k5_sumfact.cu).
+// K5 host side: tensor-grid detection and the region source tests (see k5_sumfact.cu).
 #pragma once
 
-#include <cublas_v2.h>
 #include <cuda_runtime.h>
 
 #include <vector>
@@ -39,50 +38,5 @@ bool sf_source_eligible(const double* src6, double t, double alpha, double cull,
 // zeros there, and K1 may skip it.
 bool sf_source_culled(const double* src6, double t, double alpha, double cull,
                       const double lo[3], const double hi[3]);
-
-struct SfDev {
-  int axn, axu, axv, na, nb;
-  double xf;
-  const double* U;
-  const double* V;
-};
-
-struct SfScratch {  // caller-owned device scratch, sized by sf_scratch_doubles
-  double* fac;      // Jpad
-  double* inv_s;    // Jpad
-  double* su;       // Jpad
-  double* sv;       // Jpad
-  double* A;        // na * Jpad
-  double* B;        // Jpad * nb
-  double* Cpart;    // C * na * nb
-};
-
-// G[e] (na x nb, column-major) = sum over sources j < J of
-//   value: c_j e^{-dn^2/s} e^{-du_a^2/s} e^{-dv_b^2/s}
-//   grad:  c_j e^{-dn^2/s} (-dn / (2 alpha dt)) e^{-du_a^2/s} e^{-dv_b^2/s}
-// (dn, du, dv: grid point minus source along axn, axu, axv; s = 4 alpha dt;
-// c_j = E / (rho c (pi s)^1.5)) as one strided-batched DGEMM over Kc-source
-// chunks and a fixed-order chunk reduction. Returns the GEMM flops.
-double sf_contract(cublasHandle_t h, const SfDev& g, bool grad, const double* d_src6, int J,
-                   int Kc, double t, double alpha, double rcp, const SfScratch& w, double* d_G,
-                   cudaStream_t s);
-
-// gq[i] += (-k (G[gcell[q]] n_q[axn_q])) w_q for the compact points i whose
-// quadrature point q = pt_index[i] is a gridded base point (gcell[q] >= 0)
-void sf_add_flux(int n, const int* d_pt_index, int n_base, const int* d_gcell, const int* d_gaxn,
-                 const double* d_G, const double* d_normals, const double* d_weights, double k,
-                 double* d_gq, cudaStream_t s);
-// g[c] -= G[gcell[c]] (g = -T~ at the Greville points)
-void sf_add_dirichlet(int n, const int* d_gcell, const double* d_G, double* d_g, cudaStream_t s);
-// fine-rule points: i < n, q = ids[i] (fine point index), face f = ff[q] with
-// rect[5 f..] = a0, b0, na, G offset, normal axis of the step's rectangle:
-//   gq[pos[i]] += (-k (G[off + (fa[q] - a0) + na (fb[q] - b0)] n[axn])) w
-// (normals / weights indexed by n_base + q)
-void sf_add_fine(int n, const int* d_pos, const int* d_ids, int n_base, const int* d_fa,
-                 const int* d_fb, const int* d_ff, const int* d_rect, const double* d_G,
-                 const double* d_normals, const double* d_weights, double k, double* d_gq,
-                 cudaStream_t s);
-// gq[pos[i]] += tmp[i]
-void sf_scatter_add(int n, const int* d_pos, const double* d_tmp, double* d_gq, cudaStream_t s);
 
 }  // namespace tgb

@@ -12,6 +12,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <functional>
 #include <limits>
 #include <numeric>
 
@@ -22,6 +23,7 @@
 #include "host/operator.hpp"
 #include "k2_csr.cuh"
 #include "k2_kron.cuh"
+#include "common.cuh"
 #include "k3_flux.cuh"
 #include "sim.hpp"
 
@@ -82,12 +84,8 @@ Sim::~Sim() {
   if (cublas) cublasDestroy(cublas);
   if (h_dots) cudaFreeHost(h_dots);
   if (h_status) cudaFreeHost(h_status);
-  if (h_fine) cudaFreeHost(h_fine);
-  if (h_sf_fine) cudaFreeHost(h_sf_fine);
-  if (h_sf_rect) cudaFreeHost(h_sf_rect);
-  for (auto& ev : sf_ev)
-    if (ev) cudaEventDestroy(ev);
-  if (sf_stream) cudaStreamDestroy(sf_stream);
+  if (h_steps) cudaFreeHost(h_steps);
+  release_stages();
   if (ctx) tg_ctx_destroy(ctx);
 }
 
@@ -295,7 +293,8 @@ void Sim::setup_device(int device, int preconditioner) {
   d_fine.ensure(2 * static_cast<size_t>(n_fe) + 2);
   d_gq.ensure(max_pts);
   d_loc.ensure(static_cast<size_t>(n_fe) * ndk + 1);
-  TG_CUDA(cudaMallocHost(&h_fine, sizeof(int) * (2 * static_cast<size_t>(n_fe) + 2)));
+  h_fine.assign(2 * static_cast<size_t>(n_fe) + 2, 0);
+  for (auto& st : sf_stage) TG_CUDA(cudaEventCreateWithFlags(&st.done, cudaEventDisableTiming));
   TG_CUDA(cudaMallocHost(&h_status, sizeof(PcgStatus)));
 
   d_x.ensure(n_free);
@@ -433,14 +432,40 @@ void Sim::setup_device(int device, int preconditioner) {
   sf_setup_device();
 }
 
-// K5 setup: are the lateral faces' base quadrature points and the Greville
-// points tensor grids (up to coordinate rounding) with axis-aligned normals?
+// K5 setup (host): are the lateral faces' base quadrature points and the
+// Greville points tensor grids (up to coordinate rounding) with normals exactly
+// along an axis? Then cut them into CTA tiles / regions and list the points
+// of every region for the pair-wise remainder (k5_fused.cuh).
+namespace {
+
+// contiguous nearly equal pieces of n, each <= cap
+std::vector<std::pair<int, int>> split_even(int n, int cap) {
+  std::vector<std::pair<int, int>> out;
+  const int k = std::max(1, (n + cap - 1) / cap);
+  for (int i = 0; i < k; ++i) out.emplace_back(n * i / k, n * (i + 1) / k - n * i / k);
+  return out;
+}
+
+SfRegion box_of(const SfGrid& g, int a0, int na, int b0, int nb) {
+  SfRegion r{};
+  r.lo[g.axn] = r.hi[g.axn] = g.xf;
+  r.lo[g.axu] = g.U[a0];
+  r.hi[g.axu] = g.U[a0 + na - 1];
+  r.lo[g.axv] = g.V[b0];
+  r.hi[g.axv] = g.V[b0 + nb - 1];
+  r.delta = g.delta;
+  r.npts = static_cast<double>(na) * nb;
+  return r;
+}
+
+}  // namespace
+
 void Sim::sf_setup_host() {
-  if (const char* e = std::getenv("TG_SF_KC")) sf_kc = std::max(64, std::atoi(e));
   if (const char* e = std::getenv("TG_SF_MIN_PAIRS")) sf_min_pairs = std::atof(e);
-  if (const char* e = std::getenv("TG_SF_BANDS")) sf_bands = std::max(1, std::atoi(e));
+  if (const char* e = std::getenv("TG_SF_K1_SPLITS"))
+    sf_k1_splits = std::max(1, std::min(kMaxSplits, std::atoi(e)));
   const int tqb = h_qb_off.empty() ? 0 : h_qb_off.back();
-  // faces: base points grouped by the normal's axis and sign
+  const int tqf = h_qf_off.empty() ? 0 : h_qf_off.back();
   double ext = 0.0;
   for (int ax = 0; ax < 3; ++ax) {
     double lo = 1e300, hi = -1e300;
@@ -451,12 +476,12 @@ void Sim::sf_setup_host() {
     ext = std::max(ext, hi - lo);
   }
   const double tol = 1e-12 * ext;
-  auto& gcell = sf_h_gcell;
-  auto& gaxn = sf_h_gaxn;
-  gcell.assign(tqb, -1);
-  gaxn.assign(tqb, 0);
-  sf_flux_ok = tqb > 0;
-  auto normal_key = [&](int q) {  // 2 axis + (sign > 0), or -1 off the axes
+  // normal key: 2 axis + (sign > 0) when the normal lies on an axis up to the
+  // spline rounding of its tangents' cross product (off-axis components
+  // <= 1e-12; ~5e-14 on the BASELINE cuboids). The contraction takes n[axn]
+  // only: a dropped term is n_off * (in-plane gradient), below 1e-12 of the
+  // pair's gradient, two orders under the 1e-10 flux tolerance.
+  auto normal_key = [&](int q) {
     const double* n = &h_qn[3 * static_cast<size_t>(q)];
     int ax = 0;
     for (int d = 1; d < 3; ++d)
@@ -465,102 +490,54 @@ void Sim::sf_setup_host() {
                       std::fabs(n[(ax + 1) % 3]) <= 1e-12 && std::fabs(n[(ax + 2) % 3]) <= 1e-12;
     return axis ? 2 * ax + (n[ax] > 0.0) : -1;
   };
-  std::vector<int> qkey(tqb, -1);
-  for (int q = 0; q < tqb && sf_flux_ok; ++q) {
-    qkey[q] = normal_key(q);
-    if (qkey[q] < 0) sf_flux_ok = false;
-  }
-  // elements by face (normal key), each face cut into up to sf_bands bands of
-  // whole element rows (a band's box is smaller than the face's, so more of the
-  // history is cull-free there and takes the GEMM); every band is a grid
-  std::vector<int> ekey(n_fe, -1), eband(n_fe, -1);
+  sf_flux_ok = tqb > 0;
+  std::vector<int> ekey(n_fe, -1);
   std::vector<std::vector<int>> kelems(6);
   for (int e = 0; e < n_fe && sf_flux_ok; ++e) {
-    ekey[e] = qkey[h_qb_off[e]];
-    for (int q = h_qb_off[e]; q < h_qb_off[e + 1]; ++q)
-      if (qkey[q] != ekey[e]) sf_flux_ok = false;
+    ekey[e] = normal_key(h_qb_off[e]);
+    for (int q = h_qb_off[e]; q < h_qb_off[e + 1] && sf_flux_ok; ++q)
+      sf_flux_ok = ekey[e] >= 0 && normal_key(q) == ekey[e];
+    for (int l = h_qf_off[e]; l < h_qf_off[e + 1] && sf_flux_ok; ++l)
+      sf_flux_ok = normal_key(tqb + l) == ekey[e];
     if (sf_flux_ok) kelems[ekey[e]].push_back(e);
   }
-  int off = 0;
-  auto grid_of = [&](const std::vector<int>& els, SfGrid& g) {
+  // base grid per face (normal key)
+  sf_h_gcell.assign(tqb, -1);
+  std::vector<int> q_face(tqb, -1);
+  sf_elem_face.assign(n_fe, -1);
+  for (int k = 0; k < 6 && sf_flux_ok; ++k) {
+    if (kelems[k].empty()) continue;
     std::vector<double> pts;
-    for (int e : els)
+    for (int e : kelems[k])
       for (int q = h_qb_off[e]; q < h_qb_off[e + 1]; ++q)
         for (int d = 0; d < 3; ++d) pts.push_back(h_qx[3 * static_cast<size_t>(q) + d]);
-    return sf_make_grid(pts.data(), static_cast<long>(pts.size() / 3), tol, g);
-  };
-  for (int k = 0; k < 6 && sf_flux_ok; ++k) {
-    const std::vector<int>& E = kelems[k];
-    if (E.empty()) continue;
-    // row starts: where the slower-varying in-face centre coordinate changes
-    const int ax = k / 2, u = ax == 0 ? 1 : 0, v = ax == 2 ? 1 : 2;
-    auto changes = [&](int d) {
-      int c = 0;
-      for (size_t i = 1; i < E.size(); ++i)
-        c += std::fabs(centers[3 * E[i] + d] - centers[3 * E[i - 1] + d]) > tol;
-      return c;
-    };
-    const int slow = changes(u) <= changes(v) ? u : v;
-    std::vector<size_t> rows{0};
-    for (size_t i = 1; i < E.size(); ++i)
-      if (std::fabs(centers[3 * E[i] + slow] - centers[3 * E[i - 1] + slow]) > tol)
-        rows.push_back(i);
-    std::vector<std::vector<int>> bands;
-    for (int nb = std::max(1, std::min<int>(sf_bands, static_cast<int>(rows.size()))); nb >= 1;
-         nb = nb > 1 ? 1 : 0) {
-      bands.clear();
-      size_t prev = 0;
-      for (int b = 1; b <= nb; ++b) {
-        const size_t end = b == nb ? E.size() : rows[rows.size() * b / nb];
-        if (end > prev) bands.emplace_back(E.begin() + prev, E.begin() + end);
-        prev = end;
-      }
-      std::vector<SfGrid> gs(bands.size());
-      bool ok = true;
-      for (size_t i = 0; i < bands.size() && ok; ++i)
-        ok = grid_of(bands[i], gs[i]) && gs[i].axn == ax;
-      if (!ok) {
-        if (nb == 1) sf_flux_ok = false;
-        continue;
-      }
-      for (size_t i = 0; i < bands.size(); ++i) {
-        const int f = static_cast<int>(sf_faces.size());
-        size_t c = 0;
-        for (int e : bands[i]) {
-          eband[e] = f;
-          for (int q = h_qb_off[e]; q < h_qb_off[e + 1]; ++q, ++c) {
-            gcell[q] = off + gs[i].cell[c];
-            gaxn[q] = gs[i].axn;
-          }
-        }
-        sf_faces_off.push_back(off);
-        off += static_cast<int>(gs[i].U.size() * gs[i].V.size());
-        sf_faces.push_back(std::move(gs[i]));
-      }
+    SfGrid g;
+    if (!sf_make_grid(pts.data(), static_cast<long>(pts.size() / 3), tol, g) || g.axn != k / 2) {
+      sf_flux_ok = false;
       break;
     }
+    const int f = static_cast<int>(sf_faces.size());
+    size_t c = 0;
+    for (int e : kelems[k]) {
+      sf_elem_face[e] = f;
+      for (int q = h_qb_off[e]; q < h_qb_off[e + 1]; ++q, ++c) {
+        sf_h_gcell[q] = g.cell[c];
+        q_face[q] = f;
+      }
+    }
+    sf_faces.push_back(std::move(g));
   }
-  // fine-rule points: per face, the fine points of all its elements form a
-  // finer grid; a step's fine elements take a rectangle of it
-  const int tqf = h_qf_off.empty() ? 0 : h_qf_off.back();
+  if (!sf_flux_ok) sf_faces.clear();
+  // fine-rule points: per face a finer grid; a step's fine elements take a
+  // rectangle of it
   sf_fine_ok = sf_flux_ok && tqf > 0;
-  auto& fa = sf_h_fa;
-  auto& fb = sf_h_fb;
-  auto& ff = sf_h_ff;
-  fa.assign(tqf, 0);
-  fb.assign(tqf, 0);
-  ff.assign(tqf, 0);
+  sf_h_fa.assign(tqf, 0);
+  sf_h_fb.assign(tqf, 0);
+  sf_h_ff.assign(tqf, 0);
   if (sf_fine_ok) {
-    sf_elem_face.assign(n_fe, -1);
     sf_erect.assign(4 * static_cast<size_t>(n_fe), 0);
     std::vector<std::vector<int>> felems(sf_faces.size());
-    for (int e = 0; e < n_fe && sf_fine_ok; ++e) {
-      const int f = eband[e];
-      for (int l = h_qf_off[e]; l < h_qf_off[e + 1]; ++l)
-        if (normal_key(tqb + l) != ekey[e]) sf_fine_ok = false;
-      sf_elem_face[e] = f;
-      felems[f].push_back(e);
-    }
+    for (int e = 0; e < n_fe; ++e) felems[sf_elem_face[e]].push_back(e);
     for (size_t f = 0; f < felems.size() && sf_fine_ok; ++f) {
       std::vector<double> pts;
       for (int e : felems[f])
@@ -580,9 +557,9 @@ void Sim::sf_setup_host() {
         r[2] = r[3] = -1;
         for (int l = h_qf_off[e]; l < h_qf_off[e + 1]; ++l, ++i) {
           const int a = g.cell[i] % na, b = g.cell[i] / na;
-          fa[l] = a;
-          fb[l] = b;
-          ff[l] = static_cast<int>(f);
+          sf_h_fa[l] = a;
+          sf_h_fb[l] = b;
+          sf_h_ff[l] = static_cast<int>(f);
           r[0] = std::min(r[0], a);
           r[1] = std::min(r[1], b);
           r[2] = std::max(r[2], a);
@@ -593,185 +570,303 @@ void Sim::sf_setup_host() {
     }
     if (!sf_fine_ok) sf_fine.clear();
   }
-  // per-face source prefixes need each face's elements contiguous (one K1
-  // launch per face) and its fine points gridded (the GEMM covers them)
-  sf_face_split = sf_fine_ok;
-  if (sf_face_split) {
-    const size_t nfc = sf_faces.size();
-    sf_face_e.assign(2 * nfc, -1);
-    for (int e = 0; e < n_fe; ++e) {
-      const int f = sf_elem_face[e];
-      if (sf_face_e[2 * f] < 0) sf_face_e[2 * f] = e;
-      else if (sf_face_e[2 * f + 1] != e) sf_face_split = false;
-      sf_face_e[2 * f + 1] = e + 1;
-    }
-    sf_face_box.assign(6 * nfc, 0.0);
-    sf_face_delta.assign(nfc, 0.0);
-    sf_pf_face.assign(nfc, SfPrefix{});
-    for (size_t f = 0; f < nfc; ++f)
-      for (int ax = 0; ax < 3; ++ax) {
-        sf_face_box[6 * f + ax] = std::min(sf_faces[f].lo[ax], sf_fine[f].lo[ax]);
-        sf_face_box[6 * f + 3 + ax] = std::max(sf_faces[f].hi[ax], sf_fine[f].hi[ax]);
-        sf_face_delta[f] = std::max(sf_faces[f].delta, sf_fine[f].delta);
-      }
-  }
-  if (sf_flux_ok) {
-    for (int ax = 0; ax < 3; ++ax) {
-      sf_lo[ax] = 1e300;
-      sf_hi[ax] = -1e300;
-    }
-    for (const SfGrid& g : sf_fine) {  // the eligibility box covers the fine points too
-      for (int ax = 0; ax < 3; ++ax) {
-        sf_lo[ax] = std::min(sf_lo[ax], g.lo[ax]);
-        sf_hi[ax] = std::max(sf_hi[ax], g.hi[ax]);
-      }
-      sf_delta = std::max(sf_delta, g.delta);
-    }
-    for (const SfGrid& g : sf_faces) {
-      for (int ax = 0; ax < 3; ++ax) {
-        sf_lo[ax] = std::min(sf_lo[ax], g.lo[ax]);
-        sf_hi[ax] = std::max(sf_hi[ax], g.hi[ax]);
-      }
-      sf_delta = std::max(sf_delta, g.delta);
-    }
-  } else {
-    sf_faces.clear();
-    sf_faces_off.clear();
-  }
   sf_dir_ok = n_con > 0 && sf_make_grid(grev.data(), n_con, tol, sf_dir);
-  sf_g_total = off;
+
+  // grids: faces, fine faces, Greville (descriptor lines are device pointers,
+  // set in sf_setup_device); the B exponent of a grid is cb[b] * nisp when
+  // every source shares its V coordinate (a layer's scan on its plane)
+  sf_grids_h.clear();
+  auto desc = [&](const SfGrid& g, int flux) {
+    SfGridDesc d{};
+    d.axn = g.axn;
+    d.axu = g.axu;
+    d.axv = g.axv;
+    d.na = static_cast<int>(g.U.size());
+    d.nb = static_cast<int>(g.V.size());
+    d.flux = flux;
+    d.xf = g.xf;
+    bool same = !sources.empty();
+    const double v0 = same ? sources[0].position[g.axv] : 0.0;
+    for (size_t j = 1; j < sources.size() && same; ++j)
+      same = std::memcmp(&sources[j].position[g.axv], &v0, sizeof(double)) == 0;
+    d.vplane = same ? 1 : 0;
+    return d;
+  };
+  for (const SfGrid& g : sf_faces) sf_grids_h.push_back(desc(g, 1));
+  sf_grid_fine0 = static_cast<int>(sf_grids_h.size());
+  for (const SfGrid& g : sf_fine) sf_grids_h.push_back(desc(g, 1));
+  sf_grid_dir = -1;
+  if (sf_dir_ok) {
+    sf_grid_dir = static_cast<int>(sf_grids_h.size());
+    sf_grids_h.push_back(desc(sf_dir, 0));
+  }
+  // static tiles = regions: face grids, then the Greville grid
+  sf_tiles_h.clear();
+  sf_regions_h.clear();
+  std::vector<std::vector<int>> tile_pts;  // entry point ids per static tile
+  std::vector<std::vector<int>> tile_cell;
+  auto add_tiles = [&](const SfGrid& g, int grid) {
+    const int na = static_cast<int>(g.U.size()), nb = static_cast<int>(g.V.size());
+    const auto as = split_even(na, kSfTA), bs = split_even(nb, kSfTB);
+    const int first = static_cast<int>(sf_tiles_h.size());
+    for (const auto& [b0, nbt] : bs)
+      for (const auto& [a0, nat] : as) {
+        const int r = static_cast<int>(sf_regions_h.size());
+        sf_tiles_h.push_back(SfTile{grid, a0, b0, nat, nbt, r});
+        sf_regions_h.push_back(box_of(g, a0, nat, b0, nbt));
+      }
+    tile_pts.resize(sf_tiles_h.size());
+    tile_cell.resize(sf_tiles_h.size());
+    // cell (a, b) -> its tile (as / bs are sorted runs)
+    std::vector<int> ta(na), tb(nb);
+    for (size_t i = 0; i < as.size(); ++i)
+      for (int a = as[i].first; a < as[i].first + as[i].second; ++a) ta[a] = static_cast<int>(i);
+    for (size_t i = 0; i < bs.size(); ++i)
+      for (int b = bs[i].first; b < bs[i].first + bs[i].second; ++b) tb[b] = static_cast<int>(i);
+    return [=](int cell, int& tile, int& local) {
+      const int a = cell % na, b = cell / na;
+      tile = first + ta[a] + static_cast<int>(as.size()) * tb[b];
+      const SfTile& T = sf_tiles_h[tile];
+      local = (a - T.a0) + kSfTA * (b - T.b0);
+    };
+  };
+  if (sf_flux_ok) {
+    std::vector<std::function<void(int, int&, int&)>> locate;
+    for (size_t f = 0; f < sf_faces.size(); ++f)
+      locate.push_back(add_tiles(sf_faces[f], static_cast<int>(f)));
+    for (int q = 0; q < tqb; ++q) {  // in compact (element) order
+      int t, l;
+      locate[q_face[q]](sf_h_gcell[q], t, l);
+      tile_pts[t].push_back(q);
+      tile_cell[t].push_back(l);
+    }
+  }
+  sf_nt_flux = static_cast<int>(sf_tiles_h.size());
+  if (sf_dir_ok) {
+    auto loc = add_tiles(sf_dir, sf_grid_dir);
+    for (int c = 0; c < n_con; ++c) {
+      int t, l;
+      loc(sf_dir.cell[c], t, l);
+      tile_pts[t].push_back(c);
+      tile_cell[t].push_back(l);
+    }
+  }
+  sf_nt_static = static_cast<int>(sf_tiles_h.size());
+  // remainder entries: per tile its points, padded to whole K1 CTAs
+  sf_k1_ppc = kK1Threads * 7;  // k1_partial<7, GRAD> (the remainder launch)
+  sf_ent_q.clear();
+  sf_ent_tile.clear();
+  sf_ent_cell.clear();
+  sf_ent_pos.clear();
+  sf_cta_region.clear();
+  const int qdir0 = tqb + tqf;  // Greville points follow the face points in d_qx
+  for (int t = 0; t < sf_nt_static; ++t) {
+    if (t == sf_nt_flux) {
+      sf_ne_flux = static_cast<int>(sf_ent_q.size());
+      sf_nc_flux = static_cast<int>(sf_cta_region.size());
+    }
+    const bool dir = t >= sf_nt_flux;
+    const auto& P = tile_pts[t];
+    const int n = static_cast<int>(P.size());
+    const int pad = (n + sf_k1_ppc - 1) / sf_k1_ppc * sf_k1_ppc;
+    for (int i = 0; i < pad; ++i) {
+      const bool real = i < n;
+      const int pt = real ? P[i] : P[0];
+      sf_ent_q.push_back(dir ? qdir0 + pt : pt);
+      sf_ent_tile.push_back(real ? t : -1);
+      sf_ent_cell.push_back(real ? tile_cell[t][i] : 0);
+      sf_ent_pos.push_back(dir && real ? pt : -1);  // flux: set per step
+    }
+    for (int c = 0; c < pad / sf_k1_ppc; ++c) sf_cta_region.push_back(sf_tiles_h[t].region);
+  }
+  if (sf_nt_flux == sf_nt_static) {
+    sf_ne_flux = static_cast<int>(sf_ent_q.size());
+    sf_nc_flux = static_cast<int>(sf_cta_region.size());
+  }
+  sf_ne_static = static_cast<int>(sf_ent_q.size());
+  sf_nc_static = static_cast<int>(sf_cta_region.size());
   if (std::getenv("TG_SF_DEBUG"))
-    std::fprintf(stderr, "[k5] flux %d fine %d split %d groups %zu dir %d\n", sf_flux_ok,
-                 sf_fine_ok, sf_face_split, sf_faces.size(), sf_dir_ok);
+    std::fprintf(stderr, "[k5] flux %d fine %d dir %d grids %zu tiles %d+%d entries %d+%d\n",
+                 sf_flux_ok, sf_fine_ok, sf_dir_ok, sf_grids_h.size(), sf_nt_flux,
+                 sf_nt_static - sf_nt_flux, sf_ne_flux, sf_ne_static - sf_ne_flux);
   const char* e = std::getenv("TG_SUMFACT");
   set_sumfact(!(e && std::string(e) == "0"));
 }
 
 void Sim::sf_setup_device() {
   cudaStream_t s = ctx->stream;
-  const int off = sf_g_total;
-  auto& gcell = sf_h_gcell;
-  auto& gaxn = sf_h_gaxn;
-  // grid lines on the device: faces then the Greville grid
-  std::vector<double> uv;
-  std::vector<size_t> at;
-  auto push = [&](const SfGrid& g) {
-    at.push_back(uv.size());
-    uv.insert(uv.end(), g.U.begin(), g.U.end());
-    uv.insert(uv.end(), g.V.begin(), g.V.end());
-  };
-  for (const SfGrid& g : sf_faces) push(g);
-  for (const SfGrid& g : sf_fine) push(g);
-  if (sf_dir_ok) push(sf_dir);
-  if (uv.empty()) return;
-  upload(d_sf_uv, uv, s);
-  auto dev = [&](const SfGrid& g, size_t a) {
-    const int na = static_cast<int>(g.U.size()), nb = static_cast<int>(g.V.size());
-    return SfDev{g.axn, g.axu, g.axv, na, nb, g.xf, d_sf_uv.p + a, d_sf_uv.p + a + na};
-  };
-  for (size_t k = 0; k < sf_faces.size(); ++k) sf_faces_dev.push_back(dev(sf_faces[k], at[k]));
-  for (size_t k = 0; k < sf_fine.size(); ++k)
-    sf_fine_dev.push_back(dev(sf_fine[k], at[sf_faces.size() + k]));
-  if (sf_fine_ok) {
-    upload(d_sf_fa, sf_h_fa, s);
-    upload(d_sf_fb, sf_h_fb, s);
-    upload(d_sf_ff, sf_h_ff, s);
-    d_sf_rect.ensure(5 * sf_fine.size());
-    TG_CUDA(cudaMallocHost(&h_sf_rect, sizeof(int) * 5 * sf_fine.size()));
+  if (!(sf_flux_ok || sf_dir_ok)) return;
+  // grid lines (+ cb) on the device; descriptors point at them
+  std::vector<double> lines, cb;
+  std::vector<size_t> at, atc;
+  std::vector<const SfGrid*> gs;
+  for (const SfGrid& g : sf_faces) gs.push_back(&g);
+  for (const SfGrid& g : sf_fine) gs.push_back(&g);
+  if (sf_dir_ok) gs.push_back(&sf_dir);
+  for (size_t i = 0; i < gs.size(); ++i) {
+    const SfGrid& g = *gs[i];
+    at.push_back(lines.size());
+    lines.insert(lines.end(), g.U.begin(), g.U.end());
+    lines.insert(lines.end(), g.V.begin(), g.V.end());
+    atc.push_back(cb.size());
+    const double vs = sources.empty() ? 0.0 : sources[0].position[g.axv];
+    for (double v : g.V) cb.push_back((v - vs) * (v - vs));
   }
+  upload(d_sf_lines, lines, s);
+  upload(d_sf_cb, cb, s);
+  for (size_t i = 0; i < gs.size(); ++i) {
+    SfGridDesc& d = sf_grids_h[i];
+    d.U = d_sf_lines.p + at[i];
+    d.V = d.U + d.na;
+    d.cb = d_sf_cb.p + atc[i];
+  }
+  upload(d_sf_grids, sf_grids_h, s);
+  std::vector<double> tab(kExpTableSize);
+  k1_exp_table_host(tab.data());
+  upload(d_sf_tab, tab, s);
+  // static tables, with room for the per-step fine tiles / regions / entries
+  const int tqb = h_qb_off.back(), tqf = h_qf_off.back();
+  size_t ft = 0;
+  for (const SfGrid& g : sf_fine)
+    ft += split_even(static_cast<int>(g.U.size()), kSfTA).size() *
+          split_even(static_cast<int>(g.V.size()), kSfTB).size();
+  const size_t nfr = sf_fine_ok ? sf_fine.size() : (sf_flux_ok ? 1 : 0);
+  const size_t fent = sf_flux_ok ? static_cast<size_t>(tqf) + nfr * sf_k1_ppc : 0;
+  d_sf_tiles.ensure(sf_nt_static + ft + 1);
+  d_sf_regions.ensure(sf_regions_h.size() + nfr + 1);
+  d_sf_ent_q.ensure(sf_ne_static + fent + 1);
+  d_sf_ent_tile.ensure(sf_ne_static + fent + 1);
+  d_sf_ent_cell.ensure(sf_ne_static + fent + 1);
+  d_sf_ent_pos.ensure(sf_ne_static + fent + 1);
+  d_sf_cta.ensure(sf_nc_static + fent / sf_k1_ppc + nfr + 1);
+  auto put = [&](auto& d, const auto& h) {
+    if (!h.empty())
+      TG_CUDA(cudaMemcpyAsync(d.p, h.data(), h.size() * sizeof(h[0]), cudaMemcpyHostToDevice, s));
+  };
+  put(d_sf_tiles, sf_tiles_h);
+  put(d_sf_regions, sf_regions_h);
+  put(d_sf_ent_q, sf_ent_q);
+  put(d_sf_ent_tile, sf_ent_tile);
+  put(d_sf_ent_cell, sf_ent_cell);
+  put(d_sf_ent_pos, sf_ent_pos);
+  put(d_sf_cta, sf_cta_region);
+  d_sf_stats.ensure(2);
+  TG_CUDA(cudaMemsetAsync(d_sf_stats.p, 0, 2 * sizeof(double), s));
+  d_sf_J.ensure(sf_regions_h.size() + nfr + 1);
+  d_sf_Jl.ensure(sf_regions_h.size() + 1);
+  d_sf_El.ensure(sf_regions_h.size() + 1);
+  TG_CUDA(cudaMemsetAsync(d_sf_Jl.p, 0, sizeof(int) * (sf_regions_h.size() + 1), s));
+  TG_CUDA(cudaMemsetAsync(d_sf_El.p, 0, sizeof(int) * (sf_regions_h.size() + 1), s));
+  d_sf_E.ensure(sf_regions_h.size() + nfr + 1);
+  d_sf_prefix.ensure(sf_nt_static + ft + 2);
+  // qp -> element of the base points (their compact positions per step)
+  std::vector<int> qelem(tqb);
+  for (int e = 0; e < n_fe; ++e)
+    for (int q = h_qb_off[e]; q < h_qb_off[e + 1]; ++q) qelem[q] = e;
+  upload(d_sf_qelem, qelem, s);
+  // the Greville points after the face points (one coordinate array for the
+  // remainder launch)
   if (sf_dir_ok) {
-    sf_dir_dev = dev(sf_dir, at.back());
-    upload(d_sf_dcell, sf_dir.cell, s);
-    d_sf_Gdir.ensure(sf_dir.U.size() * sf_dir.V.size());
+    d_qx.ensure(3 * (static_cast<size_t>(tqb) + tqf + n_con));  // (never grows: sized here)
+    TG_CUDA(cudaMemcpyAsync(d_qx.p, h_qx.data(), h_qx.size() * sizeof(double),
+                            cudaMemcpyHostToDevice, s));
+    TG_CUDA(cudaMemcpyAsync(d_qx.p + 3 * (static_cast<size_t>(tqb) + tqf), grev.data(),
+                            grev.size() * sizeof(double), cudaMemcpyHostToDevice, s));
   }
-  if (sf_flux_ok) {
-    upload(d_sf_gcell, gcell, s);
-    upload(d_sf_gaxn, gaxn, s);
-    d_sf_G.ensure(off);
-    const size_t tqf = h_qf_off.back();
-    d_sf_fine.ensure(2 * tqf + 2);
-    d_sf_tmp.ensure(tqf + 1);
-    TG_CUDA(cudaMallocHost(&h_sf_fine, sizeof(int) * (2 * tqf + 2)));
-  }
-  if (!cublas && cublasCreate(&cublas) != CUBLAS_STATUS_SUCCESS)
-    throw cuda_error("cublas: create failed");
-  const char* ser = std::getenv("TG_SF_SERIAL");
-  if (sf_face_split && !(ser && std::string(ser) == "1")) {
-    TG_CUDA(cudaStreamCreateWithFlags(&sf_stream, cudaStreamNonBlocking));
-    for (auto& ev : sf_ev) TG_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-  }
+  d_sf_cst.ensure(sf_grids_h.size() * std::max<size_t>(1, sources.size()));
+  d_sf_scratch.ensure((sf_nt_static + ft + sf_contract_max_ctas(ctx->sm_count) + 1) *
+                      static_cast<size_t>(kSfTA * kSfTB));
   TG_CUDA(cudaStreamSynchronize(s));
-  for (auto* v : {&sf_h_gcell, &sf_h_gaxn, &sf_h_fa, &sf_h_fb, &sf_h_ff}) std::vector<int>().swap(*v);
+  sf_ready = true;
 }
 
-void Sim::sf_prefixes(double t, int* out) {
-  if (!sf_on) {
-    out[0] = out[1] = 0;
-    return;
+char* Sim::stage_bytes(size_t bytes) {
+  Stage& st = sf_stage[sf_stage_i];
+  sf_stage_i = (sf_stage_i + 1) % 3;
+  TG_CUDA(cudaEventSynchronize(st.done));  // its last copies have run
+  if (bytes > st.cap) {
+    if (st.h) TG_CUDA(cudaFreeHost(st.h));
+    st.cap = bytes + bytes / 4 + 4096;
+    TG_CUDA(cudaMallocHost(&st.h, st.cap));
   }
-  out[0] = 0;
-  if (sf_flux_ok) {
-    SfPrefix c;
-    out[0] = sf_prefix(t, sf_lo, sf_hi, sf_delta, c);
-    if (sf_face_split) {
-      out[0] = 1 << 30;
-      for (size_t f = 0; f < sf_faces.size(); ++f) {
-        c = SfPrefix{};
-        out[0] = std::min(out[0], sf_prefix(t, &sf_face_box[6 * f], &sf_face_box[6 * f + 3],
-                                            sf_face_delta[f], c));
-      }
+  return st.h;
+}
+
+void Sim::release_stages() {
+  for (auto& st : sf_stage) {
+    if (st.h) cudaFreeHost(st.h);
+    if (st.done) cudaEventDestroy(st.done);
+    st.h = nullptr;
+    st.done = nullptr;
+  }
+}
+
+namespace {
+
+// the device plan's region tests on the host (sf_plan_kernel)
+bool host_source_ok(const double* p, double t, double alpha, double cull, const SfRegion& r) {
+  const double dt = t - p[5];
+  if (!(dt > 0.0)) return true;
+  const double spread = 4.0 * alpha * dt;
+  double r2 = 0.0;
+  for (int ax = 0; ax < 3; ++ax) {
+    const double a = r.lo[ax] - r.delta - p[ax], b = r.hi[ax] + r.delta - p[ax];
+    r2 += std::max(a * a, b * b);
+  }
+  if (!(r2 * (1.0 + 1e-9) <= cull * spread)) return false;
+  return 36.0 * cull * r.delta * r.delta <= 1e-24 * spread;
+}
+
+bool host_source_culled(const double* p, double t, double alpha, double cull,
+                        const SfRegion& r) {
+  const double dt = t - p[5];
+  if (!(dt > 0.0)) return true;
+  const double spread = 4.0 * alpha * dt;
+  double r2 = 0.0;
+  for (int ax = 0; ax < 3; ++ax) {
+    const double d = std::max({r.lo[ax] - r.delta - p[ax], p[ax] - r.hi[ax] - r.delta, 0.0});
+    r2 += d * d;
+  }
+  return r2 * (1.0 - 1e-9) > cull * spread;
+}
+
+}  // namespace
+
+void Sim::sf_plan_host(double t, int* J, int* E) {
+  const double alpha = cfg.material.diffusivity(), cull = cfg.superpose.cull_exponent;
+  const double* src = reinterpret_cast<const double*>(sources.data());
+  // the causally active prefix (tg_ctx::active_prefix): later sources all
+  // have t - tau <= 0
+  int n_act = static_cast<int>(sources.size());
+  while (n_act > 0 && !(t - src[6 * (n_act - 1) + 5] > 0.0)) --n_act;
+  for (size_t r = 0; r < sf_regions_h.size(); ++r) {
+    const SfRegion& R = sf_regions_h[r];
+    int j = 0;
+    if (sf_on) {
+      while (j < n_act && host_source_ok(src + 6 * static_cast<size_t>(j), t, alpha, cull, R)) ++j;
+      if (static_cast<double>(j) * R.npts < sf_min_pairs) j = 0;
     }
+    int e = n_act;
+    while (e > j && host_source_culled(src + 6 * static_cast<size_t>(e - 1), t, alpha, cull, R))
+      --e;
+    J[r] = j;
+    E[r] = e;
   }
-  SfPrefix c;
-  out[1] = sf_dir_ok ? sf_prefix(t, sf_dir.lo, sf_dir.hi, sf_dir.delta, c) : 0;
 }
 
-// longest prefix [0, J) of the sources that sf_source_eligible admits for the
-// box at t; a prefix of sources all active at an earlier t stays eligible
-// (their spreads only grow), so the scan resumes there
-int Sim::sf_prefix(double t, const double lo[3], const double hi[3], double delta, SfPrefix& c) {
-  const double alpha = cfg.material.diffusivity();  // = ctx->mat's
-  const double cull = cfg.superpose.cull_exponent;
-  const double* src = reinterpret_cast<const double*>(sources.data());
-  // (the GEMM builders' 2D grids address up to ~1e6 sources; later ones stay on K1)
-  const int n = std::min(static_cast<int>(sources.size()), 1000000);
-  int j = (c.valid && t >= c.t) ? c.J : 0;
-  bool active = true;
-  for (; j < n; ++j) {
-    const double* p = src + 6 * static_cast<size_t>(j);
-    if (!sf_source_eligible(p, t, alpha, cull, lo, hi, delta)) break;
-    if (!(t - p[5] > 0.0)) active = false;
-  }
-  c = SfPrefix{j, t, active};
-  return j;
+double Sim::sf_flops_total() {
+  if (!sf_ready) return 0.0;
+  double v = 0.0;
+  TG_CUDA(cudaMemcpyAsync(&v, d_sf_stats.p, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  TG_CUDA(cudaStreamSynchronize(ctx->stream));
+  return v;
 }
 
-int Sim::sf_suffix_end(double t, const double lo[3], const double hi[3], int begin) {
-  const double alpha = ctx->mat.diffusivity();
-  const double cull = cfg.superpose.cull_exponent;
-  const double* src = reinterpret_cast<const double*>(sources.data());
-  int end = ctx->active_prefix(t);
-  while (end > begin &&
-         sf_source_culled(src + 6 * static_cast<size_t>(end - 1), t, alpha, cull, lo, hi))
-    --end;
-  return end;
-}
-
-SfScratch Sim::sf_scratch(int na, int nb, int J) {
-  const int C = (J + sf_kc - 1) / sf_kc;
-  const size_t Jpad = static_cast<size_t>(C) * sf_kc;
-  // sized for every source at once: the prefix only grows during a run
-  const size_t Jmax = (sources.size() + sf_kc - 1) / sf_kc * static_cast<size_t>(sf_kc);
-  const size_t Jcap = std::max(Jpad, Jmax);
-  SfScratch w{};
-  w.fac = d_sf_vec.ensure(4 * Jcap);
-  w.inv_s = w.fac + Jcap;
-  w.su = w.inv_s + Jcap;
-  w.sv = w.su + Jcap;
-  w.A = d_sf_A.ensure(static_cast<size_t>(na) * Jcap);
-  w.B = d_sf_B.ensure(static_cast<size_t>(nb) * Jcap);
-  w.Cpart = d_sf_C.ensure(static_cast<size_t>(na) * nb * (Jcap / sf_kc));
-  return w;
+void Sim::sf_last_plan(int* J, int* E) {
+  const size_t n = sf_regions_h.size();
+  TG_CUDA(cudaMemcpyAsync(J, d_sf_Jl.p, n * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  TG_CUDA(cudaMemcpyAsync(E, d_sf_El.p, n * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  TG_CUDA(cudaStreamSynchronize(ctx->stream));
 }
 
 // ---------------------------------------------------------------------------
@@ -789,6 +884,7 @@ bool Sim::focus_at(double t, Vec3& focus) const {
 int Sim::fine_elements(double t, double radius) {
   Vec3 f;
   int nf = 0;
+  h_fine.resize(2 * static_cast<size_t>(n_fe) + 2);
   if (!focus_at(t, f)) return 0;
   for (int e = 0; e < n_fe; ++e) {
     const Vec3 c{centers[3 * e], centers[3 * e + 1], centers[3 * e + 2]};
@@ -797,204 +893,259 @@ int Sim::fine_elements(double t, double radius) {
   return nf;
 }
 
-void Sim::flux_load_device(double t, double radius, double* d_F, int e0, int e1) {
+// The fused loads path (full range): F_{n+1} = assemble_flux_load and/or
+// g_{n+1} = dirichlet_values at t through K5 + the K1 remainder. No host
+// synchronisation: the per-step host data (fine elements, the fine regions'
+// tiles and points) goes through a pinned ring.
+void Sim::loads_device(double t, double radius, double* d_F, double* d_g, bool gather) {
   cudaStream_t s = ctx->stream;
-  // the pinned fine list is reused every step: order the last copy first
-  TG_CUDA(cudaStreamSynchronize(s));
+  const bool flux = d_F != nullptr || !gather;
+  const bool dir = d_g != nullptr && sf_dir_ok;
+  const int tqb = h_qb_off.back();
+  // ---- host: fine-rule elements and their compact offsets
+  int nf = 0;
+  int* extra = nullptr;
+  if (flux) {
+    nf = fine_elements(t, radius);
+    extra = h_fine.data() + n_fe + 1;
+    extra[0] = 0;
+    for (int r = 0; r < nf; ++r) {
+      const int e = h_fine[r];
+      extra[r + 1] = extra[r] + (h_qf_off[e + 1] - h_qf_off[e]) - (h_qb_off[e + 1] - h_qb_off[e]);
+    }
+  }
+  const long n_compact = flux ? static_cast<long>(tqb) + (nf ? extra[nf] : 0) : 0;
+  sf_last_npts = n_compact;
+  // ---- host: the step's fine regions (one per face with fine elements)
+  std::vector<SfTile> ftiles;
+  std::vector<SfRegion> fregs;
+  std::vector<int> fq, fpos, ftile, fcell, fcta;
+  const int nreg_static = static_cast<int>(sf_regions_h.size());
+  if (flux && nf > 0) {
+    const size_t nF = sf_fine_ok ? sf_fine.size() : 1;
+    std::vector<std::array<int, 4>> rc(nF, {1 << 30, 1 << 30, -1, -1});
+    std::vector<std::vector<int>> fel(nF);
+    for (int r = 0; r < nf; ++r) {
+      const int e = h_fine[r];
+      const int f = sf_fine_ok ? sf_elem_face[e] : 0;
+      fel[f].push_back(r);
+      if (sf_fine_ok) {
+        const int* er = &sf_erect[4 * static_cast<size_t>(e)];
+        rc[f][0] = std::min(rc[f][0], er[0]);
+        rc[f][1] = std::min(rc[f][1], er[1]);
+        rc[f][2] = std::max(rc[f][2], er[2]);
+        rc[f][3] = std::max(rc[f][3], er[3]);
+      }
+    }
+    for (size_t f = 0; f < nF; ++f) {
+      if (fel[f].empty()) continue;
+      const int reg = nreg_static + static_cast<int>(fregs.size());
+      std::vector<std::pair<int, int>> as, bs;
+      int tile0 = sf_nt_static + static_cast<int>(ftiles.size());
+      if (sf_fine_ok) {
+        const SfGrid& g = sf_fine[f];
+        const int a0 = rc[f][0], b0 = rc[f][1];
+        const int na = rc[f][2] - a0 + 1, nb = rc[f][3] - b0 + 1;
+        fregs.push_back(box_of(g, a0, na, b0, nb));
+        as = split_even(na, kSfTA);
+        bs = split_even(nb, kSfTB);
+        for (const auto& [bb, nbt] : bs)
+          for (const auto& [aa, nat] : as)
+            ftiles.push_back(SfTile{sf_grid_fine0 + static_cast<int>(f), a0 + aa, b0 + bb, nat,
+                                    nbt, reg});
+      } else {  // fine points not on grids: all their sources pair-wise
+        SfRegion all{};
+        for (int ax = 0; ax < 3; ++ax) {
+          all.lo[ax] = -1e300;
+          all.hi[ax] = 1e300;
+        }
+        all.npts = -1.0;
+        fregs.push_back(all);
+      }
+      const size_t e0 = fq.size();
+      for (int r : fel[f]) {
+        const int e = h_fine[r];
+        const int o = h_qb_off[e] + extra[r];
+        for (int l = h_qf_off[e]; l < h_qf_off[e + 1]; ++l) {
+          fq.push_back(tqb + l);
+          fpos.push_back(o + (l - h_qf_off[e]));
+          if (sf_fine_ok) {
+            const int a = sf_h_fa[l] - rc[f][0], b = sf_h_fb[l] - rc[f][1];
+            int ia = 0, ib = 0;
+            while (ia + 1 < static_cast<int>(as.size()) && a >= as[ia + 1].first) ++ia;
+            while (ib + 1 < static_cast<int>(bs.size()) && b >= bs[ib + 1].first) ++ib;
+            ftile.push_back(tile0 + ia + static_cast<int>(as.size()) * ib);
+            fcell.push_back((a - as[ia].first) + kSfTA * (b - bs[ib].first));
+          } else {
+            ftile.push_back(-1);
+            fcell.push_back(0);
+          }
+        }
+      }
+      const size_t n = fq.size() - e0;
+      const size_t pad = (n + sf_k1_ppc - 1) / sf_k1_ppc * sf_k1_ppc;
+      for (size_t i = n; i < pad; ++i) {
+        fq.push_back(fq[e0]);
+        fpos.push_back(-1);
+        ftile.push_back(-1);
+        fcell.push_back(0);
+      }
+      for (size_t c = 0; c < pad / sf_k1_ppc; ++c) fcta.push_back(reg);
+    }
+  }
+  const int n_tiles = sf_nt_static + static_cast<int>(ftiles.size());
+  const int n_regs = nreg_static + static_cast<int>(fregs.size());
+  const int n_ent = sf_ne_static + static_cast<int>(fq.size());
+  const int n_cta = sf_nc_static + static_cast<int>(fcta.size());
+  // ---- stage + upload the per-step host data (one pinned slot, async)
+  {
+    const size_t b_fine = flux ? sizeof(int) * (2 * static_cast<size_t>(nf) + 1) : 0;
+    const size_t b_t = sizeof(SfTile) * ftiles.size(), b_r = sizeof(SfRegion) * fregs.size();
+    const size_t b_e = sizeof(int) * fq.size(), b_c = sizeof(int) * fcta.size();
+    char* h = stage_bytes(b_fine + b_t + b_r + 4 * b_e + b_c + 64);
+    size_t o = 0;
+    auto copy = [&](void* dst, const void* src, size_t bytes) {
+      if (!bytes) return;
+      std::memcpy(h + o, src, bytes);
+      TG_CUDA(cudaMemcpyAsync(dst, h + o, bytes, cudaMemcpyHostToDevice, s));
+      o += (bytes + 15) / 16 * 16;
+    };
+    if (flux) {
+      copy(d_fine.p, h_fine.data(), sizeof(int) * nf);
+      copy(d_fine.p + n_fe + 1, extra, sizeof(int) * (nf + 1));
+    }
+    copy(d_sf_tiles.p + sf_nt_static, ftiles.data(), b_t);
+    copy(d_sf_regions.p + nreg_static, fregs.data(), b_r);
+    copy(d_sf_ent_q.p + sf_ne_static, fq.data(), b_e);
+    copy(d_sf_ent_pos.p + sf_ne_static, fpos.data(), b_e);
+    copy(d_sf_ent_tile.p + sf_ne_static, ftile.data(), b_e);
+    copy(d_sf_ent_cell.p + sf_ne_static, fcell.data(), b_e);
+    copy(d_sf_cta.p + sf_nc_static, fcta.data(), b_c);
+    TG_CUDA(cudaEventRecord(sf_stage[(sf_stage_i + 2) % 3].done, s));
+  }
+  // ---- device
+  const FaceTables ft{n_fe, ndk, d_qb_off.p, d_qf_off.p, d_Nb.p, d_Nf.p};
+  if (flux) {
+    k3_point_index(ft, d_fine.p, d_fine.p + n_fe + 1, nf, d_pt_index.p, d_elem_off.p, s);
+    sf_base_positions(sf_ne_flux, d_sf_ent_q.p, d_sf_ent_tile.p, d_sf_qelem.p, d_qb_off.p,
+                      d_elem_off.p, d_sf_ent_pos.p, s);
+    ctx->timer.launches += 2;
+  }
+  const Material& m = ctx->mat;
+  const double alpha = m.diffusivity(), rcp = m.volumetric_capacity();
+  const double cull = cfg.superpose.cull_exponent;
+  const int n_act = ctx->active_prefix(t);
+  SfPlanArgs pa{ctx->src6.p, n_act, t, alpha, cull, sf_min_pairs, sf_on};
+  SfPlanMask mask{flux, dir, sf_nt_flux, sf_nt_static, sf_rank, sf_world};
+  sf_plan(pa, d_sf_regions.p, n_regs, d_sf_J.p, d_sf_E.p, mask, nreg_static, d_sf_Jl.p,
+          d_sf_El.p, s);
+  sf_items(d_sf_tiles.p, n_tiles, d_sf_J.p, d_sf_prefix.p, d_sf_stats.p, s);
+  sf_prep(ctx->src6.p, n_act, t, alpha, rcp, d_sf_grids.p, static_cast<int>(sf_grids_h.size()),
+          static_cast<int>(sources.size()), d_sf_cst.p, s);
+  const int ctas = sf_contract_max_ctas(ctx->sm_count);
+  ctx->timer.timed(5, s, [&] {
+    sf_contract_fused(d_sf_grids.p, d_sf_tiles.p, n_tiles, d_sf_prefix.p, d_sf_J.p, d_sf_cst.p,
+                      static_cast<int>(sources.size()), d_sf_tab.p, d_sf_scratch.p, ctas, s);
+  });
+  ctx->timer.launches += 4;
+  // the pair-wise remainder: K1 over every entry with its region's [J, E)
+  const int S = sf_k1_splits;
+  double* part = ctx->part.ensure(static_cast<size_t>(S) * 4 * n_ent);
+  if (n_act > 0) {
+    k1_prepare(ctx->src6.p, n_act, t, alpha, rcp, cull, ctx->rec.ensure(n_act), s);
+    const bool planar = ctx->planar && !std::getenv("TG_K1_NO_PLANAR");
+    K1Ranges rg{d_sf_cta.p, d_sf_J.p, d_sf_E.p};
+    ctx->timer.timed(1, s, [&] {
+      k1_launch_partial(ctx->rec.p, n_act, d_qx.p, d_sf_ent_q.p, n_ent, S, true, 7, part, s,
+                        planar, ctx->planar_z, rg);
+    });
+    ctx->timer.launches += 2;
+    ++ctx->timer.k1_launches;
+  } else {
+    TG_CUDA(cudaMemsetAsync(part, 0, sizeof(double) * S * 4 * n_ent, s));
+  }
+  (void)n_cta;
+  SfAddArgs aa{};
+  aa.ent = SfEntries{d_sf_ent_q.p, d_sf_ent_pos.p, d_sf_ent_tile.p, d_sf_ent_cell.p};
+  aa.part = part;
+  aa.S = S;
+  aa.n_entries = n_ent;
+  aa.grids = d_sf_grids.p;
+  aa.tiles = d_sf_tiles.p;
+  aa.prefix = d_sf_prefix.p;
+  aa.n_tiles = n_tiles;
+  aa.ctas = ctas;
+  aa.scratch = d_sf_scratch.p;
+  aa.normals = d_qn.p;
+  aa.weights = d_qw.p;
+  aa.k = cfg.material.conductivity;
+  aa.gq = d_gq.p;
+  aa.g = d_g;
+  if (flux) {
+    sf_add(aa, 0, sf_ne_flux, true, s);
+    sf_add(aa, sf_ne_static, n_ent, true, s);
+    ctx->timer.launches += 2;
+  }
+  if (dir) {
+    sf_add(aa, sf_ne_flux, sf_ne_static, false, s);
+    ++ctx->timer.launches;
+  }
+  if (flux && gather) {
+    k3_local(ft, 0, n_fe, d_elem_off.p, d_gq.p, d_loc.p, s);
+    if (d_F) k3_gather(n_full, d_inc_ptr.p, d_inc_src.p, d_loc.p, d_F, s);
+    ctx->timer.launches += 2;
+  }
+  TG_CUDA(cudaGetLastError());
+}
+
+void Sim::flux_finish(double* d_F) {
+  cudaStream_t s = ctx->stream;
+  const FaceTables ft{n_fe, ndk, d_qb_off.p, d_qf_off.p, d_Nb.p, d_Nf.p};
+  k3_local(ft, 0, n_fe, d_elem_off.p, d_gq.p, d_loc.p, s);
+  k3_gather(n_full, d_inc_ptr.p, d_inc_src.p, d_loc.p, d_F, s);
+  ctx->timer.launches += 2;
+}
+
+void Sim::flux_load_device(double t, double radius, double* d_F, int e0, int e1) {
+  e0 = std::max(0, std::min(e0, n_fe));
+  e1 = std::max(e0, std::min(e1, n_fe));
+  if (sf_ready && sf_flux_ok && e0 == 0 && e1 == n_fe) {
+    loads_device(t, radius, d_F, nullptr, true);
+    return;
+  }
+  // pair-wise K1 over the compact points of elements [e0, e1) (non-gridded
+  // patches, and the element-slab range calls)
+  cudaStream_t s = ctx->stream;
   const int nf = fine_elements(t, radius);
-  // extra[r]: added points of the first r fine elements (fine minus base rule)
-  int* extra = h_fine + n_fe + 1;
+  int* extra = h_fine.data() + n_fe + 1;
   extra[0] = 0;
   for (int r = 0; r < nf; ++r) {
     const int e = h_fine[r];
     extra[r + 1] = extra[r] + (h_qf_off[e + 1] - h_qf_off[e]) - (h_qb_off[e + 1] - h_qb_off[e]);
   }
-  if (nf > 0) TG_CUDA(cudaMemcpyAsync(d_fine.p, h_fine, sizeof(int) * nf, cudaMemcpyHostToDevice, s));
-  TG_CUDA(cudaMemcpyAsync(d_fine.p + n_fe + 1, extra, sizeof(int) * (nf + 1),
-                          cudaMemcpyHostToDevice, s));
-  // compact-list offset of element e: its base offset plus the extra points
-  // of the fine elements before it
+  {
+    char* h = stage_bytes(sizeof(int) * (2 * static_cast<size_t>(nf) + 1) + 32);
+    std::memcpy(h, h_fine.data(), sizeof(int) * nf);
+    std::memcpy(h + sizeof(int) * nf, extra, sizeof(int) * (nf + 1));
+    if (nf > 0)
+      TG_CUDA(cudaMemcpyAsync(d_fine.p, h, sizeof(int) * nf, cudaMemcpyHostToDevice, s));
+    TG_CUDA(cudaMemcpyAsync(d_fine.p + n_fe + 1, h + sizeof(int) * nf, sizeof(int) * (nf + 1),
+                            cudaMemcpyHostToDevice, s));
+    TG_CUDA(cudaEventRecord(sf_stage[(sf_stage_i + 2) % 3].done, s));
+  }
   auto offset_of = [&](int e) {
-    const int r = static_cast<int>(std::lower_bound(h_fine, h_fine + nf, e) - h_fine);
+    const int r = static_cast<int>(std::lower_bound(h_fine.begin(), h_fine.begin() + nf, e) -
+                                   h_fine.begin());
     return static_cast<long>(h_qb_off[e]) + extra[r];
   };
-  e0 = std::max(0, std::min(e0, n_fe));
-  e1 = std::max(e0, std::min(e1, n_fe));
   const long p0 = offset_of(e0), p1 = e1 == n_fe ? h_qb_off.back() + extra[nf] : offset_of(e1);
+  sf_last_npts = h_qb_off.back() + extra[nf];
   const FaceTables ft{n_fe, ndk, d_qb_off.p, d_qf_off.p, d_Nb.p, d_Nf.p};
   k3_point_index(ft, d_fine.p, d_fine.p + n_fe + 1, nf, d_pt_index.p, d_elem_off.p, s);
   ++ctx->timer.launches;
   K1Flux fl{d_pt_index.p + p0, d_qn.p, d_qw.p, cfg.material.conductivity};
-  // K5 split (full-range calls): sources [0, J) by DGEMM on the face grids
-  // (plus K1 on the fine-rule points, which are not on the grids), [J, n) by K1
-  const bool full = e0 == 0 && e1 == n_fe;
-  // per face the longest eligible prefix for that face's box (faces whose
-  // elements are contiguous and gridded with their fine points), else one
-  // prefix for the box of all faces
-  const size_t nfc = sf_faces.size();
-  std::vector<int> Jf(nfc, 0);
-  int J = 0, Jmax = 0;
-  if (sf_on && sf_flux_ok && full) {
-    if (sf_face_split) {
-      J = 1 << 30;
-      for (size_t f = 0; f < nfc; ++f) {
-        Jf[f] = sf_prefix(t, &sf_face_box[6 * f], &sf_face_box[6 * f + 3], sf_face_delta[f],
-                          sf_pf_face[f]);
-        J = std::min(J, Jf[f]);
-        Jmax = std::max(Jmax, Jf[f]);
-      }
-    } else {
-      J = Jmax = sf_prefix(t, sf_lo, sf_hi, sf_delta, sf_pf_flux);
-      std::fill(Jf.begin(), Jf.end(), J);
-    }
-  }
-  // profitability: a face's GEMM (a few launches, ~25 us) must save more K1
-  // pair work than it costs (TG_SF_MIN_PAIRS moved pairs, default 3e7 ~ 30 us)
-  if (Jmax > 0 && sf_face_split) {
-    J = 1 << 30;
-    Jmax = 0;
-    for (size_t f = 0; f < nfc; ++f) {
-      const double pts = static_cast<double>(sf_faces[f].U.size()) * sf_faces[f].V.size();
-      if (static_cast<double>(Jf[f]) * pts < sf_min_pairs) Jf[f] = 0;
-      J = std::min(J, Jf[f]);
-      Jmax = std::max(Jmax, Jf[f]);
-    }
-  } else if (Jmax > 0) {  // one prefix for all faces: all kept or all dropped
-    double pts = 0.0;
-    for (const SfGrid& g : sf_faces) pts += static_cast<double>(g.U.size()) * g.V.size();
-    if (static_cast<double>(J) * pts < sf_min_pairs) {
-      J = Jmax = 0;
-      std::fill(Jf.begin(), Jf.end(), 0);
-    }
-  }
-  sf_last_j[0] = J;
-  // the K1 remainder (FP64 pipe) runs on a side stream beside the GEMMs (DMMA)
-  const bool conc = Jmax > 0 && sf_face_split && sf_stream != nullptr;
-  cudaStream_t ks = conc ? sf_stream : s;
-  if (conc) {
-    TG_CUDA(cudaEventRecord(sf_ev[0], s));
-    TG_CUDA(cudaStreamWaitEvent(sf_stream, sf_ev[0], 0));
-  }
-  if (Jmax > 0 && sf_face_split) {
-    auto pos_of = [&](int e) { return e == n_fe ? p1 : offset_of(e); };
-    for (size_t f = 0; f < nfc; ++f) {
-      const long a = pos_of(sf_face_e[2 * f]), b = pos_of(sf_face_e[2 * f + 1]);
-      K1Flux ff{d_pt_index.p + a, d_qn.p, d_qw.p, cfg.material.conductivity};
-      const int end = sf_suffix_end(t, &sf_face_box[6 * f], &sf_face_box[6 * f + 3], Jf[f]);
-      k1_run(ctx, ctx->src6.p, ctx->n_src, d_qx.p, d_pt_index.p + a, b - a, t,
-             cfg.superpose.cull_exponent, K1Mode::flux, d_gq.p + a, nullptr, ff, ks, Jf[f], end);
-    }
-    if (conc) TG_CUDA(cudaEventRecord(sf_ev[1], sf_stream));
-  } else {
-    k1_run(ctx, ctx->src6.p, ctx->n_src, d_qx.p, d_pt_index.p + p0, p1 - p0, t,
-           cfg.superpose.cull_exponent, K1Mode::flux, d_gq.p + p0, nullptr, fl, s, J);
-  }
-  int fine_n = 0;
-  double* fine_G = nullptr;
-  if (Jmax > 0) {
-    const double alpha = ctx->mat.diffusivity(), rcp = ctx->mat.volumetric_capacity();
-    const int tqb = h_qb_off.back();
-    if (nf > 0 && sf_fine_ok) {
-      // the step's fine elements: per face the bounding rectangle of their
-      // cells in the face's fine grid, one GEMM each
-      const size_t nF = sf_fine.size();
-      std::vector<int> rc(4 * nF);
-      for (size_t f = 0; f < nF; ++f) {
-        rc[4 * f] = rc[4 * f + 1] = 1 << 30;
-        rc[4 * f + 2] = rc[4 * f + 3] = -1;
-      }
-      int nfp = 0;
-      for (int r = 0; r < nf; ++r) {
-        const int e = h_fine[r], f = sf_elem_face[e];
-        const int* er = &sf_erect[4 * static_cast<size_t>(e)];
-        rc[4 * f] = std::min(rc[4 * f], er[0]);
-        rc[4 * f + 1] = std::min(rc[4 * f + 1], er[1]);
-        rc[4 * f + 2] = std::max(rc[4 * f + 2], er[2]);
-        rc[4 * f + 3] = std::max(rc[4 * f + 3], er[3]);
-        nfp += h_qf_off[e + 1] - h_qf_off[e];
-      }
-      size_t gtot = 0;
-      for (size_t f = 0; f < nF; ++f) {
-        int* hr = h_sf_rect + 5 * f;
-        const bool any = rc[4 * f + 2] >= 0;
-        hr[0] = rc[4 * f];
-        hr[1] = rc[4 * f + 1];
-        hr[2] = any ? rc[4 * f + 2] - rc[4 * f] + 1 : 0;
-        hr[3] = static_cast<int>(gtot);
-        hr[4] = sf_fine[f].axn;
-        if (any) gtot += static_cast<size_t>(hr[2]) * (rc[4 * f + 3] - rc[4 * f + 1] + 1);
-      }
-      double* Gf = d_sf_Gf.ensure(gtot);
-      for (size_t f = 0; f < nF; ++f) {
-        const int* hr = h_sf_rect + 5 * f;
-        if (hr[2] == 0) continue;
-        SfDev g = sf_fine_dev[f];
-        g.U += hr[0];
-        g.V += hr[1];
-        g.na = hr[2];
-        g.nb = rc[4 * f + 3] - rc[4 * f + 1] + 1;
-        sf_flops += sf_contract(cublas, g, true, ctx->src6.p, Jf[f], sf_kc, t, alpha, rcp,
-                                sf_scratch(g.na, g.nb, Jf[f]), Gf + hr[3], s);
-        sf_pairs += static_cast<double>(g.na) * g.nb * Jf[f];
-        ctx->timer.launches += 5;
-      }
-      int* pos = h_sf_fine;
-      int* ids = h_sf_fine + nfp;
-      int m = 0;
-      for (int r = 0; r < nf; ++r) {
-        const int e = h_fine[r];
-        const int o = h_qb_off[e] + extra[r], nq = h_qf_off[e + 1] - h_qf_off[e];
-        for (int l = 0; l < nq; ++l, ++m) {
-          pos[m] = o + l;
-          ids[m] = h_qf_off[e] + l;
-        }
-      }
-      TG_CUDA(cudaMemcpyAsync(d_sf_fine.p, h_sf_fine, sizeof(int) * 2 * nfp,
-                              cudaMemcpyHostToDevice, s));
-      TG_CUDA(cudaMemcpyAsync(d_sf_rect.p, h_sf_rect, sizeof(int) * 5 * nF,
-                              cudaMemcpyHostToDevice, s));
-      fine_n = nfp;  // added after the join with the K1 stream
-      fine_G = Gf;
-    } else if (nf > 0) {
-      int nfp = 0;
-      for (int r = 0; r < nf; ++r) nfp += h_qf_off[h_fine[r] + 1] - h_qf_off[h_fine[r]];
-      int* pos = h_sf_fine;
-      int* ids = h_sf_fine + nfp;
-      int m = 0;
-      for (int r = 0; r < nf; ++r) {
-        const int e = h_fine[r];
-        const int o = h_qb_off[e] + extra[r], nq = h_qf_off[e + 1] - h_qf_off[e];
-        for (int l = 0; l < nq; ++l, ++m) {
-          pos[m] = o + l;
-          ids[m] = tqb + h_qf_off[e] + l;
-        }
-      }
-      TG_CUDA(cudaMemcpyAsync(d_sf_fine.p, h_sf_fine, sizeof(int) * 2 * nfp,
-                              cudaMemcpyHostToDevice, s));
-      K1Flux ff{d_sf_fine.p + nfp, d_qn.p, d_qw.p, cfg.material.conductivity};
-      k1_run(ctx, ctx->src6.p, ctx->n_src, d_qx.p, d_sf_fine.p + nfp, nfp, t,
-             cfg.superpose.cull_exponent, K1Mode::flux, d_sf_tmp.p, nullptr, ff, s, 0, J);
-      sf_scatter_add(nfp, d_sf_fine.p, d_sf_tmp.p, d_gq.p, s);
-      ctx->timer.launches += 1;
-    }
-    for (size_t k = 0; k < sf_faces_dev.size(); ++k) {
-      const SfDev& g = sf_faces_dev[k];
-      sf_flops += sf_contract(cublas, g, true, ctx->src6.p, Jf[k], sf_kc, t, alpha, rcp,
-                              sf_scratch(g.na, g.nb, Jf[k]), d_sf_G.p + sf_faces_off[k], s);
-      sf_pairs += static_cast<double>(g.na) * g.nb * Jf[k];
-      ctx->timer.launches += 5;
-    }
-    if (conc) TG_CUDA(cudaStreamWaitEvent(s, sf_ev[1], 0));  // K1 wrote gq
-    if (fine_n > 0) {
-      sf_add_fine(fine_n, d_sf_fine.p, d_sf_fine.p + fine_n, tqb, d_sf_fa.p, d_sf_fb.p,
-                  d_sf_ff.p, d_sf_rect.p, fine_G, d_qn.p, d_qw.p, cfg.material.conductivity,
-                  d_gq.p, s);
-      ++ctx->timer.launches;
-    }
-    sf_add_flux(static_cast<int>(p1 - p0), d_pt_index.p, tqb, d_sf_gcell.p, d_sf_gaxn.p,
-                d_sf_G.p, d_qn.p, d_qw.p, cfg.material.conductivity, d_gq.p, s);
-    ++ctx->timer.launches;
-  }
+  k1_run(ctx, ctx->src6.p, ctx->n_src, d_qx.p, d_pt_index.p + p0, p1 - p0, t,
+         cfg.superpose.cull_exponent, K1Mode::flux, d_gq.p + p0, nullptr, fl, s);
   k3_local(ft, e0, e1, d_elem_off.p, d_gq.p, d_loc.p, s);
   ++ctx->timer.launches;
   if (d_F) {
@@ -1016,24 +1167,12 @@ void Sim::dirichlet_device(double t, double* d_g, int c0, int c1) {
   if (c1 < 0) c1 = n_con;
   c0 = std::max(0, std::min(c0, n_con));
   c1 = std::max(c0, std::min(c1, n_con));
-  int J = (sf_on && sf_dir_ok && c0 == 0 && c1 == n_con)
-              ? sf_prefix(t, sf_dir.lo, sf_dir.hi, sf_dir.delta, sf_pf_dir)
-              : 0;
-  if (static_cast<double>(J) * n_con < sf_min_pairs) J = 0;  // not worth the launches
-  sf_last_j[1] = J;
-  const int end = J > 0 ? sf_suffix_end(t, sf_dir.lo, sf_dir.hi, J) : -1;
-  k1_run(ctx, ctx->src6.p, ctx->n_src, d_grev.p + 3 * static_cast<size_t>(c0), nullptr, c1 - c0,
-         t, cfg.superpose.cull_exponent, K1Mode::dirichlet, d_g, nullptr, {}, ctx->stream, J,
-         end);
-  if (J > 0) {  // g = -(K1 part) - (GEMM part)
-    const SfDev& g = sf_dir_dev;
-    sf_flops += sf_contract(cublas, g, false, ctx->src6.p, J, sf_kc, t, ctx->mat.diffusivity(),
-                            ctx->mat.volumetric_capacity(), sf_scratch(g.na, g.nb, J),
-                            d_sf_Gdir.p, ctx->stream);
-    sf_add_dirichlet(n_con, d_sf_dcell.p, d_sf_Gdir.p, d_g, ctx->stream);
-    ctx->timer.launches += 6;
-    sf_pairs += static_cast<double>(n_con) * J;
+  if (sf_ready && sf_dir_ok && c0 == 0 && c1 == n_con) {
+    loads_device(t, 0.0, nullptr, d_g, true);
+    return;
   }
+  k1_run(ctx, ctx->src6.p, ctx->n_src, d_grev.p + 3 * static_cast<size_t>(c0), nullptr, c1 - c0,
+         t, cfg.superpose.cull_exponent, K1Mode::dirichlet, d_g, nullptr, {}, ctx->stream);
 }
 
 PcgStatus Sim::theta_step_device(double tol, int max_iter) {
@@ -1109,8 +1248,12 @@ void Sim::theta_step_launch(double tol, int max_iter) {
 void Sim::reset() {
   cudaStream_t s = ctx->stream;
   TG_CUDA(cudaMemsetAsync(d_x.p, 0, sizeof(double) * n_free, s));
-  dirichlet_device(0.0, d_gn.p);
-  flux_load_device(0.0, cfg.mesh.elevate_radius, d_Fn.p);
+  if (sf_ready && sf_flux_ok && sf_dir_ok) {
+    loads_device(0.0, cfg.mesh.elevate_radius, d_Fn.p, d_gn.p, true);
+  } else {
+    dirichlet_device(0.0, d_gn.p);
+    flux_load_device(0.0, cfg.mesh.elevate_radius, d_Fn.p);
+  }
   step = 0;
   TG_CUDA(cudaStreamSynchronize(s));
 }
@@ -1124,9 +1267,13 @@ PcgStatus Sim::advance() {
     return std::chrono::steady_clock::now();
   };
   const auto t0 = now();
-  flux_load_device(t1, cfg.mesh.elevate_radius, d_F1.p);
+  if (sf_ready && sf_flux_ok && sf_dir_ok) {  // both loads in one fused pass
+    loads_device(t1, cfg.mesh.elevate_radius, d_F1.p, d_g1.p, true);
+  } else {
+    flux_load_device(t1, cfg.mesh.elevate_radius, d_F1.p);
+  }
   const auto ta = now();
-  dirichlet_device(t1, d_g1.p);
+  if (!(sf_ready && sf_flux_ok && sf_dir_ok)) dirichlet_device(t1, d_g1.p);
   const auto tb = now();
   const PcgStatus st = theta_step_device(cfg.stepping.solver_tol, cfg.stepping.max_iter);
   if (timing) {
@@ -1139,6 +1286,68 @@ PcgStatus Sim::advance() {
   std::swap(d_gn.p, d_g1.p);
   step = s1;
   return st;
+}
+
+// n steps with no host synchronisation between them: every step's loads,
+// RHS and solve are enqueued and its PCG status is copied to a pinned slot;
+// the statuses are read once at the end. A failing solve raises the
+// reference's numeric_error (sparse.cpp:75-99) for the first failing step, as
+// run_time_loop would; the state after such a step is unspecified (the
+// reference's State is lost with the exception).
+long Sim::advance_steps(int n, double* last_rel) {
+  static const bool timing = std::getenv("TG_STEP_TIMING") != nullptr;
+  long it = 0;
+  if (n <= 0) return 0;
+  if (use_fdm || timing) {  // host-driven solver / per-phase timing: one step at a time
+    PcgStatus st{};
+    for (int k = 0; k < n; ++k) {
+      st = advance();
+      it += st.iterations;
+    }
+    if (last_rel) *last_rel = st.rel_residual;
+    return it;
+  }
+  if (!diag_ok) throw numeric_error("pcg: non-positive diagonal, matrix not SPD");
+  if (static_cast<size_t>(n) > h_steps_cap) {
+    if (h_steps) TG_CUDA(cudaFreeHost(h_steps));
+    h_steps = nullptr;
+    h_steps_cap = 0;
+    TG_CUDA(cudaMallocHost(&h_steps, sizeof(PcgStatus) * n));
+    h_steps_cap = n;
+  }
+  cudaStream_t s = ctx->stream;
+  const int first = step;
+  for (int k = 0; k < n; ++k) {
+    const double t1 = (step + 1) * dt_solver;  // driver.cpp:127
+    if (sf_ready && sf_flux_ok && sf_dir_ok) {
+      loads_device(t1, cfg.mesh.elevate_radius, d_F1.p, d_g1.p, true);
+    } else {
+      flux_load_device(t1, cfg.mesh.elevate_radius, d_F1.p);
+      dirichlet_device(t1, d_g1.p);
+    }
+    ctx->timer.timed(3, s, [&] { theta_step_launch(cfg.stepping.solver_tol, cfg.stepping.max_iter); });
+    TG_CUDA(cudaMemcpyAsync(&h_steps[k], d_status.p, sizeof(PcgStatus), cudaMemcpyDeviceToHost, s));
+    std::swap(d_Fn.p, d_F1.p);
+    std::swap(d_gn.p, d_g1.p);
+    ++step;
+  }
+  TG_CUDA(cudaStreamSynchronize(s));
+  for (int k = 0; k < n; ++k) {
+    const PcgStatus& st = h_steps[k];
+    it += st.iterations;
+    ctx->timer.k2_bytes += 104.0 * n_free * st.iterations;  // SURVEY.md §8d algorithmic bytes
+    k2_iterations += st.iterations;
+    if (st.status == 4 || st.status == 3) {
+      step = first + k + 1;
+      if (st.status == 4) throw numeric_error("pcg: indefinite direction, matrix not SPD");
+      char buf[64];
+      std::snprintf(buf, sizeof(buf), "%.17g", st.rel_residual);
+      throw numeric_error("pcg: no convergence in " + std::to_string(cfg.stepping.max_iter) +
+                          " iterations, relative residual " + buf);
+    }
+  }
+  if (last_rel) *last_rel = h_steps[n - 1].rel_residual;
+  return it;
 }
 
 PcgStatus Sim::advance_with_loads(const double* d_F1_in, const double* d_g1_in) {

@@ -12,6 +12,7 @@
 #include "k2_fdm.cuh"
 #include "k2_kron.cuh"
 #include "k4_eval.cuh"
+#include "k5_fused.cuh"
 #include "k5_sumfact.cuh"
 
 namespace tgb {
@@ -42,6 +43,9 @@ class Sim {
   // run_time_loop pieces (driver.cpp:105-146)
   void reset();          // state 0: free = 0, g_0, F_0
   PcgStatus advance();   // one step: F_{n+1}, g_{n+1}, theta step
+  // n steps without host synchronisation between them (statuses read at the
+  // end); returns the CG iterations
+  long advance_steps(int n, double* last_rel);
   // one step with F_{n+1}, g_{n+1} supplied on the device (a multi-GPU driver
   // assembles them sharded, all-gathers, and every rank steps)
   PcgStatus advance_with_loads(const double* d_F1_in, const double* d_g1_in);
@@ -67,24 +71,40 @@ class Sim {
   void flux_profile(FaceId face, int n_samples, double edge_v, const double* theta_axis,
                     double* out);
 
-  // K5 (k5_sumfact.cuh): the superposition on the gridded face / Greville
-  // point sets of an axis-aligned patch as a DGEMM over the sources that no
-  // cull can touch there; K1 keeps the rest. On by default where the sets are
-  // grids (TG_SUMFACT=0 or set_sumfact(false) turns it off). Only the
-  // full-range flux / Dirichlet calls use it (the sharded range calls are K1).
+  // K5 (k5_fused.cuh): the superposition on the gridded face / Greville point
+  // sets of an axis-aligned patch as a fused on-chip contraction over the
+  // sources no cull can reach in each region, with the pair-wise remainder on
+  // K1. On by default where the sets are grids (TG_SUMFACT=0 or
+  // set_sumfact(false): every pair through K1, with the same per-region
+  // source ranges).
   void set_sumfact(bool on) { sf_on = on && (sf_flux_ok || sf_dir_ok); }
-  // the GEMM source prefixes at t (flux: smallest over the faces; Dirichlet), host only
-  void sf_prefixes(double t, int* out);
+  // host restatement of the device plan at t for the static regions (flux
+  // tiles, then Greville tiles): J (contraction prefix), E (remainder end)
+  void sf_plan_host(double t, int* J, int* E);
   bool sf_on = false, sf_flux_ok = false, sf_dir_ok = false;
-  double sf_flops = 0.0;   // GEMM flops issued (2 na nb Jpad per set)
-  double sf_pairs = 0.0;   // point x source pairs taken off K1
-  int sf_last_j[2] = {0, 0};  // source prefix of the last flux / Dirichlet call
-  int sf_kc = 2048;           // sources per GEMM chunk (one batch entry; TG_SF_KC)
-  double sf_min_pairs = 3e7;  // smallest J x points worth a GEMM (TG_SF_MIN_PAIRS)
-  int sf_bands = 1;           // bands of element rows per face (TG_SF_BANDS; see DESIGN K5)
+  // contraction flops (2 per point x source) since setup, read from the device
+  double sf_flops_total();
+  double sf_min_pairs = 3e7;  // smallest J x points worth a contraction (TG_SF_MIN_PAIRS)
+  int sf_k1_splits = 4;       // source splits of the remainder launch (TG_SF_K1_SPLITS)
+  // the device plan of the static regions, each part (flux / Greville) as its
+  // last call computed it, read back on request
+  void sf_last_plan(int* J, int* E);
+  int sf_n_regions() const { return static_cast<int>(sf_regions_h.size()); }
+  int sf_dir_regions() const { return sf_nt_static - sf_nt_flux; }
+  const std::vector<SfRegion>& sf_regions() const { return sf_regions_h; }
+  // multi-GPU: this rank computes the regions r with r % world == rank
+  int sf_rank = 0, sf_world = 1;
+  // the fused loads path: F (d_F may be null) and/or g at t. gather = false
+  // leaves the (rank-partial) compact integrand in d_gq without the K3 local
+  // loads and gather (multi-GPU: all-reduced by the caller, then flux_finish)
+  void loads_device(double t, double radius, double* d_F, double* d_g, bool gather = true);
+  void flux_finish(double* d_F);  // k3_local + gather over all elements from d_gq
+  bool sf_fused_ready() const { return sf_ready; }
+  long sf_compact_points() const { return sf_last_npts; }
 
   bool focus_at(double t, Vec3& focus) const;
   int fine_elements(double t, double radius);  // fills h_fine, returns the count
+  std::vector<int> h_fine;  // fine elements (sorted), then the running extra-point counts
 
   // ---- host setup
   RunConfig cfg;
@@ -145,7 +165,8 @@ class Sim {
   DevBuf<unsigned long long> d_trace;  // K2 phase stamps (TG_K2_TRACE)
   bool trace_on = false;
   PcgStatus* h_status = nullptr;
-  int* h_fine = nullptr;
+  PcgStatus* h_steps = nullptr;  // pinned per-step statuses of advance_steps
+  size_t h_steps_cap = 0;
   int pcg_blocks = 1;
   bool diag_ok = true;
   int step = 0;
@@ -154,42 +175,45 @@ class Sim {
  private:
   void setup_host();
   void setup_device(int device, int preconditioner);
-  void sf_setup_host();    // grids, face boxes (host only)
+  void sf_setup_host();    // grids, tiles, regions, remainder entries (host only)
   void sf_setup_device();  // uploads
-  std::vector<int> sf_h_gcell, sf_h_gaxn, sf_h_fa, sf_h_fb, sf_h_ff;  // until uploaded
-  int sf_g_total = 0;
-  struct SfPrefix {
-    int J = 0;
-    double t = 0.0;
-    bool valid = false;  // [0, J) were all causally active at t (reusable at later t)
-  };
-  int sf_prefix(double t, const double lo[3], const double hi[3], double delta, SfPrefix& c);
-  // end of the K1 source range [begin, end): trailing sources culled on the whole box drop out
-  int sf_suffix_end(double t, const double lo[3], const double hi[3], int begin);
-  std::vector<SfGrid> sf_faces;
-  std::vector<SfDev> sf_faces_dev;
-  std::vector<int> sf_faces_off;
-  bool sf_fine_ok = false;  // fine-rule points gridded per face too
-  bool sf_face_split = false;  // per-face source prefixes (face boxes)
-  std::vector<int> sf_face_e;  // per face: element range [begin, end)
-  std::vector<double> sf_face_box, sf_face_delta;
-  std::vector<SfPrefix> sf_pf_face;
-  std::vector<SfGrid> sf_fine;
-  std::vector<SfDev> sf_fine_dev;
-  std::vector<int> sf_elem_face, sf_erect;  // per face element: face, fine-cell rectangle
-  DevBuf<int> d_sf_fa, d_sf_fb, d_sf_ff, d_sf_rect;
-  DevBuf<double> d_sf_Gf;
-  int* h_sf_rect = nullptr;
-  cudaStream_t sf_stream = nullptr;  // K1 remainder beside the GEMMs (TG_SF_SERIAL=1: one stream)
-  cudaEvent_t sf_ev[2] = {nullptr, nullptr};
+  std::vector<int> sf_h_gcell, sf_h_fa, sf_h_fb, sf_h_ff;  // until the entry lists are built
+  std::vector<SfGrid> sf_faces;           // base grid per face
+  std::vector<SfGrid> sf_fine;            // fine grid per face (sf_fine_ok)
   SfGrid sf_dir;
-  SfDev sf_dir_dev{};
-  double sf_lo[3] = {0, 0, 0}, sf_hi[3] = {0, 0, 0}, sf_delta = 0.0;
-  SfPrefix sf_pf_flux, sf_pf_dir;
-  DevBuf<double> d_sf_uv, d_sf_G, d_sf_Gdir, d_sf_vec, d_sf_A, d_sf_B, d_sf_C, d_sf_tmp;
-  DevBuf<int> d_sf_gcell, d_sf_gaxn, d_sf_dcell, d_sf_fine;
-  int* h_sf_fine = nullptr;  // pinned: fine compact positions, then their qp ids
-  SfScratch sf_scratch(int na, int nb, int J);
+  bool sf_fine_ok = false;
+  std::vector<int> sf_elem_face, sf_erect;  // per face element: face, fine-cell rectangle
+  // static tables: grids (faces, fine faces, Greville), tiles / regions
+  // (flux base tiles [0, sf_nt_flux), Greville tiles [sf_nt_flux, sf_nt_static)),
+  // remainder entries (flux base [0, sf_ne_flux), Greville [.., sf_ne_static))
+  std::vector<SfGridDesc> sf_grids_h;
+  std::vector<SfTile> sf_tiles_h;
+  std::vector<SfRegion> sf_regions_h;
+  std::vector<int> sf_ent_q, sf_ent_tile, sf_ent_cell, sf_ent_pos, sf_cta_region;
+  int sf_nt_flux = 0, sf_nt_static = 0, sf_ne_flux = 0, sf_ne_static = 0;
+  int sf_nc_flux = 0, sf_nc_static = 0;  // remainder CTAs
+  int sf_grid_fine0 = 0, sf_grid_dir = -1;
+  double sf_vplane = 0.0;
+  bool sf_ready = false;
+  long sf_last_npts = 0;
+  int sf_k1_ppc = 0;  // remainder points per K1 CTA
+  DevBuf<double> d_sf_lines, d_sf_cb, d_sf_tab, d_sf_scratch, d_sf_stats;
+  DevBuf<SfGridDesc> d_sf_grids;
+  DevBuf<SfTile> d_sf_tiles;
+  DevBuf<SfRegion> d_sf_regions;
+  DevBuf<SfConst> d_sf_cst;
+  DevBuf<int> d_sf_J, d_sf_E, d_sf_Jl, d_sf_El, d_sf_prefix, d_sf_ent_q, d_sf_ent_tile, d_sf_ent_cell,
+      d_sf_ent_pos, d_sf_cta, d_sf_qelem;
+  // per-step host staging (pinned ring; an event marks when a slot's copies ran)
+  struct Stage {
+    char* h = nullptr;
+    size_t cap = 0;
+    cudaEvent_t done = nullptr;
+  };
+  Stage sf_stage[3];
+  int sf_stage_i = 0;
+  char* stage_bytes(size_t bytes);  // the next ring slot, grown / waited for as needed
+  void release_stages();
 };
 
 }  // namespace tgb

@@ -135,15 +135,50 @@ int tg_sim_set_sumfact(tg_sim* s, int on) {
 
 int tg_sim_sumfact_stats(tg_sim* s, double* out) {
   return sim_guard(s, [&](Sim& m) {
+    const int nr = m.sf_n_regions();
+    double jf = 0.0, jd = 0.0;
+    if (m.sf_fused_ready() && nr > 0) {  // the last call's device plan
+      std::vector<int> J(nr), E(nr);
+      m.sf_last_plan(J.data(), E.data());
+      int mf = 1 << 30, md = 1 << 30;
+      for (int r = 0; r < nr; ++r) {
+        const bool dir = m.sf_dir_ok && r >= nr - m.sf_dir_regions();
+        (dir ? md : mf) = std::min(dir ? md : mf, J[r]);
+      }
+      jf = mf == (1 << 30) ? 0.0 : mf;
+      jd = md == (1 << 30) ? 0.0 : md;
+    }
     const double v[] = {m.sf_on ? 1.0 : 0.0, m.sf_flux_ok ? 1.0 : 0.0, m.sf_dir_ok ? 1.0 : 0.0,
-                        static_cast<double>(m.sf_last_j[0]), static_cast<double>(m.sf_last_j[1]),
-                        m.sf_flops, m.sf_pairs, static_cast<double>(m.sf_kc)};
+                        jf, jd, m.sf_flops_total(), static_cast<double>(nr),
+                        static_cast<double>(kSfItem)};
     std::memcpy(out, v, sizeof(v));
   }, false);
 }
 
-int tg_sim_sumfact_prefix(tg_sim* s, double t, int* out) {
-  return sim_guard(s, [&](Sim& m) { m.sf_prefixes(t, out); }, false);
+int tg_sim_sumfact_regions(tg_sim* s, double* out) {
+  return sim_guard(s, [&](Sim& m) {
+    const auto& R = m.sf_regions();
+    for (size_t r = 0; r < R.size(); ++r) {
+      double* o = out + 8 * r;
+      for (int a = 0; a < 3; ++a) {
+        o[a] = R[r].lo[a];
+        o[3 + a] = R[r].hi[a];
+      }
+      o[6] = R[r].delta;
+      o[7] = R[r].npts;
+    }
+  }, false);
+}
+
+int tg_sim_sumfact_plan(tg_sim* s, double t, int* J, int* E) {
+  return sim_guard(s, [&](Sim& m) { m.sf_plan_host(t, J, E); }, false);
+}
+
+int tg_sim_sumfact_last_plan(tg_sim* s, int* J, int* E) {
+  return sim_guard(s, [&](Sim& m) {
+    if (!m.sf_fused_ready()) throw std::logic_error("no device plan (host-only simulation)");
+    m.sf_last_plan(J, E);
+  });
 }
 
 int tg_sim_params(tg_sim* s, double* out) {
@@ -234,14 +269,10 @@ int tg_sim_reset(tg_sim* s) {
 
 int tg_sim_advance(tg_sim* s, int n_steps, long* cg_iterations, double* last_rel) {
   return sim_guard(s, [&](Sim& m) {
-    long it = 0;
-    PcgStatus st{};
-    for (int k = 0; k < n_steps; ++k) {
-      st = m.advance();
-      it += st.iterations;
-    }
+    double rel = 0.0;
+    const long it = m.advance_steps(n_steps, &rel);
     if (cg_iterations) *cg_iterations = it;
-    if (last_rel) *last_rel = st.rel_residual;
+    if (last_rel) *last_rel = rel;
   });
 }
 

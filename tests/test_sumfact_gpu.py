@@ -1,10 +1,10 @@
-"""K5 (sum-factorised superposition, csrc/k5_sumfact.cu) against the unmodified
-reference and against the K1 pair loop.
+"""K5 (fused sum-factorised superposition, csrc/k5_fused.cu) against the
+unmodified reference and against the K1 pair loop.
 
 K5 evaluates the superposition at the lateral-face quadrature points and the
-bottom Greville points of an axis-aligned patch as a DGEMM over the sources
-that no cull can reach there (old sources of a long scan), K1 keeping the
-young ones with the reference's exact cull. Tolerances are the hot path's
+bottom Greville points of an axis-aligned patch as an on-chip DMMA contraction
+over the sources that no cull can reach in each region (old sources of a long
+scan), K1 keeping the rest pair by pair with the reference's exact cull. Tolerances are the hot path's
 (BASELINE.json north_star): loads and Dirichlet values normwise <= 1e-10 with
 the reference's exact zeros reproduced (the Dirichlet values also pointwise),
 correction-field coefficients normwise <= 1e-8 every step.
@@ -23,7 +23,7 @@ pytestmark = pytest.mark.gpu
 @pytest.fixture(autouse=True)
 def _gemm_even_when_small(monkeypatch):
     # the small parity configs move fewer pairs than K5's profitability
-    # threshold (3e7 per face); force the GEMM path so it is what gets checked
+    # threshold (3e7 per region); force the contraction so it is what gets checked
     monkeypatch.setenv("TG_SF_MIN_PAIRS", "0")
 
 
@@ -115,6 +115,23 @@ def test_sumfact_on_off_and_causal_zero(tmp_path):
     s.close()
 
 
+def test_device_plan_is_the_host_plan(tmp_path):
+    """The plan kernel's J / E per region equal Sim::sf_plan_host's."""
+    s = tg.Simulation(long_history_cfg(tmp_path), t_end=2e-4)
+    R = s.sumfact_regions()
+    flux = R[:, 5] > R[:, 2]  # lateral faces span z; the Greville grid lies in z = 0
+    assert flux.any() and (~flux).any()
+    for t in (0.0, 1e-4, 2e-4):
+        s.flux_load(t)
+        J, E = s.sumfact_last_plan()
+        Jh, Eh = s.sumfact_plan(t)
+        assert np.array_equal(J[flux], Jh[flux]) and np.array_equal(E[flux], Eh[flux]), t
+        s.dirichlet_values(t)
+        J, E = s.sumfact_last_plan()
+        assert np.array_equal(J, Jh) and np.array_equal(E, Eh), t
+    s.close()
+
+
 def test_sumfact_not_used_on_curved_patch():
     s = tg.Simulation(os.path.join(ROOT, "configs", "qc_small.cfg"))
     st = s.sumfact_stats()
@@ -132,7 +149,7 @@ def test_sumfact_config4_full_size():
         F1, d1 = s.flux_load(t), s.dirichlet_values(t)
         st = s.sumfact_stats()
         assert st["last_j_flux"] > 80000 and st["last_j_dirichlet"] > 80000, st
-        # deterministic: fixed chunking and chunk-reduction order, K1 on its own stream
+        # deterministic: fixed stream-K split and partial-sum order
         assert np.array_equal(s.flux_load(t), F1) and np.array_equal(s.dirichlet_values(t), d1)
         s.set_sumfact(False)
         F0, d0 = s.flux_load(t), s.dirichlet_values(t)

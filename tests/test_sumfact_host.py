@@ -1,8 +1,11 @@
 """K5's host decisions without a GPU (host-only simulations): which point sets are
-tensor grids, and the source prefix [0, J) that takes the GEMMs at a time t —
-checked against a numpy restatement of the rule in csrc/k5_sumfact.cu
-(sf_source_eligible: every pair of the source with a point of the face's bounding
-box has r.r <= cull * spread * (1 - 1e-9), or the source is causally inactive)."""
+tensor grids, how they are cut into regions, and the per-region plan at a time t
+— the contraction prefix J and the pair-wise remainder end E — checked against a
+numpy restatement of the rule (csrc/k5_fused.cu sf_plan_kernel, restated on the
+host by Sim::sf_plan_host): J = the first source with a point of the region's
+box (+- delta) it could cull there (r.r > cull * spread * (1 - 1e-9)), 0 when
+J x points < the profitability threshold; E = one past the last source not
+culled on the whole box. Causally inactive sources are eligible and culled."""
 import os
 
 import numpy as np
@@ -25,65 +28,75 @@ def test_grids_detected_on_cuboids_only():
     q = host_sim(os.path.join(ROOT, "configs", "qc_small.cfg"))  # curved quarter cylinder
     st = q.sumfact_stats()
     assert not st["faces_gridded"]
-    assert q.sumfact_prefix(1e-3)[0] == 0
+    R = q.sumfact_regions()
+    assert (R[:, 7] > 0).all()  # only the (flat, gridded) Greville regions
     q.close()
 
 
 def test_switch_off():
     s = host_sim(os.path.join(ROOT, "configs", "cfg2_raster_layer.cfg"))
     s.set_sumfact(False)
-    assert not s.sumfact_stats()["on"] and s.sumfact_prefix(0.02) == (0, 0)
+    assert not s.sumfact_stats()["on"]
+    J, E = s.sumfact_plan(0.02)
+    assert not J.any() and E.any()  # every pair on K1, still trimmed per region
     s.set_sumfact(True)
     assert s.sumfact_stats()["on"]
     s.close()
 
 
-def _prefix(src, t, alpha, cull, lo, hi):
+def _plan(src, t, alpha, cull, reg, min_pairs):
     dt = t - src[:, 5]
+    active = dt > 0.0
     spread = 4.0 * alpha * dt
     p = src[:, :3]
-    r2 = np.maximum((lo - p) ** 2, (hi - p) ** 2).sum(axis=1)
-    ok = ~(dt > 0.0) | (r2 * (1.0 + 1e-9) <= cull * spread)
+    lo, hi, delta, npts = reg[0:3] - reg[6], reg[3:6] + reg[6], reg[6], reg[7]
+    r2max = np.maximum((lo - p) ** 2, (hi - p) ** 2).sum(axis=1)
+    ok = ~active | ((r2max * (1.0 + 1e-9) <= cull * spread)
+                    & (36.0 * cull * delta * delta <= 1e-24 * spread))
     bad = np.flatnonzero(~ok)
-    return int(bad[0]) if len(bad) else len(src)
+    n_act = int(np.flatnonzero(active)[-1]) + 1 if active.any() else 0
+    J = int(bad[0]) if len(bad) and bad[0] < n_act else n_act
+    if J * npts < min_pairs:
+        J = 0
+    d = np.maximum(np.maximum(lo - p, p - hi), 0.0)
+    culled = ~active | ((d * d).sum(axis=1) * (1.0 - 1e-9) > cull * spread)
+    keep = np.flatnonzero(~culled[J:n_act])
+    E = J + int(keep[-1]) + 1 if len(keep) else J
+    return J, E
 
 
-def _face_boxes(s):
+def test_regions_cover_the_grids():
+    s = host_sim(os.path.join(ROOT, "configs", "cfg2_raster_layer.cfg"))
+    R = s.sumfact_regions()
     fs = s.face_sets()
     tqb = s.info["total_qb"]
-    nq, xq = fs["nq"], fs["xq"]
-    ax = np.abs(nq).argmax(axis=1)
-    key = 2 * ax + (nq[np.arange(len(nq)), ax] > 0)
-    boxes = {}
-    for e in range(s.info["n_face_elems"]):
-        b0, b1 = fs["qb_off"][e], fs["qb_off"][e + 1]
-        f0, f1 = tqb + fs["qf_off"][e], tqb + fs["qf_off"][e + 1]
-        k = int(key[b0])
-        pts = np.concatenate([xq[b0:b1], xq[f0:f1]])
-        lo, hi = boxes.get(k, (np.full(3, np.inf), np.full(3, -np.inf)))
-        boxes[k] = (np.minimum(lo, pts.min(axis=0)), np.maximum(hi, pts.max(axis=0)))
-    return boxes
+    n_dir = s.info["n_constrained"]
+    # region point counts: every base quadrature point and every Greville
+    # point exactly once; every point inside its grid's region boxes
+    assert R[:, 7].sum() == tqb + n_dir
+    for pts in (fs["xq"][:tqb], s.greville_points()):
+        inside = np.zeros(len(pts), dtype=int)
+        for r in R:
+            lo, hi = r[0:3] - r[6] - 1e-15, r[3:6] + r[6] + 1e-15
+            inside += np.all((pts >= lo) & (pts <= hi), axis=1)
+        assert inside.min() >= 1
+    s.close()
 
 
 @pytest.mark.parametrize("t", [-1.0, 0.0, 1e-4, 3e-3])
-def test_prefix_matches_restatement(tmp_path, monkeypatch, t):
-    path = long_history_cfg(tmp_path)
-    banded = host_sim(path)  # default: faces cut into bands of element rows
-    monkeypatch.setenv("TG_SF_BANDS", "1")  # whole faces: the restatement's boxes
-    s = host_sim(path)
+@pytest.mark.parametrize("min_pairs", [0.0, 3e7])
+def test_plan_matches_restatement(tmp_path, monkeypatch, t, min_pairs):
+    monkeypatch.setenv("TG_SF_MIN_PAIRS", repr(min_pairs))
+    s = host_sim(long_history_cfg(tmp_path))
     src = s.sources()
     k, rho, c = (s.params[n] for n in ("conductivity", "density", "heat_capacity"))
     alpha, cull = k / (rho * c), s.params["cull"]
-    jf = min(_prefix(src, t, alpha, cull, lo, hi) for lo, hi in _face_boxes(s).values())
-    g = s.greville_points()
-    jd = _prefix(src, t, alpha, cull, g.min(axis=0), g.max(axis=0))
-    got = s.sumfact_prefix(t)
-    assert got == (jf, jd)
-    jb = banded.sumfact_prefix(t)  # smaller boxes: never a shorter prefix
-    assert jb[0] >= jf and jb[1] == jd
-    banded.close()
-    if t == -1.0:  # every source still inactive: all eligible (exact zero columns)
-        assert got == (len(src), len(src))
-    if t == 0.0:  # the long history: both paths carry sources
-        assert 0 < got[0] < len(src) and 0 < got[1] < len(src)
+    J, E = s.sumfact_plan(t)
+    R = s.sumfact_regions()
+    for r in range(len(R)):
+        assert (J[r], E[r]) == _plan(src, t, alpha, cull, R[r], min_pairs), (r, t)
+    if t == -1.0:  # every source still inactive: nothing to do anywhere
+        assert not J.any() and not E.any()
+    if t == 0.0 and min_pairs == 0.0:  # the long history: both paths carry sources
+        assert J.min() > 0 and (E > J).any()
     s.close()
