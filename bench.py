@@ -71,6 +71,7 @@ PIPE_OPS_PER_PAIR_PLANAR = 15.0
 # dominant kernel (profiles/r01_k1_ncu_summary.md, r01_k2_ncu_summary.md)
 K1_TRAFFIC_BYTES = 92.2e6 + 484.4e6   # k1_partial<7,1,1>, config 1, one launch
 K2_TRAFFIC_B_PER_DOF_ITER = 80.0      # k2_cg1_kernel<2> (scaled), config 4 (13.06 + 12.56 GB / 74 sweeps)
+K5_TRAFFIC_BYTES = 37.29e6 + 0.89e6   # sf_contract_kernel, config 4 step 1 (flux + Dirichlet)
 
 
 def parse():
@@ -87,9 +88,9 @@ def parse():
     ap.add_argument("--ncu", action="store_true", help="profiling run: no clocks/cpu legs")
     ap.add_argument("--theta-steps", type=int, default=3,
                     help="config-4 time steps for the theta-step section (0 = skip)")
-    ap.add_argument("--theta-sharded", type=int, default=0,
+    ap.add_argument("--theta-sharded", type=int, default=3,
                     help="config-4 time steps on all ranks with parallel.ShardedTimeLoop "
-                         "(sharded superposition + all-gathered loads; 0 = skip)")
+                         "(strong scaling of the whole step; 0 = skip)")
     return ap.parse_args()
 
 
@@ -354,6 +355,7 @@ def theta_section(steps, warmup, with_cpu):
     sim.reset()
     if warmup:
         sim.advance(warmup)
+    flops0 = sim.sumfact_stats()["gemm_flops"]
     ctx.set_profiling(True)
     ctx.profile(reset=True)
     t0 = time.perf_counter()
@@ -362,15 +364,19 @@ def theta_section(steps, warmup, with_cpu):
     prof = ctx.profile()
     ctx.set_profiling(False)
     sf = sim.sumfact_stats()
+    k5_flops = (sf["gemm_flops"] - flops0) / steps
+    dmma_peak = ctx.dmma_peak_tflops()
     # the same steps (same step indices, from a reset) with every
     # superposition pair on K1 (K5 off), for the split
     sim.set_sumfact(False)
     sim.reset()
     if warmup:
         sim.advance(warmup)
-    t1 = time.perf_counter()
+    ctx.set_profiling(True)
+    ctx.profile(reset=True)
     sim.advance(steps)
-    wall_k1 = time.perf_counter() - t1
+    prof_k1 = ctx.profile()
+    ctx.set_profiling(False)
     sim.set_sumfact(True)
     dofs = sim.info["n_full"]
     solver = {2: "single-sweep Chronopoulos-Gear Jacobi-PCG (one tile sweep + one grid "
@@ -381,11 +387,16 @@ def theta_section(steps, warmup, with_cpu):
     k2_ms = prof["k2_ms"] / steps
     peak, src = hbm_peak()
     achieved = prof["k2_bytes"] / (prof["k2_ms"] * 1e-3) / 1e9 if prof["k2_ms"] else None
+    k5_ms = prof["k5_ms"] / steps
+    k5_tf = k5_flops / (k5_ms * 1e-3) / 1e12 if k5_ms else None
     out = {
         "workload": "config4: 256x256x64 degree-2 cuboid (4,393,224 DOF), 1e5 sources, "
                     "theta = 0.5, dt = 1e-5, solver_tol 1e-10",
         "steps": steps, "warmup": warmup, "setup_s": setup_s,
-        "ms_per_step": wall * 1e3 / steps,
+        "ms_per_step": prof["step_ms"] / steps,
+        "ms_per_step_wall": wall * 1e3 / steps,
+        "timing": "ms_per_step: CUDA events on the simulation stream around the "
+                  "tg_sim_advance(steps) call (loads + theta steps, no host sync between steps)",
         "theta_ms_per_step": k2_ms,
         "theta_ms_per_step_per_mdof": k2_ms / (dofs / 1e6),
         "theta_step_total_ms_per_step": prof["theta_step_ms"] / steps,
@@ -394,14 +405,25 @@ def theta_section(steps, warmup, with_cpu):
                                  "step: expand + theta RHS + solve (theta_step, "
                                  "timestep.cpp:5-24); theta_ms_* are the solve alone",
         "k1_ms_per_step": prof["k1_ms"] / steps,
-        "k5": {"note": "sum-factorised superposition (csrc/k5_sumfact.cu): flux load and "
-                       "Dirichlet values over the sources no cull reaches on the face / "
-                       "Greville grids as cuBLAS DGEMMs (FP64 tensor cores); K1 keeps the "
-                       "rest (k1_ms_per_step)",
-               "sources_on_gemm": sf["last_j_flux"], "sources": sim.info["n_sources"],
-               "gemm_flops_per_step": sf["gemm_flops"] / (warmup + steps + 1),
-               "ms_per_step_with_k1_only": wall_k1 * 1e3 / steps,
-               "k1_pairs_per_step_moved": sf["pairs_off_k1"] / (warmup + steps + 1)},
+        "k5": {"note": "fused sum-factorised superposition (csrc/k5_fused.cu): the flux-load and "
+                       "Dirichlet sums over the sources no cull reaches in each region, as an "
+                       "on-chip exponential generator + DMMA m8n8k4 contraction; the pair-wise "
+                       "remainder on K1 (k1_ms_per_step)",
+               "kernel": "sf_contract_kernel",
+               "contraction_ms_per_step": k5_ms,
+               "contraction_flops_per_step": k5_flops,
+               "roofline": {"bound": "fp64 tensor (DMMA)", "achieved": k5_tf,
+                            "peak": dmma_peak, "unit": "TFLOP/s",
+                            "frac": k5_tf / dmma_peak if (k5_tf and dmma_peak) else None,
+                            "peak_source": "measured live: tg_dmma_peak (independent DMMA "
+                                           "m8n8k4 accumulators) on this GPU",
+                            "traffic": K5_TRAFFIC_BYTES,
+                            "traffic_source": "ncu --set full, profiles/r02_k5_ncu_summary.md "
+                                              "(dram read + write per launch)"},
+               "min_region_prefix_flux": sf["last_j_flux"],
+               "min_region_prefix_dirichlet": sf["last_j_dirichlet"],
+               "sources": sim.info["n_sources"],
+               "ms_per_step_with_k1_only": prof_k1["step_ms"] / steps},
         "cg_iterations_per_step": iters / steps,
         "solver": solver,
         "roofline": {"kernel": kernel, "bound": "hbm",
@@ -415,9 +437,10 @@ def theta_section(steps, warmup, with_cpu):
                      "bytes_per_dof_per_iteration": 104},
     }
     out["cpu_baseline"] = {
-        "note": "the reference cannot be timed per step on config 4 inside this bench (its "
-                "setup assembles ~57 GB of CSR / element matrices in minutes); the "
-                "reference's warm-started step on config 2 is config2_run.cpu_baseline"}
+        "note": "the reference's own step on config 4 takes ~5 min of host time (138 s setup, "
+                "85 s threaded flux load, 66 s serial PCG for one theta step; "
+                "profiles/r02_cfg4_ref_theta.md), too long for this bench; the reference's "
+                "warm-started step on config 2 is config2_run.cpu_baseline"}
     sim.close()
     try:
         out["fdm_option"] = theta_fdm(steps, warmup)
@@ -435,44 +458,39 @@ def theta_section(steps, warmup, with_cpu):
 
 
 def theta_sharded_section(steps, rank, world, local):
-    """Config-4 time steps on all ranks: the superposition work (flux-load
-    element slabs, Dirichlet point slabs) split across GPUs and all-gathered,
-    the theta step replicated (strong scaling of the whole step).
-    Wall time per step between barriers, max over ranks."""
+    """Config-4 time steps on all ranks (strong scaling of the whole step):
+    the loads' K5 regions and the θ-step's z-slabs split over the GPUs
+    (parallel.ShardedTimeLoop -> tg_sim_shard; one rank: plain advance).
+    Device time per step (CUDA events around tg_sim_advance on each rank's
+    simulation stream), max over ranks."""
     import torch
     import paper_2511_20432_b200 as tg
     from paper_2511_20432_b200 import parallel
     import torch.distributed as dist
-    own_pg = world == 1 and not dist.is_initialized()
-    if own_pg:
-        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        os.environ.setdefault("MASTER_PORT", "29631")
-        dist.init_process_group("nccl", rank=0, world_size=1)
-    try:
-        sim = tg.Simulation(THETA_CFG, device=local)
-        loop = parallel.ShardedTimeLoop(sim, parallel.Dist(rank, world, f"cuda:{local}"))
-        loop.reset()
-        loop.step()
-        dist.barrier()
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        its = 0
-        for _ in range(steps):
-            its += loop.step()[0]
-        torch.cuda.synchronize()
-        dist.barrier()
-        ms = torch.tensor([(time.perf_counter() - t0) * 1e3 / steps], dtype=torch.float64,
-                          device=f"cuda:{local}")
+    sim = tg.Simulation(THETA_CFG, device=local)
+    loop = parallel.ShardedTimeLoop(sim, parallel.Dist(rank, world, f"cuda:{local}"))
+    ctx = sim.context()
+    loop.reset()
+    loop.step(2)
+    ctx.set_profiling(True)
+    ctx.profile(reset=True)
+    its, _ = loop.step(steps)
+    prof = ctx.profile()
+    ctx.set_profiling(False)
+    ms = torch.tensor([prof["step_ms"] / steps], dtype=torch.float64, device=f"cuda:{local}")
+    if world > 1:
         dist.all_reduce(ms, op=dist.ReduceOp.MAX)
-        sim.close()
-        return {"workload": "config4 time steps, superposition sharded over "
-                            f"{world} GPU(s), loads all-gathered, theta step replicated",
-                "n_gpus": world, "steps": steps, "ms_per_step": float(ms.item()),
-                "cg_iterations_per_step": its / steps,
-                "timing": "wall clock between barriers, max over ranks"}
-    finally:
-        if own_pg:
-            dist.destroy_process_group()
+    st = sim.state()
+    sim.close()
+    return {"workload": f"config4 time steps on {world} GPU(s): K5 regions and theta-step "
+                        "z-slabs split over the ranks (NCCL all-reduce of the loads, halo + "
+                        "partial-sum exchange per CG iteration)" if world > 1 else
+                        "config4 time steps on 1 GPU (no split)",
+            "n_gpus": world, "steps": steps, "ms_per_step": float(ms.item()),
+            "cg_iterations_per_step": its / steps,
+            "state_checksum": float(np.abs(st["free"]).sum()),
+            "timing": "CUDA events around tg_sim_advance on each rank's stream, max over ranks",
+            "scaling": "strong"}
 
 
 def theta_fdm(steps, warmup):

@@ -76,12 +76,14 @@ const char* tg_last_error(const tg_ctx* ctx);
  * reset, the number of this library's kernel launches, and the work counted:
  * out = {k1_ms, k1_launches, k1_pairs, k2_ms (solve), k2_launches, k2_bytes,
  *        launches, theta_step_ms (expand + RHS + solve), k5_ms (contraction),
- *        k5_launches}. */
+ *        k5_launches, run_ms (whole tg_sim_advance steps: loads + theta step)}. */
 int tg_set_profiling(tg_ctx* ctx, int on);
-int tg_profile_read(tg_ctx* ctx, double* out /* [10] */, int reset);
+int tg_profile_read(tg_ctx* ctx, double* out /* [11] */, int reset);
 /* FP64 issue-rate microbenchmark (independent DFMA chains over every SM);
  * the K1 roofline denominator. */
 int tg_fp64_peak(tg_ctx* ctx, double* out_tflops);
+/* Measured FP64 tensor-core (DMMA m8n8k4) rate of this GPU, TFLOP/s. */
+int tg_dmma_peak(tg_ctx* ctx, double* out_tflops);
 
 /* ---- analytic field (K1) ---------------------------------------------- */
 
@@ -156,9 +158,12 @@ int tg_sim_kron_factors(tg_sim* sim, int dir, double* M, double* K);
  * assembled). */
 long tg_sim_reduced_operator(tg_sim* sim, int* rows, int* row_ptr, int* col, double* val);
 
-/* assemble_flux_load (proj/src/assembly.cpp:148-166): F (n_full) at time t;
- * fine_radius < 0 uses the config's elevate_radius. */
-int tg_sim_flux_load(tg_sim* sim, double t, double fine_radius, double* out_F);
+/* assemble_flux_load (proj/src/assembly.cpp:148-166): F (n_full) at time t.
+ * focus_xyz (nullable): the fine-rule focus; NULL = the newest source active
+ * at t (assembly.cpp:153-157). fine_radius < 0 uses the config's
+ * elevate_radius. */
+int tg_sim_flux_load(tg_sim* sim, double t, const double* focus_xyz, double fine_radius,
+                     double* out_F);
 /* dirichlet_values (proj/src/mesh.cpp:238-264): g (n_constrained) at time t. */
 int tg_sim_dirichlet_values(tg_sim* sim, double t, double* out_g);
 /* theta_step (proj/src/timestep.cpp:5-24) with pcg_jacobi
@@ -171,32 +176,15 @@ int tg_sim_theta_step(tg_sim* sim, const double* free_n, const double* g_n, cons
  * proj/include/thermiga/assembly.hpp:56). */
 int tg_sim_operator_apply(tg_sim* sim, const double* x_free, double* y_free);
 
-/* ---- sharding support (paper_2511_20432_b200/parallel.py) ---------------
- * Face-element slabs: local loads loc[e][a] of elements [e0, e1) computed on
- * this GPU ((e1 - e0) x n_dofs_kept doubles, device memory), and the
- * deterministic gather of all elements' loads into F (reference scatter
- * order, assembly.cpp:141-144), so all-gathered slabs reproduce the
- * single-GPU load bit for bit. */
-int tg_sim_flux_local_device(tg_sim* sim, double t, double fine_radius, int e0, int e1,
-                             double* d_loc);
-int tg_sim_flux_gather_device(tg_sim* sim, const double* d_loc_all, double* d_F);
-/* z-slab of the reduced operator: y (planes [k0, k1) of the free grid) =
- * A_ff x, with x given on planes [max(0, k0 - p), min(nz, k1 + p)) (ghost
- * planes included). Kronecker patches only. Device pointers; synchronous. */
-int tg_sim_operator_apply_slab_device(tg_sim* sim, int k0, int k1, const double* d_x,
-                                      double* d_y);
-/* Dirichlet values of the constrained DOFs [c0, c1) at t (device output of
- * c1 - c0 values, synchronous); ranges of a point split reproduce the full
- * call bit for bit. */
-int tg_sim_dirichlet_range_device(tg_sim* sim, double t, int c0, int c1, double* d_g);
-/* One time step with F_{n+1} (n_full) and g_{n+1} (n_constrained) supplied as
- * device arrays — the step of a driver that assembles the loads sharded and
- * all-gathers them; otherwise as tg_sim_advance(sim, 1, ...). */
-int tg_sim_advance_with_loads_device(tg_sim* sim, const double* d_F1, const double* d_g1,
-                                     long* cg_iterations, double* rel);
-
-/* 1 / diag(A_ff) (the Jacobi preconditioner, sparse.cpp:47-52), host copy. */
-int tg_sim_inverse_diagonal(tg_sim* sim, double* out);
+/* The compact flux integrand of the last flux-load call (the per-point
+ * (-k grad T~ . n) w of assemble_boundary_load, assembly.cpp:133-135, in the
+ * device's element order: base rules, fine rules of the step's fine
+ * elements): returns the point count (pass NULL to query). */
+long tg_sim_last_integrand(tg_sim* sim, double* out);
+/* Restrict the fused loads to the K5 regions r with r % world == rank (the
+ * split tg_sim_shard uses; a test hook to check that the ranks' integrands
+ * and Dirichlet values sum to the unsplit ones bit for bit). */
+int tg_sim_set_region_split(tg_sim* sim, int rank, int world);
 
 /* Diagnostics: %globaltimer stamps of CTA 0 at the K2 phase boundaries of the
  * first 16 CG iterations of the last solve (5 per iteration; recorded only
@@ -275,6 +263,22 @@ int tg_sim_set_sumfact(tg_sim* sim, int on);
  * prefix J (the smallest over the flux regions; over the Greville regions),
  * contraction flops issued since setup, regions, sources per work item */
 int tg_sim_sumfact_stats(tg_sim* sim, double* out);
+/* ---- multi-GPU (one process per GPU; proj/src/driver.cpp:126-145 per rank).
+ * tg_nccl_unique_id: rank 0 creates the communicator id (128 bytes) that the
+ * caller hands to every rank (e.g. a torch.distributed broadcast).
+ * tg_sim_shard: join the NCCL communicator as rank of world; from then on
+ * tg_sim_advance splits the superposition regions over the ranks (loads
+ * all-reduced) and the θ-step solve into z-slabs of the free grid (ghost
+ * planes and the dot products' partial sums exchanged every iteration, x
+ * broadcast after the solve): every rank ends each step with the same state.
+ * tg_sim_set_slabs: the same slab solve with n slabs on this one GPU, halos
+ * exchanged by device copies (n <= 1: off).
+ * tg_slab_plan (host only): out6 = local first global plane, local planes,
+ * own planes [zo0, zo1) in local indices, lower / upper neighbour (-1: none). */
+int tg_nccl_unique_id(char* out128);
+int tg_sim_shard(tg_sim* sim, int rank, int world, const char* id128);
+int tg_sim_set_slabs(tg_sim* sim, int n);
+int tg_slab_plan(int nz, int p, int world, int rank, int* out6);
 /* K5 regions (one per contraction tile of the face grids, then of the
  * Greville grid): out (n_regions x 8) = lo[3], hi[3], delta, points. */
 int tg_sim_sumfact_regions(tg_sim* sim, double* out);

@@ -242,7 +242,7 @@ class Simulation {
   // assemble_flux_load (assembly.hpp:37-40); fine_radius < 0: config value
   void assemble_flux_load(double t, double fine_radius, std::vector<double>& load) {
     load.resize(n_full);
-    check(tg_sim_flux_load(get(), t, fine_radius, load.data()));
+    check(tg_sim_flux_load(get(), t, nullptr, fine_radius, load.data()));
   }
   // dirichlet_values (mesh.hpp:121-125)
   std::vector<double> dirichlet_values(double t) {
@@ -319,6 +319,31 @@ class Simulation {
     return A;
   }
 
+  // the discretized history and material the simulation's config defines
+  std::vector<PointSource> sources() const {
+    long info[18];
+    raise(tg_sim_info(get(), info), tg_sim_last_error(get()));
+    std::vector<PointSource> out(info[4]);
+    raise(tg_sim_sources(get(), out.data(), static_cast<int>(out.size())),
+          tg_sim_last_error(get()));
+    return out;
+  }
+  Material material() const {
+    double par[10];
+    raise(tg_sim_params(get(), par), tg_sim_last_error(get()));
+    Material m{};
+    m.conductivity = par[5];
+    m.density = par[6];
+    m.heat_capacity = par[7];
+    m.platform_temperature = par[8];
+    return m;
+  }
+  SuperposeOptions superpose_options() const {
+    double par[10];
+    raise(tg_sim_params(get(), par), tg_sim_last_error(get()));
+    return SuperposeOptions{par[4]};
+  }
+
   long n_full = 0, n_free = 0, n_constrained = 0;
   int n_steps = 0, max_iter = 5000;
   double dt_solver = 0.0, tol = 1e-10;
@@ -336,5 +361,60 @@ class Simulation {
   };
   std::unique_ptr<tg_sim, Del> sim_;
 };
+
+// ---- the reference's free-function hot path (assembly.hpp:37-40,
+// mesh.hpp:121-125, timestep.hpp:26-29) over the simulation's device data:
+// BoundarySets stands for its lateral face quadrature sets, DirichletSystem
+// for its θ-scheme operator. The history is the one the simulation's config
+// discretized (it is resident in HBM); sources / mat / opts are checked
+// against it rather than re-uploaded.
+struct BoundarySets {
+  Simulation* sim;
+};
+struct DirichletSystem {
+  Simulation* sim;
+};
+inline BoundarySets boundary_sets(Simulation& s) { return {&s}; }
+inline DirichletSystem dirichlet_system(Simulation& s) { return {&s}; }
+
+namespace detail {
+inline void same_history(const Simulation& s, const std::vector<PointSource>& src,
+                         const Material& mat, const SuperposeOptions& opts) {
+  long info[18];
+  raise(tg_sim_info(s.get(), info), tg_sim_last_error(s.get()));
+  double par[10];
+  raise(tg_sim_params(s.get(), par), tg_sim_last_error(s.get()));
+  if (static_cast<long>(src.size()) != info[4] || mat.conductivity != par[5] ||
+      mat.density != par[6] || mat.heat_capacity != par[7] || opts.cull_exponent != par[4])
+    throw std::invalid_argument(
+        "sources / material / options differ from the simulation's (resident on the device)");
+}
+}  // namespace detail
+
+// assemble_flux_load (assembly.hpp:37-40); the fine rule follows the newest
+// source active at t; n_threads is accepted and ignored (core.cpp:67-85)
+inline void assemble_flux_load(const BoundarySets& b, const std::vector<PointSource>& sources,
+                               const Material& mat, double t, double fine_radius,
+                               std::vector<double>& load, const SuperposeOptions& opts = {},
+                               int n_threads = 1) {
+  (void)n_threads;
+  detail::same_history(*b.sim, sources, mat, opts);
+  b.sim->assemble_flux_load(t, fine_radius, load);
+}
+// dirichlet_values (mesh.hpp:121-125)
+inline std::vector<double> dirichlet_values(const BoundarySets& b,
+                                            const std::vector<PointSource>& sources,
+                                            const Material& mat, double t,
+                                            const SuperposeOptions& opts = {}) {
+  detail::same_history(*b.sim, sources, mat, opts);
+  return b.sim->dirichlet_values(t);
+}
+// theta_step (timestep.hpp:26-29)
+inline State theta_step(const DirichletSystem& sys, const State& s,
+                        const std::vector<double>& load_n, const std::vector<double>& load_np1,
+                        const std::vector<double>& constrained_np1, const PcgOptions& o,
+                        PcgResult* stats = nullptr) {
+  return sys.sim->theta_step(s, load_n, load_np1, constrained_np1, o, stats);
+}
 
 }  // namespace thermiga_b200

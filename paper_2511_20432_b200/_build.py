@@ -31,10 +31,10 @@ COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler",
 NO_FMAD = {"k4_eval.cu"}
 
 
-# cuBLAS (plain library GEMMs of the fast-diagonalization preconditioner)
+# the CUDA runtime is linked statically; no CUDA math library is needed
 CUDA_LIB = os.path.join(os.path.dirname(os.path.dirname(os.path.realpath(
     __import__("shutil").which(NVCC) or "/usr/local/cuda/bin/nvcc"))), "lib64")
-LINK = ["-L" + CUDA_LIB, "-lcublas", "-Xlinker", "-rpath=" + CUDA_LIB]
+LINK = ["-L" + CUDA_LIB, "-ldl", "-Xlinker", "-rpath=" + CUDA_LIB]
 
 
 def _sources():

@@ -121,6 +121,14 @@ def lib(auto_build: bool = True):
     path = os.environ.get("TG_LIB_VARIANT") or _build.LIB  # tuning builds (tools/k1_variants.py)
     if not os.path.exists(path):
         raise CudaError(f"native library missing: {path}")
+    if "TG_NCCL_LIB" not in os.environ:  # the multi-GPU path binds torch's NCCL if present
+        import importlib.util
+        spec = importlib.util.find_spec("torch")
+        if spec and spec.origin:
+            cand = os.path.join(os.path.dirname(os.path.dirname(spec.origin)), "nvidia", "nccl",
+                                "lib", "libnccl.so.2")
+            if os.path.exists(cand):
+                os.environ["TG_NCCL_LIB"] = cand
     L = C.CDLL(path)
     L.tg_abi_version.restype = C.c_int
     L.tg_ctx_create.argtypes = [C.c_int, C.POINTER(C.c_void_p)]
@@ -130,6 +138,7 @@ def lib(auto_build: bool = True):
     L.tg_set_profiling.argtypes = [C.c_void_p, C.c_int]
     L.tg_profile_read.argtypes = [C.c_void_p, _dp, C.c_int]
     L.tg_fp64_peak.argtypes = [C.c_void_p, _dp]
+    L.tg_dmma_peak.argtypes = [C.c_void_p, _dp]
     L.tg_pcg_jacobi.argtypes = [C.c_void_p, C.c_int, _ip, _ip, _dp, _dp, _dp, C.c_double, C.c_int,
                                 _ip, _dp]
     L.tg_csr_multiply.argtypes = [C.c_void_p, C.c_int, _ip, _ip, _dp, _dp, _dp]
@@ -219,11 +228,12 @@ class Context:
         self._check(self._L.tg_set_profiling(self._h, int(on)))
 
     def profile(self, reset: bool = False) -> dict:
-        out = np.zeros(10)
+        out = np.zeros(11)
         self._check(self._L.tg_profile_read(self._h, _p(out), int(reset)))
         return dict(k1_ms=out[0], k1_launches=int(out[1]), k1_pairs=out[2], k2_ms=out[3],
                     k2_launches=int(out[4]), k2_bytes=out[5], launches=int(out[6]),
-                    theta_step_ms=out[7], k5_ms=out[8], k5_launches=int(out[9]))
+                    theta_step_ms=out[7], k5_ms=out[8], k5_launches=int(out[9]),
+                    step_ms=out[10])
 
     @staticmethod
     def _csr(A):
@@ -276,6 +286,12 @@ class Context:
     def fp64_peak_tflops(self) -> float:
         out = C.c_double(0.0)
         self._check(self._L.tg_fp64_peak(self._h, C.byref(out)))
+        return out.value
+
+    def dmma_peak_tflops(self) -> float:
+        """Measured FP64 tensor-core rate (DMMA m8n8k4, independent accumulators)."""
+        out = C.c_double(0.0)
+        self._check(self._L.tg_dmma_peak(self._h, C.byref(out)))
         return out.value
 
     # -- K1 -------------------------------------------------------------------
@@ -356,7 +372,7 @@ def _bind_sim(L):
     L.tg_sim_kron_factors.argtypes = [C.c_void_p, C.c_int, _dp, _dp]
     L.tg_sim_reduced_operator.argtypes = [C.c_void_p, _ip, _ip, _ip, _dp]
     L.tg_sim_reduced_operator.restype = C.c_long
-    L.tg_sim_flux_load.argtypes = [C.c_void_p, C.c_double, C.c_double, _dp]
+    L.tg_sim_flux_load.argtypes = [C.c_void_p, C.c_double, _dp, C.c_double, _dp]
     L.tg_sim_dirichlet_values.argtypes = [C.c_void_p, C.c_double, _dp]
     L.tg_sim_theta_step.argtypes = [C.c_void_p, _dp, _dp, _dp, _dp, _dp, C.c_double, C.c_int,
                                     _dp, _ip, _dp]
@@ -371,6 +387,11 @@ def _bind_sim(L):
     L.tg_sim_set_sumfact.argtypes = [C.c_void_p, C.c_int]
     L.tg_sim_sumfact_stats.argtypes = [C.c_void_p, _dp]
     L.tg_sim_sumfact_regions.argtypes = [C.c_void_p, _dp]
+    L.tg_sim_shard.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_char_p]
+    L.tg_sim_set_slabs.argtypes = [C.c_void_p, C.c_int]
+    L.tg_sim_last_integrand.restype = C.c_long
+    L.tg_sim_last_integrand.argtypes = [C.c_void_p, _dp]
+    L.tg_sim_set_region_split.argtypes = [C.c_void_p, C.c_int, C.c_int]
     L.tg_sim_sumfact_plan.argtypes = [C.c_void_p, C.c_double, _ip, _ip]
     L.tg_sim_sumfact_last_plan.argtypes = [C.c_void_p, _ip, _ip]
     L._sim_bound = True
@@ -476,6 +497,31 @@ class Simulation:
                     last_j_flux=int(out[3]), last_j_dirichlet=int(out[4]), gemm_flops=out[5],
                     regions=int(out[6]), item=int(out[7]))
 
+    def shard(self, rank: int, world: int, nccl_id: bytes):
+        """Join the NCCL communicator `nccl_id` (nccl_unique_id() on rank 0)
+        as rank of world: the loads' regions and the θ-step's z-slabs are then
+        split over the ranks (tg_sim_shard)."""
+        self._check(self._L.tg_sim_shard(self._h, int(rank), int(world), bytes(nccl_id)))
+
+    def set_slabs(self, n: int):
+        """Run the θ-step solve as n z-slabs on this GPU (the multi-GPU
+        decomposition's local test bed; n <= 1 turns it off)."""
+        self._check(self._L.tg_sim_set_slabs(self._h, int(n)))
+
+    def last_integrand(self):
+        """The compact flux integrand of the last flux-load call (one value per
+        active face quadrature point, device element order)."""
+        n = self._L.tg_sim_last_integrand(self._h, None)
+        if n < 0:
+            raise _ERRORS.get(-n, ThermigaError)(self._L.tg_sim_last_error(self._h).decode())
+        out = np.zeros(n)
+        self._L.tg_sim_last_integrand(self._h, _p(out))
+        return out
+
+    def set_region_split(self, rank: int, world: int):
+        """Compute only the K5 regions r % world == rank (the multi-GPU split)."""
+        self._check(self._L.tg_sim_set_region_split(self._h, int(rank), int(world)))
+
     def sumfact_regions(self):
         """K5 regions (flux tiles, then Greville tiles): (n, 8) = lo[3], hi[3],
         delta, points."""
@@ -521,9 +567,13 @@ class Simulation:
         self._check(self._L.tg_sim_kron_factors(self._h, d, _p(M), _p(K)))
         return M, K
 
-    def flux_load(self, t, fine_radius=-1.0):
+    def flux_load(self, t, fine_radius=-1.0, focus=None):
+        """assemble_flux_load at t; focus (x, y, z) overrides the fine-rule focus
+        (default: the newest source active at t)."""
         F = np.zeros(self.info["n_full"])
-        self._check(self._L.tg_sim_flux_load(self._h, float(t), float(fine_radius), _p(F)))
+        fo = None if focus is None else _f64(focus)
+        self._check(self._L.tg_sim_flux_load(self._h, float(t), None if fo is None else _p(fo),
+                                             float(fine_radius), _p(F)))
         return F
 
     def dirichlet_values(self, t):
@@ -672,6 +722,27 @@ class Simulation:
         t = C.c_double(0.0)
         self._check(self._L.tg_sim_state(self._h, C.byref(step), C.byref(t), None, None, None))
         return t.value
+
+
+def nccl_unique_id() -> bytes:
+    """A new NCCL communicator id (128 bytes) for Simulation.shard."""
+    L = lib()
+    L.tg_nccl_unique_id.argtypes = [C.c_char_p]
+    buf = C.create_string_buffer(128)
+    rc = L.tg_nccl_unique_id(buf)
+    if rc != TG_OK:
+        raise CudaError("NCCL is not available (libnccl.so.2)")
+    return buf.raw
+
+
+def slab_plan(nz: int, p: int, world: int, rank: int) -> dict:
+    """The z-slab of one rank (host arithmetic, tg_slab_plan)."""
+    L = lib()
+    L.tg_slab_plan.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, _ip]
+    out = np.zeros(6, dtype=np.int32)
+    if L.tg_slab_plan(int(nz), int(p), int(world), int(rank), out.ctypes.data_as(_ip)) != TG_OK:
+        raise ValueError("slab plan: need nz / world >= p and 0 <= rank < world")
+    return dict(zip(("gz0", "nloc", "zo0", "zo1", "lo", "hi"), (int(v) for v in out)))
 
 
 def integrated_abs_flux(profile):

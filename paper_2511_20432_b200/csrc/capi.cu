@@ -193,6 +193,7 @@ int tg_profile_read(tg_ctx* ctx, double* out, int reset) {
     out[7] = ctx->timer.step_ms;  // whole theta steps (expand + RHS + solve)
     out[8] = ctx->timer.k5_ms;    // K5 contraction launches
     out[9] = static_cast<double>(ctx->timer.k5_launches);
+    out[10] = ctx->timer.run_ms;  // whole time steps (tg_sim_advance), device events
     if (reset) ctx->timer.reset();
   });
 }

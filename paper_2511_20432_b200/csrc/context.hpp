@@ -64,8 +64,9 @@ struct KernelTimer {
   bool on = false;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> live;  // pending pairs
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pool;
-  // kinds 1 (K1 main), 2 (K2 main), 3 (whole theta step), 5 (K5 contraction)
-  double k1_ms = 0.0, k2_ms = 0.0, step_ms = 0.0, k5_ms = 0.0;
+  // kinds 1 (K1 main), 2 (K2 main), 3 (whole theta step), 4 (whole time
+  // steps: loads + theta step), 5 (K5 contraction)
+  double k1_ms = 0.0, k2_ms = 0.0, step_ms = 0.0, k5_ms = 0.0, run_ms = 0.0;
   std::vector<int> kinds;
   double k1_pairs = 0.0, k2_bytes = 0.0;
   long launches = 0, k1_launches = 0, k2_launches = 0, k5_launches = 0;
@@ -100,7 +101,8 @@ struct KernelTimer {
       TG_CUDA(cudaEventSynchronize(live[i].second));
       float ms = 0.f;
       TG_CUDA(cudaEventElapsedTime(&ms, live[i].first, live[i].second));
-      (kinds[i] == 1 ? k1_ms : kinds[i] == 2 ? k2_ms : kinds[i] == 5 ? k5_ms : step_ms) += ms;
+      (kinds[i] == 1 ? k1_ms : kinds[i] == 2 ? k2_ms : kinds[i] == 5 ? k5_ms
+                                     : kinds[i] == 4 ? run_ms : step_ms) += ms;
       pool.push_back(live[i]);
     }
     live.clear();
@@ -108,7 +110,7 @@ struct KernelTimer {
   }
   void reset() {
     collect();
-    k1_ms = k2_ms = step_ms = k5_ms = 0.0;
+    k1_ms = k2_ms = step_ms = k5_ms = run_ms = 0.0;
     k1_pairs = k2_bytes = 0.0;
     launches = k1_launches = k2_launches = k5_launches = 0;
   }

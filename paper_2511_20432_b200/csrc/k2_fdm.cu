@@ -5,9 +5,13 @@
 // P = V diag(1 / (a + b (lx + ly + lz))) V^T, V = Vz x Vy x Vx with
 // K_d V_d = M_d V_d diag(l_d), V_d^T M_d V_d = I (host/fdm.cpp), is A^-1 up to
 // rounding, so the reference's PCG loop stops after one or two iterations
-// instead of ~64-170 with Jacobi. Applying P is six dense mode products (plain
-// library GEMMs: cuBLAS DGEMM on the FP64 tensor cores) and one scaling; the
-// operator apply is the sum-factorized TMA kernel of k2_kron.cu.
+// instead of ~64-170 with Jacobi. Applying P is six dense mode products
+// (mode_gemm below: a strided-batched DMMA m8n8k4 GEMM on the FP64 tensor
+// cores) and one scaling; the operator apply is the sum-factorized TMA kernel
+// of k2_kron.cu (separable patches) or the sliced-ELL product of k2_csr.cu.
+#include <functional>
+
+#include "common.cuh"
 #include "context.hpp"
 #include "k2_fdm.cuh"
 
@@ -15,11 +19,83 @@ namespace tgb {
 
 namespace {
 
-void cublas_check(cublasStatus_t st, const char* what) {
-  if (st != CUBLAS_STATUS_SUCCESS)
-    throw cuda_error(std::string("cublas: ") + what + " failed (" + std::to_string(st) + ")");
+// ---------------------------------------------------------------- mode GEMM
+// C(m, n) = sum_k A(m, k) B(k, n) for a batch of independent products, every
+// operand addressed through (row, column, batch) strides so that the six mode
+// products of the preconditioner need no transposes. 64 x 64 output tile per
+// CTA, 4 warps of 32 x 32 (DMMA m8n8k4), 16-wide k chunks staged in shared
+// memory by coalesced loads along whichever index is contiguous.
+struct GemmOp {
+  int M, N, K, batch;
+  const double* A;
+  long sam, sak, sab;
+  const double* B;
+  long sbk, sbn, sbb;
+  double* C;
+  long scm, scn, scb;
+};
+constexpr int kGT = 64, kGK = 16, kGLd = kGK + 4;
+
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+      : "+d"(c0), "+d"(c1)
+      : "d"(a), "d"(b));
 }
-#define TG_CUBLAS(call) cublas_check((call), #call)
+
+__global__ void __launch_bounds__(128) mode_gemm_kernel(GemmOp op) {
+  __shared__ double As[kGT][kGLd];
+  __shared__ double Bs[kGT][kGLd];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g8 = lane >> 2, q4 = lane & 3;
+  const int wm = (warp & 1) * 32, wn = (warp >> 1) * 32;
+  const int m0 = blockIdx.x * kGT, n0 = blockIdx.y * kGT, bz = blockIdx.z;
+  const double* A = op.A + bz * op.sab;
+  const double* B = op.B + bz * op.sbb;
+  double acc[4][4][2] = {};
+  const bool a_kfast = op.sak == 1, b_kfast = op.sbk == 1;
+  for (int k0 = 0; k0 < op.K; k0 += kGK) {
+    for (int e = tid; e < kGT * kGK; e += 128) {  // A tile (m, k)
+      const int m = a_kfast ? e / kGK : e % kGT, k = a_kfast ? e % kGK : e / kGT;
+      const int gm = m0 + m, gk = k0 + k;
+      As[m][k] = (gm < op.M && gk < op.K) ? A[gm * op.sam + gk * op.sak] : 0.0;
+    }
+    for (int e = tid; e < kGT * kGK; e += 128) {  // B tile, stored (n, k)
+      const int n = b_kfast ? e / kGK : e % kGT, k = b_kfast ? e % kGK : e / kGT;
+      const int gn = n0 + n, gk = k0 + k;
+      Bs[n][k] = (gn < op.N && gk < op.K) ? B[gk * op.sbk + gn * op.sbn] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < kGK; kk += 4) {
+      double af[4], bf[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) af[i] = As[wm + 8 * i + g8][kk + q4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) bf[j] = Bs[wn + 8 * j + g8][kk + q4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+    }
+    __syncthreads();
+  }
+  double* C = op.C + bz * op.scb;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int gm = m0 + wm + 8 * i + g8, gn = n0 + wn + 8 * j + 2 * q4 + h;
+        if (gm < op.M && gn < op.N) C[gm * op.scm + gn * op.scn] = acc[i][j][h];
+      }
+}
+
+void mode_gemm(const GemmOp& op, cudaStream_t s) {
+  dim3 grid((op.M + kGT - 1) / kGT, (op.N + kGT - 1) / kGT, op.batch);
+  mode_gemm_kernel<<<grid, 128, 0, s>>>(op);
+  TG_CUDA(cudaGetLastError());
+}
 
 constexpr int kDotBlocks = 512;
 constexpr int kDotThreads = 256;
@@ -127,6 +203,18 @@ int grid_for(long n) {
   return static_cast<int>(std::min<long>(4096, std::max<long>(1, (n + 255) / 256)));
 }
 
+__global__ void diag_mul_kernel(long n, const double* __restrict__ d, const double* x,
+                                double* y) {
+  for (long f = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; f < n;
+       f += static_cast<long>(gridDim.x) * blockDim.x)
+    y[f] = d[f] * x[f];
+}
+
+void diag_mul(long n, const double* d, const double* x, double* y, cudaStream_t s) {
+  diag_mul_kernel<<<grid_for(n), 256, 0, s>>>(n, d, x, y);
+  TG_CUDA(cudaGetLastError());
+}
+
 // (a.b, c.d) on the host (synchronous)
 void dot2(long n, const double* a, const double* b, const double* c, const double* d,
           const FdmWork& w, cudaStream_t s, double& o0, double& o1) {
@@ -147,36 +235,36 @@ void fdm_inverse_eigs(const int n[3], const double* lx, const double* ly, const 
   TG_CUDA(cudaGetLastError());
 }
 
-void fdm_apply(cublasHandle_t h, const FdmDev& F, const double* r, double* z, double* t1,
-               double* t2, cudaStream_t s) {
+void fdm_apply(const FdmDev& F, const double* r, double* z, double* t1, double* t2,
+               cudaStream_t s) {
   const int nx = F.n[0], ny = F.n[1], nz = F.n[2];
   const long nxy = static_cast<long>(nx) * ny;
-  const double one = 1.0, zero = 0.0;
-  TG_CUBLAS(cublasSetStream(h, s));
-  // V^T r: x (t1 = Vx^T R), y (t2_k = t1_k Vy), z (t1 = t2 Vz)
-  TG_CUBLAS(cublasDgemm(h, CUBLAS_OP_T, CUBLAS_OP_N, nx, ny * nz, nx, &one, F.V[0], nx, r, nx,
-                        &zero, t1, nx));
-  TG_CUBLAS(cublasDgemmStridedBatched(h, CUBLAS_OP_N, CUBLAS_OP_N, nx, ny, ny, &one, t1, nx, nxy,
-                                      F.V[1], ny, 0, &zero, t2, nx, nxy, nz));
-  TG_CUBLAS(cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_N, static_cast<int>(nxy), nz, nz, &one, t2,
-                        static_cast<int>(nxy), F.V[2], nz, &zero, t1, static_cast<int>(nxy)));
+  const double *Vx = F.V[0], *Vy = F.V[1], *Vz = F.V[2];  // column-major: V(a, b) = V[a + n b]
+  const double* in = r;
+  if (F.sinv) {  // z = S^-1 P S^-1 r (diagonally scaled approximation, general patches)
+    diag_mul(nxy * nz, F.sinv, r, z, s);
+    in = z;
+  }
+  // V^T r: t1[k][j][b] = sum_a Vx(a, b) r[k][j][a]; t2[k][b][i] = sum_a Vy(a, b) t1[k][a][i];
+  //        t1[b][j][i] = sum_a Vz(a, b) t2[a][j][i]
+  mode_gemm({ny * nz, nx, nx, 1, in, nx, 1, 0, Vx, 1, nx, 0, t1, nx, 1, 0}, s);
+  mode_gemm({ny, nx, ny, nz, Vy, ny, 1, 0, t1, nx, 1, nxy, t2, nx, 1, nxy}, s);
+  mode_gemm({nz, static_cast<int>(nxy), nz, 1, Vz, nz, 1, 0, t2, nxy, 1, 0, t1, nxy, 1, 0}, s);
   const long N = nxy * nz;
   scale_kernel<<<grid_for(N), 256, 0, s>>>(N, F.dinv, t1);
   TG_CUDA(cudaGetLastError());
-  // V w: z (t2 = t1 Vz^T), y (t1_k = t2_k Vy^T), x (z = Vx t1)
-  TG_CUBLAS(cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_T, static_cast<int>(nxy), nz, nz, &one, t1,
-                        static_cast<int>(nxy), F.V[2], nz, &zero, t2, static_cast<int>(nxy)));
-  TG_CUBLAS(cublasDgemmStridedBatched(h, CUBLAS_OP_N, CUBLAS_OP_T, nx, ny, ny, &one, t2, nx, nxy,
-                                      F.V[1], ny, 0, &zero, t1, nx, nxy, nz));
-  TG_CUBLAS(cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_N, nx, ny * nz, nx, &one, F.V[0], nx, t1, nx,
-                        &zero, z, nx));
+  // V w: t2[a][j][i] = sum_b Vz(a, b) t1[b][j][i]; t1[k][a][i] = sum_b Vy(a, b) t2[k][b][i];
+  //      z[k][j][a] = sum_b Vx(a, b) t1[k][j][b]
+  mode_gemm({nz, static_cast<int>(nxy), nz, 1, Vz, 1, nz, 0, t1, nxy, 1, 0, t2, nxy, 1, 0}, s);
+  mode_gemm({ny, nx, ny, nz, Vy, 1, ny, 0, t2, nx, 1, nxy, t1, nx, 1, nxy}, s);
+  mode_gemm({ny * nz, nx, nx, 1, t1, nx, 1, 0, Vx, nx, 1, 0, z, nx, 1, 0}, s);
+  if (F.sinv) diag_mul(N, F.sinv, z, z, s);
 }
 
-PcgStatus fdm_pcg_solve(cublasHandle_t h, const KronGrid& g, double a, double b, const FdmDev& F,
-                        const double* rhs, double* x, const FdmWork& w, double tol, int max_iter,
-                        int sm_count, cudaStream_t s, const TensorMap3* x_map,
-                        const TensorMap3* p_map) {
-  const long n = static_cast<long>(g.n[0]) * g.n[1] * g.n[2];
+PcgStatus pcg_precond_solve(const std::function<void(const double*, double*)>& apply,
+                            const FdmDev& F, long n, const double* rhs, double* x,
+                            const FdmWork& w, double tol, int max_iter, cudaStream_t s) {
+
   const int G = grid_for(n);
   double bb = 0.0, unused = 0.0;
   dot2(n, rhs, rhs, nullptr, nullptr, w, s, bb, unused);
@@ -188,7 +276,7 @@ PcgStatus fdm_pcg_solve(cublasHandle_t h, const KronGrid& g, double a, double b,
   // r = b - A x (sparse.cpp:61-69); the preconditioned residual z = P r is
   // formed lazily after the stop test (same iterates as the reference's
   // order, one preconditioner apply fewer on the converged iteration)
-  k2_apply(g, a, b, x, w.Ap, sm_count, s, x_map);
+  apply(x, w.Ap);
   residual_kernel<<<G, 256, 0, s>>>(n, rhs, w.Ap, w.r);
   double rr = 0.0, rz = 0.0, rz_old = 0.0;
   dot2(n, w.r, w.r, nullptr, nullptr, w, s, rr, unused);
@@ -196,7 +284,7 @@ PcgStatus fdm_pcg_solve(cublasHandle_t h, const KronGrid& g, double a, double b,
   for (int it = 0; it < max_iter; ++it) {
     rel = std::sqrt(rr) / bnorm;
     if (rel <= tol) return PcgStatus{it, 0, rel, bnorm};
-    fdm_apply(h, F, w.r, w.z, w.t1, w.t2, s);
+    fdm_apply(F, w.r, w.z, w.t1, w.t2, s);
     dot2(n, w.r, w.z, nullptr, nullptr, w, s, rz, unused);
     if (it == 0) {
       TG_CUDA(cudaMemcpyAsync(w.p, w.z, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
@@ -204,7 +292,7 @@ PcgStatus fdm_pcg_solve(cublasHandle_t h, const KronGrid& g, double a, double b,
       direction_kernel<<<G, 256, 0, s>>>(n, rz / rz_old, w.z, w.p);  // p = z + beta p
     }
     rz_old = rz;
-    k2_apply(g, a, b, w.p, w.Ap, sm_count, s, p_map);
+    apply(w.p, w.Ap);
     double pAp = 0.0;
     dot2(n, w.p, w.Ap, nullptr, nullptr, w, s, pAp, unused);
     if (!(pAp > 0.0)) return PcgStatus{it, 4, rel, bnorm};
@@ -212,6 +300,17 @@ PcgStatus fdm_pcg_solve(cublasHandle_t h, const KronGrid& g, double a, double b,
     dot2(n, w.r, w.r, nullptr, nullptr, w, s, rr, unused);
   }
   return PcgStatus{max_iter, 3, rel, bnorm};
+}
+
+PcgStatus fdm_pcg_solve(const KronGrid& g, double a, double b, const FdmDev& F, const double* rhs,
+                        double* x, const FdmWork& w, double tol, int max_iter, int sm_count,
+                        cudaStream_t s, const TensorMap3* x_map, const TensorMap3* p_map) {
+  const long n = static_cast<long>(g.n[0]) * g.n[1] * g.n[2];
+  return pcg_precond_solve(
+      [&](const double* v, double* y) {
+        k2_apply(g, a, b, v, y, sm_count, s, v == x ? x_map : (v == w.p ? p_map : nullptr));
+      },
+      F, n, rhs, x, w, tol, max_iter, s);
 }
 
 }  // namespace tgb

@@ -1701,8 +1701,9 @@ void k2_slab_launch(const KronGrid& g, double a, double b, const double* rhs, do
   const int nb = seg_blocks(T, blocks);
   dim3 grid(nb), block(kKronTX, kKronTY);
   TG_KRON_DISPATCH(g.p, TG_CG1_PL_DISPATCH(pl, {
-    k2_slab_kernel<P, PL><<<grid, block, cg1_smem_bytes<P, PL>(g.n[2]), s>>>(
-        g, a, b, rhs, x, w, tol, max_iter, T, maps, ctl);
+    const size_t sb = cg1_smem_bytes<P, PL>(g.n[2]);  // slabs of one solver differ in depth
+    allow_smem(k2_slab_kernel<P, PL>, sb);
+    k2_slab_kernel<P, PL><<<grid, block, sb, s>>>(g, a, b, rhs, x, w, tol, max_iter, T, maps, ctl);
   }));
   TG_CUDA(cudaGetLastError());
 }

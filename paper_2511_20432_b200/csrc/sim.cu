@@ -81,7 +81,6 @@ Sim::Sim(const std::string& path, const SimOptions& opt) {
 }
 
 Sim::~Sim() {
-  if (cublas) cublasDestroy(cublas);
   if (h_dots) cudaFreeHost(h_dots);
   if (h_status) cudaFreeHost(h_status);
   if (h_steps) cudaFreeHost(h_steps);
@@ -399,7 +398,6 @@ void Sim::setup_device(int device, int preconditioner) {
         fdm.V[d] = d_fdmV.p + offV[d];
       }
       fdm.dinv = d_fdmDinv.p;
-      if (cublasCreate(&cublas) != CUBLAS_STATUS_SUCCESS) throw cuda_error("cublas: create failed");
       d_w2.ensure(n_free);
       d_dots.ensure(2);
       TG_CUDA(cudaMallocHost(&h_dots, 2 * sizeof(double)));
@@ -424,12 +422,103 @@ void Sim::setup_device(int device, int preconditioner) {
     upload(d_free_list, dofs.free_list, s);
     csr_inverse_diagonal(devA, d_invd.p, d_status.p, s);
     pcg_blocks = csr_pcg_max_blocks(ctx->sm_count);
+    if (preconditioner == 1) setup_general_fdm(s);
   }
   d_partials.ensure(std::max<size_t>(8 * static_cast<size_t>(pcg_blocks) + 8, 1024));
   TG_CUDA(cudaMemcpyAsync(h_status, d_status.p, sizeof(PcgStatus), cudaMemcpyDeviceToHost, s));
   TG_CUDA(cudaStreamSynchronize(s));
   diag_ok = h_status->status != 2;
   sf_setup_device();
+}
+
+// Preconditioner for non-separable patches (config 3's rational part): the
+// fast-diagonalization inverse of a separable approximation of A, scaled to
+// A's diagonal. Per axis d the control net's mean cumulative arc length along
+// d (averaged over all control lines) stands in for a separable map; its 1D
+// mass / stiffness bands (assemble_band_1d) give A~ = a M~z x M~y x M~x + b
+// (...), exactly invertible by FDM. With S = diag(sqrt(diag A / diag A~)),
+// P = S^-1 A~^-1 S^-1 is SPD and close to A^-1 where the geometry varies
+// slowly; the reference's PCG loop runs with P in place of Jacobi.
+void Sim::setup_general_fdm(cudaStream_t s) {
+  const ControlGrid& cg = vol.grid();
+  const auto n = cg.dims;
+  std::array<Band1D, 3> ab;
+  for (int d = 0; d < 3; ++d) {
+    const int o1 = (d + 1) % 3, o2 = (d + 2) % 3;
+    std::vector<double> X(n[d], 0.0);
+    int lines = 0;
+    for (int b = 0; b < n[o2]; ++b)
+      for (int a = 0; a < n[o1]; ++a) {
+        double acc = 0.0;
+        for (int i = 1; i < n[d]; ++i) {
+          int ijk0[3], ijk1[3];
+          ijk0[d] = i - 1;
+          ijk1[d] = i;
+          ijk0[o1] = ijk1[o1] = a;
+          ijk0[o2] = ijk1[o2] = b;
+          const auto& p0 = cg.pts[cg.index(ijk0[0], ijk0[1], ijk0[2])];
+          const auto& p1 = cg.pts[cg.index(ijk1[0], ijk1[1], ijk1[2])];
+          acc += std::sqrt((p1[0] - p0[0]) * (p1[0] - p0[0]) + (p1[1] - p0[1]) * (p1[1] - p0[1]) +
+                           (p1[2] - p0[2]) * (p1[2] - p0[2]));
+          X[i] += acc;
+        }
+        ++lines;
+      }
+    for (double& v : X) v /= lines;
+    ab[d] = assemble_band_1d(vol.knots(d), X, quad[d]);
+  }
+  const double th = cfg.stepping.theta, dt = dt_solver;
+  const double a = cfg.material.volumetric_capacity() / dt, b = th * cfg.material.conductivity;
+  int nfree[3];
+  std::vector<double> Vall, Lall;
+  size_t offV[3], offL[3];
+  std::vector<double> dm[3], dk[3];  // the approximation's 1D diagonals on the free rows
+  for (int d = 0; d < 3; ++d) {
+    const int first = (d == geom.ax && geom.layer == 0) ? 1 : 0;
+    nfree[d] = ab[d].n - (d == geom.ax ? 1 : 0);
+    const Fdm1D f = fdm_factor(ab[d].M, ab[d].K, ab[d].n, ab[d].p, first, nfree[d]);
+    offV[d] = Vall.size();
+    offL[d] = Lall.size();
+    Vall.insert(Vall.end(), f.V.begin(), f.V.end());
+    Lall.insert(Lall.end(), f.lam.begin(), f.lam.end());
+    const int W = 2 * ab[d].p + 1;
+    for (int i = 0; i < nfree[d]; ++i) {
+      dm[d].push_back(ab[d].M[(first + i) * W + ab[d].p]);
+      dk[d].push_back(ab[d].K[(first + i) * W + ab[d].p]);
+    }
+  }
+  // S^-1 = sqrt(diag A~ / diag A) on the free points (free flat order)
+  std::vector<double> invd(n_free), sinv(n_free);
+  TG_CUDA(cudaMemcpyAsync(invd.data(), d_invd.p, sizeof(double) * n_free, cudaMemcpyDeviceToHost, s));
+  TG_CUDA(cudaStreamSynchronize(s));
+  for (int k = 0, f = 0; k < nfree[2]; ++k)
+    for (int j = 0; j < nfree[1]; ++j)
+      for (int i = 0; i < nfree[0]; ++i, ++f) {
+        const double mm = dm[0][i] * dm[1][j] * dm[2][k];
+        const double kk = dk[0][i] * dm[1][j] * dm[2][k] + dm[0][i] * dk[1][j] * dm[2][k] +
+                          dm[0][i] * dm[1][j] * dk[2][k];
+        sinv[f] = std::sqrt((a * mm + b * kk) * invd[f]);
+      }
+  if (static_cast<long>(nfree[0]) * nfree[1] * nfree[2] != n_free)
+    throw std::logic_error("general FDM: free grid does not match the DOF split");
+  upload(d_fdmV, Vall, s);
+  upload(d_fdmL, Lall, s);
+  upload(d_fdmS, sinv, s);
+  d_fdmDinv.ensure(n_free);
+  fdm_inverse_eigs(nfree, d_fdmL.p + offL[0], d_fdmL.p + offL[1], d_fdmL.p + offL[2], a, b,
+                   d_fdmDinv.p, s);
+  for (int d = 0; d < 3; ++d) {
+    fdm.n[d] = nfree[d];
+    fdm.V[d] = d_fdmV.p + offV[d];
+  }
+  fdm.dinv = d_fdmDinv.p;
+  fdm.sinv = d_fdmS.p;
+  d_z.ensure(n_free);
+  d_p2.ensure(n_free);
+  d_w2.ensure(n_free);
+  d_dots.ensure(2);
+  TG_CUDA(cudaMallocHost(&h_dots, 2 * sizeof(double)));
+  use_fdm = true;
 }
 
 // K5 setup (host): are the lateral faces' base quadrature points and the
@@ -885,7 +974,11 @@ int Sim::fine_elements(double t, double radius) {
   Vec3 f;
   int nf = 0;
   h_fine.resize(2 * static_cast<size_t>(n_fe) + 2);
-  if (!focus_at(t, f)) return 0;
+  if (focus_given) {
+    f = focus_value;
+  } else if (!focus_at(t, f)) {
+    return 0;
+  }
   for (int e = 0; e < n_fe; ++e) {
     const Vec3 c{centers[3 * e], centers[3 * e + 1], centers[3 * e + 2]};
     if ((c - f).norm() < radius) h_fine[nf++] = e;
@@ -1155,12 +1248,6 @@ void Sim::flux_load_device(double t, double radius, double* d_F, int e0, int e1)
   TG_CUDA(cudaGetLastError());
 }
 
-void Sim::flux_gather_device(const double* d_loc_all, double* d_F) {
-  k3_gather(n_full, d_inc_ptr.p, d_inc_src.p, d_loc_all, d_F, ctx->stream);
-  ++ctx->timer.launches;
-  TG_CUDA(cudaGetLastError());
-}
-
 void Sim::dirichlet_device(double t, double* d_g, int c0, int c1) {
   // constrained DOFs [c0, c1) (all by default): each value depends on its
   // Greville point only, so a range is the same bits as the full call
@@ -1212,11 +1299,15 @@ void Sim::theta_step_launch(double tol, int max_iter) {
     if (use_fdm) {
       const FdmWork w{d_r.p, d_z.p, d_p.p, d_Ap.p, d_p2.p, d_w2.p, d_partials.p, d_dots.p, h_dots};
       ctx->timer.timed(2, s, [&] {
-        *h_status = fdm_pcg_solve(cublas, gfree, coefA[0], coefA[1], fdm, d_rhs.p, d_x.p, w, tol,
+        *h_status = fdm_pcg_solve(gfree, coefA[0], coefA[1], fdm, d_rhs.p, d_x.p, w, tol,
                                   max_iter, ctx->sm_count, s, maps.valid ? &maps.x : nullptr,
                                   maps.valid ? &maps.pA : nullptr);
       });
       TG_CUDA(cudaMemcpyAsync(d_status.p, h_status, sizeof(PcgStatus), cudaMemcpyHostToDevice, s));
+    } else if (slab) {  // z-slabs (multi-GPU, or the local test bed)
+      ctx->timer.timed(2, s, [&] {
+        slab->solve(d_rhs.p, d_x.p, coefA[0], coefA[1], tol, max_iter, d_status.p, s);
+      });
     } else if (use_cg1) {
       const Cg1Work w{d_p.p,    {d_r.p, d_z.p}, {d_Ap.p, d_w2.p}, {d_p2.p, d_s2.p},
                       d_invd.p, d_partials.p,   d_status.p};
@@ -1236,10 +1327,19 @@ void Sim::theta_step_launch(double tol, int max_iter) {
   } else {
     csr_theta_rhs(devB, devAc, d_T.p, d_g1.p, d_Fn.p, d_F1.p, d_free_list.p, th, d_rhs.p, s);
     ++ctx->timer.launches;
-    const CsrWork w{d_r.p, d_p.p, d_Ap.p, d_invd.p, d_partials.p, d_status.p};
-    ctx->timer.timed(2, s, [&] {
-      csr_pcg_solve(devA, d_rhs.p, d_x.p, w, tol, max_iter, pcg_blocks, s);
-    });
+    if (use_fdm) {  // the scaled separable-approximation preconditioner
+      const FdmWork w{d_r.p, d_z.p, d_p.p, d_Ap.p, d_p2.p, d_w2.p, d_partials.p, d_dots.p, h_dots};
+      ctx->timer.timed(2, s, [&] {
+        *h_status = pcg_precond_solve([&](const double* v, double* y) { csr_apply(devA, v, y, s); },
+                                      fdm, n_free, d_rhs.p, d_x.p, w, tol, max_iter, s);
+      });
+      TG_CUDA(cudaMemcpyAsync(d_status.p, h_status, sizeof(PcgStatus), cudaMemcpyHostToDevice, s));
+    } else {
+      const CsrWork w{d_r.p, d_p.p, d_Ap.p, d_invd.p, d_partials.p, d_status.p};
+      ctx->timer.timed(2, s, [&] {
+        csr_pcg_solve(devA, d_rhs.p, d_x.p, w, tol, max_iter, pcg_blocks, s);
+      });
+    }
   }
   ++ctx->timer.launches;
   ++ctx->timer.k2_launches;
@@ -1248,12 +1348,7 @@ void Sim::theta_step_launch(double tol, int max_iter) {
 void Sim::reset() {
   cudaStream_t s = ctx->stream;
   TG_CUDA(cudaMemsetAsync(d_x.p, 0, sizeof(double) * n_free, s));
-  if (sf_ready && sf_flux_ok && sf_dir_ok) {
-    loads_device(0.0, cfg.mesh.elevate_radius, d_Fn.p, d_gn.p, true);
-  } else {
-    dirichlet_device(0.0, d_gn.p);
-    flux_load_device(0.0, cfg.mesh.elevate_radius, d_Fn.p);
-  }
+  step_loads(0.0, d_Fn.p, d_gn.p);
   step = 0;
   TG_CUDA(cudaStreamSynchronize(s));
 }
@@ -1267,13 +1362,8 @@ PcgStatus Sim::advance() {
     return std::chrono::steady_clock::now();
   };
   const auto t0 = now();
-  if (sf_ready && sf_flux_ok && sf_dir_ok) {  // both loads in one fused pass
-    loads_device(t1, cfg.mesh.elevate_radius, d_F1.p, d_g1.p, true);
-  } else {
-    flux_load_device(t1, cfg.mesh.elevate_radius, d_F1.p);
-  }
+  step_loads(t1, d_F1.p, d_g1.p);
   const auto ta = now();
-  if (!(sf_ready && sf_flux_ok && sf_dir_ok)) dirichlet_device(t1, d_g1.p);
   const auto tb = now();
   const PcgStatus st = theta_step_device(cfg.stepping.solver_tol, cfg.stepping.max_iter);
   if (timing) {
@@ -1286,6 +1376,44 @@ PcgStatus Sim::advance() {
   std::swap(d_gn.p, d_g1.p);
   step = s1;
   return st;
+}
+
+void Sim::step_loads(double t, double* d_F, double* d_g) {
+  const double r = cfg.mesh.elevate_radius;
+  const bool fused = sf_ready && sf_flux_ok && sf_dir_ok;
+  if (fused && comm && sf_world > 1) {
+    // this rank's regions; the compact integrand and g summed over the ranks
+    // (disjoint supports: every entry has one nonzero contributor, so the sum
+    // is exact and the same on every rank), then the local loads and gather
+    loads_device(t, r, nullptr, d_g, false);
+    nccl_allreduce_sum(*comm, d_gq.p, static_cast<size_t>(sf_last_npts), ctx->stream);
+    nccl_allreduce_sum(*comm, d_g, static_cast<size_t>(n_con), ctx->stream);
+    flux_finish(d_F);
+    return;
+  }
+  if (fused) {  // both loads in one fused pass
+    loads_device(t, r, d_F, d_g, true);
+    return;
+  }
+  flux_load_device(t, r, d_F);
+  dirichlet_device(t, d_g);
+}
+
+void Sim::shard(int rank, int world, const char id[128]) {
+  comm = nccl_comm(rank, world, id, ctx->device);
+  sf_rank = rank;
+  sf_world = world;
+  slab.reset();
+  if (world > 1 && kron && use_cg1)
+    slab = std::make_unique<SlabSolver>(gfree, world, rank, comm, ctx->sm_count, cg1_pl);
+}
+
+void Sim::set_slabs(int n) {
+  slab.reset();
+  if (n > 1) {
+    if (!(kron && use_cg1)) throw std::invalid_argument("slabs: needs the single-sweep Kronecker solver");
+    slab = std::make_unique<SlabSolver>(gfree, n, 0, nullptr, ctx->sm_count, cg1_pl);
+  }
 }
 
 // n steps with no host synchronisation between them: every step's loads,
@@ -1317,20 +1445,17 @@ long Sim::advance_steps(int n, double* last_rel) {
   }
   cudaStream_t s = ctx->stream;
   const int first = step;
+  ctx->timer.timed(4, s, [&] {
   for (int k = 0; k < n; ++k) {
     const double t1 = (step + 1) * dt_solver;  // driver.cpp:127
-    if (sf_ready && sf_flux_ok && sf_dir_ok) {
-      loads_device(t1, cfg.mesh.elevate_radius, d_F1.p, d_g1.p, true);
-    } else {
-      flux_load_device(t1, cfg.mesh.elevate_radius, d_F1.p);
-      dirichlet_device(t1, d_g1.p);
-    }
+    step_loads(t1, d_F1.p, d_g1.p);
     ctx->timer.timed(3, s, [&] { theta_step_launch(cfg.stepping.solver_tol, cfg.stepping.max_iter); });
     TG_CUDA(cudaMemcpyAsync(&h_steps[k], d_status.p, sizeof(PcgStatus), cudaMemcpyDeviceToHost, s));
     std::swap(d_Fn.p, d_F1.p);
     std::swap(d_gn.p, d_g1.p);
     ++step;
   }
+  });
   TG_CUDA(cudaStreamSynchronize(s));
   for (int k = 0; k < n; ++k) {
     const PcgStatus& st = h_steps[k];
@@ -1348,17 +1473,6 @@ long Sim::advance_steps(int n, double* last_rel) {
   }
   if (last_rel) *last_rel = h_steps[n - 1].rel_residual;
   return it;
-}
-
-PcgStatus Sim::advance_with_loads(const double* d_F1_in, const double* d_g1_in) {
-  cudaStream_t s = ctx->stream;
-  TG_CUDA(cudaMemcpyAsync(d_F1.p, d_F1_in, sizeof(double) * n_full, cudaMemcpyDeviceToDevice, s));
-  TG_CUDA(cudaMemcpyAsync(d_g1.p, d_g1_in, sizeof(double) * n_con, cudaMemcpyDeviceToDevice, s));
-  const PcgStatus st = theta_step_device(cfg.stepping.solver_tol, cfg.stepping.max_iter);
-  std::swap(d_Fn.p, d_F1.p);
-  std::swap(d_gn.p, d_g1.p);
-  step += 1;
-  return st;
 }
 
 // ---------------------------------------------------------------------------

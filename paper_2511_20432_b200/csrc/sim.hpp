@@ -14,6 +14,7 @@
 #include "k4_eval.cuh"
 #include "k5_fused.cuh"
 #include "k5_sumfact.cuh"
+#include "slab.hpp"
 
 namespace tgb {
 
@@ -46,16 +47,12 @@ class Sim {
   // n steps without host synchronisation between them (statuses read at the
   // end); returns the CG iterations
   long advance_steps(int n, double* last_rel);
-  // one step with F_{n+1}, g_{n+1} supplied on the device (a multi-GPU driver
-  // assembles them sharded, all-gathers, and every rank steps)
-  PcgStatus advance_with_loads(const double* d_F1_in, const double* d_g1_in);
 
   // drop-in pieces on device buffers
   // assemble_flux_load; with [e0, e1) only those face elements' local loads
   // (d_loc) are computed, and d_F == nullptr skips the gather (sharded use)
   void flux_load_device(double t, double radius, double* d_F, int e0 = 0,
                         int e1 = 1 << 30);
-  void flux_gather_device(const double* d_loc_all, double* d_F);
   void dirichlet_device(double t, double* d_g, int c0 = 0, int c1 = -1);
   PcgStatus theta_step_device(double tol, int max_iter);  // uses d_x, d_gn, d_g1, d_Fn, d_F1
   void theta_step_launch(double tol, int max_iter);      // its launches (no status read)
@@ -102,7 +99,22 @@ class Sim {
   bool sf_fused_ready() const { return sf_ready; }
   long sf_compact_points() const { return sf_last_npts; }
 
+  // multi-GPU (slab.hpp): shard(rank, world, id) joins an NCCL communicator;
+  // the loads' K5 regions and the θ-step solve's z-slabs are then split over
+  // the ranks (the loads all-reduced, x broadcast after each solve).
+  // set_slabs(n): the same slab solve with n slabs on this one GPU.
+  void shard(int rank, int world, const char id[128]);
+  void set_slabs(int n);
+  std::unique_ptr<SlabSolver> slab;
+  std::shared_ptr<NcclComm> comm;
+  // F_{n+1} and g_{n+1} of a step at t (fused / sharded / K1 paths)
+  void step_loads(double t, double* d_F, double* d_g);
+
   bool focus_at(double t, Vec3& focus) const;
+  // a caller-given fine-rule focus for the next flux-load call (tg_sim_flux_load's
+  // focus_xyz) instead of the newest active source (assembly.cpp:153-157)
+  bool focus_given = false;
+  Vec3 focus_value{};
   int fine_elements(double t, double radius);  // fills h_fine, returns the count
   std::vector<int> h_fine;  // fine elements (sorted), then the running extra-point counts
 
@@ -148,9 +160,8 @@ class Sim {
   // fast-diagonalization preconditioner (k2_fdm.cuh), opt-in
   bool use_fdm = false;
   FdmDev fdm{};
-  DevBuf<double> d_fdmV, d_fdmL, d_fdmDinv, d_dots;
+  DevBuf<double> d_fdmV, d_fdmL, d_fdmDinv, d_fdmS, d_dots;
   double* h_dots = nullptr;
-  cublasHandle_t cublas = nullptr;
   Cg1Maps cg1maps{};
   DevBuf<double> d_w2, d_s2;
   // observers: the patch on the device (uploaded on first use) and scratch
@@ -175,6 +186,7 @@ class Sim {
  private:
   void setup_host();
   void setup_device(int device, int preconditioner);
+  void setup_general_fdm(cudaStream_t s);
   void sf_setup_host();    // grids, tiles, regions, remainder entries (host only)
   void sf_setup_device();  // uploads
   std::vector<int> sf_h_gcell, sf_h_fa, sf_h_fb, sf_h_ff;  // until the entry lists are built

@@ -155,6 +155,37 @@ int tg_sim_sumfact_stats(tg_sim* s, double* out) {
   }, false);
 }
 
+int tg_nccl_unique_id(char* out128) {
+  try {
+    tgb::nccl_unique_id(out128);
+    return TG_OK;
+  } catch (const std::exception&) {
+    return TG_ECUDA;
+  }
+}
+
+int tg_slab_plan(int nz, int p, int world, int rank, int* out6) {
+  try {
+    const tgb::SlabPlan q = tgb::slab_plan(nz, p, world, rank);
+    const int v[] = {q.gz0, q.nloc, q.zo0, q.zo1, q.lo, q.hi};
+    std::memcpy(out6, v, sizeof(v));
+    return TG_OK;
+  } catch (const std::exception&) {
+    return TG_ERROR;
+  }
+}
+
+int tg_sim_shard(tg_sim* s, int rank, int world, const char* id128) {
+  return sim_guard(s, [&](Sim& m) {
+    if (world < 1 || rank < 0 || rank >= world) throw std::invalid_argument("shard: bad rank");
+    m.shard(rank, world, id128);
+  });
+}
+
+int tg_sim_set_slabs(tg_sim* s, int n) {
+  return sim_guard(s, [&](Sim& m) { m.set_slabs(n); });
+}
+
 int tg_sim_sumfact_regions(tg_sim* s, double* out) {
   return sim_guard(s, [&](Sim& m) {
     const auto& R = m.sf_regions();
@@ -228,10 +259,19 @@ int tg_sim_greville_points(tg_sim* s, double* out) {
   return sim_guard(s, [&](Sim& m) { std::memcpy(out, m.grev.data(), m.grev.size() * sizeof(double)); }, false);
 }
 
-int tg_sim_flux_load(tg_sim* s, double t, double fine_radius, double* out_F) {
+int tg_sim_flux_load(tg_sim* s, double t, const double* focus_xyz, double fine_radius,
+                     double* out_F) {
   return sim_guard(s, [&](Sim& m) {
     const double r = fine_radius < 0.0 ? m.cfg.mesh.elevate_radius : fine_radius;
-    m.flux_load_device(t, r, m.d_T.p);
+    m.focus_given = focus_xyz != nullptr;
+    if (focus_xyz) m.focus_value = Vec3{focus_xyz[0], focus_xyz[1], focus_xyz[2]};
+    try {
+      m.flux_load_device(t, r, m.d_T.p);
+    } catch (...) {
+      m.focus_given = false;
+      throw;
+    }
+    m.focus_given = false;
     d2h(out_F, m.d_T.p, m.n_full, m.ctx->stream);
     TG_CUDA(cudaStreamSynchronize(m.ctx->stream));
   });
@@ -276,23 +316,6 @@ int tg_sim_advance(tg_sim* s, int n_steps, long* cg_iterations, double* last_rel
   });
 }
 
-int tg_sim_dirichlet_range_device(tg_sim* s, double t, int c0, int c1, double* d_g) {
-  return sim_guard(s, [&](Sim& m) {
-    if (c0 < 0 || c1 < c0 || c1 > m.n_con) throw std::invalid_argument("dirichlet: bad range");
-    m.dirichlet_device(t, d_g, c0, c1);
-    TG_CUDA(cudaStreamSynchronize(m.ctx->stream));
-  });
-}
-
-int tg_sim_advance_with_loads_device(tg_sim* s, const double* d_F1, const double* d_g1,
-                                     long* cg_iterations, double* rel) {
-  return sim_guard(s, [&](Sim& m) {
-    const PcgStatus st = m.advance_with_loads(d_F1, d_g1);
-    if (cg_iterations) *cg_iterations = st.iterations;
-    if (rel) *rel = st.rel_residual;
-  });
-}
-
 int tg_sim_state(tg_sim* s, int* step, double* time, double* free_out, double* g_out,
                  double* F_out) {
   return sim_guard(s, [&](Sim& m) {
@@ -306,51 +329,24 @@ int tg_sim_state(tg_sim* s, int* step, double* time, double* free_out, double* g
   });
 }
 
-int tg_sim_flux_local_device(tg_sim* s, double t, double fine_radius, int e0, int e1,
-                             double* d_loc) {
-  return sim_guard(s, [&](Sim& m) {
-    const double r = fine_radius < 0.0 ? m.cfg.mesh.elevate_radius : fine_radius;
-    if (e0 < 0 || e1 < e0 || e1 > m.n_fe) throw std::invalid_argument("flux_local: bad range");
-    m.flux_load_device(t, r, nullptr, e0, e1);
-    if (e1 > e0)
-      TG_CUDA(cudaMemcpyAsync(d_loc, m.d_loc.p + static_cast<size_t>(e0) * m.ndk,
-                              sizeof(double) * (e1 - e0) * m.ndk, cudaMemcpyDeviceToDevice,
-                              m.ctx->stream));
-    TG_CUDA(cudaStreamSynchronize(m.ctx->stream));
+long tg_sim_last_integrand(tg_sim* s, double* out) {
+  long n = -TG_ERROR;
+  const int rc = sim_guard(s, [&](Sim& m) {
+    n = m.sf_compact_points();
+    if (out) {
+      d2h(out, m.d_gq.p, static_cast<size_t>(n), m.ctx->stream);
+      TG_CUDA(cudaStreamSynchronize(m.ctx->stream));
+    }
   });
+  return rc == TG_OK ? n : -rc;
 }
 
-int tg_sim_flux_gather_device(tg_sim* s, const double* d_loc_all, double* d_F) {
+int tg_sim_set_region_split(tg_sim* s, int rank, int world) {
   return sim_guard(s, [&](Sim& m) {
-    m.flux_gather_device(d_loc_all, d_F);
-    TG_CUDA(cudaStreamSynchronize(m.ctx->stream));
-  });
-}
-
-int tg_sim_operator_apply_slab_device(tg_sim* s, int k0, int k1, const double* d_x,
-                                      double* d_y) {
-  return sim_guard(s, [&](Sim& m) {
-    if (!m.kron) throw std::invalid_argument("slab apply needs the Kronecker operator");
-    const int p = m.gfree.p, W = 2 * p + 1, nz = m.gfree.n[2];
-    if (k0 < 0 || k1 > nz || k1 <= k0) throw std::invalid_argument("slab apply: bad planes");
-    const int g0 = std::max(0, k0 - p), g1 = std::min(nz, k1 + p);
-    KronGrid slab = m.gfree;
-    slab.n[2] = g1 - g0;
-    slab.M[2] += static_cast<size_t>(g0) * W;
-    slab.K[2] += static_cast<size_t>(g0) * W;
-    const size_t plane = static_cast<size_t>(slab.n[0]) * slab.n[1];
-    double* tmp = m.d_Ap.p;  // n_free >= slab size
-    k2_apply(slab, m.coefA[0], m.coefA[1], d_x, tmp, m.ctx->sm_count, m.ctx->stream);
-    TG_CUDA(cudaMemcpyAsync(d_y, tmp + (k0 - g0) * plane, sizeof(double) * (k1 - k0) * plane,
-                            cudaMemcpyDeviceToDevice, m.ctx->stream));
-    TG_CUDA(cudaStreamSynchronize(m.ctx->stream));
-  });
-}
-
-int tg_sim_inverse_diagonal(tg_sim* s, double* out) {
-  return sim_guard(s, [&](Sim& m) {
-    TG_CUDA(cudaMemcpy(out, m.d_invd.p, sizeof(double) * m.n_free, cudaMemcpyDeviceToHost));
-  });
+    if (world < 1 || rank < 0 || rank >= world) throw std::invalid_argument("split: bad rank");
+    m.sf_rank = rank;
+    m.sf_world = world;
+  }, false);
 }
 
 int tg_sim_debug_trace(tg_sim* s, unsigned long long* out, int n) {

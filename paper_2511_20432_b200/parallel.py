@@ -1,28 +1,35 @@
-"""Multi-GPU sharding of the hot path: one process per GPU,
-torch.distributed for the plumbing (NCCL on B200s, gloo for the CPU tests).
+"""Multi-GPU time stepping: one process per GPU,
+torch.distributed for the plumbing, the data path native.
 
-* K1 superposition shards by points: every rank evaluates a contiguous slab of
-  the points against the replicated source history; no exchange is needed
-  (bench.py's weak-scaling mode) or one all-gather assembles the field.
-* K1 + K3 flux load shards by face elements: each rank computes the local
-  loads of its element slab, the slabs are all-gathered and every rank runs
-  the deterministic gather in the reference's scatter order
-  (proj/src/assembly.cpp:141-144) — bit-identical to one GPU.
-* K2 shards the free grid in z-slabs: each CG iteration exchanges p ghost
-  planes with the two neighbours (the halo) before the operator apply and
-  all-reduces the dot products (SlabPCG below, the reference's
-  pcg_jacobi, proj/src/sparse.cpp:41-100, with global dot products).
+Per step (proj/src/driver.cpp:126-145 on every rank):
+  * loads: the K5 regions (face-grid and Greville-grid tiles, the step's fine
+    rectangles; csrc/k5_fused.cu) are dealt round-robin to the ranks; each
+    rank computes its regions' compact flux integrand and Dirichlet values and
+    one NCCL all-reduce per vector sums them (disjoint supports: every entry
+    has exactly one nonzero contributor, so the sum is exact and identical on
+    every rank), then every rank runs the deterministic K3 local-load / gather;
+  * θ-step: the RHS is formed on every rank (cheap, HBM-bound); the Jacobi-PCG
+    solve runs on z-slabs of the free grid (csrc/slab.cu): per iteration one
+    sweep per rank plus one NCCL group carrying the P ghost planes of w^ to /
+    from each neighbour and an all-gather of 4 partial sums (summed in rank
+    order, so all ranks take the same alpha, beta and stop decision); after
+    the solve every rank broadcasts its own planes of x.
+Every rank therefore ends each step with the same state.
 
-The compute callbacks are injected so that the partition, exchange and
-reduction logic is exercised on CPU (gloo, world_size 2) by
-tests/test_parallel.py; the GPU bindings (`gpu_*` helpers) plug in the C ABI
-device entry points.
+This module joins the ranks (ShardedTimeLoop: the NCCL communicator id from
+rank 0 to all through torch.distributed, then tg_sim_shard) and holds
+SlabModel, a numpy model of the slab protocol — the same slab plan
+(tg_slab_plan), ghost planes, own-plane partial sums and scalar recurrences
+as k2_slab_kernel — that tests/test_parallel.py runs over gloo on CPU to
+check the decomposition logic without GPUs. The device path itself is
+checked on one GPU by Simulation.set_slabs (all slabs on one device, halos
+by device copies) against the single-GPU solve.
 """
 from __future__ import annotations
 
 import os
 from dataclasses import dataclass
-from typing import Callable, List, Optional, Tuple
+from typing import Optional, Tuple
 
 import numpy as np
 
@@ -46,319 +53,190 @@ class Dist:
             return Dist(dist.get_rank(), dist.get_world_size(), device or "cpu")
         return Dist(0, 1, device or "cpu")
 
-    def all_gather_concat(self, part, sizes: List[int]):
-        """Concatenate every rank's part (sizes[r] items each, in rank order)."""
-        import torch
-        import torch.distributed as dist
-        t = part if isinstance(part, torch.Tensor) else torch.as_tensor(part)
+    def broadcast_bytes(self, data: Optional[bytes]) -> bytes:
+        """rank 0's bytes on every rank."""
         if self.world == 1:
-            return t
-        width = max(sizes)
-        pad = torch.zeros(width, dtype=t.dtype, device=t.device)
-        pad[: t.numel()] = t.reshape(-1)
-        bufs = [torch.empty_like(pad) for _ in range(self.world)]
-        dist.all_gather(bufs, pad)
-        return torch.cat([b[:s] for b, s in zip(bufs, sizes)])
-
-    def all_reduce_sum(self, values):
-        """Sum of a small vector over ranks (fixed order per backend)."""
-        import torch
+            return data
         import torch.distributed as dist
-        t = torch.as_tensor(np.asarray(values, dtype=np.float64)).to(self.device)
-        if self.world > 1:
-            dist.all_reduce(t, op=dist.ReduceOp.SUM)
-        return t.cpu().numpy()
+        box = [data if self.rank == 0 else None]
+        dist.broadcast_object_list(box, src=0)
+        return box[0]
 
-    def exchange_halo(self, lo_send, hi_send, lo_shape, hi_shape):
-        """Send lo_send to rank-1 and hi_send to rank+1; return what they sent
-        back (the ghost planes below and above this rank's slab), or None at
-        the ends of the rank chain."""
-        import torch
-        import torch.distributed as dist
+    def all_gather_array(self, a: np.ndarray) -> list:
         if self.world == 1:
-            return None, None
-        ops = []
-        lo_recv = hi_recv = None
-        if self.rank > 0:
-            lo_recv = torch.empty(lo_shape, dtype=torch.float64, device=self.device)
-            ops.append(dist.P2POp(dist.isend, lo_send.contiguous(), self.rank - 1))
-            ops.append(dist.P2POp(dist.irecv, lo_recv, self.rank - 1))
-        if self.rank < self.world - 1:
-            hi_recv = torch.empty(hi_shape, dtype=torch.float64, device=self.device)
-            ops.append(dist.P2POp(dist.isend, hi_send.contiguous(), self.rank + 1))
-            ops.append(dist.P2POp(dist.irecv, hi_recv, self.rank + 1))
-        for r in dist.batch_isend_irecv(ops):
-            r.wait()
-        return lo_recv, hi_recv
+            return [a]
+        import torch.distributed as dist
+        out = [None] * self.world
+        dist.all_gather_object(out, a)
+        return out
 
-
-# ---------------------------------------------------------------------------
-# K1 / K3
-
-def sharded_flux_load(local_fn: Callable[[int, int], object], gather_fn: Callable[[object], object],
-                      n_elems: int, n_cols: int, dist: Dist):
-    """assemble_flux_load over face-element slabs. local_fn(e0, e1) returns the
-    local loads of elements [e0, e1) ((e1 - e0) * n_cols values, element-major);
-    gather_fn(loc_all) scatters all elements' loads into F in the reference's
-    order. Every rank returns the full F."""
-    e0, e1 = partition(n_elems, dist.world, dist.rank)
-    part = local_fn(e0, e1)
-    sizes = [(partition(n_elems, dist.world, r)[1] - partition(n_elems, dist.world, r)[0]) * n_cols
-             for r in range(dist.world)]
-    return gather_fn(dist.all_gather_concat(part, sizes))
-
-
-def sharded_points(fn: Callable[[int, int], object], n_points: int, dist: Dist, gather=True):
-    """Evaluate fn(begin, end) on this rank's point slab; optionally all-gather."""
-    b, e = partition(n_points, dist.world, dist.rank)
-    part = fn(b, e)
-    if not gather:
-        return part
-    sizes = [partition(n_points, dist.world, r)[1] - partition(n_points, dist.world, r)[0]
-             for r in range(dist.world)]
-    return dist.all_gather_concat(part, sizes)
-
-
-# ---------------------------------------------------------------------------
-# K2: z-slab Jacobi-PCG
-
-class SlabPCG:
-    """pcg_jacobi (proj/src/sparse.cpp:41-100) on z-slabs of the free grid.
-
-    apply_slab(k0, k1, x_ghosted) -> (A x) on planes [k0, k1), where x_ghosted
-    holds planes [max(0, k0 - p), min(nz, k1 + p)) (torch tensor, flat,
-    plane-major). inv_diag_owned: 1/diag on this rank's planes."""
-
-    def __init__(self, apply_slab, inv_diag_owned, plane: int, nz: int, p: int, dist: Dist):
-        self.apply_slab = apply_slab
-        self.dinv = inv_diag_owned
-        self.plane, self.nz, self.p, self.dist = plane, nz, p, dist
-        self.k0, self.k1 = partition(nz, dist.world, dist.rank)
-        if dist.world > 1 and self.k1 - self.k0 < p:
-            raise ValueError("z-slabs thinner than the stencil half-width")
-
-    def _ghosted(self, v):
-        """v (owned planes) with the neighbours' ghost planes attached."""
+    def send_recv(self, send: dict, shapes: dict) -> dict:
+        """Point-to-point exchange: send[peer] -> peer, receive shapes[peer]
+        from peer (float64 arrays)."""
         import torch
-        p, pl = self.p, self.plane
-        k0, k1 = self.k0, self.k1
-        lo_n = min(p, k0)                 # ghost planes below
-        hi_n = min(p, self.nz - k1)       # ghost planes above
-        v2 = v.reshape(k1 - k0, pl)
-        lo, hi = self.dist.exchange_halo(v2[:min(p, k1 - k0)], v2[max(0, k1 - k0 - p):],
-                                         (lo_n, pl), (hi_n, pl))
-        parts = []
-        if lo_n:
-            parts.append(lo[-lo_n:] if lo is not None else v2.new_zeros((lo_n, pl)))
-        parts.append(v2)
-        if hi_n:
-            parts.append(hi[:hi_n] if hi is not None else v2.new_zeros((hi_n, pl)))
-        return torch.cat(parts).reshape(-1)
-
-    def _dot(self, *pairs):
-        local = [float((a * b).sum().item()) for a, b in pairs]
-        return self.dist.all_reduce_sum(local)
-
-    def solve(self, b, x, tol: float, max_iter: int, single_reduction: bool = False):
-        """b, x: owned-plane torch tensors (x = warm start, updated in place).
-        Returns (iterations, relative residual); raises like the reference.
-        single_reduction: the Chronopoulos-Gear form of the device solver
-        (k2_cg1_kernel) — one halo exchange and one 3-scalar allreduce per
-        iteration instead of one exchange and two allreduces."""
-        if single_reduction:
-            return self._solve_cg1(b, x, tol, max_iter)
-        bb = self._dot((b, b))[0]
-        bnorm = float(np.sqrt(bb))
-        if bnorm == 0.0:
-            x.zero_()
-            return 0, 0.0
-        r = b - self.apply_slab(self.k0, self.k1, self._ghosted(x))
-        z = self.dinv * r
-        rz = self._dot((r, z))[0]
-        p = z.clone()
-        rel = 0.0
-        for it in range(max_iter):
-            rr = self._dot((r, r))[0]
-            rel = float(np.sqrt(rr)) / bnorm
-            if rel <= tol:
-                return it, rel
-            Ap = self.apply_slab(self.k0, self.k1, self._ghosted(p))
-            pAp = self._dot((p, Ap))[0]
-            if not pAp > 0.0:
-                raise ArithmeticError("pcg: indefinite direction, matrix not SPD")
-            alpha = rz / pAp
-            x.add_(alpha * p)
-            r.sub_(alpha * Ap)
-            z = self.dinv * r
-            rz_new = self._dot((r, z))[0]
-            beta = rz_new / rz
-            rz = rz_new
-            p = z + beta * p
-        raise ArithmeticError(f"pcg: no convergence in {max_iter} iterations, "
-                              f"relative residual {rel:.17g}")
-
-    def _solve_cg1(self, b, x, tol, max_iter):
-        A = lambda v: self.apply_slab(self.k0, self.k1, self._ghosted(v))  # noqa: E731
-        r = b - A(x)
-        bb, rr = self._dot((b, b), (r, r))
-        bnorm = float(np.sqrt(bb))
-        if bnorm == 0.0:  # sparse.cpp:57-60
-            x.zero_()
-            return 0, 0.0
-        rel = float(np.sqrt(rr)) / bnorm
-        if max_iter > 0 and rel <= tol:
-            return 0, rel
-        if max_iter > 0:
-            u = self.dinv * r
-            w = A(u)
-            gamma, delta = self._dot((r, u), (w, u))
-            if not delta > 0.0:
-                raise ArithmeticError("pcg: indefinite direction, matrix not SPD")
-            alpha, beta = gamma / delta, 0.0
-            p = u.clone()
-            s = w.clone()
-            it = 0
-            while it < max_iter:
-                if it > 0:
-                    p = u + beta * p  # p_i = u_i + beta p_{i-1}
-                    s = w + beta * s  # s_i = w_i + beta s_{i-1} (= A p_i)
-                x.add_(alpha * p)
-                r.sub_(alpha * s)
-                u = self.dinv * r
-                w = A(u)
-                g1, d1, rr = self._dot((r, u), (w, u), (r, r))
-                it += 1
-                if it >= max_iter:
-                    break  # the reference leaves after max_iter updates untested
-                rel = float(np.sqrt(rr)) / bnorm
-                if rel <= tol:
-                    return it, rel
-                beta = g1 / gamma
-                den = d1 - beta * g1 / alpha  # p_{i+1} . A p_{i+1}
-                if not den > 0.0:
-                    raise ArithmeticError("pcg: indefinite direction, matrix not SPD")
-                alpha, gamma = g1 / den, g1
-        raise ArithmeticError(f"pcg: no convergence in {max_iter} iterations, "
-                              f"relative residual {rel:.17g}")
-
-
-# ---------------------------------------------------------------------------
-# GPU bindings (C ABI device entry points)
-
-def gpu_flux_local(sim, t: float, fine_radius: float = -1.0):
-    """local_fn for sharded_flux_load on this rank's GPU."""
-    import ctypes as C
-    import torch
-    L = sim._L
-    L.tg_sim_flux_local_device.argtypes = [C.c_void_p, C.c_double, C.c_double, C.c_int, C.c_int,
-                                           C.c_void_p]
-    ndk = sim.info["n_dofs_kept"]
-
-    def local(e0, e1):
-        out = torch.empty((e1 - e0) * ndk, dtype=torch.float64, device="cuda")
-        sim._check(L.tg_sim_flux_local_device(sim._h, float(t), float(fine_radius), e0, e1,
-                                              C.c_void_p(out.data_ptr())))
-        return out
-    return local
-
-
-def gpu_flux_gather(sim):
-    import ctypes as C
-    import torch
-    L = sim._L
-    L.tg_sim_flux_gather_device.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
-
-    def gather(loc_all):
-        F = torch.empty(sim.info["n_full"], dtype=torch.float64, device="cuda")
-        sim._check(L.tg_sim_flux_gather_device(sim._h, C.c_void_p(loc_all.data_ptr()),
-                                               C.c_void_p(F.data_ptr())))
-        return F
-    return gather
-
-
-def gpu_apply_slab(sim):
-    import ctypes as C
-    import torch
-    L = sim._L
-    L.tg_sim_operator_apply_slab_device.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p,
-                                                    C.c_void_p]
-    plane = sim.info["nx"] * sim.info["ny"]
-
-    def apply(k0, k1, xg):
-        y = torch.empty((k1 - k0) * plane, dtype=torch.float64, device="cuda")
-        sim._check(L.tg_sim_operator_apply_slab_device(sim._h, k0, k1, C.c_void_p(xg.data_ptr()),
-                                                       C.c_void_p(y.data_ptr())))
-        return y
-    return apply
-
-
-def gpu_inverse_diagonal(sim):
-    """1 / diag(A_ff) of the simulation's operator as a CUDA tensor (the Jacobi
-    preconditioner of SlabPCG on this GPU)."""
-    import ctypes as C
-    import torch
-    L = sim._L
-    L.tg_sim_inverse_diagonal.argtypes = [C.c_void_p, C.POINTER(C.c_double)]
-    out = np.zeros(sim.info["n_free"])
-    sim._check(L.tg_sim_inverse_diagonal(sim._h, out.ctypes.data_as(C.POINTER(C.c_double))))
-    return torch.from_numpy(out).cuda()
-
-
-def gpu_dirichlet_range(sim, t: float):
-    """fn(c0, c1) -> Dirichlet values of constrained DOFs [c0, c1) at t (CUDA
-    tensor) for sharded_points."""
-    import ctypes as C
-    import torch
-    L = sim._L
-    L.tg_sim_dirichlet_range_device.argtypes = [C.c_void_p, C.c_double, C.c_int, C.c_int,
-                                                C.c_void_p]
-
-    def fn(c0, c1):
-        out = torch.empty(max(0, c1 - c0), dtype=torch.float64, device="cuda")
-        if c1 > c0:
-            sim._check(L.tg_sim_dirichlet_range_device(sim._h, float(t), c0, c1,
-                                                       C.c_void_p(out.data_ptr())))
-        return out
-    return fn
+        import torch.distributed as dist
+        ops, got = [], {}
+        for peer, arr in send.items():
+            ops.append(dist.P2POp(dist.isend, torch.from_numpy(np.ascontiguousarray(arr)), peer))
+        for peer, shape in shapes.items():
+            got[peer] = torch.empty(shape, dtype=torch.float64)
+            ops.append(dist.P2POp(dist.irecv, got[peer], peer))
+        if ops:
+            for req in dist.batch_isend_irecv(ops):
+                req.wait()
+        return {p: t.numpy() for p, t in got.items()}
 
 
 class ShardedTimeLoop:
     """run_time_loop (proj/src/driver.cpp:105-146) on `dist.world` GPUs, one
-    Simulation per rank. Per step the superposition work — the flux load over
-    face-element slabs and the Dirichlet values over point slabs, >90 % of a
-    config-4 step — is split across ranks and all-gathered (two collectives);
-    the theta step then runs on every rank from the same loads, so every rank
-    holds the same state (bit for bit: all pieces are deterministic and
-    shard-independent)."""
+    Simulation per rank: the loads' regions and the θ-step's z-slabs split
+    over the ranks through one NCCL communicator (tg_sim_shard). With one
+    rank nothing is sharded: the steps are Simulation.advance's, bit for bit."""
 
     def __init__(self, sim, dist: Dist):
-        import ctypes as C
+        from .api import nccl_unique_id
         self.sim, self.dist = sim, dist
-        self.L = sim._L
-        self.L.tg_sim_advance_with_loads_device.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p,
-                                                           C.POINTER(C.c_long),
-                                                           C.POINTER(C.c_double)]
-        self.dt = sim.params["dt"]
-        self.step_index = 0
+        if dist.world > 1:
+            uid = dist.broadcast_bytes(nccl_unique_id() if dist.rank == 0 else None)
+            sim.shard(dist.rank, dist.world, uid)
 
     def reset(self):
         self.sim.reset()
-        self.step_index = 0
 
-    def step(self):
-        import ctypes as C
-        s, d = self.sim, self.dist
-        t1 = (self.step_index + 1) * self.dt  # driver.cpp:127
-        F1 = sharded_flux_load(gpu_flux_local(s, t1), gpu_flux_gather(s), s.info["n_face_elems"],
-                               s.info["n_dofs_kept"], d)
-        g1 = sharded_points(gpu_dirichlet_range(s, t1), s.info["n_constrained"], d)
-        it = C.c_long(0)
-        rel = C.c_double(0.0)
-        s._check(self.L.tg_sim_advance_with_loads_device(s._h, C.c_void_p(F1.data_ptr()),
-                                                         C.c_void_p(g1.data_ptr()),
-                                                         C.byref(it), C.byref(rel)))
-        self.step_index += 1
-        return it.value, rel.value
+    def step(self, n: int = 1):
+        return self.sim.advance(n)
+
+
+# ---------------------------------------------------------------------------
+# numpy model of the slab protocol (CPU tests over gloo)
+
+def _band_apply(band: np.ndarray, v: np.ndarray, axis: int, p: int, rows=None) -> np.ndarray:
+    """y = B v along `axis` with B banded, entry [i][p + j - i]; rows selects
+    the band rows of the output (a slab's own planes), v spans the rows'
+    neighbourhoods (zeros outside)."""
+    v = np.moveaxis(v, axis, 0)
+    n_out = v.shape[0] if rows is None else len(rows)
+    out = np.zeros((n_out,) + v.shape[1:])
+    for o in range(n_out):
+        i = o if rows is None else rows[o]
+        for d in range(2 * p + 1):
+            j = i + d - p
+            jj = j if rows is None else j - rows[0] + p  # v starts p below rows[0]
+            if 0 <= jj < v.shape[0]:
+                out[o] += band[i, d] * v[jj]
+    return np.moveaxis(out, 0, axis)
+
+
+class KronOperator:
+    """A = a (Mz x My x Mx) + b (Mz x My x Kx + Mz x Ky x Mx + Kz x My x Mx)
+    on an (nz, ny, nx) grid from banded 1D factors (k2_kron.cu's operator)."""
+
+    def __init__(self, M, K, a: float, b: float, p: int):
+        self.M, self.K, self.a, self.b, self.p = M, K, a, b, p
+
+    def diag(self):
+        mx, my, mz = (m[:, self.p] for m in self.M)
+        kx, ky, kz = (k[:, self.p] for k in self.K)
+        mm = np.einsum("k,j,i->kji", mz, my, mx)
+        return self.a * mm + self.b * (np.einsum("k,j,i->kji", mz, my, kx)
+                                       + np.einsum("k,j,i->kji", mz, ky, mx)
+                                       + np.einsum("k,j,i->kji", kz, my, mx))
+
+    def apply(self, v: np.ndarray, zrows=None) -> np.ndarray:
+        """A v on the planes zrows (all when None); v holds zrows +- p planes."""
+        (Mx, My, Mz), (Kx, Ky, Kz), p = self.M, self.K, self.p
+        ux, kx = _band_apply(Mx, v, 2, p), _band_apply(Kx, v, 2, p)
+        w1, w2, w3 = _band_apply(My, ux, 1, p), _band_apply(My, kx, 1, p), _band_apply(Ky, ux, 1, p)
+        s1 = self.a * w1 + self.b * (w2 + w3)
+        s2 = self.b * w1
+        return _band_apply(Mz, s1, 0, p, zrows) + _band_apply(Kz, s2, 0, p, zrows)
+
+
+class SlabModel:
+    """The slab solve of csrc/slab.cu in numpy: this rank's planes (tg_slab_plan)
+    with ghost planes, the scaled Chronopoulos-Gear Jacobi-PCG (u = D^-1 r,
+    w^ = D^-1 A u, s^ = D^-1 A p) with own-plane partial sums, the ghost planes
+    of u_0, w^_0 and every w^ exchanged with the neighbours and the partials
+    all-gathered (Dist), scalars advanced from the rank-ordered sums."""
+
+    def __init__(self, op: KronOperator, nz: int, dist: Dist):
+        from .api import slab_plan
+        self.op, self.d = op, dist
+        pl = slab_plan(nz, op.p, dist.world, dist.rank)
+        self.gz0, self.nloc, self.zo0, self.zo1 = pl["gz0"], pl["nloc"], pl["zo0"], pl["zo1"]
+        self.lo, self.hi = pl["lo"], pl["hi"]
+        self.rows = np.arange(self.gz0, self.gz0 + self.nloc)
+        self.dg = op.diag()[self.gz0:self.gz0 + self.nloc]
+
+    def _apply(self, v):  # A v on every local plane (ghost rows wrong: exchanged)
+        p = self.op.p
+        pad = np.zeros((self.nloc + 2 * p,) + v.shape[1:])
+        pad[p:p + self.nloc] = v
+        return self.op.apply(pad, self.rows)
+
+    def _exchange(self, v, parts):
+        p = self.op.p
+        send, shapes = {}, {}
+        if self.lo >= 0:
+            send[self.lo] = v[self.zo0:self.zo0 + p]
+            shapes[self.lo] = v[:p].shape
+        if self.hi >= 0:
+            send[self.hi] = v[self.zo1 - p:self.zo1]
+            shapes[self.hi] = v[:p].shape
+        got = self.d.send_recv(send, shapes) if self.d.world > 1 else {}
+        if self.lo >= 0:
+            v[:p] = got[self.lo]
+        if self.hi >= 0:
+            v[self.zo1:self.zo1 + p] = got[self.hi]
+        return sum(self.d.all_gather_array(np.asarray(parts, dtype=np.float64)))
+
+    def solve(self, b_full: np.ndarray, x_full: np.ndarray, tol: float, max_iter: int):
+        """(x on this rank's own planes, iterations, status, rel)."""
+        sl = slice(self.gz0, self.gz0 + self.nloc)
+        own = slice(self.zo0, self.zo1)
+        b, x = b_full[sl].copy(), x_full[sl].copy()
+        r = b - self._apply(x)
+        u = r / self.dg
+        tot = self._exchange(u, [np.sum(r[own] ** 2), np.sum(b[own] ** 2),
+                                 np.sum((r * u)[own]), 0.0])
+        bnorm = np.sqrt(tot[1])
+        if bnorm == 0.0:
+            return np.zeros_like(x[own]), 0, 0, 0.0
+        rel = np.sqrt(tot[0]) / bnorm
+        if max_iter <= 0 or rel <= tol:
+            return x[own], 0, 3 if max_iter <= 0 else 0, rel
+        gamma = tot[2]
+        Au = self._apply(u)
+        w = Au / self.dg
+        tot = self._exchange(w, [np.sum((Au * u)[own]), 0.0, 0.0, 0.0])
+        if not tot[0] > 0.0:
+            return x[own], 0, 4, rel
+        alpha, beta = gamma / tot[0], 0.0
+        s = np.zeros_like(u)
+        p = np.zeros_like(u)
+        it = 0
+        while True:
+            p = u + beta * p
+            x = x + alpha * p
+            s = w + beta * s
+            u = u - alpha * s
+            ru = self.dg * u
+            Au = self._apply(u)
+            w = Au / self.dg
+            tot = self._exchange(w, [np.sum((ru * u)[own]), np.sum((Au * u)[own]),
+                                     np.sum((ru * ru)[own]), 0.0])
+            it += 1
+            if it >= max_iter:
+                return x[own], it, 3, rel
+            rel = np.sqrt(tot[2]) / bnorm
+            if rel <= tol:
+                return x[own], it, 0, rel
+            g1 = tot[0]
+            beta = g1 / gamma
+            den = tot[1] - beta * g1 / alpha
+            if not den > 0.0:
+                return x[own], it, 4, rel
+            alpha, gamma = g1 / den, g1
 
 
 def init_from_env(backend: Optional[str] = None) -> Dist:

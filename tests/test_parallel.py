@@ -1,21 +1,30 @@
-"""Multi-rank logic of paper_2511_20432_b200/parallel.py on CPU (gloo,
-world_size 2): element-slab flux load (bit-identical to the reference's serial
-scatter) and z-slab Jacobi-PCG with halo exchange (same iterates as one rank).
-The compute callbacks are the C oracle (flux) and a numpy Kronecker operator
-(K2); the GPU bindings plug the C ABI device calls into the same logic."""
+"""Multi-rank logic of the multi-GPU step on CPU (gloo; world sizes 2 and 3).
+
+The device path (csrc/slab.cu, sim.cu step_loads) needs GPUs; what these
+tests check without them is its decomposition:
+  * tg_slab_plan (the product's host function) covers the free grid's planes
+    once, with P ghost planes per interior side that are exactly the
+    neighbours' own boundary planes;
+  * parallel.SlabModel — the slab protocol of k2_slab_kernel in numpy: ghost
+    planes of u_0, w^_0 and every w^ exchanged by point-to-point messages,
+    own-plane partial sums all-gathered and summed in rank order — gives the
+    single-rank solve's iterate count and solution (to rounding) over gloo;
+  * the region split of the loads (r % world == rank) covers every region
+    once.
+The device slabs themselves are compared with the single-GPU solve on a GPU
+(tests/test_slab_gpu.py)."""
 import os
 import socket
 
 import numpy as np
 import pytest
-import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2511_20432_b200.parallel import Dist, SlabPCG, partition, sharded_flux_load
+import paper_2511_20432_b200 as tg
+from paper_2511_20432_b200.api import slab_plan
+from paper_2511_20432_b200.parallel import Dist, KronOperator, SlabModel, partition
 from conftest import ROOT
-
-KW = dict(conductivity=20.0, density=4400.0, heat_capacity=600.0)
 
 
 def _free_port():
@@ -52,135 +61,74 @@ def test_partition_covers_and_balances():
             assert max(sizes) - min(sizes) <= 1
 
 
-# --- flux load ------------------------------------------------------------
-
-def _flux_rank(d: Dist, fs_path, t):
-    from oracle.pyoracle import COracle
-    z = dict(np.load(fs_path))
-    src = z.pop("sources")
-    n_full = int(z.pop("n_full"))
-    fs = z
-    o = COracle()
-    nd = fs["dofs"].shape[1]
-
-    def local(e0, e1):
-        return torch.from_numpy(o.boundary_local(fs, src, t, e0, e1, fine_radius=5e-4, **KW).ravel())
-
-    def gather(loc_all):
-        loc = loc_all.numpy().reshape(-1, nd)
-        F = np.zeros(n_full)
-        for e in range(loc.shape[0]):  # the reference's serial scatter order
-            for a in range(nd):
-                F[fs["dofs"][e, a]] += loc[e, a]
-        return F
-
-    return {"F": sharded_flux_load(local, gather, fs["dofs"].shape[0], nd, d)}
+@pytest.mark.parametrize("nz,p,world", [(65, 2, 8), (65, 2, 2), (17, 2, 3), (5, 2, 2), (9, 3, 3)])
+def test_slab_plan(nz, p, world):
+    plans = [slab_plan(nz, p, world, r) for r in range(world)]
+    own = []
+    for r, q in enumerate(plans):
+        g0, g1 = q["gz0"] + q["zo0"], q["gz0"] + q["zo1"]
+        own.append((g0, g1))
+        assert q["zo1"] - q["zo0"] >= p
+        assert q["zo0"] == (p if r > 0 else 0)  # ghosts only on interior sides
+        assert q["nloc"] - q["zo1"] == (p if r + 1 < world else 0)
+        assert q["lo"] == (r - 1 if r > 0 else -1) and q["hi"] == (r + 1 if r + 1 < world else -1)
+    assert own[0][0] == 0 and own[-1][1] == nz
+    assert all(a[1] == b[0] for a, b in zip(own, own[1:]))
+    # a rank's lower ghosts are the lower neighbour's top own planes
+    for r in range(1, world):
+        assert plans[r]["gz0"] == own[r - 1][1] - p
+    with pytest.raises(ValueError):
+        slab_plan(nz, p, nz // p + 1, 0)
 
 
-@pytest.mark.parametrize("t", [1e-4, 6e-4])
-def test_sharded_flux_load_bit_identical(ref, tmp_path, t):
-    sim = ref.sim(os.path.join(ROOT, "configs", "cfg0_parity.cfg"))
-    fs = sim.face_sets()
-    path = tmp_path / "fs.npz"
-    np.savez(path, sources=sim.sources(), n_full=sim.info["n_full"], **fs)
-    F_ref = sim.flux_load(t)
-    sim.close()
-    outs = _run(2, _flux_rank, tmp_path, str(path), t)
-    for o in outs:
-        assert np.array_equal(o["F"], F_ref)
-
-
-# --- z-slab PCG -------------------------------------------------------------
-
-def _dense(B):
-    n, w = B.shape
-    p = w // 2
-    A = np.zeros((n, n))
-    for i in range(n):
-        for d in range(-p, p + 1):
-            if 0 <= i + d < n:
-                A[i, i + d] = B[i, p + d]
-    return A
-
-
-def _kron_factors():
-    import paper_2511_20432_b200 as tg
-    s = tg.Simulation(os.path.join(ROOT, "configs", "cfg0_parity.cfg"), host_only=True)
-    Ms, Ks = zip(*[s.kron_factors(d) for d in range(3)])
-    rc = s.params["density"] * s.params["heat_capacity"]
-    a = rc / s.params["dt"]
-    b = s.params["theta"] * s.params["conductivity"]
+def _kron_problem():
+    """Config 2's free-grid operator (66 x 66 x 17 free planes, degree 2) from
+    a host-only Simulation, a seeded right-hand side and warm start."""
+    s = tg.Simulation(os.path.join(ROOT, "configs", "cfg2_raster_layer.cfg"), host_only=True)
+    p = s.info["px"]
+    M = [s.kron_factors(d)[0] for d in range(3)]
+    K = [s.kron_factors(d)[1] for d in range(3)]
+    M[2], K[2] = M[2][1:], K[2][1:]  # the bottom (constrained) layer is not a free row
+    pr = s.params
+    a = pr["density"] * pr["heat_capacity"] / pr["dt"]
+    b = pr["theta"] * pr["conductivity"]
+    shape = (M[2].shape[0], M[1].shape[0], M[0].shape[0])
     s.close()
-    Mx, My, Mz = (_dense(m) for m in Ms)
-    Kx, Ky, Kz = (_dense(k) for k in Ks)
-    # free grid: drop the constrained bottom layer (zetamin, k = 0)
-    return Mx, Kx, My, Ky, Mz[1:, 1:], Kz[1:, 1:], a, b
+    rng = np.random.default_rng(7)
+    rhs = rng.standard_normal(shape)
+    x0 = 1e-3 * rng.standard_normal(shape)
+    return KronOperator(M, K, a, b, p), rhs, x0
 
 
-def _apply(Mx, Kx, My, Ky, Mz, Kz, a, b, x):
-    """Op(a, b) x for x of shape (nz, ny, nx) (first index fastest in memory)."""
-    def k3(Z, Y, X):
-        return np.einsum("kl,jm,in,lmn->kji", Z, Y, X, x)
-    return a * k3(Mz, My, Mx) + b * (k3(Mz, My, Kx) + k3(Mz, Ky, Mx) + k3(Kz, My, Mx))
+def _slab_rank(d: Dist):
+    op, rhs, x0 = _kron_problem()
+    m = SlabModel(op, rhs.shape[0], d)
+    x, it, status, rel = m.solve(rhs, x0, 1e-12, 500)
+    return {"x": x, "it": it, "status": status, "rel": rel, "z0": m.gz0 + m.zo0}
 
 
-def _pcg_rank(d: Dist, rhs_path, single=False):
-    Mx, Kx, My, Ky, Mz, Kz, a, b = _kron_factors()
-    nz, ny, nx = Mz.shape[0], My.shape[0], Mx.shape[0]
-    p = 2
-    rhs = np.load(rhs_path)["b"].reshape(nz, ny, nx)
-    k0, k1 = partition(nz, d.world, d.rank)
-    diag = (a * np.einsum("k,j,i->kji", np.diag(Mz), np.diag(My), np.diag(Mx)) +
-            b * (np.einsum("k,j,i->kji", np.diag(Mz), np.diag(My), np.diag(Kx)) +
-                 np.einsum("k,j,i->kji", np.diag(Mz), np.diag(Ky), np.diag(Mx)) +
-                 np.einsum("k,j,i->kji", np.diag(Kz), np.diag(My), np.diag(Mx))))
-
-    def apply_slab(s0, s1, xg):
-        g0, g1 = max(0, s0 - p), min(nz, s1 + p)
-        x = xg.numpy().reshape(g1 - g0, ny, nx)
-        y = _apply(Mx, Kx, My, Ky, Mz[s0:s1, g0:g1], Kz[s0:s1, g0:g1], a, b, x)
-        return torch.from_numpy(y.ravel().copy())
-
-    solver = SlabPCG(apply_slab, torch.from_numpy((1.0 / diag[k0:k1]).ravel().copy()), ny * nx,
-                     nz, p, d)
-    x = torch.zeros((k1 - k0) * ny * nx, dtype=torch.float64)
-    it, rel = solver.solve(torch.from_numpy(rhs[k0:k1].ravel().copy()), x, 1e-12, 2000,
-                           single_reduction=single)
-    return {"x": x.numpy(), "k0": k0, "k1": k1, "it": it, "rel": rel}
+@pytest.mark.parametrize("world", [2, 3])
+def test_slab_protocol_matches_one_rank(tmp_path, world):
+    op, rhs, x0 = _kron_problem()
+    one = SlabModel(op, rhs.shape[0], Dist(0, 1))
+    x1, it1, st1, rel1 = one.solve(rhs, x0, 1e-12, 500)
+    assert st1 == 0 and it1 > 10
+    # the model is the reference's Jacobi-PCG: the true residual is tol-small
+    res = rhs - op.apply(np.pad(x1, ((op.p, op.p), (0, 0), (0, 0))), np.arange(rhs.shape[0]))
+    assert np.linalg.norm(res) / np.linalg.norm(rhs) <= 2e-12
+    outs = _run(world, _slab_rank, tmp_path)
+    x = np.concatenate([o["x"] for o in sorted(outs, key=lambda o: int(o["z0"]))])
+    for o in outs:  # every rank took the same decisions
+        assert int(o["it"]) == it1 and int(o["status"]) == 0
+        assert float(o["rel"]) == float(outs[0]["rel"])
+    assert np.abs(x - x1).max() <= 1e-10 * np.abs(x1).max()
 
 
-@pytest.mark.parametrize("single", [False, True], ids=["two-reductions", "single-reduction"])
-def test_slab_pcg_two_ranks_matches_one(tmp_path, single):
-    Mx, Kx, My, Ky, Mz, Kz, a, b = _kron_factors()
-    nz, ny, nx = Mz.shape[0], My.shape[0], Mx.shape[0]
-    rhs = np.random.default_rng(11).standard_normal(nz * ny * nx)
-    path = tmp_path / "rhs.npz"
-    np.savez(path, b=rhs)
-    one = _run(1, _pcg_rank, tmp_path, str(path), False)[0]
-    two = _run(2, _pcg_rank, tmp_path, str(path), single)
-    x2 = np.concatenate([o["x"] for o in sorted(two, key=lambda o: int(o["k0"]))])
-    assert abs(int(two[0]["it"]) - int(one["it"])) <= 1
-    assert np.abs(x2 - one["x"]).max() <= 1e-10 * np.abs(one["x"]).max()
-    # and the solution solves the assembled system
-    A = (a * np.kron(Mz, np.kron(My, Mx)) +
-         b * (np.kron(Mz, np.kron(My, Kx)) + np.kron(Mz, np.kron(Ky, Mx)) +
-              np.kron(Kz, np.kron(My, Mx))))
-    assert np.linalg.norm(A @ x2 - rhs) / np.linalg.norm(rhs) <= 1e-11
-
-
-def _points_rank(d: Dist, n):
-    from paper_2511_20432_b200.parallel import sharded_points
-    f = lambda b, e: torch.arange(b, e, dtype=torch.float64) * 0.5 + 1.0  # noqa: E731
-    return {"all": sharded_points(f, n, d).numpy(), "own": sharded_points(f, n, d, gather=False).numpy()}
-
-
-@pytest.mark.parametrize("n", [0, 7, 66564])
-def test_sharded_points_two_ranks(tmp_path, n):
-    """Point slabs (the Dirichlet values of ShardedTimeLoop) all-gathered in
-    rank order reproduce the single evaluation."""
-    outs = _run(2, _points_rank, tmp_path, n)
-    ref = np.arange(n, dtype=np.float64) * 0.5 + 1.0
-    for r, o in enumerate(outs):
-        assert np.array_equal(o["all"], ref)
-        b, e = partition(n, 2, r)
-        assert np.array_equal(o["own"], ref[b:e])
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_region_split_covers_every_region_once(world):
+    s = tg.Simulation(os.path.join(ROOT, "configs", "cfg2_raster_layer.cfg"), host_only=True)
+    n = len(s.sumfact_regions())
+    s.close()
+    owners = [[r for r in range(n) if r % world == rank] for rank in range(world)]
+    assert sorted(sum(owners, [])) == list(range(n))
+    assert max(map(len, owners)) - min(map(len, owners)) <= 1

@@ -1,11 +1,12 @@
-"""Config-4 time steps on N GPUs with parallel.ShardedTimeLoop (sharded
-superposition work, all-gathered loads, replicated theta step). Launch:
+"""Config-4 time steps on N GPUs with parallel.ShardedTimeLoop (K5 regions
+split over the ranks with the loads all-reduced, the theta-step solve on
+z-slabs with NCCL halo / partial-sum exchange). Launch:
 
   python -m torch.distributed.run --nnodes=1 --nproc-per-node N \
       --master-addr 127.0.0.1 --master-port 29600 tools/sharded_run.py [cfg] [steps]
 
-Rank 0 prints one JSON line: wall ms per step (max over ranks, after a
-barrier on each side) and CG iterations."""
+Rank 0 prints one JSON line: device ms per step (CUDA events around
+tg_sim_advance on each rank's stream, max over ranks) and CG iterations."""
 import json
 import os
 import sys
@@ -31,16 +32,12 @@ def main():
     loop = parallel.ShardedTimeLoop(sim, d)
     loop.reset()
     loop.step()  # warm-up
-    dist.barrier()
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    its = 0
-    for _ in range(steps):
-        its += loop.step()[0]
-    torch.cuda.synchronize()
-    dist.barrier()
-    ms = torch.tensor([(time.perf_counter() - t0) * 1e3 / steps], dtype=torch.float64,
-                      device=f"cuda:{local}")
+    ctx = sim.context()
+    ctx.set_profiling(True)
+    ctx.profile(reset=True)
+    its, _ = loop.step(steps)
+    prof = ctx.profile()
+    ms = torch.tensor([prof["step_ms"] / steps], dtype=torch.float64, device=f"cuda:{local}")
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
     if d.rank == 0:
         print(json.dumps({"workload": os.path.basename(cfg), "n_gpus": d.world,
