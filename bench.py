@@ -216,53 +216,68 @@ def hbm_peak():
 def config3_steps(with_cpu, steps=10):
     """Config 3 (degree-3 rational plate-with-hole part, 128x64x32 elements,
     302,974 free DOF; SURVEY.md Appendix C option A): the assembled-operator
-    path. `steps` time steps from the start (contour scan) on the device; the
-    reference's own pcg_jacobi timed beside it on the identical A_ff for a
-    bounded number of iterations."""
+    path. `steps` time steps from the start (contour scan) on the device with
+    the reference's Jacobi-PCG and with the scaled separable-approximation
+    preconditioner; the reference's own pcg_jacobi timed beside it on the
+    identical A_ff for a bounded number of iterations."""
     import paper_2511_20432_b200 as tg
-    t0 = time.perf_counter()
-    sim = tg.Simulation(CFG3)
-    setup_s = time.perf_counter() - t0
-    ctx = sim.context()
-    sim.reset()
-    sim.advance(1)
-    ctx.set_profiling(True)
-    ctx.profile(reset=True)
-    t0 = time.perf_counter()
-    iters, rel = sim.advance(steps)
-    wall = time.perf_counter() - t0
-    prof = ctx.profile()
-    ctx.set_profiling(False)
-    rp, ci, v = sim.reduced_operator()
-    n, nnz = len(rp) - 1, len(v)
-    peak, src = hbm_peak()
-    us_it = 1e3 * prof["k2_ms"] / max(1, iters)
-    # per CG iteration: A_ff once (8 B value + 4 B column per entry) and the
-    # vectors p (r), Ap (w, r), x (r, w), r (r, w), D^-1 (r, twice), p (r, w)
-    alg_bytes = 12.0 * nnz + 8.0 * n * 11
-    achieved = alg_bytes / (us_it * 1e-6) / 1e9
-    out = {"workload": "config3: degree-(3,3,3) rational plate-with-hole part (Appendix C "
+    out = {}
+    for pc in ("jacobi", "fdm"):
+        t0 = time.perf_counter()
+        sim = tg.Simulation(CFG3, preconditioner=pc)
+        setup_s = time.perf_counter() - t0
+        ctx = sim.context()
+        sim.reset()
+        sim.advance(1)
+        ctx.set_profiling(True)
+        ctx.profile(reset=True)
+        t0 = time.perf_counter()
+        iters, rel = sim.advance(steps)
+        wall = time.perf_counter() - t0
+        prof = ctx.profile()
+        ctx.set_profiling(False)
+        res = {"setup_s": setup_s, "steps": steps, "ms_per_step": wall * 1e3 / steps,
+               "theta_ms_per_step": prof["k2_ms"] / steps,
+               "theta_step_total_ms_per_step": prof["theta_step_ms"] / steps,
+               "theta_step_total_ms_per_mdof": prof["theta_step_ms"] / steps
+                                               / (sim.info["n_full"] / 1e6),
+               "cg_iterations_per_step": iters / steps}
+        if pc == "jacobi":
+            rp, ci, v = sim.reduced_operator()
+            n, nnz = len(rp) - 1, len(v)
+            peak, src = hbm_peak()
+            us_it = 1e3 * prof["k2_ms"] / max(1, iters)
+            # per CG iteration: A_ff once (8 B value + 4 B column per entry) and the
+            # vectors p (r), Ap (w, r), x (r, w), r (r, w), D^-1 (r, twice), p (r, w)
+            alg_bytes = 12.0 * nnz + 8.0 * n * 11
+            achieved = alg_bytes / (us_it * 1e-6) / 1e9
+            res.update({"us_per_cg_iteration": us_it, "nnz": nnz,
+                        "operator": "assembled A_ff in sliced ELL (32-row slices), one thread "
+                                    "per row, row sums in the reference's CSR order (bit-exact "
+                                    "rows)",
+                        "roofline": {"kernel": "csr_pcg_kernel<DevSell>", "bound": "hbm",
+                                     "achieved": achieved, "peak": peak, "unit": "GB/s",
+                                     "frac": achieved / peak, "peak_source": src,
+                                     "bytes_per_iteration": alg_bytes,
+                                     "bytes_note": "12 B per A_ff entry + 11 vector streams of "
+                                                   "8 B/DOF"}})
+        else:
+            res["preconditioner"] = ("S^-1 A~^-1 S^-1: A~ the separable approximation "
+                                     "(mean control-net arc length per axis), inverted by fast "
+                                     "diagonalization on DMMA mode products; S = sqrt(diag A / "
+                                     "diag A~)")
+        out[pc] = res
+        sim.close()
+    out["workload"] = ("config3: degree-(3,3,3) rational plate-with-hole part (Appendix C "
                        "option A), 128x64x32 elements, 311,885 DOF (302,974 free), contour + "
-                       f"hatch path; steps 2..{steps + 1} of the 5000-step run",
-           "setup_s": setup_s, "steps": steps, "ms_per_step": wall * 1e3 / steps,
-           "theta_ms_per_step": prof["k2_ms"] / steps,
-           "theta_step_total_ms_per_step": prof["theta_step_ms"] / steps,
-           "theta_ms_per_step_per_mdof": prof["k2_ms"] / steps / (sim.info["n_full"] / 1e6),
-           "theta_step_total_ms_per_mdof": prof["theta_step_ms"] / steps
-                                           / (sim.info["n_full"] / 1e6),
-           "cg_iterations_per_step": iters / steps, "us_per_cg_iteration": us_it,
-           "operator": "assembled A_ff in sliced ELL (32-row slices), one thread per row, "
-                       "row sums in the reference's CSR order (bit-exact rows)",
-           "nnz": nnz,
-           "roofline": {"kernel": "csr_pcg_kernel<DevSell>", "bound": "hbm",
-                        "achieved": achieved, "peak": peak, "unit": "GB/s",
-                        "frac": achieved / peak, "peak_source": src,
-                        "bytes_per_iteration": alg_bytes,
-                        "bytes_note": "12 B per A_ff entry + 11 vector streams of 8 B/DOF"}}
-    sim.close()
+                       f"hatch path; steps 2..{steps + 1} of the 5000-step run")
     if with_cpu:
         from oracle import pyoracle
         if pyoracle.ref_available():
+            sim = tg.Simulation(CFG3)
+            rp, ci, v = sim.reduced_operator()
+            sim.close()
+            n = len(rp) - 1
             R = pyoracle.RefLib()
             b = np.random.default_rng(3).standard_normal(n)
             k = 8
@@ -278,7 +293,8 @@ def config3_steps(with_cpu, steps=10):
                                    "sample": f"pcg_jacobi (proj/src/sparse.cpp:41-100, serial "
                                              f"as shipped) on the identical A_ff, capped at {k} "
                                              "iterations (time / (k + 1))",
-                                   "theta_ms_per_step_estimate": ms_it * iters / steps}
+                                   "theta_ms_per_step_estimate":
+                                       ms_it * out["jacobi"]["cg_iterations_per_step"]}
     return out
 
 
@@ -511,7 +527,7 @@ def theta_fdm(steps, warmup):
     k2_ms = prof["k2_ms"] / steps
     sim.close()
     return {"preconditioner": "fast diagonalization (V diag(1/(a + b(lx+ly+lz))) V^T, "
-                              "cuBLAS DGEMM mode products), same PCG stop test",
+                              "mode products on the hand-written DMMA GEMM), same PCG stop test",
             "theta_ms_per_step": k2_ms, "theta_ms_per_step_per_mdof": k2_ms / (dofs / 1e6),
             "theta_step_total_ms_per_step": prof["theta_step_ms"] / steps,
             "theta_step_total_ms_per_mdof": prof["theta_step_ms"] / steps / (dofs / 1e6),
