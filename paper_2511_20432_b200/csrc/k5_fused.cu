@@ -30,9 +30,8 @@
 // contracted on the FP64 tensor cores with mma.sync m8n8k4 (DMMA; tcgen05 has
 // no FP64 kind). DMMA and DFMA issue from one FP64 pipe on this part
 // (tools/dmma_pipe.cu: 37.0 TF/s DMMA alone, 34.1 DFMA alone, ~35 mixed), so
-// the generator's share is set by the tile shape (64 x 96: ~1/5 of the pipe
-// time on exponentials); two CTAs per SM keep their stage barriers out of
-// phase, so one CTA's exponentials overlap the other's MMAs. Work is split stream-K style: the
+// the generator's share is set by the tile shape (128 x 192: ~1/10 of the
+// pipe time on exponentials), with 16 warps per SM issuing DMMA. Work is split stream-K style: the
 // (tile, 1024-source) items of all tiles are cut evenly over one CTA per SM;
 // a CTA accumulates its run of a tile's items in registers and writes one
 // partial tile; the epilogue sums the partials in CTA order (deterministic).
@@ -240,9 +239,10 @@ __device__ __forceinline__ double sf_exp(double r2, double nisp, double magicL, 
 
 constexpr int kLd = kSfKS + 4;  // row pitch (doubles) of the A / B stages: conflict-free frags
 constexpr int kWarps = kSfThreads / 32;
-constexpr int kWN = 2 * kSfTB / kWarps;  // warp tile columns
-constexpr int kNT = kWN / 8;             // n8 fragments per warp
-static_assert(kSfTA == 64, "two warp rows of 32");
+constexpr int kWR = kSfTA / 32;               // warp rows of 32
+constexpr int kWN = kWR * kSfTB / kWarps;     // warp tile columns
+constexpr int kNT = kWN / 8;                  // n8 fragments per warp
+static_assert(kSfTA % 32 == 0 && kWarps % kWR == 0 && kWN % 8 == 0, "warp tiling");
 
 struct SfSmem {
   double tab[kExpTableSize];
@@ -253,7 +253,7 @@ struct SfSmem {
   double V[kSfTB];  // V[b], or cb[b] for vplane grids
 };
 
-__global__ void __launch_bounds__(kSfThreads, 2)
+__global__ void __launch_bounds__(kSfThreads, kSfMinBlocks)
     sf_contract_kernel(const SfGridDesc* __restrict__ grids, const SfTile* __restrict__ tiles,
                        int n_tiles, const int* __restrict__ prefix, const int* __restrict__ J,
                        const SfConst* __restrict__ cst, int max_src,
@@ -265,8 +265,8 @@ __global__ void __launch_bounds__(kSfThreads, 2)
   // the accumulators at 48 registers so 16 warps per SM issue DMMA (a warp
   // issues one only every few cycles: 2 warps per SM sub-partition left the
   // tensor pipe half idle)
-  const int wa = warp & 1, wb = warp >> 1;
-  static_assert(kSfTB == kWN * (kWarps / 2), "the warps tile the CTA tile");
+  const int wa = warp % kWR, wb = warp / kWR;
+  static_assert(kSfTB == kWN * (kWarps / kWR), "the warps tile the CTA tile");
   const int g8 = lane >> 2, q4 = lane & 3;
   for (int i = tid; i < kExpTableSize; i += kSfThreads) sm.tab[i] = tab_g[i];
 
@@ -489,7 +489,7 @@ void sf_prep(const double* d_src6, int n_act, double t, double alpha, double rcp
   sf_prep_kernel<<<grid, 256, 0, s>>>(d_src6, n_act, t, alpha, rcp, d_grids, max_src, d_cst);
 }
 
-int sf_contract_max_ctas(int sm_count) { return 2 * sm_count; }  // 2 CTAs per SM
+int sf_contract_max_ctas(int sm_count) { return kSfMinBlocks * sm_count; }
 
 void sf_contract_fused(const SfGridDesc* d_grids, const SfTile* d_tiles, int n_tiles,
                        const int* d_prefix, const int* d_J, const SfConst* d_cst, int max_src,

@@ -12,11 +12,27 @@ namespace tgb {
 
 // CTA output tile of the contraction (a rows x b columns of one grid) and the
 // sources per shared-memory stage / per stream-K work item.
-constexpr int kSfTA = 64;
-constexpr int kSfTB = 96;
+// measured (config 4, tools/k5_time.py): 64 x 96 / 256 threads / 2 CTAs per SM
+// 5.97 ms per step's contraction, 128 x 96 / 512 / 1: 5.78, 64 x 192: 5.95,
+// 128 x 192 / 512 / 1: 5.58
+#ifndef K5_TA
+#define K5_TA 128
+#endif
+#ifndef K5_TB
+#define K5_TB 192
+#endif
+#ifndef K5_THREADS
+#define K5_THREADS 512
+#endif
+#ifndef K5_MINB
+#define K5_MINB 1
+#endif
+constexpr int kSfTA = K5_TA;
+constexpr int kSfTB = K5_TB;
 constexpr int kSfKS = 32;
 constexpr int kSfItem = 1024;
-constexpr int kSfThreads = 256;  // 8 warps (2 x 4 of 32 x 24), 2 CTAs per SM
+constexpr int kSfThreads = K5_THREADS;  // 16 warps (4 x 4 of 32 x 48), 1 CTA per SM
+constexpr int kSfMinBlocks = K5_MINB;
 
 // A point set that is a tensor grid up to coordinate rounding: point (a, b)
 // sits at (xf on axis axn, U[a] on axu, V[b] on axv).
