@@ -108,47 +108,83 @@ __device__ __forceinline__ int block_max_int(int v, int* red) {
   return m;
 }
 
-// one CTA per region: J (first source failing sf_source_ok, or 0 when the
-// contraction would not pay), then E (one past the last source not culled on
-// the box, over [J, n_act))
-__global__ void sf_plan_kernel(SfPlanArgs a, const SfRegion* __restrict__ regions,
-                               int* __restrict__ Jo, int* __restrict__ Eo, SfPlanMask mask,
-                               int n_static, int* __restrict__ Jl, int* __restrict__ El) {
+// The plan in two passes over (region, source chunk) CTAs (integer min / max
+// through atomics: order-independent, so deterministic):
+//   pass 1: Jraw[r] = the first source failing sf_source_ok (n_act if none);
+//   pass 2: J[r] = Jraw, or 0 when the contraction would not pay; E[r] = one
+//           past the last source in [J, n_act) not culled on the box.
+constexpr int kPlanChunks = 16;
+
+__device__ __forceinline__ bool plan_active(const SfPlanMask& mask, int ri) {
+  const bool part = ri < mask.nt_flux ? mask.flux : ri < mask.nt_static ? mask.dir : mask.flux;
+  return part && ri % mask.world == mask.rank;
+}
+
+__global__ void sf_plan_init_kernel(int n, int n_act, int* __restrict__ Jraw,
+                                    int* __restrict__ Eo) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < n) {
+    Jraw[r] = n_act;
+    Eo[r] = 0;
+  }
+}
+
+__global__ void sf_plan_j_kernel(SfPlanArgs a, const SfRegion* __restrict__ regions,
+                                 int* __restrict__ Jraw, SfPlanMask mask) {
   __shared__ int red[32];
   const int ri = blockIdx.x;
-  const bool part = ri < mask.nt_flux ? mask.flux : ri < mask.nt_static ? mask.dir : mask.flux;
-  if (!part || ri % mask.world != mask.rank) {
-    if (threadIdx.x == 0) Jo[ri] = Eo[ri] = 0;
-    return;
-  }
+  if (!a.gemm || !plan_active(mask, ri)) return;
   const SfRegion r = regions[ri];
+  const int L = (a.n_act + kPlanChunks - 1) / kPlanChunks;
+  const int j0 = blockIdx.y * L, j1 = min(a.n_act, j0 + L);
   int J = a.n_act;
-  if (a.gemm) {
-    for (int j = threadIdx.x; j < a.n_act; j += blockDim.x)
-      if (!sf_source_ok(a.src6 + 6 * static_cast<size_t>(j), a.t, a.alpha, a.cull, r)) {
-        J = j;
-        break;
-      }
-    J = block_min_int(J, red);
-    if (r.npts < 0.0 || static_cast<double>(J) * r.npts < a.min_pairs) J = 0;
-  } else {
-    J = 0;
-  }
-  int last = J - 1;
-  for (int j = a.n_act - 1 - static_cast<int>(threadIdx.x); j >= J; j -= blockDim.x)
-    if (!sf_source_culled(a.src6 + 6 * static_cast<size_t>(j), a.t, a.alpha, a.cull, r)) {
-      last = j;
+  for (int j = j0 + threadIdx.x; j < j1; j += blockDim.x)
+    if (!sf_source_ok(a.src6 + 6 * static_cast<size_t>(j), a.t, a.alpha, a.cull, r)) {
+      J = j;
       break;
     }
-  last = block_max_int(last, red);
-  if (threadIdx.x == 0) {
-    Jo[ri] = J;
-    Eo[ri] = last + 1;
-    if (Jl && ri < n_static) {  // the static regions' last computed plan (queries)
-      Jl[ri] = J;
-      El[ri] = last + 1;
-    }
+  J = block_min_int(J, red);
+  if (threadIdx.x == 0 && J < a.n_act) atomicMin(&Jraw[ri], J);
+}
+
+__global__ void sf_plan_e_kernel(SfPlanArgs a, const SfRegion* __restrict__ regions,
+                                 const int* __restrict__ Jraw, int* __restrict__ Jo,
+                                 int* __restrict__ Eo, SfPlanMask mask, int n_static,
+                                 int* __restrict__ Jl, int* __restrict__ El) {
+  __shared__ int red[32];
+  const int ri = blockIdx.x;
+  const bool act = plan_active(mask, ri);
+  const SfRegion r = regions[ri];
+  int J = 0;
+  if (act && a.gemm) {
+    J = Jraw[ri];
+    if (r.npts < 0.0 || static_cast<double>(J) * r.npts < a.min_pairs) J = 0;
   }
+  int last = J - 1;
+  if (act) {
+    const int L = (a.n_act + kPlanChunks - 1) / kPlanChunks;
+    const int j0 = max(J, blockIdx.y * L), j1 = min(a.n_act, (blockIdx.y + 1) * L);
+    for (int j = j1 - 1 - static_cast<int>(threadIdx.x); j >= j0; j -= blockDim.x)
+      if (!sf_source_culled(a.src6 + 6 * static_cast<size_t>(j), a.t, a.alpha, a.cull, r)) {
+        last = j;
+        break;
+      }
+    last = block_max_int(last, red);
+  }
+  if (threadIdx.x == 0) {
+    if (blockIdx.y == 0) {
+      Jo[ri] = act ? J : 0;
+      if (Jl && ri < n_static && act) Jl[ri] = J;
+    }
+    if (act) atomicMax(&Eo[ri], max(J, last + 1));
+  }
+}
+
+// the static regions' last computed E (queries), after pass 2
+__global__ void sf_plan_keep_kernel(int n_static, const int* __restrict__ Eo, SfPlanMask mask,
+                                    int* __restrict__ El) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < n_static && El && plan_active(mask, r)) El[r] = Eo[r];
 }
 
 // item prefix over the tiles (one CTA; a serial scan is plenty for <= a few
@@ -470,10 +506,15 @@ __global__ void sf_add_kernel(SfAddArgs a, int e0, int e1, bool flux) {
 
 void sf_plan(const SfPlanArgs& a, const SfRegion* d_regions, int n_regions, int* d_J, int* d_E,
              const SfPlanMask& mask, int n_static_regions, int* d_Jlast, int* d_Elast,
-             cudaStream_t s) {
+             int* d_Jraw, cudaStream_t s) {
   if (n_regions <= 0) return;
-  sf_plan_kernel<<<n_regions, 256, 0, s>>>(a, d_regions, d_J, d_E, mask, n_static_regions,
-                                           d_Jlast, d_Elast);
+  sf_plan_init_kernel<<<(n_regions + 127) / 128, 128, 0, s>>>(n_regions, a.n_act, d_Jraw, d_E);
+  const dim3 grid(n_regions, kPlanChunks);
+  sf_plan_j_kernel<<<grid, 256, 0, s>>>(a, d_regions, d_Jraw, mask);
+  sf_plan_e_kernel<<<grid, 256, 0, s>>>(a, d_regions, d_Jraw, d_J, d_E, mask, n_static_regions,
+                                        d_Jlast, d_Elast);
+  sf_plan_keep_kernel<<<(n_static_regions + 127) / 128, 128, 0, s>>>(n_static_regions, d_E, mask,
+                                                                      d_Elast);
 }
 
 void sf_items(const SfTile* d_tiles, int n_tiles, const int* d_J, int* d_prefix, double* stats,

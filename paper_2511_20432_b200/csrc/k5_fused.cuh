@@ -92,7 +92,7 @@ struct SfPlanMask {
 // contraction flops (2 na nb J summed over the tiles) added to stats[0]
 void sf_plan(const SfPlanArgs& a, const SfRegion* d_regions, int n_regions, int* d_J, int* d_E,
              const SfPlanMask& mask, int n_static_regions, int* d_Jlast, int* d_Elast,
-             cudaStream_t s);
+             int* d_Jraw, cudaStream_t s);
 void sf_items(const SfTile* d_tiles, int n_tiles, const int* d_J, int* d_prefix, double* stats,
               cudaStream_t s);
 void sf_prep(const double* d_src6, int n_act, double t, double alpha, double rcp,

@@ -842,6 +842,7 @@ void Sim::sf_setup_device() {
   d_sf_stats.ensure(2);
   TG_CUDA(cudaMemsetAsync(d_sf_stats.p, 0, 2 * sizeof(double), s));
   d_sf_J.ensure(sf_regions_h.size() + nfr + 1);
+  d_sf_Jraw.ensure(sf_regions_h.size() + nfr + 1);
   d_sf_Jl.ensure(sf_regions_h.size() + 1);
   d_sf_El.ensure(sf_regions_h.size() + 1);
   TG_CUDA(cudaMemsetAsync(d_sf_Jl.p, 0, sizeof(int) * (sf_regions_h.size() + 1), s));
@@ -1131,7 +1132,7 @@ void Sim::loads_device(double t, double radius, double* d_F, double* d_g, bool g
   SfPlanArgs pa{ctx->src6.p, n_act, t, alpha, cull, sf_min_pairs, sf_on};
   SfPlanMask mask{flux, dir, sf_nt_flux, sf_nt_static, sf_rank, sf_world};
   sf_plan(pa, d_sf_regions.p, n_regs, d_sf_J.p, d_sf_E.p, mask, nreg_static, d_sf_Jl.p,
-          d_sf_El.p, s);
+          d_sf_El.p, d_sf_Jraw.p, s);
   sf_items(d_sf_tiles.p, n_tiles, d_sf_J.p, d_sf_prefix.p, d_sf_stats.p, s);
   sf_prep(ctx->src6.p, n_act, t, alpha, rcp, d_sf_grids.p, static_cast<int>(sf_grids_h.size()),
           static_cast<int>(sources.size()), d_sf_cst.p, s);

@@ -214,7 +214,7 @@ class Sim {
   DevBuf<SfTile> d_sf_tiles;
   DevBuf<SfRegion> d_sf_regions;
   DevBuf<SfConst> d_sf_cst;
-  DevBuf<int> d_sf_J, d_sf_E, d_sf_Jl, d_sf_El, d_sf_prefix, d_sf_ent_q, d_sf_ent_tile, d_sf_ent_cell,
+  DevBuf<int> d_sf_J, d_sf_E, d_sf_Jl, d_sf_El, d_sf_Jraw, d_sf_prefix, d_sf_ent_q, d_sf_ent_tile, d_sf_ent_cell,
       d_sf_ent_pos, d_sf_cta, d_sf_qelem;
   // per-step host staging (pinned ring; an event marks when a slot's copies ran)
   struct Stage {
