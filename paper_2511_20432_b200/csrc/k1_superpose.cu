@@ -104,7 +104,14 @@ constexpr int kK1Unroll = K1_UNROLL;
 // scan paths; k1_run checks it). Then rz = z - zs and fl(rz * rz) are per
 // point — the reference's own values for every pair of that point — and the
 // z-gradient is rz * sum_j w_j: two FP64 instructions fewer per pair.
-template <int P, bool GRAD, bool PLANAR>
+// BOX (K5's remainder launch): per source chunk the CTA first drops the
+// sources whose every pair with the CTA's points is culled — the squared
+// distance from the source to the bounding box of those points exceeds the
+// source's exact keep threshold (with a relative margin far above the box
+// arithmetic's rounding) — and loops over the kept ones only. The dropped
+// pairs are exact zeros in the reference too, and a kept source's pairs run
+// the exact per-pair test below, so the sums are unchanged.
+template <int P, bool GRAD, bool PLANAR, bool BOX = false>
 __global__ void __launch_bounds__(kK1Threads,
                                   P >= 6 ? 256 / kK1Threads : (P >= 4 ? K1_MINB4 : 3))
     k1_partial(const SrcRec* __restrict__ src, int n_src, int split_len,
@@ -113,6 +120,9 @@ __global__ void __launch_bounds__(kK1Threads,
   __shared__ __align__(128) SrcRec ring[kK1Stages][kK1Chunk];
   __shared__ double tab[kExpTableSize];
   __shared__ __align__(8) uint64_t bars[kK1Stages];
+  __shared__ double boxs[BOX ? 6 : 1];
+  __shared__ int keep_list[BOX ? kK1Chunk : 1];
+  __shared__ int keep_n[BOX ? kK1Chunk / 32 + 1 : 1];
 
   const int tid = threadIdx.x;
   const int s = blockIdx.y;
@@ -166,14 +176,69 @@ __global__ void __launch_bounds__(kK1Threads,
       rz2[k] = __dmul_rn(pz[k], pz[k]);
     }
   }
+  if constexpr (BOX) {  // the bounding box of the CTA's points (PLANAR: z as rz)
+    double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+    for (int k = 0; k < P; ++k)
+      if (base + k * kK1Threads < n_pts) {
+        lo[0] = fmin(lo[0], px[k]); hi[0] = fmax(hi[0], px[k]);
+        lo[1] = fmin(lo[1], py[k]); hi[1] = fmax(hi[1], py[k]);
+        lo[2] = fmin(lo[2], pz[k]); hi[2] = fmax(hi[2], pz[k]);
+      }
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        lo[c] = fmin(lo[c], __shfl_xor_sync(0xffffffffu, lo[c], o));
+        hi[c] = fmax(hi[c], __shfl_xor_sync(0xffffffffu, hi[c], o));
+      }
+    __shared__ double wbox[kK1Threads / 32][6];
+    if ((tid & 31) == 0)
+      for (int c = 0; c < 3; ++c) {
+        wbox[tid >> 5][c] = lo[c];
+        wbox[tid >> 5][3 + c] = hi[c];
+      }
+    __syncthreads();
+    if (tid < 6) {
+      double v = wbox[0][tid];
+      for (int w = 1; w < kK1Threads / 32; ++w)
+        v = tid < 3 ? fmin(v, wbox[w][tid]) : fmax(v, wbox[w][tid]);
+      boxs[tid] = v;
+    }
+    __syncthreads();
+  }
 
   for (int c = 0; c < n_chunks; ++c) {
     const int buf = c % kK1Stages;
     mbar_wait(&bars[buf], static_cast<uint32_t>((c / kK1Stages) & 1));
     const int cnt = min(kK1Chunk, len - c * kK1Chunk);
     const SrcRec* rb = ring[buf];
+    int n_iter = cnt;
+    if constexpr (BOX) {  // the chunk's sources that reach the CTA's box, in order
+      bool keep = false;
+      if (tid < cnt) {
+        const SrcRec& q = rb[tid];
+        const double dx = fmax(fmax(boxs[0] - q.sx, q.sx - boxs[3]), 0.0);
+        const double dy = fmax(fmax(boxs[1] - q.sy, q.sy - boxs[4]), 0.0);
+        const double dz = PLANAR ? fmax(fmax(boxs[2], -boxs[5]), 0.0)
+                                 : fmax(fmax(boxs[2] - q.sz, q.sz - boxs[5]), 0.0);
+        keep = (dx * dx + dy * dy + dz * dz) * (1.0 - 1e-9) <= q.thr;
+      }
+      const unsigned m = __ballot_sync(0xffffffffu, keep);
+      if (tid < kK1Chunk && (tid & 31) == 0) keep_n[tid >> 5] = __popc(m);
+      __syncthreads();
+      if (tid < kK1Chunk && keep) {
+        int pos = __popc(m & ((1u << (tid & 31)) - 1u));
+        for (int w = 0; w < (tid >> 5); ++w) pos += keep_n[w];
+        keep_list[pos] = tid;
+      }
+      n_iter = 0;
+      for (int w = 0; w < kK1Chunk / 32; ++w) n_iter += keep_n[w];
+      __syncthreads();
+    }
 #pragma unroll kK1Unroll
-    for (int j = 0; j < cnt; ++j) {
+    for (int jj = 0; jj < n_iter; ++jj) {
+      const int j = BOX ? keep_list[jj] : jj;
       const double4 a = *reinterpret_cast<const double4*>(&rb[j].sx);      // sx sy sz nisp
       const double4 b = *reinterpret_cast<const double4*>(&rb[j].magicL);  // magicL gfac thr band
       const double4 q = *reinterpret_cast<const double4*>(&rb[j].q0);      // q0 q1 q2 -
@@ -359,6 +424,15 @@ void k1_launch_partial(const SrcRec* d_rec, int n_src, const double* d_pts,
   const int split_len = (n_src + S - 1) / S;
   const int ppc = kK1Threads * P;
   dim3 grid((n_pts + ppc - 1) / ppc, S);
+  if (rg.cta_region && grad && P == 7) {  // K5's remainder: per-CTA box culling of sources
+    if (planar)
+      k1_partial<7, true, true, true><<<grid, kK1Threads, 0, stream>>>(
+          d_rec, n_src, split_len, d_pts, d_index, n_pts, d_part, zs, rg);
+    else
+      k1_partial<7, true, false, true><<<grid, kK1Threads, 0, stream>>>(
+          d_rec, n_src, split_len, d_pts, d_index, n_pts, d_part, zs, rg);
+    return;
+  }
 #define TG_K1_LAUNCH(PP, GG, PLN)                                                         \
   k1_partial<PP, GG, PLN><<<grid, kK1Threads, 0, stream>>>(d_rec, n_src, split_len, d_pts,     \
                                                           d_index, n_pts, d_part, zs, rg)

@@ -15,6 +15,7 @@
 #include <functional>
 #include <limits>
 #include <numeric>
+#include <tuple>
 
 #include "context.hpp"
 #include "host/config.hpp"
@@ -741,8 +742,29 @@ void Sim::sf_setup_host() {
     }
   }
   sf_nt_static = static_cast<int>(sf_tiles_h.size());
-  // remainder entries: per tile its points, padded to whole K1 CTAs
+  // remainder entries: per tile its points in compact 2D blocks (columns of
+  // kBlockA cells along a, b slower, a fastest), so that each K1 CTA's 1792
+  // points span a small box and its per-CTA source culling drops more of the
+  // history; padded to whole K1 CTAs
   sf_k1_ppc = kK1Threads * 7;  // k1_partial<7, GRAD> (the remainder launch)
+  constexpr int kBlockA = 48;
+  for (int t = 0; t < sf_nt_static; ++t) {
+    std::vector<int> ord(tile_pts[t].size());
+    std::iota(ord.begin(), ord.end(), 0);
+    const auto& cells = tile_cell[t];
+    auto key = [&](int i) {
+      const int a = cells[i] % kSfTA, b = cells[i] / kSfTA;
+      return std::make_tuple(a / kBlockA, b, a);
+    };
+    std::stable_sort(ord.begin(), ord.end(), [&](int x, int y) { return key(x) < key(y); });
+    std::vector<int> p2(ord.size()), c2(ord.size());
+    for (size_t i = 0; i < ord.size(); ++i) {
+      p2[i] = tile_pts[t][ord[i]];
+      c2[i] = cells[ord[i]];
+    }
+    tile_pts[t].swap(p2);
+    tile_cell[t].swap(c2);
+  }
   sf_ent_q.clear();
   sf_ent_tile.clear();
   sf_ent_cell.clear();
@@ -1077,6 +1099,24 @@ void Sim::loads_device(double t, double radius, double* d_F, double* d_g, bool g
         }
       }
       const size_t n = fq.size() - e0;
+      if (sf_fine_ok) {  // compact 2D blocks per K1 CTA, as the static regions
+        std::vector<int> ord(n);
+        std::iota(ord.begin(), ord.end(), 0);
+        auto key = [&](int i) {
+          const int l = fq[e0 + i] - tqb;
+          return std::make_tuple(sf_h_fa[l] / 48, sf_h_fb[l], sf_h_fa[l]);
+        };
+        std::stable_sort(ord.begin(), ord.end(), [&](int x, int y) { return key(x) < key(y); });
+        auto permute = [&](std::vector<int>& v) {
+          std::vector<int> tmp(n);
+          for (size_t i = 0; i < n; ++i) tmp[i] = v[e0 + ord[i]];
+          std::copy(tmp.begin(), tmp.end(), v.begin() + e0);
+        };
+        permute(fq);
+        permute(fpos);
+        permute(ftile);
+        permute(fcell);
+      }
       const size_t pad = (n + sf_k1_ppc - 1) / sf_k1_ppc * sf_k1_ppc;
       for (size_t i = n; i < pad; ++i) {
         fq.push_back(fq[e0]);
