@@ -53,18 +53,31 @@ __global__ void __launch_bounds__(128) mode_gemm_kernel(GemmOp op) {
   const double* B = op.B + bz * op.sbb;
   double acc[4][4][2] = {};
   const bool a_kfast = op.sak == 1, b_kfast = op.sbk == 1;
-  for (int k0 = 0; k0 < op.K; k0 += kGK) {
-    for (int e = tid; e < kGT * kGK; e += 128) {  // A tile (m, k)
+  constexpr int kPer = kGT * kGK / 128;  // elements of each tile per thread
+  double ra[kPer], rb[kPer];
+  // the next k chunk into registers (its latency overlaps this chunk's MMAs)
+  auto fetch = [&](int k0) {
+#pragma unroll
+    for (int r = 0; r < kPer; ++r) {
+      const int e = tid + 128 * r;
       const int m = a_kfast ? e / kGK : e % kGT, k = a_kfast ? e % kGK : e / kGT;
       const int gm = m0 + m, gk = k0 + k;
-      As[m][k] = (gm < op.M && gk < op.K) ? A[gm * op.sam + gk * op.sak] : 0.0;
+      ra[r] = (gm < op.M && gk < op.K) ? A[gm * op.sam + gk * op.sak] : 0.0;
+      const int n = b_kfast ? e / kGK : e % kGT, kb = b_kfast ? e % kGK : e / kGT;
+      const int gn = n0 + n, gkb = k0 + kb;
+      rb[r] = (gn < op.N && gkb < op.K) ? B[gkb * op.sbk + gn * op.sbn] : 0.0;
     }
-    for (int e = tid; e < kGT * kGK; e += 128) {  // B tile, stored (n, k)
-      const int n = b_kfast ? e / kGK : e % kGT, k = b_kfast ? e % kGK : e / kGT;
-      const int gn = n0 + n, gk = k0 + k;
-      Bs[n][k] = (gn < op.N && gk < op.K) ? B[gk * op.sbk + gn * op.sbn] : 0.0;
+  };
+  fetch(0);
+  for (int k0 = 0; k0 < op.K; k0 += kGK) {
+#pragma unroll
+    for (int r = 0; r < kPer; ++r) {
+      const int e = tid + 128 * r;
+      As[a_kfast ? e / kGK : e % kGT][a_kfast ? e % kGK : e / kGT] = ra[r];
+      Bs[b_kfast ? e / kGK : e % kGT][b_kfast ? e % kGK : e / kGT] = rb[r];
     }
     __syncthreads();
+    if (k0 + kGK < op.K) fetch(k0 + kGK);
 #pragma unroll
     for (int kk = 0; kk < kGK; kk += 4) {
       double af[4], bf[4];

@@ -135,6 +135,38 @@ def test_config2_mid_run_consecutive_steps(cfg2, ref):
     r.close()
 
 
+def test_config2_contraction_forced_mid_run(ref, monkeypatch):
+    """Config 2's loads with K5's contraction forced on every region
+    (TG_SF_MIN_PAIRS=0; by default config 2's <= 2k active sources stay on K1)
+    against the reference at mid-run instants, including a fine-rule step."""
+    monkeypatch.setenv("TG_SF_MIN_PAIRS", "0")
+    s = tg.Simulation(CFG[2], solver_tol=1e-12)
+    r = ref.sim(CFG[2], threads=THREADS, solver_tol=1e-12)
+    dt = r.params["dt"]
+    for k in (700, 1500, 1999):
+        F, g = s.flux_load(k * dt), s.dirichlet_values(k * dt)
+        assert s.sumfact_stats()["last_j_flux"] > 0
+        check_loads(F, r.flux_load(k * dt, threads=THREADS), g, r.dirichlet(k * dt), f"t{k}")
+    r.close()
+    s.close()
+
+
+def test_flux_load_focus_argument(ref):
+    """tg_sim_flux_load's focus_xyz (SURVEY §8(b)): the newest active source's
+    position reproduces the default call bit for bit; a focus far from every
+    face selects no fine-rule element, as the reference's radius 0 does."""
+    s = tg.Simulation(CFG[2])
+    r = ref.sim(CFG[2], threads=THREADS)
+    t = 1234 * s.params["dt"]
+    src = s.sources()
+    newest = src[np.nonzero(src[:, 4] <= t)[0][-1], :3]
+    assert np.array_equal(s.flux_load(t, focus=newest), s.flux_load(t))
+    far = s.flux_load(t, focus=(1.0, 1.0, 1.0))
+    assert normwise(far, r.flux_load_radius(t, 0.0)) <= 1e-10
+    r.close()
+    s.close()
+
+
 # ------------------------------------------------------------------ config 3
 def test_config3_full_size_steps(ref):
     s = tg.Simulation(CFG[3], solver_tol=1e-12)
