@@ -145,7 +145,8 @@ def test_config2_contraction_forced_mid_run(ref, monkeypatch):
     dt = r.params["dt"]
     for k in (700, 1500, 1999):
         F, g = s.flux_load(k * dt), s.dirichlet_values(k * dt)
-        assert s.sumfact_stats()["last_j_flux"] > 0
+        J, _ = s.sumfact_last_plan()
+        assert (J > 0).any()  # regions far from the young part of the scan contract
         check_loads(F, r.flux_load(k * dt, threads=THREADS), g, r.dirichlet(k * dt), f"t{k}")
     r.close()
     s.close()
