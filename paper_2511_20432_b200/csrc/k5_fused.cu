@@ -404,13 +404,15 @@ __global__ void __launch_bounds__(kSfThreads, kSfMinBlocks)
       generate(0);
       if (n_stage > 1) load_cst(1, 1);
       __syncthreads();
+      // one barrier per stage: the constants of stage st + 2 go into cs[buf]
+      // (read by generate(st) before the previous barrier), stage st + 1 is
+      // generated into buffer buf ^ 1 (last read by contract(st - 1)) beside
+      // stage st's MMAs on buffer buf
       for (int st = 0; st < n_stage; ++st) {
         const int buf = st & 1;
-        if (st + 1 < n_stage) generate(buf ^ 1);  // next stage beside this one's MMAs
-        if (active) contract(buf);
-        __syncthreads();  // stage buf consumed; buf ^ 1 generated; cst[buf] free
         if (st + 2 < n_stage) load_cst(st + 2, buf);
-        // (cst[buf ^ 1] was read by generate(buf ^ 1) above, before the barrier)
+        if (st + 1 < n_stage) generate(buf ^ 1);
+        if (active) contract(buf);
         __syncthreads();
       }
     }
