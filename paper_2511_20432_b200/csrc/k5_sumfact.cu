@@ -84,29 +84,27 @@ bool sf_make_grid(const double* pts, long n, double tol, SfGrid& g) {
   return true;
 }
 
-bool sf_source_eligible(const double* p, double t, double alpha, double cull, const double lo[3],
-                        const double hi[3], double delta) {
+bool sf_region_ok(const double* p, double t, double alpha, double cull, const SfRegion& r) {
   const double dt = t - p[5];
-  if (!(dt > 0.0)) return true;  // skipped by the reference, zero column here
+  if (!(dt > 0.0)) return true;  // skipped by the reference: a zero column
   const double spread = 4.0 * alpha * dt;
   double r2 = 0.0;
   for (int ax = 0; ax < 3; ++ax) {
-    const double a = lo[ax] - p[ax], b = hi[ax] - p[ax];
+    const double a = r.lo[ax] - r.delta - p[ax], b = r.hi[ax] + r.delta - p[ax];
     r2 += std::max(a * a, b * b);
   }
   if (!(r2 * (1.0 + 1e-9) <= cull * spread)) return false;
   // grid rounding: |d(arg)| <= sum over axes 2 |d| delta / s with |d| <= sqrt(cull s)
-  return 36.0 * cull * delta * delta <= 1e-24 * spread;
+  return 36.0 * cull * r.delta * r.delta <= 1e-24 * spread;
 }
 
-bool sf_source_culled(const double* p, double t, double alpha, double cull, const double lo[3],
-                      const double hi[3]) {
+bool sf_region_culled(const double* p, double t, double alpha, double cull, const SfRegion& r) {
   const double dt = t - p[5];
   if (!(dt > 0.0)) return true;
   const double spread = 4.0 * alpha * dt;
   double r2 = 0.0;  // squared distance from the source to the box
   for (int ax = 0; ax < 3; ++ax) {
-    const double d = std::max({lo[ax] - p[ax], p[ax] - hi[ax], 0.0});
+    const double d = std::max({r.lo[ax] - r.delta - p[ax], p[ax] - r.hi[ax] - r.delta, 0.0});
     r2 += d * d;
   }
   return r2 * (1.0 - 1e-9) > cull * spread;

@@ -5,6 +5,8 @@
 
 #include <vector>
 
+#include "k5_fused.cuh"
+
 namespace tgb {
 
 // A point set that is a tensor grid up to coordinate rounding: point i sits at
@@ -25,18 +27,12 @@ struct SfGrid {
 // cluster and the other two span exactly one point per (a, b) cell.
 bool sf_make_grid(const double* pts, long n, double tol, SfGrid& out);
 
-// Sources [0, J) may take the GEMM path for points in the box [lo, hi] at t
-// when none of their pairs can be culled there (the reference skips a pair iff
-// r.r / spread > cull) and the grid's coordinate rounding moves no term by
-// more than ~1e-12 relative. Causally inactive sources are eligible (their
-// terms are exact zeros on both paths).
-bool sf_source_eligible(const double* src6, double t, double alpha, double cull,
-                        const double lo[3], const double hi[3], double delta);
-
-// Every pair of the source with a point in [lo, hi] is culled by the
-// reference (or the source is causally inactive at t): its terms are exact
-// zeros there, and K1 may skip it.
-bool sf_source_culled(const double* src6, double t, double alpha, double cull,
-                      const double lo[3], const double hi[3]);
+// The region tests of the K5 plan (restated on the device in k5_fused.cu's
+// sf_source_ok / sf_source_culled): `ok` = no point of the region's box
+// (+- delta) is in the source's cull range and the grid rounding moves no term
+// by more than ~1e-12 relative (causally inactive sources are ok: zero
+// columns); `culled` = every pair of the source with the box is culled.
+bool sf_region_ok(const double* src6, double t, double alpha, double cull, const SfRegion& r);
+bool sf_region_culled(const double* src6, double t, double alpha, double cull, const SfRegion& r);
 
 }  // namespace tgb

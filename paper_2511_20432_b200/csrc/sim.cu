@@ -913,36 +913,6 @@ void Sim::release_stages() {
   }
 }
 
-namespace {
-
-// the device plan's region tests on the host (sf_plan_kernel)
-bool host_source_ok(const double* p, double t, double alpha, double cull, const SfRegion& r) {
-  const double dt = t - p[5];
-  if (!(dt > 0.0)) return true;
-  const double spread = 4.0 * alpha * dt;
-  double r2 = 0.0;
-  for (int ax = 0; ax < 3; ++ax) {
-    const double a = r.lo[ax] - r.delta - p[ax], b = r.hi[ax] + r.delta - p[ax];
-    r2 += std::max(a * a, b * b);
-  }
-  if (!(r2 * (1.0 + 1e-9) <= cull * spread)) return false;
-  return 36.0 * cull * r.delta * r.delta <= 1e-24 * spread;
-}
-
-bool host_source_culled(const double* p, double t, double alpha, double cull,
-                        const SfRegion& r) {
-  const double dt = t - p[5];
-  if (!(dt > 0.0)) return true;
-  const double spread = 4.0 * alpha * dt;
-  double r2 = 0.0;
-  for (int ax = 0; ax < 3; ++ax) {
-    const double d = std::max({r.lo[ax] - r.delta - p[ax], p[ax] - r.hi[ax] - r.delta, 0.0});
-    r2 += d * d;
-  }
-  return r2 * (1.0 - 1e-9) > cull * spread;
-}
-
-}  // namespace
 
 void Sim::sf_plan_host(double t, int* J, int* E) {
   const double alpha = cfg.material.diffusivity(), cull = cfg.superpose.cull_exponent;
@@ -955,11 +925,11 @@ void Sim::sf_plan_host(double t, int* J, int* E) {
     const SfRegion& R = sf_regions_h[r];
     int j = 0;
     if (sf_on) {
-      while (j < n_act && host_source_ok(src + 6 * static_cast<size_t>(j), t, alpha, cull, R)) ++j;
+      while (j < n_act && sf_region_ok(src + 6 * static_cast<size_t>(j), t, alpha, cull, R)) ++j;
       if (static_cast<double>(j) * R.npts < sf_min_pairs) j = 0;
     }
     int e = n_act;
-    while (e > j && host_source_culled(src + 6 * static_cast<size_t>(e - 1), t, alpha, cull, R))
+    while (e > j && sf_region_culled(src + 6 * static_cast<size_t>(e - 1), t, alpha, cull, R))
       --e;
     J[r] = j;
     E[r] = e;
