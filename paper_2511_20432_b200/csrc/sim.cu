@@ -1278,7 +1278,7 @@ PcgStatus Sim::theta_step_device(double tol, int max_iter) {
   if (!diag_ok) throw numeric_error("pcg: non-positive diagonal, matrix not SPD");
   ctx->timer.timed(3, s, [&] { theta_step_launch(tol, max_iter); });
   TG_CUDA(cudaMemcpyAsync(h_status, d_status.p, sizeof(PcgStatus), cudaMemcpyDeviceToHost, s));
-  TG_CUDA(cudaStreamSynchronize(s));
+  stream_wait(comm.get(), s);
   const PcgStatus st = *h_status;
   ctx->timer.k2_bytes += 104.0 * n_free * st.iterations;  // SURVEY.md §8d algorithmic bytes
   k2_iterations += st.iterations;
@@ -1361,7 +1361,7 @@ void Sim::reset() {
   TG_CUDA(cudaMemsetAsync(d_x.p, 0, sizeof(double) * n_free, s));
   step_loads(0.0, d_Fn.p, d_gn.p);
   step = 0;
-  TG_CUDA(cudaStreamSynchronize(s));
+  stream_wait(comm.get(), s);
 }
 
 PcgStatus Sim::advance() {
@@ -1467,7 +1467,7 @@ long Sim::advance_steps(int n, double* last_rel) {
     ++step;
   }
   });
-  TG_CUDA(cudaStreamSynchronize(s));
+  stream_wait(comm.get(), s);
   for (int k = 0; k < n; ++k) {
     const PcgStatus& st = h_steps[k];
     it += st.iterations;

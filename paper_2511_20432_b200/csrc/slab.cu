@@ -21,10 +21,12 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <chrono>
 #include <cstdlib>
 #include <cstring>
 #include <stdexcept>
 #include <string>
+#include <thread>
 
 namespace tgb {
 
@@ -51,6 +53,7 @@ struct NcclApi {
   ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
   ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
   ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*CommAbort)(ncclComm_t) = nullptr;
   ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t,
@@ -84,7 +87,7 @@ NcclApi& api() {
            sym(n.Recv, "ncclRecv") && sym(n.AllGather, "ncclAllGather") &&
            sym(n.AllReduce, "ncclAllReduce") && sym(n.Broadcast, "ncclBroadcast") &&
            sym(n.GroupStart, "ncclGroupStart") && sym(n.GroupEnd, "ncclGroupEnd") &&
-           sym(n.ErrorString, "ncclGetErrorString");
+           sym(n.ErrorString, "ncclGetErrorString") && sym(n.CommAbort, "ncclCommAbort");
     return n;
   }();
   return a;
@@ -125,6 +128,31 @@ std::shared_ptr<NcclComm> nccl_comm(int rank, int world, const char id[128], int
   c->rank = rank;
   c->world = world;
   return c;
+}
+
+void stream_wait(NcclComm* c, cudaStream_t s) {
+  if (!c || c->world == 1) {
+    TG_CUDA(cudaStreamSynchronize(s));
+    return;
+  }
+  // a rank that never joins a collective must not hang the others forever:
+  // poll, and abort the communicator after TG_NCCL_TIMEOUT seconds (120)
+  static const double limit = [] {
+    const char* e = std::getenv("TG_NCCL_TIMEOUT");
+    return e ? std::atof(e) : 120.0;
+  }();
+  const auto t0 = std::chrono::steady_clock::now();
+  for (;;) {
+    const cudaError_t q = cudaStreamQuery(s);
+    if (q == cudaSuccess) return;
+    if (q != cudaErrorNotReady) TG_CUDA(q);
+    if (std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() > limit) {
+      if (c->c) api().CommAbort(c->c);
+      c->c = nullptr;
+      throw cuda_error("multi-GPU step timed out (a rank missed a collective); NCCL aborted");
+    }
+    std::this_thread::sleep_for(std::chrono::microseconds(20));
+  }
 }
 
 void nccl_allreduce_sum(NcclComm& c, double* buf, size_t n, cudaStream_t s) {
@@ -291,7 +319,7 @@ void SlabSolver::solve(const double* d_rhs, double* d_x, double a, double b, dou
       // the state the last launch wrote (identical on every slab)
       TG_CUDA(cudaMemcpyAsync(h_state_, ranks_[0]->st.p + (launch & 1), sizeof(SlabState),
                               cudaMemcpyDeviceToHost, s));
-      TG_CUDA(cudaStreamSynchronize(s));
+      stream_wait(comm_.get(), s);
       if (h_state_->done) break;
     }
   }

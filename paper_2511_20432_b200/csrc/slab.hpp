@@ -29,6 +29,9 @@ bool nccl_available();
 void nccl_unique_id(char out[128]);
 std::shared_ptr<NcclComm> nccl_comm(int rank, int world, const char id[128], int device);
 void nccl_allreduce_sum(NcclComm& c, double* buf, size_t n, cudaStream_t s);
+// cudaStreamSynchronize, bounded in time when a multi-rank communicator is in
+// use (the communicator is aborted and cuda_error thrown after TG_NCCL_TIMEOUT s)
+void stream_wait(NcclComm* c, cudaStream_t s);
 void nccl_broadcast_parts(NcclComm& c, double* buf, const std::vector<size_t>& off,
                           const std::vector<size_t>& count, cudaStream_t s);
 
