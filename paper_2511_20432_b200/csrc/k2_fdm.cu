@@ -274,10 +274,53 @@ void fdm_apply(const FdmDev& F, const double* r, double* z, double* t1, double* 
   if (F.sinv) diag_mul(N, F.sinv, z, z, s);
 }
 
+namespace {
+// device scalars of the preconditioned solve (FdmWork::dots, 8 doubles)
+enum { kRz = 0, kRzOld = 1, kPap = 2, kRr = 3, kFail = 4 };
+
+// p = z (first) or z + (rz / rz_old) p
+__global__ void direction_dev_kernel(long n, bool first, const double* __restrict__ sc,
+                                     const double* __restrict__ z, double* __restrict__ p) {
+  const double beta = first ? 0.0 : sc[kRz] / sc[kRzOld];
+  for (long f = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; f < n;
+       f += static_cast<long>(gridDim.x) * blockDim.x)
+    p[f] = first ? z[f] : z[f] + beta * p[f];
+}
+
+// x += alpha p, r -= alpha Ap with alpha = rz / pAp; pAp <= 0: no update, the
+// failure flag is set (sparse.cpp:83-86); rz_old = rz for the next direction
+__global__ void update_dev_kernel(long n, double* __restrict__ sc, const double* __restrict__ p,
+                                  const double* __restrict__ Ap, double* __restrict__ x,
+                                  double* __restrict__ r) {
+  const double pAp = sc[kPap], rz = sc[kRz];
+  if (!(pAp > 0.0)) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) sc[kFail] = 1.0;
+    return;
+  }
+  const double alpha = rz / pAp;
+  for (long f = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; f < n;
+       f += static_cast<long>(gridDim.x) * blockDim.x) {
+    x[f] += alpha * p[f];
+    r[f] -= alpha * Ap[f];
+  }
+}
+
+__global__ void shift_rz_kernel(double* sc) { sc[kRzOld] = sc[kRz]; }
+
+// a.b into the device scalar slot (fixed-order reduction)
+void dot_dev(long n, const double* a, const double* b, const FdmWork& w, double* slot,
+             cudaStream_t s) {
+  dot2_partial<<<kDotBlocks, kDotThreads, 0, s>>>(n, a, b, nullptr, nullptr, w.partials);
+  dot2_final<<<1, kDotThreads, 0, s>>>(kDotBlocks, w.partials, w.dots + 6);
+  TG_CUDA(cudaMemcpyAsync(slot, w.dots + 6, sizeof(double), cudaMemcpyDeviceToDevice, s));
+}
+}  // namespace
+
+// The reference's loop with every scalar kept on the device: per iteration
+// one host synchronisation (the stop test on r.r), none for r.z and p.Ap.
 PcgStatus pcg_precond_solve(const std::function<void(const double*, double*)>& apply,
                             const FdmDev& F, long n, const double* rhs, double* x,
                             const FdmWork& w, double tol, int max_iter, cudaStream_t s) {
-
   const int G = grid_for(n);
   double bb = 0.0, unused = 0.0;
   dot2(n, rhs, rhs, nullptr, nullptr, w, s, bb, unused);
@@ -286,31 +329,29 @@ PcgStatus pcg_precond_solve(const std::function<void(const double*, double*)>& a
     TG_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * n, s));
     return PcgStatus{0, 0, 0.0, 0.0};
   }
-  // r = b - A x (sparse.cpp:61-69); the preconditioned residual z = P r is
-  // formed lazily after the stop test (same iterates as the reference's
-  // order, one preconditioner apply fewer on the converged iteration)
+  double* sc = w.dots;
+  TG_CUDA(cudaMemsetAsync(sc, 0, 6 * sizeof(double), s));
+  // r = b - A x (sparse.cpp:61-69); z = P r is formed after the stop test
   apply(x, w.Ap);
   residual_kernel<<<G, 256, 0, s>>>(n, rhs, w.Ap, w.r);
-  double rr = 0.0, rz = 0.0, rz_old = 0.0;
+  double rr = 0.0;
   dot2(n, w.r, w.r, nullptr, nullptr, w, s, rr, unused);
   double rel = 0.0;
   for (int it = 0; it < max_iter; ++it) {
     rel = std::sqrt(rr) / bnorm;
     if (rel <= tol) return PcgStatus{it, 0, rel, bnorm};
     fdm_apply(F, w.r, w.z, w.t1, w.t2, s);
-    dot2(n, w.r, w.z, nullptr, nullptr, w, s, rz, unused);
-    if (it == 0) {
-      TG_CUDA(cudaMemcpyAsync(w.p, w.z, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
-    } else {
-      direction_kernel<<<G, 256, 0, s>>>(n, rz / rz_old, w.z, w.p);  // p = z + beta p
-    }
-    rz_old = rz;
+    dot_dev(n, w.r, w.z, w, sc + kRz, s);
+    direction_dev_kernel<<<G, 256, 0, s>>>(n, it == 0, sc, w.z, w.p);  // p = z + beta p
+    shift_rz_kernel<<<1, 1, 0, s>>>(sc);
     apply(w.p, w.Ap);
-    double pAp = 0.0;
-    dot2(n, w.p, w.Ap, nullptr, nullptr, w, s, pAp, unused);
-    if (!(pAp > 0.0)) return PcgStatus{it, 4, rel, bnorm};
-    update_kernel<<<G, 256, 0, s>>>(n, rz / pAp, w.p, w.Ap, x, w.r);
-    dot2(n, w.r, w.r, nullptr, nullptr, w, s, rr, unused);
+    dot_dev(n, w.p, w.Ap, w, sc + kPap, s);
+    update_dev_kernel<<<G, 256, 0, s>>>(n, sc, w.p, w.Ap, x, w.r);
+    dot_dev(n, w.r, w.r, w, sc + kRr, s);
+    TG_CUDA(cudaMemcpyAsync(w.h_dots, sc + kRr, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
+    TG_CUDA(cudaStreamSynchronize(s));
+    if (w.h_dots[1] != 0.0) return PcgStatus{it, 4, rel, bnorm};
+    rr = w.h_dots[0];
   }
   return PcgStatus{max_iter, 3, rel, bnorm};
 }

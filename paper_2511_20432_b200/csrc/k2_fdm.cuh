@@ -39,7 +39,7 @@ struct FdmWork {
   double* t1;
   double* t2;
   double* partials;  // >= 2 * 512
-  double* dots;      // device, 2
+  double* dots;      // device, 8 (the solve's scalars)
   double* h_dots;    // pinned host, 2
 };
 // x_map / p_map: TMA descriptors of x and w.p for the operator applies (or null)

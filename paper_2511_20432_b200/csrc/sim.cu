@@ -400,7 +400,7 @@ void Sim::setup_device(int device, int preconditioner) {
       }
       fdm.dinv = d_fdmDinv.p;
       d_w2.ensure(n_free);
-      d_dots.ensure(2);
+      d_dots.ensure(8);
       TG_CUDA(cudaMallocHost(&h_dots, 2 * sizeof(double)));
       use_fdm = true;
       use_cg1 = false;
@@ -517,7 +517,7 @@ void Sim::setup_general_fdm(cudaStream_t s) {
   d_z.ensure(n_free);
   d_p2.ensure(n_free);
   d_w2.ensure(n_free);
-  d_dots.ensure(2);
+  d_dots.ensure(8);
   TG_CUDA(cudaMallocHost(&h_dots, 2 * sizeof(double)));
   use_fdm = true;
 }
