@@ -523,9 +523,9 @@ class Simulation:
         self._check(self._L.tg_sim_set_region_split(self._h, int(rank), int(world)))
 
     def sumfact_regions(self):
-        """K5 regions (flux tiles, then Greville tiles): (n, 8) = lo[3], hi[3],
-        delta, points."""
-        out = np.zeros((self.sumfact_stats()["regions"], 8))
+        """K5 regions (flux tiles, then Greville tiles): (n, 9) = lo[3], hi[3],
+        delta, points, work (contraction cost per source in points)."""
+        out = np.zeros((self.sumfact_stats()["regions"], 9))
         self._check(self._L.tg_sim_sumfact_regions(self._h, _p(out)))
         return out
 

@@ -939,13 +939,22 @@ struct ProCg1S {  // rings: 0 u_i, 1 w^_i, 2 s^_{i-1}; centre ring: x, p_{i-1}
   OwnDiag<P> od;
   double gamma, rr;
   int zo0 = -(1 << 30), zo1 = 1 << 30;  // planes whose points enter the dot products
+  // x update: 0 every sweep (x += alpha p_i); deferred (the single solve):
+  // 1 = this sweep leaves x alone (no x traffic), 2 = x += alpha_prev p_{i-1}
+  // + alpha p_i (the same two fma roundings as two sweeps of mode 0)
+  int xmode = 0;
+  double alpha_prev = 0.0;
 
   __device__ void issue(const Seg& sg, int step) const {
     const int q = *cseq + step, slot = q & 1;
     constexpr uint32_t bytes = CentreRing<PL>::kBox * 8;
     const int kin0 = sg.k0 - P + PL * step;
-    mbar_arrive_expect_tx(&cr->bar[0][slot], bytes);
-    tma_load_box(cr->buf[0][slot], mx, sg.x0, sg.y0, kin0, &cr->bar[0][slot]);
+    if (xmode == 1) {
+      mbar_arrive(&cr->bar[0][slot]);  // completes the slot's phase without a copy
+    } else {
+      mbar_arrive_expect_tx(&cr->bar[0][slot], bytes);
+      tma_load_box(cr->buf[0][slot], mx, sg.x0, sg.y0, kin0, &cr->bar[0][slot]);
+    }
     mbar_arrive_expect_tx(&cr->bar[1][slot], bytes);
     tma_load_box(cr->buf[1][slot], mp, sg.x0, sg.y0, kin0, &cr->bar[1][slot]);
   }
@@ -964,7 +973,7 @@ struct ProCg1S {  // rings: 0 u_i, 1 w^_i, 2 s^_{i-1}; centre ring: x, p_{i-1}
     if (s == 0 && own) od.set(*g, i, j);
     const int q = *cseq + s, cs = q & 1;
     const uint32_t par = static_cast<uint32_t>((q >> 1) & 1);
-    mbar_wait(&cr->bar[0][cs], par);
+    if (xmode != 1) mbar_wait(&cr->bar[0][cs], par);
     mbar_wait(&cr->bar[1][cs], par);
     if (s + 1 == nsteps) *cseq += nsteps;
     const double* u_ = sm.ring[0][slot[0]];
@@ -978,10 +987,13 @@ struct ProCg1S {  // rings: 0 u_i, 1 w^_i, 2 s^_{i-1}; centre ring: x, p_{i-1}
           const int e = l * D::PLANE + (ty + P) * D::RX + tx + P;
           const int c = (l * kKronTY + ty) * kKronTX + tx;
           const size_t f = (static_cast<size_t>(kin) * ny + j) * nx + i;
-          const double uo = u_[e];
-          const double pnew = fma(beta, cr->buf[1][cs][c], uo);    // p_i = u_i + beta p_{i-1}
+          const double uo = u_[e], pold = cr->buf[1][cs][c];
+          const double pnew = fma(beta, pold, uo);                 // p_i = u_i + beta p_{i-1}
           p[f] = pnew;
-          x[f] = fma(alpha, pnew, cr->buf[0][cs][c]);              // x_{i+1}
+          if (xmode == 0)
+            x[f] = fma(alpha, pnew, cr->buf[0][cs][c]);            // x_{i+1}
+          else if (xmode == 2)
+            x[f] = fma(alpha, pnew, fma(alpha_prev, pold, cr->buf[0][cs][c]));
           const double snew = fma(beta, s_[e], w_[e]);             // s^_i = w^_i + beta s^_{i-1}
           const double unew = fma(-alpha, snew, uo);               // u_{i+1}
           s_out[f] = snew;
@@ -1233,7 +1245,7 @@ __global__ void __launch_bounds__(kThreads, K2_MINB)
     if (lead) *w.status = PcgStatus{0, 4, rel, bnorm};
     return;
   }
-  double alpha = gamma / tot[0], beta = 0.0;
+  double alpha = gamma / tot[0], beta = 0.0, alpha_prev = 0.0;
   int cur = 0;
   Seg seg0{};
   const bool has_seg = first_segment(T, gridDim.x, blockIdx.x, seg0);
@@ -1244,6 +1256,9 @@ __global__ void __launch_bounds__(kThreads, K2_MINB)
   while (it < max_iter) {
     ProCg1S<P, PL> pc{alpha, beta, x,   w.p,  w.r[cur ^ 1], w.s[cur ^ 1], nx, ny, cr, &maps.xc,
                       &maps.pc, &cseq, &g, a,   b,            {{}, zb, g.n[2]}, 0.0, 0.0};
+    // x is read and written every second sweep only (80 -> 72 B/DOF/iteration)
+    pc.xmode = (it & 1) ? 2 : 1;
+    pc.alpha_prev = alpha_prev;
     EpiCg1S<P, ProCg1S<P, PL>> e{w.w[cur ^ 1], &pc, a, b, 0.0};
     const Inputs<NIN> in = inputs(cur);
 #if K2_STUDY_NOSWEEP  // latency study only (tools/k2_iter_time.py): barrier + reduction alone
@@ -1287,8 +1302,15 @@ __global__ void __launch_bounds__(kThreads, K2_MINB)
       if (primed) drain_ring<P, PL, NIN>(seg0, sm, seq);
       break;
     }
+    alpha_prev = alpha;
     alpha = g1 / den;
     gamma = g1;
+  }
+  if (it > 0 && ((it - 1) & 1) == 0) {  // the last sweep deferred its x update
+    const size_t n = static_cast<size_t>(nx) * ny * g.n[2];
+    for (size_t f = static_cast<size_t>(blockIdx.x) * kThreads + threadIdx.y * kKronTX + threadIdx.x;
+         f < n; f += static_cast<size_t>(gridDim.x) * kThreads)
+      x[f] = fma(alpha, w.p[f], x[f]);
   }
   if (lead) *w.status = PcgStatus{it, status, rel, bnorm};
 #endif

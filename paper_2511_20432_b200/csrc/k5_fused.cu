@@ -158,7 +158,7 @@ __global__ void sf_plan_e_kernel(SfPlanArgs a, const SfRegion* __restrict__ regi
   int J = 0;
   if (act && a.gemm) {
     J = Jraw[ri];
-    if (r.npts < 0.0 || static_cast<double>(J) * r.npts < a.min_pairs) J = 0;
+    if (r.work < 0.0 || static_cast<double>(J) * r.work < a.min_pairs) J = 0;
   }
   int last = J - 1;
   if (act) {
@@ -273,10 +273,19 @@ __device__ __forceinline__ double sf_exp(double r2, double nisp, double magicL, 
   return __dmul_rn(sc, q);
 }
 
+__device__ __forceinline__ void cp_async8(double* dst, const double* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src)
+               : "memory");
+}
+
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.wait_all;" ::: "memory");
+}
+
 constexpr int kLd = kSfKS + 4;  // row pitch (doubles) of the A / B stages: conflict-free frags
-constexpr int kWarps = kSfThreads / 32;
-constexpr int kWR = kSfTA / 32;               // warp rows of 32
-constexpr int kWN = kWR * kSfTB / kWarps;     // warp tile columns
+constexpr int kWarps = kSfWarps;
+constexpr int kWR = kSfWR;
+constexpr int kWN = kSfWN;
 constexpr int kNT = kWN / 8;                  // n8 fragments per warp
 static_assert(kSfTA % 32 == 0 && kWarps % kWR == 0 && kWN % 8 == 0, "warp tiling");
 
@@ -301,7 +310,8 @@ __global__ void __launch_bounds__(kSfThreads, kSfMinBlocks)
   // the accumulators at 48 registers so 16 warps per SM issue DMMA (a warp
   // issues one only every few cycles: 2 warps per SM sub-partition left the
   // tensor pipe half idle)
-  const int wa = warp % kWR, wb = warp / kWR;
+  int wa, wb;
+  sf_warp_block(warp, wa, wb);
   static_assert(kSfTB == kWN * (kWarps / kWR), "the warps tile the CTA tile");
   const int g8 = lane >> 2, q4 = lane & 3;
   for (int i = tid; i < kExpTableSize; i += kSfThreads) sm.tab[i] = tab_g[i];
@@ -342,11 +352,14 @@ __global__ void __launch_bounds__(kSfThreads, kSfMinBlocks)
     const int n_stage = (j1 - j0 + kSfKS - 1) / kSfKS;
     // stage constants: thread tid loads field tid & 7 of source tid >> 3
     // (coalesced); padded sources get zero columns
+    // (cp.async: the copy lands while the stage's MMAs run; each thread waits
+    // for its own copies before the stage barrier that publishes them)
     auto load_cst = [&](int st, int buf) {
       for (int e = tid; e < 8 * kSfKS; e += kSfThreads) {
         const int j = j0 + st * kSfKS + (e >> 3), f = e & 7;
-        const double* src = reinterpret_cast<const double*>(cg + min(j, max_src - 1)) + f;
-        sm.cs[buf][f][e >> 3] = (j < j1) ? *src : (f == 3 ? kExpMagic : 0.0);
+        // padding columns (j >= j1) read entry max_src - 1: always a zero factor
+        const double* src = reinterpret_cast<const double*>(cg + (j < j1 ? j : max_src - 1));
+        cp_async8(&sm.cs[buf][f][e >> 3], src + f);
       }
     };
     auto generate = [&](int buf) {
@@ -400,9 +413,11 @@ __global__ void __launch_bounds__(kSfThreads, kSfMinBlocks)
 
     if (n_stage > 0) {
       load_cst(0, 0);
+      cp_async_wait_all();
       __syncthreads();
       generate(0);
       if (n_stage > 1) load_cst(1, 1);
+      cp_async_wait_all();
       __syncthreads();
       // one barrier per stage: the constants of stage st + 2 go into cs[buf]
       // (read by generate(st) before the previous barrier), stage st + 1 is
@@ -413,6 +428,7 @@ __global__ void __launch_bounds__(kSfThreads, kSfMinBlocks)
         if (st + 2 < n_stage) load_cst(st + 2, buf);
         if (st + 1 < n_stage) generate(buf ^ 1);
         if (active) contract(buf);
+        cp_async_wait_all();
         __syncthreads();
       }
     }

@@ -33,6 +33,18 @@ constexpr int kSfKS = 32;
 constexpr int kSfItem = 1024;
 constexpr int kSfThreads = K5_THREADS;  // 16 warps (4 x 4 of 32 x 48), 1 CTA per SM
 constexpr int kSfMinBlocks = K5_MINB;
+constexpr int kSfWarps = kSfThreads / 32;
+constexpr int kSfWR = kSfTA / 32;                 // warp blocks per tile column (32 rows each)
+constexpr int kSfWN = kSfWR * kSfTB / kSfWarps;   // columns per warp block
+
+// Warp w of a CTA -> its block (rows [32 wa, +32), columns [kSfWN wb, +kSfWN)):
+// the rows rotate with the column, so the blocks of one block row or column
+// sit on different SM sub-partitions (w % 4, one FP64 pipe each) and a partial
+// tile's active warps spread over the four pipes.
+__host__ __device__ inline void sf_warp_block(int w, int& wa, int& wb) {
+  wb = w / kSfWR;
+  wa = (w + wb) % kSfWR;
+}
 
 // A point set that is a tensor grid up to coordinate rounding: point (a, b)
 // sits at (xf on axis axn, U[a] on axu, V[b] on axv).
@@ -55,18 +67,21 @@ struct SfTile {
 // A region: points whose box [lo, hi] (+- delta per axis) decides which
 // sources no cull can reach anywhere in it (the contraction's prefix [0, J))
 // and which are culled everywhere in it (dropped from the pair-wise
-// remainder [J, E)). npts: its point count (profitability).
+// remainder [J, E)). npts: its point count; work: the contraction cost of its tiles per source, in
+// points (sf_tile_cost x kSfTA x kSfTB summed over the tiles; the profitability
+// test), < 0: never contracted.
 struct SfRegion {
   double lo[3], hi[3];
   double delta;
   double npts;
+  double work;
 };
 
 struct SfPlanArgs {
   const double* src6;
   int n_act;           // the causally active prefix (later sources are exact zeros)
   double t, alpha, cull;
-  double min_pairs;    // J * npts below this: no contraction for the region (K1 is cheaper)
+  double min_pairs;    // J * work below this: no contraction for the region (K1 is cheaper)
   bool gemm;           // false: J = 0 everywhere (every pair on K1)
 };
 
@@ -103,7 +118,8 @@ void sf_prep(const double* d_src6, int n_act, double t, double alpha, double rcp
 // items per tile in registers (DMMA m8n8k4) and writes one partial tile per
 // (tile t, CTA c) to slot t + c of `scratch` (kSfTA * kSfTB doubles each, cell
 // (a, b) at a + kSfTA * b). Deterministic: the split depends only on the item
-// count and `ctas`.
+// count and `ctas`. d_cst: one row of max_src SfConst per grid (sf_prep); entry
+// max_src - 1 of every row must be a zero factor (max_src > the source count).
 void sf_contract_fused(const SfGridDesc* d_grids, const SfTile* d_tiles, int n_tiles,
                        const int* d_prefix, const int* d_J, const SfConst* d_cst, int max_src,
                        const double* d_tab, double* d_scratch, int ctas, cudaStream_t s);

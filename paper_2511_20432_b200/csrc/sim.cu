@@ -536,6 +536,50 @@ std::vector<std::pair<int, int>> split_even(int n, int cap) {
   return out;
 }
 
+// the same number of pieces: full pieces of cap, the remainder last
+std::vector<std::pair<int, int>> split_full(int n, int cap) {
+  std::vector<std::pair<int, int>> out;
+  for (int a = 0; a < n; a += cap) out.emplace_back(a, std::min(cap, n - a));
+  if (out.empty()) out.emplace_back(0, n);
+  return out;
+}
+
+// A tile's time per stage in full-tile stages: the MMAs of its busiest SM
+// sub-partition (the active warp blocks, sf_warp_block) plus the generator
+// (every row of A and B, partial tiles too: about 0.13 of a full stage,
+// profiles/r02_k5_ncu_summary.md).
+double sf_tile_cost(int na, int nb) {
+  int per[4] = {0, 0, 0, 0};
+  for (int w = 0; w < kSfWarps; ++w) {
+    int wa, wb;
+    sf_warp_block(w, wa, wb);
+    if (32 * wa < na && kSfWN * wb < nb) ++per[w % 4];
+  }
+  const int m = *std::max_element(per, per + 4);
+  return m / (kSfWarps / 4.0) + 0.13;
+}
+
+// the CTA tiles of an na x nb grid (row pieces, column pieces): nearly equal
+// pieces, or full pieces and a remainder, per axis, whichever costs less
+// (e.g. 258 x 258: 128 + 128 + 2 rows x 129 + 129 columns beats 3 x 86 rows)
+void sf_split_tiles(int na, int nb, std::vector<std::pair<int, int>>& as,
+                    std::vector<std::pair<int, int>>& bs) {
+  const std::vector<std::pair<int, int>> ca[2] = {split_even(na, kSfTA), split_full(na, kSfTA)};
+  const std::vector<std::pair<int, int>> cb[2] = {split_even(nb, kSfTB), split_full(nb, kSfTB)};
+  double best = 1e300;
+  for (int i = 0; i < 2; ++i)
+    for (int j = 0; j < 2; ++j) {
+      double c = 0.0;
+      for (const auto& a : ca[i])
+        for (const auto& b : cb[j]) c += sf_tile_cost(a.second, b.second);
+      if (c < best - 1e-9) {
+        best = c;
+        as = ca[i];
+        bs = cb[j];
+      }
+    }
+}
+
 SfRegion box_of(const SfGrid& g, int a0, int na, int b0, int nb) {
   SfRegion r{};
   r.lo[g.axn] = r.hi[g.axn] = g.xf;
@@ -545,6 +589,7 @@ SfRegion box_of(const SfGrid& g, int a0, int na, int b0, int nb) {
   r.hi[g.axv] = g.V[b0 + nb - 1];
   r.delta = g.delta;
   r.npts = static_cast<double>(na) * nb;
+  r.work = 0.0;  // set with the region's tiles
   return r;
 }
 
@@ -697,13 +742,15 @@ void Sim::sf_setup_host() {
   std::vector<std::vector<int>> tile_cell;
   auto add_tiles = [&](const SfGrid& g, int grid) {
     const int na = static_cast<int>(g.U.size()), nb = static_cast<int>(g.V.size());
-    const auto as = split_even(na, kSfTA), bs = split_even(nb, kSfTB);
+    std::vector<std::pair<int, int>> as, bs;
+    sf_split_tiles(na, nb, as, bs);
     const int first = static_cast<int>(sf_tiles_h.size());
     for (const auto& [b0, nbt] : bs)
       for (const auto& [a0, nat] : as) {
         const int r = static_cast<int>(sf_regions_h.size());
         sf_tiles_h.push_back(SfTile{grid, a0, b0, nat, nbt, r});
         sf_regions_h.push_back(box_of(g, a0, nat, b0, nbt));
+        sf_regions_h.back().work = sf_tile_cost(nat, nbt) * kSfTA * kSfTB;
       }
     tile_pts.resize(sf_tiles_h.size());
     tile_cell.resize(sf_tiles_h.size());
@@ -885,7 +932,9 @@ void Sim::sf_setup_device() {
     TG_CUDA(cudaMemcpyAsync(d_qx.p + 3 * (static_cast<size_t>(tqb) + tqf), grev.data(),
                             grev.size() * sizeof(double), cudaMemcpyHostToDevice, s));
   }
-  d_sf_cst.ensure(sf_grids_h.size() * std::max<size_t>(1, sources.size()));
+  // one row of max_src = n_sources + 1 per grid: entry n_sources is always a zero
+  // factor (the contraction's padding columns)
+  d_sf_cst.ensure(sf_grids_h.size() * (sources.size() + 1));
   d_sf_scratch.ensure((sf_nt_static + ft + sf_contract_max_ctas(ctx->sm_count) + 1) *
                       static_cast<size_t>(kSfTA * kSfTB));
   TG_CUDA(cudaStreamSynchronize(s));
@@ -926,7 +975,7 @@ void Sim::sf_plan_host(double t, int* J, int* E) {
     int j = 0;
     if (sf_on) {
       while (j < n_act && sf_region_ok(src + 6 * static_cast<size_t>(j), t, alpha, cull, R)) ++j;
-      if (static_cast<double>(j) * R.npts < sf_min_pairs) j = 0;
+      if (R.work < 0.0 || static_cast<double>(j) * R.work < sf_min_pairs) j = 0;
     }
     int e = n_act;
     while (e > j && sf_region_culled(src + 6 * static_cast<size_t>(e - 1), t, alpha, cull, R))
@@ -1033,12 +1082,13 @@ void Sim::loads_device(double t, double radius, double* d_F, double* d_g, bool g
         const int a0 = rc[f][0], b0 = rc[f][1];
         const int na = rc[f][2] - a0 + 1, nb = rc[f][3] - b0 + 1;
         fregs.push_back(box_of(g, a0, na, b0, nb));
-        as = split_even(na, kSfTA);
-        bs = split_even(nb, kSfTB);
+        sf_split_tiles(na, nb, as, bs);
         for (const auto& [bb, nbt] : bs)
-          for (const auto& [aa, nat] : as)
+          for (const auto& [aa, nat] : as) {
             ftiles.push_back(SfTile{sf_grid_fine0 + static_cast<int>(f), a0 + aa, b0 + bb, nat,
                                     nbt, reg});
+            fregs.back().work += sf_tile_cost(nat, nbt) * kSfTA * kSfTB;
+          }
       } else {  // fine points not on grids: all their sources pair-wise
         SfRegion all{};
         for (int ax = 0; ax < 3; ++ax) {
@@ -1046,6 +1096,7 @@ void Sim::loads_device(double t, double radius, double* d_F, double* d_g, bool g
           all.hi[ax] = 1e300;
         }
         all.npts = -1.0;
+        all.work = -1.0;
         fregs.push_back(all);
       }
       const size_t e0 = fq.size();
@@ -1145,11 +1196,11 @@ void Sim::loads_device(double t, double radius, double* d_F, double* d_g, bool g
           d_sf_El.p, d_sf_Jraw.p, s);
   sf_items(d_sf_tiles.p, n_tiles, d_sf_J.p, d_sf_prefix.p, d_sf_stats.p, s);
   sf_prep(ctx->src6.p, n_act, t, alpha, rcp, d_sf_grids.p, static_cast<int>(sf_grids_h.size()),
-          static_cast<int>(sources.size()), d_sf_cst.p, s);
+          static_cast<int>(sources.size()) + 1, d_sf_cst.p, s);
   const int ctas = sf_contract_max_ctas(ctx->sm_count);
   ctx->timer.timed(5, s, [&] {
     sf_contract_fused(d_sf_grids.p, d_sf_tiles.p, n_tiles, d_sf_prefix.p, d_sf_J.p, d_sf_cst.p,
-                      static_cast<int>(sources.size()), d_sf_tab.p, d_sf_scratch.p, ctas, s);
+                      static_cast<int>(sources.size()) + 1, d_sf_tab.p, d_sf_scratch.p, ctas, s);
   });
   ctx->timer.launches += 4;
   // the pair-wise remainder: K1 over every entry with its region's [J, E)

@@ -190,13 +190,14 @@ int tg_sim_sumfact_regions(tg_sim* s, double* out) {
   return sim_guard(s, [&](Sim& m) {
     const auto& R = m.sf_regions();
     for (size_t r = 0; r < R.size(); ++r) {
-      double* o = out + 8 * r;
+      double* o = out + 9 * r;
       for (int a = 0; a < 3; ++a) {
         o[a] = R[r].lo[a];
         o[3 + a] = R[r].hi[a];
       }
       o[6] = R[r].delta;
       o[7] = R[r].npts;
+      o[8] = R[r].work;
     }
   }, false);
 }

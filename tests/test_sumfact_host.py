@@ -49,14 +49,14 @@ def _plan(src, t, alpha, cull, reg, min_pairs):
     active = dt > 0.0
     spread = 4.0 * alpha * dt
     p = src[:, :3]
-    lo, hi, delta, npts = reg[0:3] - reg[6], reg[3:6] + reg[6], reg[6], reg[7]
+    lo, hi, delta, work = reg[0:3] - reg[6], reg[3:6] + reg[6], reg[6], reg[8]
     r2max = np.maximum((lo - p) ** 2, (hi - p) ** 2).sum(axis=1)
     ok = ~active | ((r2max * (1.0 + 1e-9) <= cull * spread)
                     & (36.0 * cull * delta * delta <= 1e-24 * spread))
     bad = np.flatnonzero(~ok)
     n_act = int(np.flatnonzero(active)[-1]) + 1 if active.any() else 0
     J = int(bad[0]) if len(bad) and bad[0] < n_act else n_act
-    if J * npts < min_pairs:
+    if work < 0 or J * work < min_pairs:
         J = 0
     d = np.maximum(np.maximum(lo - p, p - hi), 0.0)
     culled = ~active | ((d * d).sum(axis=1) * (1.0 - 1e-9) > cull * spread)
