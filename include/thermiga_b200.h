@@ -280,9 +280,7 @@ int tg_sim_shard(tg_sim* sim, int rank, int world, const char* id128);
 int tg_sim_set_slabs(tg_sim* sim, int n);
 int tg_slab_plan(int nz, int p, int world, int rank, int* out6);
 /* K5 regions (one per contraction tile of the face grids, then of the
- * Greville grid): out (n_regions x 9) = lo[3], hi[3], delta, points, work
- * (the contraction cost of its tiles per source in points: J * work below
- * the profitability threshold sends the region to the pair-wise path). */
+ * Greville grid): out (n_regions x 8) = lo[3], hi[3], delta, points. */
 int tg_sim_sumfact_regions(tg_sim* sim, double* out);
 /* The K5 plan at time t restated on the host (no device needed): per region
  * the contraction prefix J (sources [0, J)) and the end E of the pair-wise
@@ -290,6 +288,12 @@ int tg_sim_sumfact_regions(tg_sim* sim, double* out);
 int tg_sim_sumfact_plan(tg_sim* sim, double t, int* J, int* E);
 /* The plan the device computed in the last flux-load / Dirichlet call. */
 int tg_sim_sumfact_last_plan(tg_sim* sim, int* J, int* E);
+/* Per region the contraction's source count Jc: J plus the sources of
+ * [J, E) that no cull reaches anywhere in the region either (they join the
+ * contraction; the pair-wise remainder skips them). Host restatement at t /
+ * the last device plan. */
+int tg_sim_sumfact_counts(tg_sim* sim, double t, int* Jc);
+int tg_sim_sumfact_last_counts(tg_sim* sim, int* Jc);
 
 #ifdef __cplusplus
 }

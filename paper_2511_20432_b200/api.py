@@ -394,6 +394,8 @@ def _bind_sim(L):
     L.tg_sim_set_region_split.argtypes = [C.c_void_p, C.c_int, C.c_int]
     L.tg_sim_sumfact_plan.argtypes = [C.c_void_p, C.c_double, _ip, _ip]
     L.tg_sim_sumfact_last_plan.argtypes = [C.c_void_p, _ip, _ip]
+    L.tg_sim_sumfact_counts.argtypes = [C.c_void_p, C.c_double, _ip]
+    L.tg_sim_sumfact_last_counts.argtypes = [C.c_void_p, _ip]
     L._sim_bound = True
 
 
@@ -523,9 +525,9 @@ class Simulation:
         self._check(self._L.tg_sim_set_region_split(self._h, int(rank), int(world)))
 
     def sumfact_regions(self):
-        """K5 regions (flux tiles, then Greville tiles): (n, 9) = lo[3], hi[3],
-        delta, points, work (contraction cost per source in points)."""
-        out = np.zeros((self.sumfact_stats()["regions"], 9))
+        """K5 regions (flux tiles, then Greville tiles): (n, 8) = lo[3], hi[3],
+        delta, points."""
+        out = np.zeros((self.sumfact_stats()["regions"], 8))
         self._check(self._L.tg_sim_sumfact_regions(self._h, _p(out)))
         return out
 
@@ -546,6 +548,17 @@ class Simulation:
         self._check(self._L.tg_sim_sumfact_last_plan(self._h, J.ctypes.data_as(_ip),
                                                      E.ctypes.data_as(_ip)))
         return J, E
+
+    def sumfact_counts(self, t: float = None):
+        """Per region the contraction's source count Jc (J + the eligible
+        sources of [J, E)): the host restatement at t, or (t None) the last
+        device plan."""
+        Jc = np.zeros(self.sumfact_stats()["regions"], dtype=np.int32)
+        if t is None:
+            self._check(self._L.tg_sim_sumfact_last_counts(self._h, Jc.ctypes.data_as(_ip)))
+        else:
+            self._check(self._L.tg_sim_sumfact_counts(self._h, float(t), Jc.ctypes.data_as(_ip)))
+        return Jc
 
     def last_local_loads(self):
         """Per face element local loads of the last flux_load ((n_face_elems,

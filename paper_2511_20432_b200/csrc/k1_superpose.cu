@@ -223,6 +223,13 @@ __global__ void __launch_bounds__(kK1Threads,
         const double dz = PLANAR ? fmax(fmax(boxs[2], -boxs[5]), 0.0)
                                  : fmax(fmax(boxs[2] - q.sz, q.sz - boxs[5]), 0.0);
         keep = (dx * dx + dy * dy + dz * dz) * (1.0 - 1e-9) <= q.thr;
+        if (rg.okbits && keep) {  // in the region's contraction (k5_fused.cu's list)
+          // (re-read per chunk: nothing stays live across the pair loop)
+          const int r = rg.cta_region[blockIdx.x], Jr = rg.J[r];
+          const int d = begin + c * kK1Chunk + tid - Jr;
+          if (Jr > 0)
+            keep = !((rg.okbits[static_cast<size_t>(r) * rg.words + (d >> 5)] >> (d & 31)) & 1u);
+        }
       }
       const unsigned m = __ballot_sync(0xffffffffu, keep);
       if (tid < kK1Chunk && (tid & 31) == 0) keep_n[tid >> 5] = __popc(m);

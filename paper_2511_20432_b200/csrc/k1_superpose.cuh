@@ -33,11 +33,14 @@ constexpr int kMaxSplits = 16;  // source splits of one launch (k1_choose_splits
 
 // Per-CTA source ranges (K5's remainder launch): CTA x takes only the sources
 // [J[r], E[r]) of its region r = cta_region[x], split over grid.y; null =
-// the launch's one range.
+// the launch's one range. okbits (when J[r] > 0): bit j - J[r] of row r
+// (words per row) set = source j is in the region's contraction; skipped here.
 struct K1Ranges {
   const int* cta_region = nullptr;
   const int* J = nullptr;
   const int* E = nullptr;
+  const unsigned* okbits = nullptr;
+  int words = 0;
 };
 
 void k1_upload_exp_table(cudaStream_t stream);

@@ -158,7 +158,8 @@ __global__ void sf_plan_e_kernel(SfPlanArgs a, const SfRegion* __restrict__ regi
   int J = 0;
   if (act && a.gemm) {
     J = Jraw[ri];
-    if (r.work < 0.0 || static_cast<double>(J) * r.work < a.min_pairs) J = 0;
+    if (r.npts < 0.0 || (static_cast<double>(J) * r.npts < a.min_pairs && J < a.min_sources))
+      J = 0;
   }
   int last = J - 1;
   if (act) {
@@ -187,9 +188,47 @@ __global__ void sf_plan_keep_kernel(int n_static, const int* __restrict__ Eo, Sf
   if (r < n_static && El && plan_active(mask, r)) El[r] = Eo[r];
 }
 
+// the eligible sources of [J, E) per region, in order (one CTA per region)
+__global__ void sf_plan_list_kernel(SfPlanArgs a, const SfRegion* __restrict__ regions,
+                                    const int* __restrict__ Jo, const int* __restrict__ Eo,
+                                    SfLists L, SfPlanMask mask, int n_static) {
+  __shared__ int wcount[8];
+  const int ri = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int J = Jo[ri], E = Eo[ri];
+  int count = 0;
+  if (J > 0) {
+    const SfRegion r = regions[ri];
+    int* el = L.elist + static_cast<size_t>(ri) * L.cap;
+    unsigned* bits = L.okbits + static_cast<size_t>(ri) * L.words;
+    for (int base = J; base < E; base += 256) {
+      const int j = base + tid;
+      const bool ok =
+          j < E && sf_source_ok(a.src6 + 6 * static_cast<size_t>(j), a.t, a.alpha, a.cull, r);
+      const unsigned m = __ballot_sync(0xffffffffu, ok);
+      if (lane == 0) {
+        wcount[warp] = __popc(m);
+        if (base - J + 32 * warp < E - J) bits[((base - J) >> 5) + warp] = m;
+      }
+      __syncthreads();
+      int pos = count + __popc(m & ((1u << lane) - 1u)), tot = 0;
+      for (int w = 0; w < 8; ++w) {
+        if (w < warp) pos += wcount[w];
+        tot += wcount[w];
+      }
+      if (ok) el[pos] = j;
+      count += tot;
+      __syncthreads();
+    }
+  }
+  if (tid == 0) {
+    L.Jc[ri] = J + count;
+    if (L.Jclast && ri < n_static && plan_active(mask, ri)) L.Jclast[ri] = J + count;
+  }
+}
+
 // item prefix over the tiles (one CTA; a serial scan is plenty for <= a few
 // thousand tiles)
-__global__ void sf_items_kernel(const SfTile* __restrict__ tiles, int n, const int* __restrict__ J,
+__global__ void sf_items_kernel(const SfTile* __restrict__ tiles, int n, const int* __restrict__ Jc,
                                 int* __restrict__ prefix, double* __restrict__ stats) {
   if (threadIdx.x != 0) return;
   int acc = 0;
@@ -198,7 +237,7 @@ __global__ void sf_items_kernel(const SfTile* __restrict__ tiles, int n, const i
     prefix[t] = acc;
     const SfTile tl = tiles[t];
     if (tl.na > 0 && tl.nb > 0) {
-      const int j = J[tl.region];
+      const int j = Jc[tl.region];
       acc += (j + kSfItem - 1) / kSfItem;
       flops += 2.0 * tl.na * tl.nb * static_cast<double>(j);
     }
@@ -301,7 +340,7 @@ struct SfSmem {
 __global__ void __launch_bounds__(kSfThreads, kSfMinBlocks)
     sf_contract_kernel(const SfGridDesc* __restrict__ grids, const SfTile* __restrict__ tiles,
                        int n_tiles, const int* __restrict__ prefix, const int* __restrict__ J,
-                       const SfConst* __restrict__ cst, int max_src,
+                       SfLists L, const SfConst* __restrict__ cst, int max_src,
                        const double* __restrict__ tab_g, double* __restrict__ scratch) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   SfSmem& sm = *reinterpret_cast<SfSmem*>(smem_raw);
@@ -333,7 +372,9 @@ __global__ void __launch_bounds__(kSfThreads, kSfMinBlocks)
     const SfGridDesc G = grids[T.grid];
     const int seg_end = min(hi, prefix[t + 1]);
     const int j0 = (it - prefix[t]) * kSfItem;
-    const int j1 = min(J[T.region], (seg_end - prefix[t]) * kSfItem);
+    const int j1 = min(L.Jc[T.region], (seg_end - prefix[t]) * kSfItem);
+    const int jp = J[T.region];  // positions >= jp: the eligible list
+    const int* el = L.elist + static_cast<size_t>(T.region) * L.cap;
     const SfConst* cg = cst + static_cast<size_t>(T.grid) * max_src;
     __syncthreads();  // the previous segment is done with U / V
     for (int i = tid; i < kSfTA; i += kSfThreads) sm.U[i] = i < T.na ? G.U[T.a0 + i] : 0.0;
@@ -358,7 +399,8 @@ __global__ void __launch_bounds__(kSfThreads, kSfMinBlocks)
       for (int e = tid; e < 8 * kSfKS; e += kSfThreads) {
         const int j = j0 + st * kSfKS + (e >> 3), f = e & 7;
         // padding columns (j >= j1) read entry max_src - 1: always a zero factor
-        const double* src = reinterpret_cast<const double*>(cg + (j < j1 ? j : max_src - 1));
+        const int js = j >= j1 ? max_src - 1 : (j < jp ? j : el[j - jp]);
+        const double* src = reinterpret_cast<const double*>(cg + js);
         cp_async8(&sm.cs[buf][f][e >> 3], src + f);
       }
     };
@@ -524,7 +566,7 @@ __global__ void sf_add_kernel(SfAddArgs a, int e0, int e1, bool flux) {
 
 void sf_plan(const SfPlanArgs& a, const SfRegion* d_regions, int n_regions, int* d_J, int* d_E,
              const SfPlanMask& mask, int n_static_regions, int* d_Jlast, int* d_Elast,
-             int* d_Jraw, cudaStream_t s) {
+             int* d_Jraw, const SfLists& lists, cudaStream_t s) {
   if (n_regions <= 0) return;
   sf_plan_init_kernel<<<(n_regions + 127) / 128, 128, 0, s>>>(n_regions, a.n_act, d_Jraw, d_E);
   const dim3 grid(n_regions, kPlanChunks);
@@ -533,11 +575,13 @@ void sf_plan(const SfPlanArgs& a, const SfRegion* d_regions, int n_regions, int*
                                         d_Jlast, d_Elast);
   sf_plan_keep_kernel<<<(n_static_regions + 127) / 128, 128, 0, s>>>(n_static_regions, d_E, mask,
                                                                       d_Elast);
+  sf_plan_list_kernel<<<n_regions, 256, 0, s>>>(a, d_regions, d_J, d_E, lists, mask,
+                                                n_static_regions);
 }
 
-void sf_items(const SfTile* d_tiles, int n_tiles, const int* d_J, int* d_prefix, double* stats,
+void sf_items(const SfTile* d_tiles, int n_tiles, const int* d_Jc, int* d_prefix, double* stats,
               cudaStream_t s) {
-  sf_items_kernel<<<1, 32, 0, s>>>(d_tiles, n_tiles, d_J, d_prefix, stats);
+  sf_items_kernel<<<1, 32, 0, s>>>(d_tiles, n_tiles, d_Jc, d_prefix, stats);
 }
 
 void sf_prep(const double* d_src6, int n_act, double t, double alpha, double rcp,
@@ -551,8 +595,9 @@ void sf_prep(const double* d_src6, int n_act, double t, double alpha, double rcp
 int sf_contract_max_ctas(int sm_count) { return kSfMinBlocks * sm_count; }
 
 void sf_contract_fused(const SfGridDesc* d_grids, const SfTile* d_tiles, int n_tiles,
-                       const int* d_prefix, const int* d_J, const SfConst* d_cst, int max_src,
-                       const double* d_tab, double* d_scratch, int ctas, cudaStream_t s) {
+                       const int* d_prefix, const int* d_J, const SfLists& lists,
+                       const SfConst* d_cst, int max_src, const double* d_tab, double* d_scratch,
+                       int ctas, cudaStream_t s) {
   static bool attr = false;
   const size_t bytes = sizeof(SfSmem);
   if (!attr) {
@@ -561,7 +606,7 @@ void sf_contract_fused(const SfGridDesc* d_grids, const SfTile* d_tiles, int n_t
     attr = true;
   }
   sf_contract_kernel<<<ctas, kSfThreads, bytes, s>>>(d_grids, d_tiles, n_tiles, d_prefix, d_J,
-                                                     d_cst, max_src, d_tab, d_scratch);
+                                                     lists, d_cst, max_src, d_tab, d_scratch);
 }
 
 void sf_base_positions(int n, const int* d_q, const int* d_tile, const int* d_qelem,

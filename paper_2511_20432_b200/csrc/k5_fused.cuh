@@ -67,21 +67,20 @@ struct SfTile {
 // A region: points whose box [lo, hi] (+- delta per axis) decides which
 // sources no cull can reach anywhere in it (the contraction's prefix [0, J))
 // and which are culled everywhere in it (dropped from the pair-wise
-// remainder [J, E)). npts: its point count; work: the contraction cost of its tiles per source, in
-// points (sf_tile_cost x kSfTA x kSfTB summed over the tiles; the profitability
-// test), < 0: never contracted.
+// remainder [J, E)). npts: its point count (profitability; < 0: never contracted).
 struct SfRegion {
   double lo[3], hi[3];
   double delta;
   double npts;
-  double work;
 };
 
 struct SfPlanArgs {
   const double* src6;
   int n_act;           // the causally active prefix (later sources are exact zeros)
   double t, alpha, cull;
-  double min_pairs;    // J * work below this: no contraction for the region (K1 is cheaper)
+  double min_pairs;    // J * npts below this and J below min_sources: no contraction for the
+  int min_sources;     // region (its pairs are cheap on K1; a long J is not: one remainder CTA
+                       // would run all of it over its points)
   bool gemm;           // false: J = 0 everywhere (every pair on K1)
 };
 
@@ -102,13 +101,28 @@ struct SfPlanMask {
   int nt_flux, nt_static;
   int rank, world;
 };
+// The sources of [J, E) that no cull reaches anywhere in the region's box
+// either (a later source of the history can be eligible again: the prefix
+// stops at the first failure) join the contraction: per region r with J > 0
+// their indices in order, elist[r * cap + k] for k < Jc[r] - J[r], and their
+// bits okbits[r * words + (j - J) / 32] (the remainder launch skips them).
+struct SfLists {
+  int* elist;
+  unsigned* okbits;
+  int* Jc;      // the contraction's source count: J + the eligible ones in [J, E)
+  int* Jclast;  // Jc of the computed static regions (queries)
+  int cap, words;
+};
+
 // regions' J, E (the computed static regions' also into Jlast / Elast, kept
-// across calls for queries); tiles' item prefix (n_tiles + 1) and the call's
-// contraction flops (2 na nb J summed over the tiles) added to stats[0]
+// across calls for queries) and the eligible lists
 void sf_plan(const SfPlanArgs& a, const SfRegion* d_regions, int n_regions, int* d_J, int* d_E,
              const SfPlanMask& mask, int n_static_regions, int* d_Jlast, int* d_Elast,
-             int* d_Jraw, cudaStream_t s);
-void sf_items(const SfTile* d_tiles, int n_tiles, const int* d_J, int* d_prefix, double* stats,
+             int* d_Jraw, const SfLists& lists, cudaStream_t s);
+// tiles' item prefix (n_tiles + 1) over their regions' contraction counts Jc
+// and the call's contraction flops (2 na nb Jc summed over the tiles) added to
+// stats[0]
+void sf_items(const SfTile* d_tiles, int n_tiles, const int* d_Jc, int* d_prefix, double* stats,
               cudaStream_t s);
 void sf_prep(const double* d_src6, int n_act, double t, double alpha, double rcp,
              const SfGridDesc* d_grids, int n_grids, int max_src, SfConst* d_cst, cudaStream_t s);
@@ -120,9 +134,12 @@ void sf_prep(const double* d_src6, int n_act, double t, double alpha, double rcp
 // (a, b) at a + kSfTA * b). Deterministic: the split depends only on the item
 // count and `ctas`. d_cst: one row of max_src SfConst per grid (sf_prep); entry
 // max_src - 1 of every row must be a zero factor (max_src > the source count).
+// Contraction position k of region r is source k for k < J[r], else
+// lists.elist[r * cap + k - J[r]].
 void sf_contract_fused(const SfGridDesc* d_grids, const SfTile* d_tiles, int n_tiles,
-                       const int* d_prefix, const int* d_J, const SfConst* d_cst, int max_src,
-                       const double* d_tab, double* d_scratch, int ctas, cudaStream_t s);
+                       const int* d_prefix, const int* d_J, const SfLists& lists,
+                       const SfConst* d_cst, int max_src, const double* d_tab, double* d_scratch,
+                       int ctas, cudaStream_t s);
 int sf_contract_max_ctas(int sm_count);
 
 // Entries of the pair-wise remainder launch (K1 with per-region ranges): one

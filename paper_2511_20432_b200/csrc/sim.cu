@@ -589,7 +589,6 @@ SfRegion box_of(const SfGrid& g, int a0, int na, int b0, int nb) {
   r.hi[g.axv] = g.V[b0 + nb - 1];
   r.delta = g.delta;
   r.npts = static_cast<double>(na) * nb;
-  r.work = 0.0;  // set with the region's tiles
   return r;
 }
 
@@ -597,6 +596,7 @@ SfRegion box_of(const SfGrid& g, int a0, int na, int b0, int nb) {
 
 void Sim::sf_setup_host() {
   if (const char* e = std::getenv("TG_SF_MIN_PAIRS")) sf_min_pairs = std::atof(e);
+  if (const char* e = std::getenv("TG_SF_MIN_SOURCES")) sf_min_sources = std::atoi(e);
   if (const char* e = std::getenv("TG_SF_K1_SPLITS"))
     sf_k1_splits = std::max(1, std::min(kMaxSplits, std::atoi(e)));
   const int tqb = h_qb_off.empty() ? 0 : h_qb_off.back();
@@ -750,7 +750,6 @@ void Sim::sf_setup_host() {
         const int r = static_cast<int>(sf_regions_h.size());
         sf_tiles_h.push_back(SfTile{grid, a0, b0, nat, nbt, r});
         sf_regions_h.push_back(box_of(g, a0, nat, b0, nbt));
-        sf_regions_h.back().work = sf_tile_cost(nat, nbt) * kSfTA * kSfTB;
       }
     tile_pts.resize(sf_tiles_h.size());
     tile_cell.resize(sf_tiles_h.size());
@@ -914,8 +913,17 @@ void Sim::sf_setup_device() {
   d_sf_Jraw.ensure(sf_regions_h.size() + nfr + 1);
   d_sf_Jl.ensure(sf_regions_h.size() + 1);
   d_sf_El.ensure(sf_regions_h.size() + 1);
+  d_sf_Jcl.ensure(sf_regions_h.size() + 1);
   TG_CUDA(cudaMemsetAsync(d_sf_Jl.p, 0, sizeof(int) * (sf_regions_h.size() + 1), s));
   TG_CUDA(cudaMemsetAsync(d_sf_El.p, 0, sizeof(int) * (sf_regions_h.size() + 1), s));
+  TG_CUDA(cudaMemsetAsync(d_sf_Jcl.p, 0, sizeof(int) * (sf_regions_h.size() + 1), s));
+  // eligible lists: one row of n_sources indices / bits per region
+  sf_list_cap = std::max<int>(1, static_cast<int>(sources.size()));
+  sf_list_words = (sf_list_cap + 31) / 32;
+  const size_t nrows = sf_regions_h.size() + nfr + 1;
+  d_sf_Jc.ensure(nrows);
+  d_sf_elist.ensure(nrows * sf_list_cap);
+  d_sf_okbits.ensure(nrows * sf_list_words);
   d_sf_E.ensure(sf_regions_h.size() + nfr + 1);
   d_sf_prefix.ensure(sf_nt_static + ft + 2);
   // qp -> element of the base points (their compact positions per step)
@@ -963,7 +971,7 @@ void Sim::release_stages() {
 }
 
 
-void Sim::sf_plan_host(double t, int* J, int* E) {
+void Sim::sf_plan_host(double t, int* J, int* E, int* Jc) {
   const double alpha = cfg.material.diffusivity(), cull = cfg.superpose.cull_exponent;
   const double* src = reinterpret_cast<const double*>(sources.data());
   // the causally active prefix (tg_ctx::active_prefix): later sources all
@@ -975,13 +983,21 @@ void Sim::sf_plan_host(double t, int* J, int* E) {
     int j = 0;
     if (sf_on) {
       while (j < n_act && sf_region_ok(src + 6 * static_cast<size_t>(j), t, alpha, cull, R)) ++j;
-      if (R.work < 0.0 || static_cast<double>(j) * R.work < sf_min_pairs) j = 0;
+      if (R.npts < 0.0 ||
+          (static_cast<double>(j) * R.npts < sf_min_pairs && j < sf_min_sources))
+        j = 0;
     }
     int e = n_act;
     while (e > j && sf_region_culled(src + 6 * static_cast<size_t>(e - 1), t, alpha, cull, R))
       --e;
     J[r] = j;
     E[r] = e;
+    if (Jc) {  // + the eligible sources of [J, E) (k5_fused.cuh SfLists)
+      int c = j;
+      for (int k = j; k < e && j > 0; ++k)
+        c += sf_region_ok(src + 6 * static_cast<size_t>(k), t, alpha, cull, R) ? 1 : 0;
+      Jc[r] = c;
+    }
   }
 }
 
@@ -993,10 +1009,12 @@ double Sim::sf_flops_total() {
   return v;
 }
 
-void Sim::sf_last_plan(int* J, int* E) {
+void Sim::sf_last_plan(int* J, int* E, int* Jc) {
   const size_t n = sf_regions_h.size();
   TG_CUDA(cudaMemcpyAsync(J, d_sf_Jl.p, n * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
   TG_CUDA(cudaMemcpyAsync(E, d_sf_El.p, n * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  if (Jc)
+    TG_CUDA(cudaMemcpyAsync(Jc, d_sf_Jcl.p, n * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
   TG_CUDA(cudaStreamSynchronize(ctx->stream));
 }
 
@@ -1084,11 +1102,9 @@ void Sim::loads_device(double t, double radius, double* d_F, double* d_g, bool g
         fregs.push_back(box_of(g, a0, na, b0, nb));
         sf_split_tiles(na, nb, as, bs);
         for (const auto& [bb, nbt] : bs)
-          for (const auto& [aa, nat] : as) {
+          for (const auto& [aa, nat] : as)
             ftiles.push_back(SfTile{sf_grid_fine0 + static_cast<int>(f), a0 + aa, b0 + bb, nat,
                                     nbt, reg});
-            fregs.back().work += sf_tile_cost(nat, nbt) * kSfTA * kSfTB;
-          }
       } else {  // fine points not on grids: all their sources pair-wise
         SfRegion all{};
         for (int ax = 0; ax < 3; ++ax) {
@@ -1096,7 +1112,6 @@ void Sim::loads_device(double t, double radius, double* d_F, double* d_g, bool g
           all.hi[ax] = 1e300;
         }
         all.npts = -1.0;
-        all.work = -1.0;
         fregs.push_back(all);
       }
       const size_t e0 = fq.size();
@@ -1190,26 +1205,29 @@ void Sim::loads_device(double t, double radius, double* d_F, double* d_g, bool g
   const double alpha = m.diffusivity(), rcp = m.volumetric_capacity();
   const double cull = cfg.superpose.cull_exponent;
   const int n_act = ctx->active_prefix(t);
-  SfPlanArgs pa{ctx->src6.p, n_act, t, alpha, cull, sf_min_pairs, sf_on};
+  SfPlanArgs pa{ctx->src6.p, n_act, t, alpha, cull, sf_min_pairs, sf_min_sources, sf_on};
   SfPlanMask mask{flux, dir, sf_nt_flux, sf_nt_static, sf_rank, sf_world};
+  const SfLists lists{d_sf_elist.p, d_sf_okbits.p, d_sf_Jc.p, d_sf_Jcl.p, sf_list_cap,
+                      sf_list_words};
   sf_plan(pa, d_sf_regions.p, n_regs, d_sf_J.p, d_sf_E.p, mask, nreg_static, d_sf_Jl.p,
-          d_sf_El.p, d_sf_Jraw.p, s);
-  sf_items(d_sf_tiles.p, n_tiles, d_sf_J.p, d_sf_prefix.p, d_sf_stats.p, s);
+          d_sf_El.p, d_sf_Jraw.p, lists, s);
+  sf_items(d_sf_tiles.p, n_tiles, d_sf_Jc.p, d_sf_prefix.p, d_sf_stats.p, s);
   sf_prep(ctx->src6.p, n_act, t, alpha, rcp, d_sf_grids.p, static_cast<int>(sf_grids_h.size()),
           static_cast<int>(sources.size()) + 1, d_sf_cst.p, s);
   const int ctas = sf_contract_max_ctas(ctx->sm_count);
   ctx->timer.timed(5, s, [&] {
-    sf_contract_fused(d_sf_grids.p, d_sf_tiles.p, n_tiles, d_sf_prefix.p, d_sf_J.p, d_sf_cst.p,
-                      static_cast<int>(sources.size()) + 1, d_sf_tab.p, d_sf_scratch.p, ctas, s);
+    sf_contract_fused(d_sf_grids.p, d_sf_tiles.p, n_tiles, d_sf_prefix.p, d_sf_J.p, lists,
+                      d_sf_cst.p, static_cast<int>(sources.size()) + 1, d_sf_tab.p,
+                      d_sf_scratch.p, ctas, s);
   });
-  ctx->timer.launches += 4;
+  ctx->timer.launches += 5;
   // the pair-wise remainder: K1 over every entry with its region's [J, E)
   const int S = sf_k1_splits;
   double* part = ctx->part.ensure(static_cast<size_t>(S) * 4 * n_ent);
   if (n_act > 0) {
     k1_prepare(ctx->src6.p, n_act, t, alpha, rcp, cull, ctx->rec.ensure(n_act), s);
     const bool planar = ctx->planar && !std::getenv("TG_K1_NO_PLANAR");
-    K1Ranges rg{d_sf_cta.p, d_sf_J.p, d_sf_E.p};
+    K1Ranges rg{d_sf_cta.p, d_sf_J.p, d_sf_E.p, d_sf_okbits.p, sf_list_words};
     ctx->timer.timed(1, s, [&] {
       k1_launch_partial(ctx->rec.p, n_act, d_qx.p, d_sf_ent_q.p, n_ent, S, true, 7, part, s,
                         planar, ctx->planar_z, rg);

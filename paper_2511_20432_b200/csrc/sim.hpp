@@ -77,15 +77,16 @@ class Sim {
   void set_sumfact(bool on) { sf_on = on && (sf_flux_ok || sf_dir_ok); }
   // host restatement of the device plan at t for the static regions (flux
   // tiles, then Greville tiles): J (contraction prefix), E (remainder end)
-  void sf_plan_host(double t, int* J, int* E);
+  void sf_plan_host(double t, int* J, int* E, int* Jc = nullptr);
   bool sf_on = false, sf_flux_ok = false, sf_dir_ok = false;
   // contraction flops (2 per point x source) since setup, read from the device
   double sf_flops_total();
   double sf_min_pairs = 3e7;  // smallest J x points worth a contraction (TG_SF_MIN_PAIRS)
+  int sf_min_sources = 16384;  // ... unless J reaches this (TG_SF_MIN_SOURCES)
   int sf_k1_splits = 4;       // source splits of the remainder launch (TG_SF_K1_SPLITS)
   // the device plan of the static regions, each part (flux / Greville) as its
   // last call computed it, read back on request
-  void sf_last_plan(int* J, int* E);
+  void sf_last_plan(int* J, int* E, int* Jc = nullptr);
   int sf_n_regions() const { return static_cast<int>(sf_regions_h.size()); }
   int sf_dir_regions() const { return sf_nt_static - sf_nt_flux; }
   const std::vector<SfRegion>& sf_regions() const { return sf_regions_h; }
@@ -214,6 +215,9 @@ class Sim {
   DevBuf<SfTile> d_sf_tiles;
   DevBuf<SfRegion> d_sf_regions;
   DevBuf<SfConst> d_sf_cst;
+  DevBuf<int> d_sf_elist, d_sf_Jc, d_sf_Jcl;
+  DevBuf<unsigned> d_sf_okbits;
+  int sf_list_cap = 1, sf_list_words = 1;
   DevBuf<int> d_sf_J, d_sf_E, d_sf_Jl, d_sf_El, d_sf_Jraw, d_sf_prefix, d_sf_ent_q, d_sf_ent_tile, d_sf_ent_cell,
       d_sf_ent_pos, d_sf_cta, d_sf_qelem;
   // per-step host staging (pinned ring; an event marks when a slot's copies ran)

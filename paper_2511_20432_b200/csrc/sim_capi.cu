@@ -190,20 +190,34 @@ int tg_sim_sumfact_regions(tg_sim* s, double* out) {
   return sim_guard(s, [&](Sim& m) {
     const auto& R = m.sf_regions();
     for (size_t r = 0; r < R.size(); ++r) {
-      double* o = out + 9 * r;
+      double* o = out + 8 * r;
       for (int a = 0; a < 3; ++a) {
         o[a] = R[r].lo[a];
         o[3 + a] = R[r].hi[a];
       }
       o[6] = R[r].delta;
       o[7] = R[r].npts;
-      o[8] = R[r].work;
     }
   }, false);
 }
 
 int tg_sim_sumfact_plan(tg_sim* s, double t, int* J, int* E) {
   return sim_guard(s, [&](Sim& m) { m.sf_plan_host(t, J, E); }, false);
+}
+
+int tg_sim_sumfact_counts(tg_sim* s, double t, int* Jc) {
+  return sim_guard(s, [&](Sim& m) {
+    std::vector<int> J(m.sf_n_regions()), E(m.sf_n_regions());
+    m.sf_plan_host(t, J.data(), E.data(), Jc);
+  }, false);
+}
+
+int tg_sim_sumfact_last_counts(tg_sim* s, int* Jc) {
+  return sim_guard(s, [&](Sim& m) {
+    if (!m.sf_fused_ready()) throw std::logic_error("no device plan (host-only simulation)");
+    std::vector<int> J(m.sf_n_regions()), E(m.sf_n_regions());
+    m.sf_last_plan(J.data(), E.data(), Jc);
+  });
 }
 
 int tg_sim_sumfact_last_plan(tg_sim* s, int* J, int* E) {

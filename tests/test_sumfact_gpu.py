@@ -80,6 +80,29 @@ def test_sumfact_against_live_reference(ref, tmp_path):
     r.close()
 
 
+def test_eligible_list_against_live_reference(ref, tmp_path):
+    """A history whose prefix J stops early: sources of [J, E) that no cull
+    reaches anywhere in a region join its contraction (Jc > J), the
+    remainder skips them; loads match the reference and the K1-only path."""
+    path = long_history_cfg(tmp_path, -0.019)
+    s = tg.Simulation(path, t_end=2e-4)
+    r = ref.sim(path, t_end=2e-4)
+    F, Fr = s.flux_load(0.0), r.flux_load(0.0)
+    d, dr = s.dirichlet_values(0.0), r.dirichlet(0.0)
+    J, E = s.sumfact_last_plan()
+    Jc = s.sumfact_counts()
+    assert (J > 0).any() and (Jc > J).any()
+    assert np.array_equal(Jc, s.sumfact_counts(0.0))  # device lists = host restatement
+    assert normwise(F, Fr) <= 1e-10 and np.array_equal(F == 0.0, Fr == 0.0)
+    assert normwise(d, dr) <= 1e-10 and pointwise(d, dr) <= 1e-10
+    s.set_sumfact(False)
+    F0, d0 = s.flux_load(0.0), s.dirichlet_values(0.0)
+    assert normwise(F, F0) <= 1e-12 and np.array_equal(F == 0.0, F0 == 0.0)
+    assert pointwise(d, d0) <= 1e-12
+    s.close()
+    r.close()
+
+
 def test_sumfact_time_loop_against_live_reference(ref, tmp_path):
     path = long_history_cfg(tmp_path)
     s = tg.Simulation(path, t_end=2e-4)
@@ -126,9 +149,12 @@ def test_device_plan_is_the_host_plan(tmp_path):
         J, E = s.sumfact_last_plan()
         Jh, Eh = s.sumfact_plan(t)
         assert np.array_equal(J[flux], Jh[flux]) and np.array_equal(E[flux], Eh[flux]), t
+        Jc, Jch = s.sumfact_counts(), s.sumfact_counts(t)
+        assert np.array_equal(Jc[flux], Jch[flux]), t
         s.dirichlet_values(t)
         J, E = s.sumfact_last_plan()
         assert np.array_equal(J, Jh) and np.array_equal(E, Eh), t
+        assert np.array_equal(s.sumfact_counts(), Jch), t
     s.close()
 
 

@@ -49,20 +49,22 @@ def _plan(src, t, alpha, cull, reg, min_pairs):
     active = dt > 0.0
     spread = 4.0 * alpha * dt
     p = src[:, :3]
-    lo, hi, delta, work = reg[0:3] - reg[6], reg[3:6] + reg[6], reg[6], reg[8]
+    lo, hi, delta, npts = reg[0:3] - reg[6], reg[3:6] + reg[6], reg[6], reg[7]
     r2max = np.maximum((lo - p) ** 2, (hi - p) ** 2).sum(axis=1)
     ok = ~active | ((r2max * (1.0 + 1e-9) <= cull * spread)
                     & (36.0 * cull * delta * delta <= 1e-24 * spread))
     bad = np.flatnonzero(~ok)
     n_act = int(np.flatnonzero(active)[-1]) + 1 if active.any() else 0
     J = int(bad[0]) if len(bad) and bad[0] < n_act else n_act
-    if work < 0 or J * work < min_pairs:
+    if npts < 0 or (J * npts < min_pairs and J < 16384):
         J = 0
     d = np.maximum(np.maximum(lo - p, p - hi), 0.0)
     culled = ~active | ((d * d).sum(axis=1) * (1.0 - 1e-9) > cull * spread)
     keep = np.flatnonzero(~culled[J:n_act])
     E = J + int(keep[-1]) + 1 if len(keep) else J
-    return J, E
+    # the contraction's count: + the sources of [J, E) eligible on the box too
+    Jc = J + int(ok[J:E].sum()) if J > 0 else J
+    return J, E, Jc
 
 
 def test_regions_cover_the_grids():
@@ -83,7 +85,7 @@ def test_regions_cover_the_grids():
     s.close()
 
 
-@pytest.mark.parametrize("t", [-1.0, 0.0, 1e-4, 3e-3])
+@pytest.mark.parametrize("t", [-1.0, 0.0, 1e-4, 3e-3, 6e-3])
 @pytest.mark.parametrize("min_pairs", [0.0, 3e7])
 def test_plan_matches_restatement(tmp_path, monkeypatch, t, min_pairs):
     monkeypatch.setenv("TG_SF_MIN_PAIRS", repr(min_pairs))
@@ -92,11 +94,14 @@ def test_plan_matches_restatement(tmp_path, monkeypatch, t, min_pairs):
     k, rho, c = (s.params[n] for n in ("conductivity", "density", "heat_capacity"))
     alpha, cull = k / (rho * c), s.params["cull"]
     J, E = s.sumfact_plan(t)
+    Jc = s.sumfact_counts(t)
     R = s.sumfact_regions()
     for r in range(len(R)):
-        assert (J[r], E[r]) == _plan(src, t, alpha, cull, R[r], min_pairs), (r, t)
+        assert (J[r], E[r], Jc[r]) == _plan(src, t, alpha, cull, R[r], min_pairs), (r, t)
     if t == -1.0:  # every source still inactive: nothing to do anywhere
         assert not J.any() and not E.any()
     if t == 0.0 and min_pairs == 0.0:  # the long history: both paths carry sources
         assert J.min() > 0 and (E > J).any()
+    if t == 6e-3 and min_pairs == 0.0:  # eligible sources after the prefix join the contraction
+        assert (Jc > J).any()
     s.close()
