@@ -28,7 +28,7 @@ COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler",
 
 # files whose arithmetic must round every product and sum separately (the
 # host / reference association, no FMA contraction)
-NO_FMAD = {"k4_eval.cu"}
+NO_FMAD = {"k4_eval.cu", "k6_assemble.cu"}
 
 
 # the CUDA runtime is linked statically; no CUDA math library is needed

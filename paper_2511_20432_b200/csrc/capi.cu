@@ -84,7 +84,7 @@ void k1_run(tg_ctx* ctx, const double* d_src6, int n_src, const double* d_pts,
   if (n_src > 0) {
     k1_prepare(d_src6, n_src, t, alpha, rcp, cull, ctx->rec.ensure(n_src), stream);
     ++ctx->timer.launches;
-    S = k1_choose_splits(n_pts, n_src, ctx->sm_count, kK1Threads * P);
+    S = k1_choose_splits(n_pts, n_src, ctx->sm_count, kK1Threads * P, k1_resident_ctas(P));
   }
   double* part = ctx->part.ensure(static_cast<size_t>(S) * (grad ? 4 : 1) * n_pts);
   if (n_src > 0) {

@@ -22,6 +22,7 @@
 // and, only inside the +-1 high-word band, re-forms r.r with the reference's
 // association and no FMA for the exact compare.
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 
 #include "common.cuh"
@@ -413,9 +414,25 @@ void k1_upload_exp_table(cudaStream_t stream) {
 // launch (or a shard of a multi-GPU run) evaluates: sharded loads reproduce
 // the single-launch result bit for bit. >= 128 sources per split, <= 16 splits
 // (enough CTAs for small point sets, few partial planes for large ones).
-int k1_choose_splits(int, int n_src, int, int) {
-  return std::max(1, std::min(kMaxSplits, n_src / 128));
+// The fewest source splits giving >= 12 waves of CTAs with the last one >= 95 %
+// full (each split adds a partial plane of 4 doubles per point to write and
+// combine; fewer, longer waves lose to the SMs' spread): config 1 (586 point
+// blocks of 1792, one resident CTA per SM) takes 4 (15.8 waves; measured 1
+// split 0.899e12 pairs/s, 4: 0.918e12, 16: 0.916e12); at most one per 128 sources.
+int k1_choose_splits(int n_pts, int n_src, int sm_count, int points_per_cta, int resident) {
+  const int smax = std::max(1, std::min(kMaxSplits, n_src / 128));
+  if (const char* e = std::getenv("TG_K1_SPLITS")) return std::max(1, std::min(smax, std::atoi(e)));
+  const long blocks = (static_cast<long>(n_pts) + points_per_cta - 1) / points_per_cta;
+  const long slots = static_cast<long>(std::max(1, sm_count)) * std::max(1, resident);
+  for (int S = 1; S <= smax; ++S) {
+    const long ctas = blocks * S, waves = (ctas + slots - 1) / slots;
+    if (ctas >= 12 * slots && static_cast<double>(ctas) >= 0.95 * static_cast<double>(waves * slots))
+      return S;
+  }
+  return smax;
 }
+
+int k1_resident_ctas(int P) { return P >= 6 ? 256 / kK1Threads : (P >= 4 ? K1_MINB4 : 3); }
 
 void k1_prepare(const double* d_src6, int n, double t, double alpha, double rcp, double cull,
                 SrcRec* d_rec, cudaStream_t stream) {

@@ -46,7 +46,9 @@ struct K1Ranges {
 void k1_upload_exp_table(cudaStream_t stream);
 // the src_exp table (common.cuh) on the host: kExpTableSize doubles
 void k1_exp_table_host(double* tab);
-int k1_choose_splits(int n_pts, int n_src, int sm_count, int points_per_cta);
+int k1_choose_splits(int n_pts, int n_src, int sm_count, int points_per_cta, int resident);
+// CTAs of k1_partial<P> resident per SM (its launch bounds)
+int k1_resident_ctas(int P);
 void k1_prepare(const double* d_src6, int n, double t, double alpha, double rcp, double cull,
                 SrcRec* d_rec, cudaStream_t stream);
 // planar: all sources lie on z = zs (k1_partial's PLANAR variant)

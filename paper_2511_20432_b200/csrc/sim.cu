@@ -70,25 +70,6 @@ void upload(DevBuf<T>& d, const std::vector<T>& h, cudaStream_t s) {
 
 }  // namespace
 
-Sim::Sim(const std::string& path, const SimOptions& opt) {
-  RunConfig c = parse_config(path);
-  if (opt.t_end > 0.0) c.stepping.t_end = opt.t_end;
-  if (opt.solver_tol > 0.0) c.stepping.solver_tol = opt.solver_tol;
-  if (opt.max_iter > 0) c.stepping.max_iter = opt.max_iter;
-  cfg = std::move(c);
-  setup_host();
-  sf_setup_host();
-  if (!opt.host_only) setup_device(opt.device, opt.preconditioner);
-}
-
-Sim::~Sim() {
-  if (h_dots) cudaFreeHost(h_dots);
-  if (h_status) cudaFreeHost(h_status);
-  if (h_steps) cudaFreeHost(h_steps);
-  release_stages();
-  if (ctx) tg_ctx_destroy(ctx);
-}
-
 namespace {
 // TG_SETUP_TIMING=1: per-phase wall times of the setup on stderr
 struct PhaseClock {
@@ -103,6 +84,31 @@ struct PhaseClock {
   }
 };
 }  // namespace
+
+Sim::Sim(const std::string& path, const SimOptions& opt) {
+  RunConfig c = parse_config(path);
+  if (opt.t_end > 0.0) c.stepping.t_end = opt.t_end;
+  if (opt.solver_tol > 0.0) c.stepping.solver_tol = opt.solver_tol;
+  if (opt.max_iter > 0) c.stepping.max_iter = opt.max_iter;
+  cfg = std::move(c);
+  // the general patch's operators: assembled on the device when there is one
+  csr_deferred = !opt.host_only && !std::getenv("TG_HOST_ASSEMBLY");
+  setup_host();
+  PhaseClock clk;
+  sf_setup_host();
+  clk.mark("k5 grids, tiles, entries");
+  if (!opt.host_only) setup_device(opt.device, opt.preconditioner);
+  clk.mark("device setup");
+}
+
+Sim::~Sim() {
+  if (h_dots) cudaFreeHost(h_dots);
+  if (h_status) cudaFreeHost(h_status);
+  if (h_steps) cudaFreeHost(h_steps);
+  release_stages();
+  if (ctx) tg_ctx_destroy(ctx);
+}
+
 
 void Sim::setup_host() {
   PhaseClock clk;
@@ -212,7 +218,186 @@ void Sim::setup_host() {
     coefA = {rc / dt, th * k};
     coefB = {rc / dt, -(1.0 - th) * k};
     clk.mark("kronecker factors");
-  } else {
+  } else if (!csr_deferred) {
+    assemble_csr_host();
+  }
+}
+
+// The general patch's operators on the device (K6, k6_assemble.cu): false if
+// the patch is beyond it (the host path then runs). Bit-identical to
+// assemble_csr_host (tests/test_cfg3.py).
+bool Sim::assemble_csr_device(cudaStream_t s) {
+  upload_nurbs();
+  const ElementGrid eg = element_grid(vol);
+  const auto n = vol.basis_counts();
+  const auto pd = vol.degrees();
+  AsmPatch P{};
+  P.V = nurbs;
+  std::vector<int> spans[3], elo[3], ehi[3];
+  std::vector<double> gn[3], gw[3];
+  for (int d = 0; d < 3; ++d) {
+    P.n_el[d] = eg.n_el[d];
+    P.nq[d] = quad[d];
+    const KnotVector& kv = vol.knots(d);
+    spans[d].resize(eg.n_el[d]);
+    elo[d].assign(n[d], 1 << 30);
+    ehi[d].assign(n[d], -1);
+    for (int e = 0; e < eg.n_el[d]; ++e) {
+      spans[d][e] = kv.find_span(0.5 * (eg.bp[d][e] + eg.bp[d][e + 1]));
+      for (int i = spans[d][e] - pd[d]; i <= spans[d][e]; ++i) {
+        elo[d][i] = std::min(elo[d][i], e);
+        ehi[d][i] = std::max(ehi[d][i], e);
+      }
+    }
+    const GaussRule& g = gauss_rule(quad[d]);
+    gn[d] = g.nodes;
+    gw[d] = g.weights;
+  }
+  P.rc = cfg.material.volumetric_capacity();
+  P.k = cfg.material.conductivity;
+  if (!k6_supported(P)) return false;
+  // tensor pattern row pointers (tensor_pattern's row lengths)
+  const long rows = static_cast<long>(n[0]) * n[1] * n[2];
+  std::vector<int> row_ptr(rows + 1, 0);
+  long nnz = 0;
+  for (long r = 0; r < rows; ++r) {
+    const int rc3[3] = {static_cast<int>(r % n[0]), static_cast<int>((r / n[0]) % n[1]),
+                        static_cast<int>(r / (static_cast<long>(n[0]) * n[1]))};
+    long len = 1;
+    for (int d = 0; d < 3; ++d)
+      len *= std::min(n[d] - 1, rc3[d] + pd[d]) - std::max(0, rc3[d] - pd[d]) + 1;
+    nnz += len;
+    if (nnz > std::numeric_limits<int>::max()) return false;
+    row_ptr[r + 1] = static_cast<int>(nnz);
+  }
+  // device tables (freed at the end)
+  DevBuf<double> d_bp[3], d_gn[3], d_gw[3], dM, dK, lm, lk;
+  DevBuf<int> d_sp[3], d_lo[3], d_hi[3], d_rp, d_fi, d_ci, d_len[3];
+  DevBuf<int> d_flag;
+  for (int d = 0; d < 3; ++d) {
+    upload(d_bp[d], eg.bp[d], s);
+    upload(d_gn[d], gn[d], s);
+    upload(d_gw[d], gw[d], s);
+    upload(d_sp[d], spans[d], s);
+    upload(d_lo[d], elo[d], s);
+    upload(d_hi[d], ehi[d], s);
+    P.bp[d] = d_bp[d].p;
+    P.gn[d] = d_gn[d].p;
+    P.gw[d] = d_gw[d].p;
+    P.espan[d] = d_sp[d].p;
+    P.elo[d] = d_lo[d].p;
+    P.ehi[d] = d_hi[d].p;
+  }
+  upload(d_rp, row_ptr, s);
+  dM.ensure(nnz);
+  dK.ensure(nnz);
+  TG_CUDA(cudaMemsetAsync(dM.p, 0, nnz * sizeof(double), s));
+  TG_CUDA(cudaMemsetAsync(dK.p, 0, nnz * sizeof(double), s));
+  d_flag.ensure(1);
+  TG_CUDA(cudaMemsetAsync(d_flag.p, 0, sizeof(int), s));
+  // element matrices by element layers (<= ~2 GB of them at a time), each
+  // batch gathered into the pattern before the next (element order per entry)
+  const size_t T = k6_entries_per_element(P);
+  const size_t per_layer = static_cast<size_t>(eg.n_el[0]) * eg.n_el[1] * T * 2 * sizeof(double);
+  const int layers = static_cast<int>(std::max<size_t>(
+      1, std::min<size_t>(eg.n_el[2], (size_t{2} << 30) / std::max<size_t>(per_layer, 1))));
+  const size_t cap = static_cast<size_t>(layers) * eg.n_el[0] * eg.n_el[1] * T;
+  lm.ensure(cap);
+  lk.ensure(cap);
+  const int per = eg.n_el[0] * eg.n_el[1];
+  for (int k0 = 0; k0 < eg.n_el[2]; k0 += layers) {
+    const int k1 = std::min(eg.n_el[2], k0 + layers);
+    k6_element_matrices(P, k0 * per, (k1 - k0) * per, lm.p, lk.p, d_flag.p, s);
+    const int rz0 = std::max(0, spans[2][k0] - pd[2]), rz1 = std::min(n[2] - 1, spans[2][k1 - 1]);
+    k6_gather(P, d_rp.p, rz0 * n[0] * n[1], (rz1 + 1) * n[0] * n[1], k0, k1, k0 * per, lm.p, lk.p,
+              dM.p, dK.p, s);
+  }
+  int flag = 0;
+  TG_CUDA(cudaMemcpyAsync(&flag, d_flag.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+  TG_CUDA(cudaStreamSynchronize(s));
+  if (flag) throw numeric_error("non-positive Jacobian determinant at quadrature point");
+  lm.release();
+  lk.release();
+  // A / B on the free rows as sliced ELL
+  upload(d_free_list, dofs.free_list, s);
+  upload(d_fi, dofs.free_index, s);
+  upload(d_ci, dofs.constrained_index, s);
+  const AsmMaps maps{d_free_list.p, d_fi.p, d_ci.p, n_free};
+  for (auto& b : d_len) b.ensure(std::max(1, n_free));
+  k6_row_lengths(P, maps, d_len[0].p, d_len[1].p, d_len[2].p, s);
+  std::vector<int> len[3];
+  for (int m = 0; m < 3; ++m) {
+    len[m].resize(n_free);
+    TG_CUDA(cudaMemcpyAsync(len[m].data(), d_len[m].p, sizeof(int) * n_free,
+                            cudaMemcpyDeviceToHost, s));
+  }
+  TG_CUDA(cudaStreamSynchronize(s));
+  SellBufs* bufs[3] = {&sA, &sAc, &sB};
+  SellOut outs[3];
+  const int ns = (n_free + 31) / 32;
+  for (int m = 0; m < 3; ++m) {  // to_sell's slices: 32 rows, padded to the longest
+    std::vector<long long> sp(ns + 1, 0);
+    for (int sl = 0; sl < ns; ++sl) {
+      int w = 0;
+      for (int r = sl * 32; r < std::min(n_free, sl * 32 + 32); ++r) w = std::max(w, len[m][r]);
+      sp[sl + 1] = sp[sl] + 32LL * w;
+    }
+    SellBufs& b = *bufs[m];
+    upload(b.sp, sp, s);
+    upload(b.len, len[m], s);
+    b.col.ensure(std::max<long long>(1, sp[ns]));
+    b.val.ensure(std::max<long long>(1, sp[ns]));
+    TG_CUDA(cudaMemsetAsync(b.col.p, 0, sizeof(int) * sp[ns], s));
+    TG_CUDA(cudaMemsetAsync(b.val.p, 0, sizeof(double) * sp[ns], s));
+    outs[m] = SellOut{b.sp.p, b.col.p, b.val.p};
+  }
+  const double dt = dt_solver, th = cfg.stepping.theta;
+  k6_fill(P, d_rp.p, maps, dM.p, dK.p, 1.0 / dt, th, -(1.0 - th), outs[0], outs[1], outs[2], s);
+  devA = DevSell{n_free, sA.sp.p, sA.len.p, sA.col.p, sA.val.p};
+  devAc = DevSell{n_free, sAc.sp.p, sAc.len.p, sAc.col.p, sAc.val.p};
+  devB = DevSell{n_free, sB.sp.p, sB.len.p, sB.col.p, sB.val.p};
+  TG_CUDA(cudaStreamSynchronize(s));  // the temporaries die here
+  csr_device = true;
+  return true;
+}
+
+// A_ff as CSR on the host: the host assembly's copy, or (device assembly) the
+// device's sliced ELL converted back (tg_sim_reduced_operator)
+const Csr& Sim::reduced_operator() {
+  if (csrA.rows > 0 || !csr_device) return csrA;
+  cudaStream_t s = ctx->stream;
+  const int ns = (n_free + 31) / 32;
+  std::vector<long long> sp(ns + 1);
+  std::vector<int> len(n_free);
+  TG_CUDA(cudaMemcpyAsync(sp.data(), sA.sp.p, sizeof(long long) * (ns + 1), cudaMemcpyDeviceToHost, s));
+  TG_CUDA(cudaMemcpyAsync(len.data(), sA.len.p, sizeof(int) * n_free, cudaMemcpyDeviceToHost, s));
+  TG_CUDA(cudaStreamSynchronize(s));
+  std::vector<int> col(sp[ns]);
+  std::vector<double> val(sp[ns]);
+  TG_CUDA(cudaMemcpyAsync(col.data(), sA.col.p, sizeof(int) * sp[ns], cudaMemcpyDeviceToHost, s));
+  TG_CUDA(cudaMemcpyAsync(val.data(), sA.val.p, sizeof(double) * sp[ns], cudaMemcpyDeviceToHost, s));
+  TG_CUDA(cudaStreamSynchronize(s));
+  csrA.rows = n_free;
+  csrA.row_ptr.assign(n_free + 1, 0);
+  for (int f = 0; f < n_free; ++f) csrA.row_ptr[f + 1] = csrA.row_ptr[f] + len[f];
+  csrA.col.resize(csrA.row_ptr[n_free]);
+  csrA.val.resize(csrA.row_ptr[n_free]);
+  for (int f = 0; f < n_free; ++f) {
+    const long long base = sp[f >> 5] + (f & 31);
+    for (int k = 0; k < len[f]; ++k) {
+      csrA.col[csrA.row_ptr[f] + k] = col[base + 32LL * k];
+      csrA.val[csrA.row_ptr[f] + k] = val[base + 32LL * k];
+    }
+  }
+  return csrA;
+}
+
+// The general patch's operators on the host (assembly.cpp:59-101, 194-228):
+// M, K on the tensor pattern, A / B entrywise, the free-row split.
+void Sim::assemble_csr_host() {
+  PhaseClock clk;
+  const double dt = dt_solver, th = cfg.stepping.theta;
+  {
     Csr M, K;
     assemble_mass_stiffness(vol, quad, cfg.material, M, K);
     clk.mark("csr assembly (M, K)");
@@ -406,6 +591,15 @@ void Sim::setup_device(int device, int preconditioner) {
       use_cg1 = false;
     }
   } else {
+    // the operators assembled on the device (K6) unless the patch needs the
+    // host path (basis block too large) or TG_HOST_ASSEMBLY is set
+    bool on_device = false;
+    if (csr_deferred) {
+      PhaseClock clk;
+      on_device = assemble_csr_device(s);
+      clk.mark(on_device ? "csr operators on the device" : "device assembly unsupported");
+      if (!on_device) assemble_csr_host();
+    }
     auto up = [&](const Csr& C, SellBufs& b, DevSell& out) {
       const Sell h = to_sell(C);
       upload(b.sp, h.slice_ptr, s);
@@ -415,11 +609,13 @@ void Sim::setup_device(int device, int preconditioner) {
       TG_CUDA(cudaStreamSynchronize(s));  // h dies here
       out = DevSell{C.rows, b.sp.p, b.len.p, b.col.p, b.val.p};
     };
-    up(csrA, sA, devA);
-    up(csrAc, sAc, devAc);
-    up(csrB, sB, devB);
-    csrAc = Csr{};  // host copies no longer needed (csrA stays: tg_sim_reduced_operator)
-    csrB = Csr{};
+    if (!on_device) {
+      up(csrA, sA, devA);
+      up(csrAc, sAc, devAc);
+      up(csrB, sB, devB);
+      csrAc = Csr{};  // host copies no longer needed (csrA stays: tg_sim_reduced_operator)
+      csrB = Csr{};
+    }
     upload(d_free_list, dofs.free_list, s);
     csr_inverse_diagonal(devA, d_invd.p, d_status.p, s);
     pcg_blocks = csr_pcg_max_blocks(ctx->sm_count);

@@ -13,6 +13,7 @@
 #include "k2_kron.cuh"
 #include "k4_eval.cuh"
 #include "k5_fused.cuh"
+#include "k6_assemble.cuh"
 #include "k5_sumfact.cuh"
 #include "slab.hpp"
 
@@ -137,6 +138,11 @@ class Sim {
   std::array<Band1D, 3> band;
   std::array<double, 2> coefA{0, 0}, coefB{0, 0};
   Csr csrA, csrAc, csrB;
+  bool csr_deferred = false;  // assemble the general operators on the device (setup_device)
+  bool csr_device = false;    // ... and it did (csrA then only on demand: reduced_operator)
+  void assemble_csr_host();
+  bool assemble_csr_device(cudaStream_t s);
+  const Csr& reduced_operator();
 
   // ---- device
   tg_ctx* ctx = nullptr;

@@ -104,7 +104,7 @@ long tg_sim_reduced_operator(tg_sim* s, int* rows, int* row_ptr, int* col, doubl
   long nnz = -TG_ERROR;
   const int rc = sim_guard(s, [&](Sim& m) {
     if (m.kron) throw std::invalid_argument("separable patch: the operator is not assembled");
-    const Csr& A = m.csrA;
+    const Csr& A = m.reduced_operator();
     if (rows) *rows = A.rows;
     if (row_ptr) std::memcpy(row_ptr, A.row_ptr.data(), A.row_ptr.size() * sizeof(int));
     if (col) std::memcpy(col, A.col.data(), A.col.size() * sizeof(int));
