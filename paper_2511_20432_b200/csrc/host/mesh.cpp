@@ -56,20 +56,16 @@ DofMap make_dof_map(const NurbsVolume& vol, const BoundaryTags& tags) {
   return m;
 }
 
-FaceSets build_face_sets(const NurbsVolume& vol, const BoundaryTags& tags, int fine_mult) {
+std::vector<FaceElemSpec> face_elements(const NurbsVolume& vol, const BoundaryTags& tags,
+                                        int fine_mult, FaceSets& fs) {
   tags.validate();
   fine_mult = std::max(1, fine_mult);
   const auto p = vol.degrees();
-  FaceSets fs;
-  const int nd = (p[0] + 1) * (p[1] + 1) * (p[2] + 1);
-  fs.n_dofs = nd;
+  fs = FaceSets{};
+  fs.n_dofs = (p[0] + 1) * (p[1] + 1) * (p[2] + 1);
   // element list in the reference's order (face, then v-interval, then
   // u-interval; mesh.cpp:158-236) with its rule offsets
-  struct Elem {
-    FaceId f;
-    double mu, hu, mv, hv;
-    int qu, qv;
-  };
+  using Elem = FaceElemSpec;
   std::vector<Elem> el;
   fs.qb_off.push_back(0);
   fs.qf_off.push_back(0);
@@ -90,6 +86,15 @@ FaceSets build_face_sets(const NurbsVolume& vol, const BoundaryTags& tags, int f
       }
   }
   fs.n_elems = static_cast<int>(el.size());
+  return el;
+}
+
+FaceSets build_face_sets(const NurbsVolume& vol, const BoundaryTags& tags, int fine_mult) {
+  FaceSets fs;
+  const std::vector<FaceElemSpec> el = face_elements(vol, tags, fine_mult, fs);
+  using Elem = FaceElemSpec;
+  fine_mult = std::max(1, fine_mult);
+  const int nd = fs.n_dofs;
   const size_t tqb = fs.qb_off.back(), tqf = fs.qf_off.back();
   fs.centers.assign(3 * el.size(), 0.0);
   fs.dofs.assign(nd * el.size(), 0);

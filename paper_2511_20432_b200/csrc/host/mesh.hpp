@@ -45,6 +45,17 @@ struct FaceSets {
   std::vector<double> xf, nf, wf, Nf;   // fine rule
 };
 FaceSets build_face_sets(const NurbsVolume& vol, const BoundaryTags& tags, int fine_mult);
+// The lateral face elements in the reference's order (face, v-interval,
+// u-interval) and the layout fields of fs (n_elems, n_dofs, rule sizes and
+// offsets; no per-point arrays): build_face_sets' first half, shared with the
+// device builder (k6_assemble.cu).
+struct FaceElemSpec {
+  FaceId f;
+  double mu, hu, mv, hv;
+  int qu, qv;
+};
+std::vector<FaceElemSpec> face_elements(const NurbsVolume& vol, const BoundaryTags& tags,
+                                        int fine_mult, FaceSets& fs);
 
 // Physical positions of the Greville points of the constrained DOFs, in
 // constrained order (mesh.cpp:238-264).

@@ -383,6 +383,174 @@ __global__ void k6_fill_kernel(AsmPatch P, const int* __restrict__ row_ptr, AsmM
   }
 }
 
+// ---------------------------------------------------------------- face sets
+// map_point + face_point at face parameters (u, v) of face f: x, the outward
+// unit normal, the area scale |t_u x t_v|; N (nd basis values, nullable) and
+// the basis block's grid indices (nullable)
+__device__ void face_point_dev(const NurbsDev& V, int f, double u, double v, double* x,
+                               double* nrm, double* area, double* N, int* idx, int* flags) {
+  const int ax = f / 2;
+  const bool is_min = (f % 2) == 0;
+  const int t0 = ax == 0 ? 1 : 0, t1 = ax == 2 ? 1 : 2;
+  double xi[3];
+  xi[ax] = is_min ? 0.0 : 1.0;
+  xi[t0] = u;
+  xi[t1] = v;
+  double tab[3][2 * (kNurbsMaxP + 1)];
+  int sp[3];
+  for (int d = 0; d < 3; ++d) {
+    if (!find_span(V.U[d], V.p[d], V.n[d], xi[d], sp[d])) {
+      atomicOr(flags, 4);
+      return;
+    }
+    basis_ders1(V.U[d], V.p[d], xi[d], sp[d], tab[d]);
+  }
+  const int p0 = V.p[0], p1 = V.p[1], p2 = V.p[2];
+  auto gidx = [&](int i, int j, int k) {
+    return static_cast<long>(sp[0] - p0 + i) +
+           static_cast<long>(V.n[0]) *
+               (static_cast<long>(sp[1] - p1 + j) + static_cast<long>(V.n[1]) * (sp[2] - p2 + k));
+  };
+  // basis_at: weight sums in basis order, then the rational basis (as K4)
+  double W = 0.0, dW[3] = {0.0, 0.0, 0.0};
+  for (int k = 0; k <= p2; ++k) {
+    const double n3 = tab[2][k], d3 = tab[2][p2 + 1 + k];
+    for (int j = 0; j <= p1; ++j) {
+      const double n2 = tab[1][j], d2 = tab[1][p1 + 1 + j];
+      for (int i = 0; i <= p0; ++i) {
+        const double n1 = tab[0][i], d1 = tab[0][p0 + 1 + i];
+        const double w = V.pts[4 * gidx(i, j, k) + 3];
+        W += w * n1 * n2 * n3;
+        dW[0] += w * d1 * n2 * n3;
+        dW[1] += w * n1 * d2 * n3;
+        dW[2] += w * n1 * n2 * d3;
+      }
+    }
+  }
+  double xs[3] = {0.0, 0.0, 0.0}, jac[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+  int m = 0;
+  for (int k = 0; k <= p2; ++k) {
+    const double n3 = tab[2][k], d3 = tab[2][p2 + 1 + k];
+    for (int j = 0; j <= p1; ++j) {
+      const double n2 = tab[1][j], d2 = tab[1][p1 + 1 + j];
+      for (int i = 0; i <= p0; ++i, ++m) {
+        const double n1 = tab[0][i], d1 = tab[0][p0 + 1 + i];
+        const long g = gidx(i, j, k);
+        const double* c = V.pts + 4 * g;
+        const double w = c[3];
+        const double val = (w * n1 * n2 * n3) / W;
+        const double dv[3] = {(w * d1 * n2 * n3 - dW[0] * val) / W,
+                              (w * n1 * d2 * n3 - dW[1] * val) / W,
+                              (w * n1 * n2 * d3 - dW[2] * val) / W};
+        for (int r = 0; r < 3; ++r) {
+          xs[r] += c[r] * val;
+          for (int q = 0; q < 3; ++q) jac[3 * r + q] += c[r] * dv[q];
+        }
+        if (N) N[m] = val;
+        if (idx) idx[m] = static_cast<int>(g);
+      }
+    }
+  }
+  if (!(det3(jac) > 0.0)) atomicOr(flags, 1);
+  const double tu[3] = {jac[t0], jac[3 + t0], jac[6 + t0]};
+  const double tv[3] = {jac[t1], jac[3 + t1], jac[6 + t1]};
+  const double ac[3] = {jac[ax], jac[3 + ax], jac[6 + ax]};
+  const double cr[3] = {tu[1] * tv[2] - tu[2] * tv[1], tu[2] * tv[0] - tu[0] * tv[2],
+                        tu[0] * tv[1] - tu[1] * tv[0]};
+  const double ar = sqrt(cr[0] * cr[0] + cr[1] * cr[1] + cr[2] * cr[2]);
+  if (!(ar > 0.0)) atomicOr(flags, 2);
+  double n[3] = {cr[0] / ar, cr[1] / ar, cr[2] / ar};
+  const double sdot = n[0] * ac[0] + n[1] * ac[1] + n[2] * ac[2];
+  if ((is_min && sdot > 0.0) || (!is_min && sdot < 0.0))
+    for (int c = 0; c < 3; ++c) n[c] = n[c] * -1.0;
+  for (int c = 0; c < 3; ++c) {
+    x[c] = xs[c];
+    nrm[c] = n[c];
+  }
+  *area = ar;
+}
+
+__device__ __forceinline__ int elem_of(const int* off, int n_el, int q) {
+  int lo = 0, hi = n_el;  // off[lo] <= q < off[hi]
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (off[mid] <= q) lo = mid;
+    else hi = mid;
+  }
+  return lo;
+}
+
+__global__ void k6_face_points_kernel(FaceSetDev F) {
+  const long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x;
+  if (i >= static_cast<long>(F.tqb) + F.tqf) return;
+  const bool base = i < F.tqb;
+  const int q = static_cast<int>(base ? i : i - F.tqb);
+  const int e = elem_of(base ? F.qb_off : F.qf_off, F.n_el, q);
+  const FaceElemDev E = F.el[e];
+  const int mult = base ? 1 : F.fm;
+  const int nu = mult * E.qu, nv = mult * E.qv;
+  const int loc = q - (base ? F.qb_off[e] : F.qf_off[e]);
+  const int a = loc % nu, b = loc / nu;
+  const double* gun = F.gnodes + nu * (nu - 1) / 2;
+  const double* guw = F.gweights + nu * (nu - 1) / 2;
+  const double* gvn = F.gnodes + nv * (nv - 1) / 2;
+  const double* gvw = F.gweights + nv * (nv - 1) / 2;
+  const double u = E.mu + E.hu * gun[a];
+  const double v = E.mv + E.hv * gvn[b];
+  double area;
+  double* N = (base ? F.Nb : F.Nf) + static_cast<size_t>(q) * F.nd;
+  int* idx = base && loc == 0 ? F.dofs + static_cast<size_t>(e) * F.nd : nullptr;
+  face_point_dev(F.V, E.f, u, v, F.x + 3 * i, F.nrm + 3 * i, &area, N, idx, F.flags);
+  F.w[i] = guw[a] * gvw[b] * E.hu * E.hv * area;
+}
+
+__global__ void k6_face_centers_kernel(FaceSetDev F) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= F.n_el) return;
+  const FaceElemDev E = F.el[e];
+  double nrm[3], area;
+  face_point_dev(F.V, E.f, E.mu, E.mv, F.centers + 3 * static_cast<size_t>(e), nrm, &area,
+                 nullptr, nullptr, F.flags);
+}
+
+__global__ void k6_face_keep_kernel(FaceSetDev F, int* __restrict__ keep, int* __restrict__ nkeep) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= F.n_el) return;
+  int c = 0;
+  for (int a = 0; a < F.nd; ++a) {
+    bool nz = false;
+    for (int q = F.qb_off[e]; q < F.qb_off[e + 1] && !nz; ++q)
+      nz = F.Nb[static_cast<size_t>(q) * F.nd + a] != 0.0;
+    for (int q = F.qf_off[e]; q < F.qf_off[e + 1] && !nz; ++q)
+      nz = F.Nf[static_cast<size_t>(q) * F.nd + a] != 0.0;
+    if (nz) keep[static_cast<size_t>(e) * F.nd + c++] = a;
+  }
+  nkeep[e] = c;
+}
+
+__global__ void k6_face_compact_kernel(FaceSetDev F, const int* __restrict__ keep,
+                                       const int* __restrict__ nkeep, int ndk,
+                                       double* __restrict__ Nbk, double* __restrict__ Nfk,
+                                       int* __restrict__ dofk) {
+  const long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x;
+  const long npts = static_cast<long>(F.tqb) + F.tqf;
+  if (i < npts * ndk) {
+    const long pt = i / ndk;
+    const int kk = static_cast<int>(i - pt * ndk);
+    const bool base = pt < F.tqb;
+    const int q = static_cast<int>(base ? pt : pt - F.tqb);
+    const int e = elem_of(base ? F.qb_off : F.qf_off, F.n_el, q);
+    const double* N = (base ? F.Nb : F.Nf) + static_cast<size_t>(q) * F.nd;
+    const double val = kk < nkeep[e] ? N[keep[static_cast<size_t>(e) * F.nd + kk]] : 0.0;
+    (base ? Nbk : Nfk)[static_cast<size_t>(q) * ndk + kk] = val;
+  } else if (i < npts * ndk + static_cast<long>(F.n_el) * ndk) {
+    const long j = i - npts * ndk;
+    const int e = static_cast<int>(j / ndk), kk = static_cast<int>(j - static_cast<long>(e) * ndk);
+    dofk[j] = kk < nkeep[e] ? F.dofs[static_cast<size_t>(e) * F.nd + keep[static_cast<size_t>(e) * F.nd + kk]]
+                            : -1;
+  }
+}
+
 int ept_of(const AsmPatch& P) {
   const Layout L = layout_of(P);
   const int need = (L.T + kThreads - 1) / kThreads;
@@ -431,6 +599,31 @@ void k6_gather(const AsmPatch& P, const int* d_row_ptr, int r0, int r1, int k0, 
   const int warps = 8;
   k6_gather_kernel<<<(r1 - r0 + warps - 1) / warps, 32 * warps, 0, s>>>(
       P, d_row_ptr, r0, r1, k0, k1, e_base, d_lm, d_lk, d_M, d_K);
+  TG_CUDA(cudaGetLastError());
+}
+
+void k6_face_sets(const FaceSetDev& F, cudaStream_t s) {
+  for (int d = 0; d < 3; ++d)
+    if (F.V.p[d] > kNurbsMaxP) throw std::invalid_argument("degree > 7 not supported");
+  const long n = static_cast<long>(F.tqb) + F.tqf;
+  if (n > 0)
+    k6_face_points_kernel<<<static_cast<int>((n + 127) / 128), 128, 0, s>>>(F);
+  if (F.n_el > 0) k6_face_centers_kernel<<<(F.n_el + 127) / 128, 128, 0, s>>>(F);
+  TG_CUDA(cudaGetLastError());
+}
+
+void k6_face_keep(const FaceSetDev& F, int* d_keep, int* d_nkeep, cudaStream_t s) {
+  if (F.n_el <= 0) return;
+  k6_face_keep_kernel<<<(F.n_el + 127) / 128, 128, 0, s>>>(F, d_keep, d_nkeep);
+  TG_CUDA(cudaGetLastError());
+}
+
+void k6_face_compact(const FaceSetDev& F, const int* d_keep, const int* d_nkeep, int ndk,
+                     double* d_Nbk, double* d_Nfk, int* d_dofk, cudaStream_t s) {
+  const long n = (static_cast<long>(F.tqb) + F.tqf + F.n_el) * ndk;
+  if (n <= 0) return;
+  k6_face_compact_kernel<<<static_cast<int>((n + 255) / 256), 256, 0, s>>>(F, d_keep, d_nkeep, ndk,
+                                                                         d_Nbk, d_Nfk, d_dofk);
   TG_CUDA(cudaGetLastError());
 }
 

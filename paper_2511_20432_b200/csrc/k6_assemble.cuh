@@ -65,4 +65,43 @@ void k6_fill(const AsmPatch& P, const int* d_row_ptr, const AsmMaps& m, const do
              const double* d_K, double inv_dt, double th, double mth, const SellOut& A,
              const SellOut& Ac, const SellOut& B, cudaStream_t s);
 
+// ---------------------------------------------------------------------------
+// Face quadrature sets on the device: build_face_sets (host/mesh.cpp; the
+// reference's classify_boundary / build_face_element, proj/src/mesh.cpp:158-236,
+// face_point, proj/src/splines.cpp:305-321), bit-identical to the host's.
+
+// One lateral face element: face id (FaceId order), rule sizes, the element's
+// parametric centre / half width along the face's two tangent axes.
+struct FaceElemDev {
+  int f, qu, qv;
+  double mu, hu, mv, hv;
+};
+
+struct FaceSetDev {
+  NurbsDev V;
+  const FaceElemDev* el;
+  int n_el, fm, nd;        // elements, fine-rule multiplier, basis block size
+  const int* qb_off;       // n_el + 1 base / fine point offsets
+  const int* qf_off;
+  int tqb, tqf;
+  const double* gnodes;    // Gauss rules n = 1 .. nmax at offset n (n - 1) / 2
+  const double* gweights;
+  double* x;               // 3 per point: base points, then fine points
+  double* nrm;             // 3 per point (outward unit normals)
+  double* w;               // 1 per point
+  double* Nb;              // nd per base point (basis values, basis order)
+  double* Nf;              // nd per fine point
+  int* dofs;               // nd per element (grid indices of the basis block)
+  double* centers;         // 3 per element
+  int* flags;              // 1: non-positive det in the map, 2: degenerate surface point, 4: domain
+};
+void k6_face_sets(const FaceSetDev& F, cudaStream_t s);
+// the columns of each element nonzero at one of its base or fine points, in
+// order (keep: n_el x nd, nkeep: n_el)
+void k6_face_keep(const FaceSetDev& F, int* d_keep, int* d_nkeep, cudaStream_t s);
+// tables on the kept columns: Nbk / Nfk (ndk per point, zero padded), dofk
+// (ndk per element, -1 padded)
+void k6_face_compact(const FaceSetDev& F, const int* d_keep, const int* d_nkeep, int ndk,
+                     double* d_Nbk, double* d_Nfk, int* d_dofk, cudaStream_t s);
+
 }  // namespace tgb

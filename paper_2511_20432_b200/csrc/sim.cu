@@ -93,10 +93,13 @@ Sim::Sim(const std::string& path, const SimOptions& opt) {
   cfg = std::move(c);
   // the general patch's operators: assembled on the device when there is one
   csr_deferred = !opt.host_only && !std::getenv("TG_HOST_ASSEMBLY");
+  faces_deferred = !opt.host_only && !std::getenv("TG_HOST_FACES");
   setup_host();
   PhaseClock clk;
-  sf_setup_host();
-  clk.mark("k5 grids, tiles, entries");
+  if (!faces_deferred) {
+    sf_setup_host();
+    clk.mark("k5 grids, tiles, entries");
+  }
   if (!opt.host_only) setup_device(opt.device, opt.preconditioner);
   clk.mark("device setup");
 }
@@ -141,10 +144,13 @@ void Sim::setup_host() {
   // lateral face sets, with the columns that are exactly zero on every
   // quadrature point of an element dropped (their scatter adds +0, a no-op)
   clk.mark("volume, dofs, sources");
-  FaceSets fs = build_face_sets(vol, cfg.tags, cfg.mesh.boundary_quad_multiplier);
-  clk.mark("face sets");
+  FaceSets fs;
+  if (faces_deferred)  // the per-point tables come from the device (face_tables_device)
+    face_specs = face_elements(vol, cfg.tags, cfg.mesh.boundary_quad_multiplier, fs);
+  else
+    fs = build_face_sets(vol, cfg.tags, cfg.mesh.boundary_quad_multiplier);
+  clk.mark(faces_deferred ? "face layout" : "face sets");
   n_fe = fs.n_elems;
-  const int nd = fs.n_dofs;
   const long tqb = fs.qb_off.back(), tqf = fs.qf_off.back();
   if (tqb + tqf > (1L << 31) - 1) throw std::invalid_argument("face quadrature set too large");
   h_qb_off.assign(fs.qb_off.begin(), fs.qb_off.end());
@@ -154,6 +160,40 @@ void Sim::setup_host() {
     nqb = std::max(nqb, fs.nqb[e]);
     nqf = std::max(nqf, fs.nqf[e]);
   }
+  if (!faces_deferred) face_tables_host(fs);
+  clk.mark("face tables, incidence");
+  grev = greville_points(vol, dofs, cfg.tags);
+  clk.mark("greville points");
+
+  // operator: Kronecker factors when separable, else the assembled CSR pair
+  std::array<std::vector<double>, 3> coord;
+  // the Kronecker kernels take equal degrees 1..kKronMaxP; mixed or higher
+  // degrees use the assembled operator like any non-separable patch
+  {
+    const auto pd = vol.degrees();
+    const bool eq = pd[0] == pd[1] && pd[1] == pd[2] && pd[0] >= 1 && pd[0] <= kKronMaxP;
+    kron = eq && separable_coords(vol, coord);
+  }
+  const double dt = dt_solver, th = cfg.stepping.theta;
+  if (!(dt > 0.0)) throw std::invalid_argument("theta scheme: dt must be > 0");
+  if (!(th >= 0.0 && th <= 1.0)) throw std::invalid_argument("theta scheme: theta must be in [0,1]");
+  if (kron) {
+    for (int d = 0; d < 3; ++d) band[d] = assemble_band_1d(vol.knots(d), coord[d], quad[d]);
+    const double rc = cfg.material.volumetric_capacity(), k = cfg.material.conductivity;
+    coefA = {rc / dt, th * k};
+    coefB = {rc / dt, -(1.0 - th) * k};
+    clk.mark("kronecker factors");
+  } else if (!csr_deferred) {
+    assemble_csr_host();
+  }
+}
+
+// The face tables from host face sets: the columns exactly zero at every
+// point of an element dropped (their scatter adds +0, a no-op), positions,
+// normals, weights, the kept N columns and their DOFs, incidence lists.
+void Sim::face_tables_host(const FaceSets& fs) {
+  const int nd = fs.n_dofs;
+  const long tqb = fs.qb_off.back(), tqf = fs.qf_off.back();
   std::vector<std::vector<int>> keep(n_fe);
   parallel_for(n_fe, [&](long e) {
     for (int a = 0; a < nd; ++a) {
@@ -183,8 +223,106 @@ void Sim::setup_host() {
       h_dofk[static_cast<size_t>(e) * ndk + kk] = fs.dofs[static_cast<size_t>(e) * nd + a];
     }
   });
-  // incidence lists per DOF in the reference's scatter order (face, element, a):
-  // a stable counting sort of the kept (element, column) slots by DOF
+  build_incidence();
+}
+
+// The face tables built on the device (K6 face sets, bit-identical to
+// build_face_sets): points, normals, weights and the kept N columns stay there;
+// positions, normals, weights, centres and the kept DOFs come back for the
+// host-side setup (K5 grids, the step's fine-element test, incidence lists).
+void Sim::face_tables_device(cudaStream_t s) {
+  upload_nurbs();
+  const auto pd = vol.degrees();
+  const int nd = (pd[0] + 1) * (pd[1] + 1) * (pd[2] + 1);
+  const int tqb = h_qb_off.back(), tqf = h_qf_off.back();
+  const int fm = std::max(1, cfg.mesh.boundary_quad_multiplier);
+  std::vector<FaceElemDev> el(n_fe);
+  int nmax = 1;
+  for (int e = 0; e < n_fe; ++e) {
+    const FaceElemSpec& f = face_specs[e];
+    el[e] = FaceElemDev{static_cast<int>(f.f), f.qu, f.qv, f.mu, f.hu, f.mv, f.hv};
+    nmax = std::max(nmax, fm * std::max(f.qu, f.qv));
+  }
+  std::vector<double> gn, gw;  // Gauss rules 1..nmax at offset n (n - 1) / 2
+  for (int n = 1; n <= nmax; ++n) {
+    const GaussRule& g = gauss_rule(n);
+    gn.insert(gn.end(), g.nodes.begin(), g.nodes.end());
+    gw.insert(gw.end(), g.weights.begin(), g.weights.end());
+  }
+  DevBuf<FaceElemDev> d_el;
+  DevBuf<double> d_gn, d_gw, Nb, Nf, cen;
+  DevBuf<int> dofs_all, keep, nkeep, dofk, flag;
+  upload(d_el, el, s);
+  upload(d_gn, gn, s);
+  upload(d_gw, gw, s);
+  upload(d_qb_off, h_qb_off, s);
+  upload(d_qf_off, h_qf_off, s);
+  const size_t npts = static_cast<size_t>(tqb) + tqf;
+  d_qx.ensure(3 * (npts + n_con));  // room for the Greville points (sf_setup_device)
+  d_qn.ensure(3 * npts);
+  d_qw.ensure(npts);
+  Nb.ensure(static_cast<size_t>(tqb) * nd);
+  Nf.ensure(static_cast<size_t>(tqf) * nd);
+  dofs_all.ensure(static_cast<size_t>(n_fe) * nd);
+  cen.ensure(3 * static_cast<size_t>(n_fe));
+  flag.ensure(1);
+  TG_CUDA(cudaMemsetAsync(flag.p, 0, sizeof(int), s));
+  FaceSetDev F{nurbs, d_el.p, n_fe, fm, nd, d_qb_off.p, d_qf_off.p, tqb, tqf, d_gn.p, d_gw.p,
+               d_qx.p, d_qn.p, d_qw.p, Nb.p, Nf.p, dofs_all.p, cen.p, flag.p};
+  k6_face_sets(F, s);
+  keep.ensure(static_cast<size_t>(n_fe) * nd);
+  nkeep.ensure(n_fe);
+  k6_face_keep(F, keep.p, nkeep.p, s);
+  int fl = 0;
+  std::vector<int> nk(n_fe);
+  TG_CUDA(cudaMemcpyAsync(&fl, flag.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+  if (n_fe > 0)
+    TG_CUDA(cudaMemcpyAsync(nk.data(), nkeep.p, sizeof(int) * n_fe, cudaMemcpyDeviceToHost, s));
+  TG_CUDA(cudaStreamSynchronize(s));
+  if (fl & 4) throw std::domain_error("find_span: parameter outside the knot range");
+  if (fl & 1) throw numeric_error("non-positive Jacobian determinant in geometry map");
+  if (fl & 2) throw numeric_error("degenerate surface point");
+  ndk = 1;
+  for (int e = 0; e < n_fe; ++e) ndk = std::max(ndk, nk[e]);
+  d_Nb.ensure(static_cast<size_t>(tqb) * ndk);
+  d_Nf.ensure(static_cast<size_t>(tqf) * ndk);
+  dofk.ensure(static_cast<size_t>(n_fe) * ndk);
+  k6_face_compact(F, keep.p, nkeep.p, ndk, d_Nb.p, d_Nf.p, dofk.p, s);
+  h_qx.resize(3 * npts);
+  h_qn.resize(3 * npts);
+  h_qw.resize(npts);
+  centers.resize(3 * static_cast<size_t>(n_fe));
+  h_dofk.resize(static_cast<size_t>(n_fe) * ndk);
+  auto down = [&](auto& v, const auto* src) {
+    if (!v.empty())
+      TG_CUDA(cudaMemcpyAsync(v.data(), src, v.size() * sizeof(v[0]), cudaMemcpyDeviceToHost, s));
+  };
+  down(h_qx, d_qx.p);
+  down(h_qn, d_qn.p);
+  down(h_qw, d_qw.p);
+  down(centers, cen.p);
+  down(h_dofk, dofk.p);
+  TG_CUDA(cudaStreamSynchronize(s));  // the temporaries die here
+  h_Nb.clear();  // on demand (face_tables_to_host)
+  h_Nf.clear();
+  build_incidence();
+}
+
+// the kept N tables on the host (tg_sim_face_sets) when they were built on the device
+void Sim::face_tables_to_host() {
+  if (!faces_deferred || !ctx || !h_Nb.empty()) return;
+  const size_t nb = static_cast<size_t>(h_qb_off.back()) * ndk;
+  const size_t nf = static_cast<size_t>(h_qf_off.back()) * ndk;
+  h_Nb.resize(nb);
+  h_Nf.resize(nf);
+  if (nb) TG_CUDA(cudaMemcpyAsync(h_Nb.data(), d_Nb.p, nb * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  if (nf) TG_CUDA(cudaMemcpyAsync(h_Nf.data(), d_Nf.p, nf * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  TG_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+// incidence lists per DOF in the reference's scatter order (face, element, a):
+// a stable counting sort of the kept (element, column) slots by DOF
+void Sim::build_incidence() {
   h_inc_ptr.assign(n_full + 1, 0);
   for (size_t s2 = 0; s2 < h_dofk.size(); ++s2)
     if (h_dofk[s2] >= 0) ++h_inc_ptr[h_dofk[s2] + 1];
@@ -194,32 +332,6 @@ void Sim::setup_host() {
     std::vector<int> fill(h_inc_ptr.begin(), h_inc_ptr.end() - 1);
     for (size_t s2 = 0; s2 < h_dofk.size(); ++s2)
       if (h_dofk[s2] >= 0) h_inc_src[fill[h_dofk[s2]]++] = static_cast<int>(s2);
-  }
-
-  clk.mark("face tables, incidence");
-  grev = greville_points(vol, dofs, cfg.tags);
-  clk.mark("greville points");
-
-  // operator: Kronecker factors when separable, else the assembled CSR pair
-  std::array<std::vector<double>, 3> coord;
-  // the Kronecker kernels take equal degrees 1..kKronMaxP; mixed or higher
-  // degrees use the assembled operator like any non-separable patch
-  {
-    const auto pd = vol.degrees();
-    const bool eq = pd[0] == pd[1] && pd[1] == pd[2] && pd[0] >= 1 && pd[0] <= kKronMaxP;
-    kron = eq && separable_coords(vol, coord);
-  }
-  const double dt = dt_solver, th = cfg.stepping.theta;
-  if (!(dt > 0.0)) throw std::invalid_argument("theta scheme: dt must be > 0");
-  if (!(th >= 0.0 && th <= 1.0)) throw std::invalid_argument("theta scheme: theta must be in [0,1]");
-  if (kron) {
-    for (int d = 0; d < 3; ++d) band[d] = assemble_band_1d(vol.knots(d), coord[d], quad[d]);
-    const double rc = cfg.material.volumetric_capacity(), k = cfg.material.conductivity;
-    coefA = {rc / dt, th * k};
-    coefB = {rc / dt, -(1.0 - th) * k};
-    clk.mark("kronecker factors");
-  } else if (!csr_deferred) {
-    assemble_csr_host();
   }
 }
 
@@ -462,11 +574,19 @@ void Sim::setup_device(int device, int preconditioner) {
   if (!sources.empty())
     TG_CUDA(cudaMemcpyAsync(d, sources.data(), sources.size() * sizeof(PointSource),
                             cudaMemcpyHostToDevice, s));
-  upload(d_qx, h_qx, s);
-  upload(d_qn, h_qn, s);
-  upload(d_qw, h_qw, s);
-  upload(d_Nb, h_Nb, s);
-  upload(d_Nf, h_Nf, s);
+  if (faces_deferred) {  // face tables on the device, then the K5 host setup on their points
+    PhaseClock clk;
+    face_tables_device(s);
+    clk.mark("face tables on the device");
+    sf_setup_host();
+    clk.mark("k5 grids, tiles, entries");
+  } else {
+    upload(d_qx, h_qx, s);
+    upload(d_qn, h_qn, s);
+    upload(d_qw, h_qw, s);
+    upload(d_Nb, h_Nb, s);
+    upload(d_Nf, h_Nf, s);
+  }
   upload(d_inc_ptr, h_inc_ptr, s);
   upload(d_inc_src, h_inc_src, s);
   upload(d_grev, grev, s);
@@ -824,26 +944,42 @@ void Sim::sf_setup_host() {
   sf_flux_ok = tqb > 0;
   std::vector<int> ekey(n_fe, -1);
   std::vector<std::vector<int>> kelems(6);
-  for (int e = 0; e < n_fe && sf_flux_ok; ++e) {
-    ekey[e] = normal_key(h_qb_off[e]);
-    for (int q = h_qb_off[e]; q < h_qb_off[e + 1] && sf_flux_ok; ++q)
-      sf_flux_ok = ekey[e] >= 0 && normal_key(q) == ekey[e];
-    for (int l = h_qf_off[e]; l < h_qf_off[e + 1] && sf_flux_ok; ++l)
-      sf_flux_ok = normal_key(tqb + l) == ekey[e];
-    if (sf_flux_ok) kelems[ekey[e]].push_back(e);
+  {  // per element: one axis normal shared by all its points (-1: none)
+    std::vector<char> ok(n_fe, 1);
+    parallel_for(n_fe, [&](long e) {
+      ekey[e] = normal_key(h_qb_off[e]);
+      bool good = ekey[e] >= 0;
+      for (int q = h_qb_off[e]; q < h_qb_off[e + 1] && good; ++q) good = normal_key(q) == ekey[e];
+      for (int l = h_qf_off[e]; l < h_qf_off[e + 1] && good; ++l)
+        good = normal_key(tqb + l) == ekey[e];
+      ok[e] = good;
+    }, 256);
+    for (int e = 0; e < n_fe && sf_flux_ok; ++e) {
+      sf_flux_ok = ok[e] != 0;
+      if (sf_flux_ok) kelems[ekey[e]].push_back(e);
+    }
   }
   // base grid per face (normal key)
   sf_h_gcell.assign(tqb, -1);
   std::vector<int> q_face(tqb, -1);
   sf_elem_face.assign(n_fe, -1);
+  // the faces' base grids (in parallel; used in face-key order below)
+  SfGrid kgrid[6];
+  char kgood[6] = {1, 1, 1, 1, 1, 1};
+  if (sf_flux_ok)
+    parallel_for(6, [&](long k) {
+      if (kelems[k].empty()) return;
+      std::vector<double> pts;
+      for (int e : kelems[k])
+        for (int q = h_qb_off[e]; q < h_qb_off[e + 1]; ++q)
+          for (int d = 0; d < 3; ++d) pts.push_back(h_qx[3 * static_cast<size_t>(q) + d]);
+      kgood[k] = sf_make_grid(pts.data(), static_cast<long>(pts.size() / 3), tol, kgrid[k]) &&
+                 kgrid[k].axn == k / 2;
+    }, 1);
   for (int k = 0; k < 6 && sf_flux_ok; ++k) {
     if (kelems[k].empty()) continue;
-    std::vector<double> pts;
-    for (int e : kelems[k])
-      for (int q = h_qb_off[e]; q < h_qb_off[e + 1]; ++q)
-        for (int d = 0; d < 3; ++d) pts.push_back(h_qx[3 * static_cast<size_t>(q) + d]);
-    SfGrid g;
-    if (!sf_make_grid(pts.data(), static_cast<long>(pts.size() / 3), tol, g) || g.axn != k / 2) {
+    SfGrid& g = kgrid[k];
+    if (!kgood[k]) {
       sf_flux_ok = false;
       break;
     }
@@ -869,14 +1005,19 @@ void Sim::sf_setup_host() {
     sf_erect.assign(4 * static_cast<size_t>(n_fe), 0);
     std::vector<std::vector<int>> felems(sf_faces.size());
     for (int e = 0; e < n_fe; ++e) felems[sf_elem_face[e]].push_back(e);
-    for (size_t f = 0; f < felems.size() && sf_fine_ok; ++f) {
+    std::vector<SfGrid> fgrid(felems.size());
+    std::vector<char> fgood(felems.size(), 1);
+    parallel_for(static_cast<long>(felems.size()), [&](long f) {
       std::vector<double> pts;
       for (int e : felems[f])
         for (int l = h_qf_off[e]; l < h_qf_off[e + 1]; ++l)
           for (int d = 0; d < 3; ++d) pts.push_back(h_qx[3 * static_cast<size_t>(tqb + l) + d]);
-      SfGrid g;
-      if (!sf_make_grid(pts.data(), static_cast<long>(pts.size() / 3), tol, g) ||
-          g.axn != sf_faces[f].axn) {
+      fgood[f] = sf_make_grid(pts.data(), static_cast<long>(pts.size() / 3), tol, fgrid[f]) &&
+                 fgrid[f].axn == sf_faces[f].axn;
+    }, 1);
+    for (size_t f = 0; f < felems.size() && sf_fine_ok; ++f) {
+      SfGrid& g = fgrid[f];
+      if (!fgood[f]) {
         sf_fine_ok = false;
         break;
       }
@@ -990,7 +1131,7 @@ void Sim::sf_setup_host() {
   // history; padded to whole K1 CTAs
   sf_k1_ppc = kK1Threads * 7;  // k1_partial<7, GRAD> (the remainder launch)
   constexpr int kBlockA = 48;
-  for (int t = 0; t < sf_nt_static; ++t) {
+  parallel_for(sf_nt_static, [&](long t) {
     std::vector<int> ord(tile_pts[t].size());
     std::iota(ord.begin(), ord.end(), 0);
     const auto& cells = tile_cell[t];
@@ -1006,7 +1147,7 @@ void Sim::sf_setup_host() {
     }
     tile_pts[t].swap(p2);
     tile_cell[t].swap(c2);
-  }
+  }, 1);
   sf_ent_q.clear();
   sf_ent_tile.clear();
   sf_ent_cell.clear();
@@ -1131,8 +1272,9 @@ void Sim::sf_setup_device() {
   // remainder launch)
   if (sf_dir_ok) {
     d_qx.ensure(3 * (static_cast<size_t>(tqb) + tqf + n_con));  // (never grows: sized here)
-    TG_CUDA(cudaMemcpyAsync(d_qx.p, h_qx.data(), h_qx.size() * sizeof(double),
-                            cudaMemcpyHostToDevice, s));
+    if (!faces_deferred)  // (device-built face points are in place already)
+      TG_CUDA(cudaMemcpyAsync(d_qx.p, h_qx.data(), h_qx.size() * sizeof(double),
+                              cudaMemcpyHostToDevice, s));
     TG_CUDA(cudaMemcpyAsync(d_qx.p + 3 * (static_cast<size_t>(tqb) + tqf), grev.data(),
                             grev.size() * sizeof(double), cudaMemcpyHostToDevice, s));
   }

@@ -138,6 +138,12 @@ class Sim {
   std::array<Band1D, 3> band;
   std::array<double, 2> coefA{0, 0}, coefB{0, 0};
   Csr csrA, csrAc, csrB;
+  bool faces_deferred = false;  // face tables built on the device (face_tables_device)
+  std::vector<FaceElemSpec> face_specs;
+  void face_tables_host(const FaceSets& fs);
+  void face_tables_device(cudaStream_t s);
+  void face_tables_to_host();
+  void build_incidence();
   bool csr_deferred = false;  // assemble the general operators on the device (setup_device)
   bool csr_device = false;    // ... and it did (csrA then only on demand: reduced_operator)
   void assemble_csr_host();

@@ -251,6 +251,7 @@ int tg_sim_face_sets(tg_sim* s, int* qb_off, int* qf_off, double* centers, int* 
     auto cp = [](auto* dst, const auto& v) {
       if (dst) std::memcpy(dst, v.data(), v.size() * sizeof(v[0]));
     };
+    if (Nb || Nf) m.face_tables_to_host();
     cp(qb_off, m.h_qb_off);
     cp(qf_off, m.h_qf_off);
     cp(centers, m.centers);

@@ -6,7 +6,10 @@ proj/src/assembly.cpp:59-101, 194-228; proj/src/mesh.cpp:65-117).
     pointers, columns, values), as the host assembly does (tests/test_cfg3.py);
   * A_fc and B_f (only seen through the θ-step) give time steps bit-identical
     to the host-assembled operators' (TG_HOST_ASSEMBLY=1);
-  * config 3 at full size: the device's A_ff equals the host assembly's."""
+  * config 3 at full size: the device's A_ff equals the host assembly's;
+  * the face quadrature sets built on the device (build_face_sets, the
+    reference's build_face_element, proj/src/mesh.cpp:158-236) equal the host
+    build bit for bit: points, normals, weights, kept N columns, DOFs, centres."""
 import os
 
 import numpy as np
@@ -73,3 +76,18 @@ def test_config3_full_size_device_operator_is_the_host_one():
     hp, hc, hv = h.reduced_operator()
     h.close()
     assert np.array_equal(rp, hp) and np.array_equal(ci, hc) and np.array_equal(v, hv)
+
+
+@pytest.mark.parametrize("name", ["cfg0_parity", "qc_small", "cfg3_parity", "cfg2_raster_layer"])
+def test_device_face_sets_bit_exact(name):
+    path = os.path.join(ROOT, "configs", name + ".cfg")
+    d = tg.Simulation(path)  # device face tables
+    h = tg.Simulation(path, host_only=True)
+    try:
+        assert d.info["n_dofs_kept"] == h.info["n_dofs_kept"]
+        fd, fh = d.face_sets(), h.face_sets()
+        for k in ("qb_off", "qf_off", "centers", "dofs", "xq", "nq", "wq", "Nb", "Nf"):
+            assert np.array_equal(fd[k], fh[k]), k
+    finally:
+        d.close()
+        h.close()
