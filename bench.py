@@ -68,10 +68,10 @@ PIPE_OPS_PER_PAIR = 17.0
 # PLANAR variant takes rz and rz^2 per point: 8 DFMA + 5 DADD + 2 DMUL
 PIPE_OPS_PER_PAIR_PLANAR = 15.0
 # DRAM bytes (read + write) per launch from one `ncu --set full` capture of each
-# dominant kernel (profiles/r01_k1_ncu_summary.md, r01_k2_ncu_summary.md)
-K1_TRAFFIC_BYTES = 92.2e6 + 484.4e6   # k1_partial<7,1,1>, config 1, one launch
-K2_TRAFFIC_B_PER_DOF_ITER = 80.0      # k2_cg1_kernel<2> (scaled), config 4 (13.06 + 12.56 GB / 74 sweeps)
-K5_TRAFFIC_BYTES = 37.29e6 + 0.89e6   # sf_contract_kernel, config 4 step 1 (flux + Dirichlet)
+# dominant kernel (profiles/r02b_*.ncu-rep, profiles/r02_profiles_summary.md)
+K1_TRAFFIC_BYTES = 43.07e6 + 81.90e6  # k1_partial<7,1,1>, config 1, one launch (4 source splits)
+K2_TRAFFIC_B_PER_DOF_ITER = 72.6      # k2_cg1_kernel<2,2>, config 4 (13.54 + 12.87 GB / 84 sweeps)
+K5_TRAFFIC_BYTES = 37.92e6 + 3.89e6   # sf_contract_kernel, config 4 step 1 (flux + Dirichlet)
 
 
 def parse():
@@ -434,7 +434,7 @@ def theta_section(steps, warmup, with_cpu):
                             "peak_source": "measured live: tg_dmma_peak (independent DMMA "
                                            "m8n8k4 accumulators) on this GPU",
                             "traffic": K5_TRAFFIC_BYTES,
-                            "traffic_source": "ncu --set full, profiles/r02_k5_ncu_summary.md "
+                            "traffic_source": "ncu --set full, profiles/r02b_k5_contract.ncu-rep "
                                               "(dram read + write per launch)"},
                "min_region_prefix_flux": sf["last_j_flux"],
                "min_region_prefix_dirichlet": sf["last_j_dirichlet"],
@@ -447,8 +447,8 @@ def theta_section(steps, warmup, with_cpu):
                      "frac": achieved / peak if achieved else None,
                      "traffic": (K2_TRAFFIC_B_PER_DOF_ITER * sim.info["n_free"] * iters / steps
                                  if sim.info["kronecker"] == 2 else None),
-                     "traffic_source": "ncu --set full, profiles/r01_k2_cg1s_full.ncu-rep: "
-                                       "80 B/DOF/iteration measured, per solve",
+                     "traffic_source": "ncu --set full, profiles/r02b_k2_cg1.ncu-rep: "
+                                       "72.6 B/DOF/iteration measured, per solve",
                      "peak_source": src,
                      "bytes_per_dof_per_iteration": 104},
     }
@@ -718,7 +718,7 @@ def run_ours(args):
             "unit": "T FP64 instr/s",
             "frac": (achieved_ops / pipe_peak) if (achieved_ops and pipe_peak) else None,
             "traffic": K1_TRAFFIC_BYTES,
-            "traffic_source": "ncu --set full, profiles/r01_k1_full_p7_planar.ncu-rep (dram "
+            "traffic_source": "ncu --set full, profiles/r02b_k1_full.ncu-rep (dram "
                               "read+write)",
             "peak_source": "measured live: tg_fp64_peak DFMA-chain microbenchmark on this GPU "
                            "(no FP64 entry in MEASURED_PEAKS.json or the recipe's fallback)",

@@ -739,6 +739,9 @@ constexpr int kCg1Nin = K2_CG1_SCALED ? 3 : 4;
 #ifndef K2_CG1_UB
 #define K2_CG1_UB 1
 #endif
+#ifndef K2_DEFER_X
+#define K2_DEFER_X 1  // x read / written every second sweep (bit-identical iterates)
+#endif
 #ifndef K2_STUDY_NOSWEEP
 #define K2_STUDY_NOSWEEP 0
 #endif
@@ -1257,7 +1260,7 @@ __global__ void __launch_bounds__(kThreads, K2_MINB)
     ProCg1S<P, PL> pc{alpha, beta, x,   w.p,  w.r[cur ^ 1], w.s[cur ^ 1], nx, ny, cr, &maps.xc,
                       &maps.pc, &cseq, &g, a,   b,            {{}, zb, g.n[2]}, 0.0, 0.0};
     // x is read and written every second sweep only (80 -> 72 B/DOF/iteration)
-    pc.xmode = (it & 1) ? 2 : 1;
+    pc.xmode = K2_DEFER_X ? ((it & 1) ? 2 : 1) : 0;
     pc.alpha_prev = alpha_prev;
     EpiCg1S<P, ProCg1S<P, PL>> e{w.w[cur ^ 1], &pc, a, b, 0.0};
     const Inputs<NIN> in = inputs(cur);
@@ -1306,7 +1309,7 @@ __global__ void __launch_bounds__(kThreads, K2_MINB)
     alpha = g1 / den;
     gamma = g1;
   }
-  if (it > 0 && ((it - 1) & 1) == 0) {  // the last sweep deferred its x update
+  if (K2_DEFER_X && it > 0 && ((it - 1) & 1) == 0) {  // the last sweep deferred its x update
     const size_t n = static_cast<size_t>(nx) * ny * g.n[2];
     for (size_t f = static_cast<size_t>(blockIdx.x) * kThreads + threadIdx.y * kKronTX + threadIdx.x;
          f < n; f += static_cast<size_t>(gridDim.x) * kThreads)
