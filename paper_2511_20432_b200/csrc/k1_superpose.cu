@@ -24,6 +24,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <type_traits>
 
 #include "common.cuh"
 #include "k1_superpose.cuh"
@@ -177,7 +178,7 @@ __global__ void __launch_bounds__(kK1Threads,
       rz2[k] = __dmul_rn(pz[k], pz[k]);
     }
   }
-  if constexpr (BOX) {  // the bounding box of the CTA's points (PLANAR: z as rz)
+  {  // the bounding box of the CTA's points (PLANAR: z as rz)
     double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
     for (int k = 0; k < P; ++k)
@@ -215,6 +216,23 @@ __global__ void __launch_bounds__(kK1Threads,
     const int cnt = min(kK1Chunk, len - c * kK1Chunk);
     const SrcRec* rb = ring[buf];
     int n_iter = cnt;
+    // every source of the chunk keeps every pair with the CTA's points (the
+    // farthest corner of their box within each source's exact keep threshold,
+    // with a margin far above the box and r.r roundings): the pair loop then
+    // skips the per-pair cull test — the same keep decisions, so the same sums
+    bool full = false;
+    if constexpr (!BOX) {
+      bool f = true;
+      if (tid < cnt) {
+        const SrcRec& q = rb[tid];
+        const double fx = fmax(fabs(boxs[0] - q.sx), fabs(boxs[3] - q.sx));
+        const double fy = fmax(fabs(boxs[1] - q.sy), fabs(boxs[4] - q.sy));
+        const double fz = PLANAR ? fmax(fabs(boxs[2]), fabs(boxs[5]))
+                                 : fmax(fabs(boxs[2] - q.sz), fabs(boxs[5] - q.sz));
+        f = (fx * fx + fy * fy + fz * fz) * (1.0 + 1e-9) <= q.thr;
+      }
+      full = __syncthreads_and(f) != 0;
+    }
     if constexpr (BOX) {  // the chunk's sources that reach the CTA's box, in order
       bool keep = false;
       if (tid < cnt) {
@@ -244,6 +262,8 @@ __global__ void __launch_bounds__(kK1Threads,
       for (int w = 0; w < kK1Chunk / 32; ++w) n_iter += keep_n[w];
       __syncthreads();
     }
+    auto pairs = [&](auto full_tag) {
+    constexpr bool FULL = decltype(full_tag)::value;
 #pragma unroll kK1Unroll
     for (int jj = 0; jj < n_iter; ++jj) {
       const int j = BOX ? keep_list[jj] : jj;
@@ -268,12 +288,14 @@ __global__ void __launch_bounds__(kK1Threads,
         // keep/cull decided on the high words (1 unit = 2^32 ulp >> the few-ulp
         // gap): thr < 0 (inactive source) lands in the cull branch; the band
         // hi32(r.r) in [lo, lo + 2] is re-decided exactly below
-        const int h = __double2hiint(r2[k]);
-        keep[k] = h < lo;
-        band = min(band, static_cast<unsigned>(h - lo));
+        if (!FULL) {
+          const int h = __double2hiint(r2[k]);
+          keep[k] = h < lo;
+          band = min(band, static_cast<unsigned>(h - lo));
+        }
         if (K1_VOTE_LATE) e[k] = src_exp(r2[k], a.w, b.x, q.x, q.y, q.z, tab);
       }
-      if (__any_sync(0xffffffffu, band <= 2u)) {  // warp-uniform, rare
+      if (!FULL && __any_sync(0xffffffffu, band <= 2u)) {  // warp-uniform, rare
         // the reference's exact r.r (association of core.hpp:27, no
         // contraction) and its exact compare, for every point of the warp
 #pragma unroll
@@ -287,7 +309,7 @@ __global__ void __launch_bounds__(kK1Threads,
 #pragma unroll
       for (int k = 0; k < P; ++k) {
         if (!K1_VOTE_LATE) e[k] = src_exp(r2[k], a.w, b.x, q.x, q.y, q.z, tab);
-        const double T = keep[k] ? e[k] : 0.0;
+        const double T = (FULL || keep[k]) ? e[k] : 0.0;
         v[k] = __dadd_rn(v[k], T);
         if (GRAD) {
           const double w = __dmul_rn(T, b.y);
@@ -297,6 +319,11 @@ __global__ void __launch_bounds__(kK1Threads,
         }
       }
     }
+    };
+    if (full)
+      pairs(std::true_type{});
+    else
+      pairs(std::false_type{});
     __syncthreads();  // everyone is done with ring[buf]
     if (tid == 0 && c + kK1Stages < n_chunks) {
       const int cn = c + kK1Stages;
