@@ -92,7 +92,7 @@ __global__ void k1_prepare_sources(const double* __restrict__ src6, int n, doubl
 
 // tuning knobs (tools/k1_variants.py builds and times the alternatives)
 #ifndef K1_UNROLL
-#define K1_UNROLL 4
+#define K1_UNROLL 3  // measured (config 1, chunk fast path): 1 0.977e12, 2 0.978e12, 3 0.981e12, 4 0.959e12, 8 0.962e12 pairs/s
 #endif
 #ifndef K1_MINB4
 #define K1_MINB4 2
