@@ -418,23 +418,30 @@ __global__ void __launch_bounds__(kSfThreads, kSfMinBlocks)
       // 0 and land in cells nobody reads): no divergence, 32 independent
       // exponentials per thread
 #pragma unroll
-      for (int r = 0; r < kSfTA / kWarps; ++r) {  // A: rows warp + kWarps r, column lane
+      for (int r = 0; r < (kSfTA + kWarps - 1) / kWarps; ++r) {  // A: rows warp + kWarps r, column lane
         const int a = warp + kWarps * r;
-        const double d = sm.U[a] - k.u;
-        sm.A[buf][a][lane] = sf_exp(d * d, k.nisp, k.magicL, k.q0, k.q1, k.q2, k.pad, sm.tab);
+        if (kSfTA % kWarps == 0 || a < kSfTA) {  // (compile-time true for the default shape)
+          const double d = sm.U[a] - k.u;
+          sm.A[buf][a][lane] = sf_exp(d * d, k.nisp, k.magicL, k.q0, k.q1, k.q2, k.pad, sm.tab);
+        }
       }
       if (G.vplane) {
 #pragma unroll
-        for (int r = 0; r < kSfTB / kWarps; ++r) {
+        for (int r = 0; r < (kSfTB + kWarps - 1) / kWarps; ++r) {
           const int b = warp + kWarps * r;
-          sm.B[buf][b][lane] = sf_exp(sm.V[b], k.nisp, kExpMagic, kSfE0, kSfE1, kSfE2, kSfE3, sm.tab);
+          if (kSfTB % kWarps == 0 || b < kSfTB)
+            sm.B[buf][b][lane] =
+                sf_exp(sm.V[b], k.nisp, kExpMagic, kSfE0, kSfE1, kSfE2, kSfE3, sm.tab);
         }
       } else {
 #pragma unroll
-        for (int r = 0; r < kSfTB / kWarps; ++r) {
+        for (int r = 0; r < (kSfTB + kWarps - 1) / kWarps; ++r) {
           const int b = warp + kWarps * r;
-          const double d = sm.V[b] - k.v;
-          sm.B[buf][b][lane] = sf_exp(d * d, k.nisp, kExpMagic, kSfE0, kSfE1, kSfE2, kSfE3, sm.tab);
+          if (kSfTB % kWarps == 0 || b < kSfTB) {
+            const double d = sm.V[b] - k.v;
+            sm.B[buf][b][lane] =
+                sf_exp(d * d, k.nisp, kExpMagic, kSfE0, kSfE1, kSfE2, kSfE3, sm.tab);
+          }
         }
       }
     };
