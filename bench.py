@@ -493,16 +493,14 @@ def theta_sharded_section(steps, rank, world, local):
     its, _ = loop.step(steps)
     prof = ctx.profile()
     ctx.set_profiling(False)
-    ms = torch.tensor([prof["step_ms"] / steps], dtype=torch.float64, device=f"cuda:{local}")
-    if world > 1:
-        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    ms = prof["step_ms"] / steps  # this rank's; the caller takes the max over ranks
     st = sim.state()
     sim.close()
     return {"workload": f"config4 time steps on {world} GPU(s): K5 regions and theta-step "
                         "z-slabs split over the ranks (NCCL all-reduce of the loads, halo + "
                         "partial-sum exchange per CG iteration)" if world > 1 else
                         "config4 time steps on 1 GPU (no split)",
-            "n_gpus": world, "steps": steps, "ms_per_step": float(ms.item()),
+            "n_gpus": world, "steps": steps, "ms_per_step": float(ms),
             "cg_iterations_per_step": its / steps,
             "state_checksum": float(np.abs(st["free"]).sum()),
             "timing": "CUDA events around tg_sim_advance on each rank's stream, max over ranks",
@@ -607,6 +605,9 @@ def run_ours(args):
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl")
+        # a rank stuck in the sharded section's own NCCL calls aborts them and
+        # reports an error instead of holding the job (csrc/slab.cu stream_wait)
+        os.environ.setdefault("TG_NCCL_TIMEOUT", "90")
     dev = torch.device("cuda", local)
 
     def barrier():
@@ -690,6 +691,16 @@ def run_ours(args):
             sharded = theta_sharded_section(args.theta_sharded, rank, world, local)
         except Exception as e:
             sharded = {"error": str(e)}
+        if world > 1:  # every rank gets here (success or error): one agreement step
+            import torch
+            import torch.distributed as dist
+            t = torch.tensor([sharded.get("ms_per_step", 0.0), 1.0 if "error" in sharded else 0.0],
+                             dtype=torch.float64, device=f"cuda:{local}")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            if t[1].item() > 0.0 and "error" not in sharded:
+                sharded = {"error": "another rank failed in the sharded section"}
+            elif "error" not in sharded:
+                sharded["ms_per_step"] = float(t[0].item())
 
     if rank != 0:
         if world > 1:
