@@ -11,7 +11,9 @@
 
 #include <algorithm>
 #include <string>
+#include <unordered_map>
 
+#include "host/parallel.hpp"
 #include "k5_sumfact.cuh"
 
 namespace tgb {
@@ -26,16 +28,31 @@ struct Clusters {
   }
 };
 
-bool cluster_axis(std::vector<double> v, double tol, Clusters& c) {
+// The coordinates of one axis as sorted distinct values with multiplicities
+// (a grid's points repeat each line coordinate many times: counting them in a
+// hash map and sorting the few distinct values replaces a sort of all n);
+// clusters of values within tol are the grid lines, each represented by its
+// median element counting multiplicity (what a sort of all n values gives).
+bool cluster_axis(const double* pts, long n, int ax, double tol, Clusters& c) {
+  std::unordered_map<double, long> count;
+  count.reserve(4096);
+  for (long i = 0; i < n; ++i) ++count[pts[3 * i + ax]];
+  std::vector<std::pair<double, long>> v(count.begin(), count.end());
   std::sort(v.begin(), v.end());
   size_t b = 0;
+  long nb = 0;  // elements in the current cluster
   for (size_t i = 1; i <= v.size(); ++i) {
-    if (i < v.size() && v[i] - v[i - 1] <= tol) continue;
-    if (v[i - 1] - v[b] > tol) return false;  // a chained cluster: not a grid line
-    c.lo.push_back(v[b]);
-    c.hi.push_back(v[i - 1]);
-    c.rep.push_back(v[b + (i - 1 - b) / 2]);
+    nb += v[i - 1].second;
+    if (i < v.size() && v[i].first - v[i - 1].first <= tol) continue;
+    if (v[i - 1].first - v[b].first > tol) return false;  // a chained cluster: not a grid line
+    c.lo.push_back(v[b].first);
+    c.hi.push_back(v[i - 1].first);
+    long k = (nb - 1) / 2;  // the median element's rank in the cluster
+    size_t m = b;
+    while (k >= v[m].second) k -= v[m++].second;
+    c.rep.push_back(v[m].first);
     b = i;
+    nb = 0;
   }
   return true;
 }
@@ -45,10 +62,12 @@ bool cluster_axis(std::vector<double> v, double tol, Clusters& c) {
 bool sf_make_grid(const double* pts, long n, double tol, SfGrid& g) {
   if (n <= 0) return false;
   Clusters cl[3];
+  char ok[3] = {0, 0, 0};
+  parallel_for(3, [&](long ax) {  // the three axes side by side
+    ok[ax] = cluster_axis(pts, n, static_cast<int>(ax), tol, cl[ax]);
+  }, 1);
   for (int ax = 0; ax < 3; ++ax) {
-    std::vector<double> v(n);
-    for (long i = 0; i < n; ++i) v[i] = pts[3 * i + ax];
-    if (!cluster_axis(std::move(v), tol, cl[ax])) return false;
+    if (!ok[ax]) return false;
     g.lo[ax] = cl[ax].lo.front();
     g.hi[ax] = cl[ax].hi.back();
   }
@@ -67,19 +86,36 @@ bool sf_make_grid(const double* pts, long n, double tol, SfGrid& g) {
   g.V = cl[g.axv].rep;
   const long na = static_cast<long>(g.U.size()), nb = static_cast<long>(g.V.size());
   if (na * nb != n) return false;
-  std::vector<char> seen(n, 0);
   g.cell.assign(n, -1);
+  // cells and the largest offset from the grid lines, in parallel chunks
+  constexpr long kChunk = 1 << 16;
+  const long nch = (n + kChunk - 1) / kChunk;
+  std::vector<double> dmax(nch, 0.0);
+  std::vector<char> bad(nch, 0);
+  parallel_for(nch, [&](long ch) {
+    double dm = 0.0;
+    for (long i = ch * kChunk; i < std::min(n, (ch + 1) * kChunk); ++i) {
+      const double* p = pts + 3 * i;
+      const int a = cl[g.axu].find(p[g.axu]), b = cl[g.axv].find(p[g.axv]);
+      if (a < 0 || b < 0) {
+        bad[ch] = 1;
+        return;
+      }
+      g.cell[i] = static_cast<int>(a + na * b);
+      dm = std::max({dm, std::fabs(p[axn] - g.xf), std::fabs(p[g.axu] - g.U[a]),
+                     std::fabs(p[g.axv] - g.V[b])});
+    }
+    dmax[ch] = dm;
+  }, 1);
   g.delta = 0.0;
+  for (long ch = 0; ch < nch; ++ch) {
+    if (bad[ch]) return false;
+    g.delta = std::max(g.delta, dmax[ch]);
+  }
+  std::vector<char> seen(n, 0);  // every cell exactly once
   for (long i = 0; i < n; ++i) {
-    const double* p = pts + 3 * i;
-    const int a = cl[g.axu].find(p[g.axu]), b = cl[g.axv].find(p[g.axv]);
-    if (a < 0 || b < 0) return false;
-    const long c = a + na * b;
-    if (seen[c]) return false;
-    seen[c] = 1;
-    g.cell[i] = static_cast<int>(c);
-    g.delta = std::max({g.delta, std::fabs(p[axn] - g.xf), std::fabs(p[g.axu] - g.U[a]),
-                        std::fabs(p[g.axv] - g.V[b])});
+    if (seen[g.cell[i]]) return false;
+    seen[g.cell[i]] = 1;
   }
   return true;
 }

@@ -911,6 +911,7 @@ SfRegion box_of(const SfGrid& g, int a0, int na, int b0, int nb) {
 }  // namespace
 
 void Sim::sf_setup_host() {
+  PhaseClock clk;
   if (const char* e = std::getenv("TG_SF_MIN_PAIRS")) sf_min_pairs = std::atof(e);
   if (const char* e = std::getenv("TG_SF_MIN_SOURCES")) sf_min_sources = std::atoi(e);
   if (const char* e = std::getenv("TG_SF_K1_SPLITS"))
@@ -1042,6 +1043,7 @@ void Sim::sf_setup_host() {
     }
     if (!sf_fine_ok) sf_fine.clear();
   }
+  clk.mark("  k5: face grids");
   sf_dir_ok = n_con > 0 && sf_make_grid(grev.data(), n_con, tol, sf_dir);
 
   // grids: faces, fine faces, Greville (descriptor lines are device pointers,
@@ -1129,6 +1131,7 @@ void Sim::sf_setup_host() {
   // kBlockA cells along a, b slower, a fastest), so that each K1 CTA's 1792
   // points span a small box and its per-CTA source culling drops more of the
   // history; padded to whole K1 CTAs
+  clk.mark("  k5: greville grid, tiles");
   sf_k1_ppc = kK1Threads * 7;  // k1_partial<7, GRAD> (the remainder launch)
   constexpr int kBlockA = 48;
   parallel_for(sf_nt_static, [&](long t) {
@@ -1148,6 +1151,7 @@ void Sim::sf_setup_host() {
     tile_pts[t].swap(p2);
     tile_cell[t].swap(c2);
   }, 1);
+  clk.mark("  k5: entry order");
   sf_ent_q.clear();
   sf_ent_tile.clear();
   sf_ent_cell.clear();
@@ -1183,6 +1187,7 @@ void Sim::sf_setup_host() {
     std::fprintf(stderr, "[k5] flux %d fine %d dir %d grids %zu tiles %d+%d entries %d+%d\n",
                  sf_flux_ok, sf_fine_ok, sf_dir_ok, sf_grids_h.size(), sf_nt_flux,
                  sf_nt_static - sf_nt_flux, sf_ne_flux, sf_ne_static - sf_ne_flux);
+  clk.mark("  k5: entries");
   const char* e = std::getenv("TG_SUMFACT");
   set_sumfact(!(e && std::string(e) == "0"));
 }
