@@ -69,7 +69,7 @@ PIPE_OPS_PER_PAIR = 17.0
 PIPE_OPS_PER_PAIR_PLANAR = 15.0
 # DRAM bytes (read + write) per launch from one `ncu --set full` capture of each
 # dominant kernel (profiles/r02b_*.ncu-rep, profiles/r02_profiles_summary.md)
-K1_TRAFFIC_BYTES = 43.07e6 + 81.90e6  # k1_partial<7,1,1>, config 1, one launch (4 source splits)
+K1_TRAFFIC_BYTES = 43.56e6 + 81.39e6  # k1_partial<7,1,1>, config 1, one launch (4 source splits)
 K2_TRAFFIC_B_PER_DOF_ITER = 72.6      # k2_cg1_kernel<2,2>, config 4 (13.54 + 12.87 GB / 84 sweeps)
 K5_TRAFFIC_BYTES = 37.92e6 + 3.89e6   # sf_contract_kernel, config 4 step 1 (flux + Dirichlet)
 
@@ -729,7 +729,7 @@ def run_ours(args):
             "unit": "T FP64 instr/s",
             "frac": (achieved_ops / pipe_peak) if (achieved_ops and pipe_peak) else None,
             "traffic": K1_TRAFFIC_BYTES,
-            "traffic_source": "ncu --set full, profiles/r02b_k1_full.ncu-rep (dram "
+            "traffic_source": "ncu --set full, profiles/r02c_k1_full.ncu-rep (dram "
                               "read+write)",
             "peak_source": "measured live: tg_fp64_peak DFMA-chain microbenchmark on this GPU "
                            "(no FP64 entry in MEASURED_PEAKS.json or the recipe's fallback)",
