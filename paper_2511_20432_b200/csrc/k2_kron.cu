@@ -34,6 +34,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -58,11 +59,28 @@ constexpr int kTmaPlanes = 2;  // planes per TMA box / per sweep step
 #endif
 constexpr int kL2Ahead = K2_L2_AHEAD;  // steps beyond the shared-memory ring prefetched into L2
 
-template <int P, int PL>
+#ifndef K2_STRIP_W
+#define K2_STRIP_W 6  // cost of a strip column-plane in quarters of a main one
+#endif
+// Tile shapes (control points per CTA, one per thread): the main 32 x 8
+// tiles, and for grids whose x extent leaves a ragged remainder of <= 8
+// columns (config 4: 258 = 8 * 32 + 2) a transposed 8 x 32 strip tile over
+// those last columns, so the remainder costs ceil(ny / 32) tiles per plane
+// instead of ceil(ny / 8) nearly empty 32-wide ones. Both shapes have the
+// same halo'd plane size, so they share every shared-memory ring.
+template <int TX_, int TY_, bool STRIP>
+struct TileShape {
+  static constexpr int TX = TX_, TY = TY_;
+  static constexpr bool kStrip = STRIP;
+};
+using MainTile = TileShape<kKronTX, kKronTY, false>;
+using StripTile = TileShape<kKronTY, kKronTX, true>;
+
+template <int P, int PL, class Sh = MainTile>
 struct Dims {
   static constexpr int W = 2 * P + 1;
-  static constexpr int RY = kKronTY + 2 * P;
-  static constexpr int RX = kKronTX + 2 * P;
+  static constexpr int RY = Sh::TY + 2 * P;
+  static constexpr int RX = Sh::TX + 2 * P;
   static constexpr int PLANE = RY * RX;                                    // doubles
   static constexpr int SLOT = ((PL * PLANE * 8 + 127) / 128) * 128 / 8;    // 128-byte slots
 };
@@ -81,8 +99,9 @@ struct KSmem {
   static constexpr int kUb = UB;
   double ring[NIN][ST][Dims<P, PL>::SLOT];
   double v[PL][Dims<P, PL>::PLANE];
-  double u1[NPASS][UB][PL][Dims<P, PL>::RY][kKronTX];
-  double u2[NPASS][UB][PL][Dims<P, PL>::RY][kKronTX];
+  // x-pass output rows [RY][TX] of the tile shape (the main shape's is the larger)
+  double u1[NPASS][UB][PL][Dims<P, PL>::RY * kKronTX];
+  double u2[NPASS][UB][PL][Dims<P, PL>::RY * kKronTX];
   uint64_t bar[NIN][ST];
 };
 
@@ -96,40 +115,101 @@ __host__ __device__ constexpr size_t zband_offset() {
 // `blocks` equal contiguous ranges; a CTA sweeps its range as 1-2 column
 // segments (each costs P halo planes per side). Equal shares whatever the
 // column count (a static map keeps the reductions deterministic).
+// With a strip (nsy > 0) the main tiles cover the first ntx * 32 columns and
+// nsy strip tiles of 8 x 32 the columns from xs on; strip columns follow the
+// main ones in the linearized column list.
+// The CTAs' shares are cut in work units: a main column-plane costs wm units,
+// a strip column-plane ws (strip tiles sweep slower per plane: narrow TMA
+// boxes, 2-way bank conflicts on their 12-double rows), so the CTAs holding
+// strip planes are not the last at the grid barrier.
 struct TileIdx {
   int ntx, nty, nz;
+  int nsy = 0;  // strip tiles along y (0: no strip)
+  int xs = 0;   // first column of the strip
+  int wm = 1, ws = 1;
 };
 struct Seg {
   int x0, y0, k0, k1;
+  int strip = 0;
 };
 inline TileIdx make_tiles(const KronGrid& g) {
   return {(g.n[0] + kKronTX - 1) / kKronTX, (g.n[1] + kKronTY - 1) / kKronTY, g.n[2]};
 }
+// the strip split when the ragged x remainder fits one strip tile's width
+inline bool strip_applies(const KronGrid& g) {
+  const int rx = g.n[0] % kKronTX;
+  return g.n[0] > kKronTX && rx > 0 && rx <= StripTile::TX;
+}
+inline TileIdx make_tiles_strip(const KronGrid& g) {
+  TileIdx T = make_tiles(g);
+  if (!strip_applies(g)) return T;
+  T.ntx = g.n[0] / kKronTX;
+  T.xs = T.ntx * kKronTX;
+  T.nsy = (g.n[1] + StripTile::TY - 1) / StripTile::TY;
+  T.wm = 4;
+  T.ws = K2_STRIP_W;
+  if (const char* e = std::getenv("TG_K2_STRIP_W")) T.ws = std::max(1, std::atoi(e));
+  return T;
+}
+__host__ __device__ __forceinline__ long n_columns(const TileIdx& T) {
+  return static_cast<long>(T.ntx) * T.nty + T.nsy;
+}
+__host__ __device__ __forceinline__ long n_units(const TileIdx& T) {
+  return (static_cast<long>(T.ntx) * T.nty * T.wm + static_cast<long>(T.nsy) * T.ws) * T.nz;
+}
+__device__ __forceinline__ Seg column_seg(const TileIdx& T, int col, int k0, int k1) {
+  const int nmain = T.ntx * T.nty;
+  if (col < nmain) return Seg{(col % T.ntx) * kKronTX, (col / T.ntx) * kKronTY, k0, k1, 0};
+  return Seg{T.xs, (col - nmain) * StripTile::TY, k0, k1, 1};
+}
+// The next segment of the unit range [u, e): the planes whose first unit lies
+// in it, within one column (false when none is left). Plane k of column c
+// starts at unit base(c) + k w(c), so the CTA ranges partition the planes.
+__device__ __forceinline__ bool next_segment(const TileIdx& T, long& u, long e, Seg& out) {
+  const long mtot = static_cast<long>(T.ntx) * T.nty * T.wm * T.nz;
+  const int ncol = static_cast<int>(n_columns(T));
+  while (u < e) {
+    int col, w;
+    long base;
+    if (u < mtot) {
+      w = T.wm;
+      col = static_cast<int>(u / (static_cast<long>(T.nz) * w));
+      base = static_cast<long>(col) * T.nz * w;
+    } else {
+      w = T.ws;
+      const int sc = static_cast<int>((u - mtot) / (static_cast<long>(T.nz) * w));
+      col = T.ntx * T.nty + sc;
+      base = mtot + static_cast<long>(sc) * T.nz * w;
+    }
+    if (col >= ncol) return false;
+    const long k0 = (u - base + w - 1) / w;
+    if (k0 >= T.nz) {  // no plane starts in the rest of this column
+      u = base + static_cast<long>(T.nz) * w;
+      continue;
+    }
+    if (base + k0 * w >= e) return false;
+    const long k1 = min(static_cast<long>(T.nz), (e - base + w - 1) / w);
+    out = column_seg(T, col, static_cast<int>(k0), static_cast<int>(k1));
+    u = base + k1 * w;
+    return true;
+  }
+  return false;
+}
 template <class F>
 __device__ __forceinline__ void for_segments(const TileIdx& T, int blocks, int b, F&& fn) {
-  const long total = static_cast<long>(T.ntx) * T.nty * T.nz;
-  long s = total * b / blocks;
+  const long total = n_units(T);
+  long u = total * b / blocks;
   const long e = total * (b + 1) / blocks;
-  while (s < e) {
-    const int col = static_cast<int>(s / T.nz);
-    const int k0 = static_cast<int>(s % T.nz);
-    const int k1 = static_cast<int>(min(static_cast<long>(T.nz), k0 + (e - s)));
-    fn(Seg{(col % T.ntx) * kKronTX, (col / T.ntx) * kKronTY, k0, k1});
-    s += k1 - k0;
-  }
+  Seg sg;
+  while (next_segment(T, u, e, sg)) fn(sg);
 }
 
 // The first segment for_segments hands CTA b (false when its range is empty).
 __device__ __forceinline__ bool first_segment(const TileIdx& T, int blocks, int b, Seg& out) {
-  const long total = static_cast<long>(T.ntx) * T.nty * T.nz;
-  const long s = total * b / blocks;
+  const long total = n_units(T);
+  long u = total * b / blocks;
   const long e = total * (b + 1) / blocks;
-  if (s >= e) return false;
-  const int col = static_cast<int>(s / T.nz);
-  const int k0 = static_cast<int>(s % T.nz);
-  const int k1 = static_cast<int>(min(static_cast<long>(T.nz), k0 + (e - s)));
-  out = Seg{(col % T.ntx) * kKronTX, (col / T.ntx) * kKronTY, k0, k1};
-  return true;
+  return next_segment(T, u, e, out);
 }
 
 // Jacobi diagonal of Op(a, b) = a M + b K at (i, j, k) from the diagonals of
@@ -178,6 +258,7 @@ template <int NIN>
 struct Inputs {
   const double* ptr[NIN];
   const TensorMap3* map[NIN];
+  const TensorMap3* smap[NIN] = {};  // strip-tile boxes (sweeps over strip segments)
 };
 
 template <int P, int PL, int NIN, int NPASS, int ST, int UB>
@@ -207,19 +288,35 @@ __device__ __forceinline__ void init_smem(const KronGrid& g, KSmem<P, PL, NIN, N
 // sweep uses; seqs[q] counts the boxes ring q has delivered (mbarrier phases).
 struct NoPro {
   static constexpr bool kV = false;
-  template <class SM>
-  __device__ void operator()(SM&, const int*, int, int, const Seg&) {}
+  template <class SM, class Sh>
+  __device__ void operator()(SM&, const int*, int, int, const Seg&, Sh) {}
 };
 
-template <int P, int PL, int NIN, int NPASS, bool TMA, class SM, class Pro, class Epi>
+// the thread's point of a tile of shape Sh
+template <class Sh>
+__device__ __forceinline__ void tile_xy(int& tx, int& ty) {
+  const int tid = threadIdx.y * kKronTX + threadIdx.x;
+  tx = tid % Sh::TX;
+  ty = tid / Sh::TX;
+}
+template <class Sh, int NIN>
+__device__ __forceinline__ const TensorMap3* in_map(const Inputs<NIN>& in, int q) {
+  return Sh::kStrip ? in.smap[q] : in.map[q];
+}
+
+template <int P, int PL, int NIN, int NPASS, bool TMA, class Sh = MainTile, class SM, class Pro,
+          class Epi>
 __device__ __forceinline__ void kron_tile(const KronGrid& g, const KronTerms& c,
                                           const Inputs<NIN>& in, Pro& pro, const Seg& sg,
                                           SM& sm, const double* zb, int* seqs, Epi& epi,
                                           bool primed = false) {
-  using D = Dims<P, PL>;
+  using D = Dims<P, PL, Sh>;
   constexpr int W = D::W, RY = D::RY, RX = D::RX, PLANE = D::PLANE;
-  const int tx = threadIdx.x, ty = threadIdx.y;
-  const bool leader = tx == 0 && ty == 0;
+  static_assert(PLANE == Dims<P, PL>::PLANE, "tile shapes share the ring slots");
+  int tx, ty;
+  tile_xy<Sh>(tx, ty);
+  const int tid = threadIdx.y * kKronTX + threadIdx.x;
+  const bool leader = tid == 0;
   const int x0 = sg.x0, y0 = sg.y0, k0 = sg.k0, k1 = sg.k1;
   const int nx = g.n[0], ny = g.n[1], nz = g.n[2];
   const int i = x0 + tx, j = y0 + ty;
@@ -233,11 +330,12 @@ __device__ __forceinline__ void kron_tile(const KronGrid& g, const KronTerms& c,
       for (int q = 0; q < NIN; ++q) {
         const int slot = (seqs[q] + s) % SM::kSt;
         mbar_arrive_expect_tx(&sm.bar[q][slot], kBoxBytes);
-        tma_load_box(sm.ring[q][slot], in.map[q], x0 - P, y0 - P, kfirst + PL * s,
+        tma_load_box(sm.ring[q][slot], in_map<Sh>(in, q), x0 - P, y0 - P, kfirst + PL * s,
                      &sm.bar[q][slot]);
       }
     for (int s = SM::kSt; s < SM::kSt + kL2Ahead && s < nsteps; ++s)
-      for (int q = 0; q < NIN; ++q) tma_prefetch_box(in.map[q], x0 - P, y0 - P, kfirst + PL * s);
+      for (int q = 0; q < NIN; ++q)
+        tma_prefetch_box(in_map<Sh>(in, q), x0 - P, y0 - P, kfirst + PL * s);
   }
 
   // this thread's x and y rows of the 1D factors, in registers (the sweep is
@@ -272,7 +370,7 @@ __device__ __forceinline__ void kron_tile(const KronGrid& g, const KronTerms& c,
       for (int q = 0; q < NIN; ++q)
         for (int l = 0; l < PL; ++l) {
           const int kin = kin0 + l;
-          for (int e = ty * kKronTX + tx; e < PLANE; e += kThreads) {
+          for (int e = tid; e < PLANE; e += kThreads) {
             const int gi = x0 + e % RX - P, gj = y0 + e / RX - P;
             double val = 0.0;
             if (gi >= 0 && gi < nx && gj >= 0 && gj < ny && kin >= 0 && kin < nz)
@@ -288,15 +386,16 @@ __device__ __forceinline__ void kron_tile(const KronGrid& g, const KronTerms& c,
       if (TMA && leader && s + SM::kSt < nsteps)
         for (int q = 0; q < NIN; ++q) {
           mbar_arrive_expect_tx(&sm.bar[q][slot[q]], kBoxBytes);
-          tma_load_box(sm.ring[q][slot[q]], in.map[q], x0 - P, y0 - P,
+          tma_load_box(sm.ring[q][slot[q]], in_map<Sh>(in, q), x0 - P, y0 - P,
                        kfirst + PL * (s + SM::kSt), &sm.bar[q][slot[q]]);
           if (s + SM::kSt + kL2Ahead < nsteps)
-            tma_prefetch_box(in.map[q], x0 - P, y0 - P, kfirst + PL * (s + SM::kSt + kL2Ahead));
+            tma_prefetch_box(in_map<Sh>(in, q), x0 - P, y0 - P,
+                             kfirst + PL * (s + SM::kSt + kL2Ahead));
         }
     };
     double po[PL];
     if constexpr (Pro::kV) {  // v over the halo'd tiles (and the prologue's own-point work)
-      pro(sm, slot, s, kin0, sg);
+      pro(sm, slot, s, kin0, sg, Sh{});
       __syncthreads();
       refill();  // the ring is only read by the prologue
 #pragma unroll
@@ -306,7 +405,7 @@ __device__ __forceinline__ void kron_tile(const KronGrid& g, const KronTerms& c,
 #pragma unroll
     for (int q = 0; q < NPASS; ++q)
       // (plane, row) pairs dealt round-robin to the 8 warps: equal shares
-      for (int lr = ty; lr < PL * RY; lr += kKronTY) {
+      for (int lr = ty; lr < PL * RY; lr += Sh::TY) {
         const int l = lr / RY, r = lr - l * RY;
         const double* src = Pro::kV ? sm.v[l] : sm.ring[q][slot[q < NIN ? q : 0]] + l * PLANE;
         {
@@ -317,8 +416,8 @@ __device__ __forceinline__ void kron_tile(const KronGrid& g, const KronTerms& c,
             a1 = fma(mx[d], vv, a1);
             a2 = fma(kx[d], vv, a2);
           }
-          sm.u1[q][ub][l][r][tx] = a1;
-          sm.u2[q][ub][l][r][tx] = a2;
+          sm.u1[q][ub][l][r * Sh::TX + tx] = a1;
+          sm.u2[q][ub][l][r * Sh::TX + tx] = a2;
         }
       }
     __syncthreads();
@@ -332,9 +431,9 @@ __device__ __forceinline__ void kron_tile(const KronGrid& g, const KronTerms& c,
         double w1 = 0.0, w2 = 0.0, w3 = 0.0;
 #pragma unroll
         for (int d = 0; d < W; ++d) {
-          const double p1 = sm.u1[q][ub][l][ty + d][tx];
+          const double p1 = sm.u1[q][ub][l][(ty + d) * Sh::TX + tx];
           w1 = fma(my[d], p1, w1);
-          w2 = fma(my[d], sm.u2[q][ub][l][ty + d][tx], w2);
+          w2 = fma(my[d], sm.u2[q][ub][l][(ty + d) * Sh::TX + tx], w2);
           w3 = fma(ky[d], p1, w3);
         }
         const double a = q == 0 ? c.a1 : c.a2, b = q == 0 ? c.b1 : c.b2;
@@ -364,6 +463,19 @@ __device__ __forceinline__ void kron_tile(const KronGrid& g, const KronTerms& c,
   }
 #pragma unroll
   for (int q = 0; q < NIN; ++q) seqs[q] += nsteps;
+}
+
+// kron_tile on a segment of either tile shape (sweeps whose TileIdx may hold
+// a strip)
+template <int P, int PL, int NIN, int NPASS, bool TMA, class SM, class Pro, class Epi>
+__device__ __forceinline__ void kron_seg(const KronGrid& g, const KronTerms& c,
+                                         const Inputs<NIN>& in, Pro& pro, const Seg& sg, SM& sm,
+                                         const double* zb, int* seqs, Epi& epi,
+                                         bool primed = false) {
+  if (sg.strip)
+    kron_tile<P, PL, NIN, NPASS, TMA, StripTile>(g, c, in, pro, sg, sm, zb, seqs, epi, primed);
+  else
+    kron_tile<P, PL, NIN, NPASS, TMA, MainTile>(g, c, in, pro, sg, sm, zb, seqs, epi, primed);
 }
 
 // ---------------------------------------------------------------------------
@@ -461,8 +573,8 @@ __device__ __forceinline__ void prime_ring(const Inputs<NIN>& in, const Seg& sg,
     for (int q = 0; q < NIN; ++q) {
       const int slot = (seqs[q] + s) % SM::kSt;
       mbar_arrive_expect_tx(&sm.bar[q][slot], kBoxBytes);
-      tma_load_box(sm.ring[q][slot], in.map[q], sg.x0 - P, sg.y0 - P, sg.k0 - P + PL * s,
-                   &sm.bar[q][slot]);
+      tma_load_box(sm.ring[q][slot], sg.strip ? in.smap[q] : in.map[q], sg.x0 - P, sg.y0 - P,
+                   sg.k0 - P + PL * s, &sm.bar[q][slot]);
     }
 }
 
@@ -546,8 +658,9 @@ struct EpiResidual {  // r = b - A x; z = D^-1 r; p_old = 0; rr, bb, rz
 struct ProCombine {  // v = z + beta p_old over the halo'd tiles (ring 0: z, ring 1: p_old)
   static constexpr bool kV = true;
   double beta;
-  template <class SM>
-  __device__ void operator()(SM& sm, const int* slot, int, int, const Seg&) {
+  template <class SM, class Sh>
+  __device__ void operator()(SM& sm, const int* slot, int, int, const Seg&, Sh) {
+    static_assert(!Sh::kStrip, "main tiles only");
     constexpr int N = sizeof(sm.v) / sizeof(double);
     for (int e = threadIdx.y * kKronTX + threadIdx.x; e < N; e += kThreads)
       (&sm.v[0][0])[e] = fma(beta, sm.ring[1][slot[1]][e], sm.ring[0][slot[0]][e]);
@@ -752,8 +865,9 @@ struct ProScale {  // init: v = D^-1 r0 (ring 0: r0, ring 1: D^-1); gamma0 on ow
   static constexpr bool kV = true;
   int nx, ny;
   double gamma;
-  template <class SM>
-  __device__ void operator()(SM& sm, const int* slot, int, int kin0, const Seg& sg) {
+  template <class SM, class Sh>
+  __device__ void operator()(SM& sm, const int* slot, int, int kin0, const Seg& sg, Sh) {
+    static_assert(!Sh::kStrip, "main tiles only");
     using D = Dims<P, PL>;
     constexpr int N = PL * D::PLANE;
     const double* rr = sm.ring[0][slot[0]];
@@ -806,8 +920,9 @@ struct ProCg1 {  // rings: 0 r_i, 1 w_i, 2 s_{i-1}, 3 D^-1; centre ring: x, p_{i
     mbar_arrive_expect_tx(&cr->bar[1][slot], bytes);
     tma_load_box(cr->buf[1][slot], mp, sg.x0, sg.y0, kin0, &cr->bar[1][slot]);
   }
-  template <class SM>
-  __device__ void operator()(SM& sm, const int* slot, int s, int kin0, const Seg& sg) {
+  template <class SM, class Sh>
+  __device__ void operator()(SM& sm, const int* slot, int s, int kin0, const Seg& sg, Sh) {
+    static_assert(!Sh::kStrip, "main tiles only");
     using D = Dims<P, PL>;
     constexpr int N = PL * D::PLANE;
     const int nsteps = (sg.k1 - sg.k0 + 2 * P + PL - 1) / PL;
@@ -913,10 +1028,12 @@ struct ProCopy {  // init: v = u0 (ring 0), so the epilogue sees u0 at its point
   const KronGrid* g;
   int nx, ny;
   OwnDiag<P> od;
-  template <class SM>
-  __device__ void operator()(SM& sm, const int* slot, int s, int, const Seg& sg) {
+  template <class SM, class Sh>
+  __device__ void operator()(SM& sm, const int* slot, int s, int, const Seg& sg, Sh) {
     constexpr int N = PL * Dims<P, PL>::PLANE;
-    const int i = sg.x0 + threadIdx.x, j = sg.y0 + threadIdx.y;
+    int tx, ty;
+    tile_xy<Sh>(tx, ty);
+    const int i = sg.x0 + tx, j = sg.y0 + ty;
     if (s == 0 && i < nx && j < ny) od.set(*g, i, j);
     const double* uu = sm.ring[0][slot[0]];
     for (int e = threadIdx.y * kKronTX + threadIdx.x; e < N; e += kThreads)
@@ -947,7 +1064,10 @@ struct ProCg1S {  // rings: 0 u_i, 1 w^_i, 2 s^_{i-1}; centre ring: x, p_{i-1}
   // + alpha p_i (the same two fma roundings as two sweeps of mode 0)
   int xmode = 0;
   double alpha_prev = 0.0;
+  const TensorMap3* smx = nullptr;  // strip-tile boxes of x and p
+  const TensorMap3* smp = nullptr;
 
+  template <class Sh>
   __device__ void issue(const Seg& sg, int step) const {
     const int q = *cseq + step, slot = q & 1;
     constexpr uint32_t bytes = CentreRing<PL>::kBox * 8;
@@ -956,22 +1076,24 @@ struct ProCg1S {  // rings: 0 u_i, 1 w^_i, 2 s^_{i-1}; centre ring: x, p_{i-1}
       mbar_arrive(&cr->bar[0][slot]);  // completes the slot's phase without a copy
     } else {
       mbar_arrive_expect_tx(&cr->bar[0][slot], bytes);
-      tma_load_box(cr->buf[0][slot], mx, sg.x0, sg.y0, kin0, &cr->bar[0][slot]);
+      tma_load_box(cr->buf[0][slot], Sh::kStrip ? smx : mx, sg.x0, sg.y0, kin0,
+                   &cr->bar[0][slot]);
     }
     mbar_arrive_expect_tx(&cr->bar[1][slot], bytes);
-    tma_load_box(cr->buf[1][slot], mp, sg.x0, sg.y0, kin0, &cr->bar[1][slot]);
+    tma_load_box(cr->buf[1][slot], Sh::kStrip ? smp : mp, sg.x0, sg.y0, kin0, &cr->bar[1][slot]);
   }
-  template <class SM>
-  __device__ void operator()(SM& sm, const int* slot, int s, int kin0, const Seg& sg) {
-    using D = Dims<P, PL>;
+  template <class SM, class Sh>
+  __device__ void operator()(SM& sm, const int* slot, int s, int kin0, const Seg& sg, Sh) {
+    using D = Dims<P, PL, Sh>;
     constexpr int N = PL * D::PLANE;
     const int nsteps = (sg.k1 - sg.k0 + 2 * P + PL - 1) / PL;
-    const int tx = threadIdx.x, ty = threadIdx.y;
+    int tx, ty;
+    tile_xy<Sh>(tx, ty);
     const int i = sg.x0 + tx, j = sg.y0 + ty;
     const bool own = i < nx && j < ny;
-    if (tx == 0 && ty == 0) {
-      if (s == 0) issue(sg, 0);
-      if (s + 1 < nsteps) issue(sg, s + 1);
+    if (threadIdx.x == 0 && threadIdx.y == 0) {
+      if (s == 0) issue<Sh>(sg, 0);
+      if (s + 1 < nsteps) issue<Sh>(sg, s + 1);
     }
     if (s == 0 && own) od.set(*g, i, j);
     const int q = *cseq + s, cs = q & 1;
@@ -988,7 +1110,7 @@ struct ProCg1S {  // rings: 0 u_i, 1 w^_i, 2 s^_{i-1}; centre ring: x, p_{i-1}
         const int kin = kin0 + l;
         if (kin >= sg.k0 && kin < sg.k1) {
           const int e = l * D::PLANE + (ty + P) * D::RX + tx + P;
-          const int c = (l * kKronTY + ty) * kKronTX + tx;
+          const int c = (l * Sh::TY + ty) * Sh::TX + tx;
           const size_t f = (static_cast<size_t>(kin) * ny + j) * nx + i;
           const double uo = u_[e], pold = cr->buf[1][cs][c];
           const double pnew = fma(beta, pold, uo);                 // p_i = u_i + beta p_{i-1}
@@ -1009,7 +1131,7 @@ struct ProCg1S {  // rings: 0 u_i, 1 w^_i, 2 s^_{i-1}; centre ring: x, p_{i-1}
         }
       }
     }
-    for (int e = ty * kKronTX + tx; e < N; e += kThreads)  // u_{i+1}, halo included
+    for (int e = threadIdx.y * kKronTX + threadIdx.x; e < N; e += kThreads)  // u_{i+1}, halo included
       (&sm.v[0][0])[e] = fma(-alpha, fma(beta, s_[e], w_[e]), u_[e]);
   }
 };
@@ -1210,10 +1332,10 @@ __global__ void __launch_bounds__(kThreads, K2_MINB)
   // r0 = b - A x0 (sparse.cpp:61-69), u0 = D^-1 r0; r.r, b.b, r.u
   {
     EpiCg1InitS<P> e0{rhs, w.r[0], w.s[0], w.p, &g, a, b, {{}, zb, g.n[2]}, -1, -1, {0, 0, 0, 0}};
-    Inputs<1> in1{{x}, {&maps.x}};
+    Inputs<1> in1{{x}, {&maps.x}, {&maps.sx}};
     ProCopy<P, PL> pcp{&g, nx, ny, {{}, zb, g.n[2]}};
     for_segments(T, gridDim.x, blockIdx.x, [&](const Seg& sg) {
-      kron_tile<P, PL, 1, 1, true>(g, c, in1, pcp, sg, sm, zb, seq, e0);
+      kron_seg<P, PL, 1, 1, true>(g, c, in1, pcp, sg, sm, zb, seq, e0);
     });
     grid_reduce(grid, e0.acc, w.partials, buf, red, tot);
   }
@@ -1236,9 +1358,9 @@ __global__ void __launch_bounds__(kThreads, K2_MINB)
   {
     ProCopy<P, PL> pcp{&g, nx, ny, {{}, zb, g.n[2]}};
     EpiCg1S<P, ProCopy<P, PL>> e1{w.w[0], &pcp, a, b, 0.0};
-    Inputs<1> in1{{w.r[0]}, {&maps.r[0]}};
+    Inputs<1> in1{{w.r[0]}, {&maps.r[0]}, {&maps.sr[0]}};
     for_segments(T, gridDim.x, blockIdx.x, [&](const Seg& sg) {
-      kron_tile<P, PL, 1, 1, true>(g, c, in1, pcp, sg, sm, zb, seq, e1);
+      kron_seg<P, PL, 1, 1, true>(g, c, in1, pcp, sg, sm, zb, seq, e1);
     });
     const double acc[4] = {e1.delta, 0.0, 0.0, 0.0};
     grid_reduce(grid, acc, w.partials, buf, red, tot);
@@ -1253,7 +1375,9 @@ __global__ void __launch_bounds__(kThreads, K2_MINB)
   Seg seg0{};
   const bool has_seg = first_segment(T, gridDim.x, blockIdx.x, seg0);
   auto inputs = [&](int k) {
-    return Inputs<NIN>{{w.r[k], w.w[k], w.s[k]}, {&maps.r[k], &maps.w[k], &maps.s[k]}};
+    return Inputs<NIN>{{w.r[k], w.w[k], w.s[k]},
+                       {&maps.r[k], &maps.w[k], &maps.s[k]},
+                       {&maps.sr[k], &maps.sw[k], &maps.ss[k]}};
   };
   bool primed = false;
   while (it < max_iter) {
@@ -1262,6 +1386,8 @@ __global__ void __launch_bounds__(kThreads, K2_MINB)
     // x is read and written every second sweep only (80 -> 72 B/DOF/iteration)
     pc.xmode = K2_DEFER_X ? ((it & 1) ? 2 : 1) : 0;
     pc.alpha_prev = alpha_prev;
+    pc.smx = &maps.sxc;
+    pc.smp = &maps.spc;
     EpiCg1S<P, ProCg1S<P, PL>> e{w.w[cur ^ 1], &pc, a, b, 0.0};
     const Inputs<NIN> in = inputs(cur);
 #if K2_STUDY_NOSWEEP  // latency study only (tools/k2_iter_time.py): barrier + reduction alone
@@ -1274,7 +1400,7 @@ __global__ void __launch_bounds__(kThreads, K2_MINB)
 #endif
     bool first = true;
     for_segments(T, gridDim.x, blockIdx.x, [&](const Seg& sg) {
-      kron_tile<P, PL, NIN, 1, true>(g, c, in, pc, sg, sm, zb, seq, e, first && primed);
+      kron_seg<P, PL, NIN, 1, true>(g, c, in, pc, sg, sm, zb, seq, e, first && primed);
       first = false;
     });
     const double acc[4] = {pc.gamma, e.delta, pc.rr, 0.0};
@@ -1533,13 +1659,16 @@ void allow_smem(K kernel, size_t bytes) {
 #define K2_MIN_PLANES 3  // config 2 per CG iteration: 2 -> 16.6 us, 3 -> 15.5, 4 -> 16.2, 6 -> 17.4
 #endif
 int seg_blocks(const TileIdx& T, int max_blocks) {
-  const long total = static_cast<long>(T.ntx) * T.nty * T.nz;
+  const long total = n_columns(T) * T.nz;  // column-planes
   return static_cast<int>(std::max(1L, std::min<long>(max_blocks, total / K2_MIN_PLANES)));
 }
 
 }  // namespace
 
-bool k2_make_map(const KronGrid& g, const double* base, TensorMap3* out, bool halo, int planes) {
+bool k2_strip_applies(const KronGrid& g) { return strip_applies(g); }
+
+bool k2_make_map(const KronGrid& g, const double* base, TensorMap3* out, bool halo, int planes,
+                 bool strip) {
   static_assert(sizeof(TensorMap3) == sizeof(CUtensorMap), "tensor map size");
   EncodeFn enc = encoder();
   const size_t pitch = static_cast<size_t>(g.n[0]) * sizeof(double);
@@ -1548,8 +1677,8 @@ bool k2_make_map(const KronGrid& g, const double* base, TensorMap3* out, bool ha
                               static_cast<cuuint64_t>(g.n[2])};
   const cuuint64_t strides[2] = {pitch, pitch * static_cast<cuuint64_t>(g.n[1])};
   const int h = halo ? 2 * g.p : 0;
-  const cuuint32_t box[3] = {static_cast<cuuint32_t>(kKronTX + h),
-                             static_cast<cuuint32_t>(kKronTY + h),
+  const int bx = strip ? StripTile::TX : kKronTX, by = strip ? StripTile::TY : kKronTY;
+  const cuuint32_t box[3] = {static_cast<cuuint32_t>(bx + h), static_cast<cuuint32_t>(by + h),
                              static_cast<cuuint32_t>(planes)};
   const cuuint32_t estr[3] = {1, 1, 1};
   CUtensorMap m;
@@ -1692,7 +1821,11 @@ int k2_cg1_max_blocks(int p, int sm_count, int nz, int pl) {
 void k2_cg1_solve(const KronGrid& g, double a, double b, const double* rhs, double* x,
                   const Cg1Work& w, const Cg1Maps& maps, double tol, int max_iter, int blocks,
                   cudaStream_t s, int pl) {
+#if K2_CG1_SCALED
+  const TileIdx T = maps.strip ? make_tiles_strip(g) : make_tiles(g);
+#else
   const TileIdx T = make_tiles(g);
+#endif
   const int nb = seg_blocks(T, blocks);
   dim3 grid(nb), block(kKronTX, kKronTY);
   KronGrid gg = g;

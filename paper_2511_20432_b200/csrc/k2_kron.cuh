@@ -35,8 +35,12 @@ struct alignas(64) TensorMap3 {
 // Encode the descriptor for `base` (a vector over g's grid). Returns false
 // when TMA cannot address the grid (row pitch not a multiple of 16 bytes);
 // the kernels then load planes with ordinary loads.
+// strip = true: the box of the transposed 8 x 32 strip tile (k2_kron.cu)
 bool k2_make_map(const KronGrid& g, const double* base, TensorMap3* out, bool halo = true,
-                 int planes = 2);
+                 int planes = 2, bool strip = false);
+// whether the single-sweep solve covers g's ragged last x columns with strip
+// tiles (it then needs the strip maps of Cg1Maps)
+bool k2_strip_applies(const KronGrid& g);
 
 // y = Op(a1, b1) v1 + Op(a2, b2) v2 with Op(a, b) = a (Mz x My x Mx) +
 //     b (Mz x My x Kx + Mz x Ky x Mx + Kz x My x Mx); v2 may be null.
@@ -100,6 +104,9 @@ struct Cg1Work {
 struct Cg1Maps {
   TensorMap3 x, inv_diag, r[2], w[2], s[2];
   TensorMap3 xc, pc;  // un-halo'd boxes of x and p (point-local inputs)
+  // the same boxes for the strip tiles (valid when strip != 0)
+  TensorMap3 sx, sr[2], sw[2], ss[2], sxc, spc;
+  int strip;
 };
 
 void k2_theta_rhs(const KronGrid& full, double a_b, double b_b, double a_a, double b_a,

@@ -680,6 +680,22 @@ void Sim::setup_device(int device, int preconditioner) {
                 k2_make_map(gfree, d_s2.p, &m.s[1], true, L) &&
                 k2_make_map(gfree, d_x.p, &m.xc, false, L) &&
                 k2_make_map(gfree, d_p.p, &m.pc, false, L);
+      // strip tiles over the ragged last x columns of grids that fill the GPU
+      // (2 planes per step; on latency-bound small grids the slower strip CTA
+      // sets the iteration time: config 2 16.4 -> 17.2 us per iteration with
+      // strips). TG_K2_NO_STRIP: main tiles only; TG_K2_STRIP=1 forces them.
+      const bool want_strip = std::getenv("TG_K2_STRIP") ? true : L == 2;
+      m.strip = use_cg1 && want_strip && k2_strip_applies(gfree) &&
+                !std::getenv("TG_K2_NO_STRIP") &&
+                k2_make_map(gfree, d_x.p, &m.sx, true, L, true) &&
+                k2_make_map(gfree, d_r.p, &m.sr[0], true, L, true) &&
+                k2_make_map(gfree, d_z.p, &m.sr[1], true, L, true) &&
+                k2_make_map(gfree, d_Ap.p, &m.sw[0], true, L, true) &&
+                k2_make_map(gfree, d_w2.p, &m.sw[1], true, L, true) &&
+                k2_make_map(gfree, d_p2.p, &m.ss[0], true, L, true) &&
+                k2_make_map(gfree, d_s2.p, &m.ss[1], true, L, true) &&
+                k2_make_map(gfree, d_x.p, &m.sxc, false, L, true) &&
+                k2_make_map(gfree, d_p.p, &m.spc, false, L, true);
       if (use_cg1) pcg_blocks = k2_cg1_max_blocks(p, ctx->sm_count, gfree.n[2], cg1_pl);
     }
     if (preconditioner == 1) {
