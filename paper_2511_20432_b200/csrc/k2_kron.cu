@@ -165,51 +165,47 @@ __device__ __forceinline__ Seg column_seg(const TileIdx& T, int col, int k0, int
 // The next segment of the unit range [u, e): the planes whose first unit lies
 // in it, within one column (false when none is left). Plane k of column c
 // starts at unit base(c) + k w(c), so the CTA ranges partition the planes.
-__device__ __forceinline__ bool next_segment(const TileIdx& T, long& u, long e, Seg& out) {
-  const long mtot = static_cast<long>(T.ntx) * T.nty * T.wm * T.nz;
-  const int ncol = static_cast<int>(n_columns(T));
+// 32-bit unit counts (< 2^31 for grids up to ~1e11 points): the loop state
+// stays small beside kron_tile's registers.
+__device__ __forceinline__ bool next_segment(const TileIdx& T, int& u, int e, Seg& out) {
+  const int nmain = T.ntx * T.nty;
+  const int mtot = nmain * T.wm * T.nz;
   while (u < e) {
-    int col, w;
-    long base;
-    if (u < mtot) {
-      w = T.wm;
-      col = static_cast<int>(u / (static_cast<long>(T.nz) * w));
-      base = static_cast<long>(col) * T.nz * w;
-    } else {
-      w = T.ws;
-      const int sc = static_cast<int>((u - mtot) / (static_cast<long>(T.nz) * w));
-      col = T.ntx * T.nty + sc;
-      base = mtot + static_cast<long>(sc) * T.nz * w;
-    }
-    if (col >= ncol) return false;
-    const long k0 = (u - base + w - 1) / w;
+    const bool main = u < mtot;
+    const int w = main ? T.wm : T.ws;
+    const int colu = T.nz * w;  // units per column
+    const int c = main ? u / colu : (u - mtot) / colu;
+    const int col = main ? c : nmain + c;
+    if (col >= nmain + T.nsy) return false;
+    const int base = main ? c * colu : mtot + c * colu;
+    const int k0 = (u - base + w - 1) / w;
     if (k0 >= T.nz) {  // no plane starts in the rest of this column
-      u = base + static_cast<long>(T.nz) * w;
+      u = base + colu;
       continue;
     }
     if (base + k0 * w >= e) return false;
-    const long k1 = min(static_cast<long>(T.nz), (e - base + w - 1) / w);
-    out = column_seg(T, col, static_cast<int>(k0), static_cast<int>(k1));
+    const int k1 = min(T.nz, (e - base + w - 1) / w);
+    out = column_seg(T, col, k0, k1);
     u = base + k1 * w;
     return true;
   }
   return false;
 }
+__device__ __forceinline__ int unit_bound(const TileIdx& T, int blocks, int b) {
+  return static_cast<int>(n_units(T) * b / blocks);
+}
 template <class F>
 __device__ __forceinline__ void for_segments(const TileIdx& T, int blocks, int b, F&& fn) {
-  const long total = n_units(T);
-  long u = total * b / blocks;
-  const long e = total * (b + 1) / blocks;
+  int u = unit_bound(T, blocks, b);
+  const int e = unit_bound(T, blocks, b + 1);
   Seg sg;
   while (next_segment(T, u, e, sg)) fn(sg);
 }
 
 // The first segment for_segments hands CTA b (false when its range is empty).
 __device__ __forceinline__ bool first_segment(const TileIdx& T, int blocks, int b, Seg& out) {
-  const long total = n_units(T);
-  long u = total * b / blocks;
-  const long e = total * (b + 1) / blocks;
-  return next_segment(T, u, e, out);
+  int u = unit_bound(T, blocks, b);
+  return next_segment(T, u, unit_bound(T, blocks, b + 1), out);
 }
 
 // Jacobi diagonal of Op(a, b) = a M + b K at (i, j, k) from the diagonals of

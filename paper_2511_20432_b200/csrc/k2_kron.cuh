@@ -132,6 +132,24 @@ int k2_cg1_max_blocks(int p, int sm_count, int nz, int pl);
 void k2_cg1_solve(const KronGrid& g, double a, double b, const double* rhs, double* x,
                   const Cg1Work& w, const Cg1Maps& maps, double tol, int max_iter, int blocks,
                   cudaStream_t s, int pl);
+// The same solve with the solver state resident in shared memory (small
+// grids, k2_resident.cu): one CTA per TX x TY x nz column block.
+struct K2ResPlan {
+  int TX, TY, ntx, nty;
+  size_t smem;  // dynamic shared memory per CTA
+};
+struct K2ResWork {
+  double* wx[2];     // w^ exchange buffers (free grid)
+  double* ux;        // u_0 exchange buffer (free grid)
+  double* partials;  // >= 8 * ntx * nty
+  PcgStatus* status;
+};
+// false when no tile shape fits one cooperative wave (or TG_K2_NO_RESIDENT)
+bool k2_res_plan(const KronGrid& g, int sm_count, int max_smem, K2ResPlan* out);
+void k2_res_solve(const KronGrid& g, double a, double b, const double* rhs, double* x,
+                  const K2ResWork& w, const K2ResPlan& pl, double tol, int max_iter,
+                  cudaStream_t s);
+
 // plain y = Op(a, b) v (tests / the operator alone)
 // v_map: TMA descriptor of v (k2_make_map) or null for plain loads
 void k2_apply(const KronGrid& g, double a, double b, const double* v, double* y, int sm_count,

@@ -697,6 +697,11 @@ void Sim::setup_device(int device, int preconditioner) {
                 k2_make_map(gfree, d_x.p, &m.sxc, false, L, true) &&
                 k2_make_map(gfree, d_p.p, &m.spc, false, L, true);
       if (use_cg1) pcg_blocks = k2_cg1_max_blocks(p, ctx->sm_count, gfree.n[2], cg1_pl);
+      // small grids: the solver state resident in shared memory (k2_resident.cu)
+      int max_smem = 0;
+      TG_CUDA(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin,
+                                     ctx->device));
+      use_res = use_cg1 && k2_res_plan(gfree, ctx->sm_count, max_smem, &res_plan);
     }
     if (preconditioner == 1) {
       // V_d, lambda_d per direction on the free grid (host/fdm.cpp)
@@ -1746,6 +1751,11 @@ void Sim::theta_step_launch(double tol, int max_iter) {
     } else if (slab) {  // z-slabs (multi-GPU, or the local test bed)
       ctx->timer.timed(2, s, [&] {
         slab->solve(d_rhs.p, d_x.p, coefA[0], coefA[1], tol, max_iter, d_status.p, s);
+      });
+    } else if (use_res) {
+      const K2ResWork w{{d_Ap.p, d_w2.p}, d_r.p, d_partials.p, d_status.p};
+      ctx->timer.timed(2, s, [&] {
+        k2_res_solve(gfree, coefA[0], coefA[1], d_rhs.p, d_x.p, w, res_plan, tol, max_iter, s);
       });
     } else if (use_cg1) {
       const Cg1Work w{d_p.p,    {d_r.p, d_z.p}, {d_Ap.p, d_w2.p}, {d_p2.p, d_s2.p},

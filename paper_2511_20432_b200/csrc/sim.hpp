@@ -170,6 +170,8 @@ class Sim {
   // free grid; TG_K2_ALGO=pcg selects the two-phase kernel
   int cg1_pl = 2;  // planes per sweep step of the single-sweep solver
   bool use_cg1 = false;
+  bool use_res = false;  // small grids: k2_res_solve (state resident in shared memory)
+  K2ResPlan res_plan{};
   // fast-diagonalization preconditioner (k2_fdm.cuh), opt-in
   bool use_fdm = false;
   FdmDev fdm{};

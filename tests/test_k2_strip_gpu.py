@@ -10,6 +10,9 @@ dot products changes. Checked here:
     <= 1e-10; solver_tol 1e-12 on both sides);
   * against the main-tile-only sweep (TG_K2_NO_STRIP) at config-4 size: the
     same iteration counts and free coefficients within rounding.
+The small-grid resident solve (csrc/k2_resident.cu) is checked the same way
+against the streaming kernel; the reference-loop parity of small configs
+(tests/test_sim_gpu.py) runs through it by default.
 """
 import os
 import re
@@ -60,13 +63,18 @@ def test_strip_grid_against_live_reference(xi, ref, tmp_path):
     r.close()
 
 
-def _run(cfg, steps, strip):
-    key = "TG_K2_STRIP" if strip else "TG_K2_NO_STRIP"  # (config 2 only with the forcing key)
-    os.environ[key] = "1"
+def _run(cfg, steps, strip, resident=False):
+    """Steps with the streaming single-sweep solve (strip tiles on / off) or,
+    resident=True, the shared-memory resident solve (k2_resident.cu)."""
+    keys = [] if resident else ["TG_K2_NO_RESIDENT",
+                                "TG_K2_STRIP" if strip else "TG_K2_NO_STRIP"]
+    for k in keys:
+        os.environ[k] = "1"
     try:
         s = tg.Simulation(cfg, solver_tol=1e-12)
     finally:
-        os.environ.pop(key, None)
+        for k in keys:
+            os.environ.pop(k, None)
     s.reset()
     its = [s.advance(1)[0] for _ in range(steps)]
     x = s.state()["free"]
@@ -85,3 +93,15 @@ def test_strip_matches_main_tiles_full_size(name):
     # the dot products group differently per CTA with strips, so bit-equal
     # states would mean the strip path never ran
     assert not np.array_equal(x_s, x_m)
+
+
+@pytest.mark.parametrize("name", ["cfg2_raster_layer", "cfg0_single_track"])
+def test_resident_solve_matches_streaming(name):
+    """The shared-memory resident solve (the default on grids that fit one
+    cooperative wave) against the streaming single-sweep kernel: the same
+    Krylov iterates up to the per-CTA grouping of the dot products."""
+    cfg = os.path.join(ROOT, "configs", name + ".cfg")
+    its_r, x_r = _run(cfg, 5, False, resident=True)
+    its_m, x_m = _run(cfg, 5, False)
+    assert all(abs(a - b) <= 1 for a, b in zip(its_r, its_m)), (its_r, its_m)
+    assert normwise(x_r, x_m) <= 1e-11, normwise(x_r, x_m)
