@@ -324,7 +324,13 @@ def config2_run(with_cpu):
            "steps": n, "run_s": wall, "ms_per_step": wall * 1e3 / n,
            "theta_step_total_ms_per_step": prof["theta_step_ms"] / n,
            "theta_step_total_ms_per_mdof": prof["theta_step_ms"] / n / (dofs / 1e6),
-           "cg_iterations_per_step": iters / n, "timing": "wall clock around the "
+           "cg_iterations_per_step": iters / n,
+           "solve_ms_per_step": prof["k2_ms"] / n,
+           "us_per_cg_iteration": 1e3 * prof["k2_ms"] / max(1, iters),
+           "solver": "k2_res_kernel: single-sweep Jacobi-PCG with u, s, w (block + halo), x, p "
+                     "and D resident in shared memory, one CTA per 6x6x17 column block, w's "
+                     "halo through L2 (csrc/k2_resident.cu)",
+           "timing": "wall clock around the "
            "synchronous tg_sim_advance(n) call (device-resident state)"}
     k = n // 2
     if with_cpu:

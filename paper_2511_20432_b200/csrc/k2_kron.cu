@@ -127,6 +127,11 @@ struct TileIdx {
   int nsy = 0;  // strip tiles along y (0: no strip)
   int xs = 0;   // first column of the strip
   int wm = 1, ws = 1;
+  // column-aligned split (grid = ntx * nty + 2 nsy CTAs): CTA b < ntx * nty
+  // sweeps main column b whole, the others half a strip column each, so all
+  // CTAs march through z together and a tile's x/y halo rows were just
+  // fetched by its neighbours (L2 hits instead of DRAM re-reads)
+  int aligned = 0;
 };
 struct Seg {
   int x0, y0, k0, k1;
@@ -194,8 +199,18 @@ __device__ __forceinline__ bool next_segment(const TileIdx& T, int& u, int e, Se
 __device__ __forceinline__ int unit_bound(const TileIdx& T, int blocks, int b) {
   return static_cast<int>(n_units(T) * b / blocks);
 }
+__device__ __forceinline__ Seg aligned_seg(const TileIdx& T, int b) {
+  const int nmain = T.ntx * T.nty;
+  if (b < nmain) return column_seg(T, b, 0, T.nz);
+  const int sc = (b - nmain) >> 1, h = (b - nmain) & 1, mid = T.nz / 2;
+  return column_seg(T, nmain + sc, h ? mid : 0, h ? T.nz : mid);
+}
 template <class F>
 __device__ __forceinline__ void for_segments(const TileIdx& T, int blocks, int b, F&& fn) {
+  if (T.aligned) {
+    fn(aligned_seg(T, b));
+    return;
+  }
   int u = unit_bound(T, blocks, b);
   const int e = unit_bound(T, blocks, b + 1);
   Seg sg;
@@ -204,6 +219,10 @@ __device__ __forceinline__ void for_segments(const TileIdx& T, int blocks, int b
 
 // The first segment for_segments hands CTA b (false when its range is empty).
 __device__ __forceinline__ bool first_segment(const TileIdx& T, int blocks, int b, Seg& out) {
+  if (T.aligned) {
+    out = aligned_seg(T, b);
+    return true;
+  }
   int u = unit_bound(T, blocks, b);
   return next_segment(T, u, unit_bound(T, blocks, b + 1), out);
 }
@@ -1818,11 +1837,26 @@ void k2_cg1_solve(const KronGrid& g, double a, double b, const double* rhs, doub
                   const Cg1Work& w, const Cg1Maps& maps, double tol, int max_iter, int blocks,
                   cudaStream_t s, int pl) {
 #if K2_CG1_SCALED
-  const TileIdx T = maps.strip ? make_tiles_strip(g) : make_tiles(g);
+  TileIdx T = maps.strip ? make_tiles_strip(g) : make_tiles(g);
 #else
-  const TileIdx T = make_tiles(g);
+  TileIdx T = make_tiles(g);
 #endif
-  const int nb = seg_blocks(T, blocks);
+  int nb = seg_blocks(T, blocks);
+  // the column-aligned split when every column (strip columns in halves) gets
+  // its own CTA of one wave and the columns are deep enough to amortize the
+  // 2P halo planes of a whole-column segment (TG_K2_ALIGNED=0/1 forces).
+  // Config 4: 85.5 against 89.8 us/iteration, DRAM reads 19.3 -> 13.6 GB per
+  // solve (the unit split drifted the CTAs' z positions apart, so y-neighbour
+  // tiles missed each other's halo rows in L2)
+  {
+    const int need = T.ntx * T.nty + 2 * T.nsy;
+    bool al = need <= blocks && T.nz >= 32;  // config 4: 264 + 2 x 9 = 282 CTAs
+    if (const char* e = std::getenv("TG_K2_ALIGNED")) al = std::atoi(e) != 0 && need <= blocks;
+    if (al) {
+      T.aligned = 1;
+      nb = need;
+    }
+  }
   dim3 grid(nb), block(kKronTX, kKronTY);
   KronGrid gg = g;
   Cg1Work ww = w;
