@@ -247,20 +247,27 @@ def config3_steps(with_cpu, steps=10):
             n, nnz = len(rp) - 1, len(v)
             peak, src = hbm_peak()
             us_it = 1e3 * prof["k2_ms"] / max(1, iters)
-            # per CG iteration: A_ff once (8 B value + 4 B column per entry) and the
-            # vectors p (r), Ap (w, r), x (r, w), r (r, w), D^-1 (r, twice), p (r, w)
-            alg_bytes = 12.0 * nnz + 8.0 * n * 11
+            # per CG iteration: A_ff once and the vectors p (r), Ap (w, r), x (r, w),
+            # r (r, w), D^-1 (r, twice), p (r, w). A_ff is read in the implicit-column
+            # layout (csr_make_dia): (2p+1)^3 slots of 8 B per row in 32-row slices,
+            # zeros where a boundary row has no such column
+            W3 = 7 ** 3
+            slots = ((n + 31) // 32) * 32 * W3
+            alg_bytes = 8.0 * slots + 8.0 * n * 11
             achieved = alg_bytes / (us_it * 1e-6) / 1e9
             res.update({"us_per_cg_iteration": us_it, "nnz": nnz,
-                        "operator": "assembled A_ff in sliced ELL (32-row slices), one thread "
-                                    "per row, row sums in the reference's CSR order (bit-exact "
-                                    "rows)",
-                        "roofline": {"kernel": "csr_pcg_kernel<DevSell>", "bound": "hbm",
+                        "operator": "assembled A_ff with implicit columns (DIA over the free "
+                                    "box: 343 offsets per row, 32-row slices), one thread per "
+                                    "row, row sums in the reference's CSR order (bit-exact "
+                                    "rows, equal to the sliced-ELL copy bit for bit)",
+                        "roofline": {"kernel": "csr_pcg_kernel<DevDia>", "bound": "hbm",
                                      "achieved": achieved, "peak": peak, "unit": "GB/s",
                                      "frac": achieved / peak, "peak_source": src,
                                      "bytes_per_iteration": alg_bytes,
-                                     "bytes_note": "12 B per A_ff entry + 11 vector streams of "
-                                                   "8 B/DOF"}})
+                                     "bytes_note": "8 B per stencil slot (343 per row) + 11 "
+                                                   "vector streams of 8 B/DOF; the CSR form "
+                                                   "would move 12 B per nonzero",
+                                     "csr_bytes_per_iteration": 12.0 * nnz + 8.0 * n * 11}})
         else:
             res["preconditioner"] = ("S^-1 A~^-1 S^-1: A~ the separable approximation "
                                      "(mean control-net arc length per axis), inverted by fast "

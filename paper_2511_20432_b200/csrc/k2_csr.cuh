@@ -27,6 +27,19 @@ struct DevSell {
   const double* val;
 };
 
+// The same rows with implicit columns, for operators on a structured free
+// grid (a single patch whose constrained layer is a boundary plane, so the
+// free rows are an nx x ny x nz box in flat order): row r couples to
+// r + (dk nz-plane + dj nx + di), |di|, |dj|, |dk| <= p, and entry o of the
+// (2p+1)^3 offsets, ascending = the CSR's ascending columns, sits at
+// val[(slice * noff + o) * 32 + lane] (zero where the CSR row has no such
+// column). 8 instead of 12 bytes per stored entry (SELL: value + column).
+struct DevDia {
+  int rows;
+  int nx, nxy, p, noff;
+  const double* val;
+};
+
 // Work vectors of an assembled-operator solve (stored Jacobi diagonal).
 struct CsrWork {
   double* r;
@@ -47,6 +60,14 @@ void csr_pcg_solve(const DevCsr& A, const double* rhs, double* x, const CsrWork&
                    int max_iter, int blocks, cudaStream_t s);
 void csr_pcg_solve(const DevSell& A, const double* rhs, double* x, const CsrWork& w, double tol,
                    int max_iter, int blocks, cudaStream_t s);
+// DIA copy of a SELL operator on the free box (nx, ny, nz); false (nothing
+// written) when some entry lies outside the (2p+1)^3 stencil. val must hold
+// ceil(rows / 32) * 32 * (2p+1)^3 doubles.
+bool csr_make_dia(const DevSell& A, int nx, int ny, int nz, int p, double* val, int* d_flag,
+                  DevDia* out, cudaStream_t s);
+void csr_pcg_solve(const DevDia& A, const double* rhs, double* x, const CsrWork& w, double tol,
+                   int max_iter, int blocks, cudaStream_t s);
+void csr_apply(const DevDia& A, const double* x, double* y, cudaStream_t s);
 void csr_apply(const DevCsr& A, const double* x, double* y, cudaStream_t s);
 void csr_apply(const DevSell& A, const double* x, double* y, cudaStream_t s);
 

@@ -758,6 +758,20 @@ void Sim::setup_device(int device, int preconditioner) {
       csrB = Csr{};
     }
     upload(d_free_list, dofs.free_list, s);
+    {  // the implicit-column copy of A_ff: free rows = the grid minus the bottom layer
+      const auto dg = vol.degrees();
+      int fb[3] = {geom.n[0], geom.n[1], geom.n[2]};
+      fb[geom.ax] -= 1;
+      use_dia = false;
+      if (!std::getenv("TG_K2_NO_DIA") && dg[0] == dg[1] && dg[1] == dg[2] &&
+          static_cast<long>(fb[0]) * fb[1] * fb[2] == n_free) {
+        const int W = 2 * dg[0] + 1;
+        d_dia.ensure(static_cast<size_t>((n_free + 31) / 32) * 32 * W * W * W);
+        d_dia_flag.ensure(1);
+        use_dia = csr_make_dia(devA, fb[0], fb[1], fb[2], dg[0], d_dia.p, d_dia_flag.p, &devAd, s);
+        if (!use_dia) d_dia.release();
+      }
+    }
     csr_inverse_diagonal(devA, d_invd.p, d_status.p, s);
     pcg_blocks = csr_pcg_max_blocks(ctx->sm_count);
     if (preconditioner == 1) setup_general_fdm(s);
@@ -1779,14 +1793,18 @@ void Sim::theta_step_launch(double tol, int max_iter) {
     if (use_fdm) {  // the scaled separable-approximation preconditioner
       const FdmWork w{d_r.p, d_z.p, d_p.p, d_Ap.p, d_p2.p, d_w2.p, d_partials.p, d_dots.p, h_dots};
       ctx->timer.timed(2, s, [&] {
-        *h_status = pcg_precond_solve([&](const double* v, double* y) { csr_apply(devA, v, y, s); },
+        *h_status = pcg_precond_solve([&](const double* v, double* y) {
+          if (use_dia) csr_apply(devAd, v, y, s); else csr_apply(devA, v, y, s); },
                                       fdm, n_free, d_rhs.p, d_x.p, w, tol, max_iter, s);
       });
       TG_CUDA(cudaMemcpyAsync(d_status.p, h_status, sizeof(PcgStatus), cudaMemcpyHostToDevice, s));
     } else {
       const CsrWork w{d_r.p, d_p.p, d_Ap.p, d_invd.p, d_partials.p, d_status.p};
       ctx->timer.timed(2, s, [&] {
-        csr_pcg_solve(devA, d_rhs.p, d_x.p, w, tol, max_iter, pcg_blocks, s);
+        if (use_dia)
+          csr_pcg_solve(devAd, d_rhs.p, d_x.p, w, tol, max_iter, pcg_blocks, s);
+        else
+          csr_pcg_solve(devA, d_rhs.p, d_x.p, w, tol, max_iter, pcg_blocks, s);
       });
     }
   }

@@ -162,6 +162,12 @@ class Sim {
   };
   SellBufs sA, sAc, sB;
   DevSell devA{}, devAc{}, devB{};
+  // A_ff with implicit columns on the free box (k2_csr.cuh DevDia): the solve's
+  // operator when every entry lies in the (2p+1)^3 stencil (TG_K2_NO_DIA: SELL)
+  DevDia devAd{};
+  bool use_dia = false;
+  DevBuf<double> d_dia;
+  DevBuf<int> d_dia_flag;
   KronGrid gfull{}, gfree{};
   DevBuf<double> d_x, d_r, d_z, d_p, d_p2, d_Ap, d_invd, d_rhs, d_gn, d_g1, d_Fn, d_F1, d_T, d_gfull,
       d_partials;
