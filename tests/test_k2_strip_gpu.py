@@ -107,6 +107,24 @@ def test_resident_solve_matches_streaming(name):
     assert normwise(x_r, x_m) <= 1e-11, normwise(x_r, x_m)
 
 
+@pytest.mark.parametrize("xi,zeta", [(38, 6), (128, 8)], ids=["tb4", "tb12"])
+def test_resident_block_shapes_match_streaming(xi, zeta, tmp_path):
+    """The resident solve's other block edges (4 x 4 on a 40 x 40 free grid,
+    12 x 12 with ragged edge blocks on 130 x 130) against the streaming
+    kernel on the same steps."""
+    txt = open(os.path.join(ROOT, "configs", "cfg0_parity.cfg")).read()
+    txt = re.sub(r"^xi_elements = \d+", f"xi_elements = {xi}", txt, flags=re.M)
+    txt = re.sub(r"^eta_elements = \d+", f"eta_elements = {xi}", txt, flags=re.M)
+    txt = re.sub(r"^zeta_elements = \d+", f"zeta_elements = {zeta}", txt, flags=re.M)
+    p = tmp_path / f"res{xi}.cfg"
+    p.write_text(txt)
+    its_r, x_r = _run(str(p), 4, False, resident=True)
+    its_m, x_m = _run(str(p), 4, False)
+    assert all(abs(a - b) <= 1 for a, b in zip(its_r, its_m)), (its_r, its_m)
+    assert normwise(x_r, x_m) <= 1e-11, normwise(x_r, x_m)
+    assert not np.array_equal(x_r, x_m)  # (the resident path ran: other dot grouping)
+
+
 @pytest.mark.parametrize("name", ["cfg3_parity", "qc_small"])
 def test_dia_operator_bitwise_equals_sell(name):
     """Non-separable patches: A_ff with implicit columns (DevDia, k2_csr.cu)
