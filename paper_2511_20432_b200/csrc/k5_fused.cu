@@ -321,13 +321,6 @@ __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.wait_all;" ::: "memory");
 }
 
-#ifndef K5_INTERLEAVE
-#define K5_INTERLEAVE 0
-#endif
-#ifndef K5_IL_PARTS
-#define K5_IL_PARTS 8  // generation slices per stage (1, 2, 4 or 8)
-#endif
-static_assert(kSfKS == 32, "gen_part splits a stage's generation over its 8 k-steps");
 constexpr int kLd = kSfKS + 4;  // row pitch (doubles) of the A / B stages: conflict-free frags
 constexpr int kWarps = kSfWarps;
 constexpr int kWR = kSfWR;
@@ -452,49 +445,6 @@ __global__ void __launch_bounds__(kSfThreads, kSfMinBlocks)
         }
       }
     };
-    // one eighth of generate(buf): A row r = part and B rows part, part + 8 of
-    // this warp, the stage constants re-read from shared memory (no registers
-    // held across the MMAs it is interleaved with)
-    auto gen_part = [&](int buf, int part) {
-      constexpr int NP = K5_IL_PARTS;
-      constexpr int RA = (kSfTA + kWarps - 1) / kWarps, RB = (kSfTB + kWarps - 1) / kWarps;
-      const double nisp = sm.cs[buf][2][lane];
-#pragma unroll
-      for (int r = part; r < RA; r += NP) {
-        const int a = warp + kWarps * r;
-        if (kSfTA % kWarps == 0 || a < kSfTA) {
-          const double d = sm.U[a] - sm.cs[buf][0][lane];
-          sm.A[buf][a][lane] = sf_exp(d * d, nisp, sm.cs[buf][3][lane], sm.cs[buf][4][lane],
-                                      sm.cs[buf][5][lane], sm.cs[buf][6][lane],
-                                      sm.cs[buf][7][lane], sm.tab);
-        }
-      }
-#pragma unroll
-      for (int r = part; r < RB; r += NP) {
-        const int b = warp + kWarps * r;
-        if (kSfTB % kWarps == 0 || b < kSfTB) {
-          double x;
-          if (G.vplane) {
-            x = sm.V[b];
-          } else {
-            const double d = sm.V[b] - sm.cs[buf][1][lane];
-            x = d * d;
-          }
-          sm.B[buf][b][lane] = sf_exp(x, nisp, kExpMagic, kSfE0, kSfE1, kSfE2, kSfE3, sm.tab);
-        }
-      }
-    };
-    auto contract_k = [&](int buf, int kk) {
-      double af[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) af[i] = sm.A[buf][32 * wa + 8 * i + g8][kk + q4];
-#pragma unroll
-      for (int jn = 0; jn < kNT; ++jn) {
-        const double bf = sm.B[buf][kWN * wb + 8 * jn + g8][kk + q4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) dmma884(acc[i][jn][0], acc[i][jn][1], af[i], bf);
-      }
-    };
     auto contract = [&](int buf) {
 #pragma unroll
       for (int kk = 0; kk < kSfKS; kk += 4) {
@@ -525,26 +475,8 @@ __global__ void __launch_bounds__(kSfThreads, kSfMinBlocks)
       for (int st = 0; st < n_stage; ++st) {
         const int buf = st & 1;
         if (st + 2 < n_stage) load_cst(st + 2, buf);
-#if K5_INTERLEAVE
-        // stage st + 1's exponentials interleaved with stage st's MMAs: the
-        // generator's non-FP64 work (table loads, integer ops, stores) issues
-        // while the DMMAs occupy the FP64 pipe
-        const bool gen = st + 1 < n_stage;
-        if (active) {
-#pragma unroll
-          for (int kk = 0; kk < kSfKS; kk += 4) {
-            contract_k(buf, kk);
-            constexpr int every = 8 / K5_IL_PARTS;
-            if (gen && (kk / 4) % every == every - 1) gen_part(buf ^ 1, (kk / 4) / every);
-          }
-        } else if (gen) {
-#pragma unroll
-          for (int part = 0; part < K5_IL_PARTS; ++part) gen_part(buf ^ 1, part);
-        }
-#else
         if (st + 1 < n_stage) generate(buf ^ 1);
         if (active) contract(buf);
-#endif
         cp_async_wait_all();
         __syncthreads();
       }
