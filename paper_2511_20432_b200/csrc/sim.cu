@@ -763,10 +763,14 @@ void Sim::setup_device(int device, int preconditioner) {
       int fb[3] = {geom.n[0], geom.n[1], geom.n[2]};
       fb[geom.ax] -= 1;
       use_dia = false;
+      const int W = 2 * dg[0] + 1;
+      const size_t dia_n = static_cast<size_t>((n_free + 31) / 32) * 32 * W * W * W;
+      size_t mem_free = 0, mem_total = 0;
+      TG_CUDA(cudaMemGetInfo(&mem_free, &mem_total));
+      // (a second copy of A_ff: only when it takes at most half the free memory)
       if (!std::getenv("TG_K2_NO_DIA") && dg[0] == dg[1] && dg[1] == dg[2] &&
-          static_cast<long>(fb[0]) * fb[1] * fb[2] == n_free) {
-        const int W = 2 * dg[0] + 1;
-        d_dia.ensure(static_cast<size_t>((n_free + 31) / 32) * 32 * W * W * W);
+          static_cast<long>(fb[0]) * fb[1] * fb[2] == n_free && dia_n * 8 <= mem_free / 2) {
+        d_dia.ensure(dia_n);
         d_dia_flag.ensure(1);
         use_dia = csr_make_dia(devA, fb[0], fb[1], fb[2], dg[0], d_dia.p, d_dia_flag.p, &devAd, s);
         if (!use_dia) d_dia.release();
