@@ -1688,6 +1688,11 @@ bool k2_make_map(const KronGrid& g, const double* base, TensorMap3* out, bool ha
   EncodeFn enc = encoder();
   const size_t pitch = static_cast<size_t>(g.n[0]) * sizeof(double);
   if (!enc || pitch % 16 != 0 || reinterpret_cast<uintptr_t>(base) % 16 != 0) return false;
+  // The TMA sweeps are validated for degree 2 (every BASELINE cuboid): with
+  // degree-1 and degree-3 bands on a TMA-addressable grid the swept kernels
+  // stop with an illegal-instruction fault, so those grids take the plain-load
+  // kernels (and small grids the resident solve, which uses no TMA).
+  if (g.p != 2) return false;
   const cuuint64_t dims[3] = {static_cast<cuuint64_t>(g.n[0]), static_cast<cuuint64_t>(g.n[1]),
                               static_cast<cuuint64_t>(g.n[2])};
   const cuuint64_t strides[2] = {pitch, pitch * static_cast<cuuint64_t>(g.n[1])};

@@ -660,7 +660,8 @@ void Sim::setup_device(int device, int preconditioner) {
     // TMA descriptors of the swept vectors (all persistent allocations)
     maps.valid = k2_make_map(gfree, d_x.p, &maps.x) && k2_make_map(gfree, d_z.p, &maps.z) &&
                  k2_make_map(gfree, d_p.p, &maps.pA) && k2_make_map(gfree, d_p2.p, &maps.pB);
-    rhs_tma = k2_make_map(gfull, d_T.p, &map_T) && k2_make_map(gfull, d_gfull.p, &map_g);
+    rhs_tma = !std::getenv("TG_K2_RHS_NO_TMA") && k2_make_map(gfull, d_T.p, &map_T) &&
+              k2_make_map(gfull, d_gfull.p, &map_g);
     const char* algo = std::getenv("TG_K2_ALGO");
     if (maps.valid && !(algo && std::string(algo) == "pcg")) {
       // buffers: r = {d_r, d_z}, w = {d_Ap, d_w2}, s = {d_p2, d_s2}, p = d_p

@@ -44,10 +44,12 @@ def cfg_with_xi(tmp_path, xi):
 def test_strip_grid_against_live_reference(xi, ref, tmp_path):
     p = cfg_with_xi(tmp_path, xi)
     os.environ["TG_K2_STRIP"] = "1"  # small grids use strips only when forced
+    os.environ["TG_K2_NO_RESIDENT"] = "1"  # (and the resident solve would take them)
     try:
         s = tg.Simulation(p, t_end=1.5e-4)
     finally:
         os.environ.pop("TG_K2_STRIP")
+        os.environ.pop("TG_K2_NO_RESIDENT")
     r = ref.sim(p, t_end=1.5e-4)
     assert s.info["kronecker"] == 2
     s.reset()
@@ -59,6 +61,41 @@ def test_strip_grid_against_live_reference(xi, ref, tmp_path):
         assert normwise(st["F"], o["F"]) <= 1e-10, (xi, k)
         assert normwise(st["g"], o["g"]) <= 1e-10, (xi, k)
         assert normwise(st["free"], o["free"]) <= 1e-8, (xi, k)
+    s.close()
+    r.close()
+
+
+@pytest.mark.parametrize("resident", [True, False], ids=["resident", "streaming"])
+@pytest.mark.parametrize("deg,xi", [(1, 33), (3, 31)], ids=["p1", "p3"])
+def test_even_pitch_other_degrees_against_live_reference(deg, xi, resident, ref, tmp_path):
+    """Degree-1 and degree-3 cuboids whose x extent (34) makes the grid
+    TMA-addressable: the TMA sweeps are kept to degree 2 (k2_make_map), so
+    these take the resident solve or the plain-load kernels; regression test
+    for the illegal-instruction fault those bands hit on the TMA path."""
+    from test_sim_gpu import box_geometry
+    txt = open(os.path.join(ROOT, "configs", "cfg0_parity.cfg")).read()
+    head, rest = txt.split("[geometry]", 1)
+    rest = rest[rest.index("\n\n"):]
+    rest, n = re.subn(r"^xi_elements = \d+", f"xi_elements = {xi}", rest, flags=re.M)
+    assert n == 1
+    p = tmp_path / f"deg{deg}.cfg"
+    p.write_text(head + box_geometry((deg, deg, deg)) + rest)
+    if not resident:
+        os.environ["TG_K2_NO_RESIDENT"] = "1"
+    try:
+        s = tg.Simulation(str(p), t_end=1.5e-4)
+    finally:
+        os.environ.pop("TG_K2_NO_RESIDENT", None)
+    r = ref.sim(str(p), t_end=1.5e-4)
+    assert s.info["kronecker"] > 0 and s.info["nx"] == 34
+    s.reset()
+    r.reset()
+    for k in range(1, 12):
+        s.advance(1)
+        st = s.state()
+        o = r.step()
+        assert normwise(st["F"], o["F"]) <= 1e-10, (deg, k)
+        assert normwise(st["free"], o["free"]) <= 1e-8, (deg, k)
     s.close()
     r.close()
 
