@@ -124,4 +124,49 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
   return v;
 }
 
+// Warp-wide sum of the per-CTA partials pb[b*4 + c] (b < nb, c = 0..3), in
+// the order of the loop it replaces — per lane s = 0 + pb[lane] + pb[lane+32]
+// + ..., then a shuffle tree — so the sums are bit-identical to it. Every
+// load of the first 32*K CTAs is issued (two 16-byte L2 reads per CTA, past
+// L1) before the first add: one L2 round trip instead of one per component
+// and per stride. Result valid in lane 0.
+template <int K = 5>
+__device__ __forceinline__ void warp_sum_partials(const double* pb, int nb, int lane,
+                                                  double (&s)[4]) {
+  double2 v[K][2];
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    const int b = lane + 32 * k;
+    if (b < nb) {
+      v[k][0] = __ldcg(reinterpret_cast<const double2*>(pb + 4 * static_cast<size_t>(b)));
+      v[k][1] = __ldcg(reinterpret_cast<const double2*>(pb + 4 * static_cast<size_t>(b) + 2));
+    } else {  // + 0.0 leaves a sum that started at +0.0 unchanged
+      v[k][0] = make_double2(0.0, 0.0);
+      v[k][1] = make_double2(0.0, 0.0);
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < 4; ++c) s[c] = 0.0;
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    s[0] += v[k][0].x;
+    s[1] += v[k][0].y;
+    s[2] += v[k][1].x;
+    s[3] += v[k][1].y;
+  }
+  for (int b = lane + 32 * K; b < nb; b += 32) {
+    const double2 lo = __ldcg(reinterpret_cast<const double2*>(pb + 4 * static_cast<size_t>(b)));
+    const double2 hi =
+        __ldcg(reinterpret_cast<const double2*>(pb + 4 * static_cast<size_t>(b) + 2));
+    s[0] += lo.x;
+    s[1] += lo.y;
+    s[2] += hi.x;
+    s[3] += hi.y;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) s[c] += __shfl_down_sync(0xffffffffu, s[c], o);
+}
+
 }  // namespace tgb

@@ -634,14 +634,11 @@ __device__ __forceinline__ void grid_reduce(cg::grid_group& grid, const double (
   grid.sync();
   if (warp == 1 && lane == 0) after();  // e.g. prime the next sweep's TMA ring
   if (warp == 0) {
+double s[4];
+    warp_sum_partials(pb, static_cast<int>(gridDim.x), lane, s);
+    if (lane == 0)
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      double s = 0.0;
-      for (int b = lane; b < static_cast<int>(gridDim.x); b += 32) s += pb[b * 4 + c];
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
-      if (lane == 0) red[32 + c] = s;
-    }
+      for (int c = 0; c < 4; ++c) red[32 + c] = s[c];
   }
   __syncthreads();
 #pragma unroll
@@ -1622,15 +1619,11 @@ __global__ void __launch_bounds__(kThreads, K2_MINB)
   __syncthreads();
   if (last_block && warp == 0) {
     __threadfence();
+double v[4];
+    warp_sum_partials(ctl.cta_part, static_cast<int>(gridDim.x), lane, v);
+    if (lane == 0)
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      double v = 0.0;
-      for (int bb = lane; bb < static_cast<int>(gridDim.x); bb += 32)
-        v += ctl.cta_part[bb * 4 + q];
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
-      if (lane == 0) ctl.mine[q] = v;
-    }
+      for (int q = 0; q < 4; ++q) ctl.mine[q] = v[q];
     if (lane == 0) *ctl.ticket = 0u;
   }
 }

@@ -133,21 +133,19 @@ __device__ __forceinline__ void res_reduce(cg::grid_group& grid, const double (&
   }
   grid.sync();
   if (warp == 0) {
+double s[4];
+    warp_sum_partials(pb, static_cast<int>(gridDim.x), lane, s);
+    if (lane == 0)
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      double s = 0.0;
-      for (int b = lane; b < static_cast<int>(gridDim.x); b += 32) s += pb[b * 4 + c];
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
-      if (lane == 0) red[32 + c] = s;
-    }
+      for (int c = 0; c < 4; ++c) red[32 + c] = s[c];
   } else {
     after(tid - 32, NT - 32);
   }
   __syncthreads();
 #pragma unroll
   for (int c = 0; c < 4; ++c) out[c] = red[32 + c];
-  __syncthreads();
+  // (no barrier here: red is next written by the following reduction, after
+  // the block barriers of the prologue and the stencil passes)
   buf ^= 1;
 }
 
